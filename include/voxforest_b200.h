@@ -1,0 +1,203 @@
+/*
+ * voxforest_b200.h -- C-ABI of the B200 geometry-embedding engine
+ * (libvoxforest_b200.so, hand-written sm_100a CUDA).
+ *
+ * The reference (arxiv 2512.01251, /root/reference) has no FFI: its operator
+ * API is the SPEC op set in the voxforest.binning / .forest / .voxelizer module
+ * namespaces (only geometry.py/lattice.py ship as code).  Each
+ * entry point below replaces one of those ops; the Python package
+ * paper_2512_01251_b200 binds them with ctypes under the SPEC names (see
+ * INTEGRATION.md).
+ *
+ * Conventions:
+ *   - every pointer argument named d_* is DEVICE memory owned by the caller;
+ *     the library keeps no pointer past the call and never frees caller memory.
+ *   - sizes are int64_t; level descriptors are the POD vf_config below.
+ *   - all calls are asynchronous and ordered on the given cudaStream_t
+ *     (passed as void*); device-resident counts (d_level_start, d_count ...)
+ *     are read by kernels, never by the host, so a level needs no host sync.
+ *   - scratch is a caller-allocated workspace sized by the *_workspace_size
+ *     call (CUB-style two-phase).
+ *   - return value: VF_OK or a status code; message in vf_last_error()
+ *     (thread-local).  Device-detected conditions (capacity exhausted, N_lim
+ *     cap violated) are latched in the grid's d_status word and reported by
+ *     vf_check_status().
+ *   - results never depend on launch configuration or scheduling
+ *     (SPEC.md:97,172,370,552): atomics are used only for order-free
+ *     reductions (histograms, min), bins are re-sorted by face id.
+ */
+#ifndef VOXFOREST_B200_H
+#define VOXFOREST_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VF_ABI_VERSION 1
+#define VF_MAX_LEVELS 16
+
+/* status codes (SURVEY.md §8b "Errors") */
+enum {
+    VF_OK = 0,
+    VF_EARG = 1,       /* bad argument                                      */
+    VF_ECAPACITY = 2,  /* forest / pair capacity exhausted */
+    VF_ENLIM = 3,      /* N_lim pair cap violated               */
+    VF_ECUDA = 4,      /* CUDA error                                         */
+    VF_ENCCL = 5       /* NCCL error (multi-GPU path)                        */
+};
+
+/* cell mask enum (SPEC.md:197 cell_mask values) */
+enum { VF_FLUID = 0, VF_SOLID = 1, VF_GUARD = 2, VF_GHOST = 3,
+       VF_INTERFACE = 4, VF_BOUNDARY = 5 };
+/* block flag bits (SPEC.md:197 block mask) */
+enum { VF_BF_SOLID = 1, VF_BF_SB = 2, VF_BF_SA = 4, VF_BF_MARK = 8,
+       VF_BF_REFINED = 16, VF_BF_BOUNDARY = 32 };
+/* negative neighbour codes */
+enum { VF_NB_OUTSIDE = -1, VF_NB_MISSING = -2, VF_NB_SOLID_NBR = -3 };
+
+/* Level descriptor / embed config (SPEC.md:277-280 VoxelConfig + PAPER.md:291) */
+typedef struct {
+    int32_t nb[3];        /* root blocks per axis N_B                       */
+    int32_t l_max;        /* grid levels                                    */
+    int32_t n_spec;       /* N_spec                                         */
+    int32_t n_prop;       /* N_prop                          */
+    double  dx0;          /* root cell spacing                              */
+    double  len[3];       /* domain lengths (origin 0)                      */
+    double  eps_slab;
+    double  eps_parallel; /* geometry.py:25                                 */
+} vf_config;
+
+/* ForestGrid as flat device arrays, ids grouped by level:
+ * level L occupies ids [level_start[L], level_start[L+1]). */
+typedef struct {
+    int32_t *d_coords;      /* [cap*4]  i, j, k, level                      */
+    int32_t *d_nbr;         /* [cap*27] D3Q27 slot order, slot 0 = self     */
+    int32_t *d_nbr_child;   /* [cap*27] first child of neighbour or -1      */
+    int32_t *d_child;       /* [cap]    first child id or -1                */
+    uint8_t *d_bflags;      /* [cap]    VF_BF_* bits                        */
+    uint8_t *d_masks;       /* [cap*64] VF_* cell masks, t = I + 4J + 16K   */
+    int32_t *d_level_start; /* [VF_MAX_LEVELS+1] device-resident            */
+    int32_t *d_status;      /* [4] latched device errors (0 = ok)           */
+    int32_t  capacity;
+    int32_t  n_levels;      /* host-known number of levels present          */
+} vf_grid;
+
+/* one BinLevel */
+typedef struct {
+    int32_t  level;
+    int32_t  mode;          /* 0 = x-rays (1D), 1 = all directions (MD)     */
+    int32_t *d_counts;      /* [B_L^3]                                      */
+    int32_t *d_offsets;     /* [B_L^3]                                      */
+    int32_t *d_face_ids;    /* [face_ids_cap]                               */
+    int64_t  face_ids_cap;
+    int32_t *d_n_face_ids;  /* [1] device-resident total                    */
+    int32_t *d_map;         /* [F] compact_map of kept faces (FilterMap)    */
+    int32_t *d_n_map;       /* [1] device-resident |compact_map|            */
+} vf_bins;
+
+int         vf_abi_version(void);
+const char *vf_last_error(void);
+int         vf_device_info(int *sm_count, int *cc_major, int *cc_minor);
+
+/* face records: d_faces[F*12] = v1 v2 v3 (record-major, geometry.py:86-88)
+ * followed by the host-computed unit normal (geometry.py:90), 96 B/face */
+int vf_pack_faces(const double *d_faces_coord, const double *d_normals,
+                  int64_t n_faces, double *d_faces, void *stream);
+
+/* exact FP64 SAT (geometry.py:484-500) on arrays -- test hook */
+int vf_sat_batch(const double *d_tri, const double *d_box, int64_t n,
+                 uint8_t *d_out, void *stream);
+
+/* --- binning --------------------------------------- */
+size_t vf_bins_workspace_size(const vf_config *cfg, int64_t n_faces, int level);
+/* compute_ray_indicators (Alg.1) */
+int vf_ray_indicators(const vf_config *cfg, const double *d_faces,
+                      int64_t n_faces, int level, int mode, uint8_t *d_ind,
+                      void *stream);
+/* compact_filtered_faces */
+size_t vf_compact_workspace_size(int64_t n);
+int vf_compact(const uint8_t *d_ind, int64_t n, int32_t *d_map,
+               int32_t *d_count, void *d_ws, size_t ws_bytes, void *stream);
+/* compute_bin_pairs (Alg.2): pairs in
+ * face-major emission order (deterministic); d_map NULL = all faces */
+int vf_bin_pairs(const vf_config *cfg, const double *d_faces, int64_t n_faces,
+                 const int32_t *d_map, const int32_t *d_n_map, int level,
+                 int32_t *d_pair_bin, int32_t *d_pair_face, int64_t pair_cap,
+                 int32_t *d_n_pairs, int32_t *d_status, void *d_ws,
+                 size_t ws_bytes, void *stream);
+/* assemble_bins (steps 3-9 PAPER.md:477-479) */
+size_t vf_assemble_workspace_size(int64_t pair_cap, int64_t n_bins);
+int vf_bin_assemble(const int32_t *d_pair_bin, const int32_t *d_pair_face,
+                    const int32_t *d_n_pairs, int64_t pair_cap, int64_t n_bins,
+                    int32_t *d_counts, int32_t *d_offsets, int32_t *d_face_ids,
+                    void *d_ws, size_t ws_bytes, void *stream);
+/* fused build for one level: indicators -> compact -> pairs -> assemble */
+int vf_build_bins(const vf_config *cfg, const double *d_faces, int64_t n_faces,
+                  int level, int mode, int use_filter, vf_bins *bins,
+                  int32_t *d_status, void *d_ws, size_t ws_bytes, void *stream);
+
+/* --- forest ------------------------------------------ */
+int vf_init_forest(const vf_config *cfg, vf_grid *grid, void *stream);
+/* adapt, refine-only */
+size_t vf_adapt_workspace_size(const vf_grid *grid);
+int vf_adapt_refine(const vf_config *cfg, vf_grid *grid, int level,
+                    void *d_ws, size_t ws_bytes, void *stream);
+
+/* --- voxelizer --------------------------------------- */
+/* partial_surface_voxelize (Alg.3) */
+int vf_voxelize_level(const vf_config *cfg, vf_grid *grid, int level,
+                      const vf_bins *bins, const double *d_faces, void *stream);
+/* propagate_external (Alg.5), dir = +1 / -1; with
+ * finalize != 0 the apply epilogue also runs finalize_masks */
+size_t vf_propagate_workspace_size(const vf_grid *grid);
+int vf_propagate_x(const vf_config *cfg, vf_grid *grid, int level, int dir,
+                   int finalize, void *d_ws, size_t ws_bytes, void *stream);
+int vf_finalize_level(const vf_config *cfg, vf_grid *grid, int level,
+                      void *stream);
+/* mark_near_wall_refinement */
+size_t vf_mark_workspace_size(const vf_grid *grid);
+int vf_mark_level(const vf_config *cfg, vf_grid *grid, int level, void *d_ws,
+                  size_t ws_bytes, void *stream);
+/* identify_boundary_cells, finest level */
+int vf_boundary_cells(const vf_config *cfg, vf_grid *grid, int32_t *d_bcount,
+                      void *stream);
+/* build_boundary_tables: contraction map + N_b (device) */
+size_t vf_tables_workspace_size(const vf_grid *grid);
+int vf_link_tables(const vf_config *cfg, vf_grid *grid, const int32_t *d_bcount,
+                   int32_t *d_cmap, int32_t *d_n_b, void *d_ws, size_t ws_bytes,
+                   void *stream);
+/* compute_link_lengths: face-parallel, exact min via
+ * atomicMin on the IEEE bits; d_lengths[n_b*27*64] must hold -1.0f.
+ * d_map/d_n_map: optional filtered face list (NULL = all faces). */
+size_t vf_link_workspace_size(const vf_config *cfg, const vf_grid *grid);
+int vf_link_lengths(const vf_config *cfg, vf_grid *grid, const int32_t *d_cmap,
+                    const double *d_faces, int64_t n_faces,
+                    const int32_t *d_map, const int32_t *d_n_map,
+                    float *d_lengths, void *d_ws, size_t ws_bytes, void *stream);
+
+/* --- embed_geometry driver ----------------------------
+ * Phase 1 (no host sync): init_forest + per level bins/voxelize/propagate/
+ * finalize/mark/adapt + finest boundary cells + tables.  Writes the
+ * contraction map into d_cmap[capacity] and N_b into d_n_b.
+ * Phase 2 (after the caller read N_b and allocated d_lengths/d_bc_ids):
+ * link lengths.  stage events (optional, 16 cudaEvent_t) bracket stages. */
+size_t vf_embed_workspace_size(const vf_config *cfg, int64_t n_faces,
+                               int32_t capacity);
+int vf_embed_phase1(const vf_config *cfg, const double *d_faces,
+                    int64_t n_faces, int use_filter, vf_grid *grid,
+                    int32_t *d_cmap, int32_t *d_n_b, void *d_ws,
+                    size_t ws_bytes, void *stream, void **events);
+int vf_embed_phase2(const vf_config *cfg, const double *d_faces,
+                    int64_t n_faces, vf_grid *grid, const int32_t *d_cmap,
+                    float *d_lengths, void *d_ws, size_t ws_bytes,
+                    void *stream);
+/* copy the grid's latched device status to the host (synchronizes) */
+int vf_check_status(const vf_grid *grid, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

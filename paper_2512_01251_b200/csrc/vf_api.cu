@@ -1,0 +1,401 @@
+// vf_api.cu -- C-ABI entry points (include/voxforest_b200.h) and the native
+// embed_geometry driver.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "vf_common.cuh"
+#include "vf_internal.h"
+#include "vf_scan.cuh"
+
+namespace vf {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char *msg) {
+    snprintf(g_err, sizeof(g_err), "%s", msg);
+    return code;
+}
+
+int set_cuda_error(cudaError_t e, const char *what) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+    return VF_ECUDA;
+}
+
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? VF_OK : set_cuda_error(e, what);
+}
+
+int sm_count() {
+    static int n = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+            n = 148;
+    });
+    return n;
+}
+
+LevelInfo make_level(const vf_config &cfg, int L) {
+    LevelInfo li;
+    li.dx = ldexp(cfg.dx0, -L);
+    li.h = 4.0 * li.dx;
+    li.eps = cfg.eps_slab;
+    li.eps_par = cfg.eps_parallel;
+    for (int d = 0; d < 3; ++d) {
+        li.len[d] = cfg.len[d];
+        li.bins[d] = cfg.nb[d] << L;
+        li.cells[d] = 4 * li.bins[d];
+    }
+    li.level = L;
+    return li;
+}
+
+__global__ void k_iota(int32_t *out, int64_t n, int32_t *d_n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int32_t)i;
+    if (d_n && blockIdx.x == 0 && threadIdx.x == 0) *d_n = (int32_t)n;
+}
+
+int launch_iota(int32_t *out, int64_t n, int32_t *d_n, cudaStream_t st) {
+    int64_t g = (n + 255) / 256;
+    if (g > max_ctas(8)) g = max_ctas(8);
+    if (g < 1) g = 1;
+    k_iota<<<(int)g, 256, 0, st>>>(out, n, d_n);
+    return check_launch("k_iota");
+}
+
+__global__ void k_pack_faces(const double *__restrict__ fc, const double *__restrict__ nrm, int64_t F,
+                             double *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F * kFaceStride;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = i / kFaceStride;
+        const int k = (int)(i % kFaceStride);
+        out[i] = k < 9 ? fc[9 * f + k] : nrm[3 * f + (k - 9)];
+    }
+}
+
+__global__ void k_sat_batch(const double *__restrict__ tri, const double *__restrict__ box, int64_t n,
+                            uint8_t *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        SatFace f;
+        double v[9];
+        for (int k = 0; k < 9; ++k) v[k] = tri[9 * i + k];
+        sat_face_init(f, v);
+        const double *b = box + 6 * i;
+        out[i] = sat_exact(f, b[0], b[1], b[2], b[3], b[4], b[5]) ? 1 : 0;
+    }
+}
+
+static bool valid_cfg(const vf_config *c) {
+    if (!c) return false;
+    for (int d = 0; d < 3; ++d)
+        if (c->nb[d] <= 0 || !(c->len[d] > 0)) return false;
+    return c->l_max >= 1 && c->l_max < VF_MAX_LEVELS && c->n_spec >= 1 && c->n_prop >= 0 &&
+           c->dx0 > 0 && c->eps_slab >= 0;
+}
+
+static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// embed workspace layout
+struct EmbedWs {
+    vf_bins bins;
+    void *bins_ws;
+    size_t bins_ws_bytes;
+    void *prop_ws, *mark_ws, *adapt_ws, *tab_ws, *link_ws;
+    size_t prop_b, mark_b, adapt_b, tab_b, link_b;
+    int32_t *bcount;
+};
+
+static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *base, EmbedWs *w) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        char *p = base ? base + off : nullptr;
+        off += al(bytes);
+        return (void *)p;
+    };
+    const int Lf = cfg.l_max - 1;
+    const int nlim = nlim_of(cfg);
+    const int64_t nbins = (int64_t)(cfg.nb[0] << Lf) * (cfg.nb[1] << Lf) * (cfg.nb[2] << Lf);
+    EmbedWs t;
+    memset(&t, 0, sizeof(t));
+    t.bins.d_counts = (int32_t *)take(sizeof(int32_t) * (size_t)nbins);
+    t.bins.d_offsets = (int32_t *)take(sizeof(int32_t) * (size_t)nbins);
+    t.bins.face_ids_cap = F * nlim;
+    t.bins.d_face_ids = (int32_t *)take(sizeof(int32_t) * (size_t)(F * nlim + 1));
+    t.bins.d_map = (int32_t *)take(sizeof(int32_t) * (size_t)(F + 1));
+    t.bins.d_n_map = (int32_t *)take(64);
+    t.bins.d_n_face_ids = (int32_t *)take(64);
+    t.bins_ws_bytes = bins_workspace_size(F, nlim, nbins);
+    t.bins_ws = take(t.bins_ws_bytes);
+    t.prop_b = propagate_workspace_size(cap);
+    t.prop_ws = take(t.prop_b);
+    t.mark_b = mark_workspace_size(cap);
+    t.mark_ws = take(t.mark_b);
+    t.adapt_b = adapt_workspace_size(cap);
+    t.adapt_ws = take(t.adapt_b);
+    t.tab_b = tables_workspace_size(cap);
+    t.tab_ws = take(t.tab_b);
+    t.link_b = link_workspace_size(cfg, Lf);
+    t.link_ws = take(t.link_b);
+    t.bcount = (int32_t *)take(sizeof(int32_t) * (size_t)cap);
+    if (w) *w = t;
+    return off;
+}
+
+}  // namespace vf
+
+using namespace vf;
+
+extern "C" {
+
+int vf_abi_version(void) { return VF_ABI_VERSION; }
+
+const char *vf_last_error(void) { return g_err; }
+
+int vf_device_info(int *sm, int *major, int *minor) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaGetDevice");
+    if (sm) cudaDeviceGetAttribute(sm, cudaDevAttrMultiProcessorCount, dev);
+    if (major) cudaDeviceGetAttribute(major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (minor) cudaDeviceGetAttribute(minor, cudaDevAttrComputeCapabilityMinor, dev);
+    return check_launch("vf_device_info");
+}
+
+int vf_pack_faces(const double *fc, const double *nrm, int64_t F, double *out, void *stream) {
+    if (!fc || !nrm || !out || F < 0) return set_error(VF_EARG, "vf_pack_faces: bad argument");
+    if (F == 0) return VF_OK;
+    int64_t g = (F * kFaceStride + 255) / 256;
+    if (g > max_ctas(8)) g = max_ctas(8);
+    k_pack_faces<<<(int)g, 256, 0, (cudaStream_t)stream>>>(fc, nrm, F, out);
+    return check_launch("k_pack_faces");
+}
+
+int vf_sat_batch(const double *tri, const double *box, int64_t n, uint8_t *out, void *stream) {
+    if (!tri || !box || !out || n < 0) return set_error(VF_EARG, "vf_sat_batch: bad argument");
+    if (n == 0) return VF_OK;
+    int64_t g = (n + 127) / 128;
+    if (g > max_ctas(8)) g = max_ctas(8);
+    k_sat_batch<<<(int)g, 128, 0, (cudaStream_t)stream>>>(tri, box, n, out);
+    return check_launch("k_sat_batch");
+}
+
+size_t vf_bins_workspace_size(const vf_config *cfg, int64_t F, int level) {
+    if (!valid_cfg(cfg)) return 0;
+    const int64_t nb = (int64_t)(cfg->nb[0] << level) * (cfg->nb[1] << level) * (cfg->nb[2] << level);
+    size_t a = bins_workspace_size(F, nlim_of(*cfg), nb);
+    size_t b = assemble_workspace_size(F * nlim_of(*cfg), nb);
+    return a > b ? a : b;
+}
+
+int vf_ray_indicators(const vf_config *cfg, const double *faces, int64_t F, int level, int mode,
+                      uint8_t *ind, void *stream) {
+    if (!valid_cfg(cfg) || !faces || !ind || F < 0 || level < 0 || (mode != 0 && mode != 1))
+        return set_error(VF_EARG, "vf_ray_indicators: bad argument");
+    return launch_indicators(make_level(*cfg, level), mode, faces, F, ind, (cudaStream_t)stream);
+}
+
+size_t vf_compact_workspace_size(int64_t n) { return scan_workspace_bytes(n < 1 ? 1 : n); }
+
+size_t vf_assemble_workspace_size(int64_t pair_cap, int64_t n_bins) {
+    return assemble_workspace_size(pair_cap < 1 ? 1 : pair_cap, n_bins);
+}
+
+int vf_compact(const uint8_t *ind, int64_t n, int32_t *map, int32_t *d_count, void *ws,
+               size_t ws_bytes, void *stream) {
+    if (!ind || !map || !d_count || n < 0) return set_error(VF_EARG, "vf_compact: bad argument");
+    if (ws_bytes < scan_workspace_bytes(n)) return set_error(VF_EARG, "vf_compact: workspace too small");
+    return launch_compact(ind, n, map, d_count, ws, (cudaStream_t)stream);
+}
+
+int vf_bin_pairs(const vf_config *cfg, const double *faces, int64_t F, const int32_t *map,
+                 const int32_t *d_n_map, int level, int32_t *pair_bin, int32_t *pair_face,
+                 int64_t pair_cap, int32_t *d_n_pairs, int32_t *d_status, void *ws, size_t ws_bytes,
+                 void *stream) {
+    if (!valid_cfg(cfg) || !faces || !pair_bin || !pair_face || !d_n_pairs || level < 0 ||
+        (map && !d_n_map))
+        return set_error(VF_EARG, "vf_bin_pairs: bad argument");
+    return bin_pairs_impl(make_level(*cfg, level), nlim_of(*cfg), faces, F, map, d_n_map, pair_bin,
+                          pair_face, pair_cap, d_n_pairs, d_status, ws, ws_bytes,
+                          (cudaStream_t)stream);
+}
+
+int vf_bin_assemble(const int32_t *pair_bin, const int32_t *pair_face, const int32_t *d_n_pairs,
+                    int64_t pair_cap, int64_t n_bins, int32_t *counts, int32_t *offsets,
+                    int32_t *face_ids, void *ws, size_t ws_bytes, void *stream) {
+    if (!pair_bin || !pair_face || !d_n_pairs || !counts || !offsets || !face_ids || n_bins <= 0)
+        return set_error(VF_EARG, "vf_bin_assemble: bad argument");
+    return assemble_impl(pair_bin, pair_face, d_n_pairs, pair_cap, n_bins, counts, offsets, face_ids,
+                         ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int vf_build_bins(const vf_config *cfg, const double *faces, int64_t F, int level, int mode,
+                  int use_filter, vf_bins *bins, int32_t *d_status, void *ws, size_t ws_bytes,
+                  void *stream) {
+    if (!valid_cfg(cfg) || !faces || !bins || level < 0 || !bins->d_counts || !bins->d_offsets ||
+        !bins->d_face_ids || !bins->d_map || !bins->d_n_map || !bins->d_n_face_ids)
+        return set_error(VF_EARG, "vf_build_bins: bad argument");
+    bins->level = level;
+    bins->mode = mode;
+    return build_bins_impl(make_level(*cfg, level), nlim_of(*cfg), faces, F, mode, use_filter, bins,
+                           d_status, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int vf_init_forest(const vf_config *cfg, vf_grid *grid, void *stream) {
+    if (!valid_cfg(cfg) || !grid) return set_error(VF_EARG, "vf_init_forest: bad argument");
+    return init_forest_impl(*cfg, grid, (cudaStream_t)stream);
+}
+
+size_t vf_adapt_workspace_size(const vf_grid *g) { return g ? adapt_workspace_size(g->capacity) : 0; }
+
+int vf_adapt_refine(const vf_config *cfg, vf_grid *grid, int level, void *ws, size_t ws_bytes,
+                    void *stream) {
+    if (!valid_cfg(cfg) || !grid || level < 0) return set_error(VF_EARG, "vf_adapt_refine: bad argument");
+    return adapt_impl(*cfg, grid, level, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int vf_voxelize_level(const vf_config *cfg, vf_grid *grid, int level, const vf_bins *bins,
+                      const double *faces, void *stream) {
+    if (!valid_cfg(cfg) || !grid || !bins || !faces || level < 0 || level >= grid->n_levels)
+        return set_error(VF_EARG, "vf_voxelize_level: bad argument");
+    return voxelize_impl(make_level(*cfg, level), grid, level, bins, faces, (cudaStream_t)stream);
+}
+
+size_t vf_propagate_workspace_size(const vf_grid *g) { return g ? propagate_workspace_size(g->capacity) : 0; }
+
+int vf_propagate_x(const vf_config *cfg, vf_grid *grid, int level, int dir, int finalize, void *ws,
+                   size_t ws_bytes, void *stream) {
+    if (!valid_cfg(cfg) || !grid || level < 0 || level >= grid->n_levels || (dir != 1 && dir != -1))
+        return set_error(VF_EARG, "vf_propagate_x: bad argument");
+    return propagate_impl(make_level(*cfg, level), grid, level, dir, finalize, ws, ws_bytes,
+                          (cudaStream_t)stream);
+}
+
+int vf_finalize_level(const vf_config *cfg, vf_grid *grid, int level, void *stream) {
+    if (!valid_cfg(cfg) || !grid || level < 0 || level >= grid->n_levels)
+        return set_error(VF_EARG, "vf_finalize_level: bad argument");
+    return finalize_impl(grid, level, (cudaStream_t)stream);
+}
+
+size_t vf_mark_workspace_size(const vf_grid *g) { return g ? mark_workspace_size(g->capacity) : 0; }
+
+int vf_mark_level(const vf_config *cfg, vf_grid *grid, int level, void *ws, size_t ws_bytes,
+                  void *stream) {
+    if (!valid_cfg(cfg) || !grid || level < 0 || level >= grid->n_levels)
+        return set_error(VF_EARG, "vf_mark_level: bad argument");
+    return mark_impl(*cfg, grid, level, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int vf_boundary_cells(const vf_config *cfg, vf_grid *grid, int32_t *bcount, void *stream) {
+    if (!valid_cfg(cfg) || !grid || !bcount) return set_error(VF_EARG, "vf_boundary_cells: bad argument");
+    return boundary_impl(grid, bcount, (cudaStream_t)stream);
+}
+
+size_t vf_tables_workspace_size(const vf_grid *g) { return g ? tables_workspace_size(g->capacity) : 0; }
+
+int vf_link_tables(const vf_config *cfg, vf_grid *grid, const int32_t *bcount, int32_t *cmap,
+                   int32_t *d_n_b, void *ws, size_t ws_bytes, void *stream) {
+    if (!valid_cfg(cfg) || !grid || !bcount || !cmap || !d_n_b)
+        return set_error(VF_EARG, "vf_link_tables: bad argument");
+    return tables_impl(grid, bcount, cmap, d_n_b, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t vf_link_workspace_size(const vf_config *cfg, const vf_grid *g) {
+    if (!valid_cfg(cfg) || !g) return 0;
+    return link_workspace_size(*cfg, g->n_levels - 1);
+}
+
+int vf_link_lengths(const vf_config *cfg, vf_grid *grid, const int32_t *cmap, const double *faces,
+                    int64_t F, const int32_t *map, const int32_t *d_n_map, float *lengths, void *ws,
+                    size_t ws_bytes, void *stream) {
+    if (!valid_cfg(cfg) || !grid || !cmap || !faces || !lengths || (map && !d_n_map))
+        return set_error(VF_EARG, "vf_link_lengths: bad argument");
+    return link_impl(*cfg, grid, cmap, faces, F, map, d_n_map, lengths, ws, ws_bytes,
+                     (cudaStream_t)stream);
+}
+
+size_t vf_embed_workspace_size(const vf_config *cfg, int64_t F, int32_t cap) {
+    if (!valid_cfg(cfg) || F < 0 || cap <= 0) return 0;
+    return embed_layout(*cfg, F, cap, nullptr, nullptr);
+}
+
+#define VF_TRY(x)                 \
+    do {                          \
+        int _rc = (x);            \
+        if (_rc) return _rc;      \
+    } while (0)
+
+static void rec(void **ev, int n_ev, int *k, cudaStream_t st) {
+    if (ev && *k < n_ev) cudaEventRecord((cudaEvent_t)ev[*k], st);
+    ++*k;
+}
+
+int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int use_filter,
+                    vf_grid *g, int32_t *cmap, int32_t *d_n_b, void *ws, size_t ws_bytes,
+                    void *stream, void **events) {
+    if (!valid_cfg(cfg) || !faces || !g || !cmap || !d_n_b || F <= 0)
+        return set_error(VF_EARG, "vf_embed_phase1: bad argument");
+    EmbedWs w;
+    if (embed_layout(*cfg, F, g->capacity, (char *)ws, &w) > ws_bytes)
+        return set_error(VF_EARG, "vf_embed_phase1: workspace too small");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int n_ev = 64;
+    int k = 0;
+    rec(events, n_ev, &k, st);  // 0: start
+    VF_TRY(init_forest_impl(*cfg, g, st));
+    for (int L = 0; L < cfg->l_max; ++L) {
+        const LevelInfo li = make_level(*cfg, L);
+        VF_TRY(build_bins_impl(li, nlim_of(*cfg), faces, F, 0, use_filter, &w.bins, g->d_status,
+                               w.bins_ws, w.bins_ws_bytes, st));
+        rec(events, n_ev, &k, st);  // bins done
+        VF_TRY(voxelize_impl(li, g, L, &w.bins, faces, st));
+        VF_TRY(propagate_impl(li, g, L, +1, L == 0, w.prop_ws, w.prop_b, st));
+        if (L > 0) VF_TRY(propagate_impl(li, g, L, -1, 1, w.prop_ws, w.prop_b, st));
+        rec(events, n_ev, &k, st);  // voxelization done
+        if (L == cfg->l_max - 1) break;
+        VF_TRY(mark_impl(*cfg, g, L, w.mark_ws, w.mark_b, st));
+        VF_TRY(adapt_impl(*cfg, g, L, w.adapt_ws, w.adapt_b, st));
+        rec(events, n_ev, &k, st);  // refinement done
+    }
+    VF_TRY(boundary_impl(g, w.bcount, st));
+    VF_TRY(tables_impl(g, w.bcount, cmap, d_n_b, w.tab_ws, w.tab_b, st));
+    rec(events, n_ev, &k, st);  // boundary + tables done
+    return VF_OK;
+}
+
+int vf_embed_phase2(const vf_config *cfg, const double *faces, int64_t F, vf_grid *g,
+                    const int32_t *cmap, float *lengths, void *ws, size_t ws_bytes, void *stream) {
+    if (!valid_cfg(cfg) || !faces || !g || !cmap || !lengths)
+        return set_error(VF_EARG, "vf_embed_phase2: bad argument");
+    EmbedWs w;
+    if (embed_layout(*cfg, F, g->capacity, (char *)ws, &w) > ws_bytes)
+        return set_error(VF_EARG, "vf_embed_phase2: workspace too small");
+    return link_impl(*cfg, g, cmap, faces, F, nullptr, nullptr, lengths, w.link_ws, w.link_b,
+                     (cudaStream_t)stream);
+}
+
+int vf_check_status(const vf_grid *g, void *stream) {
+    if (!g || !g->d_status) return set_error(VF_EARG, "vf_check_status: bad argument");
+    int32_t h[4] = {0, 0, 0, 0};
+    cudaError_t e = cudaMemcpyAsync(h, g->d_status, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return set_cuda_error(e, "vf_check_status");
+    if (h[0] == VF_ECAPACITY) {
+        char buf[128];
+        snprintf(buf, sizeof(buf), "forest capacity exhausted while refining level %d", h[1]);
+        return set_error(VF_ECAPACITY, buf);
+    }
+    if (h[0] == VF_ENLIM) return set_error(VF_ENLIM, "N_lim pair cap violated (refine_faces the mesh)");
+    if (h[0]) return set_error(h[0], "device-side error latched");
+    return VF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,477 @@
+// vf_bins.cu -- spatial-bin hierarchy build.
+//
+//   K-ind   face-parallel ray indicators, 1D (x-rows) or MD (13 rep. dirs)
+//           (Alg. 1, pins SURVEY A6)
+//   K-scan  compaction of kept faces (decoupled look-back, vf_scan.cuh)
+//   K-pairs face-parallel bin candidates vs the dx-expanded bin box, written
+//           into a per-face slot row (cap N_lim asserted) and, in the fused
+//           build, histogrammed straight into the dense per-bin counts
+//           (Alg. 2, pins A5)
+//   K-scan  counts -> offsets (replaces Thrust steps 3-9)
+//   K-scat  counting-sort scatter of face ids into their bin slices
+//   K-sort  per-bin ascending face-id order (deterministic BinLevel,
+//           SPEC.md:154,178) -- thread per bin for short slices, CTA per bin
+//           for long ones.
+#include <math.h>
+
+#include "vf_common.cuh"
+#include "vf_internal.h"
+#include "vf_scan.cuh"
+
+namespace vf {
+
+// --------------------------------------------------------------------------
+// K-ind
+
+__device__ bool indicator_1d(const double *v, const double *n, const LevelInfo &li) {
+    if (fabs(n[0]) < li.eps_par) return false;
+    SatFace f;
+    sat_face_init(f, v);
+    const double dx = li.dx, eps = li.eps;
+    // row range [floor(lo/dx), floor(hi/dx)] clamped; only a superset matters (A6)
+    double ja = floor(VF_DDIV(f.lo[1], dx)), jb = floor(VF_DDIV(f.hi[1], dx));
+    double ka = floor(VF_DDIV(f.lo[2], dx)), kb = floor(VF_DDIV(f.hi[2], dx));
+    ja = fmax(ja, 0.0); ka = fmax(ka, 0.0);
+    jb = fmin(jb, (double)(li.cells[1] - 1)); kb = fmin(kb, (double)(li.cells[2] - 1));
+    if (ja > jb || ka > kb) return false;
+    for (int k = (int)ka; k <= (int)kb; ++k) {
+        const double z = node_c(k, dx);
+        for (int j = (int)ja; j <= (int)jb; ++j) {
+            const double y = node_c(j, dx);
+            if (sat_exact(f, 0.0, VF_DSUB(y, eps), VF_DSUB(z, eps), li.len[0], VF_DADD(y, eps),
+                          VF_DADD(z, eps)))
+                return true;
+        }
+    }
+    return false;
+}
+
+__device__ bool indicator_md(const double *v, const double *n, const LevelInfo &li) {
+    SatFace f;
+    sat_face_init(f, v);
+    const double dx = li.dx, eps = li.eps;
+    int a[3], b[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        double fa = floor(VF_DDIV(f.lo[d], dx)) - 1.0, fb = floor(VF_DDIV(f.hi[d], dx)) + 1.0;
+        fa = fmax(fa, 0.0);
+        fb = fmin(fb, (double)(li.cells[d] - 1));
+        if (fa > fb) return false;
+        a[d] = (int)fa;
+        b[d] = (int)fb;
+    }
+    for (int q = 1; q < 27; q += 2) {
+        const double c0 = c27(q, 0), c1 = c27(q, 1), c2 = c27(q, 2);
+        const double cn = __dsqrt_rn(VF_DADD(VF_DADD(VF_DMUL(c0, c0), VF_DMUL(c1, c1)), VF_DMUL(c2, c2)));
+        const double den = VF_DADD(VF_DADD(VF_DMUL(c0, n[0]), VF_DMUL(c1, n[1])), VF_DMUL(c2, n[2]));
+        if (fabs(den) < VF_DMUL(li.eps_par, cn)) continue;
+        for (int k = a[2]; k <= b[2]; ++k) {
+            const double z = node_c(k, dx);
+            for (int j = a[1]; j <= b[1]; ++j) {
+                const double y = node_c(j, dx);
+                for (int i = a[0]; i <= b[0]; ++i) {
+                    const double x = node_c(i, dx);
+                    const double d = VF_DDIV(plane_num(v, n, x, y, z), den);
+                    const double xi = VF_DADD(x, VF_DMUL(d, c0));
+                    const double yi = VF_DADD(y, VF_DMUL(d, c1));
+                    const double zi = VF_DADD(z, VF_DMUL(d, c2));
+                    if (sat_exact(f, VF_DSUB(xi, eps), VF_DSUB(yi, eps), VF_DSUB(zi, eps),
+                                  VF_DADD(xi, eps), VF_DADD(yi, eps), VF_DADD(zi, eps)))
+                        return true;
+                }
+            }
+        }
+    }
+    return false;
+}
+
+__global__ void __launch_bounds__(256)
+    k_indicators(LevelInfo li, int mode, const double *__restrict__ faces, int64_t F,
+                 uint8_t *__restrict__ out) {
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < F;
+         f += (int64_t)gridDim.x * blockDim.x) {
+        double v[9], n[3];
+        load_face(faces, f, v, n);
+        out[f] = (uint8_t)(mode == 0 ? indicator_1d(v, n, li) : indicator_md(v, n, li));
+    }
+}
+
+// --------------------------------------------------------------------------
+// K-pairs
+
+// Candidate bins of one face (Alg. 2); returns the count or -1 on cap violation.
+__device__ int face_pairs(const double *v, const LevelInfo &li, int nlim, int32_t *slot,
+                          int32_t *counts /* nullable: fused histogram */) {
+    SatFace f;
+    sat_face_init(f, v);
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+        if (f.hi[d] < 0.0 || f.lo[d] > li.len[d]) return 0;  // outside domain
+    const double dx = li.dx, h = li.h;
+    int a[3], b[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const double s = VF_DDIV((double)li.bins[d], li.len[d]);
+        double fa = floor(VF_DMUL(f.lo[d], s)) - 1.0, fb = floor(VF_DMUL(f.hi[d], s)) + 1.0;
+        fa = fmax(fa, 0.0);
+        fb = fmin(fb, (double)(li.bins[d] - 1));
+        if (fa > fb) return 0;
+        a[d] = (int)fa;
+        b[d] = (int)fb;
+    }
+    int cnt = 0;
+    for (int bk = a[2]; bk <= b[2]; ++bk) {
+        const double mz = VF_DSUB(VF_DMUL((double)bk, h), dx), Mz = VF_DADD(VF_DMUL((double)(bk + 1), h), dx);
+        for (int bj = a[1]; bj <= b[1]; ++bj) {
+            const double my = VF_DSUB(VF_DMUL((double)bj, h), dx), My = VF_DADD(VF_DMUL((double)(bj + 1), h), dx);
+            for (int bi = a[0]; bi <= b[0]; ++bi) {
+                const double mx = VF_DSUB(VF_DMUL((double)bi, h), dx), Mx = VF_DADD(VF_DMUL((double)(bi + 1), h), dx);
+                if (sat_exact(f, mx, my, mz, Mx, My, Mz)) {
+                    if (cnt >= nlim) return -1;
+                    const int32_t bin = bi + li.bins[0] * (bj + li.bins[1] * bk);
+                    slot[cnt++] = bin;
+                    if (counts) atomicAdd(&counts[bin], 1);
+                }
+            }
+        }
+    }
+    return cnt;
+}
+
+__global__ void __launch_bounds__(256)
+    k_pairs(LevelInfo li, int nlim, const double *__restrict__ faces,
+            const int32_t *__restrict__ map, const int32_t *__restrict__ d_n_map, int64_t n_static,
+            int32_t *__restrict__ slots, int32_t *__restrict__ slot_cnt,
+            int32_t *__restrict__ counts, int32_t *__restrict__ d_status) {
+    const int64_t n = d_n_map ? (int64_t)*d_n_map : n_static;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = map ? (int64_t)map[m] : m;
+        double v[9], nn[3];
+        load_face(faces, f, v, nn);
+        int c = face_pairs(v, li, nlim, slots + m * nlim, counts);
+        if (c < 0) {
+            latch_status(d_status, VF_ENLIM);
+            c = 0;
+        }
+        slot_cnt[m] = c;
+    }
+}
+
+// pair list in face-major order (API compute_bin_pairs)
+__global__ void k_pairs_emit(int nlim, const int32_t *__restrict__ map, const int32_t *__restrict__ d_n_map,
+                             int64_t n_static, const int32_t *__restrict__ slots,
+                             const int32_t *__restrict__ slot_cnt, const int32_t *__restrict__ pos,
+                             int32_t *__restrict__ pair_bin, int32_t *__restrict__ pair_face,
+                             int64_t pair_cap, int32_t *__restrict__ d_status) {
+    const int64_t n = d_n_map ? (int64_t)*d_n_map : n_static;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t f = map ? map[m] : (int32_t)m;
+        const int c = slot_cnt[m];
+        const int64_t p0 = pos[m];
+        for (int k = 0; k < c; ++k) {
+            if (p0 + k >= pair_cap) { latch_status(d_status, VF_ECAPACITY); break; }
+            pair_bin[p0 + k] = slots[m * nlim + k];
+            pair_face[p0 + k] = f;
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
+// counting sort
+
+__global__ void k_hist_pairs(const int32_t *__restrict__ pair_bin, const int32_t *__restrict__ d_n,
+                             int32_t *__restrict__ counts) {
+    const int64_t n = *d_n;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&counts[pair_bin[p]], 1);
+}
+
+// scatter from slots: counts[] is used as a down-counting cursor and is
+// restored by k_bin_sort (counts[b] = offsets[b+1]-offsets[b]).
+__global__ void __launch_bounds__(256)
+    k_scatter_slots(int nlim, const int32_t *__restrict__ map, const int32_t *__restrict__ d_n_map,
+                    int64_t n_static, const int32_t *__restrict__ slots,
+                    const int32_t *__restrict__ slot_cnt, const int32_t *__restrict__ offsets,
+                    int32_t *__restrict__ counts, int32_t *__restrict__ face_ids,
+                    int64_t cap, int32_t *__restrict__ d_status) {
+    const int64_t n = d_n_map ? (int64_t)*d_n_map : n_static;
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t f = map ? map[m] : (int32_t)m;
+        const int c = slot_cnt[m];
+        for (int k = 0; k < c; ++k) {
+            const int32_t b = slots[m * nlim + k];
+            const int64_t p = (int64_t)offsets[b] + atomicSub(&counts[b], 1) - 1;
+            if (p < cap) face_ids[p] = f;
+            else latch_status(d_status, VF_ECAPACITY);
+        }
+    }
+}
+
+__global__ void k_scatter_pairs(const int32_t *__restrict__ pair_bin, const int32_t *__restrict__ pair_face,
+                                const int32_t *__restrict__ d_n, const int32_t *__restrict__ offsets,
+                                int32_t *__restrict__ counts, int32_t *__restrict__ face_ids) {
+    const int64_t n = *d_n;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t b = pair_bin[p];
+        const int64_t q = (int64_t)offsets[b] + atomicSub(&counts[b], 1) - 1;
+        face_ids[q] = pair_face[p];
+    }
+}
+
+constexpr int kSmallBin = 24;
+
+// restore counts, sort short bins in place (thread per bin), queue long bins
+__global__ void __launch_bounds__(256)
+    k_bin_sort_small(int64_t n_bins, const int32_t *__restrict__ offsets,
+                     const int32_t *__restrict__ d_total, int32_t *__restrict__ counts,
+                     int32_t *__restrict__ face_ids, int32_t *__restrict__ large_list,
+                     int32_t *__restrict__ d_n_large) {
+    const int64_t total = *d_total;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n_bins;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t off = offsets[b];
+        const int64_t end = (b + 1 < n_bins) ? (int64_t)offsets[b + 1] : total;
+        const int cnt = (int)(end - off);
+        counts[b] = cnt;
+        if (cnt <= 1) continue;
+        if (cnt > kSmallBin) {
+            const int k = atomicAdd(d_n_large, 1);
+            large_list[k] = (int32_t)b;
+            continue;
+        }
+        int32_t a[kSmallBin];
+        for (int i = 0; i < cnt; ++i) a[i] = face_ids[off + i];
+        for (int i = 1; i < cnt; ++i) {  // insertion sort
+            const int32_t x = a[i];
+            int j = i - 1;
+            while (j >= 0 && a[j] > x) { a[j + 1] = a[j]; --j; }
+            a[j + 1] = x;
+        }
+        for (int i = 0; i < cnt; ++i) face_ids[off + i] = a[i];
+    }
+}
+
+constexpr int kLargeSmem = 12288;  // ints staged in shared memory
+
+// CTA per long bin: rank sort (face ids within a bin are distinct)
+__global__ void __launch_bounds__(256)
+    k_bin_sort_large(const int32_t *__restrict__ large_list, const int32_t *__restrict__ d_n_large,
+                     const int32_t *__restrict__ offsets, const int32_t *__restrict__ counts,
+                     int32_t *__restrict__ face_ids, int32_t *__restrict__ scratch) {
+    extern __shared__ int32_t s_ids[];
+    const int n_large = *d_n_large;
+    for (int w = blockIdx.x; w < n_large; w += gridDim.x) {
+        const int32_t b = large_list[w];
+        const int64_t off = offsets[b];
+        const int cnt = counts[b];
+        const bool in_smem = cnt <= kLargeSmem;
+        const int32_t *src = in_smem ? s_ids : scratch + off;
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const int32_t x = face_ids[off + i];
+            if (in_smem) s_ids[i] = x;
+            else scratch[off + i] = x;
+        }
+        __syncthreads();
+        if (!in_smem) __threadfence_block();
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const int32_t x = src[i];
+            int r = 0;
+            for (int j = 0; j < cnt; ++j) r += (src[j] < x);
+            face_ids[off + r] = x;
+        }
+        __syncthreads();
+    }
+}
+
+// --------------------------------------------------------------------------
+// host side
+
+static inline int grid_for(int64_t n, int threads, int max_ctas) {
+    int64_t g = (n + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > max_ctas) g = max_ctas;
+    return (int)g;
+}
+
+int launch_indicators(const LevelInfo &li, int mode, const double *faces, int64_t F,
+                      uint8_t *out, cudaStream_t st) {
+    if (F <= 0) return VF_OK;
+    k_indicators<<<grid_for(F, 256, max_ctas(8)), 256, 0, st>>>(li, mode, faces, F, out);
+    return check_launch("k_indicators");
+}
+
+struct LoadU8 {
+    const uint8_t *p;
+    __device__ int operator()(int64_t i) const { return p[i] ? 1 : 0; }
+};
+struct EmitCompact {
+    int32_t *map;
+    __device__ void operator()(int64_t i, int v, int ex) const {
+        if (v) map[ex] = (int32_t)i;
+    }
+};
+struct LoadI32 {
+    const int32_t *p;
+    __device__ int operator()(int64_t i) const { return p[i]; }
+};
+struct EmitOffsets {
+    int32_t *out;
+    __device__ void operator()(int64_t i, int, int ex) const { out[i] = ex; }
+};
+
+int launch_compact(const uint8_t *ind, int64_t n, int32_t *map, int32_t *d_count, void *ws,
+                   cudaStream_t st) {
+    cudaError_t e = scan_launch(LoadU8{ind}, EmitCompact{map}, n, nullptr, d_count, ws, st);
+    return e == cudaSuccess ? VF_OK : set_cuda_error(e, "compact scan");
+}
+
+int launch_exclusive_scan(const int32_t *in, int64_t n_bound, const int32_t *d_n, int32_t *out,
+                          int32_t *d_total, void *ws, cudaStream_t st) {
+    cudaError_t e = scan_launch(LoadI32{in}, EmitOffsets{out}, n_bound, d_n, d_total, ws, st);
+    return e == cudaSuccess ? VF_OK : set_cuda_error(e, "exclusive scan");
+}
+
+// workspace layout of one bin build
+struct BinsWs {
+    uint8_t *ind;        // [F]
+    int32_t *slot_cnt;   // [F]
+    int32_t *pos;        // [F]
+    int32_t *slots;      // [F*nlim]
+    int32_t *large;      // [n_bins]
+    int32_t *scalars;    // [8]: 0 n_large, 1 n_pairs
+    void *scan_ws;       // scan status words
+    size_t scan_bytes;
+};
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static size_t bins_ws_layout(int64_t F, int nlim, int64_t n_bins, char *base, BinsWs *w) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        char *p = base ? base + off : nullptr;
+        off += align_up(bytes);
+        return p;
+    };
+    const int64_t scan_n = (F * nlim > n_bins ? F * nlim : n_bins) + 1;
+    BinsWs t;
+    t.ind = (uint8_t *)take((size_t)F + 1);
+    t.slot_cnt = (int32_t *)take(sizeof(int32_t) * ((size_t)F + 1));
+    t.pos = (int32_t *)take(sizeof(int32_t) * ((size_t)F + 1));
+    t.slots = (int32_t *)take(sizeof(int32_t) * ((size_t)F * nlim + 1));
+    t.large = (int32_t *)take(sizeof(int32_t) * ((size_t)n_bins + 1));
+    t.scalars = (int32_t *)take(sizeof(int32_t) * 8);
+    t.scan_bytes = scan_workspace_bytes(scan_n);
+    t.scan_ws = take(t.scan_bytes);
+    if (w) *w = t;
+    return off;
+}
+
+size_t bins_workspace_size(int64_t F, int nlim, int64_t n_bins) {
+    return bins_ws_layout(F, nlim, n_bins, nullptr, nullptr);
+}
+
+// indicators -> compact -> pairs(+hist) -> offsets -> scatter -> sort
+int build_bins_impl(const LevelInfo &li, int nlim, const double *faces, int64_t F, int mode,
+                    int use_filter, vf_bins *bins, int32_t *d_status, void *ws, size_t ws_bytes,
+                    cudaStream_t st) {
+    const int64_t n_bins = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
+    BinsWs w;
+    if (bins_ws_layout(F, nlim, n_bins, (char *)ws, &w) > ws_bytes)
+        return set_error(VF_EARG, "bins workspace too small");
+    int rc;
+    const int32_t *map = nullptr;
+    const int32_t *d_n_map = nullptr;
+    if (use_filter) {
+        if ((rc = launch_indicators(li, mode, faces, F, w.ind, st))) return rc;
+        if ((rc = launch_compact(w.ind, F, bins->d_map, bins->d_n_map, w.scan_ws, st))) return rc;
+        map = bins->d_map;
+        d_n_map = bins->d_n_map;
+    } else {
+        // identity map (filter off): still publish a FilterMap for the API
+        if ((rc = launch_iota(bins->d_map, F, bins->d_n_map, st))) return rc;
+    }
+    cudaMemsetAsync(bins->d_counts, 0, sizeof(int32_t) * (size_t)n_bins, st);
+    k_pairs<<<grid_for(F, 256, max_ctas(8)), 256, 0, st>>>(li, nlim, faces, map, d_n_map, F, w.slots,
+                                                         w.slot_cnt, bins->d_counts, d_status);
+    if ((rc = check_launch("k_pairs"))) return rc;
+    if ((rc = launch_exclusive_scan(bins->d_counts, n_bins, nullptr, bins->d_offsets,
+                                    bins->d_n_face_ids, w.scan_ws, st)))
+        return rc;
+    k_scatter_slots<<<grid_for(F, 256, max_ctas(8)), 256, 0, st>>>(
+        nlim, map, d_n_map, F, w.slots, w.slot_cnt, bins->d_offsets, bins->d_counts,
+        bins->d_face_ids, bins->face_ids_cap, d_status);
+    if ((rc = check_launch("k_scatter_slots"))) return rc;
+    return sort_bins(n_bins, bins->d_offsets, bins->d_n_face_ids, bins->d_counts, bins->d_face_ids,
+                     w.large, w.scalars, w.slots, st);
+}
+
+int sort_bins(int64_t n_bins, const int32_t *offsets, const int32_t *d_total, int32_t *counts,
+              int32_t *face_ids, int32_t *large, int32_t *scalars, int32_t *scratch,
+              cudaStream_t st) {
+    cudaMemsetAsync(scalars, 0, sizeof(int32_t), st);
+    k_bin_sort_small<<<grid_for(n_bins, 256, max_ctas(16)), 256, 0, st>>>(
+        n_bins, offsets, d_total, counts, face_ids, large, scalars);
+    int rc = check_launch("k_bin_sort_small");
+    if (rc) return rc;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_bin_sort_large, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kLargeSmem * sizeof(int32_t)));
+        attr = true;
+    }
+    k_bin_sort_large<<<max_ctas(2), 256, kLargeSmem * sizeof(int32_t), st>>>(
+        large, scalars, offsets, counts, face_ids, scratch);
+    return check_launch("k_bin_sort_large");
+}
+
+// API: pair list in face-major emission order
+int bin_pairs_impl(const LevelInfo &li, int nlim, const double *faces, int64_t F,
+                   const int32_t *map, const int32_t *d_n_map, int32_t *pair_bin,
+                   int32_t *pair_face, int64_t pair_cap, int32_t *d_n_pairs, int32_t *d_status,
+                   void *ws, size_t ws_bytes, cudaStream_t st) {
+    BinsWs w;
+    if (bins_ws_layout(F, nlim, 1, (char *)ws, &w) > ws_bytes)
+        return set_error(VF_EARG, "pairs workspace too small");
+    k_pairs<<<grid_for(F, 256, max_ctas(8)), 256, 0, st>>>(li, nlim, faces, map, d_n_map, F,
+                                                         w.slots, w.slot_cnt, nullptr, d_status);
+    int rc = check_launch("k_pairs");
+    if (rc) return rc;
+    if ((rc = launch_exclusive_scan(w.slot_cnt, F, d_n_map, w.pos, d_n_pairs, w.scan_ws, st)))
+        return rc;
+    k_pairs_emit<<<grid_for(F, 256, max_ctas(8)), 256, 0, st>>>(nlim, map, d_n_map, F, w.slots,
+                                                              w.slot_cnt, w.pos, pair_bin,
+                                                              pair_face, pair_cap, d_status);
+    return check_launch("k_pairs_emit");
+}
+
+// API: assemble from a pair list
+int assemble_impl(const int32_t *pair_bin, const int32_t *pair_face, const int32_t *d_n_pairs,
+                  int64_t pair_cap, int64_t n_bins, int32_t *counts, int32_t *offsets,
+                  int32_t *face_ids, void *ws, size_t ws_bytes, cudaStream_t st) {
+    BinsWs w;
+    if (bins_ws_layout(pair_cap, 1, n_bins, (char *)ws, &w) > ws_bytes)
+        return set_error(VF_EARG, "assemble workspace too small");
+    // total pairs -> w.scalars[1]
+    cudaMemsetAsync(counts, 0, sizeof(int32_t) * (size_t)n_bins, st);
+    k_hist_pairs<<<grid_for(pair_cap, 256, max_ctas(8)), 256, 0, st>>>(pair_bin, d_n_pairs, counts);
+    int rc = check_launch("k_hist_pairs");
+    if (rc) return rc;
+    if ((rc = launch_exclusive_scan(counts, n_bins, nullptr, offsets, w.scalars + 1, w.scan_ws, st)))
+        return rc;
+    k_scatter_pairs<<<grid_for(pair_cap, 256, max_ctas(8)), 256, 0, st>>>(
+        pair_bin, pair_face, d_n_pairs, offsets, counts, face_ids);
+    if ((rc = check_launch("k_scatter_pairs"))) return rc;
+    return sort_bins(n_bins, offsets, w.scalars + 1, counts, face_ids, w.large, w.scalars,
+                     w.slots, st);
+}
+
+size_t assemble_workspace_size(int64_t pair_cap, int64_t n_bins) {
+    return bins_ws_layout(pair_cap, 1, n_bins, nullptr, nullptr);
+}
+
+}  // namespace vf

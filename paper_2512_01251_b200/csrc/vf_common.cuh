@@ -1,0 +1,198 @@
+// vf_common.cuh -- shared device code for the B200 geometry-embedding engine.
+//
+// Exact FP64 predicates: every floating-point operation that feeds a decision
+// (SAT, plane distance, cell/box coordinates) is written with explicit
+// round-to-nearest intrinsics (__dadd_rn/__dsub_rn/__dmul_rn/__ddiv_rn) so
+// nvcc can never contract into FMA and the association matches the
+// reference's numba code (geometry.py:441-500, compiled without contraction)
+// operation for operation.  The library is additionally built -fmad=false.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/voxforest_b200.h"
+
+#define VF_DADD(a, b) __dadd_rn((a), (b))
+#define VF_DSUB(a, b) __dsub_rn((a), (b))
+#define VF_DMUL(a, b) __dmul_rn((a), (b))
+#define VF_DDIV(a, b) __ddiv_rn((a), (b))
+
+namespace vf {
+
+constexpr int kFaceStride = 12;  // doubles per face record: v1 v2 v3 n (96 B)
+constexpr int kWarp = 32;
+
+// D3Q27 order of lattice.py:19-39 (rest first, antiparallel pairs (2k-1,2k))
+__host__ __device__ __forceinline__ int c27(int q, int d) {
+    // packed as base-3 digits (c+1): x + 3y + 9z
+    constexpr int code[27] = {13, 14, 12, 16, 10, 22, 4,  17, 9,  23, 3,  5,  21, 11,
+                              15, 25, 1,  7,  19, 26, 0,  8,  18, 20, 6,  2,  24};
+    int v = code[q];
+    if (d == 0) return v % 3 - 1;
+    if (d == 1) return (v / 3) % 3 - 1;
+    return v / 9 - 1;
+}
+
+// slot of direction (dx,dy,dz) in {-1,0,1}^3
+__host__ __device__ __forceinline__ int slot_of(int dx, int dy, int dz) {
+    constexpr int inv[27] = {20, 16, 25, 10, 6,  11, 24, 17, 21, 8,  4,  13, 2,  0,
+                             1,  14, 3,  7,  22, 18, 23, 12, 5,  9,  26, 15, 19};
+    return inv[(dx + 1) + 3 * (dy + 1) + 9 * (dz + 1)];
+}
+
+// per-level constants, computed on the host (ldexp => exact dx_L)
+struct LevelInfo {
+    double dx;       // cell spacing dx_L
+    double h;        // block / bin edge 4*dx_L
+    double eps;      // eps_slab
+    double eps_par;  // EPS_PARALLEL
+    double len[3];   // domain lengths
+    int cells[3];    // cells per axis at L
+    int bins[3];     // bins (= blocks) per axis at L
+    int level;
+};
+
+// A2: lattice node / cell centre, one rounding
+__device__ __forceinline__ double node_c(int gi, double dx) {
+    return VF_DMUL(VF_DADD((double)gi, 0.5), dx);
+}
+
+// A7/A17: plane-distance numerator (v0-x).n with fixed association
+__device__ __forceinline__ double plane_num(const double *v, const double *n, double x,
+                                           double y, double z) {
+    return VF_DADD(VF_DMUL(VF_DSUB(v[0], x), n[0]),
+                   VF_DADD(VF_DMUL(VF_DSUB(v[1], y), n[1]), VF_DMUL(VF_DSUB(v[2], z), n[2])));
+}
+
+// ---------------------------------------------------------------------------
+// SAT triangle/AABB overlap, bit-exact port of geometry.py:441-500.
+// The predicate is a conjunction of independent tests (plane cut, 15 axis
+// gaps); each test is evaluated exactly as the reference evaluates it, and
+// because AND is order-free the cheap box-axis comparisons run first.
+
+struct SatFace {
+    double v[9];     // v1 v2 v3
+    double lo[3];    // per-axis vertex min (== tmin of the box-axis tests)
+    double hi[3];    // per-axis vertex max
+    double pn[3];    // un-normalised plane normal of _plane_cuts_box
+};
+
+__device__ __forceinline__ void sat_face_init(SatFace &f, const double *v) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) f.v[k] = v[k];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        f.lo[d] = fmin(fmin(v[d], v[3 + d]), v[6 + d]);
+        f.hi[d] = fmax(fmax(v[d], v[3 + d]), v[6 + d]);
+    }
+    const double v1x = v[0], v1y = v[1], v1z = v[2], v2x = v[3], v2y = v[4], v2z = v[5],
+                 v3x = v[6], v3y = v[7], v3z = v[8];
+    // geometry.py:444-446
+    f.pn[0] = VF_DSUB(VF_DMUL(VF_DSUB(v2y, v1y), VF_DSUB(v3z, v1z)),
+                      VF_DMUL(VF_DSUB(v2z, v1z), VF_DSUB(v3y, v1y)));
+    f.pn[1] = VF_DSUB(VF_DMUL(VF_DSUB(v2z, v1z), VF_DSUB(v3x, v1x)),
+                      VF_DMUL(VF_DSUB(v2x, v1x), VF_DSUB(v3z, v1z)));
+    f.pn[2] = VF_DSUB(VF_DMUL(VF_DSUB(v2x, v1x), VF_DSUB(v3y, v1y)),
+                      VF_DMUL(VF_DSUB(v2y, v1y), VF_DSUB(v3x, v1x)));
+}
+
+// geometry.py:447-454
+__device__ __forceinline__ bool sat_plane_cut(const SatFace &f, double mx, double my, double mz,
+                                              double Mx, double My, double Mz) {
+    const double nx = f.pn[0], ny = f.pn[1], nz = f.pn[2];
+    const double v1x = f.v[0], v1y = f.v[1], v1z = f.v[2];
+    const double cx = (nx > 0.0) ? VF_DSUB(Mx, mx) : 0.0;
+    const double cy = (ny > 0.0) ? VF_DSUB(My, my) : 0.0;
+    const double cz = (nz > 0.0) ? VF_DSUB(Mz, mz) : 0.0;
+    const double d = VF_DADD(VF_DADD(VF_DMUL(nx, mx), VF_DMUL(ny, my)), VF_DMUL(nz, mz));
+    const double d1 = VF_DADD(VF_DADD(VF_DMUL(nx, VF_DSUB(cx, v1x)), VF_DMUL(ny, VF_DSUB(cy, v1y))),
+                              VF_DMUL(nz, VF_DSUB(cz, v1z)));
+    const double d2 = VF_DADD(
+        VF_DADD(VF_DMUL(nx, VF_DSUB(VF_DSUB(VF_DSUB(Mx, mx), cx), v1x)),
+                VF_DMUL(ny, VF_DSUB(VF_DSUB(VF_DSUB(My, my), cy), v1y))),
+        VF_DMUL(nz, VF_DSUB(VF_DSUB(VF_DSUB(Mz, mz), cz), v1z)));
+    return VF_DMUL(VF_DADD(d, d1), VF_DADD(d, d2)) <= 0.0;
+}
+
+// geometry.py:457-481 for the edge axes (k = 2,3,4); true = separated
+__device__ __forceinline__ bool sat_edge_gap(double ex, double ey, double a1, double b1,
+                                             double a2, double b2, double a3, double b3,
+                                             double ra, double rb, double Ra, double Rb) {
+    const double t1 = VF_DADD(VF_DMUL(a1, ex), VF_DMUL(b1, ey));
+    const double t2 = VF_DADD(VF_DMUL(a2, ex), VF_DMUL(b2, ey));
+    const double t3 = VF_DADD(VF_DMUL(a3, ex), VF_DMUL(b3, ey));
+    const double tmin = fmin(fmin(t1, t2), t3);
+    const double tmax = fmax(fmax(t1, t2), t3);
+    const double r1 = VF_DADD(VF_DMUL(ra, ex), VF_DMUL(rb, ey));
+    const double r2 = VF_DADD(VF_DMUL(Ra, ex), VF_DMUL(rb, ey));
+    const double r3 = VF_DADD(VF_DMUL(ra, ex), VF_DMUL(Rb, ey));
+    const double r4 = VF_DADD(VF_DMUL(Ra, ex), VF_DMUL(Rb, ey));
+    const double rmin = fmin(fmin(r1, r2), fmin(r3, r4));
+    const double rmax = fmax(fmax(r1, r2), fmax(r3, r4));
+    return (tmax < rmin) || (rmax < tmin);
+}
+
+// the three edge axes of one projection plane (a, b) = coordinate pair
+__device__ __forceinline__ bool sat_plane_edges_gap(double a1, double b1, double a2, double b2,
+                                                    double a3, double b3, double ra, double rb,
+                                                    double Ra, double Rb) {
+    if (sat_edge_gap(VF_DSUB(b2, b1), VF_DSUB(a1, a2), a1, b1, a2, b2, a3, b3, ra, rb, Ra, Rb))
+        return true;
+    if (sat_edge_gap(VF_DSUB(b3, b2), VF_DSUB(a2, a3), a1, b1, a2, b2, a3, b3, ra, rb, Ra, Rb))
+        return true;
+    if (sat_edge_gap(VF_DSUB(b1, b3), VF_DSUB(a3, a1), a1, b1, a2, b2, a3, b3, ra, rb, Ra, Rb))
+        return true;
+    return false;
+}
+
+// box-axis tests: axis 0/1 of each plane reduce to exact comparisons
+// (t = v*1.0 + w*0.0 == v up to the sign of zero; r likewise)
+__device__ __forceinline__ bool sat_box_axes_overlap(const SatFace &f, double mx, double my,
+                                                     double mz, double Mx, double My, double Mz) {
+    const double m[3] = {mx, my, mz}, M[3] = {Mx, My, Mz};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const double rmin = fmin(m[d], M[d]), rmax = fmax(m[d], M[d]);
+        if (f.hi[d] < rmin || rmax < f.lo[d]) return false;
+    }
+    return true;
+}
+
+__device__ __forceinline__ bool sat_exact(const SatFace &f, double mx, double my, double mz,
+                                          double Mx, double My, double Mz) {
+    if (!sat_box_axes_overlap(f, mx, my, mz, Mx, My, Mz)) return false;
+    const double *v = f.v;
+    // yz plane (geometry.py:494-496)
+    if (sat_plane_edges_gap(v[1], v[2], v[4], v[5], v[7], v[8], my, mz, My, Mz)) return false;
+    // xy plane (geometry.py:491-493)
+    if (sat_plane_edges_gap(v[0], v[1], v[3], v[4], v[6], v[7], mx, my, Mx, My)) return false;
+    // zx plane (geometry.py:497-499)
+    if (sat_plane_edges_gap(v[2], v[0], v[5], v[3], v[8], v[6], mz, mx, Mz, Mx)) return false;
+    return sat_plane_cut(f, mx, my, mz, Mx, My, Mz);
+}
+
+// ---------------------------------------------------------------------------
+// small helpers
+
+__device__ __forceinline__ void load_face(const double *__restrict__ faces, int64_t f,
+                                          double *v, double *n) {
+    const double2 *p = reinterpret_cast<const double2 *>(faces + f * kFaceStride);
+    double2 a = __ldg(p + 0), b = __ldg(p + 1), c = __ldg(p + 2), d = __ldg(p + 3),
+            e = __ldg(p + 4), g = __ldg(p + 5);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y;
+    v[6] = d.x; v[7] = d.y; v[8] = e.x;
+    n[0] = e.y; n[1] = g.x; n[2] = g.y;
+}
+
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ void latch_status(int32_t *d_status, int code) {
+    if (d_status) atomicMax(d_status, code);
+}
+
+}  // namespace vf

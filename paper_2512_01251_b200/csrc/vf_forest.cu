@@ -1,0 +1,358 @@
+// vf_forest.cu -- forest-of-octrees kernels: root grid, near-wall marking and
+// refine-only adaptation.
+//
+//   K-init    root blocks + full-halo links
+//   K-mark*   (i) solid-boundary, (ii) adjacent + solid-adjacent, (iii) N_prop
+//             ping-pong sweeps; block-parallel, 26-neighbour reads (pin A12)
+//   K-adapt   child ids by exclusive scan over the level's marks (deterministic,
+//             no hash table, no free-list atomics: the gap set is always
+//             [n_used, capacity), pin A13), child metadata + links from the
+//             parent's neighbours, ghost layer (A14); then the level's
+//             neighbour-child links and interface layer.
+#include "vf_common.cuh"
+#include "vf_internal.h"
+#include "vf_scan.cuh"
+
+namespace vf {
+
+__global__ void k_init_forest(int nx, int ny, int nz, int32_t *__restrict__ coords,
+                              int32_t *__restrict__ nbr, int32_t *__restrict__ nbr_child,
+                              int32_t *__restrict__ child, uint8_t *__restrict__ bflags,
+                              uint8_t *__restrict__ masks, int32_t *__restrict__ level_start,
+                              int32_t *__restrict__ status) {
+    const int64_t n = (int64_t)nx * ny * nz;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(b % nx), j = (int)((b / nx) % ny), k = (int)(b / ((int64_t)nx * ny));
+        reinterpret_cast<int4 *>(coords)[b] = make_int4(i, j, k, 0);
+        for (int q = 0; q < 27; ++q) {
+            const int ti = i + c27(q, 0), tj = j + c27(q, 1), tk = k + c27(q, 2);
+            int32_t v = VF_NB_OUTSIDE;
+            if (ti >= 0 && tj >= 0 && tk >= 0 && ti < nx && tj < ny && tk < nz)
+                v = (int32_t)(ti + nx * (tj + ny * tk));
+            nbr[27 * b + q] = v;
+            nbr_child[27 * b + q] = -1;
+        }
+        child[b] = -1;
+        bflags[b] = 0;
+        uint4 *m = reinterpret_cast<uint4 *>(masks + 64 * b);
+        m[0] = m[1] = m[2] = m[3] = make_uint4(0, 0, 0, 0);  // VF_FLUID
+    }
+    if (blockIdx.x == 0 && threadIdx.x <= VF_MAX_LEVELS) {
+        level_start[threadIdx.x] = threadIdx.x == 0 ? 0 : (int32_t)n;
+        if (threadIdx.x < 4) status[threadIdx.x] = 0;
+    }
+}
+
+int init_forest_impl(const vf_config &cfg, vf_grid *g, cudaStream_t st) {
+    const int64_t n = (int64_t)cfg.nb[0] * cfg.nb[1] * cfg.nb[2];
+    if (n > g->capacity) return set_error(VF_ECAPACITY, "capacity below root block count");
+    int grid = (int)((n + 255) / 256);
+    if (grid > max_ctas(8)) grid = max_ctas(8);
+    k_init_forest<<<grid, 256, 0, st>>>(cfg.nb[0], cfg.nb[1], cfg.nb[2], g->d_coords, g->d_nbr,
+                                        g->d_nbr_child, g->d_child, g->d_bflags, g->d_masks,
+                                        g->d_level_start, g->d_status);
+    g->n_levels = 1;
+    return check_launch("k_init_forest");
+}
+
+// --------------------------------------------------------------------------
+// marking (pin A12).  aux bits: 1 eligible, 2 solid-boundary.
+
+enum { AUX_ELIG = 1, AUX_SB = 2 };
+
+__global__ void __launch_bounds__(256)
+    k_mark_sb(int L, const int32_t *__restrict__ level_start, const int32_t *__restrict__ nbr,
+              const uint8_t *__restrict__ bflags, uint8_t *__restrict__ aux) {
+    const int32_t s = level_start[L], e = level_start[L + 1];
+    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t *nb = nbr + 27 * b;
+        bool el = true, fluid_nb = false;
+#pragma unroll 2
+        for (int q = 1; q < 27; ++q) {
+            const int32_t v = nb[q];
+            if (v == VF_NB_MISSING || v == VF_NB_SOLID_NBR) el = false;
+            if (v >= 0 && !(bflags[v] & VF_BF_SOLID)) fluid_nb = true;
+        }
+        const bool sb = (bflags[b] & VF_BF_SOLID) && fluid_nb;
+        aux[b] = (uint8_t)((el ? AUX_ELIG : 0) | (sb ? AUX_SB : 0));
+    }
+}
+
+__global__ void __launch_bounds__(256)
+    k_mark_adj(int L, const int32_t *__restrict__ level_start, const int32_t *__restrict__ nbr,
+               uint8_t *__restrict__ bflags, const uint8_t *__restrict__ aux,
+               uint8_t *__restrict__ m0) {
+    const int32_t s = level_start[L], e = level_start[L + 1];
+    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t *nb = nbr + 27 * b;
+        bool has_sb = false;
+#pragma unroll 2
+        for (int q = 1; q < 27; ++q) {
+            const int32_t v = nb[q];
+            if (v >= 0 && (aux[v] & AUX_SB)) has_sb = true;
+        }
+        const uint8_t a = aux[b];
+        const uint8_t f0 = bflags[b];
+        const bool solid = f0 & VF_BF_SOLID, sb = a & AUX_SB, el = a & AUX_ELIG;
+        uint8_t f = (uint8_t)(f0 & ~(VF_BF_SB | VF_BF_SA | VF_BF_MARK));
+        if (sb) f |= VF_BF_SB;
+        if (has_sb && !solid) f |= VF_BF_SA;
+        bflags[b] = f;
+        m0[b] = (uint8_t)(el && (sb || has_sb));
+    }
+}
+
+__global__ void __launch_bounds__(256)
+    k_mark_prop(int L, int it, const int32_t *__restrict__ level_start,
+                const int32_t *__restrict__ nbr, const uint8_t *__restrict__ bflags,
+                const uint8_t *__restrict__ aux, const uint8_t *__restrict__ src,
+                uint8_t *__restrict__ dst) {
+    const int32_t s = level_start[L], e = level_start[L + 1];
+    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        uint8_t m = src[b];
+        if (!m && (aux[b] & AUX_ELIG) && (!(bflags[b] & VF_BF_SOLID) || it == 0)) {
+            const int32_t *nb = nbr + 27 * b;
+            for (int q = 1; q < 27; ++q) {
+                const int32_t v = nb[q];
+                if (v >= 0 && src[v]) { m = 1; break; }
+            }
+        }
+        dst[b] = m;
+    }
+}
+
+__global__ void k_mark_commit(int L, const int32_t *__restrict__ level_start,
+                              const uint8_t *__restrict__ m, uint8_t *__restrict__ bflags) {
+    const int32_t s = level_start[L], e = level_start[L + 1];
+    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
+         b += (int64_t)gridDim.x * blockDim.x)
+        if (m[b]) bflags[b] |= VF_BF_MARK;
+}
+
+size_t mark_workspace_size(int32_t capacity) { return 3 * (((size_t)capacity + 255) & ~(size_t)255); }
+
+int mark_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (ws_bytes < mark_workspace_size(g->capacity)) return set_error(VF_EARG, "mark workspace too small");
+    const size_t stride = ((size_t)g->capacity + 255) & ~(size_t)255;
+    uint8_t *aux = (uint8_t *)ws, *m[2] = {aux + stride, aux + 2 * stride};
+    const int grid = max_ctas(8);
+    k_mark_sb<<<grid, 256, 0, st>>>(L, g->d_level_start, g->d_nbr, g->d_bflags, aux);
+    int rc = check_launch("k_mark_sb");
+    if (rc) return rc;
+    k_mark_adj<<<grid, 256, 0, st>>>(L, g->d_level_start, g->d_nbr, g->d_bflags, aux, m[0]);
+    if ((rc = check_launch("k_mark_adj"))) return rc;
+    int cur = 0;
+    for (int it = 0; it < cfg.n_prop; ++it) {
+        k_mark_prop<<<grid, 256, 0, st>>>(L, it, g->d_level_start, g->d_nbr, g->d_bflags, aux,
+                                          m[cur], m[cur ^ 1]);
+        if ((rc = check_launch("k_mark_prop"))) return rc;
+        cur ^= 1;
+    }
+    k_mark_commit<<<grid, 256, 0, st>>>(L, g->d_level_start, m[cur], g->d_bflags);
+    return check_launch("k_mark_commit");
+}
+
+// --------------------------------------------------------------------------
+// adapt (pins A13, A14)
+
+struct LoadMark {
+    const int32_t *level_start;
+    int L;
+    const uint8_t *bflags;
+    __device__ int operator()(int64_t i) const {
+        return (bflags[level_start[L] + i] & VF_BF_MARK) ? 1 : 0;
+    }
+};
+struct EmitChild {
+    const int32_t *level_start;
+    int L;
+    int32_t *child;
+    uint8_t *bflags;
+    int32_t *parents;
+    __device__ void operator()(int64_t i, int v, int ex) const {
+        const int32_t s = level_start[L], e = level_start[L + 1];
+        const int64_t b = s + i;
+        const uint8_t f = bflags[b];
+        if (v) {
+            child[b] = e + 8 * ex;
+            parents[ex] = (int32_t)b;
+            bflags[b] = (uint8_t)(f | VF_BF_REFINED);
+        } else {
+            child[b] = -1;
+            bflags[b] = (uint8_t)(f & ~VF_BF_REFINED);
+        }
+    }
+};
+
+__global__ void k_level_count(int L, const int32_t *__restrict__ level_start, int32_t *__restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *out = level_start[L + 1] - level_start[L];
+}
+
+__global__ void k_adapt_finish(int L, int32_t capacity, int32_t *__restrict__ level_start,
+                               const int32_t *__restrict__ n_marked, int32_t *__restrict__ status) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int64_t e = level_start[L + 1];
+    int64_t ne = e + 8 * (int64_t)(*n_marked);
+    if (ne > capacity) {
+        atomicMax(status, VF_ECAPACITY);
+        status[1] = L;  // level context
+        ne = e;         // drop the level: later stages see no blocks, no OOB ids
+    }
+    for (int k = L + 2; k <= VF_MAX_LEVELS; ++k) level_start[k] = (int32_t)ne;
+}
+
+// one thread per child: coords, 27 links, ghost layer
+__global__ void __launch_bounds__(256)
+    k_adapt_children(int L, int32_t capacity, int nbx1, int nby1, int nbz1,
+                     const int32_t *__restrict__ level_start, const int32_t *__restrict__ n_marked,
+                     const int32_t *__restrict__ parents, int32_t *__restrict__ coords,
+                     int32_t *__restrict__ nbr, int32_t *__restrict__ nbr_child,
+                     int32_t *__restrict__ child, uint8_t *__restrict__ bflags,
+                     uint8_t *__restrict__ masks, int32_t *__restrict__ status) {
+    const int64_t e = level_start[L + 1];
+    const int64_t nc = 8 * (int64_t)(*n_marked);
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t id = e + c;
+        if (id >= capacity) continue;
+        const int32_t P = parents[c >> 3];
+        const int cc = (int)(c & 7);
+        const int4 pc = reinterpret_cast<const int4 *>(coords)[P];
+        const int ci = 2 * pc.x + (cc & 1), cj = 2 * pc.y + ((cc >> 1) & 1), ck = 2 * pc.z + (cc >> 2);
+        reinterpret_cast<int4 *>(coords)[id] = make_int4(ci, cj, ck, L + 1);
+        uint32_t missing = 0;  // bit q: slot q is MISSING / SOLID_NBR
+        for (int q = 0; q < 27; ++q) {
+            const int ti = ci + c27(q, 0), tj = cj + c27(q, 1), tk = ck + c27(q, 2);
+            int32_t v;
+            if (ti < 0 || tj < 0 || tk < 0 || ti >= nbx1 || tj >= nby1 || tk >= nbz1) {
+                v = VF_NB_OUTSIDE;
+            } else {
+                const int qp = slot_of((ti >> 1) - pc.x, (tj >> 1) - pc.y, (tk >> 1) - pc.z);
+                const int32_t Pn = (qp == 0) ? P : nbr[27 * (int64_t)P + qp];
+                if (Pn < 0) {  // marked parents are eligible: cannot happen
+                    atomicMax(status, VF_EARG);
+                    v = VF_NB_MISSING;
+                } else {
+                    const int32_t ch = child[Pn];
+                    if (ch >= 0)
+                        v = ch + (ti & 1) + 2 * (tj & 1) + 4 * (tk & 1);
+                    else
+                        v = (bflags[Pn] & VF_BF_SOLID) ? VF_NB_SOLID_NBR : VF_NB_MISSING;
+                }
+            }
+            nbr[27 * id + q] = v;
+            nbr_child[27 * id + q] = -1;
+            if (v == VF_NB_MISSING || v == VF_NB_SOLID_NBR) missing |= 1u << q;
+        }
+        child[id] = -1;
+        bflags[id] = 0;
+        // A14 ghost layer: Chebyshev distance <= 2 fine cells from a missing block
+        uint32_t w[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int I = 0; I < 4; ++I) {
+                const int J = r & 3, K = r >> 2;
+                bool ghost = false;
+                if (missing) {
+                    for (int q = 1; q < 27 && !ghost; ++q) {
+                        if (!(missing >> q & 1)) continue;
+                        const int ox = c27(q, 0), oy = c27(q, 1), oz = c27(q, 2);
+                        const bool okx = ox == 0 || (ox < 0 ? I < 2 : I >= 2);
+                        const bool oky = oy == 0 || (oy < 0 ? J < 2 : J >= 2);
+                        const bool okz = oz == 0 || (oz < 0 ? K < 2 : K >= 2);
+                        ghost = okx && oky && okz;
+                    }
+                }
+                x |= (uint32_t)(ghost ? VF_GHOST : VF_FLUID) << (8 * I);
+            }
+            w[r] = x;
+        }
+        uint4 *m = reinterpret_cast<uint4 *>(masks + 64 * id);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) m[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+    }
+}
+
+// level-L neighbour-child links + interface layer of refined blocks (A14)
+__global__ void __launch_bounds__(256)
+    k_adapt_level(int L, const int32_t *__restrict__ level_start, const int32_t *__restrict__ nbr,
+                  int32_t *__restrict__ nbr_child, const int32_t *__restrict__ child,
+                  uint8_t *__restrict__ masks) {
+    const int32_t s = level_start[L], e = level_start[L + 1];
+    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t *nb = nbr + 27 * b;
+        uint32_t coarse = 0;  // bit q: existing unrefined neighbour
+        for (int q = 0; q < 27; ++q) {
+            const int32_t v = (q == 0) ? (int32_t)b : nb[q];
+            const int32_t ch = (v >= 0) ? child[v] : -1;
+            nbr_child[27 * b + q] = ch;
+            if (q > 0 && v >= 0 && ch < 0) coarse |= 1u << q;
+        }
+        if (child[b] < 0 || !coarse) continue;
+        uint32_t *m = reinterpret_cast<uint32_t *>(masks + 64 * b);
+        for (int r = 0; r < 16; ++r) {
+            const int J = r & 3, K = r >> 2;
+            uint32_t x = m[r];
+            const uint32_t x0 = x;
+#pragma unroll
+            for (int I = 0; I < 4; ++I) {
+                if (((x >> (8 * I)) & 0xffu) != VF_FLUID) continue;
+                bool itf = false;
+                for (int q = 1; q < 27 && !itf; ++q) {
+                    if (!(coarse >> q & 1)) continue;
+                    const int ox = c27(q, 0), oy = c27(q, 1), oz = c27(q, 2);
+                    const bool okx = ox == 0 || (ox < 0 ? I == 0 : I == 3);
+                    const bool oky = oy == 0 || (oy < 0 ? J == 0 : J == 3);
+                    const bool okz = oz == 0 || (oz < 0 ? K == 0 : K == 3);
+                    itf = okx && oky && okz;
+                }
+                if (itf) x = (x & ~(0xffu << (8 * I))) | ((uint32_t)VF_INTERFACE << (8 * I));
+            }
+            if (x != x0) m[r] = x;
+        }
+    }
+}
+
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t adapt_workspace_size(int32_t capacity) {
+    return al256(sizeof(int32_t) * ((size_t)capacity + 1)) + al256(sizeof(int32_t) * 8) +
+           al256(scan_workspace_bytes(capacity));
+}
+
+int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (ws_bytes < adapt_workspace_size(g->capacity)) return set_error(VF_EARG, "adapt workspace too small");
+    if (L != g->n_levels - 1 || L + 1 >= VF_MAX_LEVELS) return set_error(VF_EARG, "adapt: level must be the finest");
+    char *base = (char *)ws;
+    int32_t *parents = (int32_t *)base;
+    int32_t *scalars = (int32_t *)(base + al256(sizeof(int32_t) * ((size_t)g->capacity + 1)));
+    void *scan_ws = base + al256(sizeof(int32_t) * ((size_t)g->capacity + 1)) + al256(sizeof(int32_t) * 8);
+    k_level_count<<<1, 32, 0, st>>>(L, g->d_level_start, scalars);
+    int rc = check_launch("k_level_count");
+    if (rc) return rc;
+    cudaError_t ce = scan_launch(LoadMark{g->d_level_start, L, g->d_bflags},
+                                 EmitChild{g->d_level_start, L, g->d_child, g->d_bflags, parents},
+                                 g->capacity, scalars, scalars + 1, scan_ws, st);
+    if (ce != cudaSuccess) return set_cuda_error(ce, "adapt scan");
+    k_adapt_children<<<max_ctas(8), 256, 0, st>>>(
+        L, g->capacity, cfg.nb[0] << (L + 1), cfg.nb[1] << (L + 1), cfg.nb[2] << (L + 1),
+        g->d_level_start, scalars + 1, parents, g->d_coords, g->d_nbr, g->d_nbr_child, g->d_child,
+        g->d_bflags, g->d_masks, g->d_status);
+    if ((rc = check_launch("k_adapt_children"))) return rc;
+    k_adapt_level<<<max_ctas(8), 256, 0, st>>>(L, g->d_level_start, g->d_nbr, g->d_nbr_child,
+                                               g->d_child, g->d_masks);
+    if ((rc = check_launch("k_adapt_level"))) return rc;
+    k_adapt_finish<<<1, 32, 0, st>>>(L, g->capacity, g->d_level_start, scalars + 1, g->d_status);
+    if ((rc = check_launch("k_adapt_finish"))) return rc;
+    g->n_levels = L + 2;
+    return VF_OK;
+}
+
+}  // namespace vf

@@ -1,0 +1,80 @@
+// vf_internal.h -- host-side glue shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/voxforest_b200.h"
+#include "vf_common.cuh"
+
+namespace vf {
+
+// error plumbing (thread-local message, vf_last_error)
+int set_error(int code, const char *msg);
+int set_cuda_error(cudaError_t e, const char *what);
+int check_launch(const char *what);
+
+int sm_count();
+inline int max_ctas(int per_sm) { return sm_count() * per_sm; }
+
+LevelInfo make_level(const vf_config &cfg, int L);
+inline int nlim_of(const vf_config &cfg) {
+    const int a = 2 + cfg.n_spec;
+    return a * a * a;
+}
+
+int launch_iota(int32_t *out, int64_t n, int32_t *d_n, cudaStream_t st);
+
+// scans
+int launch_compact(const uint8_t *ind, int64_t n, int32_t *map, int32_t *d_count, void *ws,
+                   cudaStream_t st);
+int launch_exclusive_scan(const int32_t *in, int64_t n_bound, const int32_t *d_n, int32_t *out,
+                          int32_t *d_total, void *ws, cudaStream_t st);
+
+// bins
+int launch_indicators(const LevelInfo &li, int mode, const double *faces, int64_t F,
+                      uint8_t *out, cudaStream_t st);
+size_t bins_workspace_size(int64_t F, int nlim, int64_t n_bins);
+size_t assemble_workspace_size(int64_t pair_cap, int64_t n_bins);
+int build_bins_impl(const LevelInfo &li, int nlim, const double *faces, int64_t F, int mode,
+                    int use_filter, vf_bins *bins, int32_t *d_status, void *ws, size_t ws_bytes,
+                    cudaStream_t st);
+int sort_bins(int64_t n_bins, const int32_t *offsets, const int32_t *d_total, int32_t *counts,
+              int32_t *face_ids, int32_t *large, int32_t *scalars, int32_t *scratch,
+              cudaStream_t st);
+int bin_pairs_impl(const LevelInfo &li, int nlim, const double *faces, int64_t F,
+                   const int32_t *map, const int32_t *d_n_map, int32_t *pair_bin,
+                   int32_t *pair_face, int64_t pair_cap, int32_t *d_n_pairs, int32_t *d_status,
+                   void *ws, size_t ws_bytes, cudaStream_t st);
+int assemble_impl(const int32_t *pair_bin, const int32_t *pair_face, const int32_t *d_n_pairs,
+                  int64_t pair_cap, int64_t n_bins, int32_t *counts, int32_t *offsets,
+                  int32_t *face_ids, void *ws, size_t ws_bytes, cudaStream_t st);
+
+// voxelizer
+int voxelize_impl(const LevelInfo &li, vf_grid *g, int L, const vf_bins *bins,
+                  const double *faces, cudaStream_t st);
+size_t propagate_workspace_size(int32_t capacity);
+int propagate_impl(const LevelInfo &li, vf_grid *g, int L, int dir, int finalize, void *ws,
+                   size_t ws_bytes, cudaStream_t st);
+int finalize_impl(vf_grid *g, int L, cudaStream_t st);
+
+// forest
+int init_forest_impl(const vf_config &cfg, vf_grid *g, cudaStream_t st);
+size_t mark_workspace_size(int32_t capacity);
+int mark_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_bytes,
+              cudaStream_t st);
+size_t adapt_workspace_size(int32_t capacity);
+int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_bytes,
+               cudaStream_t st);
+
+// boundary / tables / links
+int boundary_impl(vf_grid *g, int32_t *bcount, cudaStream_t st);
+size_t tables_workspace_size(int32_t capacity);
+int tables_impl(vf_grid *g, const int32_t *bcount, int32_t *cmap, int32_t *d_n_b, void *ws,
+                size_t ws_bytes, cudaStream_t st);
+size_t link_workspace_size(const vf_config &cfg, int finest);
+int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
+              int64_t F, const int32_t *map, const int32_t *d_n_map, float *lengths, void *ws,
+              size_t ws_bytes, cudaStream_t st);
+
+}  // namespace vf

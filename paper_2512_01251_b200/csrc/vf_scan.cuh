@@ -1,0 +1,154 @@
+// vf_scan.cuh -- single-pass exclusive prefix scan with decoupled look-back.
+//
+// Used for every "stream compaction / scatter" step of the pipeline
+// (face filtering, bin offsets = Thrust steps 5-9 of PAPER.md:477-479,
+// child-id allocation, contraction map).  The element count may be
+// device-resident (d_n), so a level never needs a host round trip: CTAs
+// whose dynamic tile id lies beyond ceil(n/TILE) exit immediately.
+//
+//   Load(i)  -> int   value of element i (only called for i < n)
+//   Emit(i, v, excl)  called for every i < n with its exclusive prefix
+//   d_total          receives the sum (written by the last tile)
+//
+// Workspace: (tiles + 1) uint64 status words, zeroed by scan_launch.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace vf {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;  // 4096
+
+constexpr uint64_t kFlagAgg = 1ull << 32;
+constexpr uint64_t kFlagPre = 2ull << 32;
+
+__device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_volatile_u64(uint64_t *p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// warp-wide sum (all lanes receive the total)
+__device__ __forceinline__ int warp_sum_scan(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <typename Load, typename Emit>
+__global__ void __launch_bounds__(kScanThreads)
+    scan_kernel(Load load, Emit emit, int64_t n_static, const int32_t *__restrict__ d_n,
+                int32_t *__restrict__ d_total, uint64_t *__restrict__ status) {
+    __shared__ int s_warp[kScanThreads / 32];
+    __shared__ int s_tile;
+    __shared__ int s_prefix;
+    const int64_t n = d_n ? (int64_t)(*d_n) : n_static;
+    const int64_t n_tiles = (n + kScanTile - 1) / kScanTile;
+    uint32_t *counter = reinterpret_cast<uint32_t *>(status);
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(counter, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (n == 0) {
+        if (tile == 0 && threadIdx.x == 0 && d_total) *d_total = 0;
+        return;
+    }
+    if (tile >= n_tiles) return;
+    uint64_t *tstat = status + 1;
+
+    const int64_t base = tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    int vals[kScanItems];
+    int tsum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t i = base + k;
+        vals[k] = (i < n) ? load(i) : 0;
+        tsum += vals[k];
+    }
+    // block-wide exclusive scan of the per-thread sums
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int w = (lane < kScanThreads / 32) ? s_warp[lane] : 0;
+        int wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < kScanThreads / 32) s_warp[lane] = wi - w;  // exclusive warp offsets
+        const int agg = __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
+        // decoupled look-back (warp 0)
+        int prefix = 0;
+        if (tile == 0) {
+            if (lane == 0) st_volatile_u64(&tstat[0], kFlagPre | (uint32_t)agg);
+        } else {
+            if (lane == 0) st_volatile_u64(&tstat[tile], kFlagAgg | (uint32_t)agg);
+            int64_t pred = tile - 1;
+            while (true) {
+                const int64_t idx = pred - lane;
+                uint64_t s;
+                if (idx >= 0) {
+                    do { s = ld_volatile_u64(&tstat[idx]); } while ((s >> 32) == 0);
+                } else {
+                    s = kFlagPre;  // virtual tile with prefix 0
+                }
+                const uint32_t pre_mask = __ballot_sync(0xffffffffu, (s >> 32) == 2);
+                int v = (int)(uint32_t)(s & 0xffffffffu);
+                if (pre_mask) {
+                    const int first = __ffs(pre_mask) - 1;
+                    if (lane > first) v = 0;
+                    prefix += warp_sum_scan(v);
+                    break;
+                }
+                prefix += warp_sum_scan(v);
+                pred -= 32;
+            }
+            if (lane == 0) st_volatile_u64(&tstat[tile], kFlagPre | (uint32_t)(prefix + agg));
+        }
+        if (lane == 0) {
+            s_prefix = prefix;
+            if (tile == n_tiles - 1 && d_total) *d_total = prefix + agg;
+        }
+    }
+    __syncthreads();
+    int run = s_prefix + s_warp[warp] + incl - tsum;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t i = base + k;
+        if (i < n) emit(i, vals[k], run);
+        run += vals[k];
+    }
+}
+
+inline size_t scan_workspace_bytes(int64_t n_bound) {
+    const int64_t tiles = (n_bound + kScanTile - 1) / kScanTile;
+    return (size_t)(tiles + 2) * sizeof(uint64_t);
+}
+
+template <typename Load, typename Emit>
+cudaError_t scan_launch(Load load, Emit emit, int64_t n_bound, const int32_t *d_n,
+                        int32_t *d_total, void *ws, cudaStream_t st) {
+    const int64_t tiles = (n_bound + kScanTile - 1) / kScanTile;
+    cudaError_t e = cudaMemsetAsync(ws, 0, scan_workspace_bytes(n_bound), st);
+    if (e != cudaSuccess) return e;
+    const int64_t grid = tiles > 0 ? tiles : 1;
+    scan_kernel<<<(unsigned)grid, kScanThreads, 0, st>>>(load, emit, n_bound, d_n, d_total,
+                                                        reinterpret_cast<uint64_t *>(ws));
+    return cudaGetLastError();
+}
+
+}  // namespace vf

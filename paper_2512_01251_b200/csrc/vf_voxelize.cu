@@ -1,0 +1,324 @@
+// vf_voxelize.cu -- per-block ray-cast solid voxelizer and x-run propagation
+// (SPEC.md:283-309).
+//
+//   K-vox    one warp per level-L block.  The block's bin faces (its matched
+//            bin, pin A4) are staged 32 at a time in shared memory with their
+//            SAT precomputation; lane = (row r = lane&15, face parity =
+//            lane>>4) so the 16 x-rows x bin-faces slab tests run in parallel,
+//            each hit row evaluates its 4 cell distances, and the two face
+//            parities are merged with the (|d|, face order) tie rule (A7).
+//            A row's 4 masks are one 32-bit word, written back with the A9
+//            rule only when some cell of the block was hit (eta, Alg. 3).
+//            Internal propagation is a provable no-op with matched bins (A8).
+//   K-xfun   per block & row: transfer function of Alg. 5's carried status
+//            (2 x 16-bit masks: output for input SOLID / OTHER).
+//   K-xjump  pointer-jumping composition along same-level x-runs
+//            (ceil(log2 B_L) rounds) -- the sequential chain walk of the paper
+//             becomes an associative segmented scan (A10).
+//   K-xapply status entering each block -> SOLID fill; fused finalize
+//            (GUARD->FLUID, block solid flag).
+#include <math.h>
+
+#include "vf_common.cuh"
+#include "vf_internal.h"
+
+namespace vf {
+
+// --------------------------------------------------------------------------
+// K-vox
+
+struct VoxFace {        // shared-memory face record (21 doubles + flag)
+    SatFace s;
+    double n[3];
+};
+
+constexpr int kVoxWarps = 4;
+
+__global__ void __launch_bounds__(kVoxWarps * 32)
+    k_voxelize(LevelInfo li, int L, const int32_t *__restrict__ level_start,
+               const int32_t *__restrict__ coords, uint8_t *__restrict__ masks,
+               const int32_t *__restrict__ counts, const int32_t *__restrict__ offsets,
+               const int32_t *__restrict__ face_ids, const double *__restrict__ faces) {
+    __shared__ VoxFace s_face[kVoxWarps][32];
+    __shared__ uint8_t s_skip[kVoxWarps][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * kVoxWarps + wib, nw = (int64_t)gridDim.x * kVoxWarps;
+    const int32_t s = level_start[L], e = level_start[L + 1];
+    const int r = lane & 15, half = lane >> 4;
+    const int J = r & 3, K = r >> 2;
+    const double dx = li.dx, eps = li.eps, lx = li.len[0];
+    uint32_t *masks32 = reinterpret_cast<uint32_t *>(masks);
+
+    for (int64_t b = s + gw; b < e; b += nw) {
+        const int4 co = *reinterpret_cast<const int4 *>(coords + 4 * b);
+        const int64_t bin = co.x + (int64_t)li.bins[0] * (co.y + (int64_t)li.bins[1] * co.z);
+        const int n_f = counts[bin];
+        if (n_f == 0) continue;  // warp-uniform
+        const int32_t off = offsets[bin];
+        const double y = node_c(4 * co.y + J, dx), z = node_c(4 * co.z + K, dx);
+        const double my = VF_DSUB(y, eps), My = VF_DADD(y, eps);
+        const double mz = VF_DSUB(z, eps), Mz = VF_DADD(z, eps);
+        double x[4];
+#pragma unroll
+        for (int I = 0; I < 4; ++I) x[I] = node_c(4 * co.x + I, dx);
+        double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+        int bp[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+        uint32_t bh = 0;  // 4 x 8-bit masks, the row's new values
+
+        for (int base = 0; base < n_f; base += 32) {
+            const int cnt = min(32, n_f - base);
+            if (lane < cnt) {
+                const int64_t f = face_ids[off + base + lane];
+                double v[9], nn[3];
+                load_face(faces, f, v, nn);
+                VoxFace &vf_ = s_face[wib][lane];
+                sat_face_init(vf_.s, v);
+                vf_.n[0] = nn[0]; vf_.n[1] = nn[1]; vf_.n[2] = nn[2];
+                s_skip[wib][lane] = fabs(nn[0]) < li.eps_par;  // A7: no x distance
+            }
+            __syncwarp();
+            for (int q = half; q < cnt; q += 2) {
+                if (s_skip[wib][q]) continue;
+                const VoxFace &F = s_face[wib][q];
+                if (!sat_exact(F.s, 0.0, my, mz, lx, My, Mz)) continue;
+                const double nx = F.n[0];
+#pragma unroll
+                for (int I = 0; I < 4; ++I) {
+                    const double d = VF_DDIV(plane_num(F.s.v, F.n, x[I], y, z), nx);
+                    const double ad = fabs(d);
+                    if (ad < bd[I]) {  // strict: earlier (lower id) face wins ties
+                        bd[I] = ad;
+                        bp[I] = base + q;
+                        const uint32_t hv = (VF_DMUL(nx, d) > 0.0) ? VF_SOLID : VF_GUARD;
+                        bh = (bh & ~(0xffu << (8 * I))) | (hv << (8 * I));
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        // merge the two face parities of each row: smaller |d|, then lower face order
+        uint32_t hit = 0;
+#pragma unroll
+        for (int I = 0; I < 4; ++I) {
+            const double od = __shfl_xor_sync(0xffffffffu, bd[I], 16);
+            const int op = __shfl_xor_sync(0xffffffffu, bp[I], 16);
+            const uint32_t oh = __shfl_xor_sync(0xffffffffu, bh, 16);
+            if (od < bd[I] || (od == bd[I] && op < bp[I])) {
+                bd[I] = od;
+                bp[I] = op;
+                bh = (bh & ~(0xffu << (8 * I))) | (oh & (0xffu << (8 * I)));
+            }
+            if (bd[I] < INFINITY) hit |= 1u << I;
+        }
+        const bool any = __any_sync(0xffffffffu, hit != 0);
+        if (!any || half) continue;  // eta == 0 -> no write (Alg. 3 l.648)
+        uint32_t *w = masks32 + b * 16 + r;
+        const uint32_t orig = *w;
+        uint32_t out = orig;
+#pragma unroll
+        for (int I = 0; I < 4; ++I) {
+            if (!(hit >> I & 1)) continue;
+            const uint32_t o = (orig >> (8 * I)) & 0xffu, hn = (bh >> (8 * I)) & 0xffu;
+            // A9 write rule
+            if (hn == VF_SOLID || (o != VF_GHOST && o != VF_INTERFACE))
+                out = (out & ~(0xffu << (8 * I))) | (hn << (8 * I));
+        }
+        if (out != orig) *w = out;
+    }
+}
+
+int voxelize_impl(const LevelInfo &li, vf_grid *g, int L, const vf_bins *bins,
+                  const double *faces, cudaStream_t st) {
+    k_voxelize<<<max_ctas(8), kVoxWarps * 32, 0, st>>>(li, L, g->d_level_start, g->d_coords,
+                                                      g->d_masks, bins->d_counts, bins->d_offsets,
+                                                      bins->d_face_ids, faces);
+    return check_launch("k_voxelize");
+}
+
+// --------------------------------------------------------------------------
+// Alg. 5 as a scan.  Per block b and row r (16 rows), with H3 the row's
+// trailing cell (I=3 for +x, I=0 for -x):
+//   f_b(SOLID) = (H3 != GUARD),  f_b(OTHER) = (H3 == SOLID)      (1 = SOLID)
+// packed as A | B << 16.  A run start (back slot < 0) carries the constant
+// f_b(sigma) with sigma = SOLID iff its back code is SOLID_NBR.
+
+__device__ __forceinline__ uint32_t compose(uint32_t g, uint32_t f) {
+    // (g o f)(x) = g(f(x)); per row: f(x)=1 -> g(S) else g(O)
+    const uint32_t gA = g & 0xffffu, gB = g >> 16, fA = f & 0xffffu, fB = f >> 16;
+    const uint32_t A = (fA & gA) | (~fA & gB & 0xffffu);
+    const uint32_t B = (fB & gA) | (~fB & gB & 0xffffu);
+    return A | (B << 16);
+}
+
+__device__ __forceinline__ void load_masks64(const uint8_t *masks, int64_t b, uint32_t w[16]) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(masks + 64 * b);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint4 u = p[k];
+        w[4 * k] = u.x; w[4 * k + 1] = u.y; w[4 * k + 2] = u.z; w[4 * k + 3] = u.w;
+    }
+}
+
+__device__ __forceinline__ void store_masks64(uint8_t *masks, int64_t b, const uint32_t w[16]) {
+    uint4 *p = reinterpret_cast<uint4 *>(masks + 64 * b);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+}
+
+__global__ void __launch_bounds__(256)
+    k_xfun(int L, int back, int trail, const int32_t *__restrict__ level_start,
+           const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
+           uint32_t *__restrict__ G, int32_t *__restrict__ P) {
+    const int32_t s = level_start[L], e = level_start[L + 1];
+    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t w[16];
+        load_masks64(masks, b, w);
+        uint32_t A = 0, B = 0;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const uint32_t h3 = (w[r] >> (8 * trail)) & 0xffu;
+            A |= (uint32_t)(h3 != VF_GUARD) << r;
+            B |= (uint32_t)(h3 == VF_SOLID) << r;
+        }
+        const int32_t code = nbr[27 * b + back];
+        uint32_t fn = A | (B << 16);
+        if (code < 0) {
+            const uint32_t c = (code == VF_NB_SOLID_NBR) ? A : B;  // f_b(sigma)
+            fn = c | (c << 16);
+        }
+        G[b] = fn;
+        P[b] = code < 0 ? -1 : code;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+    k_xjump(int L, const int32_t *__restrict__ level_start, const uint32_t *__restrict__ Gi,
+            const int32_t *__restrict__ Pi, uint32_t *__restrict__ Go, int32_t *__restrict__ Po) {
+    const int32_t s = level_start[L], e = level_start[L + 1];
+    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t p = Pi[b];
+        uint32_t g = Gi[b];
+        int32_t pn = -1;
+        if (p >= 0) {
+            g = compose(g, Gi[p]);
+            pn = Pi[p];
+        }
+        Go[b] = g;
+        Po[b] = pn;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+    k_xapply(int L, int back, int finalize, const int32_t *__restrict__ level_start,
+             const int32_t *__restrict__ nbr, uint8_t *__restrict__ masks,
+             const uint32_t *__restrict__ G, uint8_t *__restrict__ bflags) {
+    const int32_t s = level_start[L], e = level_start[L + 1];
+    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t pred = nbr[27 * b + back];
+        uint32_t w[16];
+        load_masks64(masks, b, w);
+        bool changed = false;
+        if (pred >= 0) {
+            const uint32_t st = G[pred] & 0xffffu;  // constant: status leaving pred
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                uint32_t x = w[r];
+#pragma unroll
+                for (int I = 0; I < 4; ++I) {
+                    const uint32_t h = (x >> (8 * I)) & 0xffu;
+                    uint32_t hn = h;
+                    if ((st >> r & 1u) && h != VF_GUARD) hn = VF_SOLID;
+                    if (L == 0 && hn == VF_GUARD) hn = VF_FLUID;
+                    x = (x & ~(0xffu << (8 * I))) | (hn << (8 * I));
+                }
+                changed |= (x != w[r]);
+                w[r] = x;
+            }
+        }
+        if (finalize) {
+            bool solid = false;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                uint32_t x = w[r];
+#pragma unroll
+                for (int I = 0; I < 4; ++I) {
+                    const uint32_t h = (x >> (8 * I)) & 0xffu;
+                    if (h == VF_GUARD) x &= ~(0xffu << (8 * I));  // -> FLUID (0)
+                    solid |= (h == VF_SOLID);
+                }
+                changed |= (x != w[r]);
+                w[r] = x;
+            }
+            const uint8_t f0 = bflags[b];
+            bflags[b] = (uint8_t)((f0 & ~VF_BF_SOLID) | (solid ? VF_BF_SOLID : 0));
+        }
+        if (changed) store_masks64(masks, b, w);
+    }
+}
+
+__global__ void __launch_bounds__(256)
+    k_finalize(int L, const int32_t *__restrict__ level_start, uint8_t *__restrict__ masks,
+               uint8_t *__restrict__ bflags) {
+    const int32_t s = level_start[L], e = level_start[L + 1];
+    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t w[16];
+        load_masks64(masks, b, w);
+        bool solid = false, changed = false;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            uint32_t x = w[r];
+#pragma unroll
+            for (int I = 0; I < 4; ++I) {
+                const uint32_t h = (x >> (8 * I)) & 0xffu;
+                if (h == VF_GUARD) x &= ~(0xffu << (8 * I));
+                solid |= (h == VF_SOLID);
+            }
+            changed |= (x != w[r]);
+            w[r] = x;
+        }
+        if (changed) store_masks64(masks, b, w);
+        const uint8_t f0 = bflags[b];
+        bflags[b] = (uint8_t)((f0 & ~VF_BF_SOLID) | (solid ? VF_BF_SOLID : 0));
+    }
+}
+
+size_t propagate_workspace_size(int32_t capacity) {
+    return 4 * ((size_t)capacity * sizeof(int32_t) + 256);
+}
+
+int propagate_impl(const LevelInfo &li, vf_grid *g, int L, int dir, int finalize, void *ws,
+                   size_t ws_bytes, cudaStream_t st) {
+    if (ws_bytes < propagate_workspace_size(g->capacity))
+        return set_error(VF_EARG, "propagate workspace too small");
+    const size_t stride = ((size_t)g->capacity * sizeof(int32_t) + 255) & ~(size_t)255;
+    char *base = (char *)ws;
+    uint32_t *G[2] = {(uint32_t *)base, (uint32_t *)(base + stride)};
+    int32_t *P[2] = {(int32_t *)(base + 2 * stride), (int32_t *)(base + 3 * stride)};
+    const int back = dir > 0 ? 2 : 1, trail = dir > 0 ? 3 : 0;
+    const int grid = max_ctas(8);
+    k_xfun<<<grid, 256, 0, st>>>(L, back, trail, g->d_level_start, g->d_nbr, g->d_masks, G[0], P[0]);
+    int rc = check_launch("k_xfun");
+    if (rc) return rc;
+    int rounds = 0;
+    while ((1 << rounds) < li.bins[0]) ++rounds;  // runs are at most B_L,x blocks long
+    int cur = 0;
+    for (int k = 0; k < rounds; ++k) {
+        k_xjump<<<grid, 256, 0, st>>>(L, g->d_level_start, G[cur], P[cur], G[cur ^ 1], P[cur ^ 1]);
+        if ((rc = check_launch("k_xjump"))) return rc;
+        cur ^= 1;
+    }
+    k_xapply<<<grid, 256, 0, st>>>(L, back, finalize, g->d_level_start, g->d_nbr, g->d_masks,
+                                   G[cur], g->d_bflags);
+    return check_launch("k_xapply");
+}
+
+int finalize_impl(vf_grid *g, int L, cudaStream_t st) {
+    k_finalize<<<max_ctas(8), 256, 0, st>>>(L, g->d_level_start, g->d_masks, g->d_bflags);
+    return check_launch("k_finalize");
+}
+
+}  // namespace vf

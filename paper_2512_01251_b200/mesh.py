@@ -16,12 +16,10 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from .errors import MeshError
+
 __all__ = ["TriangleMesh", "Aabb", "make_icosphere", "make_torus", "translate",
            "l_spec_bound", "refine_faces", "mesh_arrays"]
-
-
-class MeshError(ValueError):
-    """Mirrors geometry.py:28 (MeshError)."""
 
 
 @dataclass(frozen=True)

@@ -1,0 +1,250 @@
+"""voxelizer -- level-by-level solid voxelization, near-wall refinement,
+boundary cells and the cut-link LUT on the GPU.
+
+Drop-in for the SPEC ops of ``voxforest.voxelizer``:
+  partial_surface_voxelize(grid, L, bins, mesh)   Alg. 3
+  propagate_external(grid, L, direction)          Alg. 5
+  finalize_masks(grid, L)
+  mark_near_wall_refinement(grid, L, d_spec)
+  identify_boundary_cells(grid)
+  build_boundary_tables(grid, counts)
+  compute_link_lengths(grid, bins, mesh, table)
+  embed_geometry(grid, mesh, config)              SPEC.md:346-354 (native driver)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import List, Optional, Tuple
+
+from . import _lib, _ws
+from .config import EmbedConfig
+from .datatypes import BinLevel, ForestGrid, LinkTable, as_device_mesh
+
+
+def _bins_struct(bins: BinLevel):
+    b = bins._struct()
+    return b
+
+
+def partial_surface_voxelize(grid: ForestGrid, level: int, bins: BinLevel, mesh) -> ForestGrid:
+    lib = _lib.require_cuda()
+    dm = as_device_mesh(mesh)
+    gs = grid._struct()
+    c = _lib.make_config(grid.cfg)
+    b = _bins_struct(bins)
+    _lib.check(lib.vf_voxelize_level(C.byref(c), C.byref(gs), int(level), C.byref(b),
+                                     _lib.ptr(dm.faces), _lib.stream_ptr()),
+               "partial_surface_voxelize")
+    return grid
+
+
+def propagate_external(grid: ForestGrid, level: int, direction: int = +1,
+                       finalize: bool = False) -> ForestGrid:
+    """direction +1 = +x (all levels), -1 = -x (L > 0 only)."""
+    lib = _lib.require_cuda()
+    gs = grid._struct()
+    c = _lib.make_config(grid.cfg)
+    ws = _ws.get("propagate", lib.vf_propagate_workspace_size(C.byref(gs)))
+    _lib.check(lib.vf_propagate_x(C.byref(c), C.byref(gs), int(level), int(direction),
+                                  int(bool(finalize)), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()),
+               "propagate_external")
+    return grid
+
+
+def finalize_masks(grid: ForestGrid, level: int) -> ForestGrid:
+    lib = _lib.require_cuda()
+    gs = grid._struct()
+    c = _lib.make_config(grid.cfg)
+    _lib.check(lib.vf_finalize_level(C.byref(c), C.byref(gs), int(level), _lib.stream_ptr()),
+               "finalize_masks")
+    return grid
+
+
+def mark_near_wall_refinement(grid: ForestGrid, level: int, d_spec: Optional[float] = None):
+    """Sets SB/SA/MARK block bits on level L; returns the level's mark mask."""
+    lib = _lib.require_cuda()
+    cfg = grid.cfg if d_spec is None else dataclasses.replace(grid.cfg, d_spec=float(d_spec))
+    gs = grid._struct()
+    c = _lib.make_config(cfg)
+    ws = _ws.get("mark", lib.vf_mark_workspace_size(C.byref(gs)))
+    _lib.check(lib.vf_mark_level(C.byref(c), C.byref(gs), int(level), _lib.ptr(ws), ws.numel(),
+                                 _lib.stream_ptr()), "mark_near_wall_refinement")
+    s, e = grid.level_range(level)
+    return (grid.bflags[s:e] & _lib.BF_MARK) != 0
+
+
+def identify_boundary_cells(grid: ForestGrid):
+    """Finest level: FLUID cells with a SOLID same-level neighbour among the 26
+    become BOUNDARY; returns per-block counts (capacity,) int32."""
+    import torch
+    lib = _lib.require_cuda()
+    gs = grid._struct()
+    c = _lib.make_config(grid.cfg)
+    counts = torch.empty(grid.capacity, dtype=torch.int32, device="cuda")
+    _lib.check(lib.vf_boundary_cells(C.byref(c), C.byref(gs), _lib.ptr(counts), _lib.stream_ptr()),
+               "identify_boundary_cells")
+    return counts
+
+
+def build_boundary_tables(grid: ForestGrid, counts) -> LinkTable:
+    """Contraction map (ascending block id) and LUT allocation, lengths = -1."""
+    import torch
+    lib = _lib.require_cuda()
+    gs = grid._struct()
+    c = _lib.make_config(grid.cfg)
+    cmap = torch.empty(grid.capacity, dtype=torch.int32, device="cuda")
+    nb = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ws = _ws.get("tables", lib.vf_tables_workspace_size(C.byref(gs)))
+    _lib.check(lib.vf_link_tables(C.byref(c), C.byref(gs), _lib.ptr(counts), _lib.ptr(cmap),
+                                  _lib.ptr(nb), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()),
+               "build_boundary_tables")
+    n_b = int(nb.item())
+    lengths = torch.full((n_b, 27, 64), -1.0, dtype=torch.float32, device="cuda")
+    bc_ids = torch.zeros((n_b, 27, 64), dtype=torch.int8, device="cuda")
+    return LinkTable(lengths, bc_ids, cmap[:grid.n_used], n_b)
+
+
+def compute_link_lengths(grid: ForestGrid, bins: Optional[BinLevel], mesh,
+                         table: LinkTable) -> LinkTable:
+    """Fill ``table.lengths`` with q = d/dx in (0, 1] (min over faces) for every
+    cell of every mapped block and q = 1..26; -1 where no wall is within one
+    link.  ``bins`` (all-directions BinLevel) only restricts the face set via
+    its filter map; the result is invariant to it."""
+    lib = _lib.require_cuda()
+    dm = as_device_mesh(mesh)
+    gs = grid._struct()
+    c = _lib.make_config(grid.cfg)
+    ws = _ws.get("links", lib.vf_link_workspace_size(C.byref(c), C.byref(gs)))
+    fmap = n_map = None
+    keep = []
+    if bins is not None and bins.filter_map is not None:
+        import torch
+        fmap = bins.filter_map.compact_map.to(torch.int32).contiguous()
+        n_map = torch.tensor([fmap.numel()], dtype=torch.int32, device="cuda")
+        keep = [fmap, n_map]
+    cmap_full = table.contraction_map
+    if cmap_full.numel() < grid.capacity:
+        import torch
+        full = torch.full((grid.capacity,), -1, dtype=torch.int32, device="cuda")
+        full[:cmap_full.numel()] = cmap_full
+        cmap_full = full
+    _lib.check(lib.vf_link_lengths(C.byref(c), C.byref(gs), _lib.ptr(cmap_full), _lib.ptr(dm.faces),
+                                   dm.n_faces, _lib.ptr(fmap), _lib.ptr(n_map),
+                                   _lib.ptr(table.lengths), _lib.ptr(ws), ws.numel(),
+                                   _lib.stream_ptr()), "compute_link_lengths")
+    del keep
+    return table
+
+
+# ---------------------------------------------------------------------------
+# embed_geometry: one native driver call per phase, no host sync inside a level
+
+@dataclasses.dataclass
+class EmbedTimings:
+    """Per-stage device times (ms) grouped like the paper's table
+    (PAPER.md:1052-1080 / SPEC.md:498)."""
+    binning: float = 0.0
+    voxelization: float = 0.0
+    refinement: float = 0.0
+    boundary: float = 0.0
+    links: float = 0.0
+    total: float = 0.0
+
+
+class EmbedEngine:
+    """Reusable embed context: device mesh, grid, workspace and the LUT are
+    allocated once for (mesh, cfg) and reused across calls (the geometry is
+    static)."""
+
+    def __init__(self, mesh, cfg: EmbedConfig, capacity: Optional[int] = None):
+        import torch
+        self.lib = _lib.require_cuda()
+        self.cfg = cfg
+        self.mesh = as_device_mesh(mesh)
+        cap = int(capacity if capacity is not None else cfg.block_capacity(self.mesh.area))
+        self.grid = ForestGrid.allocate(cfg, cap)
+        self.c = _lib.make_config(cfg)
+        wsb = self.lib.vf_embed_workspace_size(C.byref(self.c), self.mesh.n_faces, cap)
+        if wsb == 0:
+            raise ValueError("invalid embed configuration")
+        self.ws = torch.empty(int(wsb), dtype=torch.uint8, device="cuda")
+        self.cmap = torch.empty(cap, dtype=torch.int32, device="cuda")
+        self.n_b_dev = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.n_b_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self.lengths = None
+        self.bc_ids = None
+        self.n_events = 64
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(self.n_events)]
+        self._ev_arr = (C.c_void_p * self.n_events)(*[C.c_void_p(e.cuda_event) for e in self.events])
+
+    def _ensure_events(self):
+        for e in self.events:   # lazily created by torch on first record
+            e.record()
+        self._ev_arr = (C.c_void_p * self.n_events)(*[C.c_void_p(e.cuda_event) for e in self.events])
+
+    def run(self, timed: bool = False, use_filter: Optional[bool] = None):
+        """Full embed.  Returns (grid, LinkTable).  One host sync (N_b, for the
+        LUT allocation)."""
+        import torch
+        lib, g = self.lib, self.grid
+        uf = self.cfg.use_filter if use_filter is None else use_filter
+        if timed:
+            self._ensure_events()
+        st = _lib.stream_ptr()
+        gs = g._struct()
+        ev = C.cast(self._ev_arr, C.POINTER(C.c_void_p)) if timed else None
+        _lib.check(lib.vf_embed_phase1(C.byref(self.c), _lib.ptr(self.mesh.faces), self.mesh.n_faces,
+                                       int(bool(uf)), C.byref(gs), _lib.ptr(self.cmap),
+                                       _lib.ptr(self.n_b_dev), _lib.ptr(self.ws), self.ws.numel(),
+                                       st, ev), "embed_geometry")
+        g.n_levels = gs.n_levels
+        self.n_b_host.copy_(self.n_b_dev, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        _lib.check(lib.vf_check_status(C.byref(gs), st), "embed_geometry")
+        n_b = int(self.n_b_host[0])
+        if self.lengths is None or self.lengths.shape[0] < n_b:
+            self.lengths = torch.empty((max(n_b, 1), 27, 64), dtype=torch.float32, device="cuda")
+            self.bc_ids = torch.zeros((max(n_b, 1), 27, 64), dtype=torch.int8, device="cuda")
+        lengths = self.lengths[:n_b]
+        lengths.fill_(-1.0)
+        _lib.check(lib.vf_embed_phase2(C.byref(self.c), _lib.ptr(self.mesh.faces), self.mesh.n_faces,
+                                       C.byref(gs), _lib.ptr(self.cmap), _lib.ptr(lengths),
+                                       _lib.ptr(self.ws), self.ws.numel(), st), "embed_geometry")
+        if timed:
+            self.events[self.n_events - 1].record()
+        table = LinkTable(lengths, self.bc_ids[:n_b], self.cmap, n_b)
+        return g, table
+
+    def timings(self) -> EmbedTimings:
+        """Stage split of the last timed run (call after synchronize)."""
+        ev = self.events
+        L = self.cfg.l_max
+        t = EmbedTimings()
+        k = 0
+        for lv in range(L):
+            t.binning += ev[k].elapsed_time(ev[k + 1])
+            t.voxelization += ev[k + 1].elapsed_time(ev[k + 2])
+            k += 2
+            if lv < L - 1:
+                t.refinement += ev[k].elapsed_time(ev[k + 1])
+                k += 1
+        t.boundary = ev[k].elapsed_time(ev[k + 1])
+        t.links = ev[k + 1].elapsed_time(ev[self.n_events - 1])
+        t.total = ev[0].elapsed_time(ev[self.n_events - 1])
+        return t
+
+    def cells_classified(self) -> int:
+        """Sum over levels of 64 * blocks."""
+        return 64 * self.grid.n_used
+
+
+def embed_geometry(grid: Optional[ForestGrid], mesh, cfg: EmbedConfig,
+                   capacity: Optional[int] = None) -> Tuple[ForestGrid, LinkTable]:
+    """build the forest level by level around the mesh and
+    return (grid, LinkTable).  ``grid`` may be a fresh root grid from
+    init_forest (its capacity is reused) or None."""
+    if grid is not None and capacity is None:
+        capacity = grid.capacity
+    eng = EmbedEngine(mesh, cfg, capacity)
+    return eng.run()

@@ -1,0 +1,300 @@
+"""GPU parity tests: every CUDA stage against the CPU oracle on the same inputs
+(bit-exact for masks, flags, topology, bins; link lengths <= 1e-5 relative, the
+north-star FP32 tolerance), called through the C-ABI via the package API."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2512_01251_b200 import EmbedConfig, make_icosphere, make_torus  # noqa: E402
+from paper_2512_01251_b200 import binning, forest, voxelizer  # noqa: E402
+from paper_2512_01251_b200.datatypes import ForestGrid, as_device_mesh  # noqa: E402
+from paper_2512_01251_b200.mesh import translate  # noqa: E402
+from paper_2512_01251_b200.voxelizer import EmbedEngine  # noqa: E402
+
+LINK_RTOL = 1e-5  # north star: cut-link distances within 1e-5 relative (FP32)
+
+
+@pytest.fixture(scope="module")
+def O(oracle_mod):
+    return oracle_mod
+
+
+@pytest.fixture(scope="module")
+def sphere():
+    return make_icosphere((0.5, 0.5, 0.5), 0.5, 4)
+
+
+@pytest.fixture(scope="module")
+def torus():
+    return translate(make_torus(70, 40), (0.0031, -0.0017, 0.0023))
+
+
+def grid_equal(gpu, ref, n=None, keys=("coords", "nbr", "nbr_child", "child", "bflags", "masks")):
+    n = ref.n_used if n is None else n
+    for k in keys:
+        a = gpu[k][:n]
+        b = getattr(ref, k)[:n]
+        if not np.array_equal(a, b):
+            bad = np.argwhere(a != b)
+            raise AssertionError(f"{k}: {len(bad)} mismatches, first at {bad[:5].tolist()}")
+
+
+def check_links(lg, lr):
+    assert lg.shape == lr.shape
+    neg = lr < 0
+    assert np.array_equal(lg < 0, neg), "-1 pattern differs"
+    assert np.all(lg[neg] == -1.0)
+    if (~neg).any():
+        rel = np.abs(lg[~neg] - lr[~neg]) / np.abs(lr[~neg])
+        assert rel.max() <= LINK_RTOL, rel.max()
+
+
+def test_sat_golden():
+    import ctypes as C
+    from paper_2512_01251_b200 import _lib
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "sat_golden.npz"))
+    lib = _lib.require_cuda()
+    tri = torch.from_numpy(z["tri"]).cuda()
+    box = torch.from_numpy(z["box"]).cuda()
+    out = torch.empty(len(z["out"]), dtype=torch.uint8, device="cuda")
+    _lib.check(lib.vf_sat_batch(_lib.ptr(tri), _lib.ptr(box), len(out), _lib.ptr(out),
+                                _lib.stream_ptr()))
+    got = out.cpu().numpy().astype(bool)
+    assert np.array_equal(got, z["out"]), int((got != z["out"]).sum())
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("L", [0, 1, 2])
+def test_ray_indicators(O, sphere, mode, L):
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    got = binning.compute_ray_indicators(sphere, L, mode, cfg).cpu().numpy()
+    ref = O.ray_indicators(sphere.faces_coord, sphere.normals, cfg, L, mode)
+    assert np.array_equal(got, ref)
+
+
+def test_compact(O):
+    rng = np.random.default_rng(0)
+    for n in (0, 1, 5, 4096, 4097, 100003):
+        ind = (rng.random(n) < 0.3).astype(np.uint8)
+        fm = binning.compact_filtered_faces(torch.from_numpy(ind).cuda())
+        assert np.array_equal(fm.compact_map.cpu().numpy(), O.compact(ind))
+    fm = binning.compact_filtered_faces(torch.tensor([0, 1, 1, 0, 1], dtype=torch.uint8))
+    assert fm.compact_map.cpu().tolist() == [1, 2, 4]
+
+
+@pytest.mark.parametrize("L", [0, 2])
+def test_bin_pairs_and_assemble(O, torus, L):
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    ind = O.ray_indicators(torus.faces_coord, torus.normals, cfg, L, 0)
+    fmap_np = O.compact(ind)
+    pb_r, pf_r = O.bin_pairs(torus.faces_coord, fmap_np, cfg, L)
+    fm = binning.FilterMap(None, torch.from_numpy(fmap_np).cuda())
+    pb, pf = binning.compute_bin_pairs(torus, fm, L, cfg)
+    assert np.array_equal(pb.cpu().numpy(), pb_r)
+    assert np.array_equal(pf.cpu().numpy(), pf_r)
+    bl = binning.assemble_bins((pb, pf), cfg.n_bins(L), L, cfg.bins(L))
+    c, o, f = bl.to_numpy()
+    cr, orr, fr = O.assemble(pb_r, pf_r, cfg.n_bins(L))
+    assert np.array_equal(c, cr) and np.array_equal(o, orr) and np.array_equal(f, fr)
+
+
+def test_assemble_spec_example():
+    # [(2,f0),(0,f1),(2,f3)] -> counts{0:1,2:2}, offsets{0:0,2:1}, [f1,f0,f3]
+    pb = torch.tensor([2, 0, 2], dtype=torch.int32)
+    pf = torch.tensor([0, 1, 3], dtype=torch.int32)
+    bl = binning.assemble_bins((pb, pf), 4)
+    c, o, f = bl.to_numpy()
+    assert c.tolist() == [1, 0, 2, 0] and o[0] == 0 and o[2] == 1 and f.tolist() == [1, 0, 3]
+
+
+def test_assemble_large_bins(O):
+    # long bins exercise the CTA rank sort; random emission order
+    rng = np.random.default_rng(3)
+    n_bins, P = 64, 60000
+    pb = rng.integers(0, 8, size=P).astype(np.int32) * 8
+    pf = rng.permutation(P).astype(np.int32)
+    bl = binning.assemble_bins((torch.from_numpy(pb), torch.from_numpy(pf)), n_bins)
+    c, o, f = bl.to_numpy()
+    cr, orr, fr = O.assemble(pb, pf, n_bins)
+    assert np.array_equal(c, cr) and np.array_equal(o, orr)
+    for b in range(n_bins):  # within a bin: ascending face ids
+        assert np.array_equal(np.sort(fr[orr[b]:orr[b] + cr[b]]), f[o[b]:o[b] + c[b]])
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("use_filter", [True, False])
+def test_build_level(O, sphere, mode, use_filter):
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    for L in range(3):
+        bl = binning.build_level(sphere, L, cfg, mode, use_filter)
+        c, o, f = bl.to_numpy()
+        cr, orr, fr = O.build_bins(sphere.faces_coord, sphere.normals, cfg, L, mode, use_filter)
+        assert np.array_equal(c, cr) and np.array_equal(o, orr) and np.array_equal(f, fr)
+
+
+def _oracle_state_through(O, mesh, cfg, upto_level, stage):
+    """Run the oracle pipeline and return the grid state just before `stage`
+    at level `upto_level`."""
+    cap = cfg.block_capacity(mesh.face_areas().sum())
+    g = O.init_forest(cfg, cap)
+    fc, nrm = mesh.faces_coord, mesh.normals
+    for L in range(cfg.l_max):
+        bins = O.build_bins(fc, nrm, cfg, L)
+        if L == upto_level and stage == "voxelize":
+            return g, bins
+        O.voxelize_level(g, cfg, L, bins, fc, nrm)
+        if L == upto_level and stage == "propagate+":
+            return g, bins
+        O.propagate(g, cfg, L, +1)
+        if L == upto_level and stage == "propagate-":
+            return g, bins
+        if L > 0:
+            O.propagate(g, cfg, L, -1)
+        if L == upto_level and stage == "finalize":
+            return g, bins
+        O.finalize(g, cfg, L)
+        if L == upto_level and stage == "mark":
+            return g, bins
+        if L == cfg.l_max - 1:
+            return g, bins
+        O.mark(g, cfg, L)
+        if L == upto_level and stage == "adapt":
+            return g, bins
+        O.adapt(g, cfg, L)
+    return g, None
+
+
+def _gpu_grid(cfg, g):
+    return ForestGrid.from_numpy(cfg, dict(coords=g.coords, nbr=g.nbr, nbr_child=g.nbr_child,
+                                           child=g.child, bflags=g.bflags, masks=g.masks,
+                                           level_start=g.level_start, n_levels=g.n_levels))
+
+
+@pytest.mark.parametrize("L", [0, 1, 2])
+def test_stage_voxelize(O, torus, L):
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    g, bins = _oracle_state_through(O, torus, cfg, L, "voxelize")
+    gg = _gpu_grid(cfg, g)
+    bl = binning.BinLevel(L, cfg.bins(L), *(torch.from_numpy(a).cuda() for a in (bins[2], bins[0], bins[1])))
+    voxelizer.partial_surface_voxelize(gg, L, bl, torus)
+    O.voxelize_level(g, cfg, L, bins, torus.faces_coord, torus.normals)
+    grid_equal(gg.to_numpy(), g)
+
+
+@pytest.mark.parametrize("L", [0, 1, 2])
+@pytest.mark.parametrize("stage", ["propagate+", "propagate-", "finalize"])
+def test_stage_propagate(O, torus, L, stage):
+    if stage == "propagate-" and L == 0:
+        pytest.skip("no -x pass on the root grid (PAPER.md:770)")
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    g, _ = _oracle_state_through(O, torus, cfg, L, stage)
+    gg = _gpu_grid(cfg, g)
+    if stage == "propagate+":
+        voxelizer.propagate_external(gg, L, +1)
+        O.propagate(g, cfg, L, +1)
+    elif stage == "propagate-":
+        voxelizer.propagate_external(gg, L, -1)
+        O.propagate(g, cfg, L, -1)
+    else:
+        voxelizer.finalize_masks(gg, L)
+        O.finalize(g, cfg, L)
+    grid_equal(gg.to_numpy(), g)
+
+
+@pytest.mark.parametrize("L", [0, 1])
+def test_stage_mark_adapt(O, torus, L):
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    g, _ = _oracle_state_through(O, torus, cfg, L, "mark")
+    gg = _gpu_grid(cfg, g)
+    voxelizer.mark_near_wall_refinement(gg, L)
+    O.mark(g, cfg, L)
+    grid_equal(gg.to_numpy(), g)
+    forest.adapt(gg)
+    O.adapt(g, cfg, L)
+    assert gg.n_levels == g.n_levels
+    grid_equal(gg.to_numpy(), g)
+
+
+def test_stage_boundary_tables_links(O, torus):
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    g, _ = _oracle_state_through(O, torus, cfg, 2, "mark")  # finest level finalized
+    gg = _gpu_grid(cfg, g)
+    counts = voxelizer.identify_boundary_cells(gg)
+    bc = O.boundary(g, cfg)
+    grid_equal(gg.to_numpy(), g)
+    n = g.n_used
+    assert np.array_equal(counts.cpu().numpy()[:n], bc[:n])
+    table = voxelizer.build_boundary_tables(gg, counts)
+    nb, cmap = O.tables(g, bc)
+    assert table.n_b == nb
+    assert np.array_equal(table.contraction_map.cpu().numpy(), cmap)
+    md = O.build_bins(torus.faces_coord, torus.normals, cfg, 2, mode=1)
+    lr = O.link_lengths(g, cfg, cmap, nb, md, torus.faces_coord, torus.normals)
+    voxelizer.compute_link_lengths(gg, None, torus, table)
+    check_links(table.lengths.cpu().numpy(), lr)
+
+
+def _embed_compare(O, mesh, cfg, use_filter=True):
+    eng = EmbedEngine(mesh, cfg)
+    grid, table = eng.run(use_filter=use_filter)
+    torch.cuda.synchronize()
+    ref = O.embed(mesh.faces_coord, mesh.normals, cfg, capacity=grid.capacity,
+                  use_filter=use_filter)
+    gn = grid.to_numpy()
+    assert grid.n_levels == ref.grid.n_levels
+    assert np.array_equal(gn["level_start"], ref.grid.level_start)
+    grid_equal(gn, ref.grid)
+    assert table.n_b == ref.n_b
+    assert np.array_equal(table.contraction_map.cpu().numpy()[:ref.grid.n_used], ref.contraction_map)
+    check_links(table.lengths.cpu().numpy(), ref.lengths)
+    return eng, grid, table
+
+
+def test_embed_c1_sphere(O):
+    """C1: icosphere 20,480 faces, N_x=64, L_max=3."""
+    mesh = make_icosphere((0.5, 0.5, 0.5), 0.5, 5)
+    _embed_compare(O, mesh, EmbedConfig(n_x=64, l_max=3))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_embed_translated_torus(O, seed):
+    rng = np.random.default_rng(seed)
+    mesh = translate(make_torus(120, 60), rng.random(3) / 64.0 - 1 / 128.0)
+    _embed_compare(O, mesh, EmbedConfig(n_x=32, l_max=4))
+
+
+def test_embed_filter_invariance_and_determinism(O, torus):
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    eng = EmbedEngine(torus, cfg)
+    g1, t1 = eng.run(use_filter=True)
+    a = g1.to_numpy()
+    la = t1.lengths.cpu().numpy().copy()
+    g2, t2 = eng.run(use_filter=False)
+    b = g2.to_numpy()
+    for k in ("coords", "nbr", "nbr_child", "child", "bflags", "masks", "level_start"):
+        assert np.array_equal(a[k], b[k]), k
+    assert np.array_equal(la, t2.lengths.cpu().numpy())
+    g3, t3 = eng.run()
+    c = g3.to_numpy()
+    for k in ("masks", "nbr"):
+        assert np.array_equal(a[k], c[k])
+    assert np.array_equal(la, t3.lengths.cpu().numpy())
+
+
+def test_capacity_error():
+    from paper_2512_01251_b200 import CapacityError
+    mesh = make_icosphere((0.5, 0.5, 0.5), 0.5, 3)
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    with pytest.raises(CapacityError):
+        EmbedEngine(mesh, cfg, capacity=600).run()
+
+
+def test_smoke():
+    import __graft_entry__
+    __graft_entry__.smoke()
