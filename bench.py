@@ -1,0 +1,315 @@
+#!/usr/bin/env python
+"""bench.py -- geometry-embed throughput on B200 (BASELINE.json metric:
+"geometry-embed time (ms) & cells classified/s").
+
+One step = one full embed_geometry (bins -> voxelization -> near-wall
+refinement/octree split -> boundary cells -> cut-link LUT) of the workload's
+synthetic mesh, inputs resident in HBM.  Default workload is BASELINE configs[1]
+(C2: 112,000-face torus, N_x=64, L_max=4, 1 GPU).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c4]
+  python bench.py --impl reference ...   # CPU oracle port on the host cores
+
+Multi-GPU (torchrun, one process per GPU): each rank embeds its own rigidly
+translated copy of the mesh (independent objects, no data-path collective),
+"scaling": "weak"; value = cells of all ranks / max-over-ranks time.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c1": dict(desc="C1: icosphere k=5 (20,480 faces), N_x=64, L_max=3", kind="sphere", sub=5,
+               n_x=64, l_max=3),
+    "c2": dict(desc="C2: torus 280x200 (112,000 faces), N_x=64, L_max=4", kind="torus", m=280, n=200,
+               n_x=64, l_max=4),
+    "c4": dict(desc="C4: torus 3000x1200 (7,200,000 faces), N_x=64, L_max=5", kind="torus", m=3000,
+               n=1200, n_x=64, l_max=5),
+}
+METRIC = "geometry-embed cells classified/s"
+UNIT = "cells/s"
+
+
+def make_mesh(w, rank):
+    from paper_2512_01251_b200 import make_icosphere, make_torus
+    from paper_2512_01251_b200.mesh import translate
+    m = make_icosphere((0.5, 0.5, 0.5), 0.5, w["sub"]) if w["kind"] == "sphere" else make_torus(w["m"], w["n"])
+    if rank:
+        rng = np.random.default_rng(rank)
+        m = translate(m, (rng.random(3) - 0.5) / 64.0)
+    return m
+
+
+def make_cfg(w):
+    from paper_2512_01251_b200 import EmbedConfig
+    return EmbedConfig(n_x=w["n_x"], l_max=w["l_max"], n_spec=2, d_spec=0.05)
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, val in zip(names, r[5:9]):
+                if val.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_baseline(mesh, cfg, cells, repeat=1):
+    from oracle import oracle as O
+    O.build()
+    thr = len(os.sched_getaffinity(0))
+    O.set_threads(thr)
+    fc, nrm = mesh.faces_coord, mesh.normals
+    cap = cfg.block_capacity(float(mesh.face_areas().sum()))
+    best = None
+    for _ in range(repeat):
+        t0 = time.perf_counter()
+        O.embed(fc, nrm, cfg, cap)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return {"value": cells / best, "unit": UNIT, "cores": thr, "kind": "port",
+            "sample": f"full embed of the same mesh ({repeat} run, best), {best * 1e3:.1f} ms",
+            "ms": best * 1e3}
+
+
+def dist_setup():
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allmax(ws, x):
+    if ws <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_reference(args, w, ws, rank):
+    """--impl reference: the CPU oracle port (the reference ships no
+    implementation of this path) timed on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    O.build()
+    thr = len(os.sched_getaffinity(0))
+    O.set_threads(thr)
+    mesh = make_mesh(w, 0)
+    cfg = make_cfg(w)
+    fc, nrm = mesh.faces_coord, mesh.normals
+    cap = cfg.block_capacity(float(mesh.face_areas().sum()))
+    for _ in range(args.warmup):
+        r = O.embed(fc, nrm, cfg, cap)
+    cells = None
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = O.embed(fc, nrm, cfg, cap)
+    dt = time.perf_counter() - t0
+    cells = 64 * r.grid.n_used
+    value = cells * args.steps / dt
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": w["desc"], "cells_per_embed": cells, "faces": int(mesh.n_faces)},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "port",
+                             "sample": f"full embed per step x {args.steps}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    w = WORKLOADS[args.config]
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, w, ws, rank)
+        barrier(ws)
+        return
+
+    import torch
+    from paper_2512_01251_b200 import _lib
+    from paper_2512_01251_b200.voxelizer import EmbedEngine
+    lib = _lib.require_cuda()
+    dev = torch.cuda.current_device()
+    mesh = make_mesh(w, rank)
+    cfg = make_cfg(w)
+    eng = EmbedEngine(mesh, cfg)
+    for _ in range(args.warmup):
+        eng.run(timed=True)
+    torch.cuda.synchronize()
+    # L2 flush buffer (> 126 MB L2), rewritten between timed steps; per-step
+    # CUDA events exclude the flush from the step time.
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stage = []
+    link_ms = []
+    launches0 = lib.vf_launch_count()
+    clocks = Clocks(dev)
+    barrier(ws)
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        starts[k].record()
+        eng.run(timed=True)
+        ends[k].record()
+        torch.cuda.synchronize()  # stage events are read per step
+        stage.append(eng.timings())
+        link_ms.append(eng.link_kernel_ms())
+    torch.cuda.synchronize()
+    barrier(ws)
+    launches = lib.vf_launch_count() - launches0
+    ck = clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = allmax(ws, float(sum(step_ms)))
+    cells = eng.cells_classified()
+    cells_all = cells
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([cells], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        cells_all = int(t.item())
+    value = cells_all * args.steps / (total_ms / 1e3)
+    g = eng.grid
+    n_b = int(eng.n_b_host[0])
+
+    # roofline of the dominant kernel (k_links): algorithmic bytes per launch
+    # = face records read (96 B/face) + LUT read-modify-write of every cell x
+    # direction of the mapped blocks (27*64*4 B x2 per boundary block)
+    F = eng.mesh.n_faces
+    link_bytes = F * 96 + n_b * 27 * 64 * 4 * 2
+    lk = float(np.median(link_ms))
+    peak, peak_kind = peaks()
+    achieved = link_bytes / (lk / 1e3) / 1e9
+    med = lambda a: float(np.median(a))
+    stages = {k: med([getattr(s, k) for s in stage]) for k in
+              ("binning", "voxelization", "refinement", "boundary", "links", "total")}
+
+    e2e = None
+    if not args.no_e2e:
+        fc = torch.from_numpy(np.ascontiguousarray(mesh.faces_coord)).pin_memory()
+        nr = torch.from_numpy(np.ascontiguousarray(mesh.normals)).pin_memory()
+        out = None
+        for _ in range(2):
+            out, h2d, d2h = eng.embed_host(fc, nr, out)
+        torch.cuda.synchronize()
+        es = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ee = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        barrier(ws)
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            es[k].record()
+            out, h2d, d2h = eng.embed_host(fc, nr, out)
+            ee[k].record()
+        torch.cuda.synchronize()
+        barrier(ws)
+        e2e_ms = allmax(ws, float(sum(s.elapsed_time(e) for s, e in zip(es, ee))))
+        e2e = {"value": cells_all * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": e2e_ms / args.steps}
+
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        cpu = cpu_baseline(mesh, cfg, cells)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w["desc"], "faces": int(F), "cells_per_embed": int(cells),
+                   "blocks": int(g.n_used), "boundary_blocks": n_b,
+                   "embed_ms_median": med(step_ms), "stage_ms": stages,
+                   "l2": "64 Mi-float (256 MB) buffer rewritten between steps, outside step events",
+                   "parallelism": f"independent objects x{ws}" if ws > 1 else "single GPU"},
+        "roofline": {"kernel": "k_links", "bound": "hbm", "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel_ms": lk, "algorithmic_bytes": int(link_bytes)},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": ck,
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -193,7 +193,9 @@ int vf_embed_phase1(const vf_config *cfg, const double *d_faces,
 int vf_embed_phase2(const vf_config *cfg, const double *d_faces,
                     int64_t n_faces, vf_grid *grid, const int32_t *d_cmap,
                     float *d_lengths, void *d_ws, size_t ws_bytes,
-                    void *stream);
+                    void *stream, void **link_events /* 2 or NULL */);
+/* number of kernels this library has launched in the process (bench hook) */
+int64_t vf_launch_count(void);
 /* copy the grid's latched device status to the host (synchronizes) */
 int vf_check_status(const vf_grid *grid, void *stream);
 

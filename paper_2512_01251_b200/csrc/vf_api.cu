@@ -4,6 +4,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
 #include <mutex>
 
 #include "vf_common.cuh"
@@ -24,7 +25,10 @@ int set_cuda_error(cudaError_t e, const char *what) {
     return VF_ECUDA;
 }
 
+static std::atomic<long long> g_launches{0};
+
 int check_launch(const char *what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? VF_OK : set_cuda_error(e, what);
 }
@@ -167,7 +171,8 @@ int vf_device_info(int *sm, int *major, int *minor) {
     if (sm) cudaDeviceGetAttribute(sm, cudaDevAttrMultiProcessorCount, dev);
     if (major) cudaDeviceGetAttribute(major, cudaDevAttrComputeCapabilityMajor, dev);
     if (minor) cudaDeviceGetAttribute(minor, cudaDevAttrComputeCapabilityMinor, dev);
-    return check_launch("vf_device_info");
+    e = cudaGetLastError();
+    return e == cudaSuccess ? VF_OK : set_cuda_error(e, "vf_device_info");
 }
 
 int vf_pack_faces(const double *fc, const double *nrm, int64_t F, double *out, void *stream) {
@@ -211,7 +216,12 @@ size_t vf_assemble_workspace_size(int64_t pair_cap, int64_t n_bins) {
 
 int vf_compact(const uint8_t *ind, int64_t n, int32_t *map, int32_t *d_count, void *ws,
                size_t ws_bytes, void *stream) {
-    if (!ind || !map || !d_count || n < 0) return set_error(VF_EARG, "vf_compact: bad argument");
+    if (!d_count || n < 0 || (n > 0 && (!ind || !map)))
+        return set_error(VF_EARG, "vf_compact: bad argument");
+    if (n == 0) {
+        cudaError_t e = cudaMemsetAsync(d_count, 0, sizeof(int32_t), (cudaStream_t)stream);
+        return e == cudaSuccess ? VF_OK : set_cuda_error(e, "vf_compact");
+    }
     if (ws_bytes < scan_workspace_bytes(n)) return set_error(VF_EARG, "vf_compact: workspace too small");
     return launch_compact(ind, n, map, d_count, ws, (cudaStream_t)stream);
 }
@@ -319,7 +329,7 @@ int vf_link_lengths(const vf_config *cfg, vf_grid *grid, const int32_t *cmap, co
     if (!valid_cfg(cfg) || !grid || !cmap || !faces || !lengths || (map && !d_n_map))
         return set_error(VF_EARG, "vf_link_lengths: bad argument");
     return link_impl(*cfg, grid, cmap, faces, F, map, d_n_map, lengths, ws, ws_bytes,
-                     (cudaStream_t)stream);
+                     (cudaStream_t)stream, nullptr);
 }
 
 size_t vf_embed_workspace_size(const vf_config *cfg, int64_t F, int32_t cap) {
@@ -371,15 +381,18 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     return VF_OK;
 }
 
+int64_t vf_launch_count(void) { return (int64_t)g_launches.load(); }
+
 int vf_embed_phase2(const vf_config *cfg, const double *faces, int64_t F, vf_grid *g,
-                    const int32_t *cmap, float *lengths, void *ws, size_t ws_bytes, void *stream) {
+                    const int32_t *cmap, float *lengths, void *ws, size_t ws_bytes, void *stream,
+                    void **link_events) {
     if (!valid_cfg(cfg) || !faces || !g || !cmap || !lengths)
         return set_error(VF_EARG, "vf_embed_phase2: bad argument");
     EmbedWs w;
     if (embed_layout(*cfg, F, g->capacity, (char *)ws, &w) > ws_bytes)
         return set_error(VF_EARG, "vf_embed_phase2: workspace too small");
     return link_impl(*cfg, g, cmap, faces, F, nullptr, nullptr, lengths, w.link_ws, w.link_b,
-                     (cudaStream_t)stream);
+                     (cudaStream_t)stream, link_events);
 }
 
 int vf_check_status(const vf_grid *g, void *stream) {

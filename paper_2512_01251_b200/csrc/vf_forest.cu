@@ -205,6 +205,37 @@ __global__ void k_adapt_finish(int L, int32_t capacity, int32_t *__restrict__ le
     for (int k = L + 2; k <= VF_MAX_LEVELS; ++k) level_start[k] = (int32_t)ne;
 }
 
+// bit index of a direction in {-1,0,1}^3: (dx+1) + 3(dy+1) + 9(dz+1)
+__device__ __forceinline__ int dir_code(int dx, int dy, int dz) {
+    return (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1);
+}
+__device__ __forceinline__ int dir_code_of_slot(int q) {
+    return dir_code(c27(q, 0), c27(q, 1), c27(q, 2));
+}
+// any direction (ox,oy,oz) != 0 with o_d in {0, e_d} set in `bits`
+__device__ __forceinline__ bool touches(uint32_t bits, int ex, int ey, int ez) {
+    bool any = false;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b2 = 0; b2 < 2; ++b2)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int ox = a ? ex : 0, oy = b2 ? ey : 0, oz = c ? ez : 0;
+                if (ox == 0 && oy == 0 && oz == 0) continue;
+                any |= (bits >> dir_code(ox, oy, oz)) & 1u;
+            }
+    return any;
+}
+// 8 octant bits: octant o = (x>=2) | (y>=2)<<1 | (z>=2)<<2 touches a set direction
+__device__ __forceinline__ uint32_t octant_bits(uint32_t bits, int) {
+    uint32_t g = 0;
+#pragma unroll
+    for (int o = 0; o < 8; ++o)
+        g |= (uint32_t)touches(bits, (o & 1) ? 1 : -1, (o & 2) ? 1 : -1, (o & 4) ? 1 : -1) << o;
+    return g;
+}
+
 // one thread per child: coords, 27 links, ghost layer
 __global__ void __launch_bounds__(256)
     k_adapt_children(int L, int32_t capacity, int nbx1, int nby1, int nbz1,
@@ -224,7 +255,7 @@ __global__ void __launch_bounds__(256)
         const int4 pc = reinterpret_cast<const int4 *>(coords)[P];
         const int ci = 2 * pc.x + (cc & 1), cj = 2 * pc.y + ((cc >> 1) & 1), ck = 2 * pc.z + (cc >> 2);
         reinterpret_cast<int4 *>(coords)[id] = make_int4(ci, cj, ck, L + 1);
-        uint32_t missing = 0;  // bit q: slot q is MISSING / SOLID_NBR
+        uint32_t missing = 0;  // bit dir_code(q): slot q is MISSING / SOLID_NBR
         for (int q = 0; q < 27; ++q) {
             const int ti = ci + c27(q, 0), tj = cj + c27(q, 1), tk = ck + c27(q, 2);
             int32_t v;
@@ -246,30 +277,23 @@ __global__ void __launch_bounds__(256)
             }
             nbr[27 * id + q] = v;
             nbr_child[27 * id + q] = -1;
-            if (v == VF_NB_MISSING || v == VF_NB_SOLID_NBR) missing |= 1u << q;
+            if (v == VF_NB_MISSING || v == VF_NB_SOLID_NBR) missing |= 1u << dir_code_of_slot(q);
         }
         child[id] = -1;
         bflags[id] = 0;
-        // A14 ghost layer: Chebyshev distance <= 2 fine cells from a missing block
+        // A14 ghost layer: a cell is within Chebyshev distance 2 (fine cells) of
+        // a missing neighbour block iff one of the 7 blocks towards its octant
+        // is missing, so 8 octant bits decide all 64 cells.
+        const uint32_t g8 = octant_bits(missing, 2);
         uint32_t w[16];
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
+            const int J = r & 3, K = r >> 2;
             uint32_t x = 0;
 #pragma unroll
             for (int I = 0; I < 4; ++I) {
-                const int J = r & 3, K = r >> 2;
-                bool ghost = false;
-                if (missing) {
-                    for (int q = 1; q < 27 && !ghost; ++q) {
-                        if (!(missing >> q & 1)) continue;
-                        const int ox = c27(q, 0), oy = c27(q, 1), oz = c27(q, 2);
-                        const bool okx = ox == 0 || (ox < 0 ? I < 2 : I >= 2);
-                        const bool oky = oy == 0 || (oy < 0 ? J < 2 : J >= 2);
-                        const bool okz = oz == 0 || (oz < 0 ? K < 2 : K >= 2);
-                        ghost = okx && oky && okz;
-                    }
-                }
-                x |= (uint32_t)(ghost ? VF_GHOST : VF_FLUID) << (8 * I);
+                const int o = (I >= 2) | ((J >= 2) << 1) | ((K >= 2) << 2);
+                x |= (uint32_t)((g8 >> o & 1u) ? VF_GHOST : VF_FLUID) << (8 * I);
             }
             w[r] = x;
         }
@@ -288,12 +312,12 @@ __global__ void __launch_bounds__(256)
     for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
          b += (int64_t)gridDim.x * blockDim.x) {
         const int32_t *nb = nbr + 27 * b;
-        uint32_t coarse = 0;  // bit q: existing unrefined neighbour
+        uint32_t coarse = 0;  // bit dir_code(q): existing unrefined neighbour
         for (int q = 0; q < 27; ++q) {
             const int32_t v = (q == 0) ? (int32_t)b : nb[q];
             const int32_t ch = (v >= 0) ? child[v] : -1;
             nbr_child[27 * b + q] = ch;
-            if (q > 0 && v >= 0 && ch < 0) coarse |= 1u << q;
+            if (q > 0 && v >= 0 && ch < 0) coarse |= 1u << dir_code_of_slot(q);
         }
         if (child[b] < 0 || !coarse) continue;
         uint32_t *m = reinterpret_cast<uint32_t *>(masks + 64 * b);
@@ -304,15 +328,11 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
             for (int I = 0; I < 4; ++I) {
                 if (((x >> (8 * I)) & 0xffu) != VF_FLUID) continue;
-                bool itf = false;
-                for (int q = 1; q < 27 && !itf; ++q) {
-                    if (!(coarse >> q & 1)) continue;
-                    const int ox = c27(q, 0), oy = c27(q, 1), oz = c27(q, 2);
-                    const bool okx = ox == 0 || (ox < 0 ? I == 0 : I == 3);
-                    const bool oky = oy == 0 || (oy < 0 ? J == 0 : J == 3);
-                    const bool okz = oz == 0 || (oz < 0 ? K == 0 : K == 3);
-                    itf = okx && oky && okz;
-                }
+                // one coarse cell: only the faces / edges / corner the cell touches
+                const int ex = I == 0 ? -1 : (I == 3 ? 1 : 0);
+                const int ey = J == 0 ? -1 : (J == 3 ? 1 : 0);
+                const int ez = K == 0 ? -1 : (K == 3 ? 1 : 0);
+                const bool itf = touches(coarse, ex, ey, ez);
                 if (itf) x = (x & ~(0xffu << (8 * I))) | ((uint32_t)VF_INTERFACE << (8 * I));
             }
             if (x != x0) m[r] = x;

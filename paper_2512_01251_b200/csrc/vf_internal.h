@@ -75,6 +75,6 @@ int tables_impl(vf_grid *g, const int32_t *bcount, int32_t *cmap, int32_t *d_n_b
 size_t link_workspace_size(const vf_config &cfg, int finest);
 int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
               int64_t F, const int32_t *map, const int32_t *d_n_map, float *lengths, void *ws,
-              size_t ws_bytes, cudaStream_t st);
+              size_t ws_bytes, cudaStream_t st, void **events);
 
 }  // namespace vf

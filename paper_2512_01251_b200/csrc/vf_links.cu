@@ -26,56 +26,81 @@
 
 namespace vf {
 
-__global__ void __launch_bounds__(64)
+constexpr int kBndWarps = 8;
+
+// warp per finest-level block: the 27 neighbour ids decide candidacy (the
+// block or a neighbour is solid); a 6x6x6 shared-memory halo of SOLID bits is
+// gathered once, then every FLUID cell ORs its 26 halo neighbours (constant
+// offsets).  Reads of concurrently re-marked cells see FLUID or BOUNDARY,
+// both "not SOLID", so the fused single pass equals PAPER.md:941's two passes.
+__global__ void __launch_bounds__(kBndWarps * 32)
     k_boundary(int L, const int32_t *__restrict__ level_start, const int32_t *__restrict__ nbr,
                uint8_t *__restrict__ bflags, uint8_t *__restrict__ masks,
                int32_t *__restrict__ bcount) {
-    __shared__ int32_t s_nb[27];
-    __shared__ int s_cand;
+    __shared__ uint8_t s_halo[kBndWarps][216];
+    __shared__ int32_t s_nb[kBndWarps][27];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * kBndWarps + w, nw = (int64_t)gridDim.x * kBndWarps;
     const int32_t s = level_start[L], e = level_start[L + 1];
-    const int t = threadIdx.x;
-    const int I = t & 3, J = (t >> 2) & 3, K = t >> 4;
-    for (int64_t b = s + blockIdx.x; b < e; b += gridDim.x) {
-        if (t < 27) s_nb[t] = (t == 0) ? (int32_t)b : nbr[27 * b + t];
-        __syncthreads();
-        if (t == 0) s_cand = 0;
-        __syncthreads();
-        if (t < 27) {
-            const int32_t v = s_nb[t];
-            if (v >= 0 && (bflags[v] & VF_BF_SOLID)) s_cand = 1;
+    for (int64_t b = s + gw; b < e; b += nw) {
+        int32_t myn = -1;
+        if (lane < 27) myn = (lane == 0) ? (int32_t)b : nbr[27 * b + lane];
+        const bool sol = (lane < 27 && myn >= 0) ? (bflags[myn] & VF_BF_SOLID) != 0 : false;
+        if (!__any_sync(0xffffffffu, sol)) {  // not a candidate (A18): no boundary cell
+            if (lane == 0) {
+                bcount[b] = 0;
+                bflags[b] = (uint8_t)(bflags[b] & ~VF_BF_BOUNDARY);
+            }
+            continue;
         }
-        __syncthreads();
-        const bool cand = s_cand;
-        bool bnd = false;
-        if (cand && masks[64 * b + t] == VF_FLUID) {
-            for (int q = 1; q < 27 && !bnd; ++q) {
-                const int ux = I + c27(q, 0), uy = J + c27(q, 1), uz = K + c27(q, 2);
-                // A15: I' = mod(4 + mod(I + c, 4), 4); neighbour block direction
-                const int dxs = (ux < 0 || ux > 3) ? c27(q, 0) : 0;
-                const int dys = (uy < 0 || uy > 3) ? c27(q, 1) : 0;
-                const int dzs = (uz < 0 || uz > 3) ? c27(q, 2) : 0;
-                const int32_t nbk = s_nb[slot_of(dxs, dys, dzs)];
-                if (nbk < 0) continue;
-                const int tt = (ux & 3) + 4 * (uy & 3) + 16 * (uz & 3);
-                bnd = masks[64 * (int64_t)nbk + tt] == VF_SOLID;
+        if (lane < 27) s_nb[w][lane] = myn;
+        __syncwarp();
+        for (int h = lane; h < 216; h += 32) {
+            const int hx = h % 6 - 1, hy = (h / 6) % 6 - 1, hz = h / 36 - 1;
+            const int ox = hx < 0 ? -1 : (hx > 3 ? 1 : 0);
+            const int oy = hy < 0 ? -1 : (hy > 3 ? 1 : 0);
+            const int oz = hz < 0 ? -1 : (hz > 3 ? 1 : 0);
+            const int32_t nbk = s_nb[w][slot_of(ox, oy, oz)];
+            s_halo[w][h] = (nbk >= 0) ? (uint8_t)(masks[64 * (int64_t)nbk + (hx & 3) + 4 * (hy & 3) +
+                                                       16 * (hz & 3)] == VF_SOLID)
+                                      : (uint8_t)0;
+        }
+        __syncwarp();
+        int cnt = 0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int c = lane + 32 * k;
+            const int I = c & 3, J = (c >> 2) & 3, K = c >> 4;
+            if (masks[64 * b + c] != VF_FLUID) continue;
+            const uint8_t *hp = &s_halo[w][(I + 1) + 6 * (J + 1) + 36 * (K + 1)];
+            uint32_t any = 0;
+#pragma unroll
+            for (int dz = -1; dz <= 1; ++dz)
+#pragma unroll
+                for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                    for (int dx = -1; dx <= 1; ++dx)
+                        if (dx || dy || dz) any |= hp[dx + 6 * dy + 36 * dz];
+            if (any) {
+                masks[64 * b + c] = VF_BOUNDARY;
+                ++cnt;
             }
         }
-        const int cnt = __syncthreads_count(bnd);
-        if (bnd) masks[64 * b + t] = VF_BOUNDARY;
-        if (t == 0) {
+        cnt = warp_sum(cnt);
+        if (lane == 0) {
             bcount[b] = cnt;
             const uint8_t f = bflags[b];
             bflags[b] = (uint8_t)(cnt > 0 ? (f | VF_BF_BOUNDARY) : (f & ~VF_BF_BOUNDARY));
         }
-        __syncthreads();
+        __syncwarp();
     }
 }
 
 int boundary_impl(vf_grid *g, int32_t *bcount, cudaStream_t st) {
     const int L = g->n_levels - 1;
     cudaMemsetAsync(bcount, 0, sizeof(int32_t) * (size_t)g->capacity, st);
-    k_boundary<<<max_ctas(24), 64, 0, st>>>(L, g->d_level_start, g->d_nbr, g->d_bflags,
-                                            g->d_masks, bcount);
+    k_boundary<<<max_ctas(8), kBndWarps * 32, 0, st>>>(L, g->d_level_start, g->d_nbr, g->d_bflags,
+                                                       g->d_masks, bcount);
     return check_launch("k_boundary");
 }
 
@@ -137,78 +162,138 @@ __global__ void k_blockmap(int L, int bx, int by, const int32_t *__restrict__ le
     }
 }
 
+// zero-component mask of the representative direction q = 2r+1
+__device__ __forceinline__ uint32_t zero_axes(int r) {
+    const int q = 2 * r + 1;
+    return (uint32_t)(c27(q, 0) == 0) | ((uint32_t)(c27(q, 1) == 0) << 1) |
+           ((uint32_t)(c27(q, 2) == 0) << 2);
+}
+
+// lattice-node index range whose centres can lie in [A, B] (superset)
+__device__ __forceinline__ void node_range(double A, double B, double dx, int n, int &a, int &b) {
+    double fa = floor(VF_DSUB(VF_DDIV(A, dx), 0.5));
+    double fb = floor(VF_DSUB(VF_DDIV(B, dx), 0.5)) + 1.0;
+    fa = fmax(fa, 0.0);
+    fb = fmin(fb, (double)(n - 1));
+    a = (int)fa;
+    b = fa > fb ? a - 1 : (int)fb;
+}
+
+// exact decision for one (face, node, direction pair) candidate: d = num/den
+// bit-identical to the oracle, then the eps-box SAT at the piercing point.
+__device__ __noinline__ void link_candidate(const double *__restrict__ faces, int64_t f, int r,
+                                            double num, double x, double y, double z, double dx,
+                                            double eps, int32_t slot, int t,
+                                            float *__restrict__ lengths) {
+    double v[9], nn[3];
+    load_face(faces, f, v, nn);
+    const int q1 = 2 * r + 1;
+    const double den = VF_DADD(VF_DADD(VF_DMUL((double)c27(q1, 0), nn[0]),
+                                       VF_DMUL((double)c27(q1, 1), nn[1])),
+                               VF_DMUL((double)c27(q1, 2), nn[2]));
+    const double d = VF_DDIV(num, den);
+    // d > 0: slot q = 2r+1; d < 0: opposite slot with d' = -d exactly
+    // (den' = -den bitwise) and v + d'c' == v + d c
+    const bool pos = d > 0.0;
+    const double dd = pos ? d : -d;
+    if (!(dd > 0.0 && dd <= dx)) return;
+    const int q = pos ? q1 : q1 + 1;
+    const double c0 = c27(q, 0), c1 = c27(q, 1), c2 = c27(q, 2);
+    const double xi = VF_DADD(x, VF_DMUL(dd, c0));
+    const double yi = VF_DADD(y, VF_DMUL(dd, c1));
+    const double zi = VF_DADD(z, VF_DMUL(dd, c2));
+    SatFace sf;
+    sat_face_init(sf, v);
+    if (!sat_exact(sf, VF_DSUB(xi, eps), VF_DSUB(yi, eps), VF_DSUB(zi, eps), VF_DADD(xi, eps),
+                   VF_DADD(yi, eps), VF_DADD(zi, eps)))
+        return;
+    const float qv = __double2float_rn(VF_DDIV(dd, dx));
+    atomicMin(reinterpret_cast<unsigned int *>(lengths) + ((int64_t)slot * 27 + q) * 64 + t,
+              __float_as_uint(qv));
+}
+
+// Every accepted link (node v, direction c, 0 < d <= dx) has its piercing
+// point v + d c inside the face's AABB +- eps, so per axis the node lies in
+// R1 = AABB +- (dx + eps) when c_k != 0 and in R0 = AABB +- eps when c_k = 0.
+// The kernel walks R1^3 once (num is direction independent), keeps per node
+// the R0 membership bits, and only tests directions whose zero axes are all
+// in R0.  A division-free pre-check num * (1/den) rejects |d| > dx before the
+// exact d = num/den (bit-identical to the oracle) decides.
 __global__ void __launch_bounds__(128)
     k_links(LevelInfo li, const double *__restrict__ faces, int64_t F,
             const int32_t *__restrict__ map, const int32_t *__restrict__ d_n_map,
             const int32_t *__restrict__ bmap, float *__restrict__ lengths) {
     const int64_t n = d_n_map ? (int64_t)*d_n_map : F;
     const double dx = li.dx, eps = li.eps;
+    const double lim = dx * (1.0 + 1e-12);  // conservative |d| bound for the pre-check
+    // absolute slack covering the rounding of the approximate piercing point
+    const double margin = 1e-12 * fmax(fmax(li.len[0], li.len[1]), fmax(li.len[2], 1.0));
     for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < n;
          m += (int64_t)gridDim.x * blockDim.x) {
         const int64_t f = map ? (int64_t)map[m] : m;
         double v[9], nn[3];
         load_face(faces, f, v, nn);
-        SatFace sf;
-        sat_face_init(sf, v);
-        int a[3], b[3];
+        int a1[3], b1[3], a0[3], b0[3];
+        double blo[3], bhi[3];  // AABB +- (eps + margin): piercing-point pre-check
         bool empty = false;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            double fa = floor(VF_DDIV(sf.lo[d], dx)) - 1.0, fb = floor(VF_DDIV(sf.hi[d], dx)) + 1.0;
-            fa = fmax(fa, 0.0);
-            fb = fmin(fb, (double)(li.cells[d] - 1));
-            if (fa > fb) empty = true;
-            a[d] = (int)fa;
-            b[d] = (int)fb;
+            const double lo = fmin(fmin(v[d], v[3 + d]), v[6 + d]);
+            const double hi = fmax(fmax(v[d], v[3 + d]), v[6 + d]);
+            node_range(lo - dx - 2.0 * eps, hi + dx + 2.0 * eps, dx, li.cells[d], a1[d], b1[d]);
+            node_range(lo - 2.0 * eps, hi + 2.0 * eps, dx, li.cells[d], a0[d], b0[d]);
+            blo[d] = lo - eps - margin;
+            bhi[d] = hi + eps + margin;
+            if (a1[d] > b1[d]) empty = true;
         }
         if (empty) continue;
-        // 13 representative directions (odd slots): den and |den|*dx
-        double den[13];
+        double inv[13];
         uint32_t valid = 0;
 #pragma unroll
         for (int r = 0; r < 13; ++r) {
             const int q = 2 * r + 1;
             const double c0 = c27(q, 0), c1 = c27(q, 1), c2 = c27(q, 2);
             const double cn = __dsqrt_rn(VF_DADD(VF_DADD(VF_DMUL(c0, c0), VF_DMUL(c1, c1)), VF_DMUL(c2, c2)));
-            den[r] = VF_DADD(VF_DADD(VF_DMUL(c0, nn[0]), VF_DMUL(c1, nn[1])), VF_DMUL(c2, nn[2]));
-            if (!(fabs(den[r]) < VF_DMUL(li.eps_par, cn))) valid |= 1u << r;
+            const double den = VF_DADD(VF_DADD(VF_DMUL(c0, nn[0]), VF_DMUL(c1, nn[1])), VF_DMUL(c2, nn[2]));
+            const bool ok = !(fabs(den) < VF_DMUL(li.eps_par, cn));
+            valid |= (uint32_t)ok << r;
+            inv[r] = ok ? 1.0 / den : 0.0;
         }
-        for (int k = a[2]; k <= b[2]; ++k) {
+        for (int k = a1[2]; k <= b1[2]; ++k) {
             const double z = node_c(k, dx);
-            for (int j = a[1]; j <= b[1]; ++j) {
+            const uint32_t mz = (k >= a0[2] && k <= b0[2]) ? 4u : 0u;
+            for (int j = a1[1]; j <= b1[1]; ++j) {
                 const double y = node_c(j, dx);
-                for (int i = a[0]; i <= b[0]; ++i) {
+                const uint32_t myz = mz | ((j >= a0[1] && j <= b0[1]) ? 2u : 0u);
+                for (int i = a1[0]; i <= b1[0]; ++i) {
+                    const uint32_t m0 = myz | ((i >= a0[0] && i <= b0[0]) ? 1u : 0u);
                     const int32_t slot =
                         bmap[(i >> 2) + (int64_t)li.bins[0] * ((j >> 2) + (int64_t)li.bins[1] * (k >> 2))];
                     if (slot < 0) continue;
                     const double x = node_c(i, dx);
                     const double num = plane_num(v, nn, x, y, z);
                     if (num == 0.0) continue;  // d = 0 is never a link (0 < d)
-                    const double anum = fabs(num);
                     const int t = (i & 3) + 4 * (j & 3) + 16 * (k & 3);
-#pragma unroll 1
+#pragma unroll
                     for (int r = 0; r < 13; ++r) {
-                        if (!(valid >> r & 1)) continue;
-                        // |d| > 2dx for sure -> neither direction of the pair
-                        if (anum > VF_DMUL(2.0 * dx, fabs(den[r]))) continue;
-                        const double d = VF_DDIV(num, den[r]);
-                        // d > 0: slot q = 2r+1; d < 0: opposite slot, d' = -d
-                        // exactly (den' = -den bitwise), v + d'c' == v + d c
-                        const bool pos = d > 0.0;
-                        const double dd = pos ? d : -d;
-                        if (!(dd > 0.0 && dd <= dx)) continue;
-                        const int q = pos ? 2 * r + 1 : 2 * r + 2;
-                        const double c0 = c27(q, 0), c1 = c27(q, 1), c2 = c27(q, 2);
-                        const double xi = VF_DADD(x, VF_DMUL(dd, c0));
-                        const double yi = VF_DADD(y, VF_DMUL(dd, c1));
-                        const double zi = VF_DADD(z, VF_DMUL(dd, c2));
-                        if (!sat_exact(sf, VF_DSUB(xi, eps), VF_DSUB(yi, eps), VF_DSUB(zi, eps),
-                                       VF_DADD(xi, eps), VF_DADD(yi, eps), VF_DADD(zi, eps)))
-                            continue;
-                        const float qv = __double2float_rn(VF_DDIV(dd, dx));
-                        atomicMin(reinterpret_cast<unsigned int *>(lengths) +
-                                      ((int64_t)slot * 27 + q) * 64 + t,
-                                  __float_as_uint(qv));
+                        if (!(valid >> r & 1) || (zero_axes(r) & ~m0)) continue;
+                        const double da = num * inv[r];  // ~d, relative error < 1e-15
+                        if (fabs(da) > lim) continue;
+                        // the exact SAT needs v + d c inside the face AABB +- eps
+                        const int q = 2 * r + 1;
+                        if (c27(q, 0) != 0) {
+                            const double xa = x + c27(q, 0) * da;
+                            if (xa < blo[0] || xa > bhi[0]) continue;
+                        }
+                        if (c27(q, 1) != 0) {
+                            const double ya = y + c27(q, 1) * da;
+                            if (ya < blo[1] || ya > bhi[1]) continue;
+                        }
+                        if (c27(q, 2) != 0) {
+                            const double za = z + c27(q, 2) * da;
+                            if (za < blo[2] || za > bhi[2]) continue;
+                        }
+                        link_candidate(faces, f, r, num, x, y, z, dx, eps, slot, t, lengths);
                     }
                 }
             }
@@ -223,7 +308,7 @@ size_t link_workspace_size(const vf_config &cfg, int finest) {
 
 int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
               int64_t F, const int32_t *map, const int32_t *d_n_map, float *lengths, void *ws,
-              size_t ws_bytes, cudaStream_t st) {
+              size_t ws_bytes, cudaStream_t st, void **events) {
     const int L = g->n_levels - 1;
     if (ws_bytes < link_workspace_size(cfg, L)) return set_error(VF_EARG, "link workspace too small");
     const LevelInfo li = make_level(cfg, L);
@@ -237,8 +322,11 @@ int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const doubl
     int64_t grid = (F + 127) / 128;
     if (grid > max_ctas(16)) grid = max_ctas(16);
     if (grid < 1) grid = 1;
+    if (events) cudaEventRecord((cudaEvent_t)events[0], st);
     k_links<<<(int)grid, 128, 0, st>>>(li, faces, F, map, d_n_map, bmap, lengths);
-    return check_launch("k_links");
+    rc = check_launch("k_links");
+    if (events) cudaEventRecord((cudaEvent_t)events[1], st);
+    return rc;
 }
 
 }  // namespace vf

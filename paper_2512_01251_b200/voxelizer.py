@@ -208,9 +208,14 @@ class EmbedEngine:
             self.bc_ids = torch.zeros((max(n_b, 1), 27, 64), dtype=torch.int8, device="cuda")
         lengths = self.lengths[:n_b]
         lengths.fill_(-1.0)
+        lev = None
+        if timed:
+            lev = C.cast(C.byref(self._ev_arr, C.sizeof(C.c_void_p) * (self.n_events - 3)),
+                         C.POINTER(C.c_void_p))
         _lib.check(lib.vf_embed_phase2(C.byref(self.c), _lib.ptr(self.mesh.faces), self.mesh.n_faces,
                                        C.byref(gs), _lib.ptr(self.cmap), _lib.ptr(lengths),
-                                       _lib.ptr(self.ws), self.ws.numel(), st), "embed_geometry")
+                                       _lib.ptr(self.ws), self.ws.numel(), st, lev),
+                   "embed_geometry")
         if timed:
             self.events[self.n_events - 1].record()
         table = LinkTable(lengths, self.bc_ids[:n_b], self.cmap, n_b)
@@ -233,6 +238,43 @@ class EmbedEngine:
         t.links = ev[k + 1].elapsed_time(ev[self.n_events - 1])
         t.total = ev[0].elapsed_time(ev[self.n_events - 1])
         return t
+
+    def link_kernel_ms(self) -> float:
+        """Device time of the k_links launch of the last timed run."""
+        return self.events[self.n_events - 3].elapsed_time(self.events[self.n_events - 2])
+
+    # -- end-to-end path: host mesh in, host results out -------------------
+    def embed_host(self, faces_coord, normals, out=None):
+        """Upload host face arrays (pinned for async copies), embed, and copy
+        the results back into host buffers ``out`` (dict of pinned tensors,
+        allocated on first use).  Returns (out, h2d_bytes, d2h_bytes)."""
+        import torch
+        lib = self.lib
+        F = self.mesh.n_faces
+        if not hasattr(self, "_dfc"):
+            self._dfc = torch.empty((F, 9), dtype=torch.float64, device="cuda")
+            self._dn = torch.empty((F, 3), dtype=torch.float64, device="cuda")
+        self._dfc.copy_(faces_coord, non_blocking=True)
+        self._dn.copy_(normals, non_blocking=True)
+        _lib.check(lib.vf_pack_faces(_lib.ptr(self._dfc), _lib.ptr(self._dn), F,
+                                     _lib.ptr(self.mesh.faces), _lib.stream_ptr()), "pack_faces")
+        grid, table = self.run()
+        n = grid.n_used
+        res = {"coords": grid.coords[:n], "nbr": grid.nbr[:n], "child": grid.child[:n],
+               "bflags": grid.bflags[:n], "masks": grid.masks[:n],
+               "contraction_map": table.contraction_map[:n], "lengths": table.lengths}
+        if out is None:
+            out = {}
+        d2h = 0
+        for k, t in res.items():
+            buf = out.get(k)
+            if buf is None or buf.shape != t.shape:
+                buf = torch.empty(t.shape, dtype=t.dtype).pin_memory()
+                out[k] = buf
+            buf.copy_(t, non_blocking=True)
+            d2h += t.numel() * t.element_size()
+        h2d = faces_coord.numel() * 8 + normals.numel() * 8
+        return out, h2d, d2h
 
     def cells_classified(self) -> int:
         """Sum over levels of 64 * blocks."""
