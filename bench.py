@@ -216,15 +216,13 @@ def main():
     cfg = make_cfg(w)
     eng = EmbedEngine(mesh, cfg)
     for _ in range(args.warmup):
-        eng.run(timed=True)
+        eng.run()
     torch.cuda.synchronize()
     # L2 flush buffer (> 126 MB L2), rewritten between timed steps; per-step
     # CUDA events exclude the flush from the step time.
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    stage = []
-    link_ms = []
     launches0 = lib.vf_launch_count()
     clocks = Clocks(dev)
     barrier(ws)
@@ -232,11 +230,8 @@ def main():
     for k in range(args.steps):
         flush.fill_(float(k))
         starts[k].record()
-        eng.run(timed=True)
+        eng.run()  # one CUDA-graph launch + one host sync (status, N_b)
         ends[k].record()
-        torch.cuda.synchronize()  # stage events are read per step
-        stage.append(eng.timings())
-        link_ms.append(eng.link_kernel_ms())
     torch.cuda.synchronize()
     barrier(ws)
     launches = lib.vf_launch_count() - launches0
@@ -253,6 +248,18 @@ def main():
     value = cells_all * args.steps / (total_ms / 1e3)
     g = eng.grid
     n_b = int(eng.n_b_host[0])
+    # kernel launches per step: count one eager (non-graph) embed
+    l0 = lib.vf_launch_count()
+    eng.run(timed=True)
+    kernels_per_step = lib.vf_launch_count() - l0 - 0
+    # stage split + dominant-kernel time from eager runs with stage events
+    stage, link_ms = [], []
+    for k in range(max(3, min(args.steps, 5))):
+        flush.fill_(float(k))
+        eng.run(timed=True)
+        torch.cuda.synchronize()
+        stage.append(eng.timings())
+        link_ms.append(eng.link_kernel_ms())
 
     # roofline of the dominant kernel (k_links): algorithmic bytes per launch
     # = face records read (96 B/face) + LUT read-modify-write of every cell x
@@ -300,13 +307,16 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w["desc"], "faces": int(F), "cells_per_embed": int(cells),
                    "blocks": int(g.n_used), "boundary_blocks": n_b,
-                   "embed_ms_median": med(step_ms), "stage_ms": stages,
+                   "embed_ms_median": med(step_ms), "stage_ms_eager": stages,
                    "l2": "64 Mi-float (256 MB) buffer rewritten between steps, outside step events",
                    "parallelism": f"independent objects x{ws}" if ws > 1 else "single GPU"},
         "roofline": {"kernel": "k_links", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "kernel_ms": lk, "algorithmic_bytes": int(link_bytes)},
-        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": ck,
+        "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": int(kernels_per_step * args.steps),
+        "gpu_launch_note": f"{kernels_per_step} kernels per embed, issued as one CUDA graph per step",
+        "clocks": ck,
     }
     print(json.dumps(line), flush=True)
 

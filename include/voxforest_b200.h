@@ -182,8 +182,9 @@ int vf_link_lengths(const vf_config *cfg, vf_grid *grid, const int32_t *d_cmap,
  * Phase 1 (no host sync): init_forest + per level bins/voxelize/propagate/
  * finalize/mark/adapt + finest boundary cells + tables.  Writes the
  * contraction map into d_cmap[capacity] and N_b into d_n_b.
- * Phase 2 (after the caller read N_b and allocated d_lengths/d_bc_ids):
- * link lengths.  stage events (optional, 16 cudaEvent_t) bracket stages. */
+ * Phase 2: LUT initialisation (-1) for the device-resident N_b and link
+ * lengths into d_lengths (capacity lengths_cap boundary blocks).  Stage
+ * events (optional, 64 cudaEvent_t) bracket the phase-1 stages. */
 size_t vf_embed_workspace_size(const vf_config *cfg, int64_t n_faces,
                                int32_t capacity);
 int vf_embed_phase1(const vf_config *cfg, const double *d_faces,
@@ -192,8 +193,19 @@ int vf_embed_phase1(const vf_config *cfg, const double *d_faces,
                     size_t ws_bytes, void *stream, void **events);
 int vf_embed_phase2(const vf_config *cfg, const double *d_faces,
                     int64_t n_faces, vf_grid *grid, const int32_t *d_cmap,
-                    float *d_lengths, void *d_ws, size_t ws_bytes,
-                    void *stream, void **link_events /* 2 or NULL */);
+                    const int32_t *d_n_b, float *d_lengths, int64_t lengths_cap,
+                    void *d_ws, size_t ws_bytes, void *stream,
+                    void **link_events /* 2 or NULL */);
+/* Both phases captured as one CUDA graph (no host sync inside: the LUT is
+ * filled for the device-resident N_b; N_b > lengths_cap latches
+ * VF_ECAPACITY).  `stream` must not be the legacy default stream. */
+int vf_embed_graph_create(const vf_config *cfg, const double *d_faces,
+                          int64_t n_faces, int use_filter, vf_grid *grid,
+                          int32_t *d_cmap, int32_t *d_n_b, float *d_lengths,
+                          int64_t lengths_cap, void *d_ws, size_t ws_bytes,
+                          void *stream, void **graph_exec);
+int vf_graph_launch(void *graph_exec, void *stream);
+void vf_graph_destroy(void *graph_exec);
 /* number of kernels this library has launched in the process (bench hook) */
 int64_t vf_launch_count(void);
 /* copy the grid's latched device status to the host (synchronizes) */

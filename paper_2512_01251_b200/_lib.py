@@ -78,7 +78,11 @@ _SIGS = {
     "vf_link_lengths": (_I32, [_CP, _GP, _P, _P, _I64, _P, _P, _P, _P, _SZ, _P]),
     "vf_embed_workspace_size": (_SZ, [_CP, _I64, C.c_int32]),
     "vf_embed_phase1": (_I32, [_CP, _P, _I64, _I32, _GP, _P, _P, _P, _SZ, _P, C.POINTER(_P)]),
-    "vf_embed_phase2": (_I32, [_CP, _P, _I64, _GP, _P, _P, _P, _SZ, _P, C.POINTER(_P)]),
+    "vf_embed_phase2": (_I32, [_CP, _P, _I64, _GP, _P, _P, _P, _I64, _P, _SZ, _P, C.POINTER(_P)]),
+    "vf_embed_graph_create": (_I32, [_CP, _P, _I64, _I32, _GP, _P, _P, _P, _I64, _P, _SZ, _P,
+                                     C.POINTER(_P)]),
+    "vf_graph_launch": (_I32, [_P, _P]),
+    "vf_graph_destroy": (None, [_P]),
     "vf_launch_count": (_I64, []),
     "vf_check_status": (_I32, [_GP, _P]),
 }

@@ -329,7 +329,7 @@ int vf_link_lengths(const vf_config *cfg, vf_grid *grid, const int32_t *cmap, co
     if (!valid_cfg(cfg) || !grid || !cmap || !faces || !lengths || (map && !d_n_map))
         return set_error(VF_EARG, "vf_link_lengths: bad argument");
     return link_impl(*cfg, grid, cmap, faces, F, map, d_n_map, lengths, ws, ws_bytes,
-                     (cudaStream_t)stream, nullptr);
+                     (cudaStream_t)stream, nullptr, nullptr, 0);
 }
 
 size_t vf_embed_workspace_size(const vf_config *cfg, int64_t F, int32_t cap) {
@@ -384,15 +384,55 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
 int64_t vf_launch_count(void) { return (int64_t)g_launches.load(); }
 
 int vf_embed_phase2(const vf_config *cfg, const double *faces, int64_t F, vf_grid *g,
-                    const int32_t *cmap, float *lengths, void *ws, size_t ws_bytes, void *stream,
-                    void **link_events) {
-    if (!valid_cfg(cfg) || !faces || !g || !cmap || !lengths)
+                    const int32_t *cmap, const int32_t *d_n_b, float *lengths, int64_t lengths_cap,
+                    void *ws, size_t ws_bytes, void *stream, void **link_events) {
+    if (!valid_cfg(cfg) || !faces || !g || !cmap || !d_n_b || !lengths || lengths_cap < 1)
         return set_error(VF_EARG, "vf_embed_phase2: bad argument");
     EmbedWs w;
     if (embed_layout(*cfg, F, g->capacity, (char *)ws, &w) > ws_bytes)
         return set_error(VF_EARG, "vf_embed_phase2: workspace too small");
-    return link_impl(*cfg, g, cmap, faces, F, nullptr, nullptr, lengths, w.link_ws, w.link_b,
-                     (cudaStream_t)stream, link_events);
+    cudaStream_t st = (cudaStream_t)stream;
+    VF_TRY(fill_lut_impl(d_n_b, lengths, lengths_cap, g->d_status, st));
+    return link_impl(*cfg, g, cmap, faces, F, nullptr, nullptr, lengths, w.link_ws, w.link_b, st,
+                     link_events, d_n_b, lengths_cap);
+}
+
+int vf_embed_graph_create(const vf_config *cfg, const double *faces, int64_t F, int use_filter,
+                          vf_grid *g, int32_t *cmap, int32_t *d_n_b, float *lengths,
+                          int64_t lengths_cap, void *ws, size_t ws_bytes, void *stream,
+                          void **graph_exec) {
+    if (!graph_exec || !stream) return set_error(VF_EARG, "vf_embed_graph_create: bad argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaStreamBeginCapture");
+    int rc = vf_embed_phase1(cfg, faces, F, use_filter, g, cmap, d_n_b, ws, ws_bytes, stream, nullptr);
+    if (!rc)
+        rc = vf_embed_phase2(cfg, faces, F, g, cmap, d_n_b, lengths, lengths_cap, ws, ws_bytes,
+                             stream, nullptr);
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(st, &graph);
+    if (rc) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaStreamEndCapture");
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaGraphInstantiate");
+    *graph_exec = (void *)exec;
+    return VF_OK;
+}
+
+int vf_graph_launch(void *graph_exec, void *stream) {
+    if (!graph_exec) return set_error(VF_EARG, "vf_graph_launch: bad argument");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGraphLaunch((cudaGraphExec_t)graph_exec, (cudaStream_t)stream);
+    return e == cudaSuccess ? VF_OK : set_cuda_error(e, "cudaGraphLaunch");
+}
+
+void vf_graph_destroy(void *graph_exec) {
+    if (graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)graph_exec);
 }
 
 int vf_check_status(const vf_grid *g, void *stream) {
@@ -402,8 +442,11 @@ int vf_check_status(const vf_grid *g, void *stream) {
     if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
     if (e != cudaSuccess) return set_cuda_error(e, "vf_check_status");
     if (h[0] == VF_ECAPACITY) {
-        char buf[128];
-        snprintf(buf, sizeof(buf), "forest capacity exhausted while refining level %d", h[1]);
+        char buf[160];
+        if (h[2] > 0)
+            snprintf(buf, sizeof(buf), "link table capacity exhausted: %d boundary blocks", h[2]);
+        else
+            snprintf(buf, sizeof(buf), "forest capacity exhausted while refining level %d", h[1]);
         return set_error(VF_ECAPACITY, buf);
     }
     if (h[0] == VF_ENLIM) return set_error(VF_ENLIM, "N_lim pair cap violated (refine_faces the mesh)");

@@ -75,6 +75,9 @@ int tables_impl(vf_grid *g, const int32_t *bcount, int32_t *cmap, int32_t *d_n_b
 size_t link_workspace_size(const vf_config &cfg, int finest);
 int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
               int64_t F, const int32_t *map, const int32_t *d_n_map, float *lengths, void *ws,
-              size_t ws_bytes, cudaStream_t st, void **events);
+              size_t ws_bytes, cudaStream_t st, void **events, const int32_t *d_n_b,
+              int64_t lengths_cap);
+int fill_lut_impl(const int32_t *d_n_b, float *lengths, int64_t cap, int32_t *d_status,
+                  cudaStream_t st);
 
 }  // namespace vf

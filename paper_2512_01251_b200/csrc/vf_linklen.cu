@@ -2,30 +2,30 @@
 //
 // FACE-parallel formulation.  A link (lattice node v of a mapped finest-level
 // block, direction c_q, 0 < d <= dx) is accepted when the eps-cube around its
-// piercing point v + d c_q overlaps the face (exact SAT), and the LUT keeps the
+// piercing point v + d c_q overlaps the face (exact SAT); the LUT keeps the
 // minimum q = d/dx over faces.  Instead of every cell scanning its block's
 // all-directions bin (the paper's per-cell loop), every face enumerates the
-// nodes that can pierce it and min-merges q into the LUT with atomicMin on the
-// IEEE bits -- order-free, hence deterministic and equal to the per-cell
-// minimum (for q > 0 the uint32 order is the float order, and the -1.0f
-// initialisation 0xBF800000 sorts above every positive float, so "no hit"
-// needs no finalisation pass).  A dense block map of the finest level replaces
-// the bin lookup; the all-directions binning drops out of the embed path (the
-// result is invariant to it; the oracle uses the MD bins).
+// lattice LINES that pierce it and min-merges q into the LUT with atomicMin on
+// the IEEE bits -- order-free, hence deterministic and equal to the per-cell
+// minimum (for q > 0 uint32 order is float order, and the -1.0f initialisation
+// 0xBF800000 sorts above every positive float, so "no hit" needs no final
+// pass).  A dense block map of the finest level replaces the bin lookup; the
+// all-directions binning drops out of the embed path (the result is invariant
+// to it; the oracle keeps the per-cell MD-bin formulation).
 //
-// K-link, per warp and chunk of 32 faces:
-//   1. lane-parallel face setup into shared memory (struct-of-arrays: lanes
-//      reading different faces hit different banks): sweep axis a = dominant
-//      normal component, column range, slab half-width, 2D edge functions of
-//      the face projected along a.
-//   2. the items (column, slab position) of the 32 faces are flattened so the
-//      32 lanes stay busy whatever the face sizes; per node an FP32
-//      pre-filter (|num| <= |c.n| dx, piercing point inside the projected
-//      triangle, margins >= 10x the FP32 error bound) keeps candidates.
-//   3. candidates enter a per-warp shared-memory queue that is drained 32 at a
-//      time through the exact FP64 path, so the SAT runs warp-converged.
-// The pre-filter only ever passes a superset of the exact decisions; every
-// stored value comes from the exact path, bit-identical to the oracle.
+// K-link, thread per face, for each of the 13 antiparallel direction pairs c:
+//   - the lattice lines along c cut the coordinate plane x_p = v1_p (p = first
+//     axis with c_p != 0) in a square lattice of pitch dx; project the
+//     triangle along c onto that plane and enumerate the lattice points of its
+//     bounding box that fall inside the projected triangle (FP32, relative to
+//     v1, margins >= 10x the FP32 error bound);
+//   - a line through the triangle meets the face plane at one point; the
+//     (2, rarely 3) lattice nodes within one link of that crossing are the
+//     only possible link endpoints, in +c or -c direction.
+// Candidates (face, node, pair) go to a per-warp shared-memory queue drained
+// 32 at a time through the exact FP64 path (bit-identical to the oracle), so
+// the SAT runs warp-converged.  The pre-filter passes a superset of the exact
+// decisions; every stored value comes from the exact path.
 #include <math.h>
 
 #include "vf_common.cuh"
@@ -33,9 +33,13 @@
 
 namespace vf {
 
+// dense finest-level block -> LUT slot map; nothing is mapped when the
+// device-resident N_b exceeds the LUT capacity (error latched by k_fill_lut)
 __global__ void k_blockmap(int L, int bx, int by, const int32_t *__restrict__ level_start,
                            const int32_t *__restrict__ coords, const int32_t *__restrict__ cmap,
-                           int32_t *__restrict__ bmap) {
+                           int32_t *__restrict__ bmap, const int32_t *__restrict__ d_n_b,
+                           int64_t cap) {
+    if (d_n_b && *d_n_b > cap) return;
     const int32_t s = level_start[L], e = level_start[L + 1];
     for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
          b += (int64_t)gridDim.x * blockDim.x) {
@@ -85,214 +89,194 @@ __device__ __noinline__ void link_candidate(const double *__restrict__ faces, in
 }
 
 constexpr int kLinkWarps = 4;
-constexpr int kQueue = 32 + 32 * 13;
+constexpr int kQueue = 640;
 
-// per-warp face table, struct-of-arrays
-struct LinkFaces {
-    double v1[3][32];
-    float nf[3][32];
-    float ea[3][32], eb[3][32], ec[3][32];  // inward unit edge functions (u,w plane)
-    float Ef[32];                            // FP32 error bound of num (absolute)
-    float Tf[32];                            // slab half-width for |num|
-    int f[32], ax[32], cu0[32], cw0[32], ncu[32], span[32], a1a[32], b1a[32];
-    int pref[33];
+struct LinkQueue {
+    int4 e[kLinkWarps][kQueue];  // (face, slot, i | j<<16, k | r<<16)
+    int n[kLinkWarps];
 };
 
-__device__ __forceinline__ int floor_idx(double xs) { return (int)floor(xs); }
+struct LinkCtx {
+    const double *faces;
+    const int32_t *bmap;
+    float *lengths;
+    double dx, eps, eps_par;
+    int bx, by, cells[3];
+};
+
+__device__ __forceinline__ void push_candidate(LinkQueue &Q, int w, const LinkCtx &c, int f, int slot,
+                                               int i, int j, int k, int r) {
+    const int pos = atomicAdd(&Q.n[w], 1);
+    if (pos < kQueue) {
+        Q.e[w][pos] = make_int4(f, slot, i | (j << 16), k | (r << 16));
+    } else {  // overflow (pathological face): decide inline, same exact path
+        link_candidate(c.faces, f, r, i, j, k, c.dx, c.eps, c.eps_par, slot, c.lengths);
+    }
+}
+
+// drain the queue in full warps (all = drain the remainder too); warp-uniform
+__device__ __forceinline__ void drain(LinkQueue &Q, int w, int lane, const LinkCtx &c, bool all) {
+    __syncwarp();
+    int n = min(Q.n[w], kQueue);
+    while (n >= 32 || (all && n > 0)) {
+        const int take = min(n, 32);
+        int4 e = make_int4(0, -1, 0, 0);
+        if (lane < take) e = Q.e[w][n - take + lane];
+        __syncwarp();
+        if (lane < take)
+            link_candidate(c.faces, e.x, e.w >> 16, e.z & 0xffff, e.z >> 16, e.w & 0xffff, c.dx,
+                           c.eps, c.eps_par, e.y, c.lengths);
+        n -= take;
+    }
+    __syncwarp();
+    if (lane == 0) Q.n[w] = n;
+    __syncwarp();
+}
+
+// one direction pair r (compile-time): enumerate lattice lines along c that
+// pierce the face, push the nodes within one link of each crossing
+template <int R>
+__device__ __forceinline__ void face_direction(LinkQueue &Q, int w, const LinkCtx &c, int f,
+                                               const double *v, const float *nf, const float *V1,
+                                               const float *V2, float Ef, int lo_p[3], int hi_p[3]) {
+    constexpr int q = 2 * R + 1;
+    const int cc[3] = {c27(q, 0), c27(q, 1), c27(q, 2)};
+    const int p = cc[0] != 0 ? 0 : (cc[1] != 0 ? 1 : 2);
+    const int q1 = p == 0 ? 1 : 0, q2 = p == 2 ? 1 : 2;
+    const int s1 = cc[q1] * cc[p], s2 = cc[q2] * cc[p];  // c_q / c_p (c_p = +-1)
+    const float dn = (float)cc[0] * nf[0] + (float)cc[1] * nf[1] + (float)cc[2] * nf[2];
+    const double dx = c.dx;
+    const float dxf = (float)dx;
+    // projected triangle (relative to v1) on the plane x_p = v1_p
+    const float P0a = 0.0f, P0b = 0.0f;
+    const float P1a = V1[q1] - (float)s1 * V1[p], P1b = V1[q2] - (float)s2 * V1[p];
+    const float P2a = V2[q1] - (float)s1 * V2[p], P2b = V2[q2] - (float)s2 * V2[p];
+    const float cr = P1a * P2b - P1b * P2a;
+    const float ext = fmaxf(fmaxf(fabsf(P1a), fabsf(P1b)), fmaxf(fabsf(P2a), fabsf(P2b)));
+    // tolerance: eps-cube acceptance (<= 2 sqrt 6 eps after the oblique
+    // projection) + FP32 error of coordinates of magnitude ext + dx
+    const float tol = 1e-5f * (ext + dxf) + 6.0f * (float)c.eps;
+    // (a degenerate projection -- face parallel to c -- keeps only lattice
+    // points within tol of the projected segment: the edge tests stay valid)
+    const float sg = cr >= 0.0f ? 1.0f : -1.0f;
+    // inward edge functions (not normalised): E_k(P) = sg * cross(edge_k, P - P_k)
+    const float e0a = P1a - P0a, e0b = P1b - P0b;
+    const float e1a = P2a - P1a, e1b = P2b - P1b;
+    const float e2a = P0a - P2a, e2b = P0b - P2b;
+    const float l0 = sqrtf(e0a * e0a + e0b * e0b), l1 = sqrtf(e1a * e1a + e1b * e1b),
+                l2 = sqrtf(e2a * e2a + e2b * e2b);
+    // lattice of line traces: coordinate j of the trace of the line through
+    // node (i_p, i_q1, i_q2) is ((i_qj - s_j i_p) + delta_j) dx + s_j v1_p,
+    // delta_j = (1 - s_j)/2; relative to v1: subtract v1_qj
+    const double off1 = (double)s1 * v[p] - v[q1], off2 = (double)s2 * v[p] - v[q2];
+    const double d1 = 0.5 * (1 - s1), d2 = 0.5 * (1 - s2);
+    const float bmin1 = fminf(fminf(P0a, P1a), P2a) - tol, bmax1 = fmaxf(fmaxf(P0a, P1a), P2a) + tol;
+    const float bmin2 = fminf(fminf(P0b, P1b), P2b) - tol, bmax2 = fmaxf(fmaxf(P0b, P1b), P2b) + tol;
+    const double inv = 1.0 / dx;
+    const int m1a = (int)ceil(((double)bmin1 - off1) * inv - d1 - 1e-6);
+    const int m1b = (int)floor(((double)bmax1 - off1) * inv - d1 + 1e-6);
+    const int m2a = (int)ceil(((double)bmin2 - off2) * inv - d2 - 1e-6);
+    const int m2b = (int)floor(((double)bmax2 - off2) * inv - d2 + 1e-6);
+    const bool steep = fabsf(dn) >= 1e-3f;
+    for (int m2 = m2a; m2 <= m2b; ++m2) {
+        const float Rb = (float)(((double)m2 + d2) * dx + off2);
+        for (int m1 = m1a; m1 <= m1b; ++m1) {
+            const float Ra = (float)(((double)m1 + d1) * dx + off1);
+            // inside the projected triangle (with tolerance)
+            const float E0 = sg * (e0a * (Rb - P0b) - e0b * (Ra - P0a));
+            const float E1 = sg * (e1a * (Rb - P1b) - e1b * (Ra - P1a));
+            const float E2 = sg * (e2a * (Rb - P2b) - e2b * (Ra - P2a));
+            if (E0 < -tol * l0 || E1 < -tol * l1 || E2 < -tol * l2) continue;
+            // crossing with the face plane: Q = v1 + Ra e_q1 + Rb e_q2 (+0 e_p),
+            // points Q + lam c; n.(Q + lam c - v1) = 0
+            int ip_lo, ip_hi;
+            if (steep) {
+                const float lam = -(nf[q1] * Ra + nf[q2] * Rb) / dn;
+                const float xs = (float)cc[p] * lam;  // x_p* - v1_p
+                const float wid = dxf * (1.0f + 1e-4f) + (Ef + 1e-6f * fabsf(xs)) / fabsf(dn) + 1e-5f * dxf;
+                // node index i_p with |x_p* - (i_p + 0.5) dx| <= dx
+                ip_lo = (int)ceil(((double)(xs - wid) + v[p]) * inv - 0.5);
+                ip_hi = (int)floor(((double)(xs + wid) + v[p]) * inv - 0.5);
+                ip_lo = max(ip_lo, lo_p[p]);
+                ip_hi = min(ip_hi, hi_p[p]);
+            } else {  // ill-conditioned crossing: every node of the face's p-range +- dx
+                ip_lo = lo_p[p];
+                ip_hi = hi_p[p];
+            }
+            for (int ip = ip_lo; ip <= ip_hi; ++ip) {
+                int idx[3];
+                idx[p] = ip;
+                // i_qj = m_j + s_j i_p
+                idx[q1] = m1 + s1 * ip;
+                idx[q2] = m2 + s2 * ip;
+                if (idx[q1] < 0 || idx[q1] >= c.cells[q1] || idx[q2] < 0 || idx[q2] >= c.cells[q2]) continue;
+                const int32_t slot =
+                    c.bmap[(idx[0] >> 2) + (int64_t)c.bx * ((idx[1] >> 2) + (int64_t)c.by * (idx[2] >> 2))];
+                if (slot < 0) continue;
+                push_candidate(Q, w, c, f, slot, idx[0], idx[1], idx[2], R);
+            }
+        }
+    }
+}
+
+template <int R>
+struct DirLoop {
+    __device__ __forceinline__ static void run(LinkQueue &Q, int w, int lane, const LinkCtx &c, int f,
+                                               bool active, const double *v, const float *nf,
+                                               const float *V1, const float *V2, float Ef,
+                                               int *lo_p, int *hi_p) {
+        if (active) face_direction<R>(Q, w, c, f, v, nf, V1, V2, Ef, lo_p, hi_p);
+        drain(Q, w, lane, c, false);
+        DirLoop<R + 1>::run(Q, w, lane, c, f, active, v, nf, V1, V2, Ef, lo_p, hi_p);
+    }
+};
+template <>
+struct DirLoop<13> {
+    __device__ __forceinline__ static void run(LinkQueue &, int, int, const LinkCtx &, int, bool,
+                                               const double *, const float *, const float *,
+                                               const float *, float, int *, int *) {}
+};
 
 __global__ void __launch_bounds__(kLinkWarps * 32)
-    k_links(LevelInfo li, double inv_dx, int widen, const double *__restrict__ faces, int64_t F,
-            const int32_t *__restrict__ map, const int32_t *__restrict__ d_n_map,
-            const int32_t *__restrict__ bmap, float *__restrict__ lengths) {
-    __shared__ LinkFaces s_tab[kLinkWarps];
-    __shared__ int4 s_q[kLinkWarps][kQueue];
+    k_links(LinkCtx c, double inv_dx, int widen, int64_t F, const int32_t *__restrict__ map,
+            const int32_t *__restrict__ d_n_map) {
+    __shared__ LinkQueue Q;
     const int64_t n = d_n_map ? (int64_t)*d_n_map : F;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t gw = (int64_t)blockIdx.x * kLinkWarps + wib;
-    const int64_t nw = (int64_t)gridDim.x * kLinkWarps;
-    const double dx = li.dx, eps = li.eps;
-    const float dxf = (float)dx;
-    LinkFaces &T = s_tab[wib];
-    int qn = 0;  // warp-uniform queue length
-
-    for (int64_t chunk = gw * 32; chunk < n; chunk += nw * 32) {
-        // ---- 1. face setup, one face per lane --------------------------------
-        const int64_t m = chunk + lane;
-        int total = 0;
-        if (m < n) {
-            const int64_t f = map ? (int64_t)map[m] : m;
-            double v[9], nn[3];
-            load_face(faces, f, v, nn);
-            int a1[3], b1[3];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) Q.n[w] = 0;
+    __syncwarp();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // all lanes of a warp iterate together (uniform trip count) so drains are
+    // warp-synchronous; lanes past the end are inactive
+    const int64_t first = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    for (int64_t base = first; base < n; base += stride) {
+        const int64_t m = base + lane;
+        const bool active = m < n;
+        double v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, nn[3] = {0, 0, 0};
+        int f = 0;
+        float nf[3] = {0, 0, 0}, V1[3] = {0, 0, 0}, V2[3] = {0, 0, 0}, Ef = 0.0f;
+        int lo_p[3] = {0, 0, 0}, hi_p[3] = {-1, -1, -1};
+        if (active) {
+            f = map ? map[m] : (int)m;
+            load_face(c.faces, f, v, nn);
             double ext = 0.0;
-            bool empty = false;
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
+                nf[d] = (float)nn[d];
+                V1[d] = (float)(v[3 + d] - v[d]);
+                V2[d] = (float)(v[6 + d] - v[d]);
                 const double lo = fmin(fmin(v[d], v[3 + d]), v[6 + d]);
                 const double hi = fmax(fmax(v[d], v[3 + d]), v[6 + d]);
                 ext = fmax(ext, hi - lo);
-                // nodes whose centres can lie in [lo - dx - 2eps, hi + dx + 2eps]
-                // (superset; inv_dx is exact for power-of-two dx, else widened)
-                int ia = floor_idx((lo - dx - 2.0 * eps) * inv_dx - 0.5) - widen;
-                int ib = floor_idx((hi + dx + 2.0 * eps) * inv_dx - 0.5) + 1 + widen;
-                ia = max(ia, 0);
-                ib = min(ib, li.cells[d] - 1);
-                a1[d] = ia;
-                b1[d] = ib;
-                empty |= ia > ib;
+                // nodes within one link of the face AABB (fallback range)
+                lo_p[d] = max((int)floor((lo - c.dx - 2.0 * c.eps) * inv_dx - 0.5) - widen, 0);
+                hi_p[d] = min((int)floor((hi + c.dx + 2.0 * c.eps) * inv_dx - 0.5) + 1 + widen, c.cells[d] - 1);
             }
-            if (!empty) {
-                const float nf0 = (float)nn[0], nf1 = (float)nn[1], nf2 = (float)nn[2];
-                const float ax0 = fabsf(nf0), ax1 = fabsf(nf1), ax2 = fabsf(nf2);
-                const int a = (ax0 >= ax1 && ax0 >= ax2) ? 0 : (ax1 >= ax2 ? 1 : 2);
-                const int u = a == 2 ? 0 : a + 1, w = a == 0 ? 2 : a - 1;  // cyclic (a,u,w)
-                const float na = a == 0 ? nf0 : (a == 1 ? nf1 : nf2);
-                const float Ef = 4e-6f * (float)(ext + 2.0 * dx);
-                const float Tf = 1.7320508f * dxf * (1.0f + 1e-5f) + Ef;
-                const int span = (int)floorf(2.0f * Tf / (fabsf(na) * dxf)) + 2;
-                const int ncu = b1[u] - a1[u] + 1, ncw = b1[w] - a1[w] + 1;
-                total = ncu * ncw * span;
-                // 2D edge functions in the (u,w) projection, relative to v1
-                const float p1u = (float)(v[3 + u] - v[u]), p1w = (float)(v[3 + w] - v[w]);
-                const float p2u = (float)(v[6 + u] - v[u]), p2w = (float)(v[6 + w] - v[w]);
-                const float cr = p1u * p2w - p1w * p2u;
-                const float sg = cr >= 0.0f ? 1.0f : -1.0f;
-                const float Pu[3] = {0.0f, p1u, p2u}, Pw[3] = {0.0f, p1w, p2w};
-#pragma unroll
-                for (int e = 0; e < 3; ++e) {
-                    const int e1 = e == 2 ? 0 : e + 1;
-                    const float du = Pu[e1] - Pu[e], dw = Pw[e1] - Pw[e];
-                    const float len = sqrtf(du * du + dw * dw);
-                    const float il = len > 0.0f ? sg / len : 0.0f;
-                    T.ea[e][lane] = -dw * il;
-                    T.eb[e][lane] = du * il;
-                    T.ec[e][lane] = (dw * Pu[e] - du * Pw[e]) * il;
-                }
-                T.v1[0][lane] = v[0]; T.v1[1][lane] = v[1]; T.v1[2][lane] = v[2];
-                T.nf[0][lane] = nf0; T.nf[1][lane] = nf1; T.nf[2][lane] = nf2;
-                T.Ef[lane] = Ef;
-                T.Tf[lane] = Tf;
-                T.f[lane] = (int)f;
-                T.ax[lane] = a;
-                T.cu0[lane] = a1[u];
-                T.cw0[lane] = a1[w];
-                T.ncu[lane] = ncu;
-                T.span[lane] = span;
-                T.a1a[lane] = a1[a];
-                T.b1a[lane] = b1[a];
-            }
+            Ef = 4e-6f * (float)(ext + 2.0 * c.dx);
         }
-        int incl = total;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        T.pref[lane + 1] = incl;
-        if (lane == 0) T.pref[0] = 0;
-        const int grand = __shfl_sync(0xffffffffu, incl, 31);
-        __syncwarp();
-
-        // ---- 2. flattened items ---------------------------------------------
-        for (int base = 0; base < grand; base += 32) {
-            const int g = base + lane;
-            uint32_t cand = 0;
-            int ni = 0, nj = 0, nk = 0, slot = -1, fid = 0;
-            if (g < grand) {
-                int lo = 0, hi = 32;  // largest fi with pref[fi] <= g
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (T.pref[mid] <= g) lo = mid;
-                    else hi = mid;
-                }
-                const int fi = lo;
-                const int kk = g - T.pref[fi];
-                const int a = T.ax[fi];
-                const int u = a == 2 ? 0 : a + 1, w = a == 0 ? 2 : a - 1;
-                const int span = T.span[fi], ncu = T.ncu[fi];
-                const int col = kk / span, sidx = kk - col * span;
-                const int iu = T.cu0[fi] + col % ncu, iw = T.cw0[fi] + col / ncu;
-                const double va = T.v1[a][fi], vu = T.v1[u][fi], vw = T.v1[w][fi];
-                const float na = T.nf[a][fi], nu = T.nf[u][fi], nwv = T.nf[w][fi];
-                const float Tf = T.Tf[fi], Ef = T.Ef[fi];
-                const float Xu = (float)(node_c(iu, dx) - vu);
-                const float Xw = (float)(node_c(iw, dx) - vw);
-                const float C = Xu * nu + Xw * nwv;
-                // |Xa na + C| <= Tf  <=>  Xa in [(-C - Tf)/na, (-C + Tf)/na]
-                float xa0 = (-C - Tf) / na, xa1 = (-C + Tf) / na;
-                if (xa0 > xa1) { const float tmp = xa0; xa0 = xa1; xa1 = tmp; }
-                const int ia_lo = max(floor_idx(((double)xa0 + va) * inv_dx - 0.5) - widen, T.a1a[fi]);
-                const int ia_hi = min(floor_idx(((double)xa1 + va) * inv_dx - 0.5) + 1 + widen, T.b1a[fi]);
-                const int ia = ia_lo + sidx;
-                if (ia <= ia_hi) {
-                    ni = a == 0 ? ia : (u == 0 ? iu : iw);
-                    nj = a == 1 ? ia : (u == 1 ? iu : iw);
-                    nk = a == 2 ? ia : (u == 2 ? iu : iw);
-                    slot = bmap[(ni >> 2) + (int64_t)li.bins[0] * ((nj >> 2) + (int64_t)li.bins[1] * (nk >> 2))];
-                }
-                if (slot >= 0) {
-                    fid = T.f[fi];
-                    const float Xa = (float)(node_c(ia, dx) - va);
-                    const float numf = -(Xa * na + C);  // (v1 - x).n
-                    if (fabsf(numf) <= Tf) {
-                        const float ea0 = T.ea[0][fi], eb0 = T.eb[0][fi], ec0 = T.ec[0][fi];
-                        const float ea1 = T.ea[1][fi], eb1 = T.eb[1][fi], ec1 = T.ec[1][fi];
-                        const float ea2 = T.ea[2][fi], eb2 = T.eb[2][fi], ec2 = T.ec[2][fi];
-                        const float base_tol = 1e-5f * dxf + 2.0f * (float)eps;
-#pragma unroll
-                        for (int r = 0; r < 13; ++r) {
-                            const int q = 2 * r + 1;
-                            const int cx = c27(q, 0), cy = c27(q, 1), cz = c27(q, 2);
-                            const int ca = a == 0 ? cx : (a == 1 ? cy : cz);
-                            const int cu = u == 0 ? cx : (u == 1 ? cy : cz);
-                            const int cw = w == 0 ? cx : (w == 1 ? cy : cz);
-                            const float dn = (float)ca * na + (float)cu * nu + (float)cw * nwv;
-                            const float adn = fabsf(dn);
-                            bool ok = fabsf(numf) <= fmaf(adn, dxf * (1.0f + 1e-5f), Ef);
-                            ok &= adn > 0.0f;  // exact |den| >= 1e-12 |c|
-                            const float rd = 1.0f / dn;
-                            const float da = numf * rd;  // ~ d
-                            const float Pu = Xu + (float)cu * da, Pw = Xw + (float)cw * da;
-                            const float tol = fmaf(Ef, fabsf(rd), fmaf(1e-6f, fabsf(da), base_tol));
-                            ok &= fmaf(ea0, Pu, fmaf(eb0, Pw, ec0)) >= -tol;
-                            ok &= fmaf(ea1, Pu, fmaf(eb1, Pw, ec1)) >= -tol;
-                            ok &= fmaf(ea2, Pu, fmaf(eb2, Pw, ec2)) >= -tol;
-                            cand |= (uint32_t)ok << r;
-                        }
-                    }
-                }
-            }
-            // ---- 3. enqueue, drain in full warps ------------------------------
-            const int nc = __popc(cand);
-            int off = nc;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, off, o);
-                if (lane >= o) off += y;
-            }
-            const int added = __shfl_sync(0xffffffffu, off, 31);
-            off += qn - nc;
-            for (uint32_t c = cand; c; c &= c - 1)
-                s_q[wib][off++] = make_int4(fid, slot, ni | (nj << 16), nk | ((__ffs(c) - 1) << 16));
-            qn += added;
-            __syncwarp();
-            while (qn >= 32) {
-                const int4 e = s_q[wib][qn - 32 + lane];
-                __syncwarp();
-                link_candidate(faces, e.x, e.w >> 16, e.z & 0xffff, e.z >> 16, e.w & 0xffff, dx, eps,
-                               li.eps_par, e.y, lengths);
-                qn -= 32;
-            }
-            __syncwarp();
-        }
-        __syncwarp();
+        DirLoop<0>::run(Q, w, lane, c, f, active, v, nf, V1, V2, Ef, lo_p, hi_p);
     }
-    // drain the remainder
-    if (lane < qn) {
-        const int4 e = s_q[wib][lane];
-        link_candidate(faces, e.x, e.w >> 16, e.z & 0xffff, e.z >> 16, e.w & 0xffff, dx, eps,
-                       li.eps_par, e.y, lengths);
-    }
+    drain(Q, w, lane, c, true);
 }
 
 size_t link_workspace_size(const vf_config &cfg, int finest) {
@@ -300,32 +284,67 @@ size_t link_workspace_size(const vf_config &cfg, int finest) {
     return ((size_t)nb * sizeof(int32_t) + 255) & ~(size_t)255;
 }
 
+// LUT initialisation to -1 for the device-resident N_b slots (graph-safe:
+// no host knowledge of N_b); N_b > cap latches VF_ECAPACITY with the count
+__global__ void k_fill_lut(const int32_t *__restrict__ d_n_b, float *__restrict__ lengths, int64_t cap,
+                           int32_t *__restrict__ status) {
+    const int64_t nb = *d_n_b;
+    if (nb > cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            atomicMax(status, VF_ECAPACITY);
+            status[2] = (int32_t)nb;
+        }
+        return;
+    }
+    const int64_t n4 = nb * 27 * 64 / 4;
+    float4 *p = reinterpret_cast<float4 *>(lengths);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = make_float4(-1.0f, -1.0f, -1.0f, -1.0f);
+}
+
+int fill_lut_impl(const int32_t *d_n_b, float *lengths, int64_t cap, int32_t *d_status,
+                  cudaStream_t st) {
+    k_fill_lut<<<max_ctas(4), 256, 0, st>>>(d_n_b, lengths, cap, d_status);
+    return check_launch("k_fill_lut");
+}
+
 int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
               int64_t F, const int32_t *map, const int32_t *d_n_map, float *lengths, void *ws,
-              size_t ws_bytes, cudaStream_t st, void **events) {
+              size_t ws_bytes, cudaStream_t st, void **events, const int32_t *d_n_b,
+              int64_t lengths_cap) {
     const int L = g->n_levels - 1;
     if (ws_bytes < link_workspace_size(cfg, L)) return set_error(VF_EARG, "link workspace too small");
     const LevelInfo li = make_level(cfg, L);
-    if (li.cells[0] > 65535 || li.cells[1] > 65535 || li.cells[2] > 65535)
-        return set_error(VF_EARG, "link lengths: > 65535 cells per axis");
+    if (li.cells[0] > 32767 || li.cells[1] > 32767 || li.cells[2] > 32767)
+        return set_error(VF_EARG, "link lengths: > 32767 cells per axis");
     const int64_t nb = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
     int32_t *bmap = (int32_t *)ws;
     cudaMemsetAsync(bmap, 0xff, sizeof(int32_t) * (size_t)nb, st);
     k_blockmap<<<max_ctas(8), 256, 0, st>>>(L, li.bins[0], li.bins[1], g->d_level_start, g->d_coords,
-                                            cmap, bmap);
+                                            cmap, bmap, d_n_b, lengths_cap);
     int rc = check_launch("k_blockmap");
     if (rc) return rc;
+    LinkCtx c;
+    c.faces = faces;
+    c.bmap = bmap;
+    c.lengths = lengths;
+    c.dx = li.dx;
+    c.eps = li.eps;
+    c.eps_par = li.eps_par;
+    c.bx = li.bins[0];
+    c.by = li.bins[1];
+    for (int d = 0; d < 3; ++d) c.cells[d] = li.cells[d];
     // 1/dx is exact when dx is a power of two; otherwise widen the ranges by one
     int ex = 0;
     const double mant = frexp(li.dx, &ex);
     const int widen = (mant == 0.5) ? 0 : 1;
     const double inv_dx = 1.0 / li.dx;
     int64_t grid = (F + 32 * kLinkWarps - 1) / (32 * kLinkWarps);
-    if (grid > max_ctas(4)) grid = max_ctas(4);
+    if (grid > max_ctas(6)) grid = max_ctas(6);
     if (grid < 1) grid = 1;
     if (events) cudaEventRecord((cudaEvent_t)events[0], st);
-    k_links<<<(int)grid, kLinkWarps * 32, 0, st>>>(li, inv_dx, widen, faces, F, map, d_n_map, bmap,
-                                                  lengths);
+    k_links<<<(int)grid, kLinkWarps * 32, 0, st>>>(c, inv_dx, widen, F, map, d_n_map);
     rc = check_launch("k_links");
     if (events) cudaEventRecord((cudaEvent_t)events[1], st);
     return rc;

@@ -153,11 +153,14 @@ class EmbedTimings:
 
 
 class EmbedEngine:
-    """Reusable embed context: device mesh, grid, workspace and the LUT are
-    allocated once for (mesh, cfg) and reused across calls (the geometry is
-    static, PAPER.md:273)."""
+    """Reusable embed context for one (mesh, cfg): device mesh, forest arrays,
+    workspace, LUT and -- after the first run -- a CUDA graph of the whole
+    embed are allocated once and reused (the geometry is static,
+    PAPER.md:273).  All work runs on the engine's own stream, ordered after
+    the caller's current stream."""
 
-    def __init__(self, mesh, cfg: EmbedConfig, capacity: Optional[int] = None):
+    def __init__(self, mesh, cfg: EmbedConfig, capacity: Optional[int] = None,
+                 use_graph: bool = True):
         import torch
         self.lib = _lib.require_cuda()
         self.cfg = cfg
@@ -171,55 +174,117 @@ class EmbedEngine:
         self.ws = torch.empty(int(wsb), dtype=torch.uint8, device="cuda")
         self.cmap = torch.empty(cap, dtype=torch.int32, device="cuda")
         self.n_b_dev = torch.zeros(1, dtype=torch.int32, device="cuda")
-        self.n_b_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self.host = torch.zeros(8, dtype=torch.int32).pin_memory()  # 0-3 status, 4 n_b
+        self.stream = torch.cuda.Stream()
         self.lengths = None
         self.bc_ids = None
+        self.lengths_cap = 0
+        self.use_graph = use_graph
+        self._graphs = {}
         self.n_events = 64
         self.events = [torch.cuda.Event(enable_timing=True) for _ in range(self.n_events)]
-        self._ev_arr = (C.c_void_p * self.n_events)(*[C.c_void_p(e.cuda_event) for e in self.events])
+        self._ev_arr = None
+
+    def __del__(self):
+        try:
+            for g in self._graphs.values():
+                self.lib.vf_graph_destroy(g)
+        except Exception:
+            pass
 
     def _ensure_events(self):
-        for e in self.events:   # lazily created by torch on first record
-            e.record()
-        self._ev_arr = (C.c_void_p * self.n_events)(*[C.c_void_p(e.cuda_event) for e in self.events])
+        if self._ev_arr is None:
+            for e in self.events:   # handles are created lazily on first record
+                e.record(self.stream)
+            self._ev_arr = (C.c_void_p * self.n_events)(*[C.c_void_p(e.cuda_event) for e in self.events])
+
+    def _alloc_lut(self, n_b: int):
+        import torch
+        cap = int(n_b * 1.25) + 16
+        self.lengths = torch.empty((cap, 27, 64), dtype=torch.float32, device="cuda")
+        self.bc_ids = torch.zeros((cap, 27, 64), dtype=torch.int8, device="cuda")
+        self.lengths_cap = cap
+        for g in self._graphs.values():
+            self.lib.vf_graph_destroy(g)
+        self._graphs.clear()
+
+    def _phase1(self, uf, st, ev):
+        gs = self.grid._struct()
+        _lib.check(self.lib.vf_embed_phase1(
+            C.byref(self.c), _lib.ptr(self.mesh.faces), self.mesh.n_faces, int(bool(uf)), C.byref(gs),
+            _lib.ptr(self.cmap), _lib.ptr(self.n_b_dev), _lib.ptr(self.ws), self.ws.numel(), st, ev),
+            "embed_geometry")
+        self.grid.n_levels = gs.n_levels
+        return gs
+
+    def _phase2(self, gs, st, lev):
+        _lib.check(self.lib.vf_embed_phase2(
+            C.byref(self.c), _lib.ptr(self.mesh.faces), self.mesh.n_faces, C.byref(gs),
+            _lib.ptr(self.cmap), _lib.ptr(self.n_b_dev), _lib.ptr(self.lengths), self.lengths_cap,
+            _lib.ptr(self.ws), self.ws.numel(), st, lev), "embed_geometry")
+
+    def _finish(self, st_obj):
+        """Async read of status + N_b, one sync, error mapping."""
+        import torch
+        self.host[0:4].copy_(self.grid.status, non_blocking=True)
+        self.host[4:5].copy_(self.n_b_dev, non_blocking=True)
+        st_obj.synchronize()
+        h = self.host.tolist()
+        if h[0]:
+            gs = self.grid._struct()
+            _lib.check(self.lib.vf_check_status(C.byref(gs), _lib.stream_ptr(st_obj)), "embed_geometry")
+        return int(h[4])
 
     def run(self, timed: bool = False, use_filter: Optional[bool] = None):
-        """Full embed.  Returns (grid, LinkTable).  One host sync (N_b, for the
-        LUT allocation)."""
+        """Full embed -> (grid, LinkTable).  Steady state is one CUDA-graph
+        launch and one host sync at the end (status + N_b)."""
         import torch
-        lib, g = self.lib, self.grid
-        uf = self.cfg.use_filter if use_filter is None else use_filter
-        if timed:
-            self._ensure_events()
-        st = _lib.stream_ptr()
-        gs = g._struct()
-        ev = C.cast(self._ev_arr, C.POINTER(C.c_void_p)) if timed else None
-        _lib.check(lib.vf_embed_phase1(C.byref(self.c), _lib.ptr(self.mesh.faces), self.mesh.n_faces,
-                                       int(bool(uf)), C.byref(gs), _lib.ptr(self.cmap),
-                                       _lib.ptr(self.n_b_dev), _lib.ptr(self.ws), self.ws.numel(),
-                                       st, ev), "embed_geometry")
-        g.n_levels = gs.n_levels
-        self.n_b_host.copy_(self.n_b_dev, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        _lib.check(lib.vf_check_status(C.byref(gs), st), "embed_geometry")
-        n_b = int(self.n_b_host[0])
-        if self.lengths is None or self.lengths.shape[0] < n_b:
-            self.lengths = torch.empty((max(n_b, 1), 27, 64), dtype=torch.float32, device="cuda")
-            self.bc_ids = torch.zeros((max(n_b, 1), 27, 64), dtype=torch.int8, device="cuda")
-        lengths = self.lengths[:n_b]
-        lengths.fill_(-1.0)
-        lev = None
-        if timed:
-            lev = C.cast(C.byref(self._ev_arr, C.sizeof(C.c_void_p) * (self.n_events - 3)),
-                         C.POINTER(C.c_void_p))
-        _lib.check(lib.vf_embed_phase2(C.byref(self.c), _lib.ptr(self.mesh.faces), self.mesh.n_faces,
-                                       C.byref(gs), _lib.ptr(self.cmap), _lib.ptr(lengths),
-                                       _lib.ptr(self.ws), self.ws.numel(), st, lev),
-                   "embed_geometry")
-        if timed:
-            self.events[self.n_events - 1].record()
-        table = LinkTable(lengths, self.bc_ids[:n_b], self.cmap, n_b)
-        return g, table
+        uf = bool(self.cfg.use_filter if use_filter is None else use_filter)
+        cur = torch.cuda.current_stream()
+        self.stream.wait_stream(cur)
+        st = _lib.stream_ptr(self.stream)
+        with torch.cuda.stream(self.stream):
+            if self.lengths is None:
+                # first run: learn N_b (one extra sync), size the LUT
+                self.grid.status.zero_()
+                gs = self._phase1(uf, st, None)
+                n_b = self._finish(self.stream)
+                self._alloc_lut(n_b)
+            if timed or not self.use_graph:
+                self._ensure_events()
+                self.grid.status.zero_()
+                ev = C.cast(self._ev_arr, C.POINTER(C.c_void_p)) if timed else None
+                gs = self._phase1(uf, st, ev)
+                lev = (C.cast(C.byref(self._ev_arr, C.sizeof(C.c_void_p) * (self.n_events - 3)),
+                              C.POINTER(C.c_void_p)) if timed else None)
+                self._phase2(gs, st, lev)
+                if timed:
+                    self.events[self.n_events - 1].record(self.stream)
+            else:
+                g = self._graphs.get(uf)
+                if g is None:
+                    gs = self.grid._struct()
+                    h = C.c_void_p()
+                    _lib.check(self.lib.vf_embed_graph_create(
+                        C.byref(self.c), _lib.ptr(self.mesh.faces), self.mesh.n_faces, int(uf),
+                        C.byref(gs), _lib.ptr(self.cmap), _lib.ptr(self.n_b_dev),
+                        _lib.ptr(self.lengths), self.lengths_cap, _lib.ptr(self.ws), self.ws.numel(),
+                        st, C.byref(h)), "embed_geometry (graph capture)")
+                    g = self._graphs[uf] = h.value
+                self.grid.status.zero_()
+                _lib.check(self.lib.vf_graph_launch(g, st), "embed_geometry")
+                self.grid.n_levels = self.cfg.l_max
+            n_b = self._finish(self.stream)
+            if self.host[0].item() == 0 and n_b > self.lengths_cap:  # defensive
+                self._alloc_lut(n_b)
+                return self.run(timed, use_filter)
+        cur.wait_stream(self.stream)
+        table = LinkTable(self.lengths[:n_b], self.bc_ids[:n_b], self.cmap, n_b)
+        return self.grid, table
+
+    @property
+    def n_b_host(self):
+        return self.host[4:5]
 
     def timings(self) -> EmbedTimings:
         """Stage split of the last timed run (call after synchronize)."""
@@ -243,11 +308,15 @@ class EmbedEngine:
         """Device time of the k_links launch of the last timed run."""
         return self.events[self.n_events - 3].elapsed_time(self.events[self.n_events - 2])
 
+    def cells_classified(self) -> int:
+        """Sum over levels of 64 * blocks (SURVEY.md §8d)."""
+        return 64 * self.grid.n_used
+
     # -- end-to-end path: host mesh in, host results out -------------------
     def embed_host(self, faces_coord, normals, out=None):
         """Upload host face arrays (pinned for async copies), embed, and copy
-        the results back into host buffers ``out`` (dict of pinned tensors,
-        allocated on first use).  Returns (out, h2d_bytes, d2h_bytes)."""
+        the results back into pinned host buffers ``out`` (allocated on first
+        use).  Returns (out, h2d_bytes, d2h_bytes)."""
         import torch
         lib = self.lib
         F = self.mesh.n_faces
@@ -276,10 +345,6 @@ class EmbedEngine:
         h2d = faces_coord.numel() * 8 + normals.numel() * 8
         return out, h2d, d2h
 
-    def cells_classified(self) -> int:
-        """Sum over levels of 64 * blocks (SURVEY.md §8d)."""
-        return 64 * self.grid.n_used
-
 
 def embed_geometry(grid: Optional[ForestGrid], mesh, cfg: EmbedConfig,
                    capacity: Optional[int] = None) -> Tuple[ForestGrid, LinkTable]:
@@ -288,5 +353,5 @@ def embed_geometry(grid: Optional[ForestGrid], mesh, cfg: EmbedConfig,
     init_forest (its capacity is reused) or None."""
     if grid is not None and capacity is None:
         capacity = grid.capacity
-    eng = EmbedEngine(mesh, cfg, capacity)
+    eng = EmbedEngine(mesh, cfg, capacity, use_graph=False)
     return eng.run()
