@@ -133,14 +133,20 @@ __device__ __forceinline__ void drain(LinkQueue &Q, int w, int lane, const LinkC
     __syncwarp();
 }
 
-// one direction pair r (compile-time): enumerate lattice lines along c that
-// pierce the face, push the nodes within one link of each crossing
-template <int R>
-__device__ __forceinline__ void face_direction(LinkQueue &Q, int w, const LinkCtx &c, int f,
-                                               const double *v, const float *nf, const float *V1,
-                                               const float *V2, float Ef, int lo_p[3], int hi_p[3]) {
-    constexpr int q = 2 * R + 1;
-    const int cc[3] = {c27(q, 0), c27(q, 1), c27(q, 2)};
+// representative directions q = 2r+1 (lattice.py order) in constant memory
+__constant__ int8_t c_rep[13][3] = {
+    {1, 0, 0},  {0, 1, 0},  {0, 0, 1},   {1, 1, 0},  {1, 0, 1},  {1, 0, -1}, {1, -1, 0},
+    {0, 1, 1},  {0, 1, -1}, {1, 1, 1},   {1, 1, -1}, {1, -1, 1}, {1, -1, -1}};
+
+// one direction pair r: enumerate lattice lines along c that pierce the face,
+// push the nodes within one link of each crossing.  A runtime loop over r
+// (not 13 unrolled copies): the unrolled kernel was 12k SASS instructions and
+// stalled 89% on instruction fetch.
+__device__ __noinline__ void face_direction(LinkQueue &Q, int w, const LinkCtx &c, int f, int R,
+                                            const double *v, const float *nf, const float *V1,
+                                            const float *V2, float Ef, const int *lo_p,
+                                            const int *hi_p) {
+    const int cc[3] = {c_rep[R][0], c_rep[R][1], c_rep[R][2]};
     const int p = cc[0] != 0 ? 0 : (cc[1] != 0 ? 1 : 2);
     const int q1 = p == 0 ? 1 : 0, q2 = p == 2 ? 1 : 2;
     const int s1 = cc[q1] * cc[p], s2 = cc[q2] * cc[p];  // c_q / c_p (c_p = +-1)
@@ -219,23 +225,6 @@ __device__ __forceinline__ void face_direction(LinkQueue &Q, int w, const LinkCt
     }
 }
 
-template <int R>
-struct DirLoop {
-    __device__ __forceinline__ static void run(LinkQueue &Q, int w, int lane, const LinkCtx &c, int f,
-                                               bool active, const double *v, const float *nf,
-                                               const float *V1, const float *V2, float Ef,
-                                               int *lo_p, int *hi_p) {
-        if (active) face_direction<R>(Q, w, c, f, v, nf, V1, V2, Ef, lo_p, hi_p);
-        drain(Q, w, lane, c, false);
-        DirLoop<R + 1>::run(Q, w, lane, c, f, active, v, nf, V1, V2, Ef, lo_p, hi_p);
-    }
-};
-template <>
-struct DirLoop<13> {
-    __device__ __forceinline__ static void run(LinkQueue &, int, int, const LinkCtx &, int, bool,
-                                               const double *, const float *, const float *,
-                                               const float *, float, int *, int *) {}
-};
 
 __global__ void __launch_bounds__(kLinkWarps * 32)
     k_links(LinkCtx c, double inv_dx, int widen, int64_t F, const int32_t *__restrict__ map,
@@ -274,7 +263,11 @@ __global__ void __launch_bounds__(kLinkWarps * 32)
             }
             Ef = 4e-6f * (float)(ext + 2.0 * c.dx);
         }
-        DirLoop<0>::run(Q, w, lane, c, f, active, v, nf, V1, V2, Ef, lo_p, hi_p);
+#pragma unroll 1
+        for (int r = 0; r < 13; ++r) {
+            if (active) face_direction(Q, w, c, f, r, v, nf, V1, V2, Ef, lo_p, hi_p);
+            drain(Q, w, lane, c, false);
+        }
     }
     drain(Q, w, lane, c, true);
 }
