@@ -23,20 +23,34 @@ namespace vf {
 // --------------------------------------------------------------------------
 // K-ind
 
+// row index range whose centres can lie in [A, B]: j in [ceil(A/dx - 1/2),
+// floor(B/dx - 1/2)], widened by a relative 1e-9 (>> rounding).  Rows outside
+// fail the SAT's exact box-axis comparison, so this is a superset (A6).
+__device__ __forceinline__ bool tight_rows(double A, double B, double dx, int n, int &a, int &b) {
+    const double fa = ceil(VF_DDIV(A, dx) - 0.5 - 1e-9);
+    const double fb = floor(VF_DDIV(B, dx) - 0.5 + 1e-9);
+    const double ca = fmax(fa, 0.0), cb = fmin(fb, (double)(n - 1));
+    if (ca > cb) return false;
+    a = (int)ca;
+    b = (int)cb;
+    return true;
+}
+
 __device__ bool indicator_1d(const double *v, const double *n, const LevelInfo &li) {
     if (fabs(n[0]) < li.eps_par) return false;
+    const double dx = li.dx, eps = li.eps;
+    // rows (j,k) whose centre is within eps of the face's y/z extent; most
+    // faces have none at coarse levels and never build the SAT data
+    const double ylo = fmin(fmin(v[1], v[4]), v[7]), yhi = fmax(fmax(v[1], v[4]), v[7]);
+    const double zlo = fmin(fmin(v[2], v[5]), v[8]), zhi = fmax(fmax(v[2], v[5]), v[8]);
+    int ja, jb, ka, kb;
+    if (!tight_rows(ylo - eps, yhi + eps, dx, li.cells[1], ja, jb)) return false;
+    if (!tight_rows(zlo - eps, zhi + eps, dx, li.cells[2], ka, kb)) return false;
     SatFace f;
     sat_face_init(f, v);
-    const double dx = li.dx, eps = li.eps;
-    // row range [floor(lo/dx), floor(hi/dx)] clamped; only a superset matters (A6)
-    double ja = floor(VF_DDIV(f.lo[1], dx)), jb = floor(VF_DDIV(f.hi[1], dx));
-    double ka = floor(VF_DDIV(f.lo[2], dx)), kb = floor(VF_DDIV(f.hi[2], dx));
-    ja = fmax(ja, 0.0); ka = fmax(ka, 0.0);
-    jb = fmin(jb, (double)(li.cells[1] - 1)); kb = fmin(kb, (double)(li.cells[2] - 1));
-    if (ja > jb || ka > kb) return false;
-    for (int k = (int)ka; k <= (int)kb; ++k) {
+    for (int k = ka; k <= kb; ++k) {
         const double z = node_c(k, dx);
-        for (int j = (int)ja; j <= (int)jb; ++j) {
+        for (int j = ja; j <= jb; ++j) {
             const double y = node_c(j, dx);
             if (sat_exact(f, 0.0, VF_DSUB(y, eps), VF_DSUB(z, eps), li.len[0], VF_DADD(y, eps),
                           VF_DADD(z, eps)))
@@ -85,14 +99,17 @@ __device__ bool indicator_md(const double *v, const double *n, const LevelInfo &
     return false;
 }
 
-__global__ void __launch_bounds__(256)
-    k_indicators(LevelInfo li, int mode, const double *__restrict__ faces, int64_t F,
+// min 3 CTAs/SM (<= 85 registers): the face scan is memory bound and the SAT
+// path (the only register-hungry part) runs for few faces
+template <int MODE>
+__global__ void __launch_bounds__(256, 3)
+    k_indicators(LevelInfo li, const double *__restrict__ faces, int64_t F,
                  uint8_t *__restrict__ out) {
     for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < F;
          f += (int64_t)gridDim.x * blockDim.x) {
         double v[9], n[3];
         load_face(faces, f, v, n);
-        out[f] = (uint8_t)(mode == 0 ? indicator_1d(v, n, li) : indicator_md(v, n, li));
+        out[f] = (uint8_t)(MODE == 0 ? indicator_1d(v, n, li) : indicator_md(v, n, li));
     }
 }
 
@@ -301,7 +318,10 @@ static inline int grid_for(int64_t n, int threads, int max_ctas) {
 int launch_indicators(const LevelInfo &li, int mode, const double *faces, int64_t F,
                       uint8_t *out, cudaStream_t st) {
     if (F <= 0) return VF_OK;
-    k_indicators<<<grid_for(F, 256, max_ctas(8)), 256, 0, st>>>(li, mode, faces, F, out);
+    if (mode == 0)
+        k_indicators<0><<<grid_for(F, 256, max_ctas(8)), 256, 0, st>>>(li, faces, F, out);
+    else
+        k_indicators<1><<<grid_for(F, 256, max_ctas(8)), 256, 0, st>>>(li, faces, F, out);
     return check_launch("k_indicators");
 }
 
