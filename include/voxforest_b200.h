@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define VF_ABI_VERSION 1
+#define VF_ABI_VERSION 2
 #define VF_MAX_LEVELS 16
 
 /* status codes (SURVEY.md §8b "Errors") */
@@ -68,6 +68,10 @@ typedef struct {
     double  len[3];       /* domain lengths (origin 0)                      */
     double  eps_slab;
     double  eps_parallel; /* geometry.py:25                                 */
+    /* block sharding (multi-GPU): a level-L block row (j,k) is owned by rank
+     * (j + B_L,y * k) mod shard_count; x-runs never cross ranks.  0/1 = all. */
+    int32_t shard_rank;
+    int32_t shard_count;
 } vf_config;
 
 /* ForestGrid as flat device arrays, ids grouped by level:
@@ -81,6 +85,7 @@ typedef struct {
     uint8_t *d_masks;       /* [cap*64] VF_* cell masks, t = I + 4J + 16K   */
     int32_t *d_level_start; /* [VF_MAX_LEVELS+1] device-resident            */
     int32_t *d_status;      /* [4] latched device errors (0 = ok)           */
+    uint64_t *d_solid64;    /* [cap]    bit t set: cell t is SOLID (finalize) */
     int32_t  capacity;
     int32_t  n_levels;      /* host-known number of levels present          */
 } vf_grid;
@@ -208,6 +213,12 @@ int vf_graph_launch(void *graph_exec, void *stream);
 void vf_graph_destroy(void *graph_exec);
 /* number of kernels this library has launched in the process (bench hook) */
 int64_t vf_launch_count(void);
+/* multi-GPU exchange helper: zero the level-L entries of blocks this rank
+ * does not own (block flags, solid64 and, if given, d_bcount) so that one
+ * all-reduce (MAX for flags, SUM for solid64/bcount) publishes the owners'
+ * values to every rank */
+int vf_shard_zero_unowned(const vf_config *cfg, vf_grid *grid, int level,
+                          int32_t *d_bcount, void *stream);
 /* copy the grid's latched device status to the host (synchronizes) */
 int vf_check_status(const vf_grid *grid, void *stream);
 

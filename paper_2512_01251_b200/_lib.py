@@ -14,7 +14,7 @@ from .errors import (BinCapError, CapacityError, CudaError, MeshError, Voxforest
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvoxforest_b200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAX_LEVELS = 16
 
 # cell masks / block flags / neighbour codes (voxforest_b200.h)
@@ -26,14 +26,15 @@ NB_OUTSIDE, NB_MISSING, NB_SOLID_NBR = -1, -2, -3
 class VfConfig(C.Structure):
     _fields_ = [("nb", C.c_int32 * 3), ("l_max", C.c_int32), ("n_spec", C.c_int32),
                 ("n_prop", C.c_int32), ("dx0", C.c_double), ("len", C.c_double * 3),
-                ("eps_slab", C.c_double), ("eps_parallel", C.c_double)]
+                ("eps_slab", C.c_double), ("eps_parallel", C.c_double),
+                ("shard_rank", C.c_int32), ("shard_count", C.c_int32)]
 
 
 class VfGrid(C.Structure):
     _fields_ = [("d_coords", C.c_void_p), ("d_nbr", C.c_void_p), ("d_nbr_child", C.c_void_p),
                 ("d_child", C.c_void_p), ("d_bflags", C.c_void_p), ("d_masks", C.c_void_p),
                 ("d_level_start", C.c_void_p), ("d_status", C.c_void_p),
-                ("capacity", C.c_int32), ("n_levels", C.c_int32)]
+                ("d_solid64", C.c_void_p), ("capacity", C.c_int32), ("n_levels", C.c_int32)]
 
 
 class VfBins(C.Structure):
@@ -85,6 +86,7 @@ _SIGS = {
     "vf_graph_destroy": (None, [_P]),
     "vf_launch_count": (_I64, []),
     "vf_check_status": (_I32, [_GP, _P]),
+    "vf_shard_zero_unowned": (_I32, [_CP, _GP, _I32, _P, _P]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -150,8 +152,11 @@ def ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
 
-def make_config(cfg) -> VfConfig:
+def make_config(cfg, shard=(0, 1)) -> VfConfig:
+    """vf_config from an EmbedConfig; ``shard`` = (rank, n_ranks) for the
+    block-sharded multi-GPU embed (row ownership, see include/voxforest_b200.h)."""
     c = VfConfig()
+    c.shard_rank, c.shard_count = int(shard[0]), int(shard[1])
     c.nb[:] = list(cfg.nb)
     c.l_max = cfg.l_max
     c.n_spec = cfg.n_spec

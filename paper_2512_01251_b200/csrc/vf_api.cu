@@ -57,6 +57,8 @@ LevelInfo make_level(const vf_config &cfg, int L) {
         li.cells[d] = 4 * li.bins[d];
     }
     li.level = L;
+    li.shard_rank = cfg.shard_count > 1 ? cfg.shard_rank : 0;
+    li.shard_count = cfg.shard_count > 1 ? cfg.shard_count : 1;
     return li;
 }
 
@@ -102,6 +104,7 @@ static bool valid_cfg(const vf_config *c) {
     if (!c) return false;
     for (int d = 0; d < 3; ++d)
         if (c->nb[d] <= 0 || !(c->len[d] > 0)) return false;
+    if (c->shard_count > 1 && (c->shard_rank < 0 || c->shard_rank >= c->shard_count)) return false;
     return c->l_max >= 1 && c->l_max < VF_MAX_LEVELS && c->n_spec >= 1 && c->n_prop >= 0 &&
            c->dx0 > 0 && c->eps_slab >= 0;
 }
@@ -306,7 +309,7 @@ int vf_mark_level(const vf_config *cfg, vf_grid *grid, int level, void *ws, size
 
 int vf_boundary_cells(const vf_config *cfg, vf_grid *grid, int32_t *bcount, void *stream) {
     if (!valid_cfg(cfg) || !grid || !bcount) return set_error(VF_EARG, "vf_boundary_cells: bad argument");
-    return boundary_impl(grid, bcount, (cudaStream_t)stream);
+    return boundary_impl(*cfg, grid, bcount, (cudaStream_t)stream);
 }
 
 size_t vf_tables_workspace_size(const vf_grid *g) { return g ? tables_workspace_size(g->capacity) : 0; }
@@ -375,7 +378,7 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
         VF_TRY(adapt_impl(*cfg, g, L, w.adapt_ws, w.adapt_b, st));
         rec(events, n_ev, &k, st);  // refinement done
     }
-    VF_TRY(boundary_impl(g, w.bcount, st));
+    VF_TRY(boundary_impl(*cfg, g, w.bcount, st));
     VF_TRY(tables_impl(g, w.bcount, cmap, d_n_b, w.tab_ws, w.tab_b, st));
     rec(events, n_ev, &k, st);  // boundary + tables done
     return VF_OK;
@@ -433,6 +436,13 @@ int vf_graph_launch(void *graph_exec, void *stream) {
 
 void vf_graph_destroy(void *graph_exec) {
     if (graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)graph_exec);
+}
+
+int vf_shard_zero_unowned(const vf_config *cfg, vf_grid *grid, int level, int32_t *d_bcount,
+                          void *stream) {
+    if (!valid_cfg(cfg) || !grid || level < 0 || level >= grid->n_levels)
+        return set_error(VF_EARG, "vf_shard_zero_unowned: bad argument");
+    return shard_zero_impl(make_level(*cfg, level), grid, level, d_bcount, (cudaStream_t)stream);
 }
 
 int vf_check_status(const vf_grid *g, void *stream) {

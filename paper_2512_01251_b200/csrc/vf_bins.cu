@@ -36,28 +36,92 @@ __device__ __forceinline__ bool tight_rows(double A, double B, double dx, int n,
     return true;
 }
 
-__device__ bool indicator_1d(const double *v, const double *n, const LevelInfo &li) {
-    if (fabs(n[0]) < li.eps_par) return false;
-    const double dx = li.dx, eps = li.eps;
-    // rows (j,k) whose centre is within eps of the face's y/z extent; most
-    // faces have none at coarse levels and never build the SAT data
+// candidate x-rows of a face: centres within eps of its y/z extent.
+// inv_dx is exact for power-of-two dx (else the range is widened by a row).
+__device__ __forceinline__ bool face_rows(const double *v, const LevelInfo &li, double inv_dx,
+                                          int widen, int &ja, int &jb, int &ka, int &kb) {
+    const double eps = li.eps;
     const double ylo = fmin(fmin(v[1], v[4]), v[7]), yhi = fmax(fmax(v[1], v[4]), v[7]);
     const double zlo = fmin(fmin(v[2], v[5]), v[8]), zhi = fmax(fmax(v[2], v[5]), v[8]);
+    // j in [ceil((lo-eps)/dx - 1/2), floor((hi+eps)/dx - 1/2)] (+- 1e-9 relative)
+    const double fja = ceil((ylo - eps) * inv_dx - 0.5 - 1e-9) - widen;
+    const double fjb = floor((yhi + eps) * inv_dx - 0.5 + 1e-9) + widen;
+    const double fka = ceil((zlo - eps) * inv_dx - 0.5 - 1e-9) - widen;
+    const double fkb = floor((zhi + eps) * inv_dx - 0.5 + 1e-9) + widen;
+    const double cja = fmax(fja, 0.0), cjb = fmin(fjb, (double)(li.cells[1] - 1));
+    const double cka = fmax(fka, 0.0), ckb = fmin(fkb, (double)(li.cells[2] - 1));
+    if (cja > cjb || cka > ckb) return false;
+    ja = (int)cja; jb = (int)cjb; ka = (int)cka; kb = (int)ckb;
+    if (li.shard_count <= 1) return true;
+    for (int k = ka; k <= kb; ++k)  // multi-GPU: does any candidate row belong to us?
+        for (int j = ja; j <= jb; ++j)
+            if (owns_row(li, j >> 2, k >> 2)) return true;
+    return false;
+}
+
+// exact row tests of one face (rare path, run warp-converged from the queue)
+__device__ __noinline__ bool indicator_rows(const double *__restrict__ faces, int64_t f,
+                                            const LevelInfo &li, double inv_dx, int widen) {
+    double v[9], n[3];
+    load_face(faces, f, v, n);
     int ja, jb, ka, kb;
-    if (!tight_rows(ylo - eps, yhi + eps, dx, li.cells[1], ja, jb)) return false;
-    if (!tight_rows(zlo - eps, zhi + eps, dx, li.cells[2], ka, kb)) return false;
-    SatFace f;
-    sat_face_init(f, v);
+    if (!face_rows(v, li, inv_dx, widen, ja, jb, ka, kb)) return false;
+    const double dx = li.dx, eps = li.eps;
+    SatFace sf;
+    sat_face_init(sf, v);
     for (int k = ka; k <= kb; ++k) {
         const double z = node_c(k, dx);
         for (int j = ja; j <= jb; ++j) {
+            if (!owns_row(li, j >> 2, k >> 2)) continue;  // multi-GPU: rows of other ranks
             const double y = node_c(j, dx);
-            if (sat_exact(f, 0.0, VF_DSUB(y, eps), VF_DSUB(z, eps), li.len[0], VF_DADD(y, eps),
+            if (sat_exact(sf, 0.0, VF_DSUB(y, eps), VF_DSUB(z, eps), li.len[0], VF_DADD(y, eps),
                           VF_DADD(z, eps)))
                 return true;
         }
     }
     return false;
+}
+
+// 1D indicators (Alg. 1 axis-only, pin A6): a streaming pass over all faces
+// computes the candidate row ranges (most faces have none at coarse levels);
+// faces with rows enter a per-warp queue that is drained 32 at a time through
+// the exact SAT, so the FP64 path runs warp-converged.
+constexpr int kIndWarps = 8;
+
+__global__ void __launch_bounds__(kIndWarps * 32, 3)
+    k_indicators_1d(LevelInfo li, double inv_dx, int widen, const double *__restrict__ faces,
+                    int64_t F, uint8_t *__restrict__ out) {
+    __shared__ int64_t s_q[kIndWarps][64];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t first = ((int64_t)blockIdx.x * kIndWarps + w) * 32;
+    const int64_t stride = (int64_t)gridDim.x * kIndWarps * 32;
+    int qn = 0;
+    for (int64_t base = first; base < F; base += stride) {
+        const int64_t f = base + lane;
+        bool has = false;
+        if (f < F) {
+            double v[9], n[3];
+            load_face(faces, f, v, n);
+            int ja, jb, ka, kb;
+            has = !(fabs(n[0]) < li.eps_par) && face_rows(v, li, inv_dx, widen, ja, jb, ka, kb);
+            if (!has) out[f] = 0;
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, has);
+        if (has) s_q[w][qn + __popc(m & ((1u << lane) - 1u))] = f;
+        qn += __popc(m);
+        __syncwarp();
+        if (qn >= 32) {
+            const int64_t g = s_q[w][qn - 32 + lane];
+            __syncwarp();
+            out[g] = (uint8_t)indicator_rows(faces, g, li, inv_dx, widen);
+            qn -= 32;
+        }
+        __syncwarp();
+    }
+    if (lane < qn) {
+        const int64_t g = s_q[w][lane];
+        out[g] = (uint8_t)indicator_rows(faces, g, li, inv_dx, widen);
+    }
 }
 
 __device__ bool indicator_md(const double *v, const double *n, const LevelInfo &li) {
@@ -109,7 +173,7 @@ __global__ void __launch_bounds__(256, 3)
          f += (int64_t)gridDim.x * blockDim.x) {
         double v[9], n[3];
         load_face(faces, f, v, n);
-        out[f] = (uint8_t)(MODE == 0 ? indicator_1d(v, n, li) : indicator_md(v, n, li));
+        out[f] = (uint8_t)indicator_md(v, n, li);
     }
 }
 
@@ -140,6 +204,7 @@ __device__ int face_pairs(const double *v, const LevelInfo &li, int nlim, int32_
     for (int bk = a[2]; bk <= b[2]; ++bk) {
         const double mz = VF_DSUB(VF_DMUL((double)bk, h), dx), Mz = VF_DADD(VF_DMUL((double)(bk + 1), h), dx);
         for (int bj = a[1]; bj <= b[1]; ++bj) {
+            if (!owns_row(li, bj, bk)) continue;  // multi-GPU: bins of other ranks
             const double my = VF_DSUB(VF_DMUL((double)bj, h), dx), My = VF_DADD(VF_DMUL((double)(bj + 1), h), dx);
             for (int bi = a[0]; bi <= b[0]; ++bi) {
                 const double mx = VF_DSUB(VF_DMUL((double)bi, h), dx), Mx = VF_DADD(VF_DMUL((double)(bi + 1), h), dx);
@@ -318,10 +383,14 @@ static inline int grid_for(int64_t n, int threads, int max_ctas) {
 int launch_indicators(const LevelInfo &li, int mode, const double *faces, int64_t F,
                       uint8_t *out, cudaStream_t st) {
     if (F <= 0) return VF_OK;
-    if (mode == 0)
-        k_indicators<0><<<grid_for(F, 256, max_ctas(8)), 256, 0, st>>>(li, faces, F, out);
-    else
+    if (mode == 0) {
+        int ex = 0;
+        const int widen = (frexp(li.dx, &ex) == 0.5) ? 0 : 1;  // 1/dx exact for 2^-k
+        k_indicators_1d<<<grid_for((F + 31) / 32, kIndWarps, max_ctas(6)), kIndWarps * 32, 0, st>>>(
+            li, 1.0 / li.dx, widen, faces, F, out);
+    } else {
         k_indicators<1><<<grid_for(F, 256, max_ctas(8)), 256, 0, st>>>(li, faces, F, out);
+    }
     return check_launch("k_indicators");
 }
 

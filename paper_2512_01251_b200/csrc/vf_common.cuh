@@ -51,7 +51,18 @@ struct LevelInfo {
     int cells[3];    // cells per axis at L
     int bins[3];     // bins (= blocks) per axis at L
     int level;
+    int shard_rank;  // block-row ownership (multi-GPU), see owner_of
+    int shard_count;
 };
+
+// owner rank of the level-L block row (j,k); interleaved so neighbouring
+// rows land on different ranks (balance) while x-runs stay rank-local
+__host__ __device__ __forceinline__ int row_owner(int j, int k, int by, int nranks) {
+    return nranks <= 1 ? 0 : (int)(((int64_t)j + (int64_t)by * k) % nranks);
+}
+__host__ __device__ __forceinline__ bool owns_row(const LevelInfo &li, int j, int k) {
+    return li.shard_count <= 1 || row_owner(j, k, li.bins[1], li.shard_count) == li.shard_rank;
+}
 
 // A2: lattice node / cell centre, one rounding
 __device__ __forceinline__ double node_c(int gi, double dx) {

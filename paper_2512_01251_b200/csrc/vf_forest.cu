@@ -19,7 +19,7 @@ __global__ void k_init_forest(int nx, int ny, int nz, int32_t *__restrict__ coor
                               int32_t *__restrict__ nbr, int32_t *__restrict__ nbr_child,
                               int32_t *__restrict__ child, uint8_t *__restrict__ bflags,
                               uint8_t *__restrict__ masks, int32_t *__restrict__ level_start,
-                              int32_t *__restrict__ status) {
+                              int32_t *__restrict__ status, uint64_t *__restrict__ solid64) {
     const int64_t n = (int64_t)nx * ny * nz;
     for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n;
          b += (int64_t)gridDim.x * blockDim.x) {
@@ -35,6 +35,7 @@ __global__ void k_init_forest(int nx, int ny, int nz, int32_t *__restrict__ coor
         }
         child[b] = -1;
         bflags[b] = 0;
+        solid64[b] = 0;
         uint4 *m = reinterpret_cast<uint4 *>(masks + 64 * b);
         m[0] = m[1] = m[2] = m[3] = make_uint4(0, 0, 0, 0);  // VF_FLUID
     }
@@ -51,7 +52,7 @@ int init_forest_impl(const vf_config &cfg, vf_grid *g, cudaStream_t st) {
     if (grid > max_ctas(8)) grid = max_ctas(8);
     k_init_forest<<<grid, 256, 0, st>>>(cfg.nb[0], cfg.nb[1], cfg.nb[2], g->d_coords, g->d_nbr,
                                         g->d_nbr_child, g->d_child, g->d_bflags, g->d_masks,
-                                        g->d_level_start, g->d_status);
+                                        g->d_level_start, g->d_status, g->d_solid64);
     g->n_levels = 1;
     return check_launch("k_init_forest");
 }
@@ -243,7 +244,8 @@ __global__ void __launch_bounds__(256)
                      const int32_t *__restrict__ parents, int32_t *__restrict__ coords,
                      int32_t *__restrict__ nbr, int32_t *__restrict__ nbr_child,
                      int32_t *__restrict__ child, uint8_t *__restrict__ bflags,
-                     uint8_t *__restrict__ masks, int32_t *__restrict__ status) {
+                     uint8_t *__restrict__ masks, int32_t *__restrict__ status,
+                     uint64_t *__restrict__ solid64) {
     const int64_t e = level_start[L + 1];
     const int64_t nc = 8 * (int64_t)(*n_marked);
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc;
@@ -281,6 +283,7 @@ __global__ void __launch_bounds__(256)
         }
         child[id] = -1;
         bflags[id] = 0;
+        solid64[id] = 0;
         // A14 ghost layer: a cell is within Chebyshev distance 2 (fine cells) of
         // a missing neighbour block iff one of the 7 blocks towards its octant
         // is missing, so 8 octant bits decide all 64 cells.
@@ -364,7 +367,7 @@ int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_byte
     k_adapt_children<<<max_ctas(8), 256, 0, st>>>(
         L, g->capacity, cfg.nb[0] << (L + 1), cfg.nb[1] << (L + 1), cfg.nb[2] << (L + 1),
         g->d_level_start, scalars + 1, parents, g->d_coords, g->d_nbr, g->d_nbr_child, g->d_child,
-        g->d_bflags, g->d_masks, g->d_status);
+        g->d_bflags, g->d_masks, g->d_status, g->d_solid64);
     if ((rc = check_launch("k_adapt_children"))) return rc;
     k_adapt_level<<<max_ctas(8), 256, 0, st>>>(L, g->d_level_start, g->d_nbr, g->d_nbr_child,
                                                g->d_child, g->d_masks);

@@ -57,6 +57,7 @@ size_t propagate_workspace_size(int32_t capacity);
 int propagate_impl(const LevelInfo &li, vf_grid *g, int L, int dir, int finalize, void *ws,
                    size_t ws_bytes, cudaStream_t st);
 int finalize_impl(vf_grid *g, int L, cudaStream_t st);
+int shard_zero_impl(const LevelInfo &li, vf_grid *g, int L, int32_t *bcount, cudaStream_t st);
 
 // forest
 int init_forest_impl(const vf_config &cfg, vf_grid *g, cudaStream_t st);
@@ -68,7 +69,7 @@ int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_byte
                cudaStream_t st);
 
 // boundary / tables / links
-int boundary_impl(vf_grid *g, int32_t *bcount, cudaStream_t st);
+int boundary_impl(const vf_config &cfg, vf_grid *g, int32_t *bcount, cudaStream_t st);
 size_t tables_workspace_size(int32_t capacity);
 int tables_impl(vf_grid *g, const int32_t *bcount, int32_t *cmap, int32_t *d_n_b, void *ws,
                 size_t ws_bytes, cudaStream_t st);

@@ -35,7 +35,9 @@ namespace vf {
 
 // dense finest-level block -> LUT slot map; nothing is mapped when the
 // device-resident N_b exceeds the LUT capacity (error latched by k_fill_lut)
-__global__ void k_blockmap(int L, int bx, int by, const int32_t *__restrict__ level_start,
+// (multi-GPU: only this rank's blocks are mapped, so every rank fills the
+// LUT slots of the blocks it owns)
+__global__ void k_blockmap(LevelInfo li, int L, const int32_t *__restrict__ level_start,
                            const int32_t *__restrict__ coords, const int32_t *__restrict__ cmap,
                            int32_t *__restrict__ bmap, const int32_t *__restrict__ d_n_b,
                            int64_t cap) {
@@ -46,7 +48,8 @@ __global__ void k_blockmap(int L, int bx, int by, const int32_t *__restrict__ le
         const int32_t slot = cmap[b];
         if (slot < 0) continue;
         const int4 c = reinterpret_cast<const int4 *>(coords)[b];
-        bmap[c.x + (int64_t)bx * (c.y + (int64_t)by * c.z)] = slot;
+        if (!owns_row(li, c.y, c.z)) continue;
+        bmap[c.x + (int64_t)li.bins[0] * (c.y + (int64_t)li.bins[1] * c.z)] = slot;
     }
 }
 
@@ -314,8 +317,8 @@ int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const doubl
     const int64_t nb = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
     int32_t *bmap = (int32_t *)ws;
     cudaMemsetAsync(bmap, 0xff, sizeof(int32_t) * (size_t)nb, st);
-    k_blockmap<<<max_ctas(8), 256, 0, st>>>(L, li.bins[0], li.bins[1], g->d_level_start, g->d_coords,
-                                            cmap, bmap, d_n_b, lengths_cap);
+    k_blockmap<<<max_ctas(8), 256, 0, st>>>(li, L, g->d_level_start, g->d_coords, cmap, bmap, d_n_b,
+                                            lengths_cap);
     int rc = check_launch("k_blockmap");
     if (rc) return rc;
     LinkCtx c;

@@ -26,36 +26,41 @@ constexpr int kBndWarps = 8;
 // offsets).  Reads of concurrently re-marked cells see FLUID or BOUNDARY,
 // both "not SOLID", so the fused single pass equals PAPER.md:941's two passes.
 __global__ void __launch_bounds__(kBndWarps * 32)
-    k_boundary(int L, const int32_t *__restrict__ level_start, const int32_t *__restrict__ nbr,
+    k_boundary(LevelInfo li, int L, const int32_t *__restrict__ level_start,
+               const int32_t *__restrict__ nbr, const int32_t *__restrict__ coords,
                uint8_t *__restrict__ bflags, uint8_t *__restrict__ masks,
-               int32_t *__restrict__ bcount) {
+               const uint64_t *__restrict__ solid64, int32_t *__restrict__ bcount) {
     __shared__ uint8_t s_halo[kBndWarps][216];
-    __shared__ int32_t s_nb[kBndWarps][27];
+    __shared__ uint64_t s_sol[kBndWarps][27];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t gw = (int64_t)blockIdx.x * kBndWarps + w, nw = (int64_t)gridDim.x * kBndWarps;
     const int32_t s = level_start[L], e = level_start[L + 1];
     for (int64_t b = s + gw; b < e; b += nw) {
+        if (li.shard_count > 1) {  // multi-GPU: blocks of other ranks are theirs
+            const int4 c = reinterpret_cast<const int4 *>(coords)[b];
+            if (!owns_row(li, c.y, c.z)) continue;
+        }
         int32_t myn = -1;
         if (lane < 27) myn = (lane == 0) ? (int32_t)b : nbr[27 * b + lane];
-        const bool sol = (lane < 27 && myn >= 0) ? (bflags[myn] & VF_BF_SOLID) != 0 : false;
-        if (!__any_sync(0xffffffffu, sol)) {  // not a candidate (A18): no boundary cell
+        // solid64 (exchanged between ranks) rather than the masks of
+        // neighbours, which may belong to another rank
+        const uint64_t sm = (lane < 27 && myn >= 0) ? solid64[myn] : 0ull;
+        if (!__any_sync(0xffffffffu, sm != 0)) {  // not a candidate (A18): no boundary cell
             if (lane == 0) {
                 bcount[b] = 0;
                 bflags[b] = (uint8_t)(bflags[b] & ~VF_BF_BOUNDARY);
             }
             continue;
         }
-        if (lane < 27) s_nb[w][lane] = myn;
+        if (lane < 27) s_sol[w][lane] = sm;
         __syncwarp();
         for (int h = lane; h < 216; h += 32) {
             const int hx = h % 6 - 1, hy = (h / 6) % 6 - 1, hz = h / 36 - 1;
             const int ox = hx < 0 ? -1 : (hx > 3 ? 1 : 0);
             const int oy = hy < 0 ? -1 : (hy > 3 ? 1 : 0);
             const int oz = hz < 0 ? -1 : (hz > 3 ? 1 : 0);
-            const int32_t nbk = s_nb[w][slot_of(ox, oy, oz)];
-            s_halo[w][h] = (nbk >= 0) ? (uint8_t)(masks[64 * (int64_t)nbk + (hx & 3) + 4 * (hy & 3) +
-                                                       16 * (hz & 3)] == VF_SOLID)
-                                      : (uint8_t)0;
+            const uint64_t nsm = s_sol[w][slot_of(ox, oy, oz)];
+            s_halo[w][h] = (uint8_t)((nsm >> ((hx & 3) + 4 * (hy & 3) + 16 * (hz & 3))) & 1ull);
         }
         __syncwarp();
         int cnt = 0;
@@ -88,11 +93,12 @@ __global__ void __launch_bounds__(kBndWarps * 32)
     }
 }
 
-int boundary_impl(vf_grid *g, int32_t *bcount, cudaStream_t st) {
+int boundary_impl(const vf_config &cfg, vf_grid *g, int32_t *bcount, cudaStream_t st) {
     const int L = g->n_levels - 1;
     cudaMemsetAsync(bcount, 0, sizeof(int32_t) * (size_t)g->capacity, st);
-    k_boundary<<<max_ctas(8), kBndWarps * 32, 0, st>>>(L, g->d_level_start, g->d_nbr, g->d_bflags,
-                                                       g->d_masks, bcount);
+    k_boundary<<<max_ctas(8), kBndWarps * 32, 0, st>>>(make_level(cfg, L), L, g->d_level_start,
+                                                       g->d_nbr, g->d_coords, g->d_bflags,
+                                                       g->d_masks, g->d_solid64, bcount);
     return check_launch("k_boundary");
 }
 

@@ -49,12 +49,29 @@ __global__ void __launch_bounds__(kVoxWarps * 32)
     const double dx = li.dx, eps = li.eps, lx = li.len[0];
     uint32_t *masks32 = reinterpret_cast<uint32_t *>(masks);
 
-    for (int64_t b = s + gw; b < e; b += nw) {
-        const int4 co = *reinterpret_cast<const int4 *>(coords + 4 * b);
-        const int64_t bin = co.x + (int64_t)li.bins[0] * (co.y + (int64_t)li.bins[1] * co.z);
-        const int n_f = counts[bin];
-        if (n_f == 0) continue;  // warp-uniform
-        const int32_t off = offsets[bin];
+    // tiles of 32 blocks: each lane fetches one block's bin header, so the
+    // dependent coords -> counts loads of 32 blocks overlap; only blocks with
+    // a non-empty bin are then processed, one at a time by the whole warp
+    for (int64_t b0 = s + gw * 32; b0 < e; b0 += nw * 32) {
+      int4 co_l = make_int4(0, 0, 0, 0);
+      int nf_l = 0, off_l = 0;
+      if (b0 + lane < e) {
+          co_l = *reinterpret_cast<const int4 *>(coords + 4 * (b0 + lane));
+          const int64_t bin_l = co_l.x + (int64_t)li.bins[0] * (co_l.y + (int64_t)li.bins[1] * co_l.z);
+          nf_l = counts[bin_l];
+          if (nf_l) off_l = offsets[bin_l];
+      }
+      uint32_t todo = __ballot_sync(0xffffffffu, nf_l > 0);
+      while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int64_t b = b0 + src;
+        int4 co;
+        co.x = __shfl_sync(0xffffffffu, co_l.x, src);
+        co.y = __shfl_sync(0xffffffffu, co_l.y, src);
+        co.z = __shfl_sync(0xffffffffu, co_l.z, src);
+        const int n_f = __shfl_sync(0xffffffffu, nf_l, src);
+        const int32_t off = __shfl_sync(0xffffffffu, off_l, src);
         const double y = node_c(4 * co.y + J, dx), z = node_c(4 * co.z + K, dx);
         const double my = VF_DSUB(y, eps), My = VF_DADD(y, eps);
         const double mz = VF_DSUB(z, eps), Mz = VF_DADD(z, eps);
@@ -111,19 +128,22 @@ __global__ void __launch_bounds__(kVoxWarps * 32)
             if (bd[I] < INFINITY) hit |= 1u << I;
         }
         const bool any = __any_sync(0xffffffffu, hit != 0);
-        if (!any || half) continue;  // eta == 0 -> no write (Alg. 3 l.648)
-        uint32_t *w = masks32 + b * 16 + r;
-        const uint32_t orig = *w;
-        uint32_t out = orig;
+        if (any && !half) {  // eta == 0 -> no write (Alg. 3 l.648)
+            uint32_t *w = masks32 + b * 16 + r;
+            const uint32_t orig = *w;
+            uint32_t out = orig;
 #pragma unroll
-        for (int I = 0; I < 4; ++I) {
-            if (!(hit >> I & 1)) continue;
-            const uint32_t o = (orig >> (8 * I)) & 0xffu, hn = (bh >> (8 * I)) & 0xffu;
-            // A9 write rule
-            if (hn == VF_SOLID || (o != VF_GHOST && o != VF_INTERFACE))
-                out = (out & ~(0xffu << (8 * I))) | (hn << (8 * I));
+            for (int I = 0; I < 4; ++I) {
+                if (!(hit >> I & 1)) continue;
+                const uint32_t o = (orig >> (8 * I)) & 0xffu, hn = (bh >> (8 * I)) & 0xffu;
+                // A9 write rule
+                if (hn == VF_SOLID || (o != VF_GHOST && o != VF_INTERFACE))
+                    out = (out & ~(0xffu << (8 * I))) | (hn << (8 * I));
+            }
+            if (out != orig) *w = out;
         }
-        if (out != orig) *w = out;
+        __syncwarp();
+      }
     }
 }
 
@@ -210,10 +230,34 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// finalize (pin A11): GUARD -> FLUID, block solid flag, and the
+// block's 64-bit SOLID-cell mask (bit t = cell t) used by the boundary halo
+// and exchanged between ranks at the finest level
+__device__ __forceinline__ void finalize_block(uint32_t w[16], bool &changed, uint8_t *bflags,
+                                               uint64_t *solid64, int64_t b) {
+    uint64_t sm = 0;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        uint32_t x = w[r];
+#pragma unroll
+        for (int I = 0; I < 4; ++I) {
+            const uint32_t h = (x >> (8 * I)) & 0xffu;
+            if (h == VF_GUARD) x &= ~(0xffu << (8 * I));  // -> FLUID (0)
+            sm |= (uint64_t)(h == VF_SOLID) << (4 * r + I);
+        }
+        changed |= (x != w[r]);
+        w[r] = x;
+    }
+    const uint8_t f0 = bflags[b];
+    bflags[b] = (uint8_t)((f0 & ~VF_BF_SOLID) | (sm ? VF_BF_SOLID : 0));
+    solid64[b] = sm;
+}
+
 __global__ void __launch_bounds__(256)
     k_xapply(int L, int back, int finalize, const int32_t *__restrict__ level_start,
              const int32_t *__restrict__ nbr, uint8_t *__restrict__ masks,
-             const uint32_t *__restrict__ G, uint8_t *__restrict__ bflags) {
+             const uint32_t *__restrict__ G, uint8_t *__restrict__ bflags,
+             uint64_t *__restrict__ solid64) {
     const int32_t s = level_start[L], e = level_start[L + 1];
     for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
          b += (int64_t)gridDim.x * blockDim.x) {
@@ -238,52 +282,44 @@ __global__ void __launch_bounds__(256)
                 w[r] = x;
             }
         }
-        if (finalize) {
-            bool solid = false;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                uint32_t x = w[r];
-#pragma unroll
-                for (int I = 0; I < 4; ++I) {
-                    const uint32_t h = (x >> (8 * I)) & 0xffu;
-                    if (h == VF_GUARD) x &= ~(0xffu << (8 * I));  // -> FLUID (0)
-                    solid |= (h == VF_SOLID);
-                }
-                changed |= (x != w[r]);
-                w[r] = x;
-            }
-            const uint8_t f0 = bflags[b];
-            bflags[b] = (uint8_t)((f0 & ~VF_BF_SOLID) | (solid ? VF_BF_SOLID : 0));
-        }
+        if (finalize) finalize_block(w, changed, bflags, solid64, b);
         if (changed) store_masks64(masks, b, w);
     }
 }
 
 __global__ void __launch_bounds__(256)
     k_finalize(int L, const int32_t *__restrict__ level_start, uint8_t *__restrict__ masks,
-               uint8_t *__restrict__ bflags) {
+               uint8_t *__restrict__ bflags, uint64_t *__restrict__ solid64) {
     const int32_t s = level_start[L], e = level_start[L + 1];
     for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
          b += (int64_t)gridDim.x * blockDim.x) {
         uint32_t w[16];
         load_masks64(masks, b, w);
-        bool solid = false, changed = false;
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            uint32_t x = w[r];
-#pragma unroll
-            for (int I = 0; I < 4; ++I) {
-                const uint32_t h = (x >> (8 * I)) & 0xffu;
-                if (h == VF_GUARD) x &= ~(0xffu << (8 * I));
-                solid |= (h == VF_SOLID);
-            }
-            changed |= (x != w[r]);
-            w[r] = x;
-        }
+        bool changed = false;
+        finalize_block(w, changed, bflags, solid64, b);
         if (changed) store_masks64(masks, b, w);
-        const uint8_t f0 = bflags[b];
-        bflags[b] = (uint8_t)((f0 & ~VF_BF_SOLID) | (solid ? VF_BF_SOLID : 0));
     }
+}
+
+// multi-GPU exchange: zero what this rank does not own on level L
+__global__ void k_shard_zero(LevelInfo li, int L, const int32_t *__restrict__ level_start,
+                             const int32_t *__restrict__ coords, uint8_t *__restrict__ bflags,
+                             uint64_t *__restrict__ solid64, int32_t *__restrict__ bcount) {
+    const int32_t s = level_start[L], e = level_start[L + 1];
+    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int4 c = reinterpret_cast<const int4 *>(coords)[b];
+        if (owns_row(li, c.y, c.z)) continue;
+        bflags[b] = 0;
+        solid64[b] = 0;
+        if (bcount) bcount[b] = 0;
+    }
+}
+
+int shard_zero_impl(const LevelInfo &li, vf_grid *g, int L, int32_t *bcount, cudaStream_t st) {
+    k_shard_zero<<<max_ctas(8), 256, 0, st>>>(li, L, g->d_level_start, g->d_coords, g->d_bflags,
+                                              g->d_solid64, bcount);
+    return check_launch("k_shard_zero");
 }
 
 size_t propagate_workspace_size(int32_t capacity) {
@@ -312,12 +348,13 @@ int propagate_impl(const LevelInfo &li, vf_grid *g, int L, int dir, int finalize
         cur ^= 1;
     }
     k_xapply<<<grid, 256, 0, st>>>(L, back, finalize, g->d_level_start, g->d_nbr, g->d_masks,
-                                   G[cur], g->d_bflags);
+                                   G[cur], g->d_bflags, g->d_solid64);
     return check_launch("k_xapply");
 }
 
 int finalize_impl(vf_grid *g, int L, cudaStream_t st) {
-    k_finalize<<<max_ctas(8), 256, 0, st>>>(L, g->d_level_start, g->d_masks, g->d_bflags);
+    k_finalize<<<max_ctas(8), 256, 0, st>>>(L, g->d_level_start, g->d_masks, g->d_bflags,
+                                            g->d_solid64);
     return check_launch("k_finalize");
 }
 

@@ -126,6 +126,7 @@ class ForestGrid:
     masks: object           # (cap, 64) uint8 cell masks
     level_start: object     # (17,) int32 device-resident
     status: object          # (4,) int32 latched device errors
+    solid64: object = None  # (cap,) int64: bit t = cell t SOLID (set by finalize)
     n_levels: int = 0
 
     @classmethod
@@ -141,7 +142,8 @@ class ForestGrid:
                    torch.zeros((cap,), dtype=torch.uint8, device=dev),
                    torch.empty((cap, 64), dtype=torch.uint8, device=dev),
                    torch.zeros((MAX_LEVELS + 1,), dtype=torch.int32, device=dev),
-                   torch.zeros((4,), dtype=torch.int32, device=dev), 0)
+                   torch.zeros((4,), dtype=torch.int32, device=dev),
+                   torch.zeros((cap,), dtype=torch.int64, device=dev), 0)
 
     @property
     def capacity(self) -> int:
@@ -157,6 +159,7 @@ class ForestGrid:
         g.d_masks = self.masks.data_ptr()
         g.d_level_start = self.level_start.data_ptr()
         g.d_status = self.status.data_ptr()
+        g.d_solid64 = self.solid64.data_ptr()
         g.capacity = self.capacity
         g.n_levels = self.n_levels
         return g
@@ -201,6 +204,10 @@ class ForestGrid:
         fg.masks[:n] = torch.from_numpy(np.ascontiguousarray(g["masks"][:n])).cuda()
         fg.level_start.copy_(torch.from_numpy(np.ascontiguousarray(g["level_start"], dtype=np.int32)))
         fg.n_levels = int(g["n_levels"])
+        # per-block SOLID bitmask (bit t = cell t), as finalize would write it
+        bits = (np.asarray(g["masks"][:n]) == 1).astype(np.uint64)
+        sm = (bits << np.arange(64, dtype=np.uint64)[None, :]).sum(axis=1, dtype=np.uint64)
+        fg.solid64[:n] = torch.from_numpy(sm.view(np.int64)).cuda()
         return fg
 
 
