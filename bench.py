@@ -189,6 +189,25 @@ def run_reference(args, w, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+def timed_steps(run, steps, flush, ws):
+    """Barrier + sync, then `steps` runs each bracketed by CUDA events on the
+    current stream (the L2 flush between steps stays outside the events);
+    returns the per-step device times (ms) of this rank."""
+    import torch
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    barrier(ws)
+    torch.cuda.synchronize()
+    for k in range(steps):
+        flush.fill_(float(k))
+        starts[k].record()
+        run()
+        ends[k].record()
+    torch.cuda.synchronize()
+    barrier(ws)
+    return [a.elapsed_time(b) for a, b in zip(starts, ends)]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -196,6 +215,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--mode", default="shard", choices=["shard", "objects"],
+                    help="N>1: block-shard ONE mesh (strong scaling, NCCL flag exchange) or "
+                         "embed independent translated copies (weak scaling, no collective)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -212,88 +234,109 @@ def main():
     from paper_2512_01251_b200.voxelizer import EmbedEngine
     lib = _lib.require_cuda()
     dev = torch.cuda.current_device()
-    mesh = make_mesh(w, rank)
+    sharded = ws > 1 and args.mode == "shard"
+    mesh = make_mesh(w, 0 if sharded else rank)
     cfg = make_cfg(w)
-    eng = EmbedEngine(mesh, cfg)
+    if sharded:
+        from paper_2512_01251_b200.parallel import ShardedEmbed
+        eng = ShardedEmbed(mesh, cfg)
+        run = eng.run
+    else:
+        eng = EmbedEngine(mesh, cfg)
+        run = eng.run  # one CUDA-graph launch + one host sync (status, N_b)
     for _ in range(args.warmup):
-        eng.run()
+        run()
     torch.cuda.synchronize()
-    # L2 flush buffer (> 126 MB L2), rewritten between timed steps; per-step
-    # CUDA events exclude the flush from the step time.
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    launches0 = lib.vf_launch_count()
+    # clocks: sample a ~1 s load phase of the same step plus the timed region
     clocks = Clocks(dev)
-    barrier(ws)
+    t_load = time.perf_counter()
+    while time.perf_counter() - t_load < 1.0:
+        run()
     torch.cuda.synchronize()
-    for k in range(args.steps):
-        flush.fill_(float(k))
-        starts[k].record()
-        eng.run()  # one CUDA-graph launch + one host sync (status, N_b)
-        ends[k].record()
-    torch.cuda.synchronize()
-    barrier(ws)
+    launches0 = lib.vf_launch_count()
+    step_ms = timed_steps(run, args.steps, flush, ws)
     launches = lib.vf_launch_count() - launches0
     ck = clocks.stop()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = allmax(ws, float(sum(step_ms)))
     cells = eng.cells_classified()
-    cells_all = cells
-    if ws > 1:
-        import torch.distributed as dist
-        t = torch.tensor([cells], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t)
-        cells_all = int(t.item())
+    if sharded:
+        cells_all = cells  # one mesh: every rank reports the same grid
+    else:
+        cells_all = cells
+        if ws > 1:
+            import torch.distributed as dist
+            t = torch.tensor([cells], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t)
+            cells_all = int(t.item())
     value = cells_all * args.steps / (total_ms / 1e3)
     g = eng.grid
-    n_b = int(eng.n_b_host[0])
-    # kernel launches per step: count one eager (non-graph) embed
-    l0 = lib.vf_launch_count()
-    eng.run(timed=True)
-    kernels_per_step = lib.vf_launch_count() - l0 - 0
-    # stage split + dominant-kernel time from eager runs with stage events
-    stage, link_ms = [], []
-    for k in range(max(3, min(args.steps, 5))):
-        flush.fill_(float(k))
-        eng.run(timed=True)
-        torch.cuda.synchronize()
-        stage.append(eng.timings())
-        link_ms.append(eng.link_kernel_ms())
-
-    # roofline of the dominant kernel (k_links): algorithmic bytes per launch
-    # = face records read (96 B/face) + LUT read-modify-write of every cell x
-    # direction of the mapped blocks (27*64*4 B x2 per boundary block)
-    F = eng.mesh.n_faces
-    link_bytes = F * 96 + n_b * 27 * 64 * 4 * 2
-    lk = float(np.median(link_ms))
-    peak, peak_kind = peaks()
-    achieved = link_bytes / (lk / 1e3) / 1e9
     med = lambda a: float(np.median(a))
-    stages = {k: med([getattr(s, k) for s in stage]) for k in
-              ("binning", "voxelization", "refinement", "boundary", "links", "total")}
+    F = eng.mesh.n_faces
+    peak, peak_kind = peaks()
+    stages, roofline, kernels_per_step = None, None, launches // max(args.steps, 1)
+    if not sharded:
+        n_b = int(eng.n_b_host[0])
+        # kernels per step: count one eager (non-graph) embed
+        l0 = lib.vf_launch_count()
+        eng.run(timed=True)
+        kernels_per_step = lib.vf_launch_count() - l0
+        stage, link_ms = [], []
+        for k in range(max(3, min(args.steps, 5))):
+            flush.fill_(float(k))
+            eng.run(timed=True)
+            torch.cuda.synchronize()
+            stage.append(eng.timings())
+            link_ms.append(eng.link_kernel_ms())
+        stages = {k: med([getattr(s, k) for s in stage]) for k in
+                  ("binning", "voxelization", "refinement", "boundary", "links", "total")}
+        # dominant kernel k_links: algorithmic bytes per launch = face records
+        # (96 B/face) + LUT read-modify-write of the mapped blocks (2 x 6912 B)
+        link_bytes = F * 96 + n_b * 27 * 64 * 4 * 2
+        lk = med(link_ms)
+        achieved = link_bytes / (lk / 1e3) / 1e9
+        roofline = {"kernel": "k_links", "bound": "hbm", "achieved": achieved, "peak": peak,
+                    "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": None, "kernel_ms": lk, "algorithmic_bytes": int(link_bytes)}
+    else:
+        n_b = int(eng.lengths.shape[0]) if eng.lengths is not None else 0
 
     e2e = None
     if not args.no_e2e:
         fc = torch.from_numpy(np.ascontiguousarray(mesh.faces_coord)).pin_memory()
         nr = torch.from_numpy(np.ascontiguousarray(mesh.normals)).pin_memory()
-        out = None
+        if sharded:
+            dfc = torch.empty((F, 9), dtype=torch.float64, device="cuda")
+            dn = torch.empty((F, 3), dtype=torch.float64, device="cuda")
+            holder = {}
+
+            def e2e_step():
+                dfc.copy_(fc, non_blocking=True)
+                dn.copy_(nr, non_blocking=True)
+                _lib.check(lib.vf_pack_faces(_lib.ptr(dfc), _lib.ptr(dn), F, _lib.ptr(eng.mesh.faces),
+                                             _lib.stream_ptr()))
+                gg, tt = eng.run()
+                n = gg.n_used
+                outs = [gg.coords[:n], gg.nbr[:n], gg.child[:n], gg.bflags[:n], gg.masks[:n],
+                        tt.contraction_map[:n], tt.lengths]
+                d2h = 0
+                for i, t_ in enumerate(outs):
+                    buf = holder.get(i)
+                    if buf is None or buf.shape != t_.shape:
+                        buf = holder[i] = torch.empty(t_.shape, dtype=t_.dtype).pin_memory()
+                    buf.copy_(t_, non_blocking=True)
+                    d2h += t_.numel() * t_.element_size()
+                holder["d2h"] = d2h
+        else:
+            holder = {"out": None}
+
+            def e2e_step():
+                holder["out"], h2d_, holder["d2h"] = eng.embed_host(fc, nr, holder["out"])
         for _ in range(2):
-            out, h2d, d2h = eng.embed_host(fc, nr, out)
-        torch.cuda.synchronize()
-        es = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        ee = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        barrier(ws)
-        for k in range(args.steps):
-            flush.fill_(float(k))
-            es[k].record()
-            out, h2d, d2h = eng.embed_host(fc, nr, out)
-            ee[k].record()
-        torch.cuda.synchronize()
-        barrier(ws)
-        e2e_ms = allmax(ws, float(sum(s.elapsed_time(e) for s, e in zip(es, ee))))
+            e2e_step()
+        e2e_ms = allmax(ws, float(sum(timed_steps(e2e_step, args.steps, flush, ws))))
         e2e = {"value": cells_all * args.steps / (e2e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "h2d_bytes_per_step": int(F * 96), "d2h_bytes_per_step": int(holder["d2h"]),
                "ms_per_step": e2e_ms / args.steps}
 
     if rank != 0:
@@ -301,21 +344,24 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
         cpu = cpu_baseline(mesh, cfg, cells)
+    par = "single GPU"
+    if ws > 1:
+        par = (f"block-sharded x{ws} (row ownership, NCCL all-reduce of per-level flags, "
+               f"finest solid masks and boundary counts)" if sharded else f"independent objects x{ws}")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": w["desc"], "faces": int(F), "cells_per_embed": int(cells),
                    "blocks": int(g.n_used), "boundary_blocks": n_b,
                    "embed_ms_median": med(step_ms), "stage_ms_eager": stages,
                    "l2": "64 Mi-float (256 MB) buffer rewritten between steps, outside step events",
-                   "parallelism": f"independent objects x{ws}" if ws > 1 else "single GPU"},
-        "roofline": {"kernel": "k_links", "bound": "hbm", "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel_ms": lk, "algorithmic_bytes": int(link_bytes)},
-        "cpu_baseline": cpu, "e2e": e2e,
+                   "parallelism": par},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": int(kernels_per_step * args.steps),
-        "gpu_launch_note": f"{kernels_per_step} kernels per embed, issued as one CUDA graph per step",
+        "gpu_launch_note": (f"{kernels_per_step} kernels per embed" +
+                            ("" if sharded else ", issued as one CUDA graph per step")),
         "clocks": ck,
     }
     print(json.dumps(line), flush=True)

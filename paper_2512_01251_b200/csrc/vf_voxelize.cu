@@ -52,11 +52,14 @@ __global__ void __launch_bounds__(kVoxWarps * 32)
     // tiles of 32 blocks: each lane fetches one block's bin header, so the
     // dependent coords -> counts loads of 32 blocks overlap; only blocks with
     // a non-empty bin are then processed, one at a time by the whole warp
-    for (int64_t b0 = s + gw * 32; b0 < e; b0 += nw * 32) {
+    // (warp gw owns blocks s + gw + k*nw; a tile is 32 consecutive k, which
+    // keeps the strided spread of busy blocks over warps)
+    for (int64_t k0 = 0; s + gw + k0 * nw < e; k0 += 32) {
+      const int64_t bl = s + gw + (k0 + lane) * nw;
       int4 co_l = make_int4(0, 0, 0, 0);
       int nf_l = 0, off_l = 0;
-      if (b0 + lane < e) {
-          co_l = *reinterpret_cast<const int4 *>(coords + 4 * (b0 + lane));
+      if (bl < e) {
+          co_l = *reinterpret_cast<const int4 *>(coords + 4 * bl);
           const int64_t bin_l = co_l.x + (int64_t)li.bins[0] * (co_l.y + (int64_t)li.bins[1] * co_l.z);
           nf_l = counts[bin_l];
           if (nf_l) off_l = offsets[bin_l];
@@ -65,7 +68,7 @@ __global__ void __launch_bounds__(kVoxWarps * 32)
       while (todo) {
         const int src = __ffs(todo) - 1;
         todo &= todo - 1;
-        const int64_t b = b0 + src;
+        const int64_t b = s + gw + (k0 + src) * nw;
         int4 co;
         co.x = __shfl_sync(0xffffffffu, co_l.x, src);
         co.y = __shfl_sync(0xffffffffu, co_l.y, src);
