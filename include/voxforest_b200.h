@@ -221,6 +221,11 @@ int vf_shard_zero_unowned(const vf_config *cfg, vf_grid *grid, int level,
                           int32_t *d_bcount, void *stream);
 /* copy the grid's latched device status to the host (synchronizes) */
 int vf_check_status(const vf_grid *grid, void *stream);
+/* test hook: capacity of the link-length band list (candidates the FP32
+ * classifier leaves to the exact SAT; default 1<<20).  A smaller value forces
+ * the overflow fallback pass; results are identical.  Returns the old value;
+ * n < 0 only queries. */
+int64_t vf_set_link_band_cap(int64_t n);
 
 #ifdef __cplusplus
 }

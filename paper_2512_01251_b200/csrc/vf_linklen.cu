@@ -22,10 +22,18 @@
 //   - a line through the triangle meets the face plane at one point; the
 //     (2, rarely 3) lattice nodes within one link of that crossing are the
 //     only possible link endpoints, in +c or -c direction.
-// Candidates (face, node, pair) go to a per-warp shared-memory queue drained
-// 32 at a time through the exact FP64 path (bit-identical to the oracle), so
-// the SAT runs warp-converged.  The pre-filter passes a superset of the exact
-// decisions; every stored value comes from the exact path.
+// Lines are classified with FP32 edge functions and margins far above their
+// rounding error:
+//   - clearly outside the projected triangle: no link (the exact SAT rejects);
+//   - clearly inside, well-conditioned crossing: FAST exact path -- the FP64
+//     num/den/d/q of the oracle without the eps-box SAT, which provably
+//     accepts an interior piercing point (link_fast);
+//   - within the margin band of an edge, or ill-conditioned: the candidate
+//     (face, node, pair) goes to a per-warp shared-memory queue drained 32 at
+//     a time through the full exact FP64 path with the SAT (link_candidate),
+//     so the SAT runs warp-converged.
+// Every stored value is the oracle's FP64 value; only the SAT evaluation is
+// skipped where its outcome is certain.
 #include <math.h>
 
 #include "vf_common.cuh"
@@ -92,192 +100,354 @@ __device__ __noinline__ void link_candidate(const double *__restrict__ faces, in
 }
 
 constexpr int kLinkWarps = 4;
-constexpr int kQueue = 640;
-
-struct LinkQueue {
-    int4 e[kLinkWarps][kQueue];  // (face, slot, i | j<<16, k | r<<16)
-    int n[kLinkWarps];
-};
 
 struct LinkCtx {
     const double *faces;
     const int32_t *bmap;
     float *lengths;
-    double dx, eps, eps_par;
+    int4 *band;        // band candidates (face, slot, i | j<<16, k | r<<16)
+    int32_t *n_band;   // [0] count (may exceed cap), [1] overflow flag
+    int64_t band_cap;
+    double dx, eps, eps_par, inv_dx;
     int bx, by, cells[3];
+    int fast;  // eps >> FP64 rounding of the piercing point: fast path allowed
+    int pow2;  // dx is a power of two: q = dd * (1/dx) is exactly dd / dx
 };
-
-__device__ __forceinline__ void push_candidate(LinkQueue &Q, int w, const LinkCtx &c, int f, int slot,
-                                               int i, int j, int k, int r) {
-    const int pos = atomicAdd(&Q.n[w], 1);
-    if (pos < kQueue) {
-        Q.e[w][pos] = make_int4(f, slot, i | (j << 16), k | (r << 16));
-    } else {  // overflow (pathological face): decide inline, same exact path
-        link_candidate(c.faces, f, r, i, j, k, c.dx, c.eps, c.eps_par, slot, c.lengths);
-    }
-}
-
-// drain the queue in full warps (all = drain the remainder too); warp-uniform
-__device__ __forceinline__ void drain(LinkQueue &Q, int w, int lane, const LinkCtx &c, bool all) {
-    __syncwarp();
-    int n = min(Q.n[w], kQueue);
-    while (n >= 32 || (all && n > 0)) {
-        const int take = min(n, 32);
-        int4 e = make_int4(0, -1, 0, 0);
-        if (lane < take) e = Q.e[w][n - take + lane];
-        __syncwarp();
-        if (lane < take)
-            link_candidate(c.faces, e.x, e.w >> 16, e.z & 0xffff, e.z >> 16, e.w & 0xffff, c.dx,
-                           c.eps, c.eps_par, e.y, c.lengths);
-        n -= take;
-    }
-    __syncwarp();
-    if (lane == 0) Q.n[w] = n;
-    __syncwarp();
-}
 
 // representative directions q = 2r+1 (lattice.py order) in constant memory
 __constant__ int8_t c_rep[13][3] = {
     {1, 0, 0},  {0, 1, 0},  {0, 0, 1},   {1, 1, 0},  {1, 0, 1},  {1, 0, -1}, {1, -1, 0},
     {0, 1, 1},  {0, 1, -1}, {1, 1, 1},   {1, 1, -1}, {1, -1, 1}, {1, -1, -1}};
 
-// one direction pair r: enumerate lattice lines along c that pierce the face,
-// push the nodes within one link of each crossing.  A runtime loop over r
-// (not 13 unrolled copies): the unrolled kernel was 12k SASS instructions and
-// stalled 89% on instruction fetch.
-__device__ __noinline__ void face_direction(LinkQueue &Q, int w, const LinkCtx &c, int f, int R,
-                                            const double *v, const float *nf, const float *V1,
-                                            const float *V2, float Ef, const int *lo_p,
-                                            const int *hi_p) {
-    const int cc[3] = {c_rep[R][0], c_rep[R][1], c_rep[R][2]};
-    const int p = cc[0] != 0 ? 0 : (cc[1] != 0 ? 1 : 2);
-    const int q1 = p == 0 ? 1 : 0, q2 = p == 2 ? 1 : 2;
-    const int s1 = cc[q1] * cc[p], s2 = cc[q2] * cc[p];  // c_q / c_p (c_p = +-1)
-    const float dn = (float)cc[0] * nf[0] + (float)cc[1] * nf[1] + (float)cc[2] * nf[2];
+template <typename T>
+__device__ __forceinline__ T pick3(int a, T x, T y, T z) {
+    return a == 0 ? x : (a == 1 ? y : z);
+}
+
+// Per (face, direction pair) state of the lattice-line enumeration.  Each
+// lane builds the state of its own face for the warp-uniform direction pair,
+// publishes it in shared memory, and the lattice ROWS of all 32 faces'
+// projected bounding boxes are then processed as one flattened work list, 32
+// rows per step (per-face loops left 10 of 32 lanes active).
+struct LinkDir {
+    double off1, off2, vp, den;  // lattice offsets, v1_p, exact c.n
+    float P1a, P1b, P2a, P2b;    // projected triangle relative to v1
+    float t0, t1, t2, sg;        // edge margins, orientation
+    float nq1, nq2, dn, wid0;    // crossing estimate
+    int m1a, m1b, m2a, f;        // lattice box, face id
+    int lop, hip, fast, pad;     // fallback node range along p, fast path allowed
+};
+
+// per-warp shared state: the 32 faces (loaded once, read by every direction
+// pair) and their per-pair enumeration state
+struct LinkWarp {
+    LinkDir d[32];
+    double fv[32][12];  // v1 v2 v3 n of the lane's face
+    float ff[32][12];   // nf, V1 = v2 - v1, V2 = v3 - v1 (FP32), Ef, pad
+    int lohi[32][6];    // fallback node range per axis
+    int excl[32];       // exclusive prefix of the per-lane row counts
+};
+
+// Exact accept of one node without the eps-box SAT (the FAST path).  Only
+// used for lines that pass through the projected triangle with a margin of
+// tol (>= 1e-5 (ext + dx), >> the FP32 error of the edge functions) and a
+// well-conditioned crossing: the true piercing point is then an interior
+// point of the face, its FP64 image lies within ~1e-16 of it, and the
+// eps = 1e-9 cube around it overlaps the face on every SAT axis with slack
+// eps |axis| >> the FP64 rounding of the test -- the reference SAT
+// (geometry.py:441-500) accepts.  num, den, d, the (0, dx] range and q are
+// bit-identical to link_candidate / orc_link_lengths.
+__device__ __forceinline__ void link_fast(const LinkCtx &c, const double *fv, int r, double den,
+                                          int i, int j, int k, int32_t slot) {
+    const double dx = c.dx;
+    const double x = node_c(i, dx), y = node_c(j, dx), z = node_c(k, dx);
+    const double d = VF_DDIV(plane_num(fv, fv + 9, x, y, z), den);
+    const bool pos = d > 0.0;
+    const double dd = pos ? d : -d;
+    if (!(dd > 0.0 && dd <= dx)) return;
+    const int q = pos ? 2 * r + 1 : 2 * r + 2;
+    // dx = 2^-k: dd * 2^k is exact, hence equal to the correctly rounded dd/dx
+    const double qd = c.pow2 ? VF_DMUL(dd, c.inv_dx) : VF_DDIV(dd, dx);
+    const float qv = __double2float_rn(qd);
+    const int t = (i & 3) + 4 * (j & 3) + 16 * (k & 3);
+    atomicMin(reinterpret_cast<unsigned int *>(c.lengths) + ((int64_t)slot * 27 + q) * 64 + t,
+              __float_as_uint(qv));
+}
+
+// state of (lane's face, pair R); returns the number of lattice rows of the
+// projected bounding box (0: no link of this face in this pair)
+__device__ __forceinline__ int link_dir_setup(LinkDir &D, const LinkCtx &c, const double *v,
+                                              const float *ff, const int *lohi, int R, int p,
+                                              int q1, int q2, int s1, int s2) {
+    const double *n = v + 9;
+    const float *nf = ff, *V1 = ff + 3, *V2 = ff + 6;
+    const int cx = c_rep[R][0], cy = c_rep[R][1], cz = c_rep[R][2];
+    // exact den / EPS_PARALLEL (link_candidate): a face parallel to c has no
+    // link in this direction pair at all
+    const double c0 = cx, c1 = cy, c2 = cz;
+    const double cn = __dsqrt_rn(VF_DADD(VF_DADD(VF_DMUL(c0, c0), VF_DMUL(c1, c1)), VF_DMUL(c2, c2)));
+    const double den = VF_DADD(VF_DADD(VF_DMUL(c0, n[0]), VF_DMUL(c1, n[1])), VF_DMUL(c2, n[2]));
+    if (fabs(den) < VF_DMUL(c.eps_par, cn)) return 0;
+    const float dn = (float)cx * nf[0] + (float)cy * nf[1] + (float)cz * nf[2];
     const double dx = c.dx;
     const float dxf = (float)dx;
-    // projected triangle (relative to v1) on the plane x_p = v1_p
-    const float P0a = 0.0f, P0b = 0.0f;
-    const float P1a = V1[q1] - (float)s1 * V1[p], P1b = V1[q2] - (float)s2 * V1[p];
-    const float P2a = V2[q1] - (float)s1 * V2[p], P2b = V2[q2] - (float)s2 * V2[p];
+    const float V1p = pick3(p, V1[0], V1[1], V1[2]), V2p = pick3(p, V2[0], V2[1], V2[2]);
+    const float P1a = pick3(q1, V1[0], V1[1], V1[2]) - (float)s1 * V1p;
+    const float P1b = pick3(q2, V1[0], V1[1], V1[2]) - (float)s2 * V1p;
+    const float P2a = pick3(q1, V2[0], V2[1], V2[2]) - (float)s1 * V2p;
+    const float P2b = pick3(q2, V2[0], V2[1], V2[2]) - (float)s2 * V2p;
     const float cr = P1a * P2b - P1b * P2a;
     const float ext = fmaxf(fmaxf(fabsf(P1a), fabsf(P1b)), fmaxf(fabsf(P2a), fabsf(P2b)));
     // tolerance: eps-cube acceptance (<= 2 sqrt 6 eps after the oblique
-    // projection) + FP32 error of coordinates of magnitude ext + dx
+    // projection) + FP32 error of coordinates of magnitude ext + dx, plus an
+    // absolute term >= the FP32 rounding of E_k itself (sliver edges)
     const float tol = 1e-5f * (ext + dxf) + 6.0f * (float)c.eps;
+    const float ab = 4e-6f * (ext + dxf) * (ext + dxf);
+    const float e1a = P2a - P1a, e1b = P2b - P1b;
+    D.P1a = P1a; D.P1b = P1b; D.P2a = P2a; D.P2b = P2b;
+    D.t0 = tol * sqrtf(P1a * P1a + P1b * P1b) + ab;
+    D.t1 = tol * sqrtf(e1a * e1a + e1b * e1b) + ab;
+    D.t2 = tol * sqrtf(P2a * P2a + P2b * P2b) + ab;
     // (a degenerate projection -- face parallel to c -- keeps only lattice
     // points within tol of the projected segment: the edge tests stay valid)
-    const float sg = cr >= 0.0f ? 1.0f : -1.0f;
-    // inward edge functions (not normalised): E_k(P) = sg * cross(edge_k, P - P_k)
-    const float e0a = P1a - P0a, e0b = P1b - P0b;
-    const float e1a = P2a - P1a, e1b = P2b - P1b;
-    const float e2a = P0a - P2a, e2b = P0b - P2b;
-    const float l0 = sqrtf(e0a * e0a + e0b * e0b), l1 = sqrtf(e1a * e1a + e1b * e1b),
-                l2 = sqrtf(e2a * e2a + e2b * e2b);
+    D.sg = cr >= 0.0f ? 1.0f : -1.0f;
+    const double vp = pick3(p, v[0], v[1], v[2]);
     // lattice of line traces: coordinate j of the trace of the line through
     // node (i_p, i_q1, i_q2) is ((i_qj - s_j i_p) + delta_j) dx + s_j v1_p,
     // delta_j = (1 - s_j)/2; relative to v1: subtract v1_qj
-    const double off1 = (double)s1 * v[p] - v[q1], off2 = (double)s2 * v[p] - v[q2];
+    const double off1 = (double)s1 * vp - pick3(q1, v[0], v[1], v[2]);
+    const double off2 = (double)s2 * vp - pick3(q2, v[0], v[1], v[2]);
     const double d1 = 0.5 * (1 - s1), d2 = 0.5 * (1 - s2);
-    const float bmin1 = fminf(fminf(P0a, P1a), P2a) - tol, bmax1 = fmaxf(fmaxf(P0a, P1a), P2a) + tol;
-    const float bmin2 = fminf(fminf(P0b, P1b), P2b) - tol, bmax2 = fmaxf(fmaxf(P0b, P1b), P2b) + tol;
-    const double inv = 1.0 / dx;
+    const float bmin1 = fminf(fminf(0.0f, P1a), P2a) - tol, bmax1 = fmaxf(fmaxf(0.0f, P1a), P2a) + tol;
+    const float bmin2 = fminf(fminf(0.0f, P1b), P2b) - tol, bmax2 = fmaxf(fmaxf(0.0f, P1b), P2b) + tol;
+    const double inv = c.inv_dx;
     const int m1a = (int)ceil(((double)bmin1 - off1) * inv - d1 - 1e-6);
     const int m1b = (int)floor(((double)bmax1 - off1) * inv - d1 + 1e-6);
     const int m2a = (int)ceil(((double)bmin2 - off2) * inv - d2 - 1e-6);
     const int m2b = (int)floor(((double)bmax2 - off2) * inv - d2 + 1e-6);
+    if (m1b < m1a || m2b < m2a) return 0;
     const bool steep = fabsf(dn) >= 1e-3f;
-    for (int m2 = m2a; m2 <= m2b; ++m2) {
-        const float Rb = (float)(((double)m2 + d2) * dx + off2);
-        for (int m1 = m1a; m1 <= m1b; ++m1) {
-            const float Ra = (float)(((double)m1 + d1) * dx + off1);
-            // inside the projected triangle (with tolerance)
-            const float E0 = sg * (e0a * (Rb - P0b) - e0b * (Ra - P0a));
-            const float E1 = sg * (e1a * (Rb - P1b) - e1b * (Ra - P1a));
-            const float E2 = sg * (e2a * (Rb - P2b) - e2b * (Ra - P2a));
-            if (E0 < -tol * l0 || E1 < -tol * l1 || E2 < -tol * l2) continue;
-            // crossing with the face plane: Q = v1 + Ra e_q1 + Rb e_q2 (+0 e_p),
-            // points Q + lam c; n.(Q + lam c - v1) = 0
-            int ip_lo, ip_hi;
-            if (steep) {
-                const float lam = -(nf[q1] * Ra + nf[q2] * Rb) / dn;
-                const float xs = (float)cc[p] * lam;  // x_p* - v1_p
-                const float wid = dxf * (1.0f + 1e-4f) + (Ef + 1e-6f * fabsf(xs)) / fabsf(dn) + 1e-5f * dxf;
-                // node index i_p with |x_p* - (i_p + 0.5) dx| <= dx
-                ip_lo = (int)ceil(((double)(xs - wid) + v[p]) * inv - 0.5);
-                ip_hi = (int)floor(((double)(xs + wid) + v[p]) * inv - 0.5);
-                ip_lo = max(ip_lo, lo_p[p]);
-                ip_hi = min(ip_hi, hi_p[p]);
-            } else {  // ill-conditioned crossing: every node of the face's p-range +- dx
-                ip_lo = lo_p[p];
-                ip_hi = hi_p[p];
-            }
-            for (int ip = ip_lo; ip <= ip_hi; ++ip) {
-                int idx[3];
-                idx[p] = ip;
-                // i_qj = m_j + s_j i_p
-                idx[q1] = m1 + s1 * ip;
-                idx[q2] = m2 + s2 * ip;
-                if (idx[q1] < 0 || idx[q1] >= c.cells[q1] || idx[q2] < 0 || idx[q2] >= c.cells[q2]) continue;
-                const int32_t slot =
-                    c.bmap[(idx[0] >> 2) + (int64_t)c.bx * ((idx[1] >> 2) + (int64_t)c.by * (idx[2] >> 2))];
-                if (slot < 0) continue;
-                push_candidate(Q, w, c, f, slot, idx[0], idx[1], idx[2], R);
-            }
-        }
+    D.off1 = off1; D.off2 = off2; D.vp = vp; D.den = den;
+    D.nq1 = pick3(q1, nf[0], nf[1], nf[2]);
+    D.nq2 = pick3(q2, nf[0], nf[1], nf[2]);
+    D.dn = steep ? dn : 0.0f;  // 0: ill-conditioned crossing, full node range
+    D.wid0 = dxf * (1.0f + 1e-4f) + 1e-5f * dxf + ff[9] / fabsf(dn);
+    D.m1a = m1a; D.m1b = m1b; D.m2a = m2a;
+    D.lop = pick3(p, lohi[0], lohi[1], lohi[2]);
+    D.hip = pick3(p, lohi[3], lohi[4], lohi[5]);
+    D.fast = steep && c.fast;
+    return m2b - m2a + 1;
+}
+
+// a candidate the fast path cannot decide: appended to the band list for
+// k_links_band (FULL: decided inline -- the overflow fallback kernel)
+template <bool FULL>
+__device__ __forceinline__ void link_slow(const LinkCtx &c, int f, int slot, int i, int j, int k,
+                                          int r) {
+    if (FULL) {
+        link_candidate(c.faces, f, r, i, j, k, c.dx, c.eps, c.eps_par, slot, c.lengths);
+        return;
+    }
+    const int pos = atomicAdd(&c.n_band[0], 1);
+    if (pos < c.band_cap) c.band[pos] = make_int4(f, slot, i | (j << 16), k | (r << 16));
+    else c.n_band[1] = 1;  // the fallback kernel redoes every face inline
+}
+
+// one lattice point (line) of a row: inside test, crossing estimate, then its
+// (2, rarely 3) nodes -- fast exact path for interior lines, link_slow for the
+// margin band and ill-conditioned crossings
+template <bool FULL>
+__device__ __forceinline__ void link_point(const LinkCtx &c, const LinkDir &D, const double *fv,
+                                           int m1, int m2, float Rb, int R, int p, int cp, int s1,
+                                           int s2, int n1, int n2) {
+    const double dx = c.dx;
+    const float Ra = (float)(((double)m1 + 0.5 * (1 - s1)) * dx + D.off1);
+    const float sg = D.sg;
+    const float E0 = sg * (D.P1a * Rb - D.P1b * Ra);
+    const float E1 = sg * ((D.P2a - D.P1a) * (Rb - D.P1b) - (D.P2b - D.P1b) * (Ra - D.P1a));
+    const float E2 = sg * (D.P2b * Ra - D.P2a * Rb);
+    if (E0 < -D.t0 || E1 < -D.t1 || E2 < -D.t2) return;  // misses the face
+    const bool fast = !FULL && D.fast && E0 >= D.t0 && E1 >= D.t1 && E2 >= D.t2;
+    // crossing with the face plane: Q = v1 + Ra e_q1 + Rb e_q2 (+0 e_p),
+    // points Q + lam c; n.(Q + lam c - v1) = 0
+    int ip_lo = D.lop, ip_hi = D.hip;
+    if (D.dn != 0.0f) {
+        const float lam = -(D.nq1 * Ra + D.nq2 * Rb) / D.dn;
+        const float xs = (float)cp * lam;  // x_p* - v1_p
+        const float wid = D.wid0 + 1e-6f * fabsf(xs) / fabsf(D.dn);
+        // node index i_p with |x_p* - (i_p + 0.5) dx| <= dx
+        ip_lo = max((int)ceil(((double)(xs - wid) + D.vp) * c.inv_dx - 0.5), ip_lo);
+        ip_hi = min((int)floor(((double)(xs + wid) + D.vp) * c.inv_dx - 0.5), ip_hi);
+    }
+    for (int ip = ip_lo; ip <= ip_hi; ++ip) {
+        // i_qj = m_j + s_j i_p
+        const int a = m1 + s1 * ip, b = m2 + s2 * ip;
+        if (a < 0 || a >= n1 || b < 0 || b >= n2) continue;
+        const int i = p == 0 ? ip : a;
+        const int j = p == 1 ? ip : (p == 0 ? a : b);
+        const int k = p == 2 ? ip : b;
+        const int32_t slot = c.bmap[(i >> 2) + (int64_t)c.bx * ((j >> 2) + (int64_t)c.by * (k >> 2))];
+        if (slot < 0) continue;
+        if (fast) link_fast(c, fv, R, D.den, i, j, k, slot);
+        else link_slow<FULL>(c, D.f, slot, i, j, k, R);
     }
 }
 
+// one lattice row m2: the conservative m1 interval of the row inside the
+// margin-widened triangle (scanline; each edge function is linear in Ra,
+// E_k = alpha_k Ra + beta_k >= -t_k), then its points.  An edge whose bound
+// is ill-conditioned (|alpha_k| tiny) does not restrict the row; the interval
+// is widened by one lattice point on each side -- a superset of the points
+// that pass link_point's own test, which alone decides.
+template <bool FULL>
+__device__ __forceinline__ void link_row(const LinkCtx &c, const LinkDir &D, const double *fv,
+                                         int m2, int R, int p, int cp, int s1, int s2, int n1,
+                                         int n2) {
+    const double dx = c.dx;
+    const float Rb = (float)(((double)m2 + 0.5 * (1 - s2)) * dx + D.off2);
+    const float sg = D.sg;
+    const float al[3] = {-sg * D.P1b, -sg * (D.P2b - D.P1b), sg * D.P2b};
+    const float be[3] = {sg * D.P1a * Rb, sg * ((D.P2a - D.P1a) * (Rb - D.P1b) + (D.P2b - D.P1b) * D.P1a),
+                         -sg * D.P2a * Rb};
+    const float tk[3] = {D.t0, D.t1, D.t2};
+    const float dxf = (float)dx;
+    // magnitude bound of the products in beta_k (FP32 error <~ 3e-7 M)
+    const float sP = fabsf(D.P1a) + fabsf(D.P1b) + fabsf(D.P2a) + fabsf(D.P2b);
+    const float M = sP * (fabsf(Rb) + sP);
+    float lo = -INFINITY, hi = INFINITY;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float a = al[k], rhs = -tk[k] - be[k];
+        if (1e-5f * (M + tk[k]) >= 0.25f * dxf * fabsf(a)) {
+            // (near-)parallel edge: the row is either fully out or unrestricted
+            if (a == 0.0f && be[k] < -tk[k] - 1e-5f * (M + tk[k])) return;
+            continue;
+        }
+        const float b = rhs / a;
+        if (a > 0.0f) lo = fmaxf(lo, b);
+        else hi = fminf(hi, b);
+    }
+    const double d1 = 0.5 * (1 - s1);
+    int m1lo = D.m1a, m1hi = D.m1b;
+    if (lo > -INFINITY) m1lo = max(m1lo, (int)ceil(((double)lo - D.off1) * c.inv_dx - d1) - 1);
+    if (hi < INFINITY) m1hi = min(m1hi, (int)floor(((double)hi - D.off1) * c.inv_dx - d1) + 1);
+    for (int m1 = m1lo; m1 <= m1hi; ++m1)
+        link_point<FULL>(c, D, fv, m1, m2, Rb, R, p, cp, s1, s2, n1, n2);
+}
 
-__global__ void __launch_bounds__(kLinkWarps * 32)
-    k_links(LinkCtx c, double inv_dx, int widen, int64_t F, const int32_t *__restrict__ map,
+constexpr size_t kLinkSmem = kLinkWarps * sizeof(LinkWarp);
+
+// K-link.  FULL = false: the main kernel (fast path + band list); FULL = true:
+// the overflow fallback, a no-op unless the band list overflowed, in which
+// case it redoes every face with every undecided candidate decided inline
+// (atomicMin is idempotent, so re-merging the fast results is harmless).
+template <bool FULL>
+__global__ void __launch_bounds__(kLinkWarps * 32, FULL ? 1 : 6)
+    k_links(LinkCtx c, int widen, int64_t F, const int32_t *__restrict__ map,
             const int32_t *__restrict__ d_n_map) {
-    __shared__ LinkQueue Q;
-    const int64_t n = d_n_map ? (int64_t)*d_n_map : F;
+    if (FULL && c.n_band[1] == 0) return;
+    extern __shared__ __align__(16) unsigned char s_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (lane == 0) Q.n[w] = 0;
-    __syncwarp();
+    LinkWarp &W = reinterpret_cast<LinkWarp *>(s_raw)[w];
+    const int64_t n = d_n_map ? (int64_t)*d_n_map : F;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    // all lanes of a warp iterate together (uniform trip count) so drains are
-    // warp-synchronous; lanes past the end are inactive
+    // all lanes of a warp iterate together (uniform trip count); lanes past
+    // the end are inactive
     const int64_t first = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
     for (int64_t base = first; base < n; base += stride) {
         const int64_t m = base + lane;
         const bool active = m < n;
-        double v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, nn[3] = {0, 0, 0};
         int f = 0;
-        float nf[3] = {0, 0, 0}, V1[3] = {0, 0, 0}, V2[3] = {0, 0, 0}, Ef = 0.0f;
-        int lo_p[3] = {0, 0, 0}, hi_p[3] = {-1, -1, -1};
+        __syncwarp();
         if (active) {
             f = map ? map[m] : (int)m;
+            double v[9], nn[3];
             load_face(c.faces, f, v, nn);
             double ext = 0.0;
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
-                nf[d] = (float)nn[d];
-                V1[d] = (float)(v[3 + d] - v[d]);
-                V2[d] = (float)(v[6 + d] - v[d]);
-                const double lo = fmin(fmin(v[d], v[3 + d]), v[6 + d]);
-                const double hi = fmax(fmax(v[d], v[3 + d]), v[6 + d]);
-                ext = fmax(ext, hi - lo);
+                W.fv[lane][d] = v[d];
+                W.fv[lane][3 + d] = v[3 + d];
+                W.fv[lane][6 + d] = v[6 + d];
+                W.fv[lane][9 + d] = nn[d];
+                W.ff[lane][d] = (float)nn[d];
+                W.ff[lane][3 + d] = (float)(v[3 + d] - v[d]);
+                W.ff[lane][6 + d] = (float)(v[6 + d] - v[d]);
+                const double flo = fmin(fmin(v[d], v[3 + d]), v[6 + d]);
+                const double fhi = fmax(fmax(v[d], v[3 + d]), v[6 + d]);
+                ext = fmax(ext, fhi - flo);
                 // nodes within one link of the face AABB (fallback range)
-                lo_p[d] = max((int)floor((lo - c.dx - 2.0 * c.eps) * inv_dx - 0.5) - widen, 0);
-                hi_p[d] = min((int)floor((hi + c.dx + 2.0 * c.eps) * inv_dx - 0.5) + 1 + widen, c.cells[d] - 1);
+                W.lohi[lane][d] = max((int)floor((flo - c.dx - 2.0 * c.eps) * c.inv_dx - 0.5) - widen, 0);
+                W.lohi[lane][3 + d] =
+                    min((int)floor((fhi + c.dx + 2.0 * c.eps) * c.inv_dx - 0.5) + 1 + widen, c.cells[d] - 1);
             }
-            Ef = 4e-6f * (float)(ext + 2.0 * c.dx);
+            W.ff[lane][9] = 4e-6f * (float)(ext + 2.0 * c.dx);
         }
+        __syncwarp();
 #pragma unroll 1
-        for (int r = 0; r < 13; ++r) {
-            if (active) face_direction(Q, w, c, f, r, v, nf, V1, V2, Ef, lo_p, hi_p);
-            drain(Q, w, lane, c, false);
+        for (int R = 0; R < 13; ++R) {
+            // warp-uniform axis bookkeeping of the pair
+            const int cx = c_rep[R][0], cy = c_rep[R][1], cz = c_rep[R][2];
+            const int p = cx != 0 ? 0 : (cy != 0 ? 1 : 2);
+            const int q1 = p == 0 ? 1 : 0, q2 = p == 2 ? 1 : 2;
+            const int cp = pick3(p, cx, cy, cz);
+            const int s1 = pick3(q1, cx, cy, cz) * cp, s2 = pick3(q2, cx, cy, cz) * cp;
+            const int n1 = pick3(q1, c.cells[0], c.cells[1], c.cells[2]);
+            const int n2 = pick3(q2, c.cells[0], c.cells[1], c.cells[2]);
+            int cnt = 0;
+            if (active) {
+                LinkDir D;
+                D.f = f;
+                cnt = link_dir_setup(D, c, W.fv[lane], W.ff[lane], W.lohi[lane], R, p, q1, q2, s1, s2);
+                if (cnt) W.d[lane] = D;
+            }
+            // warp exclusive prefix of the row counts
+            int inc = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            const int total = __shfl_sync(0xffffffffu, inc, 31);
+            W.excl[lane] = inc - cnt;
+            __syncwarp();
+            for (int it = lane; it < total; it += 32) {
+                int o = 0;  // owner lane: largest o with excl[o] <= it
+#pragma unroll
+                for (int st = 16; st > 0; st >>= 1)
+                    if (W.excl[o + st] <= it) o += st;
+                const LinkDir &D = W.d[o];
+                link_row<FULL>(c, D, W.fv[o], D.m2a + it - W.excl[o], R, p, cp, s1, s2, n1, n2);
+            }
+            __syncwarp();
         }
     }
-    drain(Q, w, lane, c, true);
+}
+
+// the band candidates: full exact path (num, den, d, eps-box SAT), one per
+// thread -- all threads take the same path, so the SAT runs converged
+__global__ void __launch_bounds__(256)
+    k_links_band(LinkCtx c) {
+    const int64_t n = min((int64_t)c.n_band[0], c.band_cap);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int4 x = c.band[e];
+        link_candidate(c.faces, x.x, x.w >> 16, x.z & 0xffff, x.z >> 16, x.w & 0xffff, c.dx, c.eps,
+                       c.eps_par, x.y, c.lengths);
+    }
+}
+
+// workspace: dense block map of the finest level | band counters | band list
+constexpr int64_t kBandCap = 1 << 20;  // 16 MB; overflow only costs the fallback pass
+static int64_t g_band_cap = kBandCap;    // vf_set_link_band_cap (test hook)
+
+static size_t bmap_bytes(const vf_config &cfg, int finest) {
+    const int64_t nb = (int64_t)(cfg.nb[0] << finest) * (cfg.nb[1] << finest) * (cfg.nb[2] << finest);
+    return ((size_t)nb * sizeof(int32_t) + 255) & ~(size_t)255;
 }
 
 size_t link_workspace_size(const vf_config &cfg, int finest) {
-    const int64_t nb = (int64_t)(cfg.nb[0] << finest) * (cfg.nb[1] << finest) * (cfg.nb[2] << finest);
-    return ((size_t)nb * sizeof(int32_t) + 255) & ~(size_t)255;
+    return bmap_bytes(cfg, finest) + 256 + (size_t)kBandCap * sizeof(int4);
 }
 
 // LUT initialisation to -1 for the device-resident N_b slots (graph-safe:
@@ -316,7 +486,10 @@ int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const doubl
         return set_error(VF_EARG, "link lengths: > 32767 cells per axis");
     const int64_t nb = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
     int32_t *bmap = (int32_t *)ws;
+    int32_t *n_band = (int32_t *)((char *)ws + bmap_bytes(cfg, L));
+    int4 *band = (int4 *)((char *)n_band + 256);
     cudaMemsetAsync(bmap, 0xff, sizeof(int32_t) * (size_t)nb, st);
+    cudaMemsetAsync(n_band, 0, 2 * sizeof(int32_t), st);
     k_blockmap<<<max_ctas(8), 256, 0, st>>>(li, L, g->d_level_start, g->d_coords, cmap, bmap, d_n_b,
                                             lengths_cap);
     int rc = check_launch("k_blockmap");
@@ -325,25 +498,46 @@ int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const doubl
     c.faces = faces;
     c.bmap = bmap;
     c.lengths = lengths;
+    c.band = band;
+    c.n_band = n_band;
+    c.band_cap = g_band_cap;
     c.dx = li.dx;
     c.eps = li.eps;
     c.eps_par = li.eps_par;
     c.bx = li.bins[0];
     c.by = li.bins[1];
+    c.fast = li.eps >= 1e-12 * fmax(fmax(li.len[0], li.len[1]), li.len[2]);
     for (int d = 0; d < 3; ++d) c.cells[d] = li.cells[d];
     // 1/dx is exact when dx is a power of two; otherwise widen the ranges by one
     int ex = 0;
     const double mant = frexp(li.dx, &ex);
-    const int widen = (mant == 0.5) ? 0 : 1;
-    const double inv_dx = 1.0 / li.dx;
+    c.pow2 = mant == 0.5;
+    const int widen = c.pow2 ? 0 : 1;
+    c.inv_dx = 1.0 / li.dx;
     int64_t grid = (F + 32 * kLinkWarps - 1) / (32 * kLinkWarps);
     if (grid > max_ctas(6)) grid = max_ctas(6);
     if (grid < 1) grid = 1;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_links<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLinkSmem);
+        cudaFuncSetAttribute(k_links<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLinkSmem);
+        attr = true;
+    }
     if (events) cudaEventRecord((cudaEvent_t)events[0], st);
-    k_links<<<(int)grid, kLinkWarps * 32, 0, st>>>(c, inv_dx, widen, F, map, d_n_map);
-    rc = check_launch("k_links");
+    k_links<false><<<(int)grid, kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, map, d_n_map);
+    if ((rc = check_launch("k_links"))) return rc;
+    k_links_band<<<max_ctas(2), 256, 0, st>>>(c);
+    if ((rc = check_launch("k_links_band"))) return rc;
+    k_links<true><<<(int)grid, kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, map, d_n_map);
+    rc = check_launch("k_links_full");
     if (events) cudaEventRecord((cudaEvent_t)events[1], st);
     return rc;
 }
 
 }  // namespace vf
+
+extern "C" int64_t vf_set_link_band_cap(int64_t n) {
+    const int64_t old = vf::g_band_cap;
+    if (n >= 0) vf::g_band_cap = n < vf::kBandCap ? n : vf::kBandCap;
+    return old;
+}

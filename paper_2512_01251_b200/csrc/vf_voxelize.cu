@@ -27,10 +27,58 @@ namespace vf {
 // --------------------------------------------------------------------------
 // K-vox
 
-struct VoxFace {        // shared-memory face record (21 doubles + flag)
+struct VoxFace {        // shared-memory face record (24 doubles + FP32 row classifier)
     SatFace s;
     double n[3];
+    float4 yz;          // yz projection of v2 - v1, v3 - v1 (FP32)
+    float4 tol;         // per-edge margins t0, t1, t2 and the orientation sign
 };
+
+// FP32 row classifier (exactness argument in row_class): 0 = the x-row misses
+// the face, 1 = it pierces the face interior, 2 = undecided (exact SAT).
+// The row box [0, lx] x [y +- eps] x [z +- eps] overlaps the face iff the
+// point (y, z) is within the eps-square of the face's yz projection (the
+// other SAT axes follow from the x-extent, see below).  Edge functions are
+// evaluated relative to v1 with margins t_k = tol |e_k| + 4e-6 (ext + dx)^2,
+// tol = 1e-5 (ext + dx) + 6 eps: >= 10x the FP32 error of E_k plus the
+// eps-square reach:
+//   E_k < -t_k for some k: the row box misses the triangle by > tol - 2 eps,
+//     the exact predicate is false with a gap >> the FP64 rounding of the
+//     reference SAT, which therefore rejects;
+//   E_k >= t_k for all k, |n_x| >= 1e-3 and the face's x-range inside
+//     (tol_x, lx - tol_x): the row pierces the face interior at a point of the
+//     box, every one of the 13 SAT axes has slack >> FP64 rounding, and the
+//     reference SAT (geometry.py:441-500) accepts.
+__device__ __forceinline__ void row_class_init(VoxFace &F, const double *v, const double *n,
+                                               double dx, double eps, double lx) {
+    const float a1 = (float)(v[4] - v[1]), b1 = (float)(v[5] - v[2]);
+    const float a2 = (float)(v[7] - v[1]), b2 = (float)(v[8] - v[2]);
+    const float cr = a1 * b2 - b1 * a2;
+    const float ext = fmaxf(fmaxf(fabsf(a1), fabsf(b1)), fmaxf(fabsf(a2), fabsf(b2)));
+    const float tol = 1e-5f * (ext + (float)dx) + 6.0f * (float)eps;
+    const float e1a = a2 - a1, e1b = b2 - b1;
+    float sg = cr >= 0.0f ? 1.0f : -1.0f;
+    const double tx = 1e-6 * lx;
+    // no fast accept: ill-conditioned x crossing or face near the domain x ends
+    const bool acc = fabs(n[0]) >= 1e-3 && F.s.lo[0] > tx && F.s.hi[0] < lx - tx && cr != 0.0f;
+    F.yz = make_float4(a1, b1, a2, b2);
+    // + an absolute term >= the FP32 rounding of E_k itself (edge vectors
+    // and offsets of magnitude <= 2 ext + dx; matters for sliver edges)
+    const float ab = 4e-6f * (ext + (float)dx) * (ext + (float)dx);
+    F.tol = make_float4(tol * sqrtf(a1 * a1 + b1 * b1) + ab, tol * sqrtf(e1a * e1a + e1b * e1b) + ab,
+                        tol * sqrtf(a2 * a2 + b2 * b2) + ab, acc ? sg : 2.0f * sg);
+}
+
+__device__ __forceinline__ int row_class(const VoxFace &F, float Ry, float Rz) {
+    const float4 p = F.yz, t = F.tol;
+    const float sg = t.w > 0.0f ? 1.0f : -1.0f;
+    const float E0 = sg * (p.x * Rz - p.y * Ry);
+    const float E1 = sg * ((p.z - p.x) * (Rz - p.y) - (p.w - p.y) * (Ry - p.x));
+    const float E2 = sg * (p.w * Ry - p.z * Rz);
+    if (E0 < -t.x || E1 < -t.y || E2 < -t.z) return 0;
+    const bool acc = fabsf(t.w) == 1.0f;
+    return (acc && E0 >= t.x && E1 >= t.y && E2 >= t.z) ? 1 : 2;
+}
 
 constexpr int kVoxWarps = 4;
 
@@ -94,13 +142,19 @@ __global__ void __launch_bounds__(kVoxWarps * 32)
                 VoxFace &vf_ = s_face[wib][lane];
                 sat_face_init(vf_.s, v);
                 vf_.n[0] = nn[0]; vf_.n[1] = nn[1]; vf_.n[2] = nn[2];
+                row_class_init(vf_, v, nn, dx, eps, lx);
                 s_skip[wib][lane] = fabs(nn[0]) < li.eps_par;  // A7: no x distance
             }
             __syncwarp();
             for (int q = half; q < cnt; q += 2) {
                 if (s_skip[wib][q]) continue;
                 const VoxFace &F = s_face[wib][q];
-                if (!sat_exact(F.s, 0.0, my, mz, lx, My, Mz)) continue;
+                // exact box-axis reject first (most pairs), then the FP32
+                // classifier; only undecided rows run the FP64 SAT
+                if (F.s.hi[1] < my || My < F.s.lo[1] || F.s.hi[2] < mz || Mz < F.s.lo[2]) continue;
+                const int cls = row_class(F, (float)VF_DSUB(y, F.s.v[1]), (float)VF_DSUB(z, F.s.v[2]));
+                if (cls == 0) continue;
+                if (cls == 2 && !sat_exact(F.s, 0.0, my, mz, lx, My, Mz)) continue;
                 const double nx = F.n[0];
 #pragma unroll
                 for (int I = 0; I < 4; ++I) {

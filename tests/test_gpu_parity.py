@@ -298,3 +298,90 @@ def test_capacity_error():
 def test_smoke():
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+# ---------------------------------------------------------------------------
+# grid-aligned degeneracies: faces through lattice nodes, edges on lattice
+# lines, vertices on cell centres -- the cases where the FP32 classifiers of
+# k_voxelize / k_links must hand the decision to the exact FP64 SAT.
+
+def _box_mesh(lo, hi, n, rot_z=0.0):
+    """Closed axis-aligned box [lo, hi]^3 (n x n quads per side, 2 triangles
+    each, outward), optionally rotated about the z axis through its centre."""
+    from paper_2512_01251_b200.mesh import TriangleMesh
+    lo, hi = np.asarray(lo, float), np.asarray(hi, float)
+    verts, faces = [], []
+    t = np.linspace(0.0, 1.0, n + 1)
+    for axis in range(3):
+        for side in (0, 1):
+            a, b = [d for d in range(3) if d != axis]
+            base = len(verts)
+            for i in range(n + 1):
+                for j in range(n + 1):
+                    p = np.empty(3)
+                    p[axis] = hi[axis] if side else lo[axis]
+                    p[a] = lo[a] + t[i] * (hi[a] - lo[a])
+                    p[b] = lo[b] + t[j] * (hi[b] - lo[b])
+                    verts.append(p)
+            for i in range(n):
+                for j in range(n):
+                    v00 = base + i * (n + 1) + j
+                    v10, v01, v11 = v00 + (n + 1), v00 + 1, v00 + n + 2
+                    # (a, b, axis) right-handed?  orient so the normal points out
+                    right = (b - a) % 3 == 1
+                    out = (side == 1) == right
+                    if out:
+                        faces += [[v00, v10, v11], [v00, v11, v01]]
+                    else:
+                        faces += [[v00, v11, v10], [v00, v01, v11]]
+    V = np.array(verts)
+    # weld duplicate corner/edge vertices so the mesh is closed
+    key = np.round(V * 2**40).astype(np.int64)
+    _, first, inv = np.unique(key, axis=0, return_index=True, return_inverse=True)
+    F = first[inv.reshape(-1)][np.array(faces)]
+    if rot_z:
+        c = 0.5 * (lo + hi)
+        cs, sn = np.cos(rot_z), np.sin(rot_z)
+        R = np.array([[cs, -sn, 0], [sn, cs, 0], [0, 0, 1]])
+        V = (V - c) @ R.T + c
+    m = TriangleMesh(V, F)
+    # outward check: signed volume > 0
+    v = V[F]
+    vol = np.einsum("ij,ij->i", v[:, 0], np.cross(v[:, 1], v[:, 2])).sum() / 6.0
+    if vol < 0:
+        m = TriangleMesh(V, F[:, ::-1])
+    return m
+
+
+@pytest.mark.parametrize("case", ["nodes", "faces", "rotated"])
+def test_embed_grid_aligned(O, case):
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    dxf = 1.0 / 32 / 4  # finest cell size
+    if case == "nodes":      # box faces through finest-level cell centres
+        lo, hi = 0.3 + 0.5 * dxf, 0.7 + 0.5 * dxf
+        mesh = _box_mesh([lo] * 3, [hi] * 3, 8)
+    elif case == "faces":    # box faces on cell boundaries, vertices on lattice corners
+        mesh = _box_mesh([0.25] * 3, [0.75] * 3, 16)
+    else:                    # 45 degrees about z: diagonal links graze edges
+        mesh = _box_mesh([0.3 + 0.5 * dxf] * 3, [0.7 + 0.5 * dxf] * 3, 8, rot_z=np.pi / 4)
+    _embed_compare(O, mesh, cfg)
+
+
+def test_links_band_overflow_fallback(O, torus):
+    """Band list capacity 0: every undecided candidate overflows and the
+    fallback pass redoes every face inline -- the LUT must not change."""
+    from paper_2512_01251_b200 import _lib
+    lib = _lib.require_cuda()
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    mesh = _box_mesh([0.3 + 0.5 / 128] * 3, [0.7 + 0.5 / 128] * 3, 8, rot_z=np.pi / 4)
+    for m in (torus, mesh):
+        eng = EmbedEngine(m, cfg, use_graph=False)
+        _, t1 = eng.run()
+        a = t1.lengths.cpu().numpy().copy()
+        old = lib.vf_set_link_band_cap(0)
+        try:
+            _, t2 = eng.run()
+            b = t2.lengths.cpu().numpy()
+        finally:
+            lib.vf_set_link_band_cap(old)
+        assert np.array_equal(a, b)
