@@ -13,7 +13,8 @@ import threading
 from .errors import (BinCapError, CapacityError, CudaError, MeshError, VoxforestError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvoxforest_b200.so")
+# VF_LIB_PATH: an alternative in-tree build of the same library (A/B kernel experiments)
+LIB_PATH = os.environ.get("VF_LIB_PATH") or os.path.join(_HERE, "libvoxforest_b200.so")
 ABI_VERSION = 2
 MAX_LEVELS = 16
 

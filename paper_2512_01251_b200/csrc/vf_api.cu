@@ -119,6 +119,7 @@ struct EmbedWs {
     void *prop_ws, *mark_ws, *adapt_ws, *tab_ws, *link_ws;
     size_t prop_b, mark_b, adapt_b, tab_b, link_b;
     int32_t *bcount;
+    uint16_t *ind_bits;  // [F] per-level 1D indicator bits
 };
 
 static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *base, EmbedWs *w) {
@@ -142,7 +143,7 @@ static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *b
     t.bins.d_n_face_ids = (int32_t *)take(64);
     t.bins_ws_bytes = bins_workspace_size(F, nlim, nbins);
     t.bins_ws = take(t.bins_ws_bytes);
-    t.prop_b = propagate_workspace_size(cap);
+    t.prop_b = propagate_level_workspace_size(cfg, Lf);
     t.prop_ws = take(t.prop_b);
     t.mark_b = mark_workspace_size(cap);
     t.mark_ws = take(t.mark_b);
@@ -152,6 +153,7 @@ static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *b
     t.tab_ws = take(t.tab_b);
     t.link_b = link_workspace_size(cfg, Lf);
     t.link_ws = take(t.link_b);
+    t.ind_bits = (uint16_t *)take(sizeof(uint16_t) * (size_t)(F + 1));
     t.bcount = (int32_t *)take(sizeof(int32_t) * (size_t)cap);
     if (w) *w = t;
     return off;
@@ -364,14 +366,15 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     int k = 0;
     rec(events, n_ev, &k, st);  // 0: start
     VF_TRY(init_forest_impl(*cfg, g, st));
+    // Alg. 1 indicators of every level in one pass over the face records
+    if (use_filter) VF_TRY(launch_indicators_all(*cfg, faces, F, w.ind_bits, st));
     for (int L = 0; L < cfg->l_max; ++L) {
         const LevelInfo li = make_level(*cfg, L);
         VF_TRY(build_bins_impl(li, nlim_of(*cfg), faces, F, 0, use_filter, &w.bins, g->d_status,
-                               w.bins_ws, w.bins_ws_bytes, st));
+                               w.bins_ws, w.bins_ws_bytes, st, w.ind_bits));
         rec(events, n_ev, &k, st);  // bins done
         VF_TRY(voxelize_impl(li, g, L, &w.bins, faces, st));
-        VF_TRY(propagate_impl(li, g, L, +1, L == 0, w.prop_ws, w.prop_b, st));
-        if (L > 0) VF_TRY(propagate_impl(li, g, L, -1, 1, w.prop_ws, w.prop_b, st));
+        VF_TRY(propagate_level_impl(li, g, L, w.prop_ws, w.prop_b, st));
         rec(events, n_ev, &k, st);  // voxelization done
         if (L == cfg->l_max - 1) break;
         VF_TRY(mark_impl(*cfg, g, L, w.mark_ws, w.mark_b, st));

@@ -124,6 +124,76 @@ __global__ void __launch_bounds__(kIndWarps * 32, 3)
     }
 }
 
+// exact row SAT of the band path (reloads the face; rare)
+__device__ __noinline__ bool row_sat_exact(const double *__restrict__ faces, int64_t f, double y,
+                                           double z, double eps, double lx) {
+    double v[9], n[3];
+    load_face(faces, f, v, n);
+    SatFace sf;
+    sat_face_init(sf, v);
+    return sat_exact(sf, 0.0, VF_DSUB(y, eps), VF_DSUB(z, eps), lx, VF_DADD(y, eps), VF_DADD(z, eps));
+}
+
+// All levels in ONE pass over the face records (the per-level kernel reads
+// the 96 B/face records once per level): bit L of out[f] is the 1D indicator
+// of face f at level L.  Candidate rows are decided by the FP32 row
+// classifier (vf_common.cuh); only undecided rows run the exact SAT.  Same
+// predicate as indicator_rows, row for row.
+__global__ void __launch_bounds__(256, 3)
+    k_indicators_all(LevelSet ls, const double *__restrict__ faces, int64_t F,
+                     uint16_t *__restrict__ out) {
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < F;
+         f += (int64_t)gridDim.x * blockDim.x) {
+        double v[9], n[3];
+        load_face(faces, f, v, n);
+        uint32_t bits = 0;
+        if (!(fabs(n[0]) < ls.li[0].eps_par)) {
+            const double xlo = fmin(fmin(v[0], v[3]), v[6]), xhi = fmax(fmax(v[0], v[3]), v[6]);
+            for (int L = 0; L < ls.n; ++L) {
+                const LevelInfo &li = ls.li[L];
+                int ja, jb, ka, kb;
+                if (!face_rows(v, li, ls.inv_dx[L], ls.widen[L], ja, jb, ka, kb)) continue;
+                const double dx = li.dx, eps = li.eps;
+                RowClass rc;
+                row_class_init(rc, v, n, xlo, xhi, dx, eps, li.len[0]);
+                bool hit = false;
+                for (int k = ka; k <= kb && !hit; ++k) {
+                    const double z = node_c(k, dx);
+                    for (int j = ja; j <= jb; ++j) {
+                        if (!owns_row(li, j >> 2, k >> 2)) continue;
+                        const double y = node_c(j, dx);
+                        const int cls = row_class(rc, (float)VF_DSUB(y, v[1]), (float)VF_DSUB(z, v[2]));
+                        if (cls == 0) continue;
+                        if (cls == 1 || row_sat_exact(faces, f, y, z, eps, li.len[0])) {
+                            hit = true;
+                            break;
+                        }
+                    }
+                }
+                if (hit) bits |= 1u << L;
+            }
+        }
+        out[f] = (uint16_t)bits;
+    }
+}
+
+int launch_indicators_all(const vf_config &cfg, const double *faces, int64_t F, uint16_t *out,
+                          cudaStream_t st) {
+    if (F <= 0) return VF_OK;
+    LevelSet ls;
+    ls.n = cfg.l_max;
+    for (int L = 0; L < cfg.l_max; ++L) {
+        ls.li[L] = make_level(cfg, L);
+        int ex = 0;
+        ls.widen[L] = (frexp(ls.li[L].dx, &ex) == 0.5) ? 0 : 1;  // 1/dx exact for 2^-k
+        ls.inv_dx[L] = 1.0 / ls.li[L].dx;
+    }
+    int64_t g = (F + 255) / 256;
+    if (g > max_ctas(8)) g = max_ctas(8);
+    k_indicators_all<<<(int)g, 256, 0, st>>>(ls, faces, F, out);
+    return check_launch("k_indicators_all");
+}
+
 __device__ bool indicator_md(const double *v, const double *n, const LevelInfo &li) {
     SatFace f;
     sat_face_init(f, v);
@@ -404,6 +474,11 @@ struct EmitCompact {
         if (v) map[ex] = (int32_t)i;
     }
 };
+struct LoadBit {
+    const uint16_t *p;
+    int L;
+    __device__ int operator()(int64_t i) const { return (p[i] >> L) & 1; }
+};
 struct LoadI32 {
     const int32_t *p;
     __device__ int operator()(int64_t i) const { return p[i]; }
@@ -417,6 +492,12 @@ int launch_compact(const uint8_t *ind, int64_t n, int32_t *map, int32_t *d_count
                    cudaStream_t st) {
     cudaError_t e = scan_launch(LoadU8{ind}, EmitCompact{map}, n, nullptr, d_count, ws, st);
     return e == cudaSuccess ? VF_OK : set_cuda_error(e, "compact scan");
+}
+
+int launch_compact_bits(const uint16_t *bits, int L, int64_t n, int32_t *map, int32_t *d_count,
+                        void *ws, cudaStream_t st) {
+    cudaError_t e = scan_launch(LoadBit{bits, L}, EmitCompact{map}, n, nullptr, d_count, ws, st);
+    return e == cudaSuccess ? VF_OK : set_cuda_error(e, "compact scan (bits)");
 }
 
 int launch_exclusive_scan(const int32_t *in, int64_t n_bound, const int32_t *d_n, int32_t *out,
@@ -467,7 +548,7 @@ size_t bins_workspace_size(int64_t F, int nlim, int64_t n_bins) {
 // indicators -> compact -> pairs(+hist) -> offsets -> scatter -> sort
 int build_bins_impl(const LevelInfo &li, int nlim, const double *faces, int64_t F, int mode,
                     int use_filter, vf_bins *bins, int32_t *d_status, void *ws, size_t ws_bytes,
-                    cudaStream_t st) {
+                    cudaStream_t st, const uint16_t *ind_bits) {
     const int64_t n_bins = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
     BinsWs w;
     if (bins_ws_layout(F, nlim, n_bins, (char *)ws, &w) > ws_bytes)
@@ -475,7 +556,12 @@ int build_bins_impl(const LevelInfo &li, int nlim, const double *faces, int64_t 
     int rc;
     const int32_t *map = nullptr;
     const int32_t *d_n_map = nullptr;
-    if (use_filter) {
+    if (use_filter && ind_bits && mode == 0) {  // indicators of every level precomputed
+        if ((rc = launch_compact_bits(ind_bits, li.level, F, bins->d_map, bins->d_n_map, w.scan_ws, st)))
+            return rc;
+        map = bins->d_map;
+        d_n_map = bins->d_n_map;
+    } else if (use_filter) {
         if ((rc = launch_indicators(li, mode, faces, F, w.ind, st))) return rc;
         if ((rc = launch_compact(w.ind, F, bins->d_map, bins->d_n_map, w.scan_ws, st))) return rc;
         map = bins->d_map;

@@ -184,6 +184,65 @@ __device__ __forceinline__ bool sat_exact(const SatFace &f, double mx, double my
 }
 
 // ---------------------------------------------------------------------------
+// FP32 x-row classifier (voxelizer rows, 1D ray indicators).
+//
+// Decides the SAT of the row box [0, lx] x [y +- eps] x [z +- eps] against a
+// face without FP64 where the outcome is certain: 0 = the x-row misses the
+// face, 1 = it pierces the face interior, 2 = undecided (run sat_exact).
+// The box overlaps the face iff the point (y, z) is within the eps-square of
+// the face's yz projection (the other SAT axes follow from the x-extent).
+// Edge functions are evaluated relative to v1 with margins
+// t_k = tol |e_k| + 4e-6 (ext + dx)^2, tol = 1e-5 (ext + dx) + 6 eps: >= 10x
+// the FP32 error of E_k (incl. sliver edges) plus the eps-square reach:
+//   E_k < -t_k for some k: the row box misses the triangle by > tol - 2 eps;
+//     the exact predicate is false with a gap >> the FP64 rounding of the
+//     reference SAT, which therefore rejects;
+//   E_k >= t_k for all k, |n_x| >= 1e-3 and the face's x-range inside
+//     (1e-6 lx, lx - 1e-6 lx): the row pierces the face interior at a point
+//     of the box, every one of the 13 SAT axes has slack >> FP64 rounding, and
+//     the reference SAT (geometry.py:441-500) accepts.
+struct RowClass {
+    float4 yz;   // yz projection of v2 - v1, v3 - v1
+    float4 tol;  // per-edge margins t0, t1, t2; w = orientation sign, |w| = 2: no fast accept
+};
+
+__device__ __forceinline__ void row_class_init(RowClass &R, const double *v, const double *n,
+                                               double xlo, double xhi, double dx, double eps,
+                                               double lx) {
+    const float a1 = (float)(v[4] - v[1]), b1 = (float)(v[5] - v[2]);
+    const float a2 = (float)(v[7] - v[1]), b2 = (float)(v[8] - v[2]);
+    const float cr = a1 * b2 - b1 * a2;
+    const float ext = fmaxf(fmaxf(fabsf(a1), fabsf(b1)), fmaxf(fabsf(a2), fabsf(b2)));
+    const float tol = 1e-5f * (ext + (float)dx) + 6.0f * (float)eps;
+    const float ab = 4e-6f * (ext + (float)dx) * (ext + (float)dx);
+    const float e1a = a2 - a1, e1b = b2 - b1;
+    const float sg = cr >= 0.0f ? 1.0f : -1.0f;
+    const double tx = 1e-6 * lx;
+    // no fast accept: ill-conditioned x crossing or face near the domain x ends
+    const bool acc = fabs(n[0]) >= 1e-3 && xlo > tx && xhi < lx - tx && cr != 0.0f;
+    R.yz = make_float4(a1, b1, a2, b2);
+    R.tol = make_float4(tol * sqrtf(a1 * a1 + b1 * b1) + ab, tol * sqrtf(e1a * e1a + e1b * e1b) + ab,
+                        tol * sqrtf(a2 * a2 + b2 * b2) + ab, acc ? sg : 2.0f * sg);
+}
+
+__device__ __forceinline__ void row_class_init(RowClass &R, const SatFace &f, const double *n,
+                                               double dx, double eps, double lx) {
+    row_class_init(R, f.v, n, f.lo[0], f.hi[0], dx, eps, lx);
+}
+
+// (Ry, Rz) = (y - v1_y, z - v1_z) rounded to FP32
+__device__ __forceinline__ int row_class(const RowClass &R, float Ry, float Rz) {
+    const float4 p = R.yz, t = R.tol;
+    const float sg = t.w > 0.0f ? 1.0f : -1.0f;
+    const float E0 = sg * (p.x * Rz - p.y * Ry);
+    const float E1 = sg * ((p.z - p.x) * (Rz - p.y) - (p.w - p.y) * (Ry - p.x));
+    const float E2 = sg * (p.w * Ry - p.z * Rz);
+    if (E0 < -t.x || E1 < -t.y || E2 < -t.z) return 0;
+    const bool acc = fabsf(t.w) == 1.0f;
+    return (acc && E0 >= t.x && E1 >= t.y && E2 >= t.z) ? 1 : 2;
+}
+
+// ---------------------------------------------------------------------------
 // small helpers
 
 __device__ __forceinline__ void load_face(const double *__restrict__ faces, int64_t f,

@@ -38,7 +38,16 @@ size_t bins_workspace_size(int64_t F, int nlim, int64_t n_bins);
 size_t assemble_workspace_size(int64_t pair_cap, int64_t n_bins);
 int build_bins_impl(const LevelInfo &li, int nlim, const double *faces, int64_t F, int mode,
                     int use_filter, vf_bins *bins, int32_t *d_status, void *ws, size_t ws_bytes,
-                    cudaStream_t st);
+                    cudaStream_t st, const uint16_t *ind_bits = nullptr);
+// 1D indicators of every level in one pass (bit L of out[f])
+struct LevelSet {
+    LevelInfo li[VF_MAX_LEVELS];
+    double inv_dx[VF_MAX_LEVELS];
+    int widen[VF_MAX_LEVELS];
+    int n;
+};
+int launch_indicators_all(const vf_config &cfg, const double *faces, int64_t F, uint16_t *out,
+                          cudaStream_t st);
 int sort_bins(int64_t n_bins, const int32_t *offsets, const int32_t *d_total, int32_t *counts,
               int32_t *face_ids, int32_t *large, int32_t *scalars, int32_t *scratch,
               cudaStream_t st);
@@ -57,6 +66,10 @@ size_t propagate_workspace_size(int32_t capacity);
 int propagate_impl(const LevelInfo &li, vf_grid *g, int L, int dir, int finalize, void *ws,
                    size_t ws_bytes, cudaStream_t st);
 int finalize_impl(vf_grid *g, int L, cudaStream_t st);
+// Alg. 5 (+x, -x for L > 0) + finalize of one level, warp per block row
+size_t propagate_level_workspace_size(const vf_config &cfg, int L);
+int propagate_level_impl(const LevelInfo &li, vf_grid *g, int L, void *ws, size_t ws_bytes,
+                         cudaStream_t st);
 int shard_zero_impl(const LevelInfo &li, vf_grid *g, int L, int32_t *bcount, cudaStream_t st);
 
 // forest

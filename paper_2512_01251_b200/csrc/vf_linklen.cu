@@ -39,6 +39,10 @@
 #include "vf_common.cuh"
 #include "vf_internal.h"
 
+#ifndef VF_LINK_MINB
+#define VF_LINK_MINB 6
+#endif
+
 namespace vf {
 
 // dense finest-level block -> LUT slot map; nothing is mapped when the
@@ -142,9 +146,9 @@ struct LinkDir {
 // pair) and their per-pair enumeration state
 struct LinkWarp {
     LinkDir d[32];
-    double fv[32][12];  // v1 v2 v3 n of the lane's face
-    float ff[32][12];   // nf, V1 = v2 - v1, V2 = v3 - v1 (FP32), Ef, pad
-    int lohi[32][6];    // fallback node range per axis
+    double fv[32][6];   // v1 and n of the lane's face (FP64)
+    float ff[32][10];   // nf, V1 = v2 - v1, V2 = v3 - v1 (FP32), Ef
+    short lohi[32][6];  // fallback node range per axis (cells <= 32767)
     int excl[32];       // exclusive prefix of the per-lane row counts
 };
 
@@ -161,7 +165,7 @@ __device__ __forceinline__ void link_fast(const LinkCtx &c, const double *fv, in
                                           int i, int j, int k, int32_t slot) {
     const double dx = c.dx;
     const double x = node_c(i, dx), y = node_c(j, dx), z = node_c(k, dx);
-    const double d = VF_DDIV(plane_num(fv, fv + 9, x, y, z), den);
+    const double d = VF_DDIV(plane_num(fv, fv + 3, x, y, z), den);
     const bool pos = d > 0.0;
     const double dd = pos ? d : -d;
     if (!(dd > 0.0 && dd <= dx)) return;
@@ -174,21 +178,35 @@ __device__ __forceinline__ void link_fast(const LinkCtx &c, const double *fv, in
               __float_as_uint(qv));
 }
 
+// |c| of the 13 representative directions: sqrt(1), sqrt(2), sqrt(3), the
+// correctly rounded doubles __dsqrt_rn produces (link_candidate's cn)
+__constant__ double c_cn[13] = {1.0, 1.0, 1.0, 1.4142135623730951, 1.4142135623730951,
+                                1.4142135623730951, 1.4142135623730951, 1.4142135623730951,
+                                1.4142135623730951, 1.7320508075688772, 1.7320508075688772,
+                                1.7320508075688772, 1.7320508075688772};
+
+// c_k n_k for c_k in {-1, 0, 1}: exactly DMUL(c_k, n_k) up to the sign of a
+// zero product, which cannot change a nonzero sum (a zero den is rejected)
+__device__ __forceinline__ double cmul(int ck, double nk) { return ck == 0 ? 0.0 : (ck > 0 ? nk : -nk); }
+
+// margin length |e| (approximate rsqrt: the margins carry a 10x safety factor)
+__device__ __forceinline__ float mlen(float a, float b) {
+    const float x = a * a + b * b;
+    return x > 0.0f ? x * rsqrtf(x) * 1.0001f : 0.0f;
+}
+
 // state of (lane's face, pair R); returns the number of lattice rows of the
 // projected bounding box (0: no link of this face in this pair)
 __device__ __forceinline__ int link_dir_setup(LinkDir &D, const LinkCtx &c, const double *v,
-                                              const float *ff, const int *lohi, int R, int p,
+                                              const float *ff, const short *lohi, int R, int p,
                                               int q1, int q2, int s1, int s2) {
-    const double *n = v + 9;
+    const double *n = v + 3;
     const float *nf = ff, *V1 = ff + 3, *V2 = ff + 6;
     const int cx = c_rep[R][0], cy = c_rep[R][1], cz = c_rep[R][2];
     // exact den / EPS_PARALLEL (link_candidate): a face parallel to c has no
     // link in this direction pair at all
-    const double c0 = cx, c1 = cy, c2 = cz;
-    const double cn = __dsqrt_rn(VF_DADD(VF_DADD(VF_DMUL(c0, c0), VF_DMUL(c1, c1)), VF_DMUL(c2, c2)));
-    const double den = VF_DADD(VF_DADD(VF_DMUL(c0, n[0]), VF_DMUL(c1, n[1])), VF_DMUL(c2, n[2]));
-    if (fabs(den) < VF_DMUL(c.eps_par, cn)) return 0;
-    const float dn = (float)cx * nf[0] + (float)cy * nf[1] + (float)cz * nf[2];
+    const double den = VF_DADD(VF_DADD(cmul(cx, n[0]), cmul(cy, n[1])), cmul(cz, n[2]));
+    if (fabs(den) < VF_DMUL(c.eps_par, c_cn[R])) return 0;
     const double dx = c.dx;
     const float dxf = (float)dx;
     const float V1p = pick3(p, V1[0], V1[1], V1[2]), V2p = pick3(p, V2[0], V2[1], V2[2]);
@@ -196,21 +214,11 @@ __device__ __forceinline__ int link_dir_setup(LinkDir &D, const LinkCtx &c, cons
     const float P1b = pick3(q2, V1[0], V1[1], V1[2]) - (float)s2 * V1p;
     const float P2a = pick3(q1, V2[0], V2[1], V2[2]) - (float)s1 * V2p;
     const float P2b = pick3(q2, V2[0], V2[1], V2[2]) - (float)s2 * V2p;
-    const float cr = P1a * P2b - P1b * P2a;
     const float ext = fmaxf(fmaxf(fabsf(P1a), fabsf(P1b)), fmaxf(fabsf(P2a), fabsf(P2b)));
     // tolerance: eps-cube acceptance (<= 2 sqrt 6 eps after the oblique
     // projection) + FP32 error of coordinates of magnitude ext + dx, plus an
     // absolute term >= the FP32 rounding of E_k itself (sliver edges)
     const float tol = 1e-5f * (ext + dxf) + 6.0f * (float)c.eps;
-    const float ab = 4e-6f * (ext + dxf) * (ext + dxf);
-    const float e1a = P2a - P1a, e1b = P2b - P1b;
-    D.P1a = P1a; D.P1b = P1b; D.P2a = P2a; D.P2b = P2b;
-    D.t0 = tol * sqrtf(P1a * P1a + P1b * P1b) + ab;
-    D.t1 = tol * sqrtf(e1a * e1a + e1b * e1b) + ab;
-    D.t2 = tol * sqrtf(P2a * P2a + P2b * P2b) + ab;
-    // (a degenerate projection -- face parallel to c -- keeps only lattice
-    // points within tol of the projected segment: the edge tests stay valid)
-    D.sg = cr >= 0.0f ? 1.0f : -1.0f;
     const double vp = pick3(p, v[0], v[1], v[2]);
     // lattice of line traces: coordinate j of the trace of the line through
     // node (i_p, i_q1, i_q2) is ((i_qj - s_j i_p) + delta_j) dx + s_j v1_p,
@@ -223,15 +231,26 @@ __device__ __forceinline__ int link_dir_setup(LinkDir &D, const LinkCtx &c, cons
     const double inv = c.inv_dx;
     const int m1a = (int)ceil(((double)bmin1 - off1) * inv - d1 - 1e-6);
     const int m1b = (int)floor(((double)bmax1 - off1) * inv - d1 + 1e-6);
+    if (m1b < m1a) return 0;
     const int m2a = (int)ceil(((double)bmin2 - off2) * inv - d2 - 1e-6);
     const int m2b = (int)floor(((double)bmax2 - off2) * inv - d2 + 1e-6);
-    if (m1b < m1a || m2b < m2a) return 0;
+    if (m2b < m2a) return 0;
+    // (a degenerate projection -- face parallel to c -- keeps only lattice
+    // points within tol of the projected segment: the edge tests stay valid)
+    const float cr = P1a * P2b - P1b * P2a;
+    const float ab = 4e-6f * (ext + dxf) * (ext + dxf);
+    D.P1a = P1a; D.P1b = P1b; D.P2a = P2a; D.P2b = P2b;
+    D.t0 = tol * mlen(P1a, P1b) + ab;
+    D.t1 = tol * mlen(P2a - P1a, P2b - P1b) + ab;
+    D.t2 = tol * mlen(P2a, P2b) + ab;
+    D.sg = cr >= 0.0f ? 1.0f : -1.0f;
+    const float dn = (float)cx * nf[0] + (float)cy * nf[1] + (float)cz * nf[2];
     const bool steep = fabsf(dn) >= 1e-3f;
     D.off1 = off1; D.off2 = off2; D.vp = vp; D.den = den;
     D.nq1 = pick3(q1, nf[0], nf[1], nf[2]);
     D.nq2 = pick3(q2, nf[0], nf[1], nf[2]);
     D.dn = steep ? dn : 0.0f;  // 0: ill-conditioned crossing, full node range
-    D.wid0 = dxf * (1.0f + 1e-4f) + 1e-5f * dxf + ff[9] / fabsf(dn);
+    D.wid0 = steep ? dxf * (1.0f + 1e-4f) + 1e-5f * dxf + __fdividef(ff[9], fabsf(dn)) * 1.0001f : 0.0f;
     D.m1a = m1a; D.m1b = m1b; D.m2a = m2a;
     D.lop = pick3(p, lohi[0], lohi[1], lohi[2]);
     D.hip = pick3(p, lohi[3], lohi[4], lohi[5]);
@@ -272,9 +291,9 @@ __device__ __forceinline__ void link_point(const LinkCtx &c, const LinkDir &D, c
     // points Q + lam c; n.(Q + lam c - v1) = 0
     int ip_lo = D.lop, ip_hi = D.hip;
     if (D.dn != 0.0f) {
-        const float lam = -(D.nq1 * Ra + D.nq2 * Rb) / D.dn;
+        const float lam = -__fdividef(D.nq1 * Ra + D.nq2 * Rb, D.dn);
         const float xs = (float)cp * lam;  // x_p* - v1_p
-        const float wid = D.wid0 + 1e-6f * fabsf(xs) / fabsf(D.dn);
+        const float wid = D.wid0 + 1.0001e-6f * __fdividef(fabsf(xs), fabsf(D.dn));
         // node index i_p with |x_p* - (i_p + 0.5) dx| <= dx
         ip_lo = max((int)ceil(((double)(xs - wid) + D.vp) * c.inv_dx - 0.5), ip_lo);
         ip_hi = min((int)floor(((double)(xs + wid) + D.vp) * c.inv_dx - 0.5), ip_hi);
@@ -323,7 +342,7 @@ __device__ __forceinline__ void link_row(const LinkCtx &c, const LinkDir &D, con
             if (a == 0.0f && be[k] < -tk[k] - 1e-5f * (M + tk[k])) return;
             continue;
         }
-        const float b = rhs / a;
+        const float b = __fdividef(rhs, a);  // ~2 ulp: the bound is padded by a lattice step
         if (a > 0.0f) lo = fmaxf(lo, b);
         else hi = fminf(hi, b);
     }
@@ -342,7 +361,7 @@ constexpr size_t kLinkSmem = kLinkWarps * sizeof(LinkWarp);
 // case it redoes every face with every undecided candidate decided inline
 // (atomicMin is idempotent, so re-merging the fast results is harmless).
 template <bool FULL>
-__global__ void __launch_bounds__(kLinkWarps * 32, FULL ? 1 : 6)
+__global__ void __launch_bounds__(kLinkWarps * 32, FULL ? 1 : VF_LINK_MINB)
     k_links(LinkCtx c, int widen, int64_t F, const int32_t *__restrict__ map,
             const int32_t *__restrict__ d_n_map) {
     if (FULL && c.n_band[1] == 0) return;
@@ -367,9 +386,7 @@ __global__ void __launch_bounds__(kLinkWarps * 32, FULL ? 1 : 6)
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
                 W.fv[lane][d] = v[d];
-                W.fv[lane][3 + d] = v[3 + d];
-                W.fv[lane][6 + d] = v[6 + d];
-                W.fv[lane][9 + d] = nn[d];
+                W.fv[lane][3 + d] = nn[d];
                 W.ff[lane][d] = (float)nn[d];
                 W.ff[lane][3 + d] = (float)(v[3 + d] - v[d]);
                 W.ff[lane][6 + d] = (float)(v[6 + d] - v[d]);
@@ -377,11 +394,12 @@ __global__ void __launch_bounds__(kLinkWarps * 32, FULL ? 1 : 6)
                 const double fhi = fmax(fmax(v[d], v[3 + d]), v[6 + d]);
                 ext = fmax(ext, fhi - flo);
                 // nodes within one link of the face AABB (fallback range)
-                W.lohi[lane][d] = max((int)floor((flo - c.dx - 2.0 * c.eps) * c.inv_dx - 0.5) - widen, 0);
+                W.lohi[lane][d] = (short)max((int)floor((flo - c.dx - 2.0 * c.eps) * c.inv_dx - 0.5) - widen, 0);
                 W.lohi[lane][3 + d] =
-                    min((int)floor((fhi + c.dx + 2.0 * c.eps) * c.inv_dx - 0.5) + 1 + widen, c.cells[d] - 1);
+                    (short)min((int)floor((fhi + c.dx + 2.0 * c.eps) * c.inv_dx - 0.5) + 1 + widen, c.cells[d] - 1);
             }
             W.ff[lane][9] = 4e-6f * (float)(ext + 2.0 * c.dx);
+
         }
         __syncwarp();
 #pragma unroll 1

@@ -30,55 +30,8 @@ namespace vf {
 struct VoxFace {        // shared-memory face record (24 doubles + FP32 row classifier)
     SatFace s;
     double n[3];
-    float4 yz;          // yz projection of v2 - v1, v3 - v1 (FP32)
-    float4 tol;         // per-edge margins t0, t1, t2 and the orientation sign
+    RowClass rc;
 };
-
-// FP32 row classifier (exactness argument in row_class): 0 = the x-row misses
-// the face, 1 = it pierces the face interior, 2 = undecided (exact SAT).
-// The row box [0, lx] x [y +- eps] x [z +- eps] overlaps the face iff the
-// point (y, z) is within the eps-square of the face's yz projection (the
-// other SAT axes follow from the x-extent, see below).  Edge functions are
-// evaluated relative to v1 with margins t_k = tol |e_k| + 4e-6 (ext + dx)^2,
-// tol = 1e-5 (ext + dx) + 6 eps: >= 10x the FP32 error of E_k plus the
-// eps-square reach:
-//   E_k < -t_k for some k: the row box misses the triangle by > tol - 2 eps,
-//     the exact predicate is false with a gap >> the FP64 rounding of the
-//     reference SAT, which therefore rejects;
-//   E_k >= t_k for all k, |n_x| >= 1e-3 and the face's x-range inside
-//     (tol_x, lx - tol_x): the row pierces the face interior at a point of the
-//     box, every one of the 13 SAT axes has slack >> FP64 rounding, and the
-//     reference SAT (geometry.py:441-500) accepts.
-__device__ __forceinline__ void row_class_init(VoxFace &F, const double *v, const double *n,
-                                               double dx, double eps, double lx) {
-    const float a1 = (float)(v[4] - v[1]), b1 = (float)(v[5] - v[2]);
-    const float a2 = (float)(v[7] - v[1]), b2 = (float)(v[8] - v[2]);
-    const float cr = a1 * b2 - b1 * a2;
-    const float ext = fmaxf(fmaxf(fabsf(a1), fabsf(b1)), fmaxf(fabsf(a2), fabsf(b2)));
-    const float tol = 1e-5f * (ext + (float)dx) + 6.0f * (float)eps;
-    const float e1a = a2 - a1, e1b = b2 - b1;
-    float sg = cr >= 0.0f ? 1.0f : -1.0f;
-    const double tx = 1e-6 * lx;
-    // no fast accept: ill-conditioned x crossing or face near the domain x ends
-    const bool acc = fabs(n[0]) >= 1e-3 && F.s.lo[0] > tx && F.s.hi[0] < lx - tx && cr != 0.0f;
-    F.yz = make_float4(a1, b1, a2, b2);
-    // + an absolute term >= the FP32 rounding of E_k itself (edge vectors
-    // and offsets of magnitude <= 2 ext + dx; matters for sliver edges)
-    const float ab = 4e-6f * (ext + (float)dx) * (ext + (float)dx);
-    F.tol = make_float4(tol * sqrtf(a1 * a1 + b1 * b1) + ab, tol * sqrtf(e1a * e1a + e1b * e1b) + ab,
-                        tol * sqrtf(a2 * a2 + b2 * b2) + ab, acc ? sg : 2.0f * sg);
-}
-
-__device__ __forceinline__ int row_class(const VoxFace &F, float Ry, float Rz) {
-    const float4 p = F.yz, t = F.tol;
-    const float sg = t.w > 0.0f ? 1.0f : -1.0f;
-    const float E0 = sg * (p.x * Rz - p.y * Ry);
-    const float E1 = sg * ((p.z - p.x) * (Rz - p.y) - (p.w - p.y) * (Ry - p.x));
-    const float E2 = sg * (p.w * Ry - p.z * Rz);
-    if (E0 < -t.x || E1 < -t.y || E2 < -t.z) return 0;
-    const bool acc = fabsf(t.w) == 1.0f;
-    return (acc && E0 >= t.x && E1 >= t.y && E2 >= t.z) ? 1 : 2;
-}
 
 constexpr int kVoxWarps = 4;
 
@@ -142,7 +95,7 @@ __global__ void __launch_bounds__(kVoxWarps * 32)
                 VoxFace &vf_ = s_face[wib][lane];
                 sat_face_init(vf_.s, v);
                 vf_.n[0] = nn[0]; vf_.n[1] = nn[1]; vf_.n[2] = nn[2];
-                row_class_init(vf_, v, nn, dx, eps, lx);
+                row_class_init(vf_.rc, vf_.s, nn, dx, eps, lx);
                 s_skip[wib][lane] = fabs(nn[0]) < li.eps_par;  // A7: no x distance
             }
             __syncwarp();
@@ -152,7 +105,7 @@ __global__ void __launch_bounds__(kVoxWarps * 32)
                 // exact box-axis reject first (most pairs), then the FP32
                 // classifier; only undecided rows run the FP64 SAT
                 if (F.s.hi[1] < my || My < F.s.lo[1] || F.s.hi[2] < mz || Mz < F.s.lo[2]) continue;
-                const int cls = row_class(F, (float)VF_DSUB(y, F.s.v[1]), (float)VF_DSUB(z, F.s.v[2]));
+                const int cls = row_class(F.rc, (float)VF_DSUB(y, F.s.v[1]), (float)VF_DSUB(z, F.s.v[2]));
                 if (cls == 0) continue;
                 if (cls == 2 && !sat_exact(F.s, 0.0, my, mz, lx, My, Mz)) continue;
                 const double nx = F.n[0];
@@ -356,6 +309,158 @@ __global__ void __launch_bounds__(256)
         finalize_block(w, changed, bflags, solid64, b);
         if (changed) store_masks64(masks, b, w);
     }
+}
+
+// --------------------------------------------------------------------------
+// K-xrows: Alg. 5 in both directions + finalize as ONE kernel per level.
+//
+// A dense map of the level's blocks (B_L^3 ids, -1 = no level-L block) turns
+// every x-row of blocks into a contiguous array, so one warp owns one row
+// (j, k) and reads its positions 32 at a time (coalesced) instead of walking
+// the neighbour chain (the paper's sequential walk) or pointer-jumping over
+// it (k_xfun/k_xjump/k_xapply: 2 + ceil(log2 B_L) launches per direction).
+// Per chunk: transfer functions of the 32 blocks, a warp segmented scan with
+// compose() (segments start at run starts, which carry f_b(sigma), and at
+// lane 0, which folds in the status leaving the previous chunk), the status
+// entering each block = the scan value of its predecessor, then the fill /
+// finalize of that block.  The -x pass re-reads the +x results of the same
+// row (same warp, ordered by __syncwarp).  Identical results to the
+// pointer-jumping operators (same f_b, same composition, same apply).
+
+__global__ void k_level_map(int L, LevelInfo li, const int32_t *__restrict__ level_start,
+                            const int32_t *__restrict__ coords, int32_t *__restrict__ map) {
+    const int32_t s = level_start[L], e = level_start[L + 1];
+    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int4 c = reinterpret_cast<const int4 *>(coords)[b];
+        map[c.x + (int64_t)li.bins[0] * (c.y + (int64_t)li.bins[1] * c.z)] = (int32_t)b;
+    }
+}
+
+// one direction over one row; returns nothing, masks updated in place
+template <int DIR>
+__device__ __forceinline__ void xrow_pass(int L, int lane, const int32_t *__restrict__ row, int bx,
+                                          const int32_t *__restrict__ nbr, uint8_t *__restrict__ masks,
+                                          bool finalize, uint8_t *__restrict__ bflags,
+                                          uint64_t *__restrict__ solid64) {
+    constexpr int back = DIR > 0 ? 2 : 1, trail = DIR > 0 ? 3 : 0;
+    uint32_t carry = 0;        // status leaving the last block of the previous chunk
+    bool prev_present = false;  // ... and whether that position holds a level-L block
+    for (int x0 = 0; x0 < bx; x0 += 32) {
+        const int x = DIR > 0 ? x0 + lane : bx - 1 - (x0 + lane);
+        const int32_t id = (x0 + lane < bx) ? row[x] : -1;
+        const bool present = id >= 0;
+        const uint32_t pm = __ballot_sync(0xffffffffu, present);
+        if (pm == 0) {
+            prev_present = false;
+            continue;
+        }
+        const bool pred = lane > 0 ? ((pm >> (lane - 1)) & 1u) : prev_present;
+        uint32_t w[16];
+        uint32_t fn = 0;
+        bool head = true;
+        if (present) {
+            load_masks64(masks, id, w);
+            uint32_t A = 0, B = 0;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const uint32_t h3 = (w[r] >> (8 * trail)) & 0xffu;
+                A |= (uint32_t)(h3 != VF_GUARD) << r;
+                B |= (uint32_t)(h3 == VF_SOLID) << r;
+            }
+            fn = A | (B << 16);
+            if (!pred) {  // run start: back neighbour is not a level-L block
+                const int32_t code = nbr[27 * (int64_t)id + back];
+                const uint32_t c = (code == VF_NB_SOLID_NBR) ? A : B;  // f_b(sigma)
+                fn = c | (c << 16);
+            } else if (lane == 0) {  // continue the previous chunk's run
+                fn = compose(fn, carry | (carry << 16));
+            } else {
+                head = false;
+            }
+        }
+        // segmented inclusive scan (compose) across the warp
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t g = __shfl_up_sync(0xffffffffu, fn, o);
+            const int hd = __shfl_up_sync(0xffffffffu, (int)head, o);
+            if (lane >= o && !head) {
+                fn = compose(fn, g);
+                head = hd;
+            }
+        }
+        const uint32_t out = fn & 0xffffu;  // constant: status leaving this block
+        uint32_t st = __shfl_up_sync(0xffffffffu, out, 1);
+        if (lane == 0) st = carry;
+        if (present) {
+            bool changed = false;
+            if (pred) {
+#pragma unroll
+                for (int r = 0; r < 16; ++r) {
+                    uint32_t xw = w[r];
+#pragma unroll
+                    for (int I = 0; I < 4; ++I) {
+                        const uint32_t h = (xw >> (8 * I)) & 0xffu;
+                        uint32_t hn = h;
+                        if ((st >> r & 1u) && h != VF_GUARD) hn = VF_SOLID;
+                        if (L == 0 && hn == VF_GUARD) hn = VF_FLUID;
+                        xw = (xw & ~(0xffu << (8 * I))) | (hn << (8 * I));
+                    }
+                    changed |= (xw != w[r]);
+                    w[r] = xw;
+                }
+            }
+            if (finalize) finalize_block(w, changed, bflags, solid64, id);
+            if (changed) store_masks64(masks, id, w);
+        }
+        carry = __shfl_sync(0xffffffffu, out, 31);
+        prev_present = (pm >> 31) & 1u;
+    }
+}
+
+constexpr int kXrowWarps = 8;
+
+__global__ void __launch_bounds__(kXrowWarps * 32)
+    k_xrows(LevelInfo li, int L, const int32_t *__restrict__ map, const int32_t *__restrict__ nbr,
+            uint8_t *__restrict__ masks, uint8_t *__restrict__ bflags,
+            uint64_t *__restrict__ solid64) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (int64_t)blockIdx.x * kXrowWarps + (threadIdx.x >> 5);
+    const int64_t nw = (int64_t)gridDim.x * kXrowWarps;
+    const int bx = li.bins[0], by = li.bins[1];
+    const int64_t rows = (int64_t)by * li.bins[2];
+    for (int64_t r = gw; r < rows; r += nw) {
+        const int j = (int)(r % by), k = (int)(r / by);
+        if (!owns_row(li, j, k)) continue;  // multi-GPU: rows of other ranks
+        const int32_t *row = map + r * bx;
+        xrow_pass<+1>(L, lane, row, bx, nbr, masks, L == 0, bflags, solid64);
+        if (L > 0) {
+            __syncwarp();
+            xrow_pass<-1>(L, lane, row, bx, nbr, masks, true, bflags, solid64);
+        }
+    }
+}
+
+size_t propagate_level_workspace_size(const vf_config &cfg, int L) {
+    const int64_t nb = (int64_t)(cfg.nb[0] << L) * (cfg.nb[1] << L) * (cfg.nb[2] << L);
+    return ((size_t)nb * sizeof(int32_t) + 255) & ~(size_t)255;
+}
+
+int propagate_level_impl(const LevelInfo &li, vf_grid *g, int L, void *ws, size_t ws_bytes,
+                         cudaStream_t st) {
+    const int64_t nb = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
+    if (ws_bytes < (size_t)nb * sizeof(int32_t)) return set_error(VF_EARG, "propagate workspace too small");
+    int32_t *map = (int32_t *)ws;
+    cudaMemsetAsync(map, 0xff, sizeof(int32_t) * (size_t)nb, st);
+    k_level_map<<<max_ctas(8), 256, 0, st>>>(L, li, g->d_level_start, g->d_coords, map);
+    int rc = check_launch("k_level_map");
+    if (rc) return rc;
+    int64_t rows = (int64_t)li.bins[1] * li.bins[2];
+    int64_t grid = (rows + kXrowWarps - 1) / kXrowWarps;
+    if (grid > max_ctas(8)) grid = max_ctas(8);
+    k_xrows<<<(int)grid, kXrowWarps * 32, 0, st>>>(li, L, map, g->d_nbr, g->d_masks, g->d_bflags,
+                                                   g->d_solid64);
+    return check_launch("k_xrows");
 }
 
 // multi-GPU exchange: zero what this rank does not own on level L
