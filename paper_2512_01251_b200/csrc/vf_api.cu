@@ -371,7 +371,7 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     for (int L = 0; L < cfg->l_max; ++L) {
         const LevelInfo li = make_level(*cfg, L);
         VF_TRY(build_bins_impl(li, nlim_of(*cfg), faces, F, 0, use_filter, &w.bins, g->d_status,
-                               w.bins_ws, w.bins_ws_bytes, st, w.ind_bits));
+                               w.bins_ws, w.bins_ws_bytes, st, w.ind_bits, false));
         rec(events, n_ev, &k, st);  // bins done
         VF_TRY(voxelize_impl(li, g, L, &w.bins, faces, st));
         VF_TRY(propagate_level_impl(li, g, L, w.prop_ws, w.prop_b, st));

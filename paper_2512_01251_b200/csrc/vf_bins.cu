@@ -548,7 +548,7 @@ size_t bins_workspace_size(int64_t F, int nlim, int64_t n_bins) {
 // indicators -> compact -> pairs(+hist) -> offsets -> scatter -> sort
 int build_bins_impl(const LevelInfo &li, int nlim, const double *faces, int64_t F, int mode,
                     int use_filter, vf_bins *bins, int32_t *d_status, void *ws, size_t ws_bytes,
-                    cudaStream_t st, const uint16_t *ind_bits) {
+                    cudaStream_t st, const uint16_t *ind_bits, bool sorted) {
     const int64_t n_bins = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
     BinsWs w;
     if (bins_ws_layout(F, nlim, n_bins, (char *)ws, &w) > ws_bytes)
@@ -581,6 +581,10 @@ int build_bins_impl(const LevelInfo &li, int nlim, const double *faces, int64_t 
         nlim, map, d_n_map, F, w.slots, w.slot_cnt, bins->d_offsets, bins->d_counts,
         bins->d_face_ids, bins->face_ids_cap, d_status);
     if ((rc = check_launch("k_scatter_slots"))) return rc;
+    // unsorted (embed): the voxelizer tie-breaks on face ids and derives the
+    // slice lengths from the offsets, so neither the per-bin order nor the
+    // counts (used as scatter cursors) need restoring
+    if (!sorted) return VF_OK;
     return sort_bins(n_bins, bins->d_offsets, bins->d_n_face_ids, bins->d_counts, bins->d_face_ids,
                      w.large, w.scalars, w.slots, st);
 }

@@ -237,7 +237,14 @@ __device__ __forceinline__ uint32_t octant_bits(uint32_t bits, int) {
     return g;
 }
 
-// one thread per child: coords, 27 links, ghost layer
+// Children of the level's marked parents, CTA-cooperative: a CTA takes 64
+// consecutive children (8 parents), the (child, slot) pairs of the batch are
+// spread over the threads so the 27-int neighbour rows of the batch (6.9 KB,
+// contiguous) are written coalesced; the per-child MISSING/SOLID_NBR
+// direction bits are OR-ed in shared memory; then one thread per child writes
+// coords / flags / the A14 ghost-layer cell masks (16 B stores, coalesced).
+constexpr int kAdaptBatch = 64;
+
 __global__ void __launch_bounds__(256)
     k_adapt_children(int L, int32_t capacity, int nbx1, int nby1, int nbz1,
                      const int32_t *__restrict__ level_start, const int32_t *__restrict__ n_marked,
@@ -246,19 +253,28 @@ __global__ void __launch_bounds__(256)
                      int32_t *__restrict__ child, uint8_t *__restrict__ bflags,
                      uint8_t *__restrict__ masks, int32_t *__restrict__ status,
                      uint64_t *__restrict__ solid64) {
+    __shared__ uint32_t s_missing[kAdaptBatch];
+    __shared__ int4 s_pc[kAdaptBatch / 8];
+    __shared__ int32_t s_P[kAdaptBatch / 8];
     const int64_t e = level_start[L + 1];
     const int64_t nc = 8 * (int64_t)(*n_marked);
-    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc;
-         c += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t id = e + c;
-        if (id >= capacity) continue;
-        const int32_t P = parents[c >> 3];
-        const int cc = (int)(c & 7);
-        const int4 pc = reinterpret_cast<const int4 *>(coords)[P];
-        const int ci = 2 * pc.x + (cc & 1), cj = 2 * pc.y + ((cc >> 1) & 1), ck = 2 * pc.z + (cc >> 2);
-        reinterpret_cast<int4 *>(coords)[id] = make_int4(ci, cj, ck, L + 1);
-        uint32_t missing = 0;  // bit dir_code(q): slot q is MISSING / SOLID_NBR
-        for (int q = 0; q < 27; ++q) {
+    for (int64_t c0 = (int64_t)blockIdx.x * kAdaptBatch; c0 < nc; c0 += (int64_t)gridDim.x * kAdaptBatch) {
+        const int nb = (int)min((int64_t)kAdaptBatch, nc - c0);
+        if (threadIdx.x < kAdaptBatch) s_missing[threadIdx.x] = 0;
+        if (threadIdx.x < kAdaptBatch / 8 && 8 * (int)threadIdx.x < nb) {
+            const int32_t P = parents[(c0 >> 3) + threadIdx.x];
+            s_P[threadIdx.x] = P;
+            s_pc[threadIdx.x] = reinterpret_cast<const int4 *>(coords)[P];
+        }
+        __syncthreads();
+        for (int it = threadIdx.x; it < nb * 27; it += blockDim.x) {
+            const int lc = it / 27, q = it - 27 * lc;
+            const int64_t id = e + c0 + lc;
+            if (id >= capacity) continue;
+            const int32_t P = s_P[lc >> 3];
+            const int4 pc = s_pc[lc >> 3];
+            const int cc = lc & 7;
+            const int ci = 2 * pc.x + (cc & 1), cj = 2 * pc.y + ((cc >> 1) & 1), ck = 2 * pc.z + (cc >> 2);
             const int ti = ci + c27(q, 0), tj = cj + c27(q, 1), tk = ck + c27(q, 2);
             int32_t v;
             if (ti < 0 || tj < 0 || tk < 0 || ti >= nbx1 || tj >= nby1 || tk >= nbz1) {
@@ -279,52 +295,78 @@ __global__ void __launch_bounds__(256)
             }
             nbr[27 * id + q] = v;
             nbr_child[27 * id + q] = -1;
-            if (v == VF_NB_MISSING || v == VF_NB_SOLID_NBR) missing |= 1u << dir_code_of_slot(q);
+            if (v == VF_NB_MISSING || v == VF_NB_SOLID_NBR)
+                atomicOr(&s_missing[lc], 1u << dir_code_of_slot(q));
         }
-        child[id] = -1;
-        bflags[id] = 0;
-        solid64[id] = 0;
-        // A14 ghost layer: a cell is within Chebyshev distance 2 (fine cells) of
-        // a missing neighbour block iff one of the 7 blocks towards its octant
-        // is missing, so 8 octant bits decide all 64 cells.
-        const uint32_t g8 = octant_bits(missing, 2);
-        uint32_t w[16];
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const int J = r & 3, K = r >> 2;
-            uint32_t x = 0;
-#pragma unroll
-            for (int I = 0; I < 4; ++I) {
-                const int o = (I >= 2) | ((J >= 2) << 1) | ((K >= 2) << 2);
-                x |= (uint32_t)((g8 >> o & 1u) ? VF_GHOST : VF_FLUID) << (8 * I);
+        __syncthreads();
+        // per child: metadata; masks as 4 x 16 B per child (4 threads per child)
+        for (int it = threadIdx.x; it < nb * 4; it += blockDim.x) {
+            const int lc = it >> 2, part = it & 3;
+            const int64_t id = e + c0 + lc;
+            if (id >= capacity) continue;
+            if (part == 0) {
+                const int4 pc = s_pc[lc >> 3];
+                const int cc = lc & 7;
+                reinterpret_cast<int4 *>(coords)[id] =
+                    make_int4(2 * pc.x + (cc & 1), 2 * pc.y + ((cc >> 1) & 1), 2 * pc.z + (cc >> 2), L + 1);
+                child[id] = -1;
+                bflags[id] = 0;
+                solid64[id] = 0;
             }
-            w[r] = x;
-        }
-        uint4 *m = reinterpret_cast<uint4 *>(masks + 64 * id);
+            // A14 ghost layer: a cell is within Chebyshev distance 2 (fine
+            // cells) of a missing neighbour block iff one of the 7 blocks
+            // towards its octant is missing, so 8 octant bits decide all 64 cells
+            const uint32_t g8 = octant_bits(s_missing[lc], 2);
+            uint32_t w[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) m[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+            for (int rr = 0; rr < 4; ++rr) {
+                const int r = 4 * part + rr;
+                const int J = r & 3, K = r >> 2;
+                uint32_t x = 0;
+#pragma unroll
+                for (int I = 0; I < 4; ++I) {
+                    const int o = (I >= 2) | ((J >= 2) << 1) | ((K >= 2) << 2);
+                    x |= (uint32_t)((g8 >> o & 1u) ? VF_GHOST : VF_FLUID) << (8 * I);
+                }
+                w[rr] = x;
+            }
+            reinterpret_cast<uint4 *>(masks + 64 * id)[part] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        __syncthreads();
     }
 }
 
-// level-L neighbour-child links + interface layer of refined blocks (A14)
+// level-L neighbour-child links + interface layer of refined blocks (A14).
+// (block, slot) pairs spread over a CTA (coalesced nbr_child rows), the
+// per-block "existing unrefined neighbour" bits OR-ed in shared memory, then
+// the interface cells of refined blocks, one 32-bit mask row per thread.
+constexpr int kLevelBatch = 64;
+
 __global__ void __launch_bounds__(256)
     k_adapt_level(int L, const int32_t *__restrict__ level_start, const int32_t *__restrict__ nbr,
                   int32_t *__restrict__ nbr_child, const int32_t *__restrict__ child,
                   uint8_t *__restrict__ masks) {
+    __shared__ uint32_t s_coarse[kLevelBatch];
     const int32_t s = level_start[L], e = level_start[L + 1];
-    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
-         b += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t *nb = nbr + 27 * b;
-        uint32_t coarse = 0;  // bit dir_code(q): existing unrefined neighbour
-        for (int q = 0; q < 27; ++q) {
-            const int32_t v = (q == 0) ? (int32_t)b : nb[q];
+    for (int64_t b0 = s + (int64_t)blockIdx.x * kLevelBatch; b0 < e; b0 += (int64_t)gridDim.x * kLevelBatch) {
+        const int nb = (int)min((int64_t)kLevelBatch, (int64_t)e - b0);
+        if (threadIdx.x < kLevelBatch) s_coarse[threadIdx.x] = 0;
+        __syncthreads();
+        for (int it = threadIdx.x; it < nb * 27; it += blockDim.x) {
+            const int lb = it / 27, q = it - 27 * lb;
+            const int64_t b = b0 + lb;
+            const int32_t v = (q == 0) ? (int32_t)b : nbr[27 * b + q];
             const int32_t ch = (v >= 0) ? child[v] : -1;
             nbr_child[27 * b + q] = ch;
-            if (q > 0 && v >= 0 && ch < 0) coarse |= 1u << dir_code_of_slot(q);
+            if (q > 0 && v >= 0 && ch < 0) atomicOr(&s_coarse[lb], 1u << dir_code_of_slot(q));
         }
-        if (child[b] < 0 || !coarse) continue;
-        uint32_t *m = reinterpret_cast<uint32_t *>(masks + 64 * b);
-        for (int r = 0; r < 16; ++r) {
+        __syncthreads();
+        for (int it = threadIdx.x; it < nb * 16; it += blockDim.x) {
+            const int lb = it >> 4, r = it & 15;
+            const int64_t b = b0 + lb;
+            const uint32_t coarse = s_coarse[lb];
+            if (!coarse || child[b] < 0) continue;
+            uint32_t *m = reinterpret_cast<uint32_t *>(masks + 64 * b);
             const int J = r & 3, K = r >> 2;
             uint32_t x = m[r];
             const uint32_t x0 = x;
@@ -335,11 +377,11 @@ __global__ void __launch_bounds__(256)
                 const int ex = I == 0 ? -1 : (I == 3 ? 1 : 0);
                 const int ey = J == 0 ? -1 : (J == 3 ? 1 : 0);
                 const int ez = K == 0 ? -1 : (K == 3 ? 1 : 0);
-                const bool itf = touches(coarse, ex, ey, ez);
-                if (itf) x = (x & ~(0xffu << (8 * I))) | ((uint32_t)VF_INTERFACE << (8 * I));
+                if (touches(coarse, ex, ey, ez)) x = (x & ~(0xffu << (8 * I))) | ((uint32_t)VF_INTERFACE << (8 * I));
             }
             if (x != x0) m[r] = x;
         }
+        __syncthreads();
     }
 }
 

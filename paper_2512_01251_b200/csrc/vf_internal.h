@@ -38,7 +38,7 @@ size_t bins_workspace_size(int64_t F, int nlim, int64_t n_bins);
 size_t assemble_workspace_size(int64_t pair_cap, int64_t n_bins);
 int build_bins_impl(const LevelInfo &li, int nlim, const double *faces, int64_t F, int mode,
                     int use_filter, vf_bins *bins, int32_t *d_status, void *ws, size_t ws_bytes,
-                    cudaStream_t st, const uint16_t *ind_bits = nullptr);
+                    cudaStream_t st, const uint16_t *ind_bits = nullptr, bool sorted = true);
 // 1D indicators of every level in one pass (bit L of out[f])
 struct LevelSet {
     LevelInfo li[VF_MAX_LEVELS];

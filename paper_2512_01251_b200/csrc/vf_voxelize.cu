@@ -38,10 +38,13 @@ constexpr int kVoxWarps = 4;
 __global__ void __launch_bounds__(kVoxWarps * 32)
     k_voxelize(LevelInfo li, int L, const int32_t *__restrict__ level_start,
                const int32_t *__restrict__ coords, uint8_t *__restrict__ masks,
-               const int32_t *__restrict__ counts, const int32_t *__restrict__ offsets,
+               const int32_t *__restrict__ offsets, const int32_t *__restrict__ d_total,
                const int32_t *__restrict__ face_ids, const double *__restrict__ faces) {
     __shared__ VoxFace s_face[kVoxWarps][32];
     __shared__ uint8_t s_skip[kVoxWarps][32];
+    __shared__ int32_t s_fid[kVoxWarps][32];
+    const int64_t n_bins = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
+    const int32_t total = *d_total;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t gw = (int64_t)blockIdx.x * kVoxWarps + wib, nw = (int64_t)gridDim.x * kVoxWarps;
     const int32_t s = level_start[L], e = level_start[L + 1];
@@ -62,8 +65,10 @@ __global__ void __launch_bounds__(kVoxWarps * 32)
       if (bl < e) {
           co_l = *reinterpret_cast<const int4 *>(coords + 4 * bl);
           const int64_t bin_l = co_l.x + (int64_t)li.bins[0] * (co_l.y + (int64_t)li.bins[1] * co_l.z);
-          nf_l = counts[bin_l];
-          if (nf_l) off_l = offsets[bin_l];
+          // bin slice [offsets[bin], offsets[bin+1]) -- counts are not read, so
+          // the embed can skip restoring them after the counting-sort scatter
+          off_l = offsets[bin_l];
+          nf_l = (bin_l + 1 < n_bins ? offsets[bin_l + 1] : total) - off_l;
       }
       uint32_t todo = __ballot_sync(0xffffffffu, nf_l > 0);
       while (todo) {
@@ -90,6 +95,7 @@ __global__ void __launch_bounds__(kVoxWarps * 32)
             const int cnt = min(32, n_f - base);
             if (lane < cnt) {
                 const int64_t f = face_ids[off + base + lane];
+                s_fid[wib][lane] = (int32_t)f;
                 double v[9], nn[3];
                 load_face(faces, f, v, nn);
                 VoxFace &vf_ = s_face[wib][lane];
@@ -113,9 +119,11 @@ __global__ void __launch_bounds__(kVoxWarps * 32)
                 for (int I = 0; I < 4; ++I) {
                     const double d = VF_DDIV(plane_num(F.s.v, F.n, x[I], y, z), nx);
                     const double ad = fabs(d);
-                    if (ad < bd[I]) {  // strict: earlier (lower id) face wins ties
+                    // A7: smaller |d|, ties -> lower face id (bins need not be sorted)
+                    const int fid = s_fid[wib][q];
+                    if (ad < bd[I] || (ad == bd[I] && fid < bp[I])) {
                         bd[I] = ad;
-                        bp[I] = base + q;
+                        bp[I] = fid;
                         const uint32_t hv = (VF_DMUL(nx, d) > 0.0) ? VF_SOLID : VF_GUARD;
                         bh = (bh & ~(0xffu << (8 * I))) | (hv << (8 * I));
                     }
@@ -160,7 +168,7 @@ __global__ void __launch_bounds__(kVoxWarps * 32)
 int voxelize_impl(const LevelInfo &li, vf_grid *g, int L, const vf_bins *bins,
                   const double *faces, cudaStream_t st) {
     k_voxelize<<<max_ctas(8), kVoxWarps * 32, 0, st>>>(li, L, g->d_level_start, g->d_coords,
-                                                      g->d_masks, bins->d_counts, bins->d_offsets,
+                                                      g->d_masks, bins->d_offsets, bins->d_n_face_ids,
                                                       bins->d_face_ids, faces);
     return check_launch("k_voxelize");
 }
