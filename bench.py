@@ -108,6 +108,17 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_traffic(config, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed ncu --set full summary (profiles/ncu_traffic.json,
+    written by tools/ncu_traffic.py), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p)).get(config, {}).get(kernel)
+    return None if d is None else d.get("dram_bytes")
+
+
 def cpu_baseline(mesh, cfg, cells, repeat=1):
     from oracle import oracle as O
     O.build()
@@ -290,14 +301,19 @@ def main():
             link_ms.append(eng.link_kernel_ms())
         stages = {k: med([getattr(s, k) for s in stage]) for k in
                   ("binning", "voxelization", "refinement", "boundary", "links", "total")}
-        # dominant kernel k_links: algorithmic bytes per launch = face records
-        # (96 B/face) + LUT read-modify-write of the mapped blocks (2 x 6912 B)
-        link_bytes = F * 96 + n_b * 27 * 64 * 4 * 2
+        # dominant kernel k_links (the cut-link LUT):
+        # algorithmic bytes per launch = the face records read once (96 B/face)
+        # + the LUT of the mapped blocks written once (27 x 64 x 4 = 6912 B per
+        # boundary block); the -1 initialisation is the separate k_fill_lut.
+        link_bytes = F * 96 + n_b * 27 * 64 * 4
         lk = med(link_ms)
         achieved = link_bytes / (lk / 1e3) / 1e9
         roofline = {"kernel": "k_links", "bound": "hbm", "achieved": achieved, "peak": peak,
                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": None, "kernel_ms": lk, "algorithmic_bytes": int(link_bytes)}
+                    "traffic": ncu_traffic(args.config, "k_links"), "kernel_ms": lk,
+                    "algorithmic_bytes": int(link_bytes),
+                    "timed": "CUDA events on the engine stream around k_links + k_links_band + "
+                             "the overflow fallback (a no-op unless the band list overflowed)"}
     else:
         n_b = int(eng.lengths.shape[0]) if eng.lengths is not None else 0
 

@@ -18,85 +18,100 @@
 
 namespace vf {
 
-constexpr int kBndWarps = 8;
+// Bit-parallel 26-neighbour dilation of the SOLID cells.  A block's cells
+// are one 64-bit word (bit t = I + 4J + 16K, the finalize solid64 layout);
+// the 3x3x3 dilation is separable: D = Dz(Dy(Dx(S))) over the 27 blocks
+// around b -- Dx on the 9 block columns (oy, oz), Dy on the 3 planes oz, Dz
+// once -- with in-block shifts plus the facing layer of the neighbour block.
+// BOUNDARY = FLUID & D (a non-solid cell with >= 1 SOLID
+// same-level neighbour among the 26; only FLUID cells are re-marked).
+constexpr uint64_t kI0 = 0x1111111111111111ull, kI3 = 0x8888888888888888ull;
+constexpr uint64_t kJ0 = 0x000F000F000F000Full, kJ3 = 0xF000F000F000F000ull;
+constexpr uint64_t kK0 = 0x000000000000FFFFull, kK3 = 0xFFFF000000000000ull;
 
-// warp per finest-level block: the 27 neighbour ids decide candidacy (the
-// block or a neighbour is solid); a 6x6x6 shared-memory halo of SOLID bits is
-// gathered once, then every FLUID cell ORs its 26 halo neighbours (constant
-// offsets).  Reads of concurrently re-marked cells see FLUID or BOUNDARY,
-// both "not SOLID", so the fused single pass equals PAPER.md:941's two passes.
-__global__ void __launch_bounds__(kBndWarps * 32)
+__device__ __forceinline__ uint64_t dil_x(uint64_t lo, uint64_t c, uint64_t hi) {
+    return c | ((c << 1) & ~kI0) | ((c >> 1) & ~kI3) | ((lo & kI3) >> 3) | ((hi & kI0) << 3);
+}
+__device__ __forceinline__ uint64_t dil_y(uint64_t lo, uint64_t c, uint64_t hi) {
+    return c | ((c << 4) & ~kJ0) | ((c >> 4) & ~kJ3) | ((lo & kJ3) >> 12) | ((hi & kJ0) << 12);
+}
+__device__ __forceinline__ uint64_t dil_z(uint64_t lo, uint64_t c, uint64_t hi) {
+    return c | (c << 16) | (c >> 16) | ((lo & kK3) >> 48) | ((hi & kK0) << 48);
+}
+
+// thread per finest-level block: 27 solid64 words -> dilation -> FLUID cells
+// of the block's masks that the dilation covers become BOUNDARY
+__global__ void __launch_bounds__(256)
     k_boundary(LevelInfo li, int L, const int32_t *__restrict__ level_start,
                const int32_t *__restrict__ nbr, const int32_t *__restrict__ coords,
                uint8_t *__restrict__ bflags, uint8_t *__restrict__ masks,
                const uint64_t *__restrict__ solid64, int32_t *__restrict__ bcount) {
-    __shared__ uint8_t s_halo[kBndWarps][216];
-    __shared__ uint64_t s_sol[kBndWarps][27];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t gw = (int64_t)blockIdx.x * kBndWarps + w, nw = (int64_t)gridDim.x * kBndWarps;
     const int32_t s = level_start[L], e = level_start[L + 1];
-    for (int64_t b = s + gw; b < e; b += nw) {
+    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
+         b += (int64_t)gridDim.x * blockDim.x) {
         if (li.shard_count > 1) {  // multi-GPU: blocks of other ranks are theirs
             const int4 c = reinterpret_cast<const int4 *>(coords)[b];
             if (!owns_row(li, c.y, c.z)) continue;
         }
-        int32_t myn = -1;
-        if (lane < 27) myn = (lane == 0) ? (int32_t)b : nbr[27 * b + lane];
-        // solid64 (exchanged between ranks) rather than the masks of
-        // neighbours, which may belong to another rank
-        const uint64_t sm = (lane < 27 && myn >= 0) ? solid64[myn] : 0ull;
-        if (!__any_sync(0xffffffffu, sm != 0)) {  // not a candidate (A18): no boundary cell
-            if (lane == 0) {
-                bcount[b] = 0;
-                bflags[b] = (uint8_t)(bflags[b] & ~VF_BF_BOUNDARY);
-            }
-            continue;
+        // solid64 (exchanged between ranks) rather than the neighbours' masks,
+        // which may belong to another rank; missing neighbours contribute 0
+        uint64_t S[27];
+        uint64_t any = 0;
+#pragma unroll
+        for (int q = 0; q < 27; ++q) {
+            const int32_t v = q == 0 ? (int32_t)b : __ldg(nbr + 27 * b + q);
+            S[q] = v >= 0 ? __ldg(reinterpret_cast<const unsigned long long *>(solid64) + v) : 0ull;
+            any |= S[q];
         }
-        if (lane < 27) s_sol[w][lane] = sm;
-        __syncwarp();
-        for (int h = lane; h < 216; h += 32) {
-            const int hx = h % 6 - 1, hy = (h / 6) % 6 - 1, hz = h / 36 - 1;
-            const int ox = hx < 0 ? -1 : (hx > 3 ? 1 : 0);
-            const int oy = hy < 0 ? -1 : (hy > 3 ? 1 : 0);
-            const int oz = hz < 0 ? -1 : (hz > 3 ? 1 : 0);
-            const uint64_t nsm = s_sol[w][slot_of(ox, oy, oz)];
-            s_halo[w][h] = (uint8_t)((nsm >> ((hx & 3) + 4 * (hy & 3) + 16 * (hz & 3))) & 1ull);
-        }
-        __syncwarp();
         int cnt = 0;
+        if (any) {  // candidate (A18): the block or a neighbour has a SOLID cell
+            uint64_t pl[3];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int c = lane + 32 * k;
-            const int I = c & 3, J = (c >> 2) & 3, K = c >> 4;
-            if (masks[64 * b + c] != VF_FLUID) continue;
-            const uint8_t *hp = &s_halo[w][(I + 1) + 6 * (J + 1) + 36 * (K + 1)];
-            uint32_t any = 0;
+            for (int oz = -1; oz <= 1; ++oz) {
+                uint64_t col[3];
 #pragma unroll
-            for (int dz = -1; dz <= 1; ++dz)
+                for (int oy = -1; oy <= 1; ++oy)
+                    col[oy + 1] = dil_x(S[slot_of(-1, oy, oz)], S[slot_of(0, oy, oz)], S[slot_of(1, oy, oz)]);
+                pl[oz + 1] = dil_y(col[0], col[1], col[2]);
+            }
+            const uint64_t D = dil_z(pl[0], pl[1], pl[2]);
+            uint32_t w[16];
+            const uint4 *mp = reinterpret_cast<const uint4 *>(masks + 64 * b);
 #pragma unroll
-                for (int dy = -1; dy <= 1; ++dy)
+            for (int k = 0; k < 4; ++k) {
+                const uint4 u = mp[k];
+                w[4 * k] = u.x; w[4 * k + 1] = u.y; w[4 * k + 2] = u.z; w[4 * k + 3] = u.w;
+            }
+            bool changed = false;
 #pragma unroll
-                    for (int dx = -1; dx <= 1; ++dx)
-                        if (dx || dy || dz) any |= hp[dx + 6 * dy + 36 * dz];
-            if (any) {
-                masks[64 * b + c] = VF_BOUNDARY;
-                ++cnt;
+            for (int r = 0; r < 16; ++r) {
+                uint32_t x = w[r];
+#pragma unroll
+                for (int I = 0; I < 4; ++I) {
+                    if (((x >> (8 * I)) & 0xffu) == VF_FLUID && ((D >> (4 * r + I)) & 1ull)) {
+                        x |= (uint32_t)VF_BOUNDARY << (8 * I);
+                        ++cnt;
+                    }
+                }
+                changed |= x != w[r];
+                w[r] = x;
+            }
+            if (changed) {
+                uint4 *mo = reinterpret_cast<uint4 *>(masks + 64 * b);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) mo[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
             }
         }
-        cnt = warp_sum(cnt);
-        if (lane == 0) {
-            bcount[b] = cnt;
-            const uint8_t f = bflags[b];
-            bflags[b] = (uint8_t)(cnt > 0 ? (f | VF_BF_BOUNDARY) : (f & ~VF_BF_BOUNDARY));
-        }
-        __syncwarp();
+        bcount[b] = cnt;
+        const uint8_t f = bflags[b];
+        bflags[b] = (uint8_t)(cnt > 0 ? (f | VF_BF_BOUNDARY) : (f & ~VF_BF_BOUNDARY));
     }
 }
 
 int boundary_impl(const vf_config &cfg, vf_grid *g, int32_t *bcount, cudaStream_t st) {
     const int L = g->n_levels - 1;
     cudaMemsetAsync(bcount, 0, sizeof(int32_t) * (size_t)g->capacity, st);
-    k_boundary<<<max_ctas(8), kBndWarps * 32, 0, st>>>(make_level(cfg, L), L, g->d_level_start,
+    k_boundary<<<max_ctas(8), 256, 0, st>>>(make_level(cfg, L), L, g->d_level_start,
                                                        g->d_nbr, g->d_coords, g->d_bflags,
                                                        g->d_masks, g->d_solid64, bcount);
     return check_launch("k_boundary");
