@@ -150,7 +150,10 @@ struct LinkWarp {
     float ff[32][10];   // nf, V1 = v2 - v1, V2 = v3 - v1 (FP32), Ef
     short lohi[32][6];  // fallback node range per axis (cells <= 32767)
     int excl[32];       // exclusive prefix of the per-lane row counts
+    int4 lq[96];        // lines that pierce a face: (owner lane | class << 8, m1, m2, Ra bits)
+    int lqn;
 };
+constexpr int kLineQ = 96;
 
 // Exact accept of one node without the eps-box SAT (the FAST path).  Only
 // used for lines that pass through the projected triangle with a margin of
@@ -272,21 +275,13 @@ __device__ __forceinline__ void link_slow(const LinkCtx &c, int f, int slot, int
     else c.n_band[1] = 1;  // the fallback kernel redoes every face inline
 }
 
-// one lattice point (line) of a row: inside test, crossing estimate, then its
-// (2, rarely 3) nodes -- fast exact path for interior lines, link_slow for the
-// margin band and ill-conditioned crossings
+// the (2, rarely 3) nodes of one line that pierces the face: crossing
+// estimate, then the fast exact path (interior lines) or link_slow (margin
+// band, ill-conditioned crossings)
 template <bool FULL>
-__device__ __forceinline__ void link_point(const LinkCtx &c, const LinkDir &D, const double *fv,
-                                           int m1, int m2, float Rb, int R, int p, int cp, int s1,
-                                           int s2, int n1, int n2) {
-    const double dx = c.dx;
-    const float Ra = (float)(((double)m1 + 0.5 * (1 - s1)) * dx + D.off1);
-    const float sg = D.sg;
-    const float E0 = sg * (D.P1a * Rb - D.P1b * Ra);
-    const float E1 = sg * ((D.P2a - D.P1a) * (Rb - D.P1b) - (D.P2b - D.P1b) * (Ra - D.P1a));
-    const float E2 = sg * (D.P2b * Ra - D.P2a * Rb);
-    if (E0 < -D.t0 || E1 < -D.t1 || E2 < -D.t2) return;  // misses the face
-    const bool fast = !FULL && D.fast && E0 >= D.t0 && E1 >= D.t1 && E2 >= D.t2;
+__device__ __forceinline__ void link_line(const LinkCtx &c, const LinkDir &D, const double *fv,
+                                          int m1, int m2, float Ra, float Rb, bool fast, int R,
+                                          int p, int cp, int s1, int s2, int n1, int n2) {
     // crossing with the face plane: Q = v1 + Ra e_q1 + Rb e_q2 (+0 e_p),
     // points Q + lam c; n.(Q + lam c - v1) = 0
     int ip_lo = D.lop, ip_hi = D.hip;
@@ -312,24 +307,74 @@ __device__ __forceinline__ void link_point(const LinkCtx &c, const LinkDir &D, c
     }
 }
 
+// Lines found by the row scans are queued per warp and resolved 32 at a time
+// (one line per lane): the row / point loops leave few lanes active, the node
+// work (bmap lookup, FP64 num/den, atomicMin) then runs on full warps.  The
+// queue is drained before the next pair overwrites the per-lane LinkDir.
+template <bool FULL>
+__device__ __forceinline__ void line_drain(LinkWarp &W, int lane, const LinkCtx &c, bool all, int R,
+                                           int p, int cp, int s1, int s2, int n1, int n2) {
+    __syncwarp();
+    int n = min(W.lqn, kLineQ);
+    while (n >= 32 || (all && n > 0)) {
+        const int take = min(n, 32);
+        int4 e = make_int4(0, 0, 0, 0);
+        if (lane < take) e = W.lq[n - take + lane];
+        __syncwarp();
+        if (lane < take) {
+            const int o = e.x & 31;
+            const LinkDir &D = W.d[o];
+            const float Rb = (float)(((double)e.z + 0.5 * (1 - s2)) * c.dx + D.off2);
+            link_line<FULL>(c, D, W.fv[o], e.y, e.z, __int_as_float(e.w), Rb, (e.x >> 8) & 1, R, p, cp,
+                            s1, s2, n1, n2);
+        }
+        n -= take;
+    }
+    __syncwarp();
+    if (lane == 0) W.lqn = n;
+    __syncwarp();
+}
+
+// inside test of the line through (Ra, Rb): 0 misses the face, 1 interior
+// with margin and fast path allowed, 2 undecided (exact path with the SAT)
+__device__ __forceinline__ int point_class(const LinkDir &D, float Ra, float Rb) {
+    const float sg = D.sg;
+    const float E0 = sg * (D.P1a * Rb - D.P1b * Ra);
+    const float E1 = sg * ((D.P2a - D.P1a) * (Rb - D.P1b) - (D.P2b - D.P1b) * (Ra - D.P1a));
+    const float E2 = sg * (D.P2b * Ra - D.P2a * Rb);
+    if (E0 < -D.t0 || E1 < -D.t1 || E2 < -D.t2) return 0;
+    return (D.fast && E0 >= D.t0 && E1 >= D.t1 && E2 >= D.t2) ? 1 : 2;
+}
+
+// one lattice point (line) of a row: inside test; a piercing line is queued
+// (or, when the queue is full, resolved inline)
+template <bool FULL>
+__device__ __forceinline__ void link_point(LinkWarp &W, int o, const LinkCtx &c, const LinkDir &D,
+                                           const double *fv, int m1, int m2, float Rb, int R, int p,
+                                           int cp, int s1, int s2, int n1, int n2) {
+    const float Ra = (float)(((double)m1 + 0.5 * (1 - s1)) * c.dx + D.off1);
+    const int cls = point_class(D, Ra, Rb);
+    if (cls == 0) return;  // misses the face
+    const bool fast = !FULL && cls == 1;
+    const int pos = atomicAdd(&W.lqn, 1);
+    if (pos < kLineQ) W.lq[pos] = make_int4(o | ((int)fast << 8), m1, m2, __float_as_int(Ra));
+    else link_line<FULL>(c, D, fv, m1, m2, Ra, Rb, fast, R, p, cp, s1, s2, n1, n2);
+}
+
 // one lattice row m2: the conservative m1 interval of the row inside the
 // margin-widened triangle (scanline; each edge function is linear in Ra,
 // E_k = alpha_k Ra + beta_k >= -t_k), then its points.  An edge whose bound
 // is ill-conditioned (|alpha_k| tiny) does not restrict the row; the interval
 // is widened by one lattice point on each side -- a superset of the points
 // that pass link_point's own test, which alone decides.
-template <bool FULL>
-__device__ __forceinline__ void link_row(const LinkCtx &c, const LinkDir &D, const double *fv,
-                                         int m2, int R, int p, int cp, int s1, int s2, int n1,
-                                         int n2) {
-    const double dx = c.dx;
-    const float Rb = (float)(((double)m2 + 0.5 * (1 - s2)) * dx + D.off2);
+__device__ __forceinline__ bool row_interval(const LinkCtx &c, const LinkDir &D, float Rb, int s1,
+                                             int &m1lo, int &m1hi) {
     const float sg = D.sg;
     const float al[3] = {-sg * D.P1b, -sg * (D.P2b - D.P1b), sg * D.P2b};
     const float be[3] = {sg * D.P1a * Rb, sg * ((D.P2a - D.P1a) * (Rb - D.P1b) + (D.P2b - D.P1b) * D.P1a),
                          -sg * D.P2a * Rb};
     const float tk[3] = {D.t0, D.t1, D.t2};
-    const float dxf = (float)dx;
+    const float dxf = (float)c.dx;
     // magnitude bound of the products in beta_k (FP32 error <~ 3e-7 M)
     const float sP = fabsf(D.P1a) + fabsf(D.P1b) + fabsf(D.P2a) + fabsf(D.P2b);
     const float M = sP * (fabsf(Rb) + sP);
@@ -339,7 +384,7 @@ __device__ __forceinline__ void link_row(const LinkCtx &c, const LinkDir &D, con
         const float a = al[k], rhs = -tk[k] - be[k];
         if (1e-5f * (M + tk[k]) >= 0.25f * dxf * fabsf(a)) {
             // (near-)parallel edge: the row is either fully out or unrestricted
-            if (a == 0.0f && be[k] < -tk[k] - 1e-5f * (M + tk[k])) return;
+            if (a == 0.0f && be[k] < -tk[k] - 1e-5f * (M + tk[k])) return false;
             continue;
         }
         const float b = __fdividef(rhs, a);  // ~2 ulp: the bound is padded by a lattice step
@@ -347,11 +392,28 @@ __device__ __forceinline__ void link_row(const LinkCtx &c, const LinkDir &D, con
         else hi = fminf(hi, b);
     }
     const double d1 = 0.5 * (1 - s1);
-    int m1lo = D.m1a, m1hi = D.m1b;
+    m1lo = D.m1a;
+    m1hi = D.m1b;
     if (lo > -INFINITY) m1lo = max(m1lo, (int)ceil(((double)lo - D.off1) * c.inv_dx - d1) - 1);
     if (hi < INFINITY) m1hi = min(m1hi, (int)floor(((double)hi - D.off1) * c.inv_dx - d1) + 1);
+    return m1lo <= m1hi;
+}
+
+// one lattice row m2: the conservative m1 interval of the row inside the
+// margin-widened triangle (scanline; each edge function is linear in Ra,
+// E_k = alpha_k Ra + beta_k >= -t_k), then its points.  An edge whose bound
+// is ill-conditioned (|alpha_k| tiny) does not restrict the row; the interval
+// is widened by one lattice point on each side -- a superset of the points
+// that pass point_class, which alone decides.
+template <bool FULL>
+__device__ __forceinline__ void link_row(LinkWarp &W, int o, const LinkCtx &c, const LinkDir &D,
+                                         const double *fv, int m2, int R, int p, int cp, int s1,
+                                         int s2, int n1, int n2) {
+    const float Rb = (float)(((double)m2 + 0.5 * (1 - s2)) * c.dx + D.off2);
+    int m1lo, m1hi;
+    if (!row_interval(c, D, Rb, s1, m1lo, m1hi)) return;
     for (int m1 = m1lo; m1 <= m1hi; ++m1)
-        link_point<FULL>(c, D, fv, m1, m2, Rb, R, p, cp, s1, s2, n1, n2);
+        link_point<FULL>(W, o, c, D, fv, m1, m2, Rb, R, p, cp, s1, s2, n1, n2);
 }
 
 constexpr size_t kLinkSmem = kLinkWarps * sizeof(LinkWarp);
@@ -369,6 +431,7 @@ __global__ void __launch_bounds__(kLinkWarps * 32, FULL ? 1 : VF_LINK_MINB)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     LinkWarp &W = reinterpret_cast<LinkWarp *>(s_raw)[w];
     const int64_t n = d_n_map ? (int64_t)*d_n_map : F;
+    if (lane == 0) W.lqn = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     // all lanes of a warp iterate together (uniform trip count); lanes past
     // the end are inactive
@@ -429,15 +492,19 @@ __global__ void __launch_bounds__(kLinkWarps * 32, FULL ? 1 : VF_LINK_MINB)
             const int total = __shfl_sync(0xffffffffu, inc, 31);
             W.excl[lane] = inc - cnt;
             __syncwarp();
-            for (int it = lane; it < total; it += 32) {
-                int o = 0;  // owner lane: largest o with excl[o] <= it
+            for (int b0 = 0; b0 < total; b0 += 32) {
+                const int it = b0 + lane;
+                if (it < total) {
+                    int o = 0;  // owner lane: largest o with excl[o] <= it
 #pragma unroll
-                for (int st = 16; st > 0; st >>= 1)
-                    if (W.excl[o + st] <= it) o += st;
-                const LinkDir &D = W.d[o];
-                link_row<FULL>(c, D, W.fv[o], D.m2a + it - W.excl[o], R, p, cp, s1, s2, n1, n2);
+                    for (int st = 16; st > 0; st >>= 1)
+                        if (W.excl[o + st] <= it) o += st;
+                    const LinkDir &D = W.d[o];
+                    link_row<FULL>(W, o, c, D, W.fv[o], D.m2a + it - W.excl[o], R, p, cp, s1, s2, n1, n2);
+                }
+                line_drain<FULL>(W, lane, c, false, R, p, cp, s1, s2, n1, n2);
             }
-            __syncwarp();
+            line_drain<FULL>(W, lane, c, true, R, p, cp, s1, s2, n1, n2);
         }
     }
 }
