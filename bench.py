@@ -144,9 +144,10 @@ def dist_setup():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        # VF_BENCH_BACKEND=gloo: exercise the multi-rank path on one GPU (tests)
+        backend = os.environ.get("VF_BENCH_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
         if torch.cuda.is_available():
-            torch.cuda.set_device(local)
+            torch.cuda.set_device(local % torch.cuda.device_count())
         dist.init_process_group(backend)
     return ws, rank, local
 
@@ -315,7 +316,7 @@ def main():
                     "timed": "CUDA events on the engine stream around k_links + k_links_band + "
                              "the overflow fallback (a no-op unless the band list overflowed)"}
     else:
-        n_b = int(eng.lengths.shape[0]) if eng.lengths is not None else 0
+        n_b = int(run()[1].n_b)
 
     e2e = None
     if not args.no_e2e:

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define VF_ABI_VERSION 2
+#define VF_ABI_VERSION 3
 #define VF_MAX_LEVELS 16
 
 /* status codes (SURVEY.md §8b "Errors") */
@@ -68,10 +68,14 @@ typedef struct {
     double  len[3];       /* domain lengths (origin 0)                      */
     double  eps_slab;
     double  eps_parallel; /* geometry.py:25                                 */
-    /* block sharding (multi-GPU): a level-L block row (j,k) is owned by rank
-     * (j + B_L,y * k) mod shard_count; x-runs never cross ranks.  0/1 = all. */
+    /* block sharding (multi-GPU): x-runs never cross ranks because whole
+     * level-L block rows (j,k) are owned.  0/1 = all.  With d_row_owner set,
+     * rank = d_row_owner[row_base(L) + j + B_L,y * k] (contiguous row ranges
+     * balanced by block count, vf_shard_owner_map; row_base(L) = sum over
+     * l < L of B_l,y * B_l,z); without it, rank = (j + B_L,y * k) mod count. */
     int32_t shard_rank;
     int32_t shard_count;
+    uint8_t *d_row_owner;
 } vf_config;
 
 /* ForestGrid as flat device arrays, ids grouped by level:
@@ -219,6 +223,34 @@ int64_t vf_launch_count(void);
  * values to every rank */
 int vf_shard_zero_unowned(const vf_config *cfg, vf_grid *grid, int level,
                           int32_t *d_bcount, void *stream);
+/* ---- block-sharded multi-GPU embed (one process per GPU; the caller runs
+ * the NCCL exchanges between these calls, see parallel.py).  All use the
+ * embed workspace (vf_embed_workspace_size) and cfg->shard_rank/count/
+ * d_row_owner.
+ * size of cfg->d_row_owner (bytes): one owner byte per block row per level */
+size_t vf_shard_owner_bytes(const vf_config *cfg);
+/* owner map of level L from the (replicated) level-L blocks: contiguous row
+ * ranges with equal block counts, identical on every rank */
+int vf_shard_owner_map(const vf_config *cfg, vf_grid *grid, int level, void *d_ws,
+                       size_t ws_bytes, void *stream);
+/* level L on the owned rows: bins (Alg. 1-2, owned rows/bins), voxelize,
+ * Alg. 5 (+x, -x) + finalize, then zero the level's flags / solid64 of
+ * unowned blocks for the owner-zeroed all-reduce */
+int vf_shard_level(const vf_config *cfg, const double *d_faces, int64_t n_faces,
+                   int use_filter, vf_grid *grid, int level, void *d_ws, size_t ws_bytes,
+                   void *stream);
+/* replicated refinement of level L (mark + adapt) and the owner map of L+1 */
+int vf_shard_refine(const vf_config *cfg, vf_grid *grid, int level, void *d_ws,
+                    size_t ws_bytes, void *stream);
+/* finest level: boundary cells of owned blocks (counts -> d_bcount, zeroed
+ * for unowned blocks) */
+int vf_shard_boundary(const vf_config *cfg, vf_grid *grid, int32_t *d_bcount, void *stream);
+/* cut-link LUT slots of the owned blocks: LUT init (-1), faces near owned
+ * rows, k_links on them (the LUT stays distributed) */
+int vf_shard_links(const vf_config *cfg, const double *d_faces, int64_t n_faces,
+                   vf_grid *grid, const int32_t *d_cmap, const int32_t *d_n_b,
+                   float *d_lengths, int64_t lengths_cap, void *d_ws, size_t ws_bytes,
+                   void *stream);
 /* copy the grid's latched device status to the host (synchronizes) */
 int vf_check_status(const vf_grid *grid, void *stream);
 /* test hook: capacity of the link-length band list (candidates the FP32

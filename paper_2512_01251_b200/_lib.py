@@ -15,7 +15,7 @@ from .errors import (BinCapError, CapacityError, CudaError, MeshError, Voxforest
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # VF_LIB_PATH: an alternative in-tree build of the same library (A/B kernel experiments)
 LIB_PATH = os.environ.get("VF_LIB_PATH") or os.path.join(_HERE, "libvoxforest_b200.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 MAX_LEVELS = 16
 
 # cell masks / block flags / neighbour codes (voxforest_b200.h)
@@ -28,7 +28,8 @@ class VfConfig(C.Structure):
     _fields_ = [("nb", C.c_int32 * 3), ("l_max", C.c_int32), ("n_spec", C.c_int32),
                 ("n_prop", C.c_int32), ("dx0", C.c_double), ("len", C.c_double * 3),
                 ("eps_slab", C.c_double), ("eps_parallel", C.c_double),
-                ("shard_rank", C.c_int32), ("shard_count", C.c_int32)]
+                ("shard_rank", C.c_int32), ("shard_count", C.c_int32),
+                ("d_row_owner", C.c_void_p)]
 
 
 class VfGrid(C.Structure):
@@ -89,6 +90,12 @@ _SIGS = {
     "vf_check_status": (_I32, [_GP, _P]),
     "vf_shard_zero_unowned": (_I32, [_CP, _GP, _I32, _P, _P]),
     "vf_set_link_band_cap": (_I64, [_I64]),
+    "vf_shard_owner_bytes": (_SZ, [_CP]),
+    "vf_shard_owner_map": (_I32, [_CP, _GP, _I32, _P, _SZ, _P]),
+    "vf_shard_level": (_I32, [_CP, _P, _I64, _I32, _GP, _I32, _P, _SZ, _P]),
+    "vf_shard_refine": (_I32, [_CP, _GP, _I32, _P, _SZ, _P]),
+    "vf_shard_boundary": (_I32, [_CP, _GP, _P, _P]),
+    "vf_shard_links": (_I32, [_CP, _P, _I64, _GP, _P, _P, _P, _I64, _P, _SZ, _P]),
 }
 
 EXPORTED = tuple(_SIGS)

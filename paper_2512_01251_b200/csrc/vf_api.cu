@@ -59,6 +59,12 @@ LevelInfo make_level(const vf_config &cfg, int L) {
     li.level = L;
     li.shard_rank = cfg.shard_count > 1 ? cfg.shard_rank : 0;
     li.shard_count = cfg.shard_count > 1 ? cfg.shard_count : 1;
+    li.owner = nullptr;
+    if (li.shard_count > 1 && cfg.d_row_owner) {
+        int64_t base = 0;  // row_base(L): rows of the coarser levels
+        for (int l = 0; l < L; ++l) base += (int64_t)(cfg.nb[1] << l) * (cfg.nb[2] << l);
+        li.owner = cfg.d_row_owner + base;
+    }
     return li;
 }
 
@@ -120,6 +126,7 @@ struct EmbedWs {
     size_t prop_b, mark_b, adapt_b, tab_b, link_b;
     int32_t *bcount;
     uint16_t *ind_bits;  // [F] per-level 1D indicator bits
+    void *shard_ws;      // multi-GPU: row histogram / owner scan / face subset
 };
 
 static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *base, EmbedWs *w) {
@@ -155,6 +162,7 @@ static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *b
     t.link_ws = take(t.link_b);
     t.ind_bits = (uint16_t *)take(sizeof(uint16_t) * (size_t)(F + 1));
     t.bcount = (int32_t *)take(sizeof(int32_t) * (size_t)cap);
+    t.shard_ws = cfg.shard_count > 1 ? take(shard_scratch_size(cfg, F)) : nullptr;
     if (w) *w = t;
     return off;
 }
@@ -446,6 +454,73 @@ int vf_shard_zero_unowned(const vf_config *cfg, vf_grid *grid, int level, int32_
     if (!valid_cfg(cfg) || !grid || level < 0 || level >= grid->n_levels)
         return set_error(VF_EARG, "vf_shard_zero_unowned: bad argument");
     return shard_zero_impl(make_level(*cfg, level), grid, level, d_bcount, (cudaStream_t)stream);
+}
+
+// ---- block-sharded multi-GPU embed (parallel.py drives the exchanges)
+
+size_t vf_shard_owner_bytes(const vf_config *cfg) {
+    if (!valid_cfg(cfg)) return 0;
+    return shard_owner_bytes(*cfg);
+}
+
+static bool shard_args(const vf_config *cfg, vf_grid *g, void *ws, size_t ws_bytes, int64_t F,
+                       EmbedWs *w) {
+    if (!valid_cfg(cfg) || !g || cfg->shard_count < 2 || !cfg->d_row_owner) return false;
+    return embed_layout(*cfg, F, g->capacity, (char *)ws, w) <= ws_bytes;
+}
+
+int vf_shard_owner_map(const vf_config *cfg, vf_grid *g, int level, void *ws, size_t ws_bytes,
+                       void *stream) {
+    EmbedWs w;
+    // the owner map only needs the shard scratch; F = 1 sizes the layout
+    if (!shard_args(cfg, g, ws, ws_bytes, 1, &w) || level < 0 || level >= cfg->l_max)
+        return set_error(VF_EARG, "vf_shard_owner_map: bad argument");
+    return shard_owner_map_impl(*cfg, g, level, w.shard_ws, (cudaStream_t)stream);
+}
+
+int vf_shard_level(const vf_config *cfg, const double *faces, int64_t F, int use_filter,
+                   vf_grid *g, int L, void *ws, size_t ws_bytes, void *stream) {
+    EmbedWs w;
+    if (!faces || F <= 0 || !shard_args(cfg, g, ws, ws_bytes, F, &w) || L < 0 ||
+        L >= g->n_levels)
+        return set_error(VF_EARG, "vf_shard_level: bad argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const LevelInfo li = make_level(*cfg, L);
+    VF_TRY(build_bins_impl(li, nlim_of(*cfg), faces, F, 0, use_filter, &w.bins, g->d_status,
+                           w.bins_ws, w.bins_ws_bytes, st, nullptr, false));
+    VF_TRY(voxelize_impl(li, g, L, &w.bins, faces, st));
+    VF_TRY(propagate_level_impl(li, g, L, w.prop_ws, w.prop_b, st));
+    return shard_zero_impl(li, g, L, nullptr, st);
+}
+
+int vf_shard_refine(const vf_config *cfg, vf_grid *g, int L, void *ws, size_t ws_bytes,
+                    void *stream) {
+    EmbedWs w;
+    if (!shard_args(cfg, g, ws, ws_bytes, 1, &w) || L < 0 || L + 1 >= cfg->l_max)
+        return set_error(VF_EARG, "vf_shard_refine: bad argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    VF_TRY(mark_impl(*cfg, g, L, w.mark_ws, w.mark_b, st));
+    VF_TRY(adapt_impl(*cfg, g, L, w.adapt_ws, w.adapt_b, st));
+    return shard_owner_map_impl(*cfg, g, L + 1, w.shard_ws, st);
+}
+
+int vf_shard_boundary(const vf_config *cfg, vf_grid *g, int32_t *bcount, void *stream) {
+    if (!valid_cfg(cfg) || !g || !bcount) return set_error(VF_EARG, "vf_shard_boundary: bad argument");
+    return boundary_impl(*cfg, g, bcount, (cudaStream_t)stream);
+}
+
+int vf_shard_links(const vf_config *cfg, const double *faces, int64_t F, vf_grid *g,
+                   const int32_t *cmap, const int32_t *d_n_b, float *lengths, int64_t lengths_cap,
+                   void *ws, size_t ws_bytes, void *stream) {
+    EmbedWs w;
+    if (!faces || F <= 0 || !cmap || !d_n_b || !lengths || lengths_cap < 1 ||
+        !shard_args(cfg, g, ws, ws_bytes, F, &w))
+        return set_error(VF_EARG, "vf_shard_links: bad argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    VF_TRY(fill_lut_impl(d_n_b, lengths, lengths_cap, g->d_status, st));
+    VF_TRY(shard_face_subset_impl(*cfg, faces, F, w.bins.d_map, w.bins.d_n_map, w.shard_ws, st));
+    return link_impl(*cfg, g, cmap, faces, F, w.bins.d_map, w.bins.d_n_map, lengths, w.link_ws,
+                     w.link_b, st, nullptr, d_n_b, lengths_cap);
 }
 
 int vf_check_status(const vf_grid *g, void *stream) {

@@ -51,17 +51,24 @@ struct LevelInfo {
     int cells[3];    // cells per axis at L
     int bins[3];     // bins (= blocks) per axis at L
     int level;
-    int shard_rank;  // block-row ownership (multi-GPU), see owner_of
+    int shard_rank;  // block-row ownership (multi-GPU), see owns_row
     int shard_count;
+    const uint8_t *owner;  // balanced row -> rank map of this level (or null)
 };
 
-// owner rank of the level-L block row (j,k); interleaved so neighbouring
-// rows land on different ranks (balance) while x-runs stay rank-local
+// owner rank of the level-L block row (j,k) without an owner map:
+// interleaved, so neighbouring rows land on different ranks while x-runs stay
+// rank-local.  The sharded embed uses the balanced contiguous map instead
+// (vf_shard_owner_map): a face then touches the rows of one or two ranks.
 __host__ __device__ __forceinline__ int row_owner(int j, int k, int by, int nranks) {
     return nranks <= 1 ? 0 : (int)(((int64_t)j + (int64_t)by * k) % nranks);
 }
 __host__ __device__ __forceinline__ bool owns_row(const LevelInfo &li, int j, int k) {
-    return li.shard_count <= 1 || row_owner(j, k, li.bins[1], li.shard_count) == li.shard_rank;
+    if (li.shard_count <= 1) return true;
+#ifdef __CUDA_ARCH__
+    if (li.owner) return li.owner[j + (int64_t)li.bins[1] * k] == li.shard_rank;
+#endif
+    return row_owner(j, k, li.bins[1], li.shard_count) == li.shard_rank;
 }
 
 // A2: lattice node / cell centre, one rounding

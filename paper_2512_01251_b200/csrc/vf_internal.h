@@ -91,6 +91,12 @@ int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const doubl
               int64_t F, const int32_t *map, const int32_t *d_n_map, float *lengths, void *ws,
               size_t ws_bytes, cudaStream_t st, void **events, const int32_t *d_n_b,
               int64_t lengths_cap);
+// multi-GPU sharding (vf_shard.cu)
+size_t shard_owner_bytes(const vf_config &cfg);
+size_t shard_scratch_size(const vf_config &cfg, int64_t F);
+int shard_owner_map_impl(const vf_config &cfg, vf_grid *g, int L, void *scratch, cudaStream_t st);
+int shard_face_subset_impl(const vf_config &cfg, const double *faces, int64_t F, int32_t *map,
+                           int32_t *d_n_map, void *scratch, cudaStream_t st);
 int fill_lut_impl(const int32_t *d_n_b, float *lengths, int64_t cap, int32_t *d_status,
                   cudaStream_t st);
 

@@ -5,25 +5,28 @@ NVLink used only for per-level flags and counts).
 One process per GPU (torchrun), ``torch.distributed`` process group (NCCL; gloo
 works too, which is how the CPU/1-GPU tests exercise it).
 
-Ownership: at level L the block row (j, k) -- all blocks with the same (j, k),
-hence every x-run of Alg. 5 -- belongs to rank ``(j + B_L,y * k) mod N``
-(interleaved for balance; ``row_owner`` mirrors csrc/vf_common.cuh).  Per level
+Ownership: whole level-L block rows (j, k) -- hence every x-run of Alg. 5 --
+belong to one rank.  The rows are cut into contiguous ranges (row = j + B_y k)
+holding equal numbers of level-L blocks (``vf_shard_owner_map``, computed from
+the replicated topology, so every rank derives the same map without
+communication).  A face then touches the rows of one or two ranks.  Per level
 every rank
-  1. bins only faces that hit one of ITS rows and only ITS bins
-     (vf_build_bins with shard = (rank, N));
-  2. voxelizes, propagates (+x, -x) and finalizes -- exact on its rows because
-     runs never leave a row;
-  3. zeroes the level's block flags of rows it does not own and all-reduces
+  1. bins only faces that hit one of ITS rows and only ITS bins, voxelizes,
+     and runs Alg. 5 (+x, -x) + finalize on its rows (``vf_shard_level``,
+     exact because runs never leave a row);
+  2. zeroes the level's block flags of rows it does not own and all-reduces
      them (MAX over uint8, 1 B/block): every rank now holds the exact solid
      flags of the whole level;
-  4. marks and adapts REPLICATED (deterministic, identical on every rank), so
-     the block topology is identical everywhere without any exchange.
+  3. marks and adapts REPLICATED (deterministic, identical on every rank) and
+     derives the next level's owner map (``vf_shard_refine``), so the block
+     topology is identical everywhere without any exchange.
 At the finest level the exchange adds the 64-bit SOLID-cell masks (SUM over
 owner-zeroed int64, 8 B/block) for the boundary halo and, after boundary
 detection on owned blocks, the per-block boundary counts (SUM, 4 B/block)
 for the global contraction map.  Link lengths are computed for owned blocks
-only: the LUT stays distributed (rank r holds the slots of its blocks), as a
-sharded solver consumes it.
+only, from the faces near owned rows (~F/N per rank): the LUT stays
+distributed (rank r holds the slots of its blocks), as a sharded solver
+consumes it.
 
 Results on owned data are bit-identical to the single-GPU embed
 (tests/test_gpu_sharded.py); topology and flags are identical on every rank.
@@ -45,6 +48,18 @@ def row_owner(j, k, by_L: int, n_ranks: int):
     if n_ranks <= 1:
         return np.zeros_like(np.asarray(j))
     return (np.asarray(j, dtype=np.int64) + by_L * np.asarray(k, dtype=np.int64)) % n_ranks
+
+
+def balanced_row_owner(counts, n_ranks: int):
+    """numpy restatement of vf_shard_owner_map (k_row_assign): owner of each
+    block row = the rank whose 1/N share of the level's blocks holds the row's
+    first block.  ``counts`` = blocks per row (row = j + B_y k)."""
+    counts = np.asarray(counts, dtype=np.int64)
+    total = int(counts.sum())
+    if n_ranks <= 1 or total == 0:
+        return np.zeros(counts.shape, dtype=np.uint8)
+    excl = np.cumsum(counts) - counts
+    return np.minimum(excl * n_ranks // total, n_ranks - 1).astype(np.uint8)
 
 
 def owner_zero_allreduce(t, owned_mask, op, group=None):
@@ -73,49 +88,29 @@ class ShardedEmbed:
         cap = int(capacity if capacity is not None else cfg.block_capacity(self.mesh.area))
         self.grid = ForestGrid.allocate(cfg, cap)
         self.c = _lib.make_config(cfg, shard=(self.rank, self.world))
-        F, Lf = self.mesh.n_faces, cfg.l_max - 1
-        nb = cfg.n_bins(Lf)
-        dev = "cuda"
-        # bins buffers sized for the finest level, reused by every level
-        self.counts = torch.empty(nb, dtype=torch.int32, device=dev)
-        self.offsets = torch.empty(nb, dtype=torch.int32, device=dev)
-        self.face_ids = torch.empty(F * cfg.n_lim, dtype=torch.int32, device=dev)
-        self.fmap = torch.empty(F, dtype=torch.int32, device=dev)
-        self.scal = torch.zeros(8, dtype=torch.int32, device=dev)
-        self.bcount = torch.empty(cap, dtype=torch.int32, device=dev)
-        self.cmap = torch.empty(cap, dtype=torch.int32, device=dev)
-        gs = self.grid._struct()
-        sizes = {
-            "bins": max(self.lib.vf_bins_workspace_size(C.byref(self.c), F, L) for L in range(cfg.l_max)),
-            "prop": self.lib.vf_propagate_workspace_size(C.byref(gs)),
-            "mark": self.lib.vf_mark_workspace_size(C.byref(gs)),
-            "adapt": self.lib.vf_adapt_workspace_size(C.byref(gs)),
-            "tables": self.lib.vf_tables_workspace_size(C.byref(gs)),
-        }
-        self.ws = {k: torch.empty(int(v), dtype=torch.uint8, device=dev) for k, v in sizes.items()}
+        nown = self.lib.vf_shard_owner_bytes(C.byref(self.c))
+        self.row_owner = torch.zeros(max(int(nown), 1), dtype=torch.uint8, device="cuda")
+        self.c.d_row_owner = self.row_owner.data_ptr()
+        F = self.mesh.n_faces
+        wsb = self.lib.vf_embed_workspace_size(C.byref(self.c), F, cap)
+        if wsb == 0:
+            raise ValueError("invalid embed configuration")
+        self.ws = torch.empty(int(wsb), dtype=torch.uint8, device="cuda")
+        self.bcount = torch.empty(cap, dtype=torch.int32, device="cuda")
+        self.cmap = torch.empty(cap, dtype=torch.int32, device="cuda")
+        self.scal = torch.zeros(8, dtype=torch.int32, device="cuda")
+        self.tab_ws = torch.empty(int(self.lib.vf_tables_workspace_size(C.byref(self.grid._struct()))),
+                                  dtype=torch.uint8, device="cuda")
         self.lengths = None
         self.bc_ids = None
         self.comm_bytes = 0
 
-    # -- helpers --------------------------------------------------------
-    def _bins_struct(self):
-        b = _lib.VfBins()
-        b.d_counts, b.d_offsets = self.counts.data_ptr(), self.offsets.data_ptr()
-        b.d_face_ids, b.face_ids_cap = self.face_ids.data_ptr(), self.face_ids.numel()
-        b.d_n_face_ids = self.scal.data_ptr()
-        b.d_map, b.d_n_map = self.fmap.data_ptr(), self.scal.data_ptr() + 4
-        return b
-
     def _owned(self, L, s, e):
-        torch = self.torch
-        co = self.grid.coords[s:e]
+        co = self.grid.coords[s:e].long()
         by = self.cfg.bins(L)[1]
-        own = ((co[:, 1].long() + by * co[:, 2].long()) % self.world) == self.rank
-        return own
-
-    def _ws(self, k):
-        w = self.ws[k]
-        return _lib.ptr(w), w.numel()
+        rows = co[:, 1] + by * co[:, 2]
+        base = sum(self.cfg.bins(l)[1] * self.cfg.bins(l)[2] for l in range(L))
+        return self.row_owner[base + rows] == self.rank
 
     # -- the sharded pipeline ----------------------------------------------
     def run(self, use_filter: Optional[bool] = None):
@@ -124,64 +119,49 @@ class ShardedEmbed:
         uf = int(bool(cfg.use_filter if use_filter is None else use_filter))
         st = _lib.stream_ptr()
         faces, F = _lib.ptr(self.mesh.faces), self.mesh.n_faces
+        ws, wsn = _lib.ptr(self.ws), self.ws.numel()
         g.status.zero_()
         gs = g._struct()
         _lib.check(lib.vf_init_forest(C.byref(c), C.byref(gs), st), "init_forest")
         g.n_levels = gs.n_levels
+        _lib.check(lib.vf_shard_owner_map(C.byref(c), C.byref(gs), 0, ws, wsn, st), "owner map")
         self.comm_bytes = 0
-        b = self._bins_struct()
-        status1 = C.c_void_p(self.scal.data_ptr() + 8)
         for L in range(cfg.l_max):
             gs = g._struct()
-            _lib.check(lib.vf_build_bins(C.byref(c), faces, F, L, 0, uf, C.byref(b), status1,
-                                         *self._ws("bins"), st), "build_bins")
-            _lib.check(lib.vf_voxelize_level(C.byref(c), C.byref(gs), L, C.byref(b), faces, st),
-                       "voxelize")
-            _lib.check(lib.vf_propagate_x(C.byref(c), C.byref(gs), L, +1, int(L == 0),
-                                          *self._ws("prop"), st), "propagate +x")
-            if L > 0:
-                _lib.check(lib.vf_propagate_x(C.byref(c), C.byref(gs), L, -1, 1,
-                                              *self._ws("prop"), st), "propagate -x")
+            _lib.check(lib.vf_shard_level(C.byref(c), faces, F, uf, C.byref(gs), L, ws, wsn, st),
+                       "shard level")
             s, e = g.level_range(L)
             # exchange: level flags (1 B/block); finest level also SOLID masks
-            _lib.check(lib.vf_shard_zero_unowned(C.byref(c), C.byref(gs), L, None, st), "shard")
             dist.all_reduce(g.bflags[s:e], op=dist.ReduceOp.MAX, group=self.group)
             self.comm_bytes += (e - s)
             if L == cfg.l_max - 1:
                 dist.all_reduce(g.solid64[s:e], op=dist.ReduceOp.SUM, group=self.group)
                 self.comm_bytes += 8 * (e - s)
                 break
-            _lib.check(lib.vf_mark_level(C.byref(c), C.byref(gs), L, *self._ws("mark"), st), "mark")
-            _lib.check(lib.vf_adapt_refine(C.byref(c), C.byref(gs), L, *self._ws("adapt"), st),
-                       "adapt")
+            _lib.check(lib.vf_shard_refine(C.byref(c), C.byref(gs), L, ws, wsn, st), "shard refine")
             g.n_levels = gs.n_levels
         gs = g._struct()
         Lf = g.n_levels - 1
         s, e = g.level_range(Lf)
-        _lib.check(lib.vf_boundary_cells(C.byref(c), C.byref(gs), _lib.ptr(self.bcount), st),
+        _lib.check(lib.vf_shard_boundary(C.byref(c), C.byref(gs), _lib.ptr(self.bcount), st),
                    "boundary")
         dist.all_reduce(self.bcount[s:e], op=dist.ReduceOp.SUM, group=self.group)
         self.comm_bytes += 4 * (e - s)
         nb_dev = self.scal[4:5]
         _lib.check(lib.vf_link_tables(C.byref(c), C.byref(gs), _lib.ptr(self.bcount),
-                                      _lib.ptr(self.cmap), _lib.ptr(nb_dev), *self._ws("tables"), st),
-                   "tables")
+                                      _lib.ptr(self.cmap), _lib.ptr(nb_dev), _lib.ptr(self.tab_ws),
+                                      self.tab_ws.numel(), st), "tables")
         _lib.check(lib.vf_check_status(C.byref(gs), st), "embed_geometry (sharded)")
         n_b = int(nb_dev.item())
         if self.lengths is None or self.lengths.shape[0] < n_b:
             cap = int(n_b * 1.25) + 16
             self.lengths = torch.empty((cap, 27, 64), dtype=torch.float32, device="cuda")
             self.bc_ids = torch.zeros((cap, 27, 64), dtype=torch.int8, device="cuda")
-        lengths = self.lengths[:n_b]
-        lengths.fill_(-1.0)
-        lws = self.ws.get("links")
-        need = lib.vf_link_workspace_size(C.byref(c), C.byref(gs))
-        if lws is None or lws.numel() < need:
-            lws = self.ws["links"] = torch.empty(int(need), dtype=torch.uint8, device="cuda")
-        _lib.check(lib.vf_link_lengths(C.byref(c), C.byref(gs), _lib.ptr(self.cmap), faces, F, None,
-                                       None, _lib.ptr(lengths), _lib.ptr(lws), lws.numel(), st),
-                   "link lengths")
-        return g, LinkTable(lengths, self.bc_ids[:n_b], self.cmap[:g.n_used], n_b)
+        _lib.check(lib.vf_shard_links(C.byref(c), faces, F, C.byref(gs), _lib.ptr(self.cmap),
+                                      _lib.ptr(nb_dev), _lib.ptr(self.lengths), self.lengths.shape[0],
+                                      ws, wsn, st), "link lengths")
+        _lib.check(lib.vf_check_status(C.byref(gs), st), "embed_geometry (sharded links)")
+        return g, LinkTable(self.lengths[:n_b], self.bc_ids[:n_b], self.cmap[:g.n_used], n_b)
 
     def owned_blocks(self, L: int):
         """Boolean (n_L,) ownership of the level-L blocks (ids in level order)."""

@@ -69,6 +69,19 @@ def _worker(rank, world, port, q):
             if not ok:
                 errs.append(f"masks L{L}")
             owned_cells += int(own.sum())
+        # the owner map of every level is the balanced contiguous split of the
+        # replicated topology (numpy restatement in parallel.balanced_row_owner)
+        from paper_2512_01251_b200.parallel import balanced_row_owner
+        om = sh.row_owner.cpu().numpy()
+        base = 0
+        for L in range(g.n_levels):
+            s, e = g.level_range(L)
+            by, bz = cfg.bins(L)[1], cfg.bins(L)[2]
+            co = R["coords"][s:e]
+            cnt = np.bincount(co[:, 1] + by * co[:, 2], minlength=by * bz)
+            if not np.array_equal(om[base:base + by * bz], balanced_row_owner(cnt, world)):
+                errs.append(f"owner map L{L}")
+            base += by * bz
         if t.n_b != ref_t.n_b or not np.array_equal(t.contraction_map.cpu().numpy(), ref_cmap):
             errs.append("contraction map")
         Lf = g.n_levels - 1

@@ -69,3 +69,16 @@ def test_row_owner_properties():
         # neighbouring rows in y differ in owner (interleaving)
         assert np.all(o[1:, :] != o[:-1, :])
     assert np.all(row_owner(j, k, 64, 1) == 0)
+
+
+def test_balanced_row_owner_contiguous_and_balanced():
+    from paper_2512_01251_b200.parallel import balanced_row_owner
+    rng = np.random.default_rng(3)
+    counts = rng.integers(0, 40, 4096) * (rng.random(4096) < 0.3)
+    for n in (1, 2, 3, 4, 8):
+        own = balanced_row_owner(counts, n)
+        assert own.min() >= 0 and own.max() <= n - 1
+        assert np.all(np.diff(own.astype(int)) >= 0)  # contiguous row ranges
+        load = np.bincount(own, weights=counts, minlength=n)
+        assert load.max() - load.min() <= 2 * counts.max()  # balanced to within a row or two
+    assert balanced_row_owner(np.zeros(10, int), 4).max() == 0
