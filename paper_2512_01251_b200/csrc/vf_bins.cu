@@ -124,16 +124,6 @@ __global__ void __launch_bounds__(kIndWarps * 32, 3)
     }
 }
 
-// exact row SAT of the band path (reloads the face; rare)
-__device__ __noinline__ bool row_sat_exact(const double *__restrict__ faces, int64_t f, double y,
-                                           double z, double eps, double lx) {
-    double v[9], n[3];
-    load_face(faces, f, v, n);
-    SatFace sf;
-    sat_face_init(sf, v);
-    return sat_exact(sf, 0.0, VF_DSUB(y, eps), VF_DSUB(z, eps), lx, VF_DADD(y, eps), VF_DADD(z, eps));
-}
-
 // All levels in ONE pass over the face records (the per-level kernel reads
 // the 96 B/face records once per level): bit L of out[f] is the 1D indicator
 // of face f at level L.  Candidate rows are decided by the FP32 row
@@ -164,7 +154,7 @@ __global__ void __launch_bounds__(256, 3)
                         const double y = node_c(j, dx);
                         const int cls = row_class(rc, (float)VF_DSUB(y, v[1]), (float)VF_DSUB(z, v[2]));
                         if (cls == 0) continue;
-                        if (cls == 1 || row_sat_exact(faces, f, y, z, eps, li.len[0])) {
+                        if (cls == 1 || row_sat_exact_f(faces, f, y, z, eps, li.len[0])) {
                             hit = true;
                             break;
                         }

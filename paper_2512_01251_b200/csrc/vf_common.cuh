@@ -249,6 +249,11 @@ __device__ __forceinline__ int row_class(const RowClass &R, float Ry, float Rz) 
     return (acc && E0 >= t.x && E1 >= t.y && E2 >= t.z) ? 1 : 2;
 }
 
+// exact SAT of the x-row box (y, z) of the face record f (the classifiers'
+// undecided band; rare, so the face is re-read and the SAT set up here)
+static __device__ __noinline__ bool row_sat_exact_f(const double *__restrict__ faces, int64_t f,
+                                                    double y, double z, double eps, double lx);
+
 // ---------------------------------------------------------------------------
 // small helpers
 
@@ -270,6 +275,15 @@ __device__ __forceinline__ int warp_sum(int v) {
 
 __device__ __forceinline__ void latch_status(int32_t *d_status, int code) {
     if (d_status) atomicMax(d_status, code);
+}
+
+static __device__ __noinline__ bool row_sat_exact_f(const double *__restrict__ faces, int64_t f,
+                                                    double y, double z, double eps, double lx) {
+    double v[9], n[3];
+    load_face(faces, f, v, n);
+    SatFace sf;
+    sat_face_init(sf, v);
+    return sat_exact(sf, 0.0, VF_DSUB(y, eps), VF_DSUB(z, eps), lx, VF_DADD(y, eps), VF_DADD(z, eps));
 }
 
 }  // namespace vf

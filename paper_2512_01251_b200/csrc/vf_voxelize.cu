@@ -27,22 +27,26 @@ namespace vf {
 // --------------------------------------------------------------------------
 // K-vox
 
-struct VoxFace {        // shared-memory face record (24 doubles + FP32 row classifier)
-    SatFace s;
-    double n[3];
-    RowClass rc;
+struct VoxFace {  // shared-memory face record (128 B): what the row loop reads
+    double v1[3];    // first vertex (distances, classifier offsets)
+    double n[3];     // host unit normal
+    double yz[4];    // y / z extent of the face (exact box-axis reject)
+    RowClass rc;     // FP32 row classifier
+    int32_t fid;     // face id (A7 tie-break)
+    int32_t skip;    // |n_x| < EPS_PARALLEL: no x distance (A7)
 };
 
 constexpr int kVoxWarps = 4;
 
-__global__ void __launch_bounds__(kVoxWarps * 32)
+#ifndef VF_VOX_MINB
+#define VF_VOX_MINB 6
+#endif
+__global__ void __launch_bounds__(kVoxWarps * 32, VF_VOX_MINB)
     k_voxelize(LevelInfo li, int L, const int32_t *__restrict__ level_start,
                const int32_t *__restrict__ coords, uint8_t *__restrict__ masks,
                const int32_t *__restrict__ offsets, const int32_t *__restrict__ d_total,
                const int32_t *__restrict__ face_ids, const double *__restrict__ faces) {
     __shared__ VoxFace s_face[kVoxWarps][32];
-    __shared__ uint8_t s_skip[kVoxWarps][32];
-    __shared__ int32_t s_fid[kVoxWarps][32];
     const int64_t n_bins = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
     const int32_t total = *d_total;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -95,32 +99,40 @@ __global__ void __launch_bounds__(kVoxWarps * 32)
             const int cnt = min(32, n_f - base);
             if (lane < cnt) {
                 const int64_t f = face_ids[off + base + lane];
-                s_fid[wib][lane] = (int32_t)f;
                 double v[9], nn[3];
                 load_face(faces, f, v, nn);
                 VoxFace &vf_ = s_face[wib][lane];
-                sat_face_init(vf_.s, v);
-                vf_.n[0] = nn[0]; vf_.n[1] = nn[1]; vf_.n[2] = nn[2];
-                row_class_init(vf_.rc, vf_.s, nn, dx, eps, lx);
-                s_skip[wib][lane] = fabs(nn[0]) < li.eps_par;  // A7: no x distance
+                vf_.fid = (int32_t)f;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    vf_.v1[d] = v[d];
+                    vf_.n[d] = nn[d];
+                }
+                vf_.yz[0] = fmin(fmin(v[1], v[4]), v[7]);
+                vf_.yz[1] = fmax(fmax(v[1], v[4]), v[7]);
+                vf_.yz[2] = fmin(fmin(v[2], v[5]), v[8]);
+                vf_.yz[3] = fmax(fmax(v[2], v[5]), v[8]);
+                row_class_init(vf_.rc, v, nn, fmin(fmin(v[0], v[3]), v[6]), fmax(fmax(v[0], v[3]), v[6]),
+                               dx, eps, lx);
+                vf_.skip = fabs(nn[0]) < li.eps_par;  // A7: no x distance
             }
             __syncwarp();
             for (int q = half; q < cnt; q += 2) {
-                if (s_skip[wib][q]) continue;
                 const VoxFace &F = s_face[wib][q];
+                if (F.skip) continue;
                 // exact box-axis reject first (most pairs), then the FP32
                 // classifier; only undecided rows run the FP64 SAT
-                if (F.s.hi[1] < my || My < F.s.lo[1] || F.s.hi[2] < mz || Mz < F.s.lo[2]) continue;
-                const int cls = row_class(F.rc, (float)VF_DSUB(y, F.s.v[1]), (float)VF_DSUB(z, F.s.v[2]));
+                if (F.yz[1] < my || My < F.yz[0] || F.yz[3] < mz || Mz < F.yz[2]) continue;
+                const int cls = row_class(F.rc, (float)VF_DSUB(y, F.v1[1]), (float)VF_DSUB(z, F.v1[2]));
                 if (cls == 0) continue;
-                if (cls == 2 && !sat_exact(F.s, 0.0, my, mz, lx, My, Mz)) continue;
+                if (cls == 2 && !row_sat_exact_f(faces, F.fid, y, z, eps, lx)) continue;
                 const double nx = F.n[0];
+                const int fid = F.fid;
 #pragma unroll
                 for (int I = 0; I < 4; ++I) {
-                    const double d = VF_DDIV(plane_num(F.s.v, F.n, x[I], y, z), nx);
+                    const double d = VF_DDIV(plane_num(F.v1, F.n, x[I], y, z), nx);
                     const double ad = fabs(d);
                     // A7: smaller |d|, ties -> lower face id (bins need not be sorted)
-                    const int fid = s_fid[wib][q];
                     if (ad < bd[I] || (ad == bd[I] && fid < bp[I])) {
                         bd[I] = ad;
                         bp[I] = fid;
