@@ -251,6 +251,23 @@ int vf_shard_links(const vf_config *cfg, const double *d_faces, int64_t n_faces,
                    vf_grid *grid, const int32_t *d_cmap, const int32_t *d_n_b,
                    float *d_lengths, int64_t lengths_cap, void *d_ws, size_t ws_bytes,
                    void *stream);
+/* ---- LUT consumer: D3Q27 BGK collide/stream of
+ * one level with SBB / interpolated bounce-back walls from the LinkTable
+ * (SPEC.md:398-411).  State = post-collision populations f[27][(e-s)*64]
+ * (f32, SoA) over the level's block ids [s, e). */
+typedef struct {
+    double tau;       /* BGK relaxation time of the level (> 1/2)          */
+    double u_in[3];   /* inlet velocity (lattice units) at the x = 0 face  */
+    int32_t ibb;      /* 1 = Bouzidi linear IBB from the LUT, 0 = SBB      */
+    int32_t open_x;   /* 1 = inlet (x = 0) / outlet (x = l_x) faces, 0 = SBB */
+} vf_flow;
+int vf_lbm_init(const vf_grid *grid, int32_t s, int32_t e, double rho, const double *u,
+                float *d_f, void *stream);
+/* one step: d_fout = collide(stream(d_fin)); the wall-link momentum exchange
+ * is ADDED to d_force[3] (lattice units) when d_force is not NULL */
+int vf_lbm_step(const vf_config *cfg, const vf_grid *grid, int level, int32_t s, int32_t e,
+                const int32_t *d_cmap, const float *d_lengths, const float *d_fin,
+                float *d_fout, const vf_flow *flow, double *d_force, void *stream);
 /* copy the grid's latched device status to the host (synchronizes) */
 int vf_check_status(const vf_grid *grid, void *stream);
 /* test hook: capacity of the link-length band list (candidates the FP32

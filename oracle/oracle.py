@@ -77,6 +77,8 @@ def lib():
             "orc_links_copy": (None, [P, P, P]),
             "orc_links_free": (None, [P]),
             "orc_parity_inside": (None, [P, i64, P, i64, C.c_double, P]),
+            "orc_lbm_equilibrium": (None, [C.c_double, P, P]),
+            "orc_lbm_step": (i32, [P, P, P, i32, i32, i32, P, P, P, P, C.c_double, P, i32, i32, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -328,3 +330,34 @@ def parity_inside(fc, pts, tol=1e-9):
     out = np.zeros(len(pts), dtype=np.uint8)
     lib().orc_parity_inside(_p(fc), len(fc), _p(pts), len(pts), float(tol), _p(out))
     return out
+
+
+# ---------------------------------------------------------------------------
+# LUT consumer (lbm_oracle.c): D3Q27 BGK collide/stream of one level
+
+
+def lbm_equilibrium(rho, u):
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.zeros(27)
+    lib().orc_lbm_equilibrium(float(rho), _p(u), _p(out))
+    return out
+
+
+def lbm_step(coords, nbr, masks, s, e, cells_x, cmap, lengths, fin, tau, u_in, ibb=True,
+             open_x=True):
+    """One step of level blocks [s, e); fin = (27, (e-s)*64)
+    float32 post-collision populations.  Returns (fout, force[3])."""
+    coords = np.ascontiguousarray(coords, dtype=np.int32)
+    nbr = np.ascontiguousarray(nbr, dtype=np.int32)
+    masks = np.ascontiguousarray(masks, dtype=np.uint8)
+    cmap = np.ascontiguousarray(cmap, dtype=np.int32)
+    lengths = np.ascontiguousarray(lengths, dtype=np.float32)
+    fin = np.ascontiguousarray(fin, dtype=np.float32)
+    fout = np.zeros_like(fin)
+    u = np.ascontiguousarray(u_in, dtype=np.float64)
+    force = np.zeros(3)
+    rc = lib().orc_lbm_step(_p(coords), _p(nbr), _p(masks), int(s), int(e), int(cells_x), _p(cmap),
+                            _p(lengths), _p(fin), _p(fout), float(tau), _p(u), int(bool(ibb)),
+                            int(bool(open_x)), _p(force))
+    assert rc == 0
+    return fout, force

@@ -14,12 +14,12 @@ from .mesh import TriangleMesh, l_spec_bound, make_icosphere, make_torus, refine
 
 __all__ = ["EmbedConfig", "TriangleMesh", "make_icosphere", "make_torus", "refine_faces",
            "l_spec_bound", "MeshError", "CapacityError", "BinCapError", "CudaError",
-           "VoxforestError", "binning", "forest", "voxelizer"]
+           "VoxforestError", "binning", "forest", "voxelizer", "solver"]
 
 
 def __getattr__(name):
     # lazy submodules: importing the package must not require CUDA/torch
-    if name in ("binning", "forest", "voxelizer", "datatypes"):
+    if name in ("binning", "forest", "voxelizer", "datatypes", "solver", "parallel"):
         import importlib
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)

@@ -23,3 +23,20 @@ def _paired_directions():
 D3Q27_C = _paired_directions()
 D3Q27_OPPOSITE = np.array([0] + [q + 1 if q % 2 == 1 else q - 1 for q in range(1, 27)])
 REPRESENTATIVES = np.arange(1, 27, 2)
+
+# D3Q27 weights (SPEC.md VelocitySet: sum w = 1, sum w c = 0, sum w c c^T = I/3)
+_NZ = np.abs(D3Q27_C).sum(1)
+D3Q27_W = np.where(_NZ == 0, 8 / 27, np.where(_NZ == 1, 2 / 27, np.where(_NZ == 2, 1 / 54, 1 / 216)))
+
+
+class _VelocitySet:
+    """SPEC.md:384-386 VelocitySet (D3Q27)."""
+    D = 3
+    Q = 27
+    c = D3Q27_C
+    w = D3Q27_W
+    opposite = D3Q27_OPPOSITE
+    cs2 = 1.0 / 3.0
+
+
+D3Q27 = _VelocitySet()
