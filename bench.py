@@ -34,6 +34,11 @@ WORKLOADS = {
                n_x=64, l_max=4),
     "c4": dict(desc="C4: torus 3000x1200 (7,200,000 faces), N_x=64, L_max=5", kind="torus", m=3000,
                n=1200, n_x=64, l_max=5),
+    # C3: sphere D_s = 1/64 (icosphere k=5) in a 128^3 root, L_max=3, Re=20,
+    # u_in=0.05: the embed plus the LUT consumer's
+    # collide/stream step per level
+    "c3": dict(desc="C3: sphere D=1/64 (icosphere k=5, 20,480 faces), N_x=128, L_max=3, Re=20 LBM",
+               kind="sphere", sub=5, diameter=1.0 / 64, n_x=128, l_max=3, lbm=True),
 }
 METRIC = "geometry-embed cells classified/s"
 UNIT = "cells/s"
@@ -42,7 +47,8 @@ UNIT = "cells/s"
 def make_mesh(w, rank):
     from paper_2512_01251_b200 import make_icosphere, make_torus
     from paper_2512_01251_b200.mesh import translate
-    m = make_icosphere((0.5, 0.5, 0.5), 0.5, w["sub"]) if w["kind"] == "sphere" else make_torus(w["m"], w["n"])
+    m = (make_icosphere((0.5, 0.5, 0.5), w.get("diameter", 0.5), w["sub"]) if w["kind"] == "sphere"
+         else make_torus(w["m"], w["n"]))
     if rank:
         rng = np.random.default_rng(rank)
         m = translate(m, (rng.random(3) - 0.5) / 64.0)
@@ -201,6 +207,51 @@ def run_reference(args, w, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+def lbm_block(eng, w, args, flush):
+    """C3: the LUT consumer on the embedded grid.  Per level one BGK
+    collide/stream step (csrc/vf_lbm.cu; IBB walls from the LUT on the finest
+    level, SBB below), timed with CUDA events; a coarse step of the nested
+    hierarchy is sum_L 2^L t_L (the interface exchange between levels is not
+    built and not counted).  Embed overhead = embed time / coarse step."""
+    import torch
+    from paper_2512_01251_b200.solver import FlowConfig, LbmLevel
+    grid, table = eng.run()
+    Lf = grid.n_levels - 1
+    D_f = w["diameter"] * 4 * w["n_x"] // 4 * 2 ** Lf  # sphere diameter in finest cells
+    peak, peak_kind = peaks()
+    levels = []
+    coarse_ms = 0.0
+    for L in range(grid.n_levels):
+        s, e = grid.level_range(L)
+        flow = FlowConfig(Re=20.0, u_in=0.05, D_s=D_f / 2 ** (Lf - L),
+                          bc_scheme="IBB" if L == Lf else "SBB")
+        lv = LbmLevel(grid, L, table if L == Lf else None, flow).init_equilibrium(1.0, (0.05, 0, 0))
+        for _ in range(3):
+            lv.step(1, force=False)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k = max(args.steps, 10)
+        flush.fill_(1.0)
+        a.record()
+        lv.step(k, force=(L == Lf))
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / k
+        cells = (e - s) * 64
+        nbytes = cells * (27 * 4 * 2 + 1)
+        levels.append({"level": L, "blocks": e - s, "cells": cells, "tau": flow.tau,
+                       "step_ms": ms, "cell_updates_per_s": cells / (ms / 1e3),
+                       "hbm_gbs": nbytes / (ms / 1e3) / 1e9, "hbm_frac": nbytes / (ms / 1e3) / 1e9 / peak})
+        coarse_ms += 2 ** L * ms
+        if L == Lf:
+            drag = lv.force.cpu().numpy() / k
+    return {"levels": levels, "coarse_step_ms": coarse_ms,
+            "wall_force_lattice": [float(x) for x in drag],
+            "note": "one BGK collide/stream per level (f32 SoA, 216 B/cell algorithmic), IBB from the "
+                    "LUT on the finest level; coarse step = sum_L 2^L t_L without interface exchange",
+            "peak_kind": peak_kind}
+
+
 def timed_steps(run, steps, flush, ws):
     """Barrier + sync, then `steps` runs each bracketed by CUDA events on the
     current stream (the L2 flush between steps stays outside the events);
@@ -318,6 +369,11 @@ def main():
     else:
         n_b = int(run()[1].n_b)
 
+    lbm = lbm_block(eng, w, args, flush) if (w.get("lbm") and not sharded) else None
+    if lbm:
+        lbm["embed_ms"] = med(step_ms)
+        lbm["embed_over_coarse_step"] = med(step_ms) / lbm["coarse_step_ms"]
+
     e2e = None
     if not args.no_e2e:
         fc = torch.from_numpy(np.ascontiguousarray(mesh.faces_coord)).pin_memory()
@@ -375,7 +431,7 @@ def main():
                    "embed_ms_median": med(step_ms), "stage_ms_eager": stages,
                    "l2": "64 Mi-float (256 MB) buffer rewritten between steps, outside step events",
                    "parallelism": par},
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "lbm": lbm,
         "gpu_launches": int(kernels_per_step * args.steps),
         "gpu_launch_note": (f"{kernels_per_step} kernels per embed" +
                             ("" if sharded else ", issued as one CUDA graph per step")),

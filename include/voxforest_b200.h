@@ -264,10 +264,12 @@ typedef struct {
 int vf_lbm_init(const vf_grid *grid, int32_t s, int32_t e, double rho, const double *u,
                 float *d_f, void *stream);
 /* one step: d_fout = collide(stream(d_fin)); the wall-link momentum exchange
- * is ADDED to d_force[3] (lattice units) when d_force is not NULL */
+ * is ADDED to d_force[3] (lattice units) when d_force is not NULL.  d_scratch:
+ * e - s + 1 int32 (the wall-link block list of the step) */
 int vf_lbm_step(const vf_config *cfg, const vf_grid *grid, int level, int32_t s, int32_t e,
                 const int32_t *d_cmap, const float *d_lengths, const float *d_fin,
-                float *d_fout, const vf_flow *flow, double *d_force, void *stream);
+                float *d_fout, const vf_flow *flow, double *d_force, int32_t *d_scratch,
+                void *stream);
 /* copy the grid's latched device status to the host (synchronizes) */
 int vf_check_status(const vf_grid *grid, void *stream);
 /* test hook: capacity of the link-length band list (candidates the FP32

@@ -39,144 +39,154 @@ __device__ __forceinline__ int32_t cell_at(const int32_t *__restrict__ nbr, int3
     return __ldg(nbr + 27 * (int64_t)b + slot_of(ox, oy, oz));
 }
 
-// wall links (SOLID y: SBB / Bouzidi linear IBB with the LUT q_w) and domain
-// faces (inlet velocity bounce-back, outlet anti-bounce-back, lateral SBB) of
-// one cell; f[o] is NaN for the populations to resolve
-__device__ __noinline__ void resolve_links(float *f, int64_t x, int64_t n, int32_t b, int t,
-                                           int32_t s, int32_t e, int cells_x,
-                                           const int32_t *__restrict__ coords,
-                                           const int32_t *__restrict__ nbr,
-                                           const uint8_t *__restrict__ masks,
-                                           const int32_t *__restrict__ cmap,
-                                           const float *__restrict__ lengths,
-                                           const float *__restrict__ fin, const vf_flow &flow,
-                                           const float *uin, float &Fx, float &Fy, float &Fz) {
-    const int I = t & 3, J = (t >> 2) & 3, K = t >> 4;
-    // moments of x (outlet anti-bounce-back)
-    float rx = 0.f, u0 = 0.f, u1 = 0.f, u2 = 0.f;
-    for (int q = 0; q < 27; ++q) {
-        const float v = fin[q * n + x];
-        rx += v;
-        u0 += v * c27(q, 0);
-        u1 += v * c27(q, 1);
-        u2 += v * c27(q, 2);
-    }
-    const float ux[3] = {u0 / rx, u1 / rx, u2 / rx};
-    const int32_t slot = flow.ibb ? cmap[b] : -1;
-    for (int o = 0; o < 27; ++o) {
-        if (!isnan(f[o])) continue;
-        const int q = lopp(o);
-        int ty;
-        const int32_t y = cell_at(nbr, b, I, J, K, -c27(o, 0), -c27(o, 1), -c27(o, 2), ty);
-        const float fq = fin[q * n + x];
-        const float cqx = (float)c27(q, 0), cqy = (float)c27(q, 1), cqz = (float)c27(q, 2);
-        if (y == VF_NB_OUTSIDE) {  // domain face
-            const int gx = 4 * coords[4 * (int64_t)b] + I - c27(o, 0);
-            if (!flow.open_x) {
-                f[o] = fq;  // closed box: SBB on every face
-            } else if (gx < 0) {  // inlet: velocity bounce-back, rho_w = 1
-                f[o] = fq - 6.0f * c_lw[q] * (cqx * uin[0] + cqy * uin[1] + cqz * uin[2]);
-            } else if (gx >= cells_x) {  // outlet: anti-bounce-back, rho_w = 1
-                const float cq = cqx * ux[0] + cqy * ux[1] + cqz * ux[2];
-                const float uu = ux[0] * ux[0] + ux[1] * ux[1] + ux[2] * ux[2];
-                f[o] = -fq + 2.0f * c_lw[q] * (1.0f + 4.5f * cq * cq - 1.5f * uu);
-            } else {
-                f[o] = fq;  // lateral faces: SBB
-            }
-            continue;
-        }
-        // wall link x -> y (SOLID cell): Bouzidi linear with the LUT q_w
-        const float qw = slot >= 0 ? lengths[((int64_t)slot * 27 + q) * 64 + t] : -1.0f;
-        float fo;
-        if (!(qw > 0.0f)) {
-            fo = fq;  // SBB
-        } else if (qw < 0.5f) {
-            int tz;
-            const int32_t z = cell_at(nbr, b, I, J, K, c27(o, 0), c27(o, 1), c27(o, 2), tz);
-            if (z >= s && z < e && masks[64 * (int64_t)z + tz] != VF_SOLID)
-                fo = 2.0f * qw * fq + (1.0f - 2.0f * qw) * fin[q * n + (int64_t)(z - s) * 64 + tz];
-            else
-                fo = fq;
-        } else {
-            fo = fq / (2.0f * qw) + (2.0f * qw - 1.0f) / (2.0f * qw) * fin[o * n + x];
-        }
-        f[o] = fo;
-        Fx += (fq + fo) * cqx;
-        Fy += (fq + fo) * cqy;
-        Fz += (fq + fo) * cqz;
-    }
-}
+// Warp per block (two 32-cell halves): the block's 27 neighbour ids, their
+// solid64 words (finalize; bit t = cell t SOLID) and the block's x index are
+// staged in per-warp shared memory, indexed by direction code
+// (dx+1) + 3(dy+1) + 9(dz+1), so a pulled population costs one shared-memory
+// lookup and one global load that is coalesced within a block.  Domain faces
+// (lateral SBB, inlet velocity bounce-back, outlet anti-bounce-back) are
+// resolved inline.  WALLS = false is the bulk pass over every block: a wall
+// link gets a provisional SBB value and its block is appended to the wall
+// list; WALLS = true re-runs the listed blocks with the wall rule (SBB or
+// Bouzidi linear IBB with q_w from the LUT) and the momentum exchange, and
+// overwrites those cells (same f_in, so the two passes commute).
+constexpr int kLbmWarps = 8;
 
-__global__ void __launch_bounds__(256, 3)
-    k_lbm_step(int32_t s, int32_t e, int cells_x, const int32_t *__restrict__ coords,
-               const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
-               const int32_t *__restrict__ cmap, const float *__restrict__ lengths,
-               const float *__restrict__ fin, float *__restrict__ fout, vf_flow flow,
-               double *__restrict__ d_force) {
+template <bool WALLS>
+__global__ void __launch_bounds__(kLbmWarps * 32, 3)
+    k_lbm_cells(int32_t s, int32_t e, int cells_x, const int32_t *__restrict__ coords,
+                const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
+                const uint64_t *__restrict__ solid64, const int32_t *__restrict__ cmap,
+                const float *__restrict__ lengths, const float *__restrict__ fin,
+                float *__restrict__ fout, vf_flow flow, int32_t *__restrict__ wall_list,
+                int32_t *__restrict__ n_wall, double *__restrict__ d_force) {
+    __shared__ int32_t s_nb[kLbmWarps][27];
+    __shared__ unsigned long long s_sol[kLbmWarps][27];
     const int64_t n = (int64_t)(e - s) * 64;
+    const int nitems = WALLS ? *n_wall : e - s;
     const float omega = 1.0f / (float)flow.tau;
     const float uin[3] = {(float)flow.u_in[0], (float)flow.u_in[1], (float)flow.u_in[2]};
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     float Fx = 0.f, Fy = 0.f, Fz = 0.f;
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
-         x += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t b = s + (int32_t)(x >> 6);
-        const int t = (int)(x & 63);
-        const uint8_t m = masks[64 * (int64_t)b + t];
-        if (m == VF_SOLID || m == VF_GHOST) {
-#pragma unroll
-            for (int q = 0; q < 27; ++q) fout[q * n + x] = fin[q * n + x];
-            continue;
+    for (int it = blockIdx.x * kLbmWarps + w; it < nitems; it += gridDim.x * kLbmWarps) {
+        const int lb = WALLS ? wall_list[it] : it;
+        const int32_t b = s + lb;
+        __syncwarp();
+        if (lane < 27) {
+            const int dx = lane % 3 - 1, dy = (lane / 3) % 3 - 1, dz = lane / 9 - 1;
+            const int32_t v = (lane == 13) ? b : __ldg(nbr + 27 * (int64_t)b + slot_of(dx, dy, dz));
+            s_nb[w][lane] = v;
+            s_sol[w][lane] = (v >= s && v < e)
+                                 ? __ldg(reinterpret_cast<const unsigned long long *>(solid64) + v)
+                                 : ~0ull;
         }
-        const int I = t & 3, J = (t >> 2) & 3, K = t >> 4;
-        float f[27];
-        bool wall_any = false, outside_any = false;
+        const int bx = __ldg(coords + 4 * (int64_t)b);
+        const int32_t slot = (WALLS && flow.ibb) ? cmap[b] : -1;
+        __syncwarp();
+        bool wall_blk = false;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const int t = lane + 32 * h;
+            const int I = t & 3, J = (t >> 2) & 3, K = t >> 4;
+            const int64_t x = (int64_t)lb * 64 + t;
+            const uint8_t m = masks[64 * (int64_t)b + t];
+            if (m == VF_SOLID || m == VF_GHOST) {
+                if (!WALLS) {
 #pragma unroll
-        for (int o = 0; o < 27; ++o) {
-            int ty;
-            const int32_t y = cell_at(nbr, b, I, J, K, -c27(o, 0), -c27(o, 1), -c27(o, 2), ty);
-            if (y >= s && y < e && masks[64 * (int64_t)y + ty] != VF_SOLID) {
-                f[o] = fin[o * n + (int64_t)(y - s) * 64 + ty];
-            } else {
-                f[o] = __int_as_float(0x7fc00000);  // resolved below (rare)
-                if (y == VF_NB_OUTSIDE) outside_any = true;
-                else wall_any = true;
+                    for (int q = 0; q < 27; ++q) fout[q * n + x] = fin[q * n + x];
+                }
+                continue;
+            }
+            // outlet cells (x = l_x face): velocity of x for the anti-bounce-back
+            float v0 = 0.f, v1 = 0.f, v2 = 0.f;
+            if (flow.open_x && 4 * bx + I == cells_x - 1) {
+                float rx = 0.f;
+#pragma unroll
+                for (int k = 0; k < 27; ++k) {
+                    const float v = fin[k * n + x];
+                    rx += v;
+                    v0 += v * c27(k, 0);
+                    v1 += v * c27(k, 1);
+                    v2 += v * c27(k, 2);
+                }
+                v0 /= rx; v1 /= rx; v2 /= rx;
+            }
+            float f[27];
+            bool wall = false;
+#pragma unroll
+            for (int o = 0; o < 27; ++o) {
+                const int X = I - c27(o, 0), Y = J - c27(o, 1), Z = K - c27(o, 2);
+                const int code = ((X >> 2) + 1) + 3 * ((Y >> 2) + 1) + 9 * ((Z >> 2) + 1);
+                const int ty = (X & 3) + 4 * (Y & 3) + 16 * (Z & 3);
+                const int32_t y = s_nb[w][code];
+                if (!((s_sol[w][code] >> ty) & 1ull)) {  // a level cell that is not SOLID
+                    f[o] = fin[o * n + (int64_t)(y - s) * 64 + ty];
+                    continue;
+                }
+                const int q = o == 0 ? 0 : ((o & 1) ? o + 1 : o - 1);
+                const float fq = fin[q * n + x];
+                float v = fq;  // SBB: lateral faces, SBB walls (provisional in the bulk pass)
+                if (y == VF_NB_OUTSIDE) {
+                    const int gx = 4 * bx + X;
+                    if (flow.open_x && gx < 0) {  // inlet: velocity bounce-back, rho_w = 1
+                        v -= 6.0f * c_lw[q] * (c27(q, 0) * uin[0] + c27(q, 1) * uin[1] + c27(q, 2) * uin[2]);
+                    } else if (flow.open_x && gx >= cells_x) {  // outlet: anti-bounce-back, rho_w = 1
+                        const float cq = c27(q, 0) * v0 + c27(q, 1) * v1 + c27(q, 2) * v2;
+                        v = -fq + 2.0f * c_lw[q] * (1.0f + 4.5f * cq * cq - 1.5f * (v0 * v0 + v1 * v1 + v2 * v2));
+                    }
+                } else {  // wall link x -> y (SOLID cell, or a missing block next to ghosts)
+                    wall = true;
+                    if (WALLS) {
+                        const float qw = slot >= 0 ? lengths[((int64_t)slot * 27 + q) * 64 + t] : -1.0f;
+                        if (qw > 0.0f && qw < 0.5f) {
+                            // second node behind x: x + c_o = x - c_q
+                            const int X2 = I + c27(o, 0), Y2 = J + c27(o, 1), Z2 = K + c27(o, 2);
+                            const int code2 = ((X2 >> 2) + 1) + 3 * ((Y2 >> 2) + 1) + 9 * ((Z2 >> 2) + 1);
+                            const int tz = (X2 & 3) + 4 * (Y2 & 3) + 16 * (Z2 & 3);
+                            if (!((s_sol[w][code2] >> tz) & 1ull))
+                                v = 2.0f * qw * fq + (1.0f - 2.0f * qw) *
+                                                         fin[q * n + (int64_t)(s_nb[w][code2] - s) * 64 + tz];
+                        } else if (qw >= 0.5f) {
+                            v = fq / (2.0f * qw) + (2.0f * qw - 1.0f) / (2.0f * qw) * fin[o * n + x];
+                        }
+                        Fx += (fq + v) * c27(q, 0);
+                        Fy += (fq + v) * c27(q, 1);
+                        Fz += (fq + v) * c27(q, 2);
+                    }
+                }
+                f[o] = v;
+            }
+            wall_blk |= wall;
+            if (WALLS && !wall) continue;  // the bulk pass's value is exact
+            float rho = 0.f, u0 = 0.f, u1 = 0.f, u2 = 0.f;
+#pragma unroll
+            for (int o = 0; o < 27; ++o) {
+                rho += f[o];
+                u0 += f[o] * c27(o, 0);
+                u1 += f[o] * c27(o, 1);
+                u2 += f[o] * c27(o, 2);
+            }
+            const float ir = 1.0f / rho;
+            u0 *= ir; u1 *= ir; u2 *= ir;
+            const float uu = 1.5f * (u0 * u0 + u1 * u1 + u2 * u2);
+#pragma unroll
+            for (int o = 0; o < 27; ++o) {
+                const float cu = c27(o, 0) * u0 + c27(o, 1) * u1 + c27(o, 2) * u2;
+                const float feq = c_lw[o] * rho * (1.0f + 3.0f * cu + 4.5f * cu * cu - uu);
+                fout[o * n + x] = f[o] + (feq - f[o]) * omega;
             }
         }
-        if (outside_any || wall_any) {  // rare: resolved out of line on a local copy
-            float fl[27];
-#pragma unroll
-            for (int o = 0; o < 27; ++o) fl[o] = f[o];
-            resolve_links(fl, x, n, b, t, s, e, cells_x, coords, nbr, masks, cmap, lengths, fin,
-                          flow, uin, Fx, Fy, Fz);
-#pragma unroll
-            for (int o = 0; o < 27; ++o) f[o] = fl[o];
-        }
-        float rho = 0.f, u0 = 0.f, u1 = 0.f, u2 = 0.f;
-#pragma unroll
-        for (int o = 0; o < 27; ++o) {
-            rho += f[o];
-            u0 += f[o] * c27(o, 0);
-            u1 += f[o] * c27(o, 1);
-            u2 += f[o] * c27(o, 2);
-        }
-        const float ir = 1.0f / rho;
-        u0 *= ir; u1 *= ir; u2 *= ir;
-        const float uu = 1.5f * (u0 * u0 + u1 * u1 + u2 * u2);
-#pragma unroll
-        for (int o = 0; o < 27; ++o) {
-            const float cu = c27(o, 0) * u0 + c27(o, 1) * u1 + c27(o, 2) * u2;
-            const float feq = c_lw[o] * rho * (1.0f + 3.0f * cu + 4.5f * cu * cu - uu);
-            fout[o * n + x] = f[o] + (feq - f[o]) * omega;
-        }
+        if (!WALLS && __any_sync(0xffffffffu, wall_blk) && lane == 0)
+            wall_list[atomicAdd(n_wall, 1)] = lb;
     }
-    if (d_force) {
+    if (WALLS && d_force) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             Fx += __shfl_xor_sync(0xffffffffu, Fx, off);
             Fy += __shfl_xor_sync(0xffffffffu, Fy, off);
             Fz += __shfl_xor_sync(0xffffffffu, Fz, off);
         }
-        if ((threadIdx.x & 31) == 0 && (Fx != 0.f || Fy != 0.f || Fz != 0.f)) {
+        if (lane == 0 && (Fx != 0.f || Fy != 0.f || Fz != 0.f)) {
             atomicAdd(d_force + 0, (double)Fx);
             atomicAdd(d_force + 1, (double)Fy);
             atomicAdd(d_force + 2, (double)Fz);
@@ -220,18 +230,27 @@ int vf_lbm_init(const vf_grid *g, int32_t s, int32_t e, double rho, const double
 
 int vf_lbm_step(const vf_config *cfg, const vf_grid *g, int level, int32_t s, int32_t e,
                 const int32_t *cmap, const float *lengths, const float *fin, float *fout,
-                const vf_flow *flow, double *d_force, void *stream) {
-    if (!cfg || !g || !fin || !fout || !flow || fin == fout || s < 0 || e < s || e > g->capacity ||
-        level < 0 || level >= VF_MAX_LEVELS || !(flow->tau > 0.5) || (flow->ibb && (!cmap || !lengths)))
+                const vf_flow *flow, double *d_force, int32_t *d_scratch, void *stream) {
+    if (!cfg || !g || !fin || !fout || !flow || !d_scratch || fin == fout || s < 0 || e < s ||
+        e > g->capacity || level < 0 || level >= VF_MAX_LEVELS || !(flow->tau > 0.5) ||
+        (flow->ibb && (!cmap || !lengths)))
         return set_error(VF_EARG, "vf_lbm_step: bad argument (tau must exceed 1/2)");
     if (e == s) return VF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
     const int cells_x = 4 * (cfg->nb[0] << level);
-    int64_t grid = ((int64_t)(e - s) * 64 + 255) / 256;
-    if (grid > max_ctas(8)) grid = max_ctas(8);
-    k_lbm_step<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(s, e, cells_x, g->d_coords, g->d_nbr,
-                                                             g->d_masks, cmap, lengths, fin, fout,
-                                                             *flow, d_force);
-    return check_launch("k_lbm_step");
+    int32_t *n_wall = d_scratch, *wall_list = d_scratch + 1;
+    cudaMemsetAsync(n_wall, 0, sizeof(int32_t), st);
+    int64_t grid = ((int64_t)(e - s) + kLbmWarps - 1) / kLbmWarps;
+    if (grid > max_ctas(3)) grid = max_ctas(3);
+    k_lbm_cells<false><<<(int)grid, kLbmWarps * 32, 0, st>>>(
+        s, e, cells_x, g->d_coords, g->d_nbr, g->d_masks, g->d_solid64, cmap, lengths, fin, fout, *flow,
+        wall_list, n_wall, nullptr);
+    int rc = check_launch("k_lbm_cells");
+    if (rc) return rc;
+    k_lbm_cells<true><<<max_ctas(2), kLbmWarps * 32, 0, st>>>(
+        s, e, cells_x, g->d_coords, g->d_nbr, g->d_masks, g->d_solid64, cmap, lengths, fin, fout, *flow,
+        wall_list, n_wall, d_force);
+    return check_launch("k_lbm_walls");
 }
 
 }  // extern "C"

@@ -79,6 +79,7 @@ class LbmLevel:
         self.f = [torch.empty((27, n), dtype=torch.float32, device="cuda") for _ in range(2)]
         self.cur = 0
         self.force = torch.zeros(3, dtype=torch.float64, device="cuda")
+        self.scratch = torch.zeros(self.e - self.s + 1, dtype=torch.int32, device="cuda")
         self.c = _lib.make_config(grid.cfg)
         self.vf = VfFlow()
         self.vf.tau = float(tau if tau is not None else flow.tau)
@@ -116,7 +117,8 @@ class LbmLevel:
             _lib.check(self.lib.vf_lbm_step(
                 C.byref(self.c), C.byref(gs), self.level, self.s, self.e, _lib.ptr(self.cmap), lengths,
                 _lib.ptr(self.f[self.cur]), _lib.ptr(self.f[self.cur ^ 1]), C.byref(self.vf),
-                _lib.ptr(self.force) if force else None, _lib.stream_ptr()), "collide_stream_level")
+                _lib.ptr(self.force) if force else None, _lib.ptr(self.scratch), _lib.stream_ptr()),
+                "collide_stream_level")
             self.cur ^= 1
         return self.force
 
