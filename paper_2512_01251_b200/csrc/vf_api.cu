@@ -120,6 +120,7 @@ static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 // embed workspace layout
 struct EmbedWs {
     vf_bins bins;
+    vf_bins bins2;       // second bins buffer: bins(L+1) built while level L runs
     void *bins_ws;
     size_t bins_ws_bytes;
     void *prop_ws, *mark_ws, *adapt_ws, *tab_ws, *link_ws;
@@ -148,6 +149,13 @@ static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *b
     t.bins.d_map = (int32_t *)take(sizeof(int32_t) * (size_t)(F + 1));
     t.bins.d_n_map = (int32_t *)take(64);
     t.bins.d_n_face_ids = (int32_t *)take(64);
+    t.bins2 = t.bins;
+    t.bins2.d_counts = (int32_t *)take(sizeof(int32_t) * (size_t)nbins);
+    t.bins2.d_offsets = (int32_t *)take(sizeof(int32_t) * (size_t)nbins);
+    t.bins2.d_face_ids = (int32_t *)take(sizeof(int32_t) * (size_t)(F * nlim + 1));
+    t.bins2.d_map = (int32_t *)take(sizeof(int32_t) * (size_t)(F + 1));
+    t.bins2.d_n_map = (int32_t *)take(64);
+    t.bins2.d_n_face_ids = (int32_t *)take(64);
     t.bins_ws_bytes = bins_workspace_size(F, nlim, nbins);
     t.bins_ws = take(t.bins_ws_bytes);
     t.prop_b = propagate_level_workspace_size(cfg, Lf);
@@ -361,6 +369,36 @@ static void rec(void **ev, int n_ev, int *k, cudaStream_t st) {
     ++*k;
 }
 
+// side stream + events of the bins pipeline (one set per device, created on
+// first use; the embed is single-threaded per device, see the header)
+struct SideStream {
+    cudaStream_t st = nullptr;
+    cudaEvent_t fork = nullptr, bins[2] = {nullptr, nullptr}, vox[2] = {nullptr, nullptr}, join = nullptr;
+};
+static SideStream g_side[64];
+
+static int side_stream(SideStream **out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaGetDevice");
+    SideStream &s = g_side[dev & 63];
+    if (!s.st) {
+        e = cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking);
+        cudaEvent_t *evs[] = {&s.fork, &s.bins[0], &s.bins[1], &s.vox[0], &s.vox[1], &s.join};
+        for (cudaEvent_t *ev : evs)
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return set_cuda_error(e, "side stream");
+    }
+    *out = &s;
+    return VF_OK;
+}
+
+// Phase 1.  The spatial bins do not depend on the grid, so they are built on
+// a side stream one level AHEAD of the level pipeline (ping-pong buffers):
+// bins(L+1) overlaps voxelize / propagate / mark / adapt of level L; the main
+// stream only waits for bins(L) before voxelizing L, and the side stream
+// waits for voxelize(L-1) before reusing its buffer.  Captured into the
+// embed graph the two streams become parallel branches.
 int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int use_filter,
                     vf_grid *g, int32_t *cmap, int32_t *d_n_b, void *ws, size_t ws_bytes,
                     void *stream, void **events) {
@@ -370,18 +408,36 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     if (embed_layout(*cfg, F, g->capacity, (char *)ws, &w) > ws_bytes)
         return set_error(VF_EARG, "vf_embed_phase1: workspace too small");
     cudaStream_t st = (cudaStream_t)stream;
+    SideStream *side = nullptr;
+    VF_TRY(side_stream(&side));
+    cudaStream_t s2 = side->st;
+    vf_bins *buf[2] = {&w.bins, &w.bins2};
     const int n_ev = 64;
     int k = 0;
     rec(events, n_ev, &k, st);  // 0: start
     VF_TRY(init_forest_impl(*cfg, g, st));
+    // fork the bins pipeline (after init: it shares the status word)
+    cudaEventRecord(side->fork, st);
+    cudaStreamWaitEvent(s2, side->fork, 0);
     // Alg. 1 indicators of every level in one pass over the face records
-    if (use_filter) VF_TRY(launch_indicators_all(*cfg, faces, F, w.ind_bits, st));
+    if (use_filter) VF_TRY(launch_indicators_all(*cfg, faces, F, w.ind_bits, s2));
+    auto build = [&](int L) {
+        return build_bins_impl(make_level(*cfg, L), nlim_of(*cfg), faces, F, 0, use_filter, buf[L & 1],
+                               g->d_status, w.bins_ws, w.bins_ws_bytes, s2, w.ind_bits, false);
+    };
+    VF_TRY(build(0));
+    cudaEventRecord(side->bins[0], s2);
     for (int L = 0; L < cfg->l_max; ++L) {
         const LevelInfo li = make_level(*cfg, L);
-        VF_TRY(build_bins_impl(li, nlim_of(*cfg), faces, F, 0, use_filter, &w.bins, g->d_status,
-                               w.bins_ws, w.bins_ws_bytes, st, w.ind_bits, false));
+        if (L + 1 < cfg->l_max) {  // side stream: bins(L+1) while the main stream runs level L
+            if (L >= 1) cudaStreamWaitEvent(s2, side->vox[(L + 1) & 1], 0);  // voxelize(L-1) done
+            VF_TRY(build(L + 1));
+            cudaEventRecord(side->bins[(L + 1) & 1], s2);
+        }
+        cudaStreamWaitEvent(st, side->bins[L & 1], 0);
         rec(events, n_ev, &k, st);  // bins done
-        VF_TRY(voxelize_impl(li, g, L, &w.bins, faces, st));
+        VF_TRY(voxelize_impl(li, g, L, buf[L & 1], faces, st));
+        cudaEventRecord(side->vox[L & 1], st);
         VF_TRY(propagate_level_impl(li, g, L, w.prop_ws, w.prop_b, st));
         rec(events, n_ev, &k, st);  // voxelization done
         if (L == cfg->l_max - 1) break;
@@ -389,6 +445,9 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
         VF_TRY(adapt_impl(*cfg, g, L, w.adapt_ws, w.adapt_b, st));
         rec(events, n_ev, &k, st);  // refinement done
     }
+    // join the side stream (required to end a capture; bins are all consumed)
+    cudaEventRecord(side->join, s2);
+    cudaStreamWaitEvent(st, side->join, 0);
     VF_TRY(boundary_impl(*cfg, g, w.bcount, st));
     VF_TRY(tables_impl(g, w.bcount, cmap, d_n_b, w.tab_ws, w.tab_b, st));
     rec(events, n_ev, &k, st);  // boundary + tables done
