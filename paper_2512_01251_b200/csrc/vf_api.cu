@@ -3,6 +3,7 @@
 #include <math.h>
 #include <stdio.h>
 #include <string.h>
+#include <stdlib.h>
 
 #include <atomic>
 #include <mutex>
@@ -127,6 +128,7 @@ struct EmbedWs {
     size_t prop_b, mark_b, adapt_b, tab_b, link_b;
     int32_t *bcount;
     uint16_t *ind_bits;  // [F] per-level 1D indicator bits
+    void *lines_ws;      // recorded piercing lines of the link enumeration
     void *shard_ws;      // multi-GPU: row histogram / owner scan / face subset
 };
 
@@ -169,6 +171,7 @@ static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *b
     t.link_b = link_workspace_size(cfg, Lf);
     t.link_ws = take(t.link_b);
     t.ind_bits = (uint16_t *)take(sizeof(uint16_t) * (size_t)(F + 1));
+    t.lines_ws = take(link_lines_bytes(F));
     t.bcount = (int32_t *)take(sizeof(int32_t) * (size_t)cap);
     t.shard_ws = cfg.shard_count > 1 ? take(shard_scratch_size(cfg, F)) : nullptr;
     if (w) *w = t;
@@ -372,8 +375,9 @@ static void rec(void **ev, int n_ev, int *k, cudaStream_t st) {
 // side stream + events of the bins pipeline (one set per device, created on
 // first use; the embed is single-threaded per device, see the header)
 struct SideStream {
-    cudaStream_t st = nullptr;
+    cudaStream_t st = nullptr, st3 = nullptr;  // bins pipeline, link line enumeration
     cudaEvent_t fork = nullptr, bins[2] = {nullptr, nullptr}, vox[2] = {nullptr, nullptr}, join = nullptr;
+    cudaEvent_t join3 = nullptr;
 };
 static SideStream g_side[64];
 
@@ -383,8 +387,13 @@ static int side_stream(SideStream **out) {
     if (e != cudaSuccess) return set_cuda_error(e, "cudaGetDevice");
     SideStream &s = g_side[dev & 63];
     if (!s.st) {
-        e = cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking);
-        cudaEvent_t *evs[] = {&s.fork, &s.bins[0], &s.bins[1], &s.vox[0], &s.vox[1], &s.join};
+        // bins feed the level pipeline: highest priority; the link line
+        // enumeration only has to finish by phase 2: lowest priority
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        e = cudaStreamCreateWithPriority(&s.st, cudaStreamNonBlocking, hi);
+        if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&s.st3, cudaStreamNonBlocking, lo);
+        cudaEvent_t *evs[] = {&s.fork, &s.bins[0], &s.bins[1], &s.vox[0], &s.vox[1], &s.join, &s.join3};
         for (cudaEvent_t *ev : evs)
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
         if (e != cudaSuccess) return set_cuda_error(e, "side stream");
@@ -416,9 +425,14 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     int k = 0;
     rec(events, n_ev, &k, st);  // 0: start
     VF_TRY(init_forest_impl(*cfg, g, st));
-    // fork the bins pipeline (after init: it shares the status word)
+    // fork the bins pipeline (after init: it shares the status word) and the
+    // grid-independent cut-link line enumeration of the finest level (joined
+    // in phase 2, where the recorded lines are resolved)
     cudaEventRecord(side->fork, st);
     cudaStreamWaitEvent(s2, side->fork, 0);
+    cudaStreamWaitEvent(side->st3, side->fork, 0);
+    VF_TRY(link_enum_impl(*cfg, faces, F, w.link_ws, w.lines_ws, side->st3, events ? events + 58 : nullptr));
+    cudaEventRecord(side->join3, side->st3);
     // Alg. 1 indicators of every level in one pass over the face records
     if (use_filter) VF_TRY(launch_indicators_all(*cfg, faces, F, w.ind_bits, s2));
     auto build = [&](int L) {
@@ -465,9 +479,12 @@ int vf_embed_phase2(const vf_config *cfg, const double *faces, int64_t F, vf_gri
     if (embed_layout(*cfg, F, g->capacity, (char *)ws, &w) > ws_bytes)
         return set_error(VF_EARG, "vf_embed_phase2: workspace too small");
     cudaStream_t st = (cudaStream_t)stream;
+    SideStream *side = nullptr;
+    VF_TRY(side_stream(&side));
     VF_TRY(fill_lut_impl(d_n_b, lengths, lengths_cap, g->d_status, st));
-    return link_impl(*cfg, g, cmap, faces, F, nullptr, nullptr, lengths, w.link_ws, w.link_b, st,
-                     link_events, d_n_b, lengths_cap);
+    cudaStreamWaitEvent(st, side->join3, 0);  // the line enumeration of phase 1
+    return link_resolve_impl(*cfg, g, cmap, faces, F, lengths, w.link_ws, w.lines_ws, st, link_events,
+                             d_n_b, lengths_cap);
 }
 
 int vf_embed_graph_create(const vf_config *cfg, const double *faces, int64_t F, int use_filter,
@@ -489,8 +506,31 @@ int vf_embed_graph_create(const vf_config *cfg, const double *faces, int64_t F, 
         return rc;
     }
     if (e != cudaSuccess) return set_cuda_error(e, "cudaStreamEndCapture");
+    // node priorities: the level pipeline (critical path) high, the
+    // grid-independent link line enumeration (its own branch) low
+    {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        size_t nn = 0;
+        cudaGraphGetNodes(graph, nullptr, &nn);
+        cudaGraphNode_t *nodes = (cudaGraphNode_t *)malloc(sizeof(cudaGraphNode_t) * (nn ? nn : 1));
+        cudaGraphGetNodes(graph, nodes, &nn);
+        const void *enum_fn = link_enum_kernel();
+        for (size_t i = 0; i < nn; ++i) {
+            cudaGraphNodeType ty;
+            if (cudaGraphNodeGetType(nodes[i], &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) continue;
+            cudaKernelNodeParams kp;
+            if (cudaGraphKernelNodeGetParams(nodes[i], &kp) != cudaSuccess) continue;
+            cudaLaunchAttributeValue v;
+            memset(&v, 0, sizeof(v));
+            v.priority = (kp.func == enum_fn) ? lo : hi;
+            cudaGraphKernelNodeSetAttribute(nodes[i], cudaLaunchAttributePriority, &v);
+        }
+        free(nodes);
+        cudaGetLastError();  // priorities are a hint: never fail the capture over them
+    }
     cudaGraphExec_t exec = nullptr;
-    e = cudaGraphInstantiate(&exec, graph, 0);
+    e = cudaGraphInstantiate(&exec, graph, cudaGraphInstantiateFlagUseNodePriority);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaGraphInstantiate");
     *graph_exec = (void *)exec;

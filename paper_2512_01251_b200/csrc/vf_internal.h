@@ -97,6 +97,15 @@ size_t shard_scratch_size(const vf_config &cfg, int64_t F);
 int shard_owner_map_impl(const vf_config &cfg, vf_grid *g, int L, void *scratch, cudaStream_t st);
 int shard_face_subset_impl(const vf_config &cfg, const double *faces, int64_t F, int32_t *map,
                            int32_t *d_n_map, void *scratch, cudaStream_t st);
+// embed split of the link lengths: grid-independent line enumeration (side
+// stream, early) + resolution once the grid and the LUT slots exist
+size_t link_lines_bytes(int64_t F);
+const void *link_enum_kernel();  // graph node priorities
+int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *ws, void *lines_ws,
+                   cudaStream_t st, void **events);
+int link_resolve_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
+                      int64_t F, float *lengths, void *ws, void *lines_ws, cudaStream_t st,
+                      void **events, const int32_t *d_n_b, int64_t lengths_cap);
 int fill_lut_impl(const int32_t *d_n_b, float *lengths, int64_t cap, int32_t *d_status,
                   cudaStream_t st);
 

@@ -35,6 +35,7 @@
 // Every stored value is the oracle's FP64 value; only the SAT evaluation is
 // skipped where its outcome is certain.
 #include <math.h>
+#include <string.h>
 
 #include "vf_common.cuh"
 #include "vf_internal.h"
@@ -116,6 +117,14 @@ struct LinkCtx {
     int bx, by, cells[3];
     int fast;  // eps >> FP64 rounding of the piercing point: fast path allowed
     int pow2;  // dx is a power of two: q = dd * (1/dx) is exactly dd / dx
+    // MODE 2 (line enumeration ahead of the grid): piercing-line records
+    // (face, R | fast << 4 | (n_nodes - 1) << 5 | ip_lo << 8, m1, m2), and the
+    // faces whose lines overflowed the buffer (redone by k_links later)
+    int4 *lines;
+    int32_t *n_lines;     // may exceed line_cap
+    int64_t line_cap;
+    int32_t *ovf_list, *n_ovf;
+    uint32_t *ovf_bits;   // one bit per face: already listed
 };
 
 // representative directions q = 2r+1 (lattice.py order) in constant memory
@@ -262,11 +271,12 @@ __device__ __forceinline__ int link_dir_setup(LinkDir &D, const LinkCtx &c, cons
 }
 
 // a candidate the fast path cannot decide: appended to the band list for
-// k_links_band (FULL: decided inline -- the overflow fallback kernel)
-template <bool FULL>
+// k_links_band (MODE 1: decided inline -- the overflow fallback kernel; MODE 2
+// appends with slot -1: the block map does not exist yet, k_links_band looks it up)
+template <int MODE>
 __device__ __forceinline__ void link_slow(const LinkCtx &c, int f, int slot, int i, int j, int k,
                                           int r) {
-    if (FULL) {
+    if (MODE == 1) {
         link_candidate(c.faces, f, r, i, j, k, c.dx, c.eps, c.eps_par, slot, c.lengths);
         return;
     }
@@ -278,7 +288,7 @@ __device__ __forceinline__ void link_slow(const LinkCtx &c, int f, int slot, int
 // the (2, rarely 3) nodes of one line that pierces the face: crossing
 // estimate, then the fast exact path (interior lines) or link_slow (margin
 // band, ill-conditioned crossings)
-template <bool FULL>
+template <int MODE>
 __device__ __forceinline__ void link_line(const LinkCtx &c, const LinkDir &D, const double *fv,
                                           int m1, int m2, float Ra, float Rb, bool fast, int R,
                                           int p, int cp, int s1, int s2, int n1, int n2) {
@@ -293,6 +303,17 @@ __device__ __forceinline__ void link_line(const LinkCtx &c, const LinkDir &D, co
         ip_lo = max((int)ceil(((double)(xs - wid) + D.vp) * c.inv_dx - 0.5), ip_lo);
         ip_hi = min((int)floor(((double)(xs + wid) + D.vp) * c.inv_dx - 0.5), ip_hi);
     }
+    if (MODE == 2 && ip_lo <= ip_hi && ip_hi - ip_lo < 8 && fast) {
+        // record the line; its nodes are resolved once the grid exists
+        const int pos = atomicAdd(c.n_lines, 1);
+        if (pos < c.line_cap) {
+            c.lines[pos] = make_int4(D.f, R | (1 << 4) | ((ip_hi - ip_lo) << 5) | (ip_lo << 8), m1, m2);
+        } else {
+            const uint32_t bit = 1u << (D.f & 31);
+            if (!(atomicOr(&c.ovf_bits[D.f >> 5], bit) & bit)) c.ovf_list[atomicAdd(c.n_ovf, 1)] = D.f;
+        }
+        return;
+    }
     for (int ip = ip_lo; ip <= ip_hi; ++ip) {
         // i_qj = m_j + s_j i_p
         const int a = m1 + s1 * ip, b = m2 + s2 * ip;
@@ -300,10 +321,14 @@ __device__ __forceinline__ void link_line(const LinkCtx &c, const LinkDir &D, co
         const int i = p == 0 ? ip : a;
         const int j = p == 1 ? ip : (p == 0 ? a : b);
         const int k = p == 2 ? ip : b;
+        if (MODE == 2) {  // margin band / ill-conditioned lines: exact path later
+            link_slow<MODE>(c, D.f, -1, i, j, k, R);
+            continue;
+        }
         const int32_t slot = c.bmap[(i >> 2) + (int64_t)c.bx * ((j >> 2) + (int64_t)c.by * (k >> 2))];
         if (slot < 0) continue;
         if (fast) link_fast(c, fv, R, D.den, i, j, k, slot);
-        else link_slow<FULL>(c, D.f, slot, i, j, k, R);
+        else link_slow<MODE>(c, D.f, slot, i, j, k, R);
     }
 }
 
@@ -311,7 +336,7 @@ __device__ __forceinline__ void link_line(const LinkCtx &c, const LinkDir &D, co
 // (one line per lane): the row / point loops leave few lanes active, the node
 // work (bmap lookup, FP64 num/den, atomicMin) then runs on full warps.  The
 // queue is drained before the next pair overwrites the per-lane LinkDir.
-template <bool FULL>
+template <int MODE>
 __device__ __forceinline__ void line_drain(LinkWarp &W, int lane, const LinkCtx &c, bool all, int R,
                                            int p, int cp, int s1, int s2, int n1, int n2) {
     __syncwarp();
@@ -325,7 +350,7 @@ __device__ __forceinline__ void line_drain(LinkWarp &W, int lane, const LinkCtx 
             const int o = e.x & 31;
             const LinkDir &D = W.d[o];
             const float Rb = (float)(((double)e.z + 0.5 * (1 - s2)) * c.dx + D.off2);
-            link_line<FULL>(c, D, W.fv[o], e.y, e.z, __int_as_float(e.w), Rb, (e.x >> 8) & 1, R, p, cp,
+            link_line<MODE>(c, D, W.fv[o], e.y, e.z, __int_as_float(e.w), Rb, (e.x >> 8) & 1, R, p, cp,
                             s1, s2, n1, n2);
         }
         n -= take;
@@ -348,17 +373,17 @@ __device__ __forceinline__ int point_class(const LinkDir &D, float Ra, float Rb)
 
 // one lattice point (line) of a row: inside test; a piercing line is queued
 // (or, when the queue is full, resolved inline)
-template <bool FULL>
+template <int MODE>
 __device__ __forceinline__ void link_point(LinkWarp &W, int o, const LinkCtx &c, const LinkDir &D,
                                            const double *fv, int m1, int m2, float Rb, int R, int p,
                                            int cp, int s1, int s2, int n1, int n2) {
     const float Ra = (float)(((double)m1 + 0.5 * (1 - s1)) * c.dx + D.off1);
     const int cls = point_class(D, Ra, Rb);
     if (cls == 0) return;  // misses the face
-    const bool fast = !FULL && cls == 1;
+    const bool fast = MODE != 1 && cls == 1;
     const int pos = atomicAdd(&W.lqn, 1);
     if (pos < kLineQ) W.lq[pos] = make_int4(o | ((int)fast << 8), m1, m2, __float_as_int(Ra));
-    else link_line<FULL>(c, D, fv, m1, m2, Ra, Rb, fast, R, p, cp, s1, s2, n1, n2);
+    else link_line<MODE>(c, D, fv, m1, m2, Ra, Rb, fast, R, p, cp, s1, s2, n1, n2);
 }
 
 // one lattice row m2: the conservative m1 interval of the row inside the
@@ -405,7 +430,7 @@ __device__ __forceinline__ bool row_interval(const LinkCtx &c, const LinkDir &D,
 // is ill-conditioned (|alpha_k| tiny) does not restrict the row; the interval
 // is widened by one lattice point on each side -- a superset of the points
 // that pass point_class, which alone decides.
-template <bool FULL>
+template <int MODE>
 __device__ __forceinline__ void link_row(LinkWarp &W, int o, const LinkCtx &c, const LinkDir &D,
                                          const double *fv, int m2, int R, int p, int cp, int s1,
                                          int s2, int n1, int n2) {
@@ -413,20 +438,22 @@ __device__ __forceinline__ void link_row(LinkWarp &W, int o, const LinkCtx &c, c
     int m1lo, m1hi;
     if (!row_interval(c, D, Rb, s1, m1lo, m1hi)) return;
     for (int m1 = m1lo; m1 <= m1hi; ++m1)
-        link_point<FULL>(W, o, c, D, fv, m1, m2, Rb, R, p, cp, s1, s2, n1, n2);
+        link_point<MODE>(W, o, c, D, fv, m1, m2, Rb, R, p, cp, s1, s2, n1, n2);
 }
 
 constexpr size_t kLinkSmem = kLinkWarps * sizeof(LinkWarp);
 
-// K-link.  FULL = false: the main kernel (fast path + band list); FULL = true:
+// K-link.  MODE 0: the main kernel (fast path + band list); MODE 2: the
+// grid-independent line enumeration (k_links_enum, records piercing lines);
+// MODE 1:
 // the overflow fallback, a no-op unless the band list overflowed, in which
 // case it redoes every face with every undecided candidate decided inline
 // (atomicMin is idempotent, so re-merging the fast results is harmless).
-template <bool FULL>
-__global__ void __launch_bounds__(kLinkWarps * 32, FULL ? 1 : VF_LINK_MINB)
+template <int MODE>
+__global__ void __launch_bounds__(kLinkWarps * 32, MODE == 1 ? 1 : VF_LINK_MINB)
     k_links(LinkCtx c, int widen, int64_t F, const int32_t *__restrict__ map,
             const int32_t *__restrict__ d_n_map) {
-    if (FULL && c.n_band[1] == 0) return;
+    if (MODE == 1 && c.n_band[1] == 0) return;
     extern __shared__ __align__(16) unsigned char s_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     LinkWarp &W = reinterpret_cast<LinkWarp *>(s_raw)[w];
@@ -500,11 +527,47 @@ __global__ void __launch_bounds__(kLinkWarps * 32, FULL ? 1 : VF_LINK_MINB)
                     for (int st = 16; st > 0; st >>= 1)
                         if (W.excl[o + st] <= it) o += st;
                     const LinkDir &D = W.d[o];
-                    link_row<FULL>(W, o, c, D, W.fv[o], D.m2a + it - W.excl[o], R, p, cp, s1, s2, n1, n2);
+                    link_row<MODE>(W, o, c, D, W.fv[o], D.m2a + it - W.excl[o], R, p, cp, s1, s2, n1, n2);
                 }
-                line_drain<FULL>(W, lane, c, false, R, p, cp, s1, s2, n1, n2);
+                line_drain<MODE>(W, lane, c, false, R, p, cp, s1, s2, n1, n2);
             }
-            line_drain<FULL>(W, lane, c, true, R, p, cp, s1, s2, n1, n2);
+            line_drain<MODE>(W, lane, c, true, R, p, cp, s1, s2, n1, n2);
+        }
+    }
+}
+
+// Resolve the recorded lines (fast class) once the grid and the block map
+// exist: thread per line, its (2, rarely 3) nodes -> block map -> the
+// oracle's FP64 num/den/d/q -> atomicMin.  Full warps, no setup.
+__global__ void __launch_bounds__(256)
+    k_links_resolve(LinkCtx c) {
+    const int64_t n = min((int64_t)*c.n_lines, c.line_cap);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int4 rec = c.lines[e];
+        const int f = rec.x, R = rec.y & 15, cnt = (rec.y >> 5) & 7, ip_lo = rec.y >> 8;
+        const int m1 = rec.z, m2 = rec.w;
+        const int cx = c_rep[R][0], cy = c_rep[R][1], cz = c_rep[R][2];
+        const int p = cx != 0 ? 0 : (cy != 0 ? 1 : 2);
+        const int q1 = p == 0 ? 1 : 0, q2 = p == 2 ? 1 : 2;
+        const int cp = pick3(p, cx, cy, cz);
+        const int s1 = pick3(q1, cx, cy, cz) * cp, s2 = pick3(q2, cx, cy, cz) * cp;
+        const int n1 = pick3(q1, c.cells[0], c.cells[1], c.cells[2]);
+        const int n2 = pick3(q2, c.cells[0], c.cells[1], c.cells[2]);
+        const double2 *fp = reinterpret_cast<const double2 *>(c.faces + (int64_t)f * kFaceStride);
+        const double2 a0 = __ldg(fp), a1 = __ldg(fp + 1), a4 = __ldg(fp + 4), a5 = __ldg(fp + 5);
+        const double fv[6] = {a0.x, a0.y, a1.x, a4.y, a5.x, a5.y};  // v1, n
+        // exact c.n (link_dir_setup / link_candidate; nonzero: the pair passed EPS_PARALLEL)
+        const double den = VF_DADD(VF_DADD(cmul(cx, fv[3]), cmul(cy, fv[4])), cmul(cz, fv[5]));
+        for (int ip = ip_lo; ip <= ip_lo + cnt; ++ip) {
+            const int a = m1 + s1 * ip, b = m2 + s2 * ip;
+            if (a < 0 || a >= n1 || b < 0 || b >= n2) continue;
+            const int i = p == 0 ? ip : a;
+            const int j = p == 1 ? ip : (p == 0 ? a : b);
+            const int k = p == 2 ? ip : b;
+            const int32_t slot = c.bmap[(i >> 2) + (int64_t)c.bx * ((j >> 2) + (int64_t)c.by * (k >> 2))];
+            if (slot < 0) continue;
+            link_fast(c, fv, R, den, i, j, k, slot);
         }
     }
 }
@@ -517,8 +580,13 @@ __global__ void __launch_bounds__(256)
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int4 x = c.band[e];
-        link_candidate(c.faces, x.x, x.w >> 16, x.z & 0xffff, x.z >> 16, x.w & 0xffff, c.dx, c.eps,
-                       c.eps_par, x.y, c.lengths);
+        const int i = x.z & 0xffff, j = x.z >> 16, k = x.w & 0xffff;
+        int32_t slot = x.y;
+        if (slot < 0) {  // queued by the line enumeration before the block map existed
+            slot = c.bmap[(i >> 2) + (int64_t)c.bx * ((j >> 2) + (int64_t)c.by * (k >> 2))];
+            if (slot < 0) continue;
+        }
+        link_candidate(c.faces, x.x, x.w >> 16, i, j, k, c.dx, c.eps, c.eps_par, slot, c.lengths);
     }
 }
 
@@ -560,31 +628,17 @@ int fill_lut_impl(const int32_t *d_n_b, float *lengths, int64_t cap, int32_t *d_
     return check_launch("k_fill_lut");
 }
 
-int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
-              int64_t F, const int32_t *map, const int32_t *d_n_map, float *lengths, void *ws,
-              size_t ws_bytes, cudaStream_t st, void **events, const int32_t *d_n_b,
-              int64_t lengths_cap) {
-    const int L = g->n_levels - 1;
-    if (ws_bytes < link_workspace_size(cfg, L)) return set_error(VF_EARG, "link workspace too small");
-    const LevelInfo li = make_level(cfg, L);
+static int make_link_ctx(const vf_config &cfg, int L, const double *faces, float *lengths, void *ws,
+                         LinkCtx &c, int &widen, LevelInfo &li) {
+    li = make_level(cfg, L);
     if (li.cells[0] > 32767 || li.cells[1] > 32767 || li.cells[2] > 32767)
         return set_error(VF_EARG, "link lengths: > 32767 cells per axis");
-    const int64_t nb = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
-    int32_t *bmap = (int32_t *)ws;
-    int32_t *n_band = (int32_t *)((char *)ws + bmap_bytes(cfg, L));
-    int4 *band = (int4 *)((char *)n_band + 256);
-    cudaMemsetAsync(bmap, 0xff, sizeof(int32_t) * (size_t)nb, st);
-    cudaMemsetAsync(n_band, 0, 2 * sizeof(int32_t), st);
-    k_blockmap<<<max_ctas(8), 256, 0, st>>>(li, L, g->d_level_start, g->d_coords, cmap, bmap, d_n_b,
-                                            lengths_cap);
-    int rc = check_launch("k_blockmap");
-    if (rc) return rc;
-    LinkCtx c;
+    memset(&c, 0, sizeof(c));
     c.faces = faces;
-    c.bmap = bmap;
+    c.bmap = (int32_t *)ws;
     c.lengths = lengths;
-    c.band = band;
-    c.n_band = n_band;
+    c.n_band = (int32_t *)((char *)ws + bmap_bytes(cfg, L));
+    c.band = (int4 *)((char *)c.n_band + 256);
     c.band_cap = g_band_cap;
     c.dx = li.dx;
     c.eps = li.eps;
@@ -597,23 +651,121 @@ int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const doubl
     int ex = 0;
     const double mant = frexp(li.dx, &ex);
     c.pow2 = mant == 0.5;
-    const int widen = c.pow2 ? 0 : 1;
+    widen = c.pow2 ? 0 : 1;
     c.inv_dx = 1.0 / li.dx;
-    int64_t grid = (F + 32 * kLinkWarps - 1) / (32 * kLinkWarps);
-    if (grid > max_ctas(6)) grid = max_ctas(6);
-    if (grid < 1) grid = 1;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_links<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLinkSmem);
-        cudaFuncSetAttribute(k_links<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLinkSmem);
+        cudaFuncSetAttribute(k_links<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLinkSmem);
+        cudaFuncSetAttribute(k_links<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLinkSmem);
+        cudaFuncSetAttribute(k_links<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLinkSmem);
         attr = true;
     }
+    return VF_OK;
+}
+
+static int link_grid(int64_t F) {
+    int64_t grid = (F + 32 * kLinkWarps - 1) / (32 * kLinkWarps);
+    if (grid > max_ctas(6)) grid = max_ctas(6);
+    return grid < 1 ? 1 : (int)grid;
+}
+
+// the block map of the finest level (LUT slots of mapped blocks)
+static int link_blockmap(vf_grid *g, const LevelInfo &li, const int32_t *cmap, const LinkCtx &c,
+                         const int32_t *d_n_b, int64_t lengths_cap, cudaStream_t st) {
+    const int L = li.level;
+    const int64_t nb = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
+    cudaMemsetAsync(const_cast<int32_t *>(c.bmap), 0xff, sizeof(int32_t) * (size_t)nb, st);
+    k_blockmap<<<max_ctas(8), 256, 0, st>>>(li, L, g->d_level_start, g->d_coords, cmap,
+                                            const_cast<int32_t *>(c.bmap), d_n_b, lengths_cap);
+    return check_launch("k_blockmap");
+}
+
+int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
+              int64_t F, const int32_t *map, const int32_t *d_n_map, float *lengths, void *ws,
+              size_t ws_bytes, cudaStream_t st, void **events, const int32_t *d_n_b,
+              int64_t lengths_cap) {
+    const int L = g->n_levels - 1;
+    if (ws_bytes < link_workspace_size(cfg, L)) return set_error(VF_EARG, "link workspace too small");
+    LinkCtx c;
+    int widen;
+    LevelInfo li;
+    int rc = make_link_ctx(cfg, L, faces, lengths, ws, c, widen, li);
+    if (rc) return rc;
+    cudaMemsetAsync(c.n_band, 0, 2 * sizeof(int32_t), st);
+    if ((rc = link_blockmap(g, li, cmap, c, d_n_b, lengths_cap, st))) return rc;
+    const int grid = link_grid(F);
     if (events) cudaEventRecord((cudaEvent_t)events[0], st);
-    k_links<false><<<(int)grid, kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, map, d_n_map);
+    k_links<0><<<grid, kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, map, d_n_map);
     if ((rc = check_launch("k_links"))) return rc;
     k_links_band<<<max_ctas(2), 256, 0, st>>>(c);
     if ((rc = check_launch("k_links_band"))) return rc;
-    k_links<true><<<(int)grid, kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, map, d_n_map);
+    k_links<1><<<grid, kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, map, d_n_map);
+    rc = check_launch("k_links_full");
+    if (events) cudaEventRecord((cudaEvent_t)events[1], st);
+    return rc;
+}
+
+// ---- embed split: the line enumeration does not depend on the grid, so the
+// embed launches it on a side stream at the start of phase 1 (overlapping the
+// whole level pipeline) and resolves the recorded lines in phase 2.
+size_t link_lines_bytes(int64_t F) {
+    const int64_t cap = F * 2 > (1 << 22) ? F * 2 : (1 << 22);
+    return 256 + (size_t)cap * sizeof(int4) + (((size_t)(F + 1) * sizeof(int32_t) + 255) & ~(size_t)255) +
+           ((((size_t)F + 32) / 32 * sizeof(uint32_t) + 255) & ~(size_t)255);
+}
+
+static void line_bufs(LinkCtx &c, int64_t F, void *lines_ws) {
+    c.line_cap = F * 2 > (1 << 22) ? F * 2 : (1 << 22);
+    c.n_lines = (int32_t *)lines_ws;
+    c.n_ovf = c.n_lines + 1;
+    c.lines = (int4 *)((char *)lines_ws + 256);
+    c.ovf_list = (int32_t *)((char *)c.lines + (size_t)c.line_cap * sizeof(int4));
+    c.ovf_bits = (uint32_t *)((char *)c.ovf_list + (((size_t)(F + 1) * sizeof(int32_t) + 255) & ~(size_t)255));
+}
+
+int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *ws, void *lines_ws,
+                   cudaStream_t st, void **events) {
+    LinkCtx c;
+    int widen;
+    LevelInfo li;
+    int rc = make_link_ctx(cfg, cfg.l_max - 1, faces, nullptr, ws, c, widen, li);
+    if (rc) return rc;
+    line_bufs(c, F, lines_ws);
+    cudaMemsetAsync(c.n_band, 0, 2 * sizeof(int32_t), st);
+    cudaMemsetAsync(c.n_lines, 0, 2 * sizeof(int32_t), st);
+    cudaMemsetAsync(c.ovf_bits, 0, ((size_t)F + 32) / 32 * sizeof(uint32_t), st);
+    if (events) cudaEventRecord((cudaEvent_t)events[0], st);
+    // one short CTA per 128 faces (no grid-stride loop): CTAs retire quickly,
+    // so the higher-priority level pipeline can take SMs between them
+    const int64_t g2 = (F + 32 * kLinkWarps - 1) / (32 * kLinkWarps);
+    k_links<2><<<(unsigned)(g2 < 1 ? 1 : g2), kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, nullptr, nullptr);
+    rc = check_launch("k_links_enum");
+    if (events) cudaEventRecord((cudaEvent_t)events[1], st);
+    return rc;
+}
+
+const void *link_enum_kernel() { return (const void *)k_links<2>; }
+
+int link_resolve_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
+                      int64_t F, float *lengths, void *ws, void *lines_ws, cudaStream_t st,
+                      void **events, const int32_t *d_n_b, int64_t lengths_cap) {
+    LinkCtx c;
+    int widen;
+    LevelInfo li;
+    if (g->n_levels != cfg.l_max) return set_error(VF_EARG, "link resolve: the grid must reach L_max");
+    int rc = make_link_ctx(cfg, cfg.l_max - 1, faces, lengths, ws, c, widen, li);
+    if (rc) return rc;
+    line_bufs(c, F, lines_ws);
+    if ((rc = link_blockmap(g, li, cmap, c, d_n_b, lengths_cap, st))) return rc;
+    if (events) cudaEventRecord((cudaEvent_t)events[0], st);
+    k_links_resolve<<<max_ctas(8), 256, 0, st>>>(c);
+    if ((rc = check_launch("k_links_resolve"))) return rc;
+    // faces whose lines overflowed the record buffer: the direct kernel
+    k_links<0><<<link_grid(F), kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, c.ovf_list, c.n_ovf);
+    if ((rc = check_launch("k_links_ovf"))) return rc;
+    k_links_band<<<max_ctas(2), 256, 0, st>>>(c);
+    if ((rc = check_launch("k_links_band"))) return rc;
+    k_links<1><<<link_grid(F), kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, nullptr, nullptr);
     rc = check_launch("k_links_full");
     if (events) cudaEventRecord((cudaEvent_t)events[1], st);
     return rc;

@@ -175,7 +175,9 @@ class EmbedEngine:
         self.cmap = torch.empty(cap, dtype=torch.int32, device="cuda")
         self.n_b_dev = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.host = torch.zeros(8, dtype=torch.int32).pin_memory()  # 0-3 status, 4 n_b
-        self.stream = torch.cuda.Stream()
+        # high priority: the level pipeline is the critical path; the library's
+        # cut-link line enumeration runs beside it on a low-priority stream
+        self.stream = torch.cuda.Stream(priority=-1)
         self.lengths = None
         self.bc_ids = None
         self.lengths_cap = 0
@@ -305,8 +307,15 @@ class EmbedEngine:
         return t
 
     def link_kernel_ms(self) -> float:
-        """Device time of the k_links launch of the last timed run."""
-        return self.events[self.n_events - 3].elapsed_time(self.events[self.n_events - 2])
+        """Device time of the cut-link kernels of the last timed run: the line
+        enumeration (side stream, overlapped with the level pipeline, events
+        58-59) plus the resolution after the tables (events 61-62)."""
+        enum = self.events[58].elapsed_time(self.events[59])
+        return enum + self.events[self.n_events - 3].elapsed_time(self.events[self.n_events - 2])
+
+    def link_enum_ms(self) -> float:
+        """The overlapped part of link_kernel_ms (grid-independent enumeration)."""
+        return self.events[58].elapsed_time(self.events[59])
 
     def cells_classified(self) -> int:
         """Sum over levels of 64 * blocks."""
