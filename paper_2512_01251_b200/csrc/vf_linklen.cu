@@ -288,13 +288,15 @@ __device__ __forceinline__ void link_slow(const LinkCtx &c, int f, int slot, int
 // the (2, rarely 3) nodes of one line that pierces the face: crossing
 // estimate, then the fast exact path (interior lines) or link_slow (margin
 // band, ill-conditioned crossings)
-template <int MODE>
-__device__ __forceinline__ void link_line(const LinkCtx &c, const LinkDir &D, const double *fv,
-                                          int m1, int m2, float Ra, float Rb, bool fast, int R,
-                                          int p, int cp, int s1, int s2, int n1, int n2) {
+// node range along p of the line through (Ra, Rb): the nodes within one link
+// of its crossing with the face plane (crossing estimate in FP32, widened
+// past its error), or the face's full range for ill-conditioned crossings
+__device__ __forceinline__ void line_nodes(const LinkCtx &c, const LinkDir &D, float Ra, float Rb,
+                                           int cp, int &ip_lo, int &ip_hi) {
     // crossing with the face plane: Q = v1 + Ra e_q1 + Rb e_q2 (+0 e_p),
     // points Q + lam c; n.(Q + lam c - v1) = 0
-    int ip_lo = D.lop, ip_hi = D.hip;
+    ip_lo = D.lop;
+    ip_hi = D.hip;
     if (D.dn != 0.0f) {
         const float lam = -__fdividef(D.nq1 * Ra + D.nq2 * Rb, D.dn);
         const float xs = (float)cp * lam;  // x_p* - v1_p
@@ -303,8 +305,16 @@ __device__ __forceinline__ void link_line(const LinkCtx &c, const LinkDir &D, co
         ip_lo = max((int)ceil(((double)(xs - wid) + D.vp) * c.inv_dx - 0.5), ip_lo);
         ip_hi = min((int)floor(((double)(xs + wid) + D.vp) * c.inv_dx - 0.5), ip_hi);
     }
+}
+
+template <int MODE>
+__device__ __forceinline__ void link_line(const LinkCtx &c, const LinkDir &D, const double *fv,
+                                          int m1, int m2, float Ra, float Rb, bool fast, int R,
+                                          int p, int cp, int s1, int s2, int n1, int n2) {
+    int ip_lo, ip_hi;
+    line_nodes(c, D, Ra, Rb, cp, ip_lo, ip_hi);
     if (MODE == 2 && ip_lo <= ip_hi && ip_hi - ip_lo < 8 && fast) {
-        // record the line; its nodes are resolved once the grid exists
+        // (inline overflow path of the warp queue) record the line
         const int pos = atomicAdd(c.n_lines, 1);
         if (pos < c.line_cap) {
             c.lines[pos] = make_int4(D.f, R | (1 << 4) | ((ip_hi - ip_lo) << 5) | (ip_lo << 8), m1, m2);
@@ -346,7 +356,41 @@ __device__ __forceinline__ void line_drain(LinkWarp &W, int lane, const LinkCtx 
         int4 e = make_int4(0, 0, 0, 0);
         if (lane < take) e = W.lq[n - take + lane];
         __syncwarp();
-        if (lane < take) {
+        if (MODE == 2) {
+            // enumeration: record the line (warp-aggregated slot in the
+            // global line buffer); margin-band / long-range lines go to the
+            // band list node by node
+            bool want = false;
+            int4 rec = make_int4(0, 0, 0, 0);
+            if (lane < take) {
+                const int o = e.x & 31;
+                const LinkDir &D = W.d[o];
+                const float Rb = (float)(((double)e.z + 0.5 * (1 - s2)) * c.dx + D.off2);
+                const bool fast = (e.x >> 8) & 1;
+                int ip_lo, ip_hi;
+                line_nodes(c, D, __int_as_float(e.w), Rb, cp, ip_lo, ip_hi);
+                if (fast && ip_lo <= ip_hi && ip_hi - ip_lo < 8) {
+                    want = true;
+                    rec = make_int4(D.f, R | (1 << 4) | ((ip_hi - ip_lo) << 5) | (ip_lo << 8), e.y, e.z);
+                } else {
+                    link_line<MODE>(c, D, W.fv[o], e.y, e.z, __int_as_float(e.w), Rb, fast, R, p, cp, s1,
+                                    s2, n1, n2);
+                }
+            }
+            const uint32_t m = __ballot_sync(0xffffffffu, want);
+            int base = 0;
+            if (lane == 0 && m) base = atomicAdd(c.n_lines, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (want) {
+                const int pos = base + __popc(m & ((1u << lane) - 1u));
+                if (pos < c.line_cap) {
+                    c.lines[pos] = rec;
+                } else {
+                    const uint32_t bit = 1u << (rec.x & 31);
+                    if (!(atomicOr(&c.ovf_bits[rec.x >> 5], bit) & bit)) c.ovf_list[atomicAdd(c.n_ovf, 1)] = rec.x;
+                }
+            }
+        } else if (lane < take) {
             const int o = e.x & 31;
             const LinkDir &D = W.d[o];
             const float Rb = (float)(((double)e.z + 0.5 * (1 - s2)) * c.dx + D.off2);
