@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     k_mark_adj(int L, const int32_t *__restrict__ level_start, const int32_t *__restrict__ nbr,
                uint8_t *__restrict__ bflags, const uint8_t *__restrict__ aux,
-               uint8_t *__restrict__ m0) {
+               uint8_t *__restrict__ m0, int commit) {
     const int32_t s = level_start[L], e = level_start[L + 1];
     for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
          b += (int64_t)gridDim.x * blockDim.x) {
@@ -101,16 +101,18 @@ __global__ void __launch_bounds__(256)
         uint8_t f = (uint8_t)(f0 & ~(VF_BF_SB | VF_BF_SA | VF_BF_MARK));
         if (sb) f |= VF_BF_SB;
         if (has_sb && !solid) f |= VF_BF_SA;
+        const uint8_t mk = (uint8_t)(el && (sb || has_sb));
+        if (commit && mk) f |= VF_BF_MARK;  // N_prop = 0: this is the last phase
         bflags[b] = f;
-        m0[b] = (uint8_t)(el && (sb || has_sb));
+        m0[b] = mk;
     }
 }
 
 __global__ void __launch_bounds__(256)
     k_mark_prop(int L, int it, const int32_t *__restrict__ level_start,
-                const int32_t *__restrict__ nbr, const uint8_t *__restrict__ bflags,
+                const int32_t *__restrict__ nbr, uint8_t *__restrict__ bflags,
                 const uint8_t *__restrict__ aux, const uint8_t *__restrict__ src,
-                uint8_t *__restrict__ dst) {
+                uint8_t *__restrict__ dst, int commit) {
     const int32_t s = level_start[L], e = level_start[L + 1];
     for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
          b += (int64_t)gridDim.x * blockDim.x) {
@@ -123,15 +125,10 @@ __global__ void __launch_bounds__(256)
             }
         }
         dst[b] = m;
+        // last sweep: commit (only this thread touches bflags[b]; neighbours
+        // are read through src, never through bflags' MARK bit)
+        if (commit && m) bflags[b] |= VF_BF_MARK;
     }
-}
-
-__global__ void k_mark_commit(int L, const int32_t *__restrict__ level_start,
-                              const uint8_t *__restrict__ m, uint8_t *__restrict__ bflags) {
-    const int32_t s = level_start[L], e = level_start[L + 1];
-    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
-         b += (int64_t)gridDim.x * blockDim.x)
-        if (m[b]) bflags[b] |= VF_BF_MARK;
 }
 
 size_t mark_workspace_size(int32_t capacity) { return 3 * (((size_t)capacity + 255) & ~(size_t)255); }
@@ -144,17 +141,18 @@ int mark_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_bytes
     k_mark_sb<<<grid, 256, 0, st>>>(L, g->d_level_start, g->d_nbr, g->d_bflags, aux);
     int rc = check_launch("k_mark_sb");
     if (rc) return rc;
-    k_mark_adj<<<grid, 256, 0, st>>>(L, g->d_level_start, g->d_nbr, g->d_bflags, aux, m[0]);
+    // the last phase also commits the MARK bits (no separate commit pass)
+    k_mark_adj<<<grid, 256, 0, st>>>(L, g->d_level_start, g->d_nbr, g->d_bflags, aux, m[0],
+                                     cfg.n_prop == 0);
     if ((rc = check_launch("k_mark_adj"))) return rc;
     int cur = 0;
     for (int it = 0; it < cfg.n_prop; ++it) {
         k_mark_prop<<<grid, 256, 0, st>>>(L, it, g->d_level_start, g->d_nbr, g->d_bflags, aux,
-                                          m[cur], m[cur ^ 1]);
+                                          m[cur], m[cur ^ 1], it == cfg.n_prop - 1);
         if ((rc = check_launch("k_mark_prop"))) return rc;
         cur ^= 1;
     }
-    k_mark_commit<<<grid, 256, 0, st>>>(L, g->d_level_start, m[cur], g->d_bflags);
-    return check_launch("k_mark_commit");
+    return VF_OK;
 }
 
 // --------------------------------------------------------------------------
@@ -189,22 +187,24 @@ struct EmitChild {
     }
 };
 
-__global__ void k_level_count(int L, const int32_t *__restrict__ level_start, int32_t *__restrict__ out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) *out = level_start[L + 1] - level_start[L];
-}
-
-__global__ void k_adapt_finish(int L, int32_t capacity, int32_t *__restrict__ level_start,
-                               const int32_t *__restrict__ n_marked, int32_t *__restrict__ status) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const int64_t e = level_start[L + 1];
-    int64_t ne = e + 8 * (int64_t)(*n_marked);
-    if (ne > capacity) {
-        atomicMax(status, VF_ECAPACITY);
-        status[1] = L;  // level context
-        ne = e;         // drop the level: later stages see no blocks, no OOB ids
+// appends level L+1 once the number of marked blocks is known (runs as the
+// adapt scan's epilogue on the thread that publishes the total)
+struct AdaptFinish {
+    int L;
+    int32_t capacity;
+    int32_t *level_start;
+    int32_t *status;
+    __device__ void operator()(int n_marked) const {
+        const int64_t e = level_start[L + 1];
+        int64_t ne = e + 8 * (int64_t)n_marked;
+        if (ne > capacity) {
+            atomicMax(status, VF_ECAPACITY);
+            status[1] = L;  // level context
+            ne = e;         // drop the level: later stages see no blocks, no OOB ids
+        }
+        for (int k = L + 2; k <= VF_MAX_LEVELS; ++k) level_start[k] = (int32_t)ne;
     }
-    for (int k = L + 2; k <= VF_MAX_LEVELS; ++k) level_start[k] = (int32_t)ne;
-}
+};
 
 // bit index of a direction in {-1,0,1}^3: (dx+1) + 3(dy+1) + 9(dz+1)
 __device__ __forceinline__ int dir_code(int dx, int dy, int dz) {
@@ -399,13 +399,14 @@ int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_byte
     int32_t *parents = (int32_t *)base;
     int32_t *scalars = (int32_t *)(base + al256(sizeof(int32_t) * ((size_t)g->capacity + 1)));
     void *scan_ws = base + al256(sizeof(int32_t) * ((size_t)g->capacity + 1)) + al256(sizeof(int32_t) * 8);
-    k_level_count<<<1, 32, 0, st>>>(L, g->d_level_start, scalars);
-    int rc = check_launch("k_level_count");
-    if (rc) return rc;
-    cudaError_t ce = scan_launch(LoadMark{g->d_level_start, L, g->d_bflags},
-                                 EmitChild{g->d_level_start, L, g->d_child, g->d_bflags, parents},
-                                 g->capacity, scalars, scalars + 1, scan_ws, st);
+    // child ids = exclusive scan of the level's marks; the publishing thread
+    // also appends the new level (AdaptFinish: level_start[L+2..], capacity)
+    cudaError_t ce = scan_launch_fn(LoadMark{g->d_level_start, L, g->d_bflags},
+                                    EmitChild{g->d_level_start, L, g->d_child, g->d_bflags, parents},
+                                    g->capacity, ScanLevelN{g->d_level_start, L}, scalars + 1, scan_ws,
+                                    st, AdaptFinish{L, g->capacity, g->d_level_start, g->d_status});
     if (ce != cudaSuccess) return set_cuda_error(ce, "adapt scan");
+    int rc;
     k_adapt_children<<<max_ctas(8), 256, 0, st>>>(
         L, g->capacity, cfg.nb[0] << (L + 1), cfg.nb[1] << (L + 1), cfg.nb[2] << (L + 1),
         g->d_level_start, scalars + 1, parents, g->d_coords, g->d_nbr, g->d_nbr_child, g->d_child,
@@ -414,8 +415,6 @@ int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_byte
     k_adapt_level<<<max_ctas(8), 256, 0, st>>>(L, g->d_level_start, g->d_nbr, g->d_nbr_child,
                                                g->d_child, g->d_masks);
     if ((rc = check_launch("k_adapt_level"))) return rc;
-    k_adapt_finish<<<1, 32, 0, st>>>(L, g->capacity, g->d_level_start, scalars + 1, g->d_status);
-    if ((rc = check_launch("k_adapt_finish"))) return rc;
     g->n_levels = L + 2;
     return VF_OK;
 }

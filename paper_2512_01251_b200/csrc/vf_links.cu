@@ -135,10 +135,6 @@ struct EmitCmap {
     }
 };
 
-__global__ void k_level_count2(int L, const int32_t *__restrict__ level_start, int32_t *__restrict__ out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) *out = level_start[L + 1] - level_start[L];
-}
-
 size_t tables_workspace_size(int32_t capacity) {
     return 256 + ((scan_workspace_bytes(capacity) + 255) & ~(size_t)255);
 }
@@ -151,11 +147,9 @@ int tables_impl(vf_grid *g, const int32_t *bcount, int32_t *cmap, int32_t *d_n_b
     void *scan_ws = (char *)ws + 256;
     // non-finest blocks are never mapped
     cudaMemsetAsync(cmap, 0xff, sizeof(int32_t) * (size_t)g->capacity, st);
-    k_level_count2<<<1, 32, 0, st>>>(L, g->d_level_start, scal);
-    int rc = check_launch("k_level_count2");
-    if (rc) return rc;
-    cudaError_t ce = scan_launch(LoadBnd{g->d_level_start, L, bcount}, EmitCmap{g->d_level_start, L, cmap},
-                                 g->capacity, scal, d_n_b, scan_ws, st);
+    (void)scal;
+    cudaError_t ce = scan_launch_fn(LoadBnd{g->d_level_start, L, bcount}, EmitCmap{g->d_level_start, L, cmap},
+                                    g->capacity, ScanLevelN{g->d_level_start, L}, d_n_b, scan_ws, st);
     return ce == cudaSuccess ? VF_OK : set_cuda_error(ce, "tables scan");
 }
 

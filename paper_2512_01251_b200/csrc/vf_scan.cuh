@@ -42,21 +42,43 @@ __device__ __forceinline__ int warp_sum_scan(int v) {
     return v;
 }
 
-template <typename Load, typename Emit>
+// element count: device-resident value, or the static bound
+struct ScanN {
+    const int32_t *d_n;
+    int64_t n_static;
+    __device__ int64_t operator()() const { return d_n ? (int64_t)(*d_n) : n_static; }
+};
+// element count of a level: level_start[L+1] - level_start[L] (device-resident)
+struct ScanLevelN {
+    const int32_t *level_start;
+    int L;
+    __device__ int64_t operator()() const { return (int64_t)level_start[L + 1] - level_start[L]; }
+};
+struct ScanNoEpi {
+    __device__ void operator()(int) const {}
+};
+
+// Epi(total) runs once, on the thread that publishes the total (after every
+// element's prefix is known to that thread's tile; other tiles may still be
+// emitting, so Epi must not depend on Emit's outputs)
+template <typename Load, typename Emit, typename NFn = ScanN, typename Epi = ScanNoEpi>
 __global__ void __launch_bounds__(kScanThreads)
-    scan_kernel(Load load, Emit emit, int64_t n_static, const int32_t *__restrict__ d_n,
-                int32_t *__restrict__ d_total, uint64_t *__restrict__ status) {
+    scan_kernel(Load load, Emit emit, NFn nfn, int32_t *__restrict__ d_total,
+                uint64_t *__restrict__ status, Epi epi = Epi()) {
     __shared__ int s_warp[kScanThreads / 32];
     __shared__ int s_tile;
     __shared__ int s_prefix;
-    const int64_t n = d_n ? (int64_t)(*d_n) : n_static;
+    const int64_t n = nfn();
     const int64_t n_tiles = (n + kScanTile - 1) / kScanTile;
     uint32_t *counter = reinterpret_cast<uint32_t *>(status);
     if (threadIdx.x == 0) s_tile = (int)atomicAdd(counter, 1u);
     __syncthreads();
     const int64_t tile = s_tile;
     if (n == 0) {
-        if (tile == 0 && threadIdx.x == 0 && d_total) *d_total = 0;
+        if (tile == 0 && threadIdx.x == 0) {
+            if (d_total) *d_total = 0;
+            epi(0);
+        }
         return;
     }
     if (tile >= n_tiles) return;
@@ -121,7 +143,10 @@ __global__ void __launch_bounds__(kScanThreads)
         }
         if (lane == 0) {
             s_prefix = prefix;
-            if (tile == n_tiles - 1 && d_total) *d_total = prefix + agg;
+            if (tile == n_tiles - 1) {
+                if (d_total) *d_total = prefix + agg;
+                epi(prefix + agg);
+            }
         }
     }
     __syncthreads();
@@ -139,16 +164,23 @@ inline size_t scan_workspace_bytes(int64_t n_bound) {
     return (size_t)(tiles + 2) * sizeof(uint64_t);
 }
 
-template <typename Load, typename Emit>
-cudaError_t scan_launch(Load load, Emit emit, int64_t n_bound, const int32_t *d_n,
-                        int32_t *d_total, void *ws, cudaStream_t st) {
+// n_bound bounds the device count (grid size); nfn gives the count on device
+template <typename Load, typename Emit, typename NFn, typename Epi = ScanNoEpi>
+cudaError_t scan_launch_fn(Load load, Emit emit, int64_t n_bound, NFn nfn, int32_t *d_total,
+                           void *ws, cudaStream_t st, Epi epi = Epi()) {
     const int64_t tiles = (n_bound + kScanTile - 1) / kScanTile;
     cudaError_t e = cudaMemsetAsync(ws, 0, scan_workspace_bytes(n_bound), st);
     if (e != cudaSuccess) return e;
     const int64_t grid = tiles > 0 ? tiles : 1;
-    scan_kernel<<<(unsigned)grid, kScanThreads, 0, st>>>(load, emit, n_bound, d_n, d_total,
-                                                        reinterpret_cast<uint64_t *>(ws));
+    scan_kernel<<<(unsigned)grid, kScanThreads, 0, st>>>(load, emit, nfn, d_total,
+                                                        reinterpret_cast<uint64_t *>(ws), epi);
     return cudaGetLastError();
+}
+
+template <typename Load, typename Emit>
+cudaError_t scan_launch(Load load, Emit emit, int64_t n_bound, const int32_t *d_n,
+                        int32_t *d_total, void *ws, cudaStream_t st) {
+    return scan_launch_fn(load, emit, n_bound, ScanN{d_n, n_bound}, d_total, ws, st);
 }
 
 }  // namespace vf
