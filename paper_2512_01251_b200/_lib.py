@@ -97,6 +97,10 @@ _SIGS = {
     "vf_shard_boundary": (_I32, [_CP, _GP, _P, _P]),
     "vf_shard_links": (_I32, [_CP, _P, _I64, _GP, _P, _P, _P, _I64, _P, _SZ, _P]),
     "vf_lbm_init": (_I32, [_GP, C.c_int32, C.c_int32, C.c_double, _P, _P, _P]),
+    "vf_stl_workspace_size": (_SZ, [_I64]),
+    "vf_stl_scan": (_I32, [_P, _I64, _P, _SZ, _P, _P, _P, _P]),
+    "vf_stl_weld_workspace_size": (_SZ, [_I64]),
+    "vf_stl_build": (_I32, [_P, _I64, _P, _SZ, _I64, C.c_double, _P, _SZ, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vf_lbm_step": (_I32, [_CP, _GP, _I32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),
 }
 

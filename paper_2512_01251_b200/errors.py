@@ -12,6 +12,10 @@ class MeshError(ValueError):
     """Invalid mesh input (geometry.py:28)."""
 
 
+class StlParseError(MeshError):
+    """Malformed STL input (geometry.py:32)."""
+
+
 class CapacityError(VoxforestError, MemoryError):
     """Forest block capacity / scratch capacity exhausted."""
 

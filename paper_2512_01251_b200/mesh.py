@@ -50,13 +50,32 @@ class TriangleMesh:
             raise MeshError("face index out of range")
         fc = self.vertices[self.faces_indexed.reshape(-1)].reshape(len(self.faces_indexed), 9)
         self.faces_coord = np.ascontiguousarray(fc)
-        self.faces_coord_cm = np.ascontiguousarray(fc.T)
         v = self.vertices[self.faces_indexed]
         n = np.cross(v[:, 1] - v[:, 0], v[:, 2] - v[:, 0])
         lens = np.linalg.norm(n, axis=1)
         if np.any(lens == 0.0):
             raise MeshError("degenerate face (zero normal)")
         self.normals = n / lens[:, None]
+
+    @classmethod
+    def from_arrays(cls, vertices, faces_indexed, faces_coord, normals, dim=3):
+        """A mesh whose derived arrays were built elsewhere (GPU STL
+        ingestion, stl.py) with the same operations as __init__."""
+        m = cls.__new__(cls)
+        m.vertices = np.ascontiguousarray(vertices, dtype=np.float64)
+        m.faces_indexed = np.ascontiguousarray(faces_indexed, dtype=np.int64)
+        m.dim = int(dim)
+        m.faces_coord = np.ascontiguousarray(faces_coord, dtype=np.float64)
+        m.normals = np.ascontiguousarray(normals, dtype=np.float64)
+        return m
+
+    @property
+    def faces_coord_cm(self) -> np.ndarray:
+        """Column-major copy of faces_coord (geometry.py:88), built on demand."""
+        cm = self.__dict__.get("_faces_coord_cm")
+        if cm is None:
+            cm = self.__dict__["_faces_coord_cm"] = np.ascontiguousarray(self.faces_coord.T)
+        return cm
 
     @property
     def n_faces(self) -> int:
