@@ -434,7 +434,8 @@ def main():
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "lbm": lbm,
         "gpu_launches": int(kernels_per_step * args.steps),
         "gpu_launch_note": (f"{kernels_per_step} kernels per embed" +
-                            ("" if sharded else ", issued as one CUDA graph per step")),
+                            ("" if sharded else (", issued as one CUDA graph per step" if eng.use_graph
+                                                  else ", eager launches (stream priorities)"))),
         "clocks": ck,
     }
     print(json.dumps(line), flush=True)

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kVoxWarps * 32, VF_VOX_MINB)
 
 int voxelize_impl(const LevelInfo &li, vf_grid *g, int L, const vf_bins *bins,
                   const double *faces, cudaStream_t st) {
-    k_voxelize<<<max_ctas(8), kVoxWarps * 32, 0, st>>>(li, L, g->d_level_start, g->d_coords,
+    k_voxelize<<<max_ctas(VF_VOX_MINB), kVoxWarps * 32, 0, st>>>(li, L, g->d_level_start, g->d_coords,
                                                       g->d_masks, bins->d_offsets, bins->d_n_face_ids,
                                                       bins->d_face_ids, faces);
     return check_launch("k_voxelize");

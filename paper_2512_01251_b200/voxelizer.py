@@ -159,8 +159,14 @@ class EmbedEngine:
     PAPER.md:273).  All work runs on the engine's own stream, ordered after
     the caller's current stream."""
 
+    # above this many faces the embed is throughput-bound: eager launches keep
+    # the stream priorities (the low-priority cut-link enumeration yields to
+    # the level pipeline), which CUDA-graph node priorities did not reproduce
+    # (C4: 5.0 ms eager vs 5.6 ms graph); below it the graph saves launches
+    GRAPH_MAX_FACES = 1_000_000
+
     def __init__(self, mesh, cfg: EmbedConfig, capacity: Optional[int] = None,
-                 use_graph: bool = True):
+                 use_graph: Optional[bool] = None):
         import torch
         self.lib = _lib.require_cuda()
         self.cfg = cfg
@@ -181,7 +187,7 @@ class EmbedEngine:
         self.lengths = None
         self.bc_ids = None
         self.lengths_cap = 0
-        self.use_graph = use_graph
+        self.use_graph = (self.mesh.n_faces <= self.GRAPH_MAX_FACES) if use_graph is None else use_graph
         self._graphs = {}
         self.n_events = 64
         self.events = [torch.cuda.Event(enable_timing=True) for _ in range(self.n_events)]
