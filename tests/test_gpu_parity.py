@@ -385,3 +385,20 @@ def test_links_band_overflow_fallback(O, torus):
         finally:
             lib.vf_set_link_band_cap(old)
         assert np.array_equal(a, b)
+
+
+def test_cli_voxelize(tmp_path):
+    """CLI voxelize: one VTK per level, masks equal to the engine's, summary."""
+    import json
+    from paper_2512_01251_b200 import cli
+    from paper_2512_01251_b200.vtk import read_vtk_cell_data
+    rc = cli.main(["voxelize", "--primitive", "sphere", "--nx", "16", "--lmax", "2", "--out", str(tmp_path)])
+    assert rc == 0
+    summary = json.load(open(tmp_path / "summary.json"))
+    assert summary["files"] == ["level_0.vtk", "level_1.vtk"] and summary["links"] > 0
+    grid, table = EmbedEngine(make_icosphere((0.5, 0.5, 0.5), 0.5, 4), EmbedConfig(n_x=16, l_max=2)).run()
+    g = grid.to_numpy()
+    for L in range(2):
+        s, e = int(g["level_start"][L]), int(g["level_start"][L + 1])
+        d = read_vtk_cell_data(str(tmp_path / f"level_{L}.vtk"))
+        assert np.array_equal(d["mask"], g["masks"][s:e].reshape(-1))
