@@ -402,3 +402,41 @@ def test_cli_voxelize(tmp_path):
         s, e = int(g["level_start"][L]), int(g["level_start"][L + 1])
         d = read_vtk_cell_data(str(tmp_path / f"level_{L}.vtk"))
         assert np.array_equal(d["mask"], g["masks"][s:e].reshape(-1))
+
+
+# ---------------------------------------------------------------------------
+# configuration edge cases: code paths the default configs never take
+
+def _open_patch():
+    """A small open surface (two triangles) partly outside the domain."""
+    from paper_2512_01251_b200.mesh import TriangleMesh
+    V = np.array([[0.30, 0.40, 0.55], [0.80, 0.35, 0.60], [0.45, 0.85, 0.40], [1.20, 0.90, 0.50]])
+    return TriangleMesh(V, np.array([[0, 1, 2], [1, 3, 2]]))
+
+
+@pytest.mark.parametrize("case", ["nx48_nonpow2", "domain_2x1x1", "eps0", "no_filter_torus",
+                                  "open_patch", "lmax1", "nspec1", "bincap"])
+def test_embed_config_edges(O, case):
+    torus = translate(make_torus(60, 30), (0.0021, -0.0013, 0.0017))
+    if case == "nx48_nonpow2":      # dx = 1/48: inexact 1/dx, widened ranges
+        mesh, cfg = torus, EmbedConfig(n_x=48, l_max=3)
+    elif case == "domain_2x1x1":    # non-cubic domain, mesh off-centre
+        mesh, cfg = translate(torus, (0.6, 0.0, 0.0)), EmbedConfig(n_x=32, l_max=3, domain=(2.0, 1.0, 1.0))
+    elif case == "eps0":            # eps_slab = 0: the link fast path is disabled
+        mesh, cfg = torus, EmbedConfig(n_x=32, l_max=3, eps_slab=0.0)
+    elif case == "no_filter_torus":
+        mesh, cfg = torus, EmbedConfig(n_x=32, l_max=3, use_filter=False)
+    elif case == "open_patch":      # open surface leaving the domain, refined to l_spec
+        from paper_2512_01251_b200.mesh import l_spec_bound, refine_faces
+        cfg = EmbedConfig(n_x=32, l_max=3)
+        mesh = refine_faces(_open_patch(), l_spec_bound(cfg.domain, cfg.n_spec, cfg.l_max, cfg.nb[0]))
+    elif case == "lmax1":           # root level only: no refinement
+        mesh, cfg = torus, EmbedConfig(n_x=32, l_max=1)
+    elif case == "nspec1":          # N_spec = 1 -> N_lim = 27 pairs / face
+        mesh, cfg = torus, EmbedConfig(n_x=32, l_max=3, n_spec=1)
+    else:                           # faces above l_spec: the N_lim cap is asserted (SPEC.md:146)
+        from paper_2512_01251_b200 import BinCapError
+        with pytest.raises(BinCapError):
+            EmbedEngine(_open_patch(), EmbedConfig(n_x=32, l_max=3)).run()
+        return
+    _embed_compare(O, mesh, cfg, use_filter=cfg.use_filter)
