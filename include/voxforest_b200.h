@@ -215,6 +215,10 @@ int vf_embed_graph_create(const vf_config *cfg, const double *d_faces,
                           void *stream, void **graph_exec);
 int vf_graph_launch(void *graph_exec, void *stream);
 void vf_graph_destroy(void *graph_exec);
+/* wait for the library's per-device side streams (phase 1 launches the
+ * grid-independent cut-link enumeration there; phase 2 joins it).  Call after
+ * a phase 1 that is not followed by phase 2 before releasing its workspace. */
+int vf_side_sync(void);
 /* number of kernels this library has launched in the process (bench hook) */
 int64_t vf_launch_count(void);
 /* multi-GPU exchange helper: zero the level-L entries of blocks this rank

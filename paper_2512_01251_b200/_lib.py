@@ -87,6 +87,7 @@ _SIGS = {
     "vf_graph_launch": (_I32, [_P, _P]),
     "vf_graph_destroy": (None, [_P]),
     "vf_launch_count": (_I64, []),
+    "vf_side_sync": (_I32, []),
     "vf_check_status": (_I32, [_GP, _P]),
     "vf_shard_zero_unowned": (_I32, [_CP, _GP, _I32, _P, _P]),
     "vf_set_link_band_cap": (_I64, [_I64]),

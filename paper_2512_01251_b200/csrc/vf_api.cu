@@ -402,6 +402,17 @@ static int side_stream(SideStream **out) {
     return VF_OK;
 }
 
+// wait for the side streams of this device (the cut-link enumeration of a
+// phase 1 that was not followed by phase 2 -- the LUT-sizing run, an error --
+// must not outlive the caller's workspace)
+extern "C" int vf_side_sync(void) {
+    SideStream *side = nullptr;
+    VF_TRY(side_stream(&side));
+    cudaError_t e = cudaStreamSynchronize(side->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(side->st3);
+    return e == cudaSuccess ? VF_OK : set_cuda_error(e, "vf_side_sync");
+}
+
 // Phase 1.  The spatial bins do not depend on the grid, so they are built on
 // a side stream one level AHEAD of the level pipeline (ping-pong buffers):
 // bins(L+1) overlaps voxelize / propagate / mark / adapt of level L; the main

@@ -269,14 +269,16 @@ __device__ int face_pairs(const double *v, const LevelInfo &li, int nlim, int32_
             for (int bi = a[0]; bi <= b[0]; ++bi) {
                 const double mx = VF_DSUB(VF_DMUL((double)bi, h), dx), Mx = VF_DADD(VF_DMUL((double)(bi + 1), h), dx);
                 if (sat_exact(f, mx, my, mz, Mx, My, Mz)) {
-                    if (cnt >= nlim) return -1;
-                    const int32_t bin = bi + li.bins[0] * (bj + li.bins[1] * bk);
-                    slot[cnt++] = bin;
-                    if (counts) atomicAdd(&counts[bin], 1);
+                    if (cnt >= nlim) return -1;  // no histogram entry was made yet
+                    slot[cnt++] = bi + li.bins[0] * (bj + li.bins[1] * bk);
                 }
             }
         }
     }
+    // histogram only once the face is known to respect N_lim: a capped face
+    // contributes nothing, so the bin slices stay consistent with the scatter
+    if (counts)
+        for (int k = 0; k < cnt; ++k) atomicAdd(&counts[slot[k]], 1);
     return cnt;
 }
 

@@ -237,6 +237,9 @@ class EmbedEngine:
         self.host[0:4].copy_(self.grid.status, non_blocking=True)
         self.host[4:5].copy_(self.n_b_dev, non_blocking=True)
         st_obj.synchronize()
+        # the side streams (cut-link enumeration) are done after phase 2; after
+        # a phase 1 alone (LUT sizing, errors) wait for them explicitly
+        _lib.check(self.lib.vf_side_sync(), "embed_geometry")
         h = self.host.tolist()
         if h[0]:
             gs = self.grid._struct()
@@ -287,8 +290,96 @@ class EmbedEngine:
                 self._alloc_lut(n_b)
                 return self.run(timed, use_filter)
         cur.wait_stream(self.stream)
+        self._n_used = int(self.grid.level_start[self.grid.n_levels].item())  # static for a fixed mesh
         table = LinkTable(self.lengths[:n_b], self.bc_ids[:n_b], self.cmap, n_b)
         return self.grid, table
+
+    # -- pipelined serving path ---------------------------------------------
+    def run_async(self, use_filter: Optional[bool] = None):
+        """Enqueue one embed on the engine stream without a host sync (steady
+        state: the LUT is sized, N_b is static for a fixed mesh).  The status
+        and N_b are copied back asynchronously; check_async() validates them."""
+        import torch
+        if self.lengths is None:
+            return self.run(use_filter=use_filter)
+        uf = bool(self.cfg.use_filter if use_filter is None else use_filter)
+        st = _lib.stream_ptr(self.stream)
+        n_b = int(self.host[4])
+        with torch.cuda.stream(self.stream):
+            self.grid.status.zero_()
+            if self.use_graph and uf in self._graphs:
+                _lib.check(self.lib.vf_graph_launch(self._graphs[uf], st), "embed_geometry")
+            else:
+                gs = self._phase1(uf, st, None)
+                self._phase2(gs, st, None)
+            self.grid.n_levels = self.cfg.l_max
+            if not hasattr(self, "_host_async"):
+                self._host_async = torch.zeros(8, dtype=torch.int32).pin_memory()
+            self._host_async[0:4].copy_(self.grid.status, non_blocking=True)
+            self._host_async[4:5].copy_(self.n_b_dev, non_blocking=True)
+        table = LinkTable(self.lengths[:n_b], self.bc_ids[:n_b], self.cmap, n_b)
+        return self.grid, table
+
+    def check_async(self):
+        """Validate the last run_async (synchronizes the engine stream)."""
+        self.stream.synchronize()
+        h = self._host_async.tolist() if hasattr(self, "_host_async") else self.host.tolist()
+        if h[0]:
+            gs = self.grid._struct()
+            _lib.check(self.lib.vf_check_status(C.byref(gs), _lib.stream_ptr(self.stream)), "embed_geometry")
+        if h[4] != int(self.host[4]):
+            raise RuntimeError("N_b changed between pipelined embeds of the same mesh")
+
+    def embed_host_async(self, faces_coord, normals, out, in_stream, out_stream):
+        """One pipelined end-to-end step: pinned host faces -> H2D on
+        ``in_stream`` -> pack + embed on the engine stream -> D2H of the
+        results on ``out_stream`` into the pinned ``out`` buffers (allocated on
+        first use).  No host sync: with two engines alternating, the D2H of one
+        step overlaps the next step's upload and compute.  Returns (out, h2d
+        bytes, d2h bytes)."""
+        import torch
+        F = self.mesh.n_faces
+        if not hasattr(self, "_dfc"):
+            self._dfc = torch.empty((F, 9), dtype=torch.float64, device="cuda")
+            self._dn = torch.empty((F, 3), dtype=torch.float64, device="cuda")
+            self._ev_pack = torch.cuda.Event()
+            self._ev_h2d = torch.cuda.Event()
+            self._ev_done = torch.cuda.Event()
+            self._ev_d2h = torch.cuda.Event()
+            self._ev_pack.record(self.stream)
+            self._ev_d2h.record(out_stream)
+        in_stream.wait_event(self._ev_pack)        # the previous pack has read the buffers
+        with torch.cuda.stream(in_stream):
+            self._dfc.copy_(faces_coord, non_blocking=True)
+            self._dn.copy_(normals, non_blocking=True)
+            self._ev_h2d.record(in_stream)
+        self.stream.wait_event(self._ev_h2d)
+        self.stream.wait_event(self._ev_d2h)       # the previous results were copied out
+        _lib.check(self.lib.vf_pack_faces(_lib.ptr(self._dfc), _lib.ptr(self._dn), F,
+                                          _lib.ptr(self.mesh.faces), _lib.stream_ptr(self.stream)),
+                   "pack_faces")
+        self._ev_pack.record(self.stream)
+        grid, table = self.run_async()
+        self._ev_done.record(self.stream)
+        out_stream.wait_event(self._ev_done)
+        n = self._n_used  # from the last synchronous run (no host sync here)
+        res = {"coords": grid.coords[:n], "nbr": grid.nbr[:n], "child": grid.child[:n],
+               "bflags": grid.bflags[:n], "masks": grid.masks[:n],
+               "contraction_map": table.contraction_map[:n], "lengths": table.lengths}
+        if out is None:
+            out = {}
+        d2h = 0
+        with torch.cuda.stream(out_stream):
+            for k, t in res.items():
+                buf = out.get(k)
+                if buf is None or buf.shape != t.shape:
+                    buf = torch.empty(t.shape, dtype=t.dtype).pin_memory()
+                    out[k] = buf
+                buf.copy_(t, non_blocking=True)
+                d2h += t.numel() * t.element_size()
+            self._ev_d2h.record(out_stream)
+        h2d = faces_coord.numel() * 8 + normals.numel() * 8
+        return out, h2d, d2h
 
     @property
     def n_b_host(self):
