@@ -114,15 +114,17 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(config, kernel):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
-    from the committed ncu --set full summary (profiles/ncu_traffic.json,
-    written by tools/ncu_traffic.py), or None."""
+def ncu_traffic(config, *kernels):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch, summed over
+    `kernels`, from the committed ncu --set full summary
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
-    d = json.load(open(p)).get(config, {}).get(kernel)
-    return None if d is None else d.get("dram_bytes")
+    d = json.load(open(p)).get(config, {})
+    if not all(k in d for k in kernels):
+        return None
+    return float(sum(d[k]["dram_bytes"] for k in kernels))
 
 
 def cpu_baseline(mesh, cfg, cells, repeat=1):
@@ -397,10 +399,12 @@ def main():
         achieved = link_bytes / (lk / 1e3) / 1e9
         roofline = {"kernel": "k_links", "bound": "hbm", "achieved": achieved, "peak": peak,
                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": ncu_traffic(args.config, "k_links"), "kernel_ms": lk,
+                    "traffic": ncu_traffic(args.config, "k_links_enum", "k_links_resolve"), "kernel_ms": lk,
                     "algorithmic_bytes": int(link_bytes),
-                    "timed": "CUDA events on the engine stream around k_links + k_links_band + "
-                             "the overflow fallback (a no-op unless the band list overflowed)"}
+                    "timed": "CUDA events around the cut-link kernels: the grid-independent line "
+                             "enumeration (k_links<2>, side stream, overlapped with the level pipeline) "
+                             "+ the resolution after the tables (k_links_resolve, overflow faces, "
+                             "band list, fallback)"}
     else:
         n_b = int(run()[1].n_b)
 

@@ -11,6 +11,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 # steady-state launches: skip the first embed of one_embed (phase1 + phase2 eager)
 timeout 1200 ncu --set full --clock-control none -k regex:"k_links|k_voxelize|k_pairs|k_adapt_children|k_boundary|k_xrows|k_indicators_all|k_fill_lut" -s 40 -c 40 -o /tmp/full_c2 -f python tools/one_embed.py c2 2 > gpurun_out/ncu_full.log 2>&1
 python tools/ncu_traffic.py /tmp/full_c2.ncu-rep c2 > gpurun_out/ncu_traffic_c2.txt 2>&1
+timeout 1200 ncu --set full --clock-control none -k regex:"k_links|k_fill_lut" -s 5 -c 5 -o /tmp/full_c4 -f python tools/one_embed.py c4 2 > gpurun_out/ncu_full_c4.log 2>&1
+python tools/ncu_traffic.py /tmp/full_c4.ncu-rep c4 > gpurun_out/ncu_traffic_c4.txt 2>&1
 cp profiles/ncu_traffic.json gpurun_out/ncu_traffic.json
 python tools/ncu_summary.py gpurun_out/launches_c2.csv 3 > gpurun_out/launches_c2.txt
 python tools/ncu_summary.py gpurun_out/launches_c4.csv 2 > gpurun_out/launches_c4.txt

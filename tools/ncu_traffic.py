@@ -10,8 +10,8 @@ rep, key = sys.argv[1], sys.argv[2]
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h, units = rows[0], rows[1]
-MB = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-US = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+MB = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+US = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
 
 
 def val(row, name, scale=None):
@@ -26,8 +26,8 @@ res = {}
 for row in rows[2:]:
     name = re.sub(r"\(.*", "", row[h.index("Kernel Name")]).replace("void ", "").strip()
     name = re.sub(r"^vf::", "", name)
-    if name.startswith("k_links<"):
-        name = "k_links" if "<0>" in name or "<false>" in name else "k_links_full"
+    if name.startswith("k_links<"):  # MODE 0 direct / 1 overflow fallback / 2 line enumeration
+        name = {"0": "k_links", "1": "k_links_full", "2": "k_links_enum"}.get(name[8:9], name)
     name = re.sub(r"<.*", "", name)
     d = {"launches": 1,
          "time_us": val(row, "gpu__time_duration.sum", US),
