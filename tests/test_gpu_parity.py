@@ -440,3 +440,15 @@ def test_embed_config_edges(O, case):
             EmbedEngine(_open_patch(), EmbedConfig(n_x=32, l_max=3)).run()
         return
     _embed_compare(O, mesh, cfg, use_filter=cfg.use_filter)
+
+
+def test_embed_c2_bench_config(O):
+    """The bench workload itself (C2: 112,000-face torus, N_x=64, L_max=4)
+    against the oracle, end to end."""
+    _embed_compare(O, make_torus(280, 200), EmbedConfig(n_x=64, l_max=4))
+
+
+def test_embed_c4_flagship(O):
+    """C4 (7,200,000-face torus, L_max=5: the north-star mesh) against the
+    oracle, end to end -- also exercises the eager (>1M faces) launch path."""
+    _embed_compare(O, make_torus(3000, 1200), EmbedConfig(n_x=64, l_max=5))
