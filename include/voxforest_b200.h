@@ -282,6 +282,12 @@ int vf_check_status(const vf_grid *grid, void *stream);
  * n < 0 only queries. */
 int64_t vf_set_link_band_cap(int64_t n);
 
+/* Measurement hook: 1 = run the cut-link line enumeration serially on the
+ * caller's stream after the tables (its events then time the kernel alone),
+ * 0 = overlapped on the side stream (default; results identical).  Returns
+ * the old value; on < 0 only queries.  Affects graphs created afterwards. */
+int vf_set_serial_links(int on);
+
 #ifdef __cplusplus
 }
 #endif

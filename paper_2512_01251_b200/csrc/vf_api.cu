@@ -419,6 +419,11 @@ extern "C" int vf_side_sync(void) {
 // stream only waits for bins(L) before voxelizing L, and the side stream
 // waits for voxelize(L-1) before reusing its buffer.  Captured into the
 // embed graph the two streams become parallel branches.
+// vf_set_serial_links: run the cut-link enumeration on the main stream after
+// the tables instead of overlapped on the low-priority side stream, so its
+// CUDA events time the kernel alone (the roofline figure in bench.py).
+static int g_serial_links = 0;
+
 int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int use_filter,
                     vf_grid *g, int32_t *cmap, int32_t *d_n_b, void *ws, size_t ws_bytes,
                     void *stream, void **events) {
@@ -441,9 +446,11 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     // in phase 2, where the recorded lines are resolved)
     cudaEventRecord(side->fork, st);
     cudaStreamWaitEvent(s2, side->fork, 0);
-    cudaStreamWaitEvent(side->st3, side->fork, 0);
-    VF_TRY(link_enum_impl(*cfg, faces, F, w.link_ws, w.lines_ws, side->st3, events ? events + 58 : nullptr));
-    cudaEventRecord(side->join3, side->st3);
+    if (!g_serial_links) {
+        cudaStreamWaitEvent(side->st3, side->fork, 0);
+        VF_TRY(link_enum_impl(*cfg, faces, F, w.link_ws, w.lines_ws, side->st3, events ? events + 58 : nullptr));
+        cudaEventRecord(side->join3, side->st3);
+    }
     // Alg. 1 indicators of every level in one pass over the face records
     if (use_filter) VF_TRY(launch_indicators_all(*cfg, faces, F, w.ind_bits, s2));
     auto build = [&](int L) {
@@ -476,7 +483,17 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     VF_TRY(boundary_impl(*cfg, g, w.bcount, st));
     VF_TRY(tables_impl(g, w.bcount, cmap, d_n_b, w.tab_ws, w.tab_b, st));
     rec(events, n_ev, &k, st);  // boundary + tables done
+    if (g_serial_links) {  // measurement mode: the enumeration alone on the main stream
+        VF_TRY(link_enum_impl(*cfg, faces, F, w.link_ws, w.lines_ws, st, events ? events + 58 : nullptr));
+        cudaEventRecord(side->join3, st);
+    }
     return VF_OK;
+}
+
+int vf_set_serial_links(int on) {
+    const int old = g_serial_links;
+    if (on >= 0) g_serial_links = on ? 1 : 0;
+    return old;
 }
 
 int64_t vf_launch_count(void) { return (int64_t)g_launches.load(); }

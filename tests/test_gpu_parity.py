@@ -387,6 +387,24 @@ def test_links_band_overflow_fallback(O, torus):
         assert np.array_equal(a, b)
 
 
+def test_serial_links_identical(torus):
+    """The measurement schedule (enumeration serial on the main stream) gives
+    the same LUT and cut-link map as the overlapped production schedule."""
+    from paper_2512_01251_b200 import _lib
+    lib = _lib.require_cuda()
+    eng = EmbedEngine(torus, EmbedConfig(n_x=32, l_max=3), use_graph=False)
+    g1, t1 = eng.run(timed=True)
+    a, ca = t1.lengths.cpu().numpy().copy(), t1.contraction_map.cpu().numpy().copy()
+    old = lib.vf_set_serial_links(1)
+    try:
+        _, t2 = eng.run(timed=True)
+        b, cb = t2.lengths.cpu().numpy(), t2.contraction_map.cpu().numpy()
+        assert eng.link_kernel_ms() > 0
+    finally:
+        lib.vf_set_serial_links(old)
+    assert np.array_equal(a, b) and np.array_equal(ca, cb)
+
+
 def test_cli_voxelize(tmp_path):
     """CLI voxelize: one VTK per level, masks equal to the engine's, summary."""
     import json
