@@ -221,6 +221,13 @@ void vf_graph_destroy(void *graph_exec);
 int vf_side_sync(void);
 /* number of kernels this library has launched in the process (bench hook) */
 int64_t vf_launch_count(void);
+
+/* Counters of the last embed's cut-link pass on this workspace (synchronous):
+ * out[6] = {piercing lines recorded, line capacity, faces whose lines
+ * overflowed (redone by the direct kernel), band candidates, band capacity,
+ * faces enumerated by the large-face kernel}. */
+int vf_embed_link_stats(const vf_config *cfg, int64_t F, int32_t capacity, void *ws, size_t ws_bytes,
+                        int64_t *out);
 /* multi-GPU exchange helper: zero the level-L entries of blocks this rank
  * does not own (block flags, solid64 and, if given, d_bcount) so that one
  * all-reduce (MAX for flags, SUM for solid64/bcount) publishes the owners'
@@ -287,6 +294,13 @@ int64_t vf_set_link_band_cap(int64_t n);
  * 0 = overlapped on the side stream (default; results identical).  Returns
  * the old value; on < 0 only queries.  Affects graphs created afterwards. */
 int vf_set_serial_links(int on);
+
+/* Tuning / test hook: faces whose bounding box spans at most e cells are
+ * enumerated thread per face (k_links_small), larger ones by the
+ * warp-flattened kernel (default 1.5; results identical for any e; e < 0
+ * sends every face to the large-face kernel).  Returns the old value; NaN
+ * only queries. */
+float vf_set_link_small_ext(float e);
 
 #ifdef __cplusplus
 }

@@ -87,11 +87,13 @@ _SIGS = {
     "vf_graph_launch": (_I32, [_P, _P]),
     "vf_graph_destroy": (None, [_P]),
     "vf_launch_count": (_I64, []),
+    "vf_embed_link_stats": (_I32, [_CP, _I64, _I32, _P, _SZ, _P]),
     "vf_side_sync": (_I32, []),
     "vf_check_status": (_I32, [_GP, _P]),
     "vf_shard_zero_unowned": (_I32, [_CP, _GP, _I32, _P, _P]),
     "vf_set_link_band_cap": (_I64, [_I64]),
     "vf_set_serial_links": (_I32, [_I32]),
+    "vf_set_link_small_ext": (C.c_float, [C.c_float]),
     "vf_shard_owner_bytes": (_SZ, [_CP]),
     "vf_shard_owner_map": (_I32, [_CP, _GP, _I32, _P, _SZ, _P]),
     "vf_shard_level": (_I32, [_CP, _P, _I64, _I32, _GP, _I32, _P, _SZ, _P]),

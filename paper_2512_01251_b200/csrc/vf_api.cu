@@ -498,6 +498,15 @@ int vf_set_serial_links(int on) {
 
 int64_t vf_launch_count(void) { return (int64_t)g_launches.load(); }
 
+int vf_embed_link_stats(const vf_config *cfg, int64_t F, int32_t capacity, void *ws, size_t ws_bytes,
+                        int64_t *out) {
+    if (!valid_cfg(cfg) || F <= 0 || !ws || !out) return set_error(VF_EARG, "vf_embed_link_stats: bad argument");
+    EmbedWs w;
+    if (embed_layout(*cfg, F, capacity, (char *)ws, &w) > ws_bytes)
+        return set_error(VF_EARG, "vf_embed_link_stats: workspace too small");
+    return link_stats(*cfg, F, w.link_ws, w.lines_ws, out);
+}
+
 int vf_embed_phase2(const vf_config *cfg, const double *faces, int64_t F, vf_grid *g,
                     const int32_t *cmap, const int32_t *d_n_b, float *lengths, int64_t lengths_cap,
                     void *ws, size_t ws_bytes, void *stream, void **link_events) {
@@ -543,7 +552,7 @@ int vf_embed_graph_create(const vf_config *cfg, const double *faces, int64_t F, 
         cudaGraphGetNodes(graph, nullptr, &nn);
         cudaGraphNode_t *nodes = (cudaGraphNode_t *)malloc(sizeof(cudaGraphNode_t) * (nn ? nn : 1));
         cudaGraphGetNodes(graph, nodes, &nn);
-        const void *enum_fn = link_enum_kernel();
+        const void *enum_fn = link_enum_kernel(0), *enum_small = link_enum_kernel(1);
         for (size_t i = 0; i < nn; ++i) {
             cudaGraphNodeType ty;
             if (cudaGraphNodeGetType(nodes[i], &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) continue;
@@ -551,7 +560,7 @@ int vf_embed_graph_create(const vf_config *cfg, const double *faces, int64_t F, 
             if (cudaGraphKernelNodeGetParams(nodes[i], &kp) != cudaSuccess) continue;
             cudaLaunchAttributeValue v;
             memset(&v, 0, sizeof(v));
-            v.priority = (kp.func == enum_fn) ? lo : hi;
+            v.priority = (kp.func == enum_fn || kp.func == enum_small) ? lo : hi;
             cudaGraphKernelNodeSetAttribute(nodes[i], cudaLaunchAttributePriority, &v);
         }
         free(nodes);

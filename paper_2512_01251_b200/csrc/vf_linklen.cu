@@ -580,6 +580,259 @@ __global__ void __launch_bounds__(kLinkWarps * 32, MODE == 1 ? 1 : VF_LINK_MINB)
     }
 }
 
+// ---- small faces: thread per face ----------------------------------------
+// At the north-star resolution most faces are smaller than a cell (C4: ~1.3
+// piercing lines per face over all 13 pairs), so the warp-flattened row lists
+// above spend their time on bookkeeping.  Faces whose bounding box spans at
+// most g_small_ext cells are enumerated here one per thread, in lattice-local
+// FP32: lengths in units of dx, relative to v1, with v1 = (b + w + 1/2) dx for
+// the node b = floor(v1/dx - 1/2) and w in [0, 1).  The trace of the line
+// through node b + I (pair R: p, q1, q2, s_j = c_qj c_p) in the plane
+// x_p = v1_p is then (M1 + o1, M2 + o2), M_j = I_qj - s_j I_p, o_j = s_j w_p -
+// w_qj -- the same quantities link_dir_setup / link_point form in absolute
+// FP64/FP32 coordinates, scaled by 1/dx, with smaller rounding (magnitudes of
+// a few cells); the margins t_k, tol, the crossing estimate and the node range
+// are the same formulas in these units, so the accept / undecided / miss
+// classes remain conservative and the recorded lines, band candidates and
+// hence the LUT are identical.  Larger faces are appended to a list for the
+// warp-flattened kernel.
+#ifndef VF_SMALL_MINB
+#define VF_SMALL_MINB 3
+#endif
+static float g_small_ext = 1.5f;  // vf_set_link_small_ext (test / tuning hook)
+
+__device__ __forceinline__ void line_store(const LinkCtx &c, int pos, int4 rec) {
+    if (pos < c.line_cap) {
+        c.lines[pos] = rec;
+    } else {  // buffer full: the direct kernel redoes the face after the tables
+        const uint32_t bit = 1u << (rec.x & 31);
+        if (!(atomicOr(&c.ovf_bits[rec.x >> 5], bit) & bit)) c.ovf_list[atomicAdd(c.n_ovf, 1)] = rec.x;
+    }
+}
+
+// lines are staged per CTA in shared memory and written with ONE global slot
+// reservation per CTA (a per-warp-per-pair atomicAdd on the shared line
+// counter was the kernel's top stall); a full stage falls back to direct slots
+constexpr int kLineStage = 1024;
+
+__device__ __forceinline__ void stage_put(const LinkCtx &c, int4 *st, int pos, int4 rec) {
+    if (pos < kLineStage) st[pos] = rec;
+    else line_store(c, atomicAdd(c.n_lines, 1), rec);
+}
+
+// per-face state of the thread-per-face enumeration
+struct SmallFace {
+    double nn[3];                  // FP64 normal (exact den)
+    float w[3], V1[3], V2[3], nf[3];
+    int b[3], lo[3], hi[3];        // base node, fallback node range per axis
+    float epsL, ff9;
+    int f;
+};
+
+// representative direction R (lattice.py order) as compile-time constants
+__host__ __device__ constexpr int rep_c(int R, int a) {
+    return R < 3 ? (a == R ? 1 : 0)
+         : R == 3 ? (a < 2 ? 1 : 0) : R == 4 ? (a == 1 ? 0 : 1) : R == 5 ? (a == 0 ? 1 : a == 1 ? 0 : -1)
+         : R == 6 ? (a == 0 ? 1 : a == 1 ? -1 : 0) : R == 7 ? (a == 0 ? 0 : 1) : R == 8 ? (a == 0 ? 0 : a == 1 ? 1 : -1)
+         : R == 9 ? 1 : R == 10 ? (a == 2 ? -1 : 1) : R == 11 ? (a == 1 ? -1 : 1) : (a == 0 ? 1 : -1);
+}
+
+// one (face, pair R) of the thread-per-face enumeration: the lattice points
+// of the projected bounding box, their class, piercing lines as records
+// (<= 2 kept in r0 / r1 for the warp-aggregated write; more go out directly)
+// and the undecided ones node by node to the band list
+__device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S, bool small, int R, int cx,
+                                           int cy, int cz, double cn, int4 &r0, int4 &r1, int &nr) {
+    const int p = cx != 0 ? 0 : (cy != 0 ? 1 : 2);
+    const int q1 = p == 0 ? 1 : 0, q2 = p == 2 ? 1 : 2;
+    const int cp = pick3(p, cx, cy, cz);
+    const int s1 = pick3(q1, cx, cy, cz) * cp, s2 = pick3(q2, cx, cy, cz) * cp;
+    // exact den / EPS_PARALLEL, as link_dir_setup
+    const double den = VF_DADD(VF_DADD(cmul(cx, S.nn[0]), cmul(cy, S.nn[1])), cmul(cz, S.nn[2]));
+    if (!small || fabs(den) < VF_DMUL(c.eps_par, cn)) return;
+    const float V1p = pick3(p, S.V1[0], S.V1[1], S.V1[2]), V2p = pick3(p, S.V2[0], S.V2[1], S.V2[2]);
+    const float P1a = pick3(q1, S.V1[0], S.V1[1], S.V1[2]) - (float)s1 * V1p;
+    const float P1b = pick3(q2, S.V1[0], S.V1[1], S.V1[2]) - (float)s2 * V1p;
+    const float P2a = pick3(q1, S.V2[0], S.V2[1], S.V2[2]) - (float)s1 * V2p;
+    const float P2b = pick3(q2, S.V2[0], S.V2[1], S.V2[2]) - (float)s2 * V2p;
+    const float ext = fmaxf(fmaxf(fabsf(P1a), fabsf(P1b)), fmaxf(fabsf(P2a), fabsf(P2b)));
+    const float tol = 1e-5f * (ext + 1.0f) + 6.0f * S.epsL;
+    const float wp = pick3(p, S.w[0], S.w[1], S.w[2]);
+    const float o1 = (float)s1 * wp - pick3(q1, S.w[0], S.w[1], S.w[2]);
+    const float o2 = (float)s2 * wp - pick3(q2, S.w[0], S.w[1], S.w[2]);
+    const int m1a = (int)ceilf(fminf(fminf(0.0f, P1a), P2a) - tol - o1 - 1e-4f);
+    const int m1b = (int)floorf(fmaxf(fmaxf(0.0f, P1a), P2a) + tol - o1 + 1e-4f);
+    const int m2a = (int)ceilf(fminf(fminf(0.0f, P1b), P2b) - tol - o2 - 1e-4f);
+    const int m2b = (int)floorf(fmaxf(fmaxf(0.0f, P1b), P2b) + tol - o2 + 1e-4f);
+    if (m1a > m1b || m2a > m2b) return;
+    const int n1 = pick3(q1, c.cells[0], c.cells[1], c.cells[2]);
+    const int n2 = pick3(q2, c.cells[0], c.cells[1], c.cells[2]);
+    const float cr = P1a * P2b - P1b * P2a;
+    const float ab = 4e-6f * (ext + 1.0f) * (ext + 1.0f);
+    const float t0 = tol * mlen(P1a, P1b) + ab;
+    const float t1 = tol * mlen(P2a - P1a, P2b - P1b) + ab;
+    const float t2 = tol * mlen(P2a, P2b) + ab;
+    const float sg = cr >= 0.0f ? 1.0f : -1.0f;
+    const float dn = (float)cx * S.nf[0] + (float)cy * S.nf[1] + (float)cz * S.nf[2];
+    const bool steep = fabsf(dn) >= 1e-3f;
+    const bool fast = steep && c.fast;
+    const float nq1 = pick3(q1, S.nf[0], S.nf[1], S.nf[2]), nq2 = pick3(q2, S.nf[0], S.nf[1], S.nf[2]);
+    const float wid0 = 1.0f + 1e-4f + 1e-5f + __fdividef(S.ff9, fabsf(dn)) * 1.0001f;
+    const int bp = pick3(p, S.b[0], S.b[1], S.b[2]);
+    const int gm1 = pick3(q1, S.b[0], S.b[1], S.b[2]) - s1 * bp;
+    const int gm2 = pick3(q2, S.b[0], S.b[1], S.b[2]) - s2 * bp;
+    const int lop = pick3(p, S.lo[0], S.lo[1], S.lo[2]), hip = pick3(p, S.hi[0], S.hi[1], S.hi[2]);
+    for (int M2 = m2a; M2 <= m2b; ++M2) {
+        const float Rb = (float)M2 + o2;
+        for (int M1 = m1a; M1 <= m1b; ++M1) {
+            const float Ra = (float)M1 + o1;
+            const float E0 = sg * (P1a * Rb - P1b * Ra);
+            const float E1 = sg * ((P2a - P1a) * (Rb - P1b) - (P2b - P1b) * (Ra - P1a));
+            const float E2 = sg * (P2b * Ra - P2a * Rb);
+            if (E0 < -t0 || E1 < -t1 || E2 < -t2) continue;  // misses the face
+            const bool inner = fast && E0 >= t0 && E1 >= t1 && E2 >= t2;
+            // node range along p (line_nodes in lattice units)
+            int ip_lo = lop, ip_hi = hip;
+            if (steep) {
+                const float xs = (float)cp * -__fdividef(nq1 * Ra + nq2 * Rb, dn);
+                const float wid = wid0 + 1.0001e-6f * __fdividef(fabsf(xs), fabsf(dn));
+                ip_lo = max(bp + (int)ceilf(xs + wp - wid), ip_lo);
+                ip_hi = min(bp + (int)floorf(xs + wp + wid), ip_hi);
+            }
+            const int mg1 = M1 + gm1, mg2 = M2 + gm2;
+            if (inner && ip_lo <= ip_hi && ip_hi - ip_lo < 8) {
+                const int4 rec = make_int4(S.f, R | (1 << 4) | ((ip_hi - ip_lo) << 5) | (ip_lo << 8), mg1, mg2);
+                if (nr == 0) r0 = rec;
+                else if (nr == 1) r1 = rec;
+                else line_store(c, atomicAdd(c.n_lines, 1), rec);  // rare: > 2 lines
+                nr = min(nr + 1, 2);
+                continue;
+            }
+            // margin band / ill-conditioned / long range: exact path later
+            for (int ip = ip_lo; ip <= ip_hi; ++ip) {
+                const int a = mg1 + s1 * ip, bb = mg2 + s2 * ip;
+                if (a < 0 || a >= n1 || bb < 0 || bb >= n2) continue;
+                const int i = p == 0 ? ip : a;
+                const int j = p == 1 ? ip : (p == 0 ? a : bb);
+                const int k = p == 2 ? ip : bb;
+                link_slow<2>(c, S.f, -1, i, j, k, R);
+            }
+        }
+    }
+}
+
+// warp-aggregated staging of the (<= 2) lines per lane of one pair
+__device__ __forceinline__ void small_flush(const LinkCtx &c, int4 *s_rec, int *s_n, int lane, int4 r0,
+                                            int4 r1, int nr) {
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned b0 = __ballot_sync(0xffffffffu, nr & 1), b1 = __ballot_sync(0xffffffffu, nr & 2);
+    const int tot = __popc(b0) + 2 * __popc(b1);
+    if (tot) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(s_n, tot);
+        base = __shfl_sync(0xffffffffu, base, 0) + __popc(b0 & lt) + 2 * __popc(b1 & lt);
+        if (nr > 0) stage_put(c, s_rec, base, r0);
+        if (nr > 1) stage_put(c, s_rec, base + 1, r1);
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void small_pair_c(const LinkCtx &c, const SmallFace &S, bool small, int4 *s_rec,
+                                             int *s_n, int lane) {
+    constexpr int cx = rep_c(R, 0), cy = rep_c(R, 1), cz = rep_c(R, 2);
+    constexpr double cn = R < 3 ? 1.0 : (R < 9 ? 1.4142135623730951 : 1.7320508075688772);
+    int4 r0 = make_int4(0, 0, 0, 0), r1 = r0;
+    int nr = 0;
+    small_pair(c, S, small, R, cx, cy, cz, cn, r0, r1, nr);
+    small_flush(c, s_rec, s_n, lane, r0, r1, nr);
+}
+
+#ifndef VF_SMALL_UNROLL
+#define VF_SMALL_UNROLL 0
+#endif
+
+__global__ void __launch_bounds__(256, VF_SMALL_MINB)
+    k_links_small(LinkCtx c, int widen, int64_t F, float small_ext, int32_t *__restrict__ big,
+                  int32_t *__restrict__ n_big) {
+    __shared__ int4 s_rec[kLineStage];
+    __shared__ int s_n, s_base;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool act = m < F;
+    SmallFace S;
+    S.f = (int)m;
+    double v[9];
+    float extL = 0.0f;
+    bool small = false;
+    if (act) {
+        load_face(c.faces, S.f, v, S.nn);
+        double ext = 0.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+            ext = fmax(ext, fmax(fmax(v[d], v[3 + d]), v[6 + d]) - fmin(fmin(v[d], v[3 + d]), v[6 + d]));
+        extL = (float)(ext * c.inv_dx);
+        small = extL <= small_ext;
+    }
+    // large faces: warp-aggregated append to the list of the warp-flattened kernel
+    const unsigned bm = __ballot_sync(0xffffffffu, act && !small);
+    if (bm) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(n_big, __popc(bm));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (act && !small) big[base + __popc(bm & ((1u << lane) - 1u))] = S.f;
+    }
+    if (__any_sync(0xffffffffu, small)) {
+        if (small) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const double t = v[d] * c.inv_dx - 0.5, bd = floor(t);
+                S.b[d] = (int)bd;
+                S.w[d] = (float)(t - bd);
+                S.V1[d] = (float)((v[3 + d] - v[d]) * c.inv_dx);
+                S.V2[d] = (float)((v[6 + d] - v[d]) * c.inv_dx);
+                S.nf[d] = (float)S.nn[d];
+                // nodes within one link of the face AABB (k_links' fallback range)
+                const double flo = fmin(fmin(v[d], v[3 + d]), v[6 + d]);
+                const double fhi = fmax(fmax(v[d], v[3 + d]), v[6 + d]);
+                S.lo[d] = max((int)floor((flo - c.dx - 2.0 * c.eps) * c.inv_dx - 0.5) - widen, 0);
+                S.hi[d] = min((int)floor((fhi + c.dx + 2.0 * c.eps) * c.inv_dx - 0.5) + 1 + widen, c.cells[d] - 1);
+            }
+        }
+        S.epsL = (float)(c.eps * c.inv_dx);
+        S.ff9 = 4e-6f * (extL + 2.0f);
+#if VF_SMALL_UNROLL
+        small_pair_c<0>(c, S, small, s_rec, &s_n, lane);
+        small_pair_c<1>(c, S, small, s_rec, &s_n, lane);
+        small_pair_c<2>(c, S, small, s_rec, &s_n, lane);
+        small_pair_c<3>(c, S, small, s_rec, &s_n, lane);
+        small_pair_c<4>(c, S, small, s_rec, &s_n, lane);
+        small_pair_c<5>(c, S, small, s_rec, &s_n, lane);
+        small_pair_c<6>(c, S, small, s_rec, &s_n, lane);
+        small_pair_c<7>(c, S, small, s_rec, &s_n, lane);
+        small_pair_c<8>(c, S, small, s_rec, &s_n, lane);
+        small_pair_c<9>(c, S, small, s_rec, &s_n, lane);
+        small_pair_c<10>(c, S, small, s_rec, &s_n, lane);
+        small_pair_c<11>(c, S, small, s_rec, &s_n, lane);
+        small_pair_c<12>(c, S, small, s_rec, &s_n, lane);
+#else
+#pragma unroll 1
+        for (int R = 0; R < 13; ++R) {
+            int4 r0 = make_int4(0, 0, 0, 0), r1 = r0;
+            int nr = 0;
+            small_pair(c, S, small, R, c_rep[R][0], c_rep[R][1], c_rep[R][2], c_cn[R], r0, r1, nr);
+            small_flush(c, s_rec, &s_n, lane, r0, r1, nr);
+        }
+#endif
+    }
+    __syncthreads();
+    const int n = min(s_n, kLineStage);
+    if (threadIdx.x == 0) s_base = n ? atomicAdd(c.n_lines, n) : 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) line_store(c, s_base + i, s_rec[i]);
+}
+
 // Resolve the recorded lines (fast class) once the grid and the block map
 // exist: thread per line, its (2, rarely 3) nodes -> block map -> the
 // oracle's FP64 num/den/d/q -> atomicMin.  Full warps, no setup.
@@ -752,19 +1005,24 @@ int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const doubl
 // ---- embed split: the line enumeration does not depend on the grid, so the
 // embed launches it on a side stream at the start of phase 1 (overlapping the
 // whole level pipeline) and resolves the recorded lines in phase 2.
+// lines workspace: counters (n_lines, n_ovf, n_big) | lines | overflow face
+// list | overflow bits | big-face list (the warp-flattened enumeration)
+static size_t list_bytes(int64_t F) { return (((size_t)(F + 1) * sizeof(int32_t) + 255) & ~(size_t)255); }
+
 size_t link_lines_bytes(int64_t F) {
     const int64_t cap = F * 2 > (1 << 22) ? F * 2 : (1 << 22);
-    return 256 + (size_t)cap * sizeof(int4) + (((size_t)(F + 1) * sizeof(int32_t) + 255) & ~(size_t)255) +
+    return 256 + (size_t)cap * sizeof(int4) + 2 * list_bytes(F) +
            ((((size_t)F + 32) / 32 * sizeof(uint32_t) + 255) & ~(size_t)255);
 }
 
-static void line_bufs(LinkCtx &c, int64_t F, void *lines_ws) {
+static int32_t *line_bufs(LinkCtx &c, int64_t F, void *lines_ws) {
     c.line_cap = F * 2 > (1 << 22) ? F * 2 : (1 << 22);
     c.n_lines = (int32_t *)lines_ws;
     c.n_ovf = c.n_lines + 1;
     c.lines = (int4 *)((char *)lines_ws + 256);
     c.ovf_list = (int32_t *)((char *)c.lines + (size_t)c.line_cap * sizeof(int4));
-    c.ovf_bits = (uint32_t *)((char *)c.ovf_list + (((size_t)(F + 1) * sizeof(int32_t) + 255) & ~(size_t)255));
+    c.ovf_bits = (uint32_t *)((char *)c.ovf_list + list_bytes(F));
+    return (int32_t *)((char *)c.ovf_bits + ((((size_t)F + 32) / 32 * sizeof(uint32_t) + 255) & ~(size_t)255));
 }
 
 int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *ws, void *lines_ws,
@@ -774,21 +1032,51 @@ int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *w
     LevelInfo li;
     int rc = make_link_ctx(cfg, cfg.l_max - 1, faces, nullptr, ws, c, widen, li);
     if (rc) return rc;
-    line_bufs(c, F, lines_ws);
+    int32_t *big = line_bufs(c, F, lines_ws);
     cudaMemsetAsync(c.n_band, 0, 2 * sizeof(int32_t), st);
-    cudaMemsetAsync(c.n_lines, 0, 2 * sizeof(int32_t), st);
+    cudaMemsetAsync(c.n_lines, 0, 3 * sizeof(int32_t), st);
     cudaMemsetAsync(c.ovf_bits, 0, ((size_t)F + 32) / 32 * sizeof(uint32_t), st);
     if (events) cudaEventRecord((cudaEvent_t)events[0], st);
-    // one short CTA per 128 faces (no grid-stride loop): CTAs retire quickly,
-    // so the higher-priority level pipeline can take SMs between them
-    const int64_t g2 = (F + 32 * kLinkWarps - 1) / (32 * kLinkWarps);
-    k_links<2><<<(unsigned)(g2 < 1 ? 1 : g2), kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, nullptr, nullptr);
+    // small faces thread per face; the rest through the warp-flattened
+    // kernel.  Short CTAs (no grid-stride loop in the small pass): they
+    // retire quickly, so the higher-priority level pipeline takes SMs
+    // between them.
+    int32_t *n_big = c.n_lines + 2;
+    const int64_t gs = (F + 255) / 256;
+    k_links_small<<<(unsigned)gs, 256, 0, st>>>(c, widen, F, g_small_ext, big, n_big);
+    if ((rc = check_launch("k_links_small"))) return rc;
+    int64_t g2 = (F + 32 * kLinkWarps - 1) / (32 * kLinkWarps);
+    if (g2 > 4 * (int64_t)max_ctas(VF_LINK_MINB)) g2 = 4 * (int64_t)max_ctas(VF_LINK_MINB);
+    k_links<2><<<(unsigned)(g2 < 1 ? 1 : g2), kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, big, n_big);
     rc = check_launch("k_links_enum");
     if (events) cudaEventRecord((cudaEvent_t)events[1], st);
     return rc;
 }
 
-const void *link_enum_kernel() { return (const void *)k_links<2>; }
+const void *link_enum_kernel(int small) { return small ? (const void *)k_links_small : (const void *)k_links<2>; }
+
+// counters of the last embed's cut-link pass (synchronous read):
+// {lines recorded, line capacity, overflow faces, band candidates, band capacity,
+//  faces of the warp-flattened (large-face) enumeration}
+int link_stats(const vf_config &cfg, int64_t F, void *ws, void *lines_ws, int64_t out[6]) {
+    LinkCtx c;
+    int widen;
+    LevelInfo li;
+    int rc = make_link_ctx(cfg, cfg.l_max - 1, nullptr, nullptr, ws, c, widen, li);
+    if (rc) return rc;
+    line_bufs(c, F, lines_ws);
+    int32_t a[3] = {0, 0, 0}, b[2] = {0, 0};
+    cudaError_t e = cudaMemcpy(a, c.n_lines, sizeof(a), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(b, c.n_band, sizeof(b), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return set_cuda_error(e, "link stats");
+    out[0] = a[0];
+    out[1] = c.line_cap;
+    out[2] = a[1];
+    out[3] = b[0];
+    out[4] = c.band_cap;
+    out[5] = a[2];
+    return VF_OK;
+}
 
 int link_resolve_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
                       int64_t F, float *lengths, void *ws, void *lines_ws, cudaStream_t st,
@@ -816,6 +1104,12 @@ int link_resolve_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, con
 }
 
 }  // namespace vf
+
+extern "C" float vf_set_link_small_ext(float e) {
+    const float old = vf::g_small_ext;
+    if (e == e) vf::g_small_ext = e;  // NaN only queries
+    return old;
+}
 
 extern "C" int64_t vf_set_link_band_cap(int64_t n) {
     const int64_t old = vf::g_band_cap;

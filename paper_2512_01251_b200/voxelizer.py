@@ -403,6 +403,20 @@ class EmbedEngine:
         t.total = ev[0].elapsed_time(ev[self.n_events - 1])
         return t
 
+    def link_stats(self) -> dict:
+        """Counters of the last embed's cut-link pass (synchronises): lines
+        recorded by the enumeration and the buffer capacity, faces whose lines
+        overflowed it (redone by the direct kernel), band candidates (exact
+        SAT path), the band capacity and the faces of the large-face kernel."""
+        import torch
+        torch.cuda.current_stream().synchronize()
+        self.lib.vf_side_sync()
+        out = (C.c_int64 * 6)()
+        _lib.check(self.lib.vf_embed_link_stats(C.byref(self.c), self.mesh.n_faces, self.grid.capacity,
+                                                _lib.ptr(self.ws), self.ws.numel(), out), "link_stats")
+        return dict(zip(("lines", "line_cap", "overflow_faces", "band", "band_cap", "large_faces"),
+                        map(int, out)))
+
     def link_kernel_ms(self) -> float:
         """Device time of the cut-link kernels of the last timed run: the line
         enumeration (side stream, overlapped with the level pipeline, events

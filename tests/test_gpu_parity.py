@@ -387,6 +387,23 @@ def test_links_band_overflow_fallback(O, torus):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("small_ext", [-1.0, 0.5, 1e9])
+def test_links_small_face_split(O, torus, small_ext):
+    """The thread-per-face enumeration of small faces and the warp-flattened
+    one of large faces are interchangeable: every face through either kernel
+    (or a mixed split) gives the oracle's LUT."""
+    from paper_2512_01251_b200 import _lib
+    lib = _lib.require_cuda()
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    mesh = _box_mesh([0.3 + 0.5 / 128] * 3, [0.7 + 0.5 / 128] * 3, 8, rot_z=np.pi / 4)
+    old = lib.vf_set_link_small_ext(small_ext)
+    try:
+        for m in (torus, mesh, make_torus(300, 120)):
+            _embed_compare(O, m, cfg)
+    finally:
+        lib.vf_set_link_small_ext(old)
+
+
 def test_serial_links_identical(torus):
     """The measurement schedule (enumeration serial on the main stream) gives
     the same LUT and cut-link map as the overlapped production schedule."""
