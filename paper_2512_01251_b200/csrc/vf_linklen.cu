@@ -629,59 +629,74 @@ struct SmallFace {
     int f;
 };
 
-// representative direction R (lattice.py order) as compile-time constants
-__host__ __device__ constexpr int rep_c(int R, int a) {
-    return R < 3 ? (a == R ? 1 : 0)
-         : R == 3 ? (a < 2 ? 1 : 0) : R == 4 ? (a == 1 ? 0 : 1) : R == 5 ? (a == 0 ? 1 : a == 1 ? 0 : -1)
-         : R == 6 ? (a == 0 ? 1 : a == 1 ? -1 : 0) : R == 7 ? (a == 0 ? 0 : 1) : R == 8 ? (a == 0 ? 0 : a == 1 ? 1 : -1)
-         : R == 9 ? 1 : R == 10 ? (a == 2 ? -1 : 1) : R == 11 ? (a == 1 ? -1 : 1) : (a == 0 ? 1 : -1);
+// the face permuted to (p, q1, q2) for one class of pairs
+struct SmallProj {
+    double np, nq1, nq2;
+    float V1p, V1a, V1b, V2p, V2a, V2b;  // a = q1, b = q2
+    float wp, wa, wb, nfp, nfa, nfb;
+    int bp, ba, bb, lop, hip, n1, n2, p;
+};
+
+__device__ __forceinline__ void small_project(const LinkCtx &c, const SmallFace &S, int cls, SmallProj &P) {
+    const int p = cls, q1 = cls == 0 ? 1 : 0, q2 = cls == 2 ? 1 : 2;
+    P.p = p;
+    P.np = pick3(p, S.nn[0], S.nn[1], S.nn[2]);
+    P.nq1 = pick3(q1, S.nn[0], S.nn[1], S.nn[2]);
+    P.nq2 = pick3(q2, S.nn[0], S.nn[1], S.nn[2]);
+    P.V1p = pick3(p, S.V1[0], S.V1[1], S.V1[2]);
+    P.V1a = pick3(q1, S.V1[0], S.V1[1], S.V1[2]);
+    P.V1b = pick3(q2, S.V1[0], S.V1[1], S.V1[2]);
+    P.V2p = pick3(p, S.V2[0], S.V2[1], S.V2[2]);
+    P.V2a = pick3(q1, S.V2[0], S.V2[1], S.V2[2]);
+    P.V2b = pick3(q2, S.V2[0], S.V2[1], S.V2[2]);
+    P.wp = pick3(p, S.w[0], S.w[1], S.w[2]);
+    P.wa = pick3(q1, S.w[0], S.w[1], S.w[2]);
+    P.wb = pick3(q2, S.w[0], S.w[1], S.w[2]);
+    P.nfp = pick3(p, S.nf[0], S.nf[1], S.nf[2]);
+    P.nfa = pick3(q1, S.nf[0], S.nf[1], S.nf[2]);
+    P.nfb = pick3(q2, S.nf[0], S.nf[1], S.nf[2]);
+    P.bp = pick3(p, S.b[0], S.b[1], S.b[2]);
+    P.ba = pick3(q1, S.b[0], S.b[1], S.b[2]);
+    P.bb = pick3(q2, S.b[0], S.b[1], S.b[2]);
+    P.lop = pick3(p, S.lo[0], S.lo[1], S.lo[2]);
+    P.hip = pick3(p, S.hi[0], S.hi[1], S.hi[2]);
+    P.n1 = pick3(q1, c.cells[0], c.cells[1], c.cells[2]);
+    P.n2 = pick3(q2, c.cells[0], c.cells[1], c.cells[2]);
 }
 
-// one (face, pair R) of the thread-per-face enumeration: the lattice points
-// of the projected bounding box, their class, piercing lines as records
-// (<= 2 kept in r0 / r1 for the warp-aggregated write; more go out directly)
-// and the undecided ones node by node to the band list
-__device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S, bool small, int R, int cx,
-                                           int cy, int cz, double cn, int4 &r0, int4 &r1, int &nr) {
-    const int p = cx != 0 ? 0 : (cy != 0 ? 1 : 2);
-    const int q1 = p == 0 ? 1 : 0, q2 = p == 2 ? 1 : 2;
-    const int cp = pick3(p, cx, cy, cz);
-    const int s1 = pick3(q1, cx, cy, cz) * cp, s2 = pick3(q2, cx, cy, cz) * cp;
-    // exact den / EPS_PARALLEL, as link_dir_setup
-    const double den = VF_DADD(VF_DADD(cmul(cx, S.nn[0]), cmul(cy, S.nn[1])), cmul(cz, S.nn[2]));
+// one (face, pair R = (class p, s1, s2)) of the thread-per-face enumeration:
+// the lattice points of the projected bounding box, their class, piercing
+// lines as records (<= 2 kept in r0 / r1 for the warp-aggregated write; more
+// go out directly) and the undecided ones node by node to the band list
+__device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S, const SmallProj &P,
+                                           bool small, int R, int s1, int s2, int4 &r0, int4 &r1, int &nr) {
+    // exact den / EPS_PARALLEL, as link_dir_setup: c = (1, s1, s2) over
+    // (p, q1, q2) -- the same FP64 sum in the same order (a zero term is exact)
+    const double den = VF_DADD(VF_DADD(P.np, cmul(s1, P.nq1)), cmul(s2, P.nq2));
+    const int nz = (s1 != 0) + (s2 != 0);
+    const double cn = nz == 0 ? 1.0 : (nz == 1 ? 1.4142135623730951 : 1.7320508075688772);
     if (!small || fabs(den) < VF_DMUL(c.eps_par, cn)) return;
-    const float V1p = pick3(p, S.V1[0], S.V1[1], S.V1[2]), V2p = pick3(p, S.V2[0], S.V2[1], S.V2[2]);
-    const float P1a = pick3(q1, S.V1[0], S.V1[1], S.V1[2]) - (float)s1 * V1p;
-    const float P1b = pick3(q2, S.V1[0], S.V1[1], S.V1[2]) - (float)s2 * V1p;
-    const float P2a = pick3(q1, S.V2[0], S.V2[1], S.V2[2]) - (float)s1 * V2p;
-    const float P2b = pick3(q2, S.V2[0], S.V2[1], S.V2[2]) - (float)s2 * V2p;
+    const float P1a = P.V1a - (float)s1 * P.V1p, P1b = P.V1b - (float)s2 * P.V1p;
+    const float P2a = P.V2a - (float)s1 * P.V2p, P2b = P.V2b - (float)s2 * P.V2p;
     const float ext = fmaxf(fmaxf(fabsf(P1a), fabsf(P1b)), fmaxf(fabsf(P2a), fabsf(P2b)));
     const float tol = 1e-5f * (ext + 1.0f) + 6.0f * S.epsL;
-    const float wp = pick3(p, S.w[0], S.w[1], S.w[2]);
-    const float o1 = (float)s1 * wp - pick3(q1, S.w[0], S.w[1], S.w[2]);
-    const float o2 = (float)s2 * wp - pick3(q2, S.w[0], S.w[1], S.w[2]);
+    const float o1 = (float)s1 * P.wp - P.wa, o2 = (float)s2 * P.wp - P.wb;
     const int m1a = (int)ceilf(fminf(fminf(0.0f, P1a), P2a) - tol - o1 - 1e-4f);
     const int m1b = (int)floorf(fmaxf(fmaxf(0.0f, P1a), P2a) + tol - o1 + 1e-4f);
     const int m2a = (int)ceilf(fminf(fminf(0.0f, P1b), P2b) - tol - o2 - 1e-4f);
     const int m2b = (int)floorf(fmaxf(fmaxf(0.0f, P1b), P2b) + tol - o2 + 1e-4f);
     if (m1a > m1b || m2a > m2b) return;
-    const int n1 = pick3(q1, c.cells[0], c.cells[1], c.cells[2]);
-    const int n2 = pick3(q2, c.cells[0], c.cells[1], c.cells[2]);
     const float cr = P1a * P2b - P1b * P2a;
     const float ab = 4e-6f * (ext + 1.0f) * (ext + 1.0f);
     const float t0 = tol * mlen(P1a, P1b) + ab;
     const float t1 = tol * mlen(P2a - P1a, P2b - P1b) + ab;
     const float t2 = tol * mlen(P2a, P2b) + ab;
     const float sg = cr >= 0.0f ? 1.0f : -1.0f;
-    const float dn = (float)cx * S.nf[0] + (float)cy * S.nf[1] + (float)cz * S.nf[2];
+    const float dn = P.nfp + (float)s1 * P.nfa + (float)s2 * P.nfb;
     const bool steep = fabsf(dn) >= 1e-3f;
     const bool fast = steep && c.fast;
-    const float nq1 = pick3(q1, S.nf[0], S.nf[1], S.nf[2]), nq2 = pick3(q2, S.nf[0], S.nf[1], S.nf[2]);
     const float wid0 = 1.0f + 1e-4f + 1e-5f + __fdividef(S.ff9, fabsf(dn)) * 1.0001f;
-    const int bp = pick3(p, S.b[0], S.b[1], S.b[2]);
-    const int gm1 = pick3(q1, S.b[0], S.b[1], S.b[2]) - s1 * bp;
-    const int gm2 = pick3(q2, S.b[0], S.b[1], S.b[2]) - s2 * bp;
-    const int lop = pick3(p, S.lo[0], S.lo[1], S.lo[2]), hip = pick3(p, S.hi[0], S.hi[1], S.hi[2]);
+    const int gm1 = P.ba - s1 * P.bp, gm2 = P.bb - s2 * P.bp;
     for (int M2 = m2a; M2 <= m2b; ++M2) {
         const float Rb = (float)M2 + o2;
         for (int M1 = m1a; M1 <= m1b; ++M1) {
@@ -691,13 +706,13 @@ __device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S,
             const float E2 = sg * (P2b * Ra - P2a * Rb);
             if (E0 < -t0 || E1 < -t1 || E2 < -t2) continue;  // misses the face
             const bool inner = fast && E0 >= t0 && E1 >= t1 && E2 >= t2;
-            // node range along p (line_nodes in lattice units)
-            int ip_lo = lop, ip_hi = hip;
+            // node range along p (line_nodes in lattice units; c_p = 1)
+            int ip_lo = P.lop, ip_hi = P.hip;
             if (steep) {
-                const float xs = (float)cp * -__fdividef(nq1 * Ra + nq2 * Rb, dn);
+                const float xs = -__fdividef(P.nfa * Ra + P.nfb * Rb, dn);
                 const float wid = wid0 + 1.0001e-6f * __fdividef(fabsf(xs), fabsf(dn));
-                ip_lo = max(bp + (int)ceilf(xs + wp - wid), ip_lo);
-                ip_hi = min(bp + (int)floorf(xs + wp + wid), ip_hi);
+                ip_lo = max(P.bp + (int)ceilf(xs + P.wp - wid), ip_lo);
+                ip_hi = min(P.bp + (int)floorf(xs + P.wp + wid), ip_hi);
             }
             const int mg1 = M1 + gm1, mg2 = M2 + gm2;
             if (inner && ip_lo <= ip_hi && ip_hi - ip_lo < 8) {
@@ -710,11 +725,11 @@ __device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S,
             }
             // margin band / ill-conditioned / long range: exact path later
             for (int ip = ip_lo; ip <= ip_hi; ++ip) {
-                const int a = mg1 + s1 * ip, bb = mg2 + s2 * ip;
-                if (a < 0 || a >= n1 || bb < 0 || bb >= n2) continue;
-                const int i = p == 0 ? ip : a;
-                const int j = p == 1 ? ip : (p == 0 ? a : bb);
-                const int k = p == 2 ? ip : bb;
+                const int a = mg1 + s1 * ip, bq = mg2 + s2 * ip;
+                if (a < 0 || a >= P.n1 || bq < 0 || bq >= P.n2) continue;
+                const int i = P.p == 0 ? ip : a;
+                const int j = P.p == 1 ? ip : (P.p == 0 ? a : bq);
+                const int k = P.p == 2 ? ip : bq;
                 link_slow<2>(c, S.f, -1, i, j, k, R);
             }
         }
@@ -735,21 +750,6 @@ __device__ __forceinline__ void small_flush(const LinkCtx &c, int4 *s_rec, int *
         if (nr > 1) stage_put(c, s_rec, base + 1, r1);
     }
 }
-
-template <int R>
-__device__ __forceinline__ void small_pair_c(const LinkCtx &c, const SmallFace &S, bool small, int4 *s_rec,
-                                             int *s_n, int lane) {
-    constexpr int cx = rep_c(R, 0), cy = rep_c(R, 1), cz = rep_c(R, 2);
-    constexpr double cn = R < 3 ? 1.0 : (R < 9 ? 1.4142135623730951 : 1.7320508075688772);
-    int4 r0 = make_int4(0, 0, 0, 0), r1 = r0;
-    int nr = 0;
-    small_pair(c, S, small, R, cx, cy, cz, cn, r0, r1, nr);
-    small_flush(c, s_rec, s_n, lane, r0, r1, nr);
-}
-
-#ifndef VF_SMALL_UNROLL
-#define VF_SMALL_UNROLL 0
-#endif
 
 __global__ void __launch_bounds__(256, VF_SMALL_MINB)
     k_links_small(LinkCtx c, int widen, int64_t F, float small_ext, int32_t *__restrict__ big,
@@ -802,29 +802,28 @@ __global__ void __launch_bounds__(256, VF_SMALL_MINB)
         }
         S.epsL = (float)(c.eps * c.inv_dx);
         S.ff9 = 4e-6f * (extL + 2.0f);
-#if VF_SMALL_UNROLL
-        small_pair_c<0>(c, S, small, s_rec, &s_n, lane);
-        small_pair_c<1>(c, S, small, s_rec, &s_n, lane);
-        small_pair_c<2>(c, S, small, s_rec, &s_n, lane);
-        small_pair_c<3>(c, S, small, s_rec, &s_n, lane);
-        small_pair_c<4>(c, S, small, s_rec, &s_n, lane);
-        small_pair_c<5>(c, S, small, s_rec, &s_n, lane);
-        small_pair_c<6>(c, S, small, s_rec, &s_n, lane);
-        small_pair_c<7>(c, S, small, s_rec, &s_n, lane);
-        small_pair_c<8>(c, S, small, s_rec, &s_n, lane);
-        small_pair_c<9>(c, S, small, s_rec, &s_n, lane);
-        small_pair_c<10>(c, S, small, s_rec, &s_n, lane);
-        small_pair_c<11>(c, S, small, s_rec, &s_n, lane);
-        small_pair_c<12>(c, S, small, s_rec, &s_n, lane);
-#else
+        // the 13 pairs in three classes of the axis p of their first nonzero
+        // component (c_p = +1): p = x: c = (1, s1, s2), all 9 sign pairs;
+        // p = y: (0, 1, s2); p = z: (0, 0, 1).  The face is permuted to
+        // (p, q1, q2) once per class instead of per pair.
 #pragma unroll 1
-        for (int R = 0; R < 13; ++R) {
-            int4 r0 = make_int4(0, 0, 0, 0), r1 = r0;
-            int nr = 0;
-            small_pair(c, S, small, R, c_rep[R][0], c_rep[R][1], c_rep[R][2], c_cn[R], r0, r1, nr);
-            small_flush(c, s_rec, &s_n, lane, r0, r1, nr);
+        for (int cls = 0; cls < 3; ++cls) {
+            SmallProj P;
+            small_project(c, S, cls, P);
+            const int ns = cls == 0 ? 9 : (cls == 1 ? 3 : 1);
+#pragma unroll 1
+            for (int t = 0; t < ns; ++t) {
+                const int s1 = cls == 0 ? t / 3 - 1 : 0;
+                const int s2 = cls == 0 ? t % 3 - 1 : (cls == 1 ? t - 1 : 0);
+                const int idx = cls == 0 ? t : (cls == 1 ? 9 + t : 12);
+                // R of (class, s1, s2) in lattice.py order, 4 bits each
+                const int R = (int)((0x271893a405b6cull >> (4 * idx)) & 15);
+                int4 r0 = make_int4(0, 0, 0, 0), r1 = r0;
+                int nr = 0;
+                small_pair(c, S, P, small, R, s1, s2, r0, r1, nr);
+                small_flush(c, s_rec, &s_n, lane, r0, r1, nr);
+            }
         }
-#endif
     }
     __syncthreads();
     const int n = min(s_n, kLineStage);
