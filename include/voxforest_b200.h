@@ -281,6 +281,24 @@ int vf_lbm_step(const vf_config *cfg, const vf_grid *grid, int level, int32_t s,
                 const int32_t *d_cmap, const float *d_lengths, const float *d_fin,
                 float *d_fout, const vf_flow *flow, double *d_force, int32_t *d_scratch,
                 void *stream);
+/* ---- interface exchange between levels L and L+1 (SPEC.md:417-424,
+ * SURVEY.md §8(f) next #3).  Block ranges: fine [sf, ef) at L+1, coarse
+ * [sc, ec) at L; states are the levels' post-collision f[27][...] arrays.
+ * vf_lbm_parents: d_parent[b] = parent block of every child (-1 elsewhere)
+ * over ids [0, n_blocks).
+ * vf_lbm_fill_ghosts: fine GHOST cells <- tensor-product interpolation
+ * (order 3 cubic / 1 linear / 0 copy, falling back when a stencil cell is
+ * outside the level or SOLID) of (1 - theta) fc_old + theta fc_new, then
+ * f = feq + alpha (f - feq) (alpha = 1: no rescale).
+ * vf_lbm_restrict: coarse cells of refined blocks (not SOLID / INTERFACE /
+ * GHOST, no GHOST child) <- mean of their non-SOLID children, rescaled by
+ * beta. */
+int vf_lbm_parents(const vf_grid *grid, int32_t n_blocks, int32_t *d_parent, void *stream);
+int vf_lbm_fill_ghosts(const vf_grid *grid, int32_t sf, int32_t ef, int32_t sc, int32_t ec,
+                       const int32_t *d_parent, const float *d_fc_old, const float *d_fc_new,
+                       double theta, double alpha, int order, float *d_ff, void *stream);
+int vf_lbm_restrict(const vf_grid *grid, int32_t sc, int32_t ec, int32_t sf, int32_t ef,
+                    const float *d_ff, double beta, float *d_fc, void *stream);
 /* copy the grid's latched device status to the host (synchronizes) */
 int vf_check_status(const vf_grid *grid, void *stream);
 /* test hook: capacity of the link-length band list (candidates the FP32

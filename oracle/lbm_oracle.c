@@ -155,3 +155,141 @@ int orc_lbm_step(const int32_t *coords, const int32_t *nbr, const uint8_t *masks
         for (int d = 0; d < 3; ++d) force[d] = F[d];
     return 0;
 }
+
+/* ---- interface exchange: the rules of csrc/vf_lbm.cu
+ * k_lbm_fill_ghosts / k_lbm_restrict, restated in FP64.  Fine global cell g
+ * (per axis) sits in coarse cell g >> 1 at offset s/4, s = +1 for odd g, -1
+ * for even g.  GHOST fine cells take the tensor-product interpolation of
+ * (1 - theta) fc_old + theta fc_new over the coarse cells G + s k:
+ * cubic Lagrange at x = 1/4 (k = -1..2, w = (-7, 105, 35, -5)/128) when all
+ * 64 stencil cells are level cells that are not SOLID, else linear (k = 0, 1,
+ * w = (3, 1)/4) when all 8 are, else the coarse cell G itself, else held;
+ * then f = feq(rho, u) + alpha (f - feq(rho, u)) unless alpha == 1.
+ * Restriction: coarse cells of refined blocks that are not SOLID, INTERFACE
+ * or GHOST and have no GHOST child <- mean of the non-SOLID children, then
+ * the beta rescale. */
+static void orc_neq_rescale(double *f, double a) {
+    if (a == 1.0) return;
+    double rho = 0, u[3] = {0, 0, 0};
+    for (int o = 0; o < 27; ++o) {
+        rho += f[o];
+        for (int d = 0; d < 3; ++d) u[d] += f[o] * LC[o][d];
+    }
+    if (!(rho > 0)) return;
+    for (int d = 0; d < 3; ++d) u[d] /= rho;
+    double feq[27];
+    orc_lbm_equilibrium(rho, u, feq);
+    for (int o = 0; o < 27; ++o) f[o] = feq[o] + a * (f[o] - feq[o]);
+}
+
+int orc_lbm_fill_ghosts(const int32_t *coords, const int32_t *nbr, const uint8_t *masks,
+                        const int32_t *child, int32_t sf, int32_t ef, int32_t sc, int32_t ec,
+                        const float *fc_old, const float *fc_new, double theta, double alpha,
+                        int order, float *ff) {
+    static const double W3[4] = {-7.0 / 128, 105.0 / 128, 35.0 / 128, -5.0 / 128};
+    const int64_t nf = (int64_t)(ef - sf) * 64, nc = (int64_t)(ec - sc) * 64;
+    int32_t *par = (int32_t *)malloc(sizeof(int32_t) * (size_t)(ef - sf + 1));
+    if (!par) return 1;
+    for (int32_t b = sf; b < ef; ++b) par[b - sf] = -1;
+    for (int32_t P = sc; P < ec; ++P)
+        if (child[P] >= 0)
+            for (int o = 0; o < 8; ++o)
+                if (child[P] + o >= sf && child[P] + o < ef) par[child[P] + o - sf] = P;
+    for (int32_t b = sf; b < ef; ++b) {
+        const int32_t P = par[b - sf];
+        if (P < 0) continue;
+        for (int t = 0; t < 64; ++t) {
+            if (masks[64 * (int64_t)b + t] != ORC_GHOST) continue;
+            const int Il[3] = {t & 3, (t >> 2) & 3, t >> 4};
+            int Lc[3], sd[3];
+            for (int d = 0; d < 3; ++d) {
+                const int g = 4 * coords[4 * (int64_t)b + d] + Il[d];
+                Lc[d] = (int)floor(g / 2.0) - 4 * coords[4 * (int64_t)P + d];
+                sd[d] = (g % 2 != 0) ? 1 : -1;
+            }
+            /* stencil cell list for the highest usable order */
+            int64_t idx[64];
+            int ord = order;
+            for (;;) {
+                const int kn = ord == 3 ? 4 : (ord == 1 ? 2 : 1), k0 = ord == 3 ? -1 : 0;
+                int ok = 1, nk = 0;
+                for (int kz = 0; kz < kn && ok; ++kz)
+                    for (int ky = 0; ky < kn && ok; ++ky)
+                        for (int kx = 0; kx < kn && ok; ++kx) {
+                            const int l[3] = {Lc[0] + sd[0] * (kx + k0), Lc[1] + sd[1] * (ky + k0),
+                                              Lc[2] + sd[2] * (kz + k0)};
+                            int o3[3];
+                            for (int d = 0; d < 3; ++d) o3[d] = l[d] < 0 ? -1 : (l[d] > 3 ? 1 : 0);
+                            const int32_t Z = (o3[0] || o3[1] || o3[2])
+                                                  ? nbr[27 * (int64_t)P + lslot(o3[0], o3[1], o3[2])]
+                                                  : P;
+                            const int tt = (l[0] & 3) + 4 * (l[1] & 3) + 16 * (l[2] & 3);
+                            if (Z < sc || Z >= ec || masks[64 * (int64_t)Z + tt] == ORC_SOLID) ok = 0;
+                            else idx[nk++] = (int64_t)(Z - sc) * 64 + tt;
+                        }
+                if (ok) break;
+                if (ord == 0) { ord = -1; break; }
+                ord = ord == 3 ? 1 : 0;
+            }
+            if (ord < 0) continue; /* held */
+            const int kn = ord == 3 ? 4 : (ord == 1 ? 2 : 1);
+            double f[27];
+            for (int q = 0; q < 27; ++q) {
+                double acc = 0;
+                int k = 0;
+                for (int kz = 0; kz < kn; ++kz)
+                    for (int ky = 0; ky < kn; ++ky)
+                        for (int kx = 0; kx < kn; ++kx, ++k) {
+                            const double w =
+                                ord == 3 ? W3[kx] * W3[ky] * W3[kz]
+                                : ord == 1 ? (kx ? 0.25 : 0.75) * (ky ? 0.25 : 0.75) * (kz ? 0.25 : 0.75)
+                                           : 1.0;
+                            const int64_t c = (int64_t)q * nc + idx[k];
+                            const double v = theta == 0.0 ? (double)fc_old[c]
+                                                          : (1.0 - theta) * fc_old[c] + theta * fc_new[c];
+                            acc += w * v;
+                        }
+                f[q] = acc;
+            }
+            orc_neq_rescale(f, alpha);
+            for (int q = 0; q < 27; ++q) ff[(int64_t)q * nf + (int64_t)(b - sf) * 64 + t] = (float)f[q];
+        }
+    }
+    free(par);
+    return 0;
+}
+
+int orc_lbm_restrict(const uint8_t *masks, const int32_t *child, int32_t sc, int32_t ec, int32_t sf,
+                     int32_t ef, const float *ff, double beta, float *fc) {
+    const int64_t nf = (int64_t)(ef - sf) * 64, nc = (int64_t)(ec - sc) * 64;
+    for (int32_t b = sc; b < ec; ++b) {
+        if (child[b] < 0) continue;
+        for (int t = 0; t < 64; ++t) {
+            const uint8_t m = masks[64 * (int64_t)b + t];
+            if (m == ORC_SOLID || m == ORC_INTERFACE || m == ORC_GHOST) continue;
+            const int I = t & 3, J = (t >> 2) & 3, K = t >> 4;
+            const int32_t Cb = child[b] + (I >> 1) + 2 * (J >> 1) + 4 * (K >> 1);
+            if (Cb < sf || Cb >= ef) continue;
+            int64_t fine[8];
+            int n = 0, ghost = 0;
+            for (int c = 0; c < 2; ++c)
+                for (int bb = 0; bb < 2; ++bb)
+                    for (int a = 0; a < 2; ++a) {
+                        const int tt = (2 * (I & 1) + a) + 4 * (2 * (J & 1) + bb) + 16 * (2 * (K & 1) + c);
+                        const uint8_t mf = masks[64 * (int64_t)Cb + tt];
+                        if (mf == ORC_GHOST) ghost = 1;
+                        if (mf != ORC_SOLID) fine[n++] = (int64_t)(Cb - sf) * 64 + tt;
+                    }
+            if (ghost || n == 0) continue;
+            double f[27];
+            for (int q = 0; q < 27; ++q) {
+                double acc = 0;
+                for (int k = 0; k < n; ++k) acc += ff[(int64_t)q * nf + fine[k]];
+                f[q] = acc / n;
+            }
+            orc_neq_rescale(f, beta);
+            for (int q = 0; q < 27; ++q) fc[(int64_t)q * nc + (int64_t)(b - sc) * 64 + t] = (float)f[q];
+        }
+    }
+    return 0;
+}

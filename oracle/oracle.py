@@ -79,6 +79,9 @@ def lib():
             "orc_parity_inside": (None, [P, i64, P, i64, C.c_double, P]),
             "orc_lbm_equilibrium": (None, [C.c_double, P, P]),
             "orc_lbm_step": (i32, [P, P, P, i32, i32, i32, P, P, P, P, C.c_double, P, i32, i32, P]),
+            "orc_lbm_fill_ghosts": (i32, [P, P, P, P, i32, i32, i32, i32, P, P, C.c_double, C.c_double,
+                                          i32, P]),
+            "orc_lbm_restrict": (i32, [P, P, i32, i32, i32, i32, P, C.c_double, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -361,3 +364,78 @@ def lbm_step(coords, nbr, masks, s, e, cells_x, cmap, lengths, fin, tau, u_in, i
                             int(bool(open_x)), _p(force))
     assert rc == 0
     return fout, force
+
+
+# interface exchange + step_hierarchy (lbm_oracle.c)
+
+
+def lbm_fill_ghosts(g, sf, ef, sc, ec, fc_old, fc_new, theta, alpha, order, ff):
+    """Fine GHOST cells of blocks [sf, ef) from the coarse level [sc, ec);
+    returns a new fine state (27, (ef-sf)*64)."""
+    out = np.ascontiguousarray(ff, dtype=np.float32).copy()
+    fo = np.ascontiguousarray(fc_old, dtype=np.float32)
+    fn = np.ascontiguousarray(fc_new if fc_new is not None else fc_old, dtype=np.float32)
+    rc = lib().orc_lbm_fill_ghosts(_p(np.ascontiguousarray(g["coords"], dtype=np.int32)),
+                                   _p(np.ascontiguousarray(g["nbr"], dtype=np.int32)),
+                                   _p(np.ascontiguousarray(g["masks"], dtype=np.uint8)),
+                                   _p(np.ascontiguousarray(g["child"], dtype=np.int32)), int(sf), int(ef),
+                                   int(sc), int(ec), _p(fo), _p(fn), float(theta), float(alpha), int(order),
+                                   _p(out))
+    assert rc == 0
+    return out
+
+
+def lbm_restrict(g, sc, ec, sf, ef, ff, beta, fc):
+    """Coarse cells of refined blocks in [sc, ec) from their children in
+    [sf, ef); returns a new coarse state."""
+    out = np.ascontiguousarray(fc, dtype=np.float32).copy()
+    rc = lib().orc_lbm_restrict(_p(np.ascontiguousarray(g["masks"], dtype=np.uint8)),
+                                _p(np.ascontiguousarray(g["child"], dtype=np.int32)), int(sc), int(ec), int(sf),
+                                int(ef), _p(np.ascontiguousarray(ff, dtype=np.float32)), float(beta), _p(out))
+    assert rc == 0
+    return out
+
+
+def level_taus(tau0, n_levels):
+    """Acoustic scaling: nu_L = 2^L nu_0, tau_L = 3 nu_L + 1/2."""
+    nu0 = (tau0 - 0.5) / 3.0
+    return [3.0 * nu0 * 2 ** L + 0.5 for L in range(n_levels)]
+
+
+def neq_factors(tau_c, tau_f):
+    """Post-collision non-equilibrium rescale coarse -> fine (alpha) and
+    fine -> coarse (beta = 1 / alpha): (tau_f - 1) / (2 (tau_c - 1))."""
+    if abs(tau_c - 1.0) < 1e-9 or abs(tau_f - 1.0) < 1e-9:
+        raise ValueError("tau_L = 1 loses the non-equilibrium part of post-collision populations")
+    a = (tau_f - 1.0) / (2.0 * (tau_c - 1.0))
+    return a, 1.0 / a
+
+
+def lbm_step_hierarchy(g, ranges, cells_x0, cmap, lengths, states, tau0, u_in, ibb=True, open_x=True,
+                       order=3, rescale=True):
+    """One coarse step of the level hierarchy: level L
+    advances, then level L+1 takes two substeps with its ghosts filled from L
+    at theta = 0 and 1/2, then L's covered cells are restricted from L+1.
+    ranges[L] = (s, e); states[L] = (27, (e-s)*64) float32.  Returns the new
+    states and the number of collide/stream steps per level."""
+    n = len(ranges)
+    taus = level_taus(tau0, n)
+    states = [np.array(x, dtype=np.float32, copy=True) for x in states]
+    counts = [0] * n
+
+    def advance(L):
+        s, e = ranges[L]
+        old = states[L]
+        states[L], _ = lbm_step(g["coords"], g["nbr"], g["masks"], s, e, cells_x0 << L, cmap, lengths, old,
+                                taus[L], u_in, ibb, open_x)
+        counts[L] += 1
+        if L + 1 < n:
+            sf, ef = ranges[L + 1]
+            a, b = neq_factors(taus[L], taus[L + 1]) if rescale else (1.0, 1.0)
+            for th in (0.0, 0.5):
+                states[L + 1] = lbm_fill_ghosts(g, sf, ef, s, e, old, states[L], th, a, order, states[L + 1])
+                advance(L + 1)
+            states[L] = lbm_restrict(g, s, e, sf, ef, states[L + 1], b, states[L])
+
+    advance(0)
+    return states, counts

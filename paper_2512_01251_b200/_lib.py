@@ -106,6 +106,10 @@ _SIGS = {
     "vf_stl_weld_workspace_size": (_SZ, [_I64]),
     "vf_stl_build": (_I32, [_P, _I64, _P, _SZ, _I64, C.c_double, _P, _SZ, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vf_lbm_step": (_I32, [_CP, _GP, _I32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "vf_lbm_parents": (_I32, [_GP, C.c_int32, _P, _P]),
+    "vf_lbm_fill_ghosts": (_I32, [_GP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, C.c_double,
+                                  C.c_double, _I32, _P, _P]),
+    "vf_lbm_restrict": (_I32, [_GP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_double, _P, _P]),
 }
 
 EXPORTED = tuple(_SIGS)

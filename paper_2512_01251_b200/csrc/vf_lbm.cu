@@ -2,7 +2,8 @@
 // grid level with SBB / interpolated bounce-back (Bouzidi linear) wall links
 // read from the cut-link LUT (SPEC.md:398-411 collide_stream_level,
 // SPEC.md:392-397 equilibrium, SPEC.md:436-440 accumulate_forces;
-// SURVEY.md §8(f) next #1).  Oracle: oracle/lbm_oracle.c (same rules, FP64).
+// SURVEY.md §8(f) next #1) and the interface exchange between levels
+// (§8(f) next #3; step_hierarchy in solver.py).  Oracle: oracle/lbm_oracle.c (same rules, FP64).
 //
 // State = post-collision populations, SoA f[q][cell] with cell = (block - s)
 // * 64 + t over the level's blocks [s, e): a warp reads 32 consecutive cells
@@ -210,6 +211,176 @@ __global__ void k_lbm_init(int32_t s, int32_t e, const uint8_t *__restrict__ mas
     }
 }
 
+// ---- multi-level interface exchange --
+// Cell-centred 2:1 layout: fine global cell g (per axis, level L+1) lies in
+// coarse cell G = g >> 1 at offset s/4 coarse cells, s = +1 for odd g, -1
+// for even g.  Fine <- coarse fills the GHOST cells of level L+1 (A14) by
+// tensor-product interpolation of the coarse post-collision populations,
+// blended in time, f^ = sum_k w_k ((1 - theta) f_old + theta f_new)(G + s k):
+//   order 3 (cubic Lagrange, nodes k = -1, 0, 1, 2 at x = 1/4):
+//            w = (-7, 105, 35, -5) / 128,
+//   order 1 (linear, k = 0, 1): w = (3, 1) / 4,
+// falling back 3 -> 1 -> 0 (the coarse cell G itself) when a stencil cell is
+// outside the level (negative neighbour code) or SOLID; a ghost with no
+// usable G is held.  The non-equilibrium part is then rescaled,
+// f = feq(rho^, u^) + alpha (f^ - feq(rho^, u^)) (alpha = 1: f = f^).
+// Coarse <- fine (k_lbm_restrict) averages the 8 children of every coarse
+// cell of a refined block that is neither SOLID, INTERFACE nor GHOST and
+// whose children hold no GHOST cell, over the non-SOLID children, with the
+// inverse rescale beta.  Weights are dyadic (exact in FP32); sums in FP32.
+constexpr int kGhostThreads = 128;
+
+__constant__ float c_w3[4] = {-7.0f / 128, 105.0f / 128, 35.0f / 128, -5.0f / 128};
+
+// rescale of the non-equilibrium part (in place on f[27]); a == 1: identity
+__device__ __forceinline__ void neq_rescale(float *f, float a) {
+    if (a == 1.0f) return;
+    float rho = 0.f, u0 = 0.f, u1 = 0.f, u2 = 0.f;
+#pragma unroll
+    for (int o = 0; o < 27; ++o) {
+        rho += f[o];
+        u0 += f[o] * c27(o, 0);
+        u1 += f[o] * c27(o, 1);
+        u2 += f[o] * c27(o, 2);
+    }
+    if (!(rho > 0.0f)) return;
+    const float ir = 1.0f / rho;
+    u0 *= ir; u1 *= ir; u2 *= ir;
+    const float uu = 1.5f * (u0 * u0 + u1 * u1 + u2 * u2);
+#pragma unroll
+    for (int o = 0; o < 27; ++o) {
+        const float cu = c27(o, 0) * u0 + c27(o, 1) * u1 + c27(o, 2) * u2;
+        const float feq = c_lw[o] * rho * (1.0f + 3.0f * cu + 4.5f * cu * cu - uu);
+        f[o] = feq + a * (f[o] - feq);
+    }
+}
+
+__global__ void k_lbm_parents(int32_t n_blocks, const int32_t *__restrict__ child, int32_t *__restrict__ parent) {
+    for (int32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < n_blocks; b += gridDim.x * blockDim.x) {
+        const int32_t c = child[b];
+        if (c >= 0)
+#pragma unroll
+            for (int o = 0; o < 8; ++o) parent[c + o] = b;
+    }
+}
+
+__global__ void __launch_bounds__(kGhostThreads)
+    k_lbm_fill_ghosts(int32_t sf, int32_t ef, int32_t sc, int32_t ec, const int32_t *__restrict__ coords,
+                      const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
+                      const int32_t *__restrict__ parent, const float *__restrict__ fold,
+                      const float *__restrict__ fnew, float theta, float alpha, int order,
+                      float *__restrict__ ff) {
+    __shared__ int32_t s_idx[64][kGhostThreads];  // coarse stencil cells (level-local index)
+    const int64_t nf = (int64_t)(ef - sf) * 64, nc = (int64_t)(ec - sc) * 64;
+    const int tid = threadIdx.x;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + tid; x < nf; x += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t b = sf + (int32_t)(x >> 6);
+        const int t = (int)(x & 63);
+        if (masks[64 * (int64_t)b + t] != VF_GHOST) continue;
+        const int32_t P = parent[b];
+        if (P < sc || P >= ec) continue;
+        int Lc[3], sd[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const int I = d == 0 ? (t & 3) : (d == 1 ? ((t >> 2) & 3) : (t >> 4));
+            const int g = 4 * coords[4 * (int64_t)b + d] + I;
+            Lc[d] = (g >> 1) - 4 * coords[4 * (int64_t)P + d];
+            sd[d] = (g & 1) ? 1 : -1;
+        }
+        // coarse cell at local (lx, ly, lz) of P, lx in [-2, 5]: level-local
+        // index or -1 (outside the level / SOLID)
+        auto cell = [&](int lx, int ly, int lz) -> int32_t {
+            const int ox = lx < 0 ? -1 : (lx > 3 ? 1 : 0), oy = ly < 0 ? -1 : (ly > 3 ? 1 : 0),
+                      oz = lz < 0 ? -1 : (lz > 3 ? 1 : 0);
+            const int32_t Y = (ox | oy | oz) ? __ldg(nbr + 27 * (int64_t)P + slot_of(ox, oy, oz)) : P;
+            if (Y < sc || Y >= ec) return -1;
+            const int tt = (lx & 3) + 4 * (ly & 3) + 16 * (lz & 3);
+            if (masks[64 * (int64_t)Y + tt] == VF_SOLID) return -1;
+            return (Y - sc) * 64 + tt;
+        };
+        int ord = order >= 3 ? 3 : (order >= 1 ? 1 : 0);
+        if (ord == 3) {
+            for (int k = 0; k < 64 && ord == 3; ++k) {
+                const int kx = (k & 3) - 1, ky = ((k >> 2) & 3) - 1, kz = (k >> 4) - 1;
+                const int32_t c = cell(Lc[0] + sd[0] * kx, Lc[1] + sd[1] * ky, Lc[2] + sd[2] * kz);
+                s_idx[k][tid] = c;
+                if (c < 0) ord = 1;
+            }
+        }
+        if (ord == 1) {
+            for (int k = 0; k < 8 && ord == 1; ++k) {
+                const int32_t c = cell(Lc[0] + sd[0] * (k & 1), Lc[1] + sd[1] * ((k >> 1) & 1),
+                                       Lc[2] + sd[2] * (k >> 2));
+                s_idx[k][tid] = c;
+                if (c < 0) ord = 0;
+            }
+        }
+        if (ord == 0) {
+            const int32_t c = cell(Lc[0], Lc[1], Lc[2]);
+            if (c < 0) continue;  // held
+            s_idx[0][tid] = c;
+        }
+        const int nk = ord == 3 ? 64 : (ord == 1 ? 8 : 1);
+        const float th0 = 1.0f - theta;
+        float f[27];
+#pragma unroll 1
+        for (int q = 0; q < 27; ++q) {
+            float acc = 0.0f;
+            for (int k = 0; k < nk; ++k) {
+                float w;
+                if (ord == 3) w = c_w3[k & 3] * c_w3[(k >> 2) & 3] * c_w3[k >> 4];
+                else if (ord == 1) w = ((k & 1) ? 0.25f : 0.75f) * ((k & 2) ? 0.25f : 0.75f) * ((k & 4) ? 0.25f : 0.75f);
+                else w = 1.0f;
+                const int64_t c = (int64_t)q * nc + s_idx[k][tid];
+                const float v = theta == 0.0f ? fold[c] : th0 * fold[c] + theta * fnew[c];
+                acc += w * v;
+            }
+            f[q] = acc;
+        }
+        neq_rescale(f, alpha);
+#pragma unroll
+        for (int q = 0; q < 27; ++q) ff[(int64_t)q * nf + x] = f[q];
+    }
+}
+
+__global__ void k_lbm_restrict(int32_t sc, int32_t ec, int32_t sf, int32_t ef, const int32_t *__restrict__ child,
+                               const uint8_t *__restrict__ masks, const float *__restrict__ ff, float beta,
+                               float *__restrict__ fc) {
+    const int64_t nf = (int64_t)(ef - sf) * 64, nc = (int64_t)(ec - sc) * 64;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nc; x += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t b = sc + (int32_t)(x >> 6);
+        const int t = (int)(x & 63);
+        const int32_t c0 = child[b];
+        if (c0 < 0) continue;
+        const uint8_t m = masks[64 * (int64_t)b + t];
+        if (m == VF_SOLID || m == VF_INTERFACE || m == VF_GHOST) continue;
+        const int I = t & 3, J = (t >> 2) & 3, K = t >> 4;
+        const int32_t C = c0 + (I >> 1) + 2 * (J >> 1) + 4 * (K >> 1);
+        if (C < sf || C >= ef) continue;
+        int fine[8], n = 0;
+        bool ghost = false;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int tt = (2 * (I & 1) + (k & 1)) + 4 * (2 * (J & 1) + ((k >> 1) & 1)) + 16 * (2 * (K & 1) + (k >> 2));
+            const uint8_t mf = masks[64 * (int64_t)C + tt];
+            ghost |= mf == VF_GHOST;
+            if (mf != VF_SOLID) fine[n++] = (C - sf) * 64 + tt;
+        }
+        if (ghost || n == 0) continue;
+        const float inv = 1.0f / (float)n;
+        float f[27];
+#pragma unroll
+        for (int q = 0; q < 27; ++q) {
+            float acc = 0.0f;
+            for (int k = 0; k < n; ++k) acc += ff[(int64_t)q * nf + fine[k]];
+            f[q] = acc * inv;
+        }
+        neq_rescale(f, beta);
+#pragma unroll
+        for (int q = 0; q < 27; ++q) fc[(int64_t)q * nc + x] = f[q];
+    }
+}
+
 }  // namespace vf
 
 using namespace vf;
@@ -226,6 +397,44 @@ int vf_lbm_init(const vf_grid *g, int32_t s, int32_t e, double rho, const double
     k_lbm_init<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(s, e, g->d_masks, (float)rho, (float)u[0],
                                                              (float)u[1], (float)u[2], f);
     return check_launch("k_lbm_init");
+}
+
+int vf_lbm_parents(const vf_grid *g, int32_t n_blocks, int32_t *d_parent, void *stream) {
+    if (!g || !d_parent || n_blocks < 0 || n_blocks > g->capacity)
+        return set_error(VF_EARG, "vf_lbm_parents: bad argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemsetAsync(d_parent, 0xff, sizeof(int32_t) * (size_t)n_blocks, st);
+    if (n_blocks == 0) return VF_OK;
+    k_lbm_parents<<<max_ctas(4), 256, 0, st>>>(n_blocks, g->d_child, d_parent);
+    return check_launch("k_lbm_parents");
+}
+
+int vf_lbm_fill_ghosts(const vf_grid *g, int32_t sf, int32_t ef, int32_t sc, int32_t ec, const int32_t *d_parent,
+                       const float *fc_old, const float *fc_new, double theta, double alpha, int order, float *ff,
+                       void *stream) {
+    if (!g || !d_parent || !fc_old || !ff || sf < 0 || ef < sf || ef > g->capacity || sc < 0 || ec < sc ||
+        ec > g->capacity || !(theta >= 0.0 && theta <= 1.0) || (theta > 0.0 && !fc_new) ||
+        !(order == 0 || order == 1 || order == 3))
+        return set_error(VF_EARG, "vf_lbm_fill_ghosts: bad argument");
+    if (ef == sf || ec == sc) return VF_OK;
+    int64_t grid = ((int64_t)(ef - sf) * 64 + kGhostThreads - 1) / kGhostThreads;
+    if (grid > max_ctas(8)) grid = max_ctas(8);
+    k_lbm_fill_ghosts<<<(int)grid, kGhostThreads, 0, (cudaStream_t)stream>>>(
+        sf, ef, sc, ec, g->d_coords, g->d_nbr, g->d_masks, d_parent, fc_old, fc_new ? fc_new : fc_old,
+        (float)theta, (float)alpha, order, ff);
+    return check_launch("k_lbm_fill_ghosts");
+}
+
+int vf_lbm_restrict(const vf_grid *g, int32_t sc, int32_t ec, int32_t sf, int32_t ef, const float *ff, double beta,
+                    float *fc, void *stream) {
+    if (!g || !ff || !fc || sf < 0 || ef < sf || ef > g->capacity || sc < 0 || ec < sc || ec > g->capacity)
+        return set_error(VF_EARG, "vf_lbm_restrict: bad argument");
+    if (ef == sf || ec == sc) return VF_OK;
+    int64_t grid = ((int64_t)(ec - sc) * 64 + 255) / 256;
+    if (grid > max_ctas(8)) grid = max_ctas(8);
+    k_lbm_restrict<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(sc, ec, sf, ef, g->d_child, g->d_masks, ff,
+                                                                 (float)beta, fc);
+    return check_launch("k_lbm_restrict");
 }
 
 int vf_lbm_step(const vf_config *cfg, const vf_grid *g, int level, int32_t s, int32_t e,

@@ -9,9 +9,23 @@ SPEC ops:
                                                     SPEC.md:436-440
 The kernel is csrc/vf_lbm.cu (one thread per cell, pull streaming, Bouzidi
 linear IBB with q_w = LUT[contraction_map[b]][q][t]); the CPU checker is
-oracle/lbm_oracle.c.  Lattice units throughout.  Interface exchange between
-levels is not built: GHOST cells are held, as the op's
-precondition ("ghost cells of L up to date") allows.
+oracle/lbm_oracle.c.  Lattice units throughout.
+
+Multi-level:
+  interface_exchange(state, grid, order)            SPEC.md:417-425
+  step_hierarchy(state, grid, links, flow)          SPEC.md:426-434
+LbmHierarchy holds one LbmLevel per level with acoustic scaling (SPEC.md:473:
+nu_L = 2^L nu_0, tau_L = 3 nu_L + 1/2).  One coarse step advances level L
+once and, recursively, level L+1 twice: before each fine substep the fine
+GHOST cells (A14) are filled from level L by tensor-product interpolation
+(cubic or linear, cell-centred 2:1 layout) of L's post-collision populations
+at theta = 0 and 1/2 between L's old and new states (vf_lbm_fill_ghosts);
+after the two substeps the covered cells of L's refined blocks (not
+INTERFACE: those stay coupled to L's own dynamics) are restricted from
+their 8 children (vf_lbm_restrict).  Non-equilibrium parts are rescaled by
+(tau_f - 1) / (2 (tau_c - 1)) coarse -> fine and its inverse fine -> coarse
+(post-collision Dupuis-Chopard factor).  The CPU checker of the
+same schedule is oracle.lbm_step_hierarchy.
 """
 from __future__ import annotations
 
@@ -140,3 +154,118 @@ def collide_stream_level(state: LbmLevel, grid: ForestGrid, level: int, links: L
         raise ValueError("state belongs to another grid level")
     state.step(1)
     return state
+
+
+def level_taus(tau0: float, n_levels: int):
+    """Acoustic scaling: nu_L = 2^L nu_0, tau_L = 3 nu_L + 1/2."""
+    nu0 = (tau0 - 0.5) / 3.0
+    return [3.0 * nu0 * 2 ** L + 0.5 for L in range(n_levels)]
+
+
+def neq_factors(tau_c: float, tau_f: float):
+    """(alpha, beta): post-collision non-equilibrium rescale coarse -> fine
+    (tau_f - 1) / (2 (tau_c - 1)) and fine -> coarse (its inverse)."""
+    if abs(tau_c - 1.0) < 1e-9 or abs(tau_f - 1.0) < 1e-9:
+        raise ValueError("tau_L = 1 loses the non-equilibrium part of post-collision populations")
+    a = (tau_f - 1.0) / (2.0 * (tau_c - 1.0))
+    return a, 1.0 / a
+
+
+class LbmHierarchy:
+    """State of every level of an embedded grid (SPEC.md:389 LbmState): one
+    LbmLevel per level, tau_L by acoustic scaling from ``flow.tau`` at level
+    0; ``order`` 3 (cubic) or 1 (linear) ghost interpolation."""
+
+    def __init__(self, grid: ForestGrid, table: Optional[LinkTable], flow: FlowConfig, order: int = 3,
+                 rescale: bool = True):
+        import torch
+        if order not in (0, 1, 3):
+            raise ValueError("interp order must be 1 (linear) or 3 (cubic)")
+        self.lib = _lib.require_cuda()
+        self.grid, self.table, self.flow, self.order = grid, table, flow, int(order)
+        self.taus = level_taus(flow.tau, grid.n_levels)
+        for t in self.taus:
+            if not t > 0.5:
+                raise ValueError("tau_L <= 0.5: unstable configuration (SPEC.md:410)")
+        self.factors = [neq_factors(self.taus[L], self.taus[L + 1]) if rescale else (1.0, 1.0)
+                        for L in range(grid.n_levels - 1)]
+        self.levels = [LbmLevel(grid, L, table, flow, tau=self.taus[L]) for L in range(grid.n_levels)]
+        n = grid.n_used
+        self.parent = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        _lib.check(self.lib.vf_lbm_parents(C.byref(grid._struct()), n, _lib.ptr(self.parent), _lib.stream_ptr()),
+                   "lbm parents")
+        self.substeps = [0] * grid.n_levels
+
+    def init_equilibrium(self, rho: float = 1.0, u=(0.0, 0.0, 0.0)):
+        for lv in self.levels:
+            lv.init_equilibrium(rho, u)
+        return self
+
+    def fill_ghosts(self, L: int, old, new, theta: float):
+        """Ghost cells of level L+1 from level L (old/new post-collision
+        states of L, time weight theta)."""
+        fine, coarse = self.levels[L + 1], self.levels[L]
+        _lib.check(self.lib.vf_lbm_fill_ghosts(
+            C.byref(self.grid._struct()), fine.s, fine.e, coarse.s, coarse.e, _lib.ptr(self.parent), _lib.ptr(old),
+            _lib.ptr(new), float(theta), float(self.factors[L][0]), self.order, _lib.ptr(fine.state),
+            _lib.stream_ptr()), "interface_exchange (fill ghosts)")
+
+    def restrict(self, L: int):
+        """Covered cells of level L from level L+1."""
+        fine, coarse = self.levels[L + 1], self.levels[L]
+        _lib.check(self.lib.vf_lbm_restrict(
+            C.byref(self.grid._struct()), coarse.s, coarse.e, fine.s, fine.e, _lib.ptr(fine.state),
+            float(self.factors[L][1]), _lib.ptr(coarse.state), _lib.stream_ptr()), "interface_exchange (restrict)")
+
+    def _advance(self, L: int, force: bool):
+        lv = self.levels[L]
+        old = lv.state
+        lv.step(1, force=force)
+        self.substeps[L] += 1
+        if L + 1 < len(self.levels):
+            for theta in (0.0, 0.5):
+                self.fill_ghosts(L, old, lv.state, theta)
+                self._advance(L + 1, force)
+            self.restrict(L)
+
+    def step(self, n: int = 1, force: bool = False):
+        """n coarse steps (level L takes 2^L substeps each)."""
+        for _ in range(n):
+            self._advance(0, force)
+        return self
+
+    def mass(self) -> float:
+        """sum over leaf cells (not SOLID / GHOST, block not refined) of
+        rho (dx_L / dx_0)^3 -- the conservation audit of SPEC.md:434."""
+        import torch
+        g = self.grid
+        total = 0.0
+        for L, lv in enumerate(self.levels):
+            m = g.masks[lv.s:lv.e].reshape(-1)
+            leaf = (g.child[lv.s:lv.e] < 0).repeat_interleave(64)
+            keep = leaf & (m != 1) & (m != 3)
+            rho = lv.state.sum(0, dtype=torch.float64)
+            total += float(rho[keep].sum()) / 8.0 ** L
+        return total
+
+
+def interface_exchange(state: LbmHierarchy, grid: ForestGrid, order: int = 3, level: int = 0,
+                       theta: float = 0.0) -> LbmHierarchy:
+    """SPEC.md:417-425 between levels ``level`` and ``level + 1``: fine
+    ghosts <- coarse (current state, time weight theta against itself), then
+    coarse covered cells <- fine."""
+    if state.grid is not grid:
+        raise ValueError("state belongs to another grid")
+    state.order = int(order)
+    cur = state.levels[level].state
+    state.fill_ghosts(level, cur, cur, theta)
+    state.restrict(level)
+    return state
+
+
+def step_hierarchy(state: LbmHierarchy, grid: ForestGrid, links: Optional[LinkTable] = None,
+                   flow: Optional[FlowConfig] = None) -> LbmHierarchy:
+    """one coarse step of the whole hierarchy."""
+    if state.grid is not grid:
+        raise ValueError("state belongs to another grid")
+    return state.step(1)
