@@ -212,9 +212,9 @@ def run_reference(args, w, ws, rank):
 def lbm_block(eng, w, args, flush):
     """C3: the LUT consumer on the embedded grid.  Per level one BGK
     collide/stream step (csrc/vf_lbm.cu; IBB walls from the LUT on the finest
-    level, SBB below), timed with CUDA events; a coarse step of the nested
-    hierarchy is sum_L 2^L t_L (the interface exchange between levels is not
-    built and not counted).  Embed overhead = embed time / coarse step."""
+    level, SBB below), timed with CUDA events, and one coarse step of the
+    nested hierarchy (solver.step_hierarchy, interface exchange included).
+    Embed overhead = embed time / coarse step."""
     import torch
     from paper_2512_01251_b200.solver import FlowConfig, LbmLevel
     grid, table = eng.run()
@@ -247,10 +247,31 @@ def lbm_block(eng, w, args, flush):
         coarse_ms += 2 ** L * ms
         if L == Lf:
             drag = lv.force.cpu().numpy() / k
-    return {"levels": levels, "coarse_step_ms": coarse_ms,
-            "wall_force_lattice": [float(x) for x in drag],
-            "note": "one BGK collide/stream per level (f32 SoA, 216 B/cell algorithmic), IBB from the "
-                    "LUT on the finest level; coarse step = sum_L 2^L t_L without interface exchange",
+    # one coarse step of the nested hierarchy (step_hierarchy: level L takes
+    # 2^L substeps, cubic ghost fill before each fine substep, restriction
+    # after), replayed from a CUDA graph of two coarse steps
+    from paper_2512_01251_b200.solver import LbmHierarchy
+    flow0 = FlowConfig(Re=20.0, u_in=0.05, D_s=D_f / 2 ** Lf, bc_scheme="IBB")
+    h = LbmHierarchy(grid, table, flow0, order=3).init_equilibrium(1.0, (0.05, 0, 0))
+    gr = h.graph()
+    for _ in range(2):
+        gr.replay()
+    torch.cuda.synchronize()
+    k = max(args.steps // 2, 5)
+    flush.fill_(2.0)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(k):
+        gr.replay()
+    b.record()
+    torch.cuda.synchronize()
+    hier_ms = a.elapsed_time(b) / (2 * k)
+    return {"levels": levels, "coarse_step_ms": hier_ms, "coarse_step_ms_levels_only": coarse_ms,
+            "taus": h.taus, "wall_force_lattice": [float(x) for x in drag],
+            "note": "per level: one BGK collide/stream (f32 SoA, 216 B/cell algorithmic), IBB from the LUT; "
+                    "coarse_step_ms = one step_hierarchy coarse step (2^L substeps per level, cubic ghost "
+                    "fill + restriction between levels, CUDA graph); coarse_step_ms_levels_only = "
+                    "sum_L 2^L t_L without the exchange",
             "peak_kind": peak_kind}
 
 

@@ -228,8 +228,6 @@ __global__ void k_lbm_init(int32_t s, int32_t e, const uint8_t *__restrict__ mas
 // cell of a refined block that is neither SOLID, INTERFACE nor GHOST and
 // whose children hold no GHOST cell, over the non-SOLID children, with the
 // inverse rescale beta.  Weights are dyadic (exact in FP32); sums in FP32.
-constexpr int kGhostThreads = 128;
-
 __constant__ float c_w3[4] = {-7.0f / 128, 105.0f / 128, 35.0f / 128, -5.0f / 128};
 
 // rescale of the non-equilibrium part (in place on f[27]); a == 1: identity
@@ -264,82 +262,165 @@ __global__ void k_lbm_parents(int32_t n_blocks, const int32_t *__restrict__ chil
     }
 }
 
-__global__ void __launch_bounds__(kGhostThreads)
+// Warp per fine block: the block's 64 cells lie in 2x2x2 coarse cells, so
+// every stencil (cubic: +-2 coarse cells) lies in the 6x6x6 coarse cells
+// around them.  Their level-local ids (or -1: outside the level / SOLID) are
+// staged once; then per population the 216 time-blended coarse values are
+// staged and each lane interpolates its (<= 2) ghost cells separably
+// (x, then y, then z).  The interpolated populations go to ff and are then
+// rescaled in place by their owning lane.
+constexpr int kFillWarps = 8;
+
+__device__ __forceinline__ float axis_w(int ord, int k) {
+    return ord == 3 ? c_w3[k] : (ord == 1 ? (k ? 0.25f : 0.75f) : 1.0f);
+}
+
+__global__ void __launch_bounds__(kFillWarps * 32)
     k_lbm_fill_ghosts(int32_t sf, int32_t ef, int32_t sc, int32_t ec, const int32_t *__restrict__ coords,
                       const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
                       const int32_t *__restrict__ parent, const float *__restrict__ fold,
                       const float *__restrict__ fnew, float theta, float alpha, int order,
                       float *__restrict__ ff) {
-    __shared__ int32_t s_idx[64][kGhostThreads];  // coarse stencil cells (level-local index)
+    __shared__ int32_t s_c[kFillWarps][216];
+    __shared__ float s_v[kFillWarps][216];
+    __shared__ float s_t1[kFillWarps][144], s_t2[kFillWarps][96];
     const int64_t nf = (int64_t)(ef - sf) * 64, nc = (int64_t)(ec - sc) * 64;
-    const int tid = threadIdx.x;
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + tid; x < nf; x += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t b = sf + (int32_t)(x >> 6);
-        const int t = (int)(x & 63);
-        if (masks[64 * (int64_t)b + t] != VF_GHOST) continue;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const float th0 = 1.0f - theta;
+    for (int32_t b = sf + blockIdx.x * kFillWarps + w; b < ef; b += gridDim.x * kFillWarps) {
+        const bool g0 = masks[64 * (int64_t)b + lane] == VF_GHOST;
+        const bool g1 = masks[64 * (int64_t)b + lane + 32] == VF_GHOST;
+        if (!__any_sync(0xffffffffu, g0 || g1)) continue;
         const int32_t P = parent[b];
-        if (P < sc || P >= ec) continue;
-        int Lc[3], sd[3];
+        if (P < sc || P >= ec) continue;  // warp-uniform
+        int R0[3];  // the fine block's first coarse cell, relative to P
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            const int I = d == 0 ? (t & 3) : (d == 1 ? ((t >> 2) & 3) : (t >> 4));
-            const int g = 4 * coords[4 * (int64_t)b + d] + I;
-            Lc[d] = (g >> 1) - 4 * coords[4 * (int64_t)P + d];
-            sd[d] = (g & 1) ? 1 : -1;
-        }
-        // coarse cell at local (lx, ly, lz) of P, lx in [-2, 5]: level-local
-        // index or -1 (outside the level / SOLID)
-        auto cell = [&](int lx, int ly, int lz) -> int32_t {
+        for (int d = 0; d < 3; ++d) R0[d] = 2 * coords[4 * (int64_t)b + d] - 4 * coords[4 * (int64_t)P + d];
+        // staged coarse cells: local (R0 - 2 + rx, ...), r = rx + 6 ry + 36 rz
+        for (int r = lane; r < 216; r += 32) {
+            const int lx = R0[0] - 2 + r % 6, ly = R0[1] - 2 + (r / 6) % 6, lz = R0[2] - 2 + r / 36;
             const int ox = lx < 0 ? -1 : (lx > 3 ? 1 : 0), oy = ly < 0 ? -1 : (ly > 3 ? 1 : 0),
                       oz = lz < 0 ? -1 : (lz > 3 ? 1 : 0);
             const int32_t Y = (ox | oy | oz) ? __ldg(nbr + 27 * (int64_t)P + slot_of(ox, oy, oz)) : P;
-            if (Y < sc || Y >= ec) return -1;
-            const int tt = (lx & 3) + 4 * (ly & 3) + 16 * (lz & 3);
-            if (masks[64 * (int64_t)Y + tt] == VF_SOLID) return -1;
-            return (Y - sc) * 64 + tt;
-        };
-        int ord = order >= 3 ? 3 : (order >= 1 ? 1 : 0);
-        if (ord == 3) {
-            for (int k = 0; k < 64 && ord == 3; ++k) {
-                const int kx = (k & 3) - 1, ky = ((k >> 2) & 3) - 1, kz = (k >> 4) - 1;
-                const int32_t c = cell(Lc[0] + sd[0] * kx, Lc[1] + sd[1] * ky, Lc[2] + sd[2] * kz);
-                s_idx[k][tid] = c;
-                if (c < 0) ord = 1;
+            int32_t c = -1;
+            if (Y >= sc && Y < ec) {
+                const int tt = (lx & 3) + 4 * (ly & 3) + 16 * (lz & 3);
+                if (masks[64 * (int64_t)Y + tt] != VF_SOLID) c = (Y - sc) * 64 + tt;
             }
+            s_c[w][r] = c;
         }
-        if (ord == 1) {
-            for (int k = 0; k < 8 && ord == 1; ++k) {
-                const int32_t c = cell(Lc[0] + sd[0] * (k & 1), Lc[1] + sd[1] * ((k >> 1) & 1),
-                                       Lc[2] + sd[2] * (k >> 2));
-                s_idx[k][tid] = c;
-                if (c < 0) ord = 0;
+        __syncwarp();
+        // per owned ghost cell: staged base index, axis steps, order
+        int base[2], st[2][3], ord[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int t = lane + 32 * h;
+            ord[h] = -1;
+            base[h] = 0;
+            st[h][0] = st[h][1] = st[h][2] = 0;
+            if (!(h ? g1 : g0)) continue;
+            const int I[3] = {t & 3, (t >> 2) & 3, t >> 4};
+            int bx[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                bx[d] = (I[d] >> 1) + 2;  // G relative to the staged box
+                st[h][d] = (I[d] & 1) ? 1 : -1;  // fine cell 4c + I: odd iff I odd
             }
+            const int sx = st[h][0], sy = 6 * st[h][1], sz = 36 * st[h][2];
+            base[h] = bx[0] + 6 * bx[1] + 36 * bx[2];
+            int o = order >= 3 ? 3 : (order >= 1 ? 1 : 0);
+            if (o == 3) {
+                for (int k = 0; k < 64 && o == 3; ++k)
+                    if (s_c[w][base[h] + sx * ((k & 3) - 1) + sy * (((k >> 2) & 3) - 1) + sz * ((k >> 4) - 1)] < 0) o = 1;
+            }
+            if (o == 1) {
+                for (int k = 0; k < 8 && o == 1; ++k)
+                    if (s_c[w][base[h] + sx * (k & 1) + sy * ((k >> 1) & 1) + sz * (k >> 2)] < 0) o = 0;
+            }
+            if (o == 0 && s_c[w][base[h]] < 0) o = -1;  // held
+            ord[h] = o;
+            st[h][1] *= 6;
+            st[h][2] *= 36;
         }
-        if (ord == 0) {
-            const int32_t c = cell(Lc[0], Lc[1], Lc[2]);
-            if (c < 0) continue;  // held
-            s_idx[0][tid] = c;
-        }
-        const int nk = ord == 3 ? 64 : (ord == 1 ? 8 : 1);
-        const float th0 = 1.0f - theta;
-        float f[27];
 #pragma unroll 1
         for (int q = 0; q < 27; ++q) {
-            float acc = 0.0f;
-            for (int k = 0; k < nk; ++k) {
-                float w;
-                if (ord == 3) w = c_w3[k & 3] * c_w3[(k >> 2) & 3] * c_w3[k >> 4];
-                else if (ord == 1) w = ((k & 1) ? 0.25f : 0.75f) * ((k & 2) ? 0.25f : 0.75f) * ((k & 4) ? 0.25f : 0.75f);
-                else w = 1.0f;
-                const int64_t c = (int64_t)q * nc + s_idx[k][tid];
-                const float v = theta == 0.0f ? fold[c] : th0 * fold[c] + theta * fnew[c];
-                acc += w * v;
-            }
-            f[q] = acc;
-        }
-        neq_rescale(f, alpha);
+            __syncwarp();
+            // 7 independent loads per lane in flight (216 = 6 x 32 + 24)
+            float v[7];
 #pragma unroll
-        for (int q = 0; q < 27; ++q) ff[(int64_t)q * nf + x] = f[q];
+            for (int i = 0; i < 7; ++i) {
+                const int r = lane + 32 * i;
+                const int32_t c = r < 216 ? s_c[w][r] : -1;
+                v[i] = 0.0f;
+                if (c >= 0) {
+                    const int64_t a = (int64_t)q * nc + c;
+                    v[i] = theta == 0.0f ? __ldg(fold + a) : th0 * __ldg(fold + a) + theta * __ldg(fnew + a);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 7; ++i)
+                if (lane + 32 * i < 216) s_v[w][lane + 32 * i] = v[i];
+            __syncwarp();
+            // separable passes at the requested order for the whole block
+            // (x: 4 x 6 x 6, y: 4 x 4 x 6, z: 4 x 4 x 4); same association as
+            // the per-cell sum below, so a cell's value does not depend on
+            // which path computed it
+            const int og = order >= 3 ? 3 : (order >= 1 ? 1 : 0);
+            const int ng = og == 3 ? 4 : (og == 1 ? 2 : 1), kg = og == 3 ? -1 : 0;
+            for (int e = lane; e < 144; e += 32) {  // (fx, ry, rz)
+                const int fx = e & 3, ry = (e >> 2) % 6, rz = (e >> 2) / 6;
+                const int G = (fx >> 1) + 2, sg = (fx & 1) ? 1 : -1;
+                float a = 0.0f;
+                for (int k = 0; k < ng; ++k) a += axis_w(og, k) * s_v[w][G + sg * (k + kg) + 6 * ry + 36 * rz];
+                s_t1[w][e] = a;
+            }
+            __syncwarp();
+            for (int e = lane; e < 96; e += 32) {  // (fx, fy, rz)
+                const int fx = e & 3, fy = (e >> 2) & 3, rz = e >> 4;
+                const int G = (fy >> 1) + 2, sg = (fy & 1) ? 1 : -1;
+                float a = 0.0f;
+                for (int k = 0; k < ng; ++k) a += axis_w(og, k) * s_t1[w][fx + 4 * (G + sg * (k + kg)) + 24 * rz];
+                s_t2[w][e] = a;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int o = ord[h];
+                if (o < 0) continue;
+                const int t = lane + 32 * h;
+                float acc = 0.0f;
+                if (o == og) {
+                    const int fz = t >> 4, G = (fz >> 1) + 2, sg = (fz & 1) ? 1 : -1;
+                    for (int k = 0; k < ng; ++k) acc += axis_w(og, k) * s_t2[w][(t & 15) + 16 * (G + sg * (k + kg))];
+                } else {  // fallback order of this cell (a stencil cell is missing)
+                    const int n = o == 3 ? 4 : (o == 1 ? 2 : 1), k0 = o == 3 ? -1 : 0;
+                    for (int kz = 0; kz < n; ++kz) {
+                        float ay = 0.0f;
+                        for (int ky = 0; ky < n; ++ky) {
+                            float ax = 0.0f;
+                            const int row = base[h] + st[h][1] * (ky + k0) + st[h][2] * (kz + k0);
+                            for (int kx = 0; kx < n; ++kx) ax += axis_w(o, kx) * s_v[w][row + st[h][0] * (kx + k0)];
+                            ay += axis_w(o, ky) * ax;
+                        }
+                        acc += axis_w(o, kz) * ay;
+                    }
+                }
+                ff[(int64_t)q * nf + (int64_t)(b - sf) * 64 + t] = acc;
+            }
+        }
+        if (alpha != 1.0f) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (ord[h] < 0) continue;
+                const int64_t x = (int64_t)(b - sf) * 64 + lane + 32 * h;
+                float f[27];
+#pragma unroll
+                for (int q = 0; q < 27; ++q) f[q] = ff[(int64_t)q * nf + x];
+                neq_rescale(f, alpha);
+#pragma unroll
+                for (int q = 0; q < 27; ++q) ff[(int64_t)q * nf + x] = f[q];
+            }
+        }
     }
 }
 
@@ -417,9 +498,9 @@ int vf_lbm_fill_ghosts(const vf_grid *g, int32_t sf, int32_t ef, int32_t sc, int
         !(order == 0 || order == 1 || order == 3))
         return set_error(VF_EARG, "vf_lbm_fill_ghosts: bad argument");
     if (ef == sf || ec == sc) return VF_OK;
-    int64_t grid = ((int64_t)(ef - sf) * 64 + kGhostThreads - 1) / kGhostThreads;
+    int64_t grid = ((int64_t)(ef - sf) + kFillWarps - 1) / kFillWarps;
     if (grid > max_ctas(8)) grid = max_ctas(8);
-    k_lbm_fill_ghosts<<<(int)grid, kGhostThreads, 0, (cudaStream_t)stream>>>(
+    k_lbm_fill_ghosts<<<(int)grid, kFillWarps * 32, 0, (cudaStream_t)stream>>>(
         sf, ef, sc, ec, g->d_coords, g->d_nbr, g->d_masks, d_parent, fc_old, fc_new ? fc_new : fc_old,
         (float)theta, (float)alpha, order, ff);
     return check_launch("k_lbm_fill_ghosts");

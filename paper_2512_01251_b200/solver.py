@@ -234,6 +234,21 @@ class LbmHierarchy:
             self._advance(0, force)
         return self
 
+    def graph(self):
+        """A CUDA graph of two coarse steps (every level then takes an even
+        number of substeps, so the ping-pong buffers are back in place after
+        each replay); the launch-bound host loop of step() is captured once."""
+        import torch
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.step(2)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step(2)
+        return g
+
     def mass(self) -> float:
         """sum over leaf cells (not SOLID / GHOST, block not refined) of
         rho (dx_L / dx_0)^3 -- the conservation audit of SPEC.md:434."""

@@ -165,3 +165,17 @@ def test_single_level_is_a_uniform_step():
     h.step(1)
     lv.step(1)
     assert torch.equal(h.levels[0].state, lv.state)
+
+
+def test_graph_replay_equals_eager(emb):
+    """The captured two-coarse-step graph (bench C3) computes what step() does."""
+    cfg, grid, table = emb
+    flow = FlowConfig(Re=20.0, u_in=0.04, D_s=16.0)
+    a = LbmHierarchy(grid, table, flow).init_equilibrium(1.0, (0.04, 0, 0))
+    b = LbmHierarchy(grid, table, flow).init_equilibrium(1.0, (0.04, 0, 0))
+    gr = a.graph()  # a: 2 warm-up coarse steps during capture
+    gr.replay()     # + 2
+    b.step(4)
+    torch.cuda.synchronize()
+    for la, lb in zip(a.levels, b.levels):
+        assert torch.equal(la.state, lb.state)
