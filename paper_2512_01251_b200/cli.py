@@ -8,7 +8,12 @@ voxelize: embed the geometry on the GPU, write one legacy ASCII VTK file per
 level (cell masks; cut-link counts on the finest level) and a JSON summary of
 the grid and the LinkTable.  bench: repeat the embedding and print the
 TimingReport (mean and 95% confidence half-width per stage group, the paper's
-Table 2 grouping).  simulate (the full multi-level LBM) is not built: exit 2.
+Table 2 grouping).  simulate: embed, then run iters_total coarse steps of the
+multi-level LBM (solver.step_hierarchy: D3Q27 BGK, IBB/SBB walls from the LUT,
+inlet/outlet on the x faces, cubic/linear interface exchange) and write the
+wall-force samples (finest level, lattice units) to forces.csv with a JSON
+summary (mean F_x and the drag coefficient C_D = 2 F_x / (rho u_in^2 A),
+A = pi D_s^2 / 4 in finest cells, for the sphere primitive).
 """
 from __future__ import annotations
 
@@ -20,9 +25,13 @@ import sys
 from typing import Dict
 
 KEYS = {"stl": str, "primitive": str, "subdivisions": int, "torus_m": int, "torus_n": int,
-        "N_x": int, "L_max": int, "N_spec": int, "d_spec": float, "out": str, "reps": int}
-DEFAULTS = {"primitive": "sphere", "subdivisions": 4, "torus_m": 280, "torus_n": 200, "N_x": 64,
-            "L_max": 3, "N_spec": 2, "d_spec": 0.05, "out": "voxforest_out", "reps": 20}
+        "diameter": float, "N_x": int, "L_max": int, "N_spec": int, "d_spec": float, "out": str, "reps": int,
+        "Re": float, "u_in": float, "bc_scheme": str, "interp_order": str, "iters_total": int,
+        "sample_start": int, "sample_stride": int}
+DEFAULTS = {"primitive": "sphere", "subdivisions": 4, "torus_m": 280, "torus_n": 200, "diameter": 0.5,
+            "N_x": 64, "L_max": 3, "N_spec": 2, "d_spec": 0.05, "out": "voxforest_out", "reps": 20,
+            "Re": 20.0, "u_in": 0.05, "bc_scheme": "IBB", "interp_order": "cubic", "iters_total": 100,
+            "sample_start": 50, "sample_stride": 10}
 
 
 class ConfigError(ValueError):
@@ -60,7 +69,7 @@ def _mesh(c):
             return parse_stl(fh.read())
     if c["primitive"] == "torus":
         return make_torus(c["torus_m"], c["torus_n"])
-    return make_icosphere((0.5, 0.5, 0.5), 0.5, c["subdivisions"])
+    return make_icosphere((0.5, 0.5, 0.5), c["diameter"], c["subdivisions"])
 
 
 def _embed_cfg(c):
@@ -110,6 +119,47 @@ def cmd_bench(c) -> int:
     return 0
 
 
+def cmd_simulate(c) -> int:
+    import numpy as np
+    import torch
+    from .solver import FlowConfig, LbmHierarchy
+    from .voxelizer import EmbedEngine
+    if c["bc_scheme"].upper() not in ("IBB", "SBB") or c["interp_order"] not in ("linear", "cubic"):
+        raise ConfigError("bc_scheme must be IBB|SBB and interp_order linear|cubic")
+    mesh, cfg = _mesh(c), _embed_cfg(c)
+    grid, table = EmbedEngine(mesh, cfg).run()
+    L = grid.n_levels - 1
+    d0 = c["diameter"] / cfg.dx0  # body size in level-0 cells (sphere primitive / bounding box)
+    if c.get("stl") or c["primitive"] != "sphere":
+        lo, hi = np.asarray(mesh.vertices).min(0), np.asarray(mesh.vertices).max(0)
+        d0 = float((hi - lo).max()) / cfg.dx0
+    flow = FlowConfig(Re=c["Re"], u_in=c["u_in"], D_s=d0, bc_scheme=c["bc_scheme"].upper(), open_x=True)
+    h = LbmHierarchy(grid, table, flow, order=3 if c["interp_order"] == "cubic" else 1)
+    h.init_equilibrium(1.0, (c["u_in"], 0.0, 0.0))
+    fine = h.levels[L]
+    os.makedirs(c["out"], exist_ok=True)
+    rows = []
+    for it in range(c["iters_total"]):
+        h.step(1, force=True)
+        if it >= c["sample_start"] and (it - c["sample_start"]) % max(1, c["sample_stride"]) == 0:
+            f = fine.force.cpu().numpy()
+            if not np.all(np.isfinite(f)):
+                raise FloatingPointError(f"non-finite wall force at coarse step {it}")
+            rows.append((it, *map(float, f)))
+    torch.cuda.synchronize()
+    with open(os.path.join(c["out"], "forces.csv"), "w") as fh:
+        fh.write("coarse_step,F_x,F_y,F_z\n")
+        for r in rows:
+            fh.write(",".join(str(x) for x in r) + "\n")
+    fx = float(np.mean([r[1] for r in rows])) if rows else None
+    d_f = d0 * 2 ** L
+    cd = 2.0 * fx / (c["u_in"] ** 2 * np.pi * d_f * d_f / 4.0) if fx is not None else None
+    summary = {"levels": grid.n_levels, "taus": h.taus, "substeps": h.substeps, "samples": len(rows),
+               "F_x_mean_lattice": fx, "C_D": cd, "D_s_finest_cells": d_f}
+    print(json.dumps(summary))
+    return 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="paper_2512_01251_b200")
     ap.add_argument("command", choices=["voxelize", "bench", "simulate"])
@@ -132,11 +182,9 @@ def main(argv=None) -> int:
                  ("N_spec", a.nspec), ("d_spec", a.dspec), ("out", a.out), ("reps", a.reps)):
         if v is not None:
             c[k] = v
-    if a.command == "simulate":
-        print("simulate: the multi-level LBM solver is not built (only the single-level LUT "
-              "consumer, solver.py)", file=sys.stderr)
-        return 2
     try:
+        if a.command == "simulate":
+            return cmd_simulate(c)
         return cmd_voxelize(c) if a.command == "voxelize" else cmd_bench(c)
     except Exception as ex:  # non-zero exit with a message on any pipeline error
         print(f"{a.command}: {type(ex).__name__}: {ex}", file=sys.stderr)

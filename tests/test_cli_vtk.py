@@ -1,6 +1,6 @@
 """CPU checks of the outputs / CLI plumbing (SPEC.md write_outputs, load_config,
 run_cli): VTK voxel files round-trip, config errors name key and line,
-'simulate' and unknown subcommands exit 2."""
+unknown subcommands exit 2, pipeline commands without a GPU exit non-zero."""
 import os
 
 import numpy as np
@@ -45,7 +45,9 @@ def test_config_errors(tmp_path):
 
 
 def test_cli_exit_codes(capsys):
-    assert cli.main(["simulate"]) == 2
+    import torch
+    if not torch.cuda.is_available():  # no CPU fallback: a message and exit 1
+        assert cli.main(["simulate", "--nx", "16", "--lmax", "1"]) == 1
     with pytest.raises(SystemExit) as ei:
         cli.main(["frobnicate"])
     assert ei.value.code == 2

@@ -179,3 +179,19 @@ def test_graph_replay_equals_eager(emb):
     torch.cuda.synchronize()
     for la, lb in zip(a.levels, b.levels):
         assert torch.equal(la.state, lb.state)
+
+
+def test_cli_simulate(tmp_path):
+    """`simulate`: embed + step_hierarchy, force samples and a drag summary."""
+    import json
+    from paper_2512_01251_b200 import cli
+    cfgp = tmp_path / "run.cfg"
+    cfgp.write_text("primitive = sphere\nsubdivisions = 3\ndiameter = 0.25\nN_x = 32\nL_max = 2\n"
+                    "iters_total = 8\nsample_start = 2\nsample_stride = 2\nu_in = 0.04\nRe = 10\n"
+                    f"out = {tmp_path}\n")
+    rc = cli.main(["simulate", "--config", str(cfgp)])
+    assert rc == 0
+    rows = open(tmp_path / "forces.csv").read().strip().splitlines()
+    assert rows[0] == "coarse_step,F_x,F_y,F_z" and len(rows) == 1 + 3
+    fx = [float(r.split(",")[1]) for r in rows[1:]]
+    assert all(np.isfinite(fx)) and fx[-1] > 0  # drag along the inflow
