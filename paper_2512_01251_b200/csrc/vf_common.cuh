@@ -24,21 +24,18 @@ constexpr int kFaceStride = 12;  // doubles per face record: v1 v2 v3 n (96 B)
 constexpr int kWarp = 32;
 
 // D3Q27 order of lattice.py:19-39 (rest first, antiparallel pairs (2k-1,2k))
+// Component d of c_q, packed as 2-bit fields (c + 1) of one 64-bit immediate
+// per axis: a shift and a mask, no table -- a runtime-indexed table becomes a
+// constant-bank load that serialises over the distinct q of a warp.
 __host__ __device__ __forceinline__ int c27(int q, int d) {
-    // packed as base-3 digits (c+1): x + 3y + 9z
-    constexpr int code[27] = {13, 14, 12, 16, 10, 22, 4,  17, 9,  23, 3,  5,  21, 11,
-                              15, 25, 1,  7,  19, 26, 0,  8,  18, 20, 6,  2,  24};
-    int v = code[q];
-    if (d == 0) return v % 3 - 1;
-    if (d == 1) return (v / 3) % 3 - 1;
-    return v / 9 - 1;
+    const uint64_t k = d == 0 ? 0x8889548889549ull : (d == 1 ? 0x220888a1549495ull : 0x20a0a096094955ull);
+    return (int)((k >> (2 * q)) & 3u) - 1;
 }
 
-// slot of direction (dx,dy,dz) in {-1,0,1}^3
+// slot of direction (dx,dy,dz) in {-1,0,1}^3: 5-bit fields, one word per dz
 __host__ __device__ __forceinline__ int slot_of(int dx, int dy, int dz) {
-    constexpr int inv[27] = {20, 16, 25, 10, 6,  11, 24, 17, 21, 8,  4,  13, 2,  0,
-                             1,  14, 3,  7,  22, 18, 23, 12, 5,  9,  26, 15, 19};
-    return inv[(dx + 1) + 3 * (dy + 1) + 9 * (dz + 1)];
+    const uint64_t w = dz < 0 ? 0x158e16656614ull : (dz == 0 ? 0x71b82013488ull : 0x137e92565e56ull);
+    return (int)((w >> (5 * ((dx + 1) + 3 * (dy + 1)))) & 31u);
 }
 
 // per-level constants, computed on the host (ldexp => exact dx_L)

@@ -843,7 +843,7 @@ __global__ void __launch_bounds__(256)
         const int4 rec = c.lines[e];
         const int f = rec.x, R = rec.y & 15, cnt = (rec.y >> 5) & 7, ip_lo = rec.y >> 8;
         const int m1 = rec.z, m2 = rec.w;
-        const int cx = c_rep[R][0], cy = c_rep[R][1], cz = c_rep[R][2];
+        const int cx = c27(2 * R + 1, 0), cy = c27(2 * R + 1, 1), cz = c27(2 * R + 1, 2);  // c_rep[R], per-thread R
         const int p = cx != 0 ? 0 : (cy != 0 ? 1 : 2);
         const int q1 = p == 0 ? 1 : 0, q2 = p == 2 ? 1 : 2;
         const int cp = pick3(p, cx, cy, cz);
