@@ -461,6 +461,193 @@ __global__ void __launch_bounds__(kXrowWarps * 32)
     }
 }
 
+// Staged variant for rows of up to 32 * NCH blocks (levels with B_L <= 128): the row's block ids, masks (row stride 17 words: no bank
+// conflicts), run-start neighbour codes of both directions and changed
+// flags are staged in shared memory with all global loads issued up front,
+// then both passes run out of shared memory and only changed blocks are
+// stored -- the chunked passes above wait on a dependent load chain per
+// chunk and per direction.
+constexpr int kXsWarps = 4;
+static int g_xrows_chunked = 0;  // vf_set_xrows_chunked (test hook): force the chunked kernel
+
+template <int NCH>
+struct XStage {
+    int32_t id[NCH * 32];
+    int32_t cp[NCH * 32];  // +x run start: code of the -x neighbour (slot 2)
+    int32_t cm[NCH * 32];  // -x run start: code of the +x neighbour (slot 1)
+    uint8_t chg[NCH * 32];
+    uint32_t m[NCH * 32 * 17];
+};
+
+template <int DIR, int NCH>
+__device__ __forceinline__ void xrow_pass_s(int L, int lane, int bx, XStage<NCH> &S) {
+    constexpr int trail = DIR > 0 ? 3 : 0;
+    uint32_t carry = 0;
+    bool prev_present = false;
+#pragma unroll 1
+    for (int x0 = 0; x0 < bx; x0 += 32) {
+        const int x = DIR > 0 ? x0 + lane : bx - 1 - (x0 + lane);
+        const int32_t id = (x0 + lane < bx) ? S.id[x] : -1;
+        const bool present = id >= 0;
+        const uint32_t pm = __ballot_sync(0xffffffffu, present);
+        if (pm == 0) {
+            prev_present = false;
+            continue;
+        }
+        const bool pred = lane > 0 ? ((pm >> (lane - 1)) & 1u) : prev_present;
+        uint32_t *w = S.m + 17 * (x < 0 ? 0 : x);
+        uint32_t fn = 0;
+        bool head = true;
+        if (present) {
+            uint32_t A = 0, B = 0;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const uint32_t h3 = (w[r] >> (8 * trail)) & 0xffu;
+                A |= (uint32_t)(h3 != VF_GUARD) << r;
+                B |= (uint32_t)(h3 == VF_SOLID) << r;
+            }
+            fn = A | (B << 16);
+            if (!pred) {
+                const int32_t code = DIR > 0 ? S.cp[x] : S.cm[x];
+                const uint32_t c = (code == VF_NB_SOLID_NBR) ? A : B;
+                fn = c | (c << 16);
+            } else if (lane == 0) {
+                fn = compose(fn, carry | (carry << 16));
+            } else {
+                head = false;
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t g = __shfl_up_sync(0xffffffffu, fn, o);
+            const int hd = __shfl_up_sync(0xffffffffu, (int)head, o);
+            if (lane >= o && !head) {
+                fn = compose(fn, g);
+                head = hd;
+            }
+        }
+        const uint32_t out = fn & 0xffffu;
+        uint32_t st = __shfl_up_sync(0xffffffffu, out, 1);
+        if (lane == 0) st = carry;
+        if (present && pred) {
+            bool changed = false;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                uint32_t xw = w[r];
+#pragma unroll
+                for (int I = 0; I < 4; ++I) {
+                    const uint32_t h = (xw >> (8 * I)) & 0xffu;
+                    uint32_t hn = h;
+                    if ((st >> r & 1u) && h != VF_GUARD) hn = VF_SOLID;
+                    if (L == 0 && hn == VF_GUARD) hn = VF_FLUID;
+                    xw = (xw & ~(0xffu << (8 * I))) | (hn << (8 * I));
+                }
+                changed |= (xw != w[r]);
+                w[r] = xw;
+            }
+            if (changed) S.chg[x] = 1;
+        }
+        carry = __shfl_sync(0xffffffffu, out, 31);
+        prev_present = (pm >> 31) & 1u;
+        __syncwarp();
+    }
+}
+
+template <int NCH>
+__global__ void __launch_bounds__(kXsWarps * 32)
+    k_xrows_s(LevelInfo li, int L, const int32_t *__restrict__ map, const int32_t *__restrict__ nbr,
+              uint8_t *__restrict__ masks, uint8_t *__restrict__ bflags, uint64_t *__restrict__ solid64) {
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    const int lane = threadIdx.x & 31;
+    XStage<NCH> &S = reinterpret_cast<XStage<NCH> *>(s_raw)[threadIdx.x >> 5];
+    const int64_t gw = (int64_t)blockIdx.x * kXsWarps + (threadIdx.x >> 5);
+    const int64_t nw = (int64_t)gridDim.x * kXsWarps;
+    const int bx = li.bins[0], by = li.bins[1];
+    const int64_t rows = (int64_t)by * li.bins[2];
+    for (int64_t rw = gw; rw < rows; rw += nw) {
+        const int j = (int)(rw % by), k = (int)(rw / by);
+        if (!owns_row(li, j, k)) continue;
+        const int32_t *row = map + rw * bx;
+        int32_t ids[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) ids[c] = (32 * c + lane < bx) ? row[32 * c + lane] : -1;
+        uint32_t anyp = 0;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            S.id[32 * c + lane] = ids[c];
+            S.chg[32 * c + lane] = 0;
+            anyp |= __ballot_sync(0xffffffffu, ids[c] >= 0);
+        }
+        if (!anyp) continue;  // empty row
+        __syncwarp();
+        // masks + run-start codes, all loads in flight together
+        uint4 mv[NCH][4];
+        int32_t cpv[NCH], cmv[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const int x = 32 * c + lane;
+            const int32_t id = ids[c];
+            cpv[c] = 0;
+            cmv[c] = 0;
+            if (id >= 0) {
+                const uint4 *p = reinterpret_cast<const uint4 *>(masks + 64 * (int64_t)id);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) mv[c][q] = p[q];
+                if (!(x > 0 && S.id[x - 1] >= 0)) cpv[c] = nbr[27 * (int64_t)id + 2];
+                if (L > 0 && !(x + 1 < bx && S.id[x + 1] >= 0)) cmv[c] = nbr[27 * (int64_t)id + 1];
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const int x = 32 * c + lane;
+            if (ids[c] >= 0) {
+                uint32_t *w = S.m + 17 * x;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    w[4 * q] = mv[c][q].x; w[4 * q + 1] = mv[c][q].y;
+                    w[4 * q + 2] = mv[c][q].z; w[4 * q + 3] = mv[c][q].w;
+                }
+                S.cp[x] = cpv[c];
+                S.cm[x] = cmv[c];
+            }
+        }
+        __syncwarp();
+        xrow_pass_s<+1, NCH>(L, lane, bx, S);
+        if (L > 0) xrow_pass_s<-1, NCH>(L, lane, bx, S);
+        // finalize every block of the row and store the changed ones
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const int x = 32 * c + lane;
+            const int32_t id = ids[c];
+            if (id < 0) continue;
+            uint32_t w[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) w[r] = S.m[17 * x + r];
+            bool changed = S.chg[x] != 0;
+            finalize_block(w, changed, bflags, solid64, id);
+            if (changed) store_masks64(masks, id, w);
+        }
+        __syncwarp();
+    }
+}
+
+template <int NCH>
+static int launch_xrows_s(const LevelInfo &li, int L, const int32_t *map, vf_grid *g, cudaStream_t st) {
+    const size_t smem = kXsWarps * sizeof(XStage<NCH>);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_xrows_s<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const int64_t rows = (int64_t)li.bins[1] * li.bins[2];
+    int64_t grid = (rows + kXsWarps - 1) / kXsWarps;
+    const int64_t cap = max_ctas(NCH <= 2 ? 16 : (NCH <= 4 ? 8 : 4));
+    if (grid > cap) grid = cap;
+    k_xrows_s<NCH><<<(int)grid, kXsWarps * 32, smem, st>>>(li, L, map, g->d_nbr, g->d_masks, g->d_bflags,
+                                                           g->d_solid64);
+    return check_launch("k_xrows");
+}
+
 size_t propagate_level_workspace_size(const vf_config &cfg, int L) {
     const int64_t nb = (int64_t)(cfg.nb[0] << L) * (cfg.nb[1] << L) * (cfg.nb[2] << L);
     return ((size_t)nb * sizeof(int32_t) + 255) & ~(size_t)255;
@@ -475,6 +662,14 @@ int propagate_level_impl(const LevelInfo &li, vf_grid *g, int L, void *ws, size_
     k_level_map<<<max_ctas(8), 256, 0, st>>>(L, li, g->d_level_start, g->d_coords, map);
     int rc = check_launch("k_level_map");
     if (rc) return rc;
+    const int bx = li.bins[0];
+    if (!g_xrows_chunked) {
+        if (bx <= 32) return launch_xrows_s<1>(li, L, map, g, st);
+        if (bx <= 64) return launch_xrows_s<2>(li, L, map, g, st);
+        if (bx <= 128) return launch_xrows_s<4>(li, L, map, g, st);
+        // (8 chunks: 215 registers and 83 KB of shared memory per CTA -- slower
+        // than the chunked kernel next to the concurrent link enumeration)
+    }
     int64_t rows = (int64_t)li.bins[1] * li.bins[2];
     int64_t grid = (rows + kXrowWarps - 1) / kXrowWarps;
     if (grid > max_ctas(8)) grid = max_ctas(8);
@@ -541,3 +736,9 @@ int finalize_impl(vf_grid *g, int L, cudaStream_t st) {
 }
 
 }  // namespace vf
+
+extern "C" int vf_set_xrows_chunked(int on) {
+    const int old = vf::g_xrows_chunked;
+    if (on >= 0) vf::g_xrows_chunked = on ? 1 : 0;
+    return old;
+}
