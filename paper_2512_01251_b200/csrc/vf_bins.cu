@@ -124,12 +124,15 @@ __global__ void __launch_bounds__(kIndWarps * 32, 3)
     }
 }
 
+#ifndef VF_IND_MINB
+#define VF_IND_MINB 2  // 120 registers, no spills (3: 80 + 128 B stack)
+#endif
 // All levels in ONE pass over the face records (the per-level kernel reads
 // the 96 B/face records once per level): bit L of out[f] is the 1D indicator
 // of face f at level L.  Candidate rows are decided by the FP32 row
 // classifier (vf_common.cuh); only undecided rows run the exact SAT.  Same
 // predicate as indicator_rows, row for row.
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, VF_IND_MINB)
     k_indicators_all(LevelSet ls, const double *__restrict__ faces, int64_t F,
                      uint16_t *__restrict__ out) {
     for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < F;
