@@ -631,6 +631,156 @@ __global__ void __launch_bounds__(kXsWarps * 32)
     }
 }
 
+// Hybrid for wide, sparse rows (B_L = 256): block ids and run-start codes are
+// staged (all loads up front, empty 32-block chunks skipped without a load);
+// masks stay in global memory, loaded per non-empty chunk as in k_xrows,
+// with finalize fused into the last pass.
+template <int NCH>
+struct XHView {
+    const int32_t *id, *cp, *cm;
+};
+
+template <int DIR, int NCH>
+__device__ __forceinline__ void xrow_pass_hv(int L, int lane, int bx, const XHView<NCH> &S, uint32_t cmask,
+                                            uint8_t *__restrict__ masks, bool finalize,
+                                            uint8_t *__restrict__ bflags, uint64_t *__restrict__ solid64) {
+    constexpr int trail = DIR > 0 ? 3 : 0;
+    uint32_t carry = 0;
+    bool prev_present = false;
+#pragma unroll 1
+    for (int c = 0; c < NCH; ++c) {
+        const int x0 = 32 * c;
+        // chunk of this pass: +x walks chunks 0.., -x walks x = bx-1-(x0+lane)
+        const int cc = DIR > 0 ? c : (bx - 1 - x0) >> 5;
+        const bool any = DIR > 0 ? ((cmask >> c) & 1u) : (((cmask >> cc) & 1u) || (x0 + 31 < bx && ((cmask >> ((bx - 1 - x0 - 31) >> 5)) & 1u)));
+        if (x0 >= bx) break;
+        if (!any) {
+            prev_present = false;
+            continue;
+        }
+        const int x = DIR > 0 ? x0 + lane : bx - 1 - (x0 + lane);
+        const int32_t id = (x0 + lane < bx) ? S.id[x] : -1;
+        const bool present = id >= 0;
+        const uint32_t pm = __ballot_sync(0xffffffffu, present);
+        if (pm == 0) {
+            prev_present = false;
+            continue;
+        }
+        const bool pred = lane > 0 ? ((pm >> (lane - 1)) & 1u) : prev_present;
+        uint32_t w[16];
+        uint32_t fn = 0;
+        bool head = true;
+        if (present) {
+            load_masks64(masks, id, w);
+            uint32_t A = 0, B = 0;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const uint32_t h3 = (w[r] >> (8 * trail)) & 0xffu;
+                A |= (uint32_t)(h3 != VF_GUARD) << r;
+                B |= (uint32_t)(h3 == VF_SOLID) << r;
+            }
+            fn = A | (B << 16);
+            if (!pred) {
+                const int32_t code = DIR > 0 ? S.cp[x] : S.cm[x];
+                const uint32_t cb = (code == VF_NB_SOLID_NBR) ? A : B;
+                fn = cb | (cb << 16);
+            } else if (lane == 0) {
+                fn = compose(fn, carry | (carry << 16));
+            } else {
+                head = false;
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t g = __shfl_up_sync(0xffffffffu, fn, o);
+            const int hd = __shfl_up_sync(0xffffffffu, (int)head, o);
+            if (lane >= o && !head) {
+                fn = compose(fn, g);
+                head = hd;
+            }
+        }
+        const uint32_t out = fn & 0xffffu;
+        uint32_t st = __shfl_up_sync(0xffffffffu, out, 1);
+        if (lane == 0) st = carry;
+        if (present) {
+            bool changed = false;
+            if (pred) {
+#pragma unroll
+                for (int r = 0; r < 16; ++r) {
+                    uint32_t xw = w[r];
+#pragma unroll
+                    for (int I = 0; I < 4; ++I) {
+                        const uint32_t h = (xw >> (8 * I)) & 0xffu;
+                        uint32_t hn = h;
+                        if ((st >> r & 1u) && h != VF_GUARD) hn = VF_SOLID;
+                        if (L == 0 && hn == VF_GUARD) hn = VF_FLUID;
+                        xw = (xw & ~(0xffu << (8 * I))) | (hn << (8 * I));
+                    }
+                    changed |= (xw != w[r]);
+                    w[r] = xw;
+                }
+            }
+            if (finalize) finalize_block(w, changed, bflags, solid64, id);
+            if (changed) store_masks64(masks, id, w);
+        }
+        carry = __shfl_sync(0xffffffffu, out, 31);
+        prev_present = (pm >> 31) & 1u;
+    }
+}
+
+template <int NCH>
+__global__ void __launch_bounds__(kXsWarps * 32)
+    k_xrows_h(LevelInfo li, int L, const int32_t *__restrict__ map, const int32_t *__restrict__ nbr,
+              uint8_t *__restrict__ masks, uint8_t *__restrict__ bflags, uint64_t *__restrict__ solid64) {
+    __shared__ int32_t s_id[kXsWarps][NCH * 32], s_cp[kXsWarps][NCH * 32], s_cm[kXsWarps][NCH * 32];
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * kXsWarps + wi;
+    const int64_t nw = (int64_t)gridDim.x * kXsWarps;
+    const int bx = li.bins[0], by = li.bins[1];
+    const int64_t rows = (int64_t)by * li.bins[2];
+    for (int64_t rw = gw; rw < rows; rw += nw) {
+        const int j = (int)(rw % by), k = (int)(rw / by);
+        if (!owns_row(li, j, k)) continue;
+        const int32_t *row = map + rw * bx;
+        int32_t ids[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) ids[c] = (32 * c + lane < bx) ? row[32 * c + lane] : -1;
+        uint32_t cmask = 0;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            s_id[wi][32 * c + lane] = ids[c];
+            cmask |= (__ballot_sync(0xffffffffu, ids[c] >= 0) ? 1u : 0u) << c;
+        }
+        if (!cmask) continue;
+        __syncwarp();
+        int32_t cpv[NCH], cmv[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const int x = 32 * c + lane;
+            const int32_t id = ids[c];
+            cpv[c] = 0;
+            cmv[c] = 0;
+            if (id >= 0) {
+                if (!(x > 0 && s_id[wi][x - 1] >= 0)) cpv[c] = nbr[27 * (int64_t)id + 2];
+                if (L > 0 && !(x + 1 < bx && s_id[wi][x + 1] >= 0)) cmv[c] = nbr[27 * (int64_t)id + 1];
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            s_cp[wi][32 * c + lane] = cpv[c];
+            s_cm[wi][32 * c + lane] = cmv[c];
+        }
+        __syncwarp();
+        XHView<NCH> V{s_id[wi], s_cp[wi], s_cm[wi]};
+        xrow_pass_hv<+1, NCH>(L, lane, bx, V, cmask, masks, L == 0, bflags, solid64);
+        if (L > 0) {
+            __syncwarp();
+            xrow_pass_hv<-1, NCH>(L, lane, bx, V, cmask, masks, true, bflags, solid64);
+        }
+        __syncwarp();
+    }
+}
+
 template <int NCH>
 static int launch_xrows_s(const LevelInfo &li, int L, const int32_t *map, vf_grid *g, cudaStream_t st) {
     const size_t smem = kXsWarps * sizeof(XStage<NCH>);
@@ -667,8 +817,16 @@ int propagate_level_impl(const LevelInfo &li, vf_grid *g, int L, void *ws, size_
         if (bx <= 32) return launch_xrows_s<1>(li, L, map, g, st);
         if (bx <= 64) return launch_xrows_s<2>(li, L, map, g, st);
         if (bx <= 128) return launch_xrows_s<4>(li, L, map, g, st);
-        // (8 chunks: 215 registers and 83 KB of shared memory per CTA -- slower
-        // than the chunked kernel next to the concurrent link enumeration)
+        // (8 chunks staged: 215 registers and 83 KB of shared memory per CTA --
+        // slower next to the concurrent link enumeration; ids / codes only)
+        if (bx <= 256) {
+            const int64_t rows = (int64_t)li.bins[1] * li.bins[2];
+            int64_t grid = (rows + kXsWarps - 1) / kXsWarps;
+            if (grid > max_ctas(8)) grid = max_ctas(8);
+            k_xrows_h<8><<<(int)grid, kXsWarps * 32, 0, st>>>(li, L, map, g->d_nbr, g->d_masks, g->d_bflags,
+                                                              g->d_solid64);
+            return check_launch("k_xrows");
+        }
     }
     int64_t rows = (int64_t)li.bins[1] * li.bins[2];
     int64_t grid = (rows + kXrowWarps - 1) / kXrowWarps;

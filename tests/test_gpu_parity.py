@@ -406,14 +406,15 @@ def test_links_small_face_split(O, torus, small_ext):
 
 @pytest.mark.parametrize("chunked", [1, 0])
 def test_xrows_kernels(O, torus, chunked):
-    """Alg. 5 rows: the shared-memory staged kernel (rows <= 128 blocks) and
-    the chunked one give the oracle's masks."""
+    """Alg. 5 rows: the shared-memory staged kernel (rows <= 128 blocks), the
+    hybrid (256) and the chunked one give the oracle's masks."""
     from paper_2512_01251_b200 import _lib
     lib = _lib.require_cuda()
     old = lib.vf_set_xrows_chunked(chunked)
     try:
         _embed_compare(O, torus, EmbedConfig(n_x=32, l_max=3))
         _embed_compare(O, make_icosphere((0.5, 0.5, 0.5), 0.5, 4), EmbedConfig(n_x=64, l_max=3))
+        _embed_compare(O, make_torus(300, 120), EmbedConfig(n_x=64, l_max=5))  # B_L = 256 rows
     finally:
         lib.vf_set_xrows_chunked(old)
 
