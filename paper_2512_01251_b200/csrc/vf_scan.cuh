@@ -68,6 +68,10 @@ __global__ void __launch_bounds__(kScanThreads)
     __shared__ int s_warp[kScanThreads / 32];
     __shared__ int s_tile;
     __shared__ int s_prefix;
+    __shared__ int s_tile_agg;
+    // tile staged through shared memory: loads and emits in warp-striped
+    // (coalesced) order, the scan over 16 consecutive items per thread
+    __shared__ int s_v[kScanTile + kScanTile / 32];
     const int64_t n = nfn();
     const int64_t n_tiles = (n + kScanTile - 1) / kScanTile;
     uint32_t *counter = reinterpret_cast<uint32_t *>(status);
@@ -84,13 +88,20 @@ __global__ void __launch_bounds__(kScanThreads)
     if (tile >= n_tiles) return;
     uint64_t *tstat = status + 1;
 
-    const int64_t base = tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    const int64_t tbase = tile * kScanTile;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int j = k * kScanThreads + threadIdx.x;
+        const int64_t i = tbase + j;
+        s_v[j + (j >> 5)] = (i < n) ? load(i) : 0;
+    }
+    __syncthreads();
     int vals[kScanItems];
     int tsum = 0;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-        const int64_t i = base + k;
-        vals[k] = (i < n) ? load(i) : 0;
+        const int j = threadIdx.x * kScanItems + k;
+        vals[k] = s_v[j + (j >> 5)];
         tsum += vals[k];
     }
     // block-wide exclusive scan of the per-thread sums
@@ -143,6 +154,7 @@ __global__ void __launch_bounds__(kScanThreads)
         }
         if (lane == 0) {
             s_prefix = prefix;
+            s_tile_agg = agg;
             if (tile == n_tiles - 1) {
                 if (d_total) *d_total = prefix + agg;
                 epi(prefix + agg);
@@ -151,11 +163,27 @@ __global__ void __launch_bounds__(kScanThreads)
     }
     __syncthreads();
     int run = s_prefix + s_warp[warp] + incl - tsum;
+    // exclusive prefixes back to shared memory (over the values: each
+    // thread rewrites only its own 16 slots), then emit in striped order
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-        const int64_t i = base + k;
-        if (i < n) emit(i, vals[k], run);
+        const int j = threadIdx.x * kScanItems + k;
+        s_v[j + (j >> 5)] = run;
         run += vals[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int j = k * kScanThreads + threadIdx.x;
+        const int64_t i = tbase + j;
+        if (i < n) {
+            const int ex = s_v[j + (j >> 5)];
+            const int jn = j + 1;
+            // the value is the next exclusive prefix minus this one (the
+            // tile's last item: the tile aggregate)
+            const int nx = (j + 1 < kScanTile) ? s_v[jn + (jn >> 5)] : (s_prefix + s_tile_agg);
+            emit(i, nx - ex, ex);
+        }
     }
 }
 
