@@ -596,8 +596,11 @@ __global__ void __launch_bounds__(kLinkWarps * 32, MODE == 1 ? 1 : VF_LINK_MINB)
 // classes remain conservative and the recorded lines, band candidates and
 // hence the LUT are identical.  Larger faces are appended to a list for the
 // warp-flattened kernel.
+#ifndef VF_SMALL_DIRECT
+#define VF_SMALL_DIRECT 1
+#endif
 #ifndef VF_SMALL_MINB
-#define VF_SMALL_MINB 3
+#define VF_SMALL_MINB 4
 #endif
 static float g_small_ext = 1.5f;  // vf_set_link_small_ext (test / tuning hook)
 
@@ -613,7 +616,10 @@ __device__ __forceinline__ void line_store(const LinkCtx &c, int pos, int4 rec) 
 // lines are staged per CTA in shared memory and written with ONE global slot
 // reservation per CTA (a per-warp-per-pair atomicAdd on the shared line
 // counter was the kernel's top stall); a full stage falls back to direct slots
-constexpr int kLineStage = 1024;
+#ifndef VF_SMALL_THREADS
+#define VF_SMALL_THREADS 256
+#endif
+constexpr int kLineStage = 4 * VF_SMALL_THREADS;
 
 __device__ __forceinline__ void stage_put(const LinkCtx &c, int4 *st, int pos, int4 rec) {
     if (pos < kLineStage) st[pos] = rec;
@@ -626,6 +632,7 @@ struct SmallFace {
     float w[3], V1[3], V2[3], nf[3];
     int b[3], lo[3], hi[3];        // base node, fallback node range per axis
     float epsL, ff9;
+    float dthr;  // 2 EPS_PARALLEL sqrt(3) + 1e-5 > the FP32 error of c.n plus the exact threshold
     int f;
 };
 
@@ -669,13 +676,18 @@ __device__ __forceinline__ void small_project(const LinkCtx &c, const SmallFace 
 // lines as records (<= 2 kept in r0 / r1 for the warp-aggregated write; more
 // go out directly) and the undecided ones node by node to the band list
 __device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S, const SmallProj &P,
-                                           bool small, int R, int s1, int s2, int4 &r0, int4 &r1, int &nr) {
+                                           bool small, int R, int s1, int s2, int4 &r0, int4 &r1, int &nr,
+                                           int4 *s_rec, int *s_n) {
     // exact den / EPS_PARALLEL, as link_dir_setup: c = (1, s1, s2) over
     // (p, q1, q2) -- the same FP64 sum in the same order (a zero term is exact)
-    const double den = VF_DADD(VF_DADD(P.np, cmul(s1, P.nq1)), cmul(s2, P.nq2));
-    const int nz = (s1 != 0) + (s2 != 0);
-    const double cn = nz == 0 ? 1.0 : (nz == 1 ? 1.4142135623730951 : 1.7320508075688772);
-    if (!small || fabs(den) < VF_DMUL(c.eps_par, cn)) return;
+    if (!small) return;
+    const float dn = P.nfp + (float)s1 * P.nfa + (float)s2 * P.nfb;  // c.n in FP32 (error < 1e-6)
+    if (!(fabsf(dn) > S.dthr)) {  // only then can |c.n| be below EPS_PARALLEL |c|: decide exactly
+        const double den = VF_DADD(VF_DADD(P.np, cmul(s1, P.nq1)), cmul(s2, P.nq2));
+        const int nz = (s1 != 0) + (s2 != 0);
+        const double cn = nz == 0 ? 1.0 : (nz == 1 ? 1.4142135623730951 : 1.7320508075688772);
+        if (fabs(den) < VF_DMUL(c.eps_par, cn)) return;
+    }
     const float P1a = P.V1a - (float)s1 * P.V1p, P1b = P.V1b - (float)s2 * P.V1p;
     const float P2a = P.V2a - (float)s1 * P.V2p, P2b = P.V2b - (float)s2 * P.V2p;
     const float ext = fmaxf(fmaxf(fabsf(P1a), fabsf(P1b)), fmaxf(fabsf(P2a), fabsf(P2b)));
@@ -688,14 +700,15 @@ __device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S,
     if (m1a > m1b || m2a > m2b) return;
     const float cr = P1a * P2b - P1b * P2a;
     const float ab = 4e-6f * (ext + 1.0f) * (ext + 1.0f);
-    const float t0 = tol * mlen(P1a, P1b) + ab;
-    const float t1 = tol * mlen(P2a - P1a, P2b - P1b) + ab;
-    const float t2 = tol * mlen(P2a, P2b) + ab;
+    // edge margins with the L1 length |a| + |b| >= |e| (no square root: a
+    // larger margin only moves lines from the miss / interior classes into
+    // the exactly-decided band, so every class stays conservative)
+    const float t0 = tol * (fabsf(P1a) + fabsf(P1b)) * 1.0001f + ab;
+    const float t1 = tol * (fabsf(P2a - P1a) + fabsf(P2b - P1b)) * 1.0001f + ab;
+    const float t2 = tol * (fabsf(P2a) + fabsf(P2b)) * 1.0001f + ab;
     const float sg = cr >= 0.0f ? 1.0f : -1.0f;
-    const float dn = P.nfp + (float)s1 * P.nfa + (float)s2 * P.nfb;
     const bool steep = fabsf(dn) >= 1e-3f;
     const bool fast = steep && c.fast;
-    const float wid0 = 1.0f + 1e-4f + 1e-5f + __fdividef(S.ff9, fabsf(dn)) * 1.0001f;
     const int gm1 = P.ba - s1 * P.bp, gm2 = P.bb - s2 * P.bp;
     for (int M2 = m2a; M2 <= m2b; ++M2) {
         const float Rb = (float)M2 + o2;
@@ -710,6 +723,7 @@ __device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S,
             int ip_lo = P.lop, ip_hi = P.hip;
             if (steep) {
                 const float xs = -__fdividef(P.nfa * Ra + P.nfb * Rb, dn);
+                const float wid0 = 1.0f + 1e-4f + 1e-5f + __fdividef(S.ff9, fabsf(dn)) * 1.0001f;
                 const float wid = wid0 + 1.0001e-6f * __fdividef(fabsf(xs), fabsf(dn));
                 ip_lo = max(P.bp + (int)ceilf(xs + P.wp - wid), ip_lo);
                 ip_hi = min(P.bp + (int)floorf(xs + P.wp + wid), ip_hi);
@@ -717,10 +731,14 @@ __device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S,
             const int mg1 = M1 + gm1, mg2 = M2 + gm2;
             if (inner && ip_lo <= ip_hi && ip_hi - ip_lo < 8) {
                 const int4 rec = make_int4(S.f, R | (1 << 4) | ((ip_hi - ip_lo) << 5) | (ip_lo << 8), mg1, mg2);
+#if VF_SMALL_DIRECT
+                stage_put(c, s_rec, atomicAdd(s_n, 1), rec);  // CTA stage slot (shared atomic)
+#else
                 if (nr == 0) r0 = rec;
                 else if (nr == 1) r1 = rec;
                 else line_store(c, atomicAdd(c.n_lines, 1), rec);  // rare: > 2 lines
                 nr = min(nr + 1, 2);
+#endif
                 continue;
             }
             // margin band / ill-conditioned / long range: exact path later
@@ -751,7 +769,7 @@ __device__ __forceinline__ void small_flush(const LinkCtx &c, int4 *s_rec, int *
     }
 }
 
-__global__ void __launch_bounds__(256, VF_SMALL_MINB)
+__global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
     k_links_small(LinkCtx c, int widen, int64_t F, float small_ext, int32_t *__restrict__ big,
                   int32_t *__restrict__ n_big) {
     __shared__ int4 s_rec[kLineStage];
@@ -801,6 +819,7 @@ __global__ void __launch_bounds__(256, VF_SMALL_MINB)
             }
         }
         S.epsL = (float)(c.eps * c.inv_dx);
+        S.dthr = (float)(2.0 * c.eps_par * 1.7320508075688772) + 1e-5f;
         S.ff9 = 4e-6f * (extL + 2.0f);
         // the 13 pairs in three classes of the axis p of their first nonzero
         // component (c_p = +1): p = x: c = (1, s1, s2), all 9 sign pairs;
@@ -820,8 +839,10 @@ __global__ void __launch_bounds__(256, VF_SMALL_MINB)
                 const int R = (int)((0x271893a405b6cull >> (4 * idx)) & 15);
                 int4 r0 = make_int4(0, 0, 0, 0), r1 = r0;
                 int nr = 0;
-                small_pair(c, S, P, small, R, s1, s2, r0, r1, nr);
+                small_pair(c, S, P, small, R, s1, s2, r0, r1, nr, s_rec, &s_n);
+#if !VF_SMALL_DIRECT
                 small_flush(c, s_rec, &s_n, lane, r0, r1, nr);
+#endif
             }
         }
     }
@@ -1041,8 +1062,8 @@ int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *w
     // retire quickly, so the higher-priority level pipeline takes SMs
     // between them.
     int32_t *n_big = c.n_lines + 2;
-    const int64_t gs = (F + 255) / 256;
-    k_links_small<<<(unsigned)gs, 256, 0, st>>>(c, widen, F, g_small_ext, big, n_big);
+    const int64_t gs = (F + VF_SMALL_THREADS - 1) / VF_SMALL_THREADS;
+    k_links_small<<<(unsigned)gs, VF_SMALL_THREADS, 0, st>>>(c, widen, F, g_small_ext, big, n_big);
     if ((rc = check_launch("k_links_small"))) return rc;
     int64_t g2 = (F + 32 * kLinkWarps - 1) / (32 * kLinkWarps);
     if (g2 > 4 * (int64_t)max_ctas(VF_LINK_MINB)) g2 = 4 * (int64_t)max_ctas(VF_LINK_MINB);
