@@ -108,6 +108,15 @@ typedef struct {
 } vf_bins;
 
 int         vf_abi_version(void);
+/* Per-device context: selects `device`, creates its side
+ * streams (bins pipeline, cut-link enumeration) and keeps the caller's
+ * ncclComm_t (may be NULL; the library issues no NCCL calls itself -- the
+ * multi-GPU flag exchanges are the caller's all-reduces between the sharded
+ * stage calls).  Returns NULL on error (vf_last_error).  Without a context
+ * the streams are created on first use on the current device. */
+void       *vf_ctx_create(int device, void *nccl_comm);
+int         vf_ctx_destroy(void *ctx);
+int         vf_ctx_device(const void *ctx);
 const char *vf_last_error(void);
 int         vf_device_info(int *sm_count, int *cc_major, int *cc_minor);
 

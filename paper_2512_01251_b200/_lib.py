@@ -53,6 +53,9 @@ _BP = C.POINTER(VfBins)
 
 _SIGS = {
     "vf_abi_version": (_I32, []),
+    "vf_ctx_create": (_P, [_I32, _P]),
+    "vf_ctx_destroy": (_I32, [_P]),
+    "vf_ctx_device": (_I32, [_P]),
     "vf_last_error": (C.c_char_p, []),
     "vf_device_info": (_I32, [C.POINTER(C.c_int)] * 3),
     "vf_pack_faces": (_I32, [_P, _P, _I64, _P, _P]),

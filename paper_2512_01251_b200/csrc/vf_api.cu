@@ -8,6 +8,8 @@
 #include <atomic>
 #include <mutex>
 
+#include <new>
+
 #include "vf_common.cuh"
 #include "vf_internal.h"
 #include "vf_scan.cuh"
@@ -401,6 +403,55 @@ static int side_stream(SideStream **out) {
     *out = &s;
     return VF_OK;
 }
+
+// Per-device context (SURVEY.md §8b vf_ctx_create): selects the device,
+// creates its side streams / events (otherwise created on first use) and
+// records the caller's NCCL communicator.  The library never calls NCCL
+// itself: the multi-GPU exchanges are flag all-reduces issued by the caller
+// (parallel.py over torch.distributed) between the sharded stage calls; the
+// handle is carried for callers that keep it with the device state.
+struct vf_ctx_s {
+    int device;
+    void *nccl_comm;
+};
+
+extern "C" void *vf_ctx_create(int device, void *nccl_comm) {
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        set_cuda_error(e, "vf_ctx_create");
+        return nullptr;
+    }
+    SideStream *side = nullptr;
+    if (side_stream(&side) != VF_OK) return nullptr;
+    vf_ctx_s *c = new (std::nothrow) vf_ctx_s{device, nccl_comm};
+    if (!c) set_error(VF_EARG, "vf_ctx_create: out of host memory");
+    return c;
+}
+
+extern "C" int vf_ctx_destroy(void *ctx) {
+    if (!ctx) return set_error(VF_EARG, "vf_ctx_destroy: null context");
+    vf_ctx_s *c = static_cast<vf_ctx_s *>(ctx);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(c->device);
+    SideStream &s = g_side[c->device & 63];
+    cudaError_t e = cudaSuccess;
+    if (s.st) {
+        e = cudaStreamSynchronize(s.st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s.st3);
+        cudaEvent_t evs[] = {s.fork, s.bins[0], s.bins[1], s.vox[0], s.vox[1], s.join, s.join3};
+        for (cudaEvent_t ev : evs)
+            if (ev) cudaEventDestroy(ev);
+        cudaStreamDestroy(s.st);
+        cudaStreamDestroy(s.st3);
+        s = SideStream();
+    }
+    cudaSetDevice(cur);
+    delete c;
+    return e == cudaSuccess ? VF_OK : set_cuda_error(e, "vf_ctx_destroy");
+}
+
+extern "C" int vf_ctx_device(const void *ctx) { return ctx ? static_cast<const vf_ctx_s *>(ctx)->device : -1; }
 
 // wait for the side streams of this device (the cut-link enumeration of a
 // phase 1 that was not followed by phase 2 -- the LUT-sizing run, an error --

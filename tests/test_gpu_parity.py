@@ -502,3 +502,16 @@ def test_embed_c4_flagship(O):
     """C4 (7,200,000-face torus, L_max=5: the north-star mesh) against the
     oracle, end to end -- also exercises the eager (>1M faces) launch path."""
     _embed_compare(O, make_torus(3000, 1200), EmbedConfig(n_x=64, l_max=5))
+
+
+def test_ctx_create_destroy(O, torus):
+    """vf_ctx_create / vf_ctx_destroy: the context owns the
+    device's side streams; an embed after destroy recreates them."""
+    from paper_2512_01251_b200 import _lib
+    lib = _lib.require_cuda()
+    ctx = lib.vf_ctx_create(0, None)
+    assert ctx and lib.vf_ctx_device(ctx) == 0
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    _embed_compare(O, torus, cfg)
+    assert lib.vf_ctx_destroy(ctx) == 0
+    _embed_compare(O, torus, cfg)
