@@ -492,6 +492,20 @@ def test_embed_config_edges(O, case):
     _embed_compare(O, mesh, cfg, use_filter=cfg.use_filter)
 
 
+@pytest.mark.parametrize("case", ["nx48_nonpow2", "domain_2x1x1", "eps0", "open_patch"])
+def test_embed_config_edges_small_path(O, case):
+    """The same edge configurations with every face through the thread-per-
+    face cut-link enumeration (non-power-of-two dx, non-cubic domain, no
+    fast path, faces leaving the domain)."""
+    from paper_2512_01251_b200 import _lib
+    lib = _lib.require_cuda()
+    old = lib.vf_set_link_small_ext(1e9)
+    try:
+        test_embed_config_edges(O, case)
+    finally:
+        lib.vf_set_link_small_ext(old)
+
+
 def test_embed_c2_bench_config(O):
     """The bench workload itself (C2: 112,000-face torus, N_x=64, L_max=4)
     against the oracle, end to end."""
