@@ -38,6 +38,9 @@ struct VoxFace {  // shared-memory face record (128 B): what the row loop reads
 
 constexpr int kVoxWarps = 4;
 
+#ifndef VF_VOX_COMPACT
+#define VF_VOX_COMPACT 1
+#endif
 #ifndef VF_VOX_MINB
 #define VF_VOX_MINB 6
 #endif
@@ -47,6 +50,14 @@ __global__ void __launch_bounds__(kVoxWarps * 32, VF_VOX_MINB)
                const int32_t *__restrict__ offsets, const int32_t *__restrict__ d_total,
                const int32_t *__restrict__ face_ids, const double *__restrict__ faces) {
     __shared__ VoxFace s_face[kVoxWarps][32];
+#if VF_VOX_COMPACT
+    // per block: the (row, face) pairs whose row pierces the face, and per
+    // (row, cell) slot the best (|d|, face id) and its mask value
+    __shared__ uint16_t s_hit[kVoxWarps][16 * 32];
+    __shared__ unsigned long long s_ad[kVoxWarps][64], s_fad[kVoxWarps][64];  // best |d|; |d| of s_fid
+    __shared__ int32_t s_fid[kVoxWarps][64];
+    __shared__ uint8_t s_hv[kVoxWarps][64];
+#endif
     const int64_t n_bins = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
     const int32_t total = *d_total;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -91,6 +102,103 @@ __global__ void __launch_bounds__(kVoxWarps * 32, VF_VOX_MINB)
         double x[4];
 #pragma unroll
         for (int I = 0; I < 4; ++I) x[I] = node_c(4 * co.x + I, dx);
+#if VF_VOX_COMPACT
+        // Two phases per batch of 32 faces: (1) lanes = (row, face parity)
+        // classify the (row, face) pairs and compact the piercing ones into a
+        // warp list; (2) the 4 cell distances of every listed pair run on
+        // full warps (one (pair, cell) per lane), each reduced into its
+        // (row, cell) slot by the A7 order (|d| then face id) with shared
+        // 64-bit atomicMin on the IEEE bits of |d| (>= 0: monotone) and then
+        // on the face id among equal |d|; the winner records SOLID / GUARD.
+        if (lane < 64 / 2) {
+            s_ad[wib][lane] = 0x7ff0000000000000ull;  // +inf
+            s_ad[wib][lane + 32] = 0x7ff0000000000000ull;
+            s_fad[wib][lane] = 0x7ff0000000000000ull;
+            s_fad[wib][lane + 32] = 0x7ff0000000000000ull;
+            s_fid[wib][lane] = 0x7fffffff;
+            s_fid[wib][lane + 32] = 0x7fffffff;
+        }
+        for (int base = 0; base < n_f; base += 32) {
+            const int cnt = min(32, n_f - base);
+            if (lane < cnt) {
+                const int64_t f = face_ids[off + base + lane];
+                double v[9], nn[3];
+                load_face(faces, f, v, nn);
+                VoxFace &vf_ = s_face[wib][lane];
+                vf_.fid = (int32_t)f;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    vf_.v1[d] = v[d];
+                    vf_.n[d] = nn[d];
+                }
+                vf_.yz[0] = fmin(fmin(v[1], v[4]), v[7]);
+                vf_.yz[1] = fmax(fmax(v[1], v[4]), v[7]);
+                vf_.yz[2] = fmin(fmin(v[2], v[5]), v[8]);
+                vf_.yz[3] = fmax(fmax(v[2], v[5]), v[8]);
+                row_class_init(vf_.rc, v, nn, fmin(fmin(v[0], v[3]), v[6]), fmax(fmax(v[0], v[3]), v[6]),
+                               dx, eps, lx);
+                vf_.skip = fabs(nn[0]) < li.eps_par;  // A7: no x distance
+            }
+            __syncwarp();
+            int nh = 0;
+            for (int q0 = 0; q0 < cnt; q0 += 2) {
+                const int q = q0 + half;
+                bool hit = false;
+                if (q < cnt) {
+                    const VoxFace &F = s_face[wib][q];
+                    if (!F.skip && !(F.yz[1] < my || My < F.yz[0] || F.yz[3] < mz || Mz < F.yz[2])) {
+                        const int cls = row_class(F.rc, (float)VF_DSUB(y, F.v1[1]), (float)VF_DSUB(z, F.v1[2]));
+                        hit = cls == 1 || (cls == 2 && row_sat_exact_f(faces, F.fid, y, z, eps, lx));
+                    }
+                }
+                const uint32_t m = __ballot_sync(0xffffffffu, hit);
+                if (hit) s_hit[wib][nh + __popc(m & ((1u << lane) - 1u))] = (uint16_t)(r | (q << 4));
+                nh += __popc(m);
+            }
+            __syncwarp();
+            for (int k0 = 0; k0 < 4 * nh; k0 += 32) {
+                const int k = k0 + lane;
+                bool act = k < 4 * nh;
+                int slot = 0, fid = 0;
+                unsigned long long adb = 0;
+                double nx = 0.0, d = 0.0;
+                if (act) {
+                    const uint32_t h = s_hit[wib][k >> 2];
+                    const int rr = h & 15, q = h >> 4, I = k & 3;
+                    const VoxFace &F = s_face[wib][q];
+                    const double yy = node_c(4 * co.y + (rr & 3), dx), zz = node_c(4 * co.z + (rr >> 2), dx);
+                    nx = F.n[0];
+                    d = VF_DDIV(plane_num(F.v1, F.n, x[I], yy, zz), nx);
+                    adb = (unsigned long long)__double_as_longlong(fabs(d));
+                    slot = 4 * rr + I;
+                    fid = F.fid;
+                    atomicMin(&s_ad[wib][slot], adb);
+                }
+                __syncwarp();
+                act = act && s_ad[wib][slot] == adb;
+                if (act && s_fad[wib][slot] != adb) s_fid[wib][slot] = 0x7fffffff;  // a new best |d|
+                __syncwarp();
+                if (act) {
+                    s_fad[wib][slot] = adb;
+                    atomicMin(&s_fid[wib][slot], fid);
+                }
+                __syncwarp();
+                if (act && s_fid[wib][slot] == fid)
+                    s_hv[wib][slot] = (VF_DMUL(nx, d) > 0.0) ? VF_SOLID : VF_GUARD;
+                __syncwarp();
+            }
+            __syncwarp();
+        }
+        uint32_t hit = 0, bh = 0;
+        if (!half) {
+#pragma unroll
+            for (int I = 0; I < 4; ++I)
+                if (s_ad[wib][4 * r + I] != 0x7ff0000000000000ull) {
+                    hit |= 1u << I;
+                    bh |= (uint32_t)s_hv[wib][4 * r + I] << (8 * I);
+                }
+        }
+#else
         double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
         int bp[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
         uint32_t bh = 0;  // 4 x 8-bit masks, the row's new values
@@ -157,6 +265,7 @@ __global__ void __launch_bounds__(kVoxWarps * 32, VF_VOX_MINB)
             }
             if (bd[I] < INFINITY) hit |= 1u << I;
         }
+#endif
         const bool any = __any_sync(0xffffffffu, hit != 0);
         if (any && !half) {  // eta == 0 -> no write (Alg. 3 l.648)
             uint32_t *w = masks32 + b * 16 + r;
