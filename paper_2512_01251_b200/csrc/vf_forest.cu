@@ -256,6 +256,10 @@ __global__ void __launch_bounds__(256)
     __shared__ uint32_t s_missing[kAdaptBatch];
     __shared__ int4 s_pc[kAdaptBatch / 8];
     __shared__ int32_t s_P[kAdaptBatch / 8];
+    // the batch parents' 27 neighbours with their first child / flags, loaded
+    // once (one round of dependent loads) instead of per (child, slot)
+    __shared__ int32_t s_nb[kAdaptBatch / 8][27], s_ch[kAdaptBatch / 8][27];
+    __shared__ uint8_t s_fl[kAdaptBatch / 8][27];
     const int64_t e = level_start[L + 1];
     const int64_t nc = 8 * (int64_t)(*n_marked);
     for (int64_t c0 = (int64_t)blockIdx.x * kAdaptBatch; c0 < nc; c0 += (int64_t)gridDim.x * kAdaptBatch) {
@@ -267,11 +271,21 @@ __global__ void __launch_bounds__(256)
             s_pc[threadIdx.x] = reinterpret_cast<const int4 *>(coords)[P];
         }
         __syncthreads();
+        for (int it = threadIdx.x; it < ((nb + 7) >> 3) * 27; it += blockDim.x) {
+            const int p = it / 27, q = it - 27 * p;
+            const int32_t P = s_P[p];
+            const int32_t Pn = (q == 0) ? P : nbr[27 * (int64_t)P + q];
+            s_nb[p][q] = Pn;
+            if (Pn >= 0) {
+                s_ch[p][q] = child[Pn];
+                s_fl[p][q] = bflags[Pn];
+            }
+        }
+        __syncthreads();
         for (int it = threadIdx.x; it < nb * 27; it += blockDim.x) {
             const int lc = it / 27, q = it - 27 * lc;
             const int64_t id = e + c0 + lc;
             if (id >= capacity) continue;
-            const int32_t P = s_P[lc >> 3];
             const int4 pc = s_pc[lc >> 3];
             const int cc = lc & 7;
             const int ci = 2 * pc.x + (cc & 1), cj = 2 * pc.y + ((cc >> 1) & 1), ck = 2 * pc.z + (cc >> 2);
@@ -281,16 +295,16 @@ __global__ void __launch_bounds__(256)
                 v = VF_NB_OUTSIDE;
             } else {
                 const int qp = slot_of((ti >> 1) - pc.x, (tj >> 1) - pc.y, (tk >> 1) - pc.z);
-                const int32_t Pn = (qp == 0) ? P : nbr[27 * (int64_t)P + qp];
+                const int32_t Pn = s_nb[lc >> 3][qp];
                 if (Pn < 0) {  // marked parents are eligible: cannot happen
                     atomicMax(status, VF_EARG);
                     v = VF_NB_MISSING;
                 } else {
-                    const int32_t ch = child[Pn];
+                    const int32_t ch = s_ch[lc >> 3][qp];
                     if (ch >= 0)
                         v = ch + (ti & 1) + 2 * (tj & 1) + 4 * (tk & 1);
                     else
-                        v = (bflags[Pn] & VF_BF_SOLID) ? VF_NB_SOLID_NBR : VF_NB_MISSING;
+                        v = (s_fl[lc >> 3][qp] & VF_BF_SOLID) ? VF_NB_SOLID_NBR : VF_NB_MISSING;
                 }
             }
             nbr[27 * id + q] = v;
