@@ -243,6 +243,9 @@ __device__ __forceinline__ uint32_t octant_bits(uint32_t bits, int) {
 // contiguous) are written coalesced; the per-child MISSING/SOLID_NBR
 // direction bits are OR-ed in shared memory; then one thread per child writes
 // coords / flags / the A14 ghost-layer cell masks (16 B stores, coalesced).
+#ifndef VF_ADAPT_THREAD
+#define VF_ADAPT_THREAD 1
+#endif
 constexpr int kAdaptBatch = 64;
 
 __global__ void __launch_bounds__(256)
@@ -350,6 +353,113 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Thread per child (256 children = 32 parents per CTA batch): the 27 slots
+// are unrolled, so every D3Q27 component is a compile-time constant and the
+// parent-side slot of a target reduces to two adds and a shift per axis;
+// the child's nbr row is built in shared memory (row stride 27 words: no
+// bank conflicts) and copied out coalesced, nbr_child rows are -1 stores.
+// Same values as k_adapt_children, slot for slot.
+constexpr int kAdaptTBatch = 256;
+
+__global__ void __launch_bounds__(kAdaptTBatch)
+    k_adapt_children_t(int L, int32_t capacity, int nbx1, int nby1, int nbz1,
+                       const int32_t *__restrict__ level_start, const int32_t *__restrict__ n_marked,
+                       const int32_t *__restrict__ parents, int32_t *__restrict__ coords,
+                       int32_t *__restrict__ nbr, int32_t *__restrict__ nbr_child,
+                       int32_t *__restrict__ child, uint8_t *__restrict__ bflags,
+                       uint8_t *__restrict__ masks, int32_t *__restrict__ status,
+                       uint64_t *__restrict__ solid64) {
+    __shared__ int32_t s_row[kAdaptTBatch * 27];
+    __shared__ int4 s_pc[kAdaptTBatch / 8];
+    __shared__ int32_t s_nb[kAdaptTBatch / 8][27], s_ch[kAdaptTBatch / 8][27];
+    __shared__ uint8_t s_fl[kAdaptTBatch / 8][27];
+    const int64_t e = level_start[L + 1];
+    const int64_t nc = 8 * (int64_t)(*n_marked);
+    const int t = threadIdx.x;
+    for (int64_t c0 = (int64_t)blockIdx.x * kAdaptTBatch; c0 < nc; c0 += (int64_t)gridDim.x * kAdaptTBatch) {
+        const int nb = (int)min((int64_t)kAdaptTBatch, nc - c0);
+        const int np = (nb + 7) >> 3;
+        if (t < np) s_pc[t] = reinterpret_cast<const int4 *>(coords)[parents[(c0 >> 3) + t]];
+        for (int it = t; it < np * 27; it += blockDim.x) {
+            const int p = it / 27, q = it - 27 * p;
+            const int32_t P = parents[(c0 >> 3) + p];
+            const int32_t Pn = (q == 0) ? P : nbr[27 * (int64_t)P + q];
+            s_nb[p][q] = Pn;
+            if (Pn >= 0) {
+                s_ch[p][q] = child[Pn];
+                s_fl[p][q] = bflags[Pn];
+            }
+        }
+        __syncthreads();
+        const int64_t id = e + c0 + t;
+        if (t < nb && id < capacity) {
+            const int p = t >> 3, cc = t & 7;
+            const int4 pc = s_pc[p];
+            const int ox = cc & 1, oy = (cc >> 1) & 1, oz = cc >> 2;
+            const int ci = 2 * pc.x + ox, cj = 2 * pc.y + oy, ck = 2 * pc.z + oz;
+            uint32_t missing = 0;
+#pragma unroll
+            for (int q = 0; q < 27; ++q) {
+                const int cx = c27(q, 0), cy = c27(q, 1), cz = c27(q, 2);
+                const int ti = ci + cx, tj = cj + cy, tk = ck + cz;
+                int32_t v;
+                if (ti < 0 || tj < 0 || tk < 0 || ti >= nbx1 || tj >= nby1 || tk >= nbz1) {
+                    v = VF_NB_OUTSIDE;
+                } else {
+                    // parent-side direction: (o + c) >> 1 per axis (floor)
+                    const int qp = slot_of((ox + cx) >> 1, (oy + cy) >> 1, (oz + cz) >> 1);
+                    const int32_t Pn = s_nb[p][qp];
+                    if (Pn < 0) {  // marked parents are eligible: cannot happen
+                        atomicMax(status, VF_EARG);
+                        v = VF_NB_MISSING;
+                    } else {
+                        const int32_t ch = s_ch[p][qp];
+                        if (ch >= 0)
+                            v = ch + (ti & 1) + 2 * (tj & 1) + 4 * (tk & 1);
+                        else
+                            v = (s_fl[p][qp] & VF_BF_SOLID) ? VF_NB_SOLID_NBR : VF_NB_MISSING;
+                    }
+                }
+                s_row[27 * t + q] = v;
+                if (v == VF_NB_MISSING || v == VF_NB_SOLID_NBR) missing |= 1u << dir_code(cx, cy, cz);
+            }
+            reinterpret_cast<int4 *>(coords)[id] = make_int4(ci, cj, ck, L + 1);
+            child[id] = -1;
+            bflags[id] = 0;
+            solid64[id] = 0;
+            // A14 ghost layer (as k_adapt_children): 8 octant bits decide all 64 cells
+            const uint32_t g8 = octant_bits(missing, 2);
+            uint4 *mp = reinterpret_cast<uint4 *>(masks + 64 * id);
+#pragma unroll
+            for (int part = 0; part < 4; ++part) {
+                uint32_t w[4];
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr) {
+                    const int r = 4 * part + rr;
+                    const int J = r & 3, K = r >> 2;
+                    uint32_t x = 0;
+#pragma unroll
+                    for (int I = 0; I < 4; ++I) {
+                        const int o = (I >= 2) | ((J >= 2) << 1) | ((K >= 2) << 2);
+                        x |= (uint32_t)((g8 >> o & 1u) ? VF_GHOST : VF_FLUID) << (8 * I);
+                    }
+                    w[rr] = x;
+                }
+                mp[part] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        }
+        __syncthreads();
+        // coalesced copy-out of the batch's nbr rows; nbr_child rows = -1
+        const int64_t nw = (int64_t)min((int64_t)nb, (int64_t)capacity - (e + c0));
+        const int64_t base = 27 * (e + c0);
+        for (int64_t i = t; i < 27 * nw; i += blockDim.x) {
+            nbr[base + i] = s_row[i];
+            nbr_child[base + i] = -1;
+        }
+        __syncthreads();
+    }
+}
+
 // level-L neighbour-child links + interface layer of refined blocks (A14).
 // (block, slot) pairs spread over a CTA (coalesced nbr_child rows), the
 // per-block "existing unrefined neighbour" bits OR-ed in shared memory, then
@@ -421,7 +531,11 @@ int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_byte
                                     st, AdaptFinish{L, g->capacity, g->d_level_start, g->d_status});
     if (ce != cudaSuccess) return set_cuda_error(ce, "adapt scan");
     int rc;
+#if VF_ADAPT_THREAD
+    k_adapt_children_t<<<max_ctas(4), kAdaptTBatch, 0, st>>>(
+#else
     k_adapt_children<<<max_ctas(8), 256, 0, st>>>(
+#endif
         L, g->capacity, cfg.nb[0] << (L + 1), cfg.nb[1] << (L + 1), cfg.nb[2] << (L + 1),
         g->d_level_start, scalars + 1, parents, g->d_coords, g->d_nbr, g->d_nbr_child, g->d_child,
         g->d_bflags, g->d_masks, g->d_status, g->d_solid64);
