@@ -142,13 +142,30 @@ __global__ void __launch_bounds__(256, VF_IND_MINB)
         uint32_t bits = 0;
         if (!(fabs(n[0]) < ls.li[0].eps_par)) {
             const double xlo = fmin(fmin(v[0], v[3]), v[6]), xhi = fmax(fmax(v[0], v[3]), v[6]);
+            // level-independent part of the row classifier (row_class_init):
+            // the yz edge functions, their lengths, orientation, fast-accept
+            // eligibility; per level only the margins change with dx
+            const float a1 = (float)(v[4] - v[1]), b1 = (float)(v[5] - v[2]);
+            const float a2 = (float)(v[7] - v[1]), b2 = (float)(v[8] - v[2]);
+            const float cr = a1 * b2 - b1 * a2;
+            const float ext = fmaxf(fmaxf(fabsf(a1), fabsf(b1)), fmaxf(fabsf(a2), fabsf(b2)));
+            const float e1a = a2 - a1, e1b = b2 - b1;
+            const float l0 = sqrtf(a1 * a1 + b1 * b1), l1 = sqrtf(e1a * e1a + e1b * e1b), l2 = sqrtf(a2 * a2 + b2 * b2);
+            const float sg = cr >= 0.0f ? 1.0f : -1.0f;
+            const double tx = 1e-6 * ls.li[0].len[0];
+            const bool acc = fabs(n[0]) >= 1e-3 && xlo > tx && xhi < ls.li[0].len[0] - tx && cr != 0.0f;
             for (int L = 0; L < ls.n; ++L) {
                 const LevelInfo &li = ls.li[L];
                 int ja, jb, ka, kb;
                 if (!face_rows(v, li, ls.inv_dx[L], ls.widen[L], ja, jb, ka, kb)) continue;
                 const double dx = li.dx, eps = li.eps;
                 RowClass rc;
-                row_class_init(rc, v, n, xlo, xhi, dx, eps, li.len[0]);
+                {  // = row_class_init(rc, v, n, xlo, xhi, dx, eps, li.len[0])
+                    const float tol = 1e-5f * (ext + (float)dx) + 6.0f * (float)eps;
+                    const float ab = 4e-6f * (ext + (float)dx) * (ext + (float)dx);
+                    rc.yz = make_float4(a1, b1, a2, b2);
+                    rc.tol = make_float4(tol * l0 + ab, tol * l1 + ab, tol * l2 + ab, acc ? sg : 2.0f * sg);
+                }
                 bool hit = false;
                 for (int k = ka; k <= kb && !hit; ++k) {
                     const double z = node_c(k, dx);
