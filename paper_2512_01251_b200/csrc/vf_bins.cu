@@ -154,10 +154,29 @@ __global__ void __launch_bounds__(256, VF_IND_MINB)
             const float sg = cr >= 0.0f ? 1.0f : -1.0f;
             const double tx = 1e-6 * ls.li[0].len[0];
             const bool acc = fabs(n[0]) >= 1e-3 && xlo > tx && xhi < ls.li[0].len[0] - tx && cr != 0.0f;
+            // candidate row ranges in FP32 from the face's y/z extent in
+            // finest-level cells (power-of-two dx: exact level scaling; the
+            // 0.01-cell padding covers the FP32 rounding, extra rows are
+            // rejected by the row test itself -- same bits as face_rows)
+            const int Lf = ls.n - 1;
+            const double invf = ls.inv_dx[Lf], eps0 = ls.li[0].eps;
+            const float ya = (float)((fmin(fmin(v[1], v[4]), v[7]) - eps0) * invf);
+            const float yb = (float)((fmax(fmax(v[1], v[4]), v[7]) + eps0) * invf);
+            const float za = (float)((fmin(fmin(v[2], v[5]), v[8]) - eps0) * invf);
+            const float zb = (float)((fmax(fmax(v[2], v[5]), v[8]) + eps0) * invf);
             for (int L = 0; L < ls.n; ++L) {
                 const LevelInfo &li = ls.li[L];
                 int ja, jb, ka, kb;
-                if (!face_rows(v, li, ls.inv_dx[L], ls.widen[L], ja, jb, ka, kb)) continue;
+                if (ls.widen[L] == 0 && li.eps == eps0 && li.shard_count <= 1) {
+                    const float sc = ldexpf(1.0f, L - Lf);
+                    ja = max((int)ceilf(ya * sc - 0.5f - 0.01f), 0);
+                    jb = min((int)floorf(yb * sc - 0.5f + 0.01f), li.cells[1] - 1);
+                    ka = max((int)ceilf(za * sc - 0.5f - 0.01f), 0);
+                    kb = min((int)floorf(zb * sc - 0.5f + 0.01f), li.cells[2] - 1);
+                    if (ja > jb || ka > kb) continue;
+                } else if (!face_rows(v, li, ls.inv_dx[L], ls.widen[L], ja, jb, ka, kb)) {
+                    continue;
+                }
                 const double dx = li.dx, eps = li.eps;
                 RowClass rc;
                 {  // = row_class_init(rc, v, n, xlo, xhi, dx, eps, li.len[0])
