@@ -52,9 +52,12 @@ __device__ __forceinline__ int32_t cell_at(const int32_t *__restrict__ nbr, int3
 // Bouzidi linear IBB with q_w from the LUT) and the momentum exchange, and
 // overwrites those cells (same f_in, so the two passes commute).
 constexpr int kLbmWarps = 8;
+#ifndef VF_LBM_MINB
+#define VF_LBM_MINB 3
+#endif
 
 template <bool WALLS>
-__global__ void __launch_bounds__(kLbmWarps * 32, 3)
+__global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_MINB)
     k_lbm_cells(int32_t s, int32_t e, int cells_x, const int32_t *__restrict__ coords,
                 const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
                 const uint64_t *__restrict__ solid64, const int32_t *__restrict__ cmap,
@@ -531,7 +534,7 @@ int vf_lbm_step(const vf_config *cfg, const vf_grid *g, int level, int32_t s, in
     int32_t *n_wall = d_scratch, *wall_list = d_scratch + 1;
     cudaMemsetAsync(n_wall, 0, sizeof(int32_t), st);
     int64_t grid = ((int64_t)(e - s) + kLbmWarps - 1) / kLbmWarps;
-    if (grid > max_ctas(3)) grid = max_ctas(3);
+    if (grid > max_ctas(VF_LBM_MINB)) grid = max_ctas(VF_LBM_MINB);
     k_lbm_cells<false><<<(int)grid, kLbmWarps * 32, 0, st>>>(
         s, e, cells_x, g->d_coords, g->d_nbr, g->d_masks, g->d_solid64, cmap, lengths, fin, fout, *flow,
         wall_list, n_wall, nullptr);
