@@ -201,24 +201,24 @@ __constant__ double c_cn[13] = {1.0, 1.0, 1.0, 1.4142135623730951, 1.41421356237
 // zero product, which cannot change a nonzero sum (a zero den is rejected)
 __device__ __forceinline__ double cmul(int ck, double nk) { return ck == 0 ? 0.0 : (ck > 0 ? nk : -nk); }
 
-// margin length |e| (approximate rsqrt: the margins carry a 10x safety factor)
-__device__ __forceinline__ float mlen(float a, float b) {
-    const float x = a * a + b * b;
-    return x > 0.0f ? x * rsqrtf(x) * 1.0001f : 0.0f;
-}
-
 // state of (lane's face, pair R); returns the number of lattice rows of the
 // projected bounding box (0: no link of this face in this pair)
+template <int MODE>
 __device__ __forceinline__ int link_dir_setup(LinkDir &D, const LinkCtx &c, const double *v,
                                               const float *ff, const short *lohi, int R, int p,
                                               int q1, int q2, int s1, int s2) {
     const double *n = v + 3;
     const float *nf = ff, *V1 = ff + 3, *V2 = ff + 6;
     const int cx = c_rep[R][0], cy = c_rep[R][1], cz = c_rep[R][2];
+    const float dn = (float)cx * nf[0] + (float)cy * nf[1] + (float)cz * nf[2];  // c.n in FP32
     // exact den / EPS_PARALLEL (link_candidate): a face parallel to c has no
-    // link in this direction pair at all
-    const double den = VF_DADD(VF_DADD(cmul(cx, n[0]), cmul(cy, n[1])), cmul(cz, n[2]));
-    if (fabs(den) < VF_DMUL(c.eps_par, c_cn[R])) return 0;
+    // link in this direction pair at all.  The enumeration (MODE 2) never
+    // uses den itself: it decides exactly only when the FP32 c.n is near 0.
+    double den = 0.0;
+    if (MODE != 2 || !(fabsf(dn) > (float)(2.0 * c.eps_par * 1.7320508075688772) + 1e-5f)) {
+        den = VF_DADD(VF_DADD(cmul(cx, n[0]), cmul(cy, n[1])), cmul(cz, n[2]));
+        if (fabs(den) < VF_DMUL(c.eps_par, c_cn[R])) return 0;
+    }
     const double dx = c.dx;
     const float dxf = (float)dx;
     const float V1p = pick3(p, V1[0], V1[1], V1[2]), V2p = pick3(p, V2[0], V2[1], V2[2]);
@@ -252,11 +252,12 @@ __device__ __forceinline__ int link_dir_setup(LinkDir &D, const LinkCtx &c, cons
     const float cr = P1a * P2b - P1b * P2a;
     const float ab = 4e-6f * (ext + dxf) * (ext + dxf);
     D.P1a = P1a; D.P1b = P1b; D.P2a = P2a; D.P2b = P2b;
-    D.t0 = tol * mlen(P1a, P1b) + ab;
-    D.t1 = tol * mlen(P2a - P1a, P2b - P1b) + ab;
-    D.t2 = tol * mlen(P2a, P2b) + ab;
+    // edge margins with the L1 length |a| + |b| >= |e| (no square root; a
+    // larger margin only moves lines into the exactly-decided band)
+    D.t0 = tol * (fabsf(P1a) + fabsf(P1b)) * 1.0001f + ab;
+    D.t1 = tol * (fabsf(P2a - P1a) + fabsf(P2b - P1b)) * 1.0001f + ab;
+    D.t2 = tol * (fabsf(P2a) + fabsf(P2b)) * 1.0001f + ab;
     D.sg = cr >= 0.0f ? 1.0f : -1.0f;
-    const float dn = (float)cx * nf[0] + (float)cy * nf[1] + (float)cz * nf[2];
     const bool steep = fabsf(dn) >= 1e-3f;
     D.off1 = off1; D.off2 = off2; D.vp = vp; D.den = den;
     D.nq1 = pick3(q1, nf[0], nf[1], nf[2]);
@@ -550,7 +551,7 @@ __global__ void __launch_bounds__(kLinkWarps * 32, MODE == 1 ? 1 : VF_LINK_MINB)
             if (active) {
                 LinkDir D;
                 D.f = f;
-                cnt = link_dir_setup(D, c, W.fv[lane], W.ff[lane], W.lohi[lane], R, p, q1, q2, s1, s2);
+                cnt = link_dir_setup<MODE>(D, c, W.fv[lane], W.ff[lane], W.lohi[lane], R, p, q1, q2, s1, s2);
                 if (cnt) W.d[lane] = D;
             }
             // warp exclusive prefix of the row counts
