@@ -237,128 +237,14 @@ __device__ __forceinline__ uint32_t octant_bits(uint32_t bits, int) {
     return g;
 }
 
-// Children of the level's marked parents, CTA-cooperative: a CTA takes 64
-// consecutive children (8 parents), the (child, slot) pairs of the batch are
-// spread over the threads so the 27-int neighbour rows of the batch (6.9 KB,
-// contiguous) are written coalesced; the per-child MISSING/SOLID_NBR
-// direction bits are OR-ed in shared memory; then one thread per child writes
-// coords / flags / the A14 ghost-layer cell masks (16 B stores, coalesced).
-#ifndef VF_ADAPT_THREAD
-#define VF_ADAPT_THREAD 1
-#endif
-constexpr int kAdaptBatch = 64;
-
-__global__ void __launch_bounds__(256)
-    k_adapt_children(int L, int32_t capacity, int nbx1, int nby1, int nbz1,
-                     const int32_t *__restrict__ level_start, const int32_t *__restrict__ n_marked,
-                     const int32_t *__restrict__ parents, int32_t *__restrict__ coords,
-                     int32_t *__restrict__ nbr, int32_t *__restrict__ nbr_child,
-                     int32_t *__restrict__ child, uint8_t *__restrict__ bflags,
-                     uint8_t *__restrict__ masks, int32_t *__restrict__ status,
-                     uint64_t *__restrict__ solid64) {
-    __shared__ uint32_t s_missing[kAdaptBatch];
-    __shared__ int4 s_pc[kAdaptBatch / 8];
-    __shared__ int32_t s_P[kAdaptBatch / 8];
-    // the batch parents' 27 neighbours with their first child / flags, loaded
-    // once (one round of dependent loads) instead of per (child, slot)
-    __shared__ int32_t s_nb[kAdaptBatch / 8][27], s_ch[kAdaptBatch / 8][27];
-    __shared__ uint8_t s_fl[kAdaptBatch / 8][27];
-    const int64_t e = level_start[L + 1];
-    const int64_t nc = 8 * (int64_t)(*n_marked);
-    for (int64_t c0 = (int64_t)blockIdx.x * kAdaptBatch; c0 < nc; c0 += (int64_t)gridDim.x * kAdaptBatch) {
-        const int nb = (int)min((int64_t)kAdaptBatch, nc - c0);
-        if (threadIdx.x < kAdaptBatch) s_missing[threadIdx.x] = 0;
-        if (threadIdx.x < kAdaptBatch / 8 && 8 * (int)threadIdx.x < nb) {
-            const int32_t P = parents[(c0 >> 3) + threadIdx.x];
-            s_P[threadIdx.x] = P;
-            s_pc[threadIdx.x] = reinterpret_cast<const int4 *>(coords)[P];
-        }
-        __syncthreads();
-        for (int it = threadIdx.x; it < ((nb + 7) >> 3) * 27; it += blockDim.x) {
-            const int p = it / 27, q = it - 27 * p;
-            const int32_t P = s_P[p];
-            const int32_t Pn = (q == 0) ? P : nbr[27 * (int64_t)P + q];
-            s_nb[p][q] = Pn;
-            if (Pn >= 0) {
-                s_ch[p][q] = child[Pn];
-                s_fl[p][q] = bflags[Pn];
-            }
-        }
-        __syncthreads();
-        for (int it = threadIdx.x; it < nb * 27; it += blockDim.x) {
-            const int lc = it / 27, q = it - 27 * lc;
-            const int64_t id = e + c0 + lc;
-            if (id >= capacity) continue;
-            const int4 pc = s_pc[lc >> 3];
-            const int cc = lc & 7;
-            const int ci = 2 * pc.x + (cc & 1), cj = 2 * pc.y + ((cc >> 1) & 1), ck = 2 * pc.z + (cc >> 2);
-            const int ti = ci + c27(q, 0), tj = cj + c27(q, 1), tk = ck + c27(q, 2);
-            int32_t v;
-            if (ti < 0 || tj < 0 || tk < 0 || ti >= nbx1 || tj >= nby1 || tk >= nbz1) {
-                v = VF_NB_OUTSIDE;
-            } else {
-                const int qp = slot_of((ti >> 1) - pc.x, (tj >> 1) - pc.y, (tk >> 1) - pc.z);
-                const int32_t Pn = s_nb[lc >> 3][qp];
-                if (Pn < 0) {  // marked parents are eligible: cannot happen
-                    atomicMax(status, VF_EARG);
-                    v = VF_NB_MISSING;
-                } else {
-                    const int32_t ch = s_ch[lc >> 3][qp];
-                    if (ch >= 0)
-                        v = ch + (ti & 1) + 2 * (tj & 1) + 4 * (tk & 1);
-                    else
-                        v = (s_fl[lc >> 3][qp] & VF_BF_SOLID) ? VF_NB_SOLID_NBR : VF_NB_MISSING;
-                }
-            }
-            nbr[27 * id + q] = v;
-            nbr_child[27 * id + q] = -1;
-            if (v == VF_NB_MISSING || v == VF_NB_SOLID_NBR)
-                atomicOr(&s_missing[lc], 1u << dir_code_of_slot(q));
-        }
-        __syncthreads();
-        // per child: metadata; masks as 4 x 16 B per child (4 threads per child)
-        for (int it = threadIdx.x; it < nb * 4; it += blockDim.x) {
-            const int lc = it >> 2, part = it & 3;
-            const int64_t id = e + c0 + lc;
-            if (id >= capacity) continue;
-            if (part == 0) {
-                const int4 pc = s_pc[lc >> 3];
-                const int cc = lc & 7;
-                reinterpret_cast<int4 *>(coords)[id] =
-                    make_int4(2 * pc.x + (cc & 1), 2 * pc.y + ((cc >> 1) & 1), 2 * pc.z + (cc >> 2), L + 1);
-                child[id] = -1;
-                bflags[id] = 0;
-                solid64[id] = 0;
-            }
-            // A14 ghost layer: a cell is within Chebyshev distance 2 (fine
-            // cells) of a missing neighbour block iff one of the 7 blocks
-            // towards its octant is missing, so 8 octant bits decide all 64 cells
-            const uint32_t g8 = octant_bits(s_missing[lc], 2);
-            uint32_t w[4];
-#pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
-                const int r = 4 * part + rr;
-                const int J = r & 3, K = r >> 2;
-                uint32_t x = 0;
-#pragma unroll
-                for (int I = 0; I < 4; ++I) {
-                    const int o = (I >= 2) | ((J >= 2) << 1) | ((K >= 2) << 2);
-                    x |= (uint32_t)((g8 >> o & 1u) ? VF_GHOST : VF_FLUID) << (8 * I);
-                }
-                w[rr] = x;
-            }
-            reinterpret_cast<uint4 *>(masks + 64 * id)[part] = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-        __syncthreads();
-    }
-}
-
 // Thread per child (256 children = 32 parents per CTA batch): the 27 slots
 // are unrolled, so every D3Q27 component is a compile-time constant and the
 // parent-side slot of a target reduces to two adds and a shift per axis;
 // the child's nbr row is built in shared memory (row stride 27 words: no
 // bank conflicts) and copied out coalesced, nbr_child rows are -1 stores.
-// Same values as k_adapt_children, slot for slot.
+// Children of the level's marked parents (A13, A14): coords, 27 neighbour
+// slots (child of the parent-side neighbour, or MISSING / SOLID_NBR /
+// OUTSIDE), nbr_child = -1, flags, and the ghost-layer cell masks.
 constexpr int kAdaptTBatch = 256;
 
 __global__ void __launch_bounds__(kAdaptTBatch)
@@ -427,7 +313,9 @@ __global__ void __launch_bounds__(kAdaptTBatch)
             child[id] = -1;
             bflags[id] = 0;
             solid64[id] = 0;
-            // A14 ghost layer (as k_adapt_children): 8 octant bits decide all 64 cells
+            // A14 ghost layer: a cell is within Chebyshev distance 2 (fine
+            // cells) of a missing neighbour block iff one of the 7 blocks
+            // towards its octant is missing, so 8 octant bits decide all 64 cells
             const uint32_t g8 = octant_bits(missing, 2);
             uint4 *mp = reinterpret_cast<uint4 *>(masks + 64 * id);
 #pragma unroll
@@ -531,11 +419,7 @@ int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_byte
                                     st, AdaptFinish{L, g->capacity, g->d_level_start, g->d_status});
     if (ce != cudaSuccess) return set_cuda_error(ce, "adapt scan");
     int rc;
-#if VF_ADAPT_THREAD
     k_adapt_children_t<<<max_ctas(4), kAdaptTBatch, 0, st>>>(
-#else
-    k_adapt_children<<<max_ctas(8), 256, 0, st>>>(
-#endif
         L, g->capacity, cfg.nb[0] << (L + 1), cfg.nb[1] << (L + 1), cfg.nb[2] << (L + 1),
         g->d_level_start, scalars + 1, parents, g->d_coords, g->d_nbr, g->d_nbr_child, g->d_child,
         g->d_bflags, g->d_masks, g->d_status, g->d_solid64);

@@ -597,9 +597,6 @@ __global__ void __launch_bounds__(kLinkWarps * 32, MODE == 1 ? 1 : VF_LINK_MINB)
 // classes remain conservative and the recorded lines, band candidates and
 // hence the LUT are identical.  Larger faces are appended to a list for the
 // warp-flattened kernel.
-#ifndef VF_SMALL_DIRECT
-#define VF_SMALL_DIRECT 1
-#endif
 #ifndef VF_SMALL_MINB
 #define VF_SMALL_MINB 4
 #endif
@@ -674,11 +671,10 @@ __device__ __forceinline__ void small_project(const LinkCtx &c, const SmallFace 
 
 // one (face, pair R = (class p, s1, s2)) of the thread-per-face enumeration:
 // the lattice points of the projected bounding box, their class, piercing
-// lines as records (<= 2 kept in r0 / r1 for the warp-aggregated write; more
-// go out directly) and the undecided ones node by node to the band list
+// lines as records (CTA stage slots) and the undecided ones node by node to
+// the band list
 __device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S, const SmallProj &P,
-                                           bool small, int R, int s1, int s2, int4 &r0, int4 &r1, int &nr,
-                                           int4 *s_rec, int *s_n) {
+                                           bool small, int R, int s1, int s2, int4 *s_rec, int *s_n) {
     // exact den / EPS_PARALLEL, as link_dir_setup: c = (1, s1, s2) over
     // (p, q1, q2) -- the same FP64 sum in the same order (a zero term is exact)
     if (!small) return;
@@ -732,14 +728,7 @@ __device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S,
             const int mg1 = M1 + gm1, mg2 = M2 + gm2;
             if (inner && ip_lo <= ip_hi && ip_hi - ip_lo < 8) {
                 const int4 rec = make_int4(S.f, R | (1 << 4) | ((ip_hi - ip_lo) << 5) | (ip_lo << 8), mg1, mg2);
-#if VF_SMALL_DIRECT
                 stage_put(c, s_rec, atomicAdd(s_n, 1), rec);  // CTA stage slot (shared atomic)
-#else
-                if (nr == 0) r0 = rec;
-                else if (nr == 1) r1 = rec;
-                else line_store(c, atomicAdd(c.n_lines, 1), rec);  // rare: > 2 lines
-                nr = min(nr + 1, 2);
-#endif
                 continue;
             }
             // margin band / ill-conditioned / long range: exact path later
@@ -752,21 +741,6 @@ __device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S,
                 link_slow<2>(c, S.f, -1, i, j, k, R);
             }
         }
-    }
-}
-
-// warp-aggregated staging of the (<= 2) lines per lane of one pair
-__device__ __forceinline__ void small_flush(const LinkCtx &c, int4 *s_rec, int *s_n, int lane, int4 r0,
-                                            int4 r1, int nr) {
-    const unsigned lt = (1u << lane) - 1u;
-    const unsigned b0 = __ballot_sync(0xffffffffu, nr & 1), b1 = __ballot_sync(0xffffffffu, nr & 2);
-    const int tot = __popc(b0) + 2 * __popc(b1);
-    if (tot) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(s_n, tot);
-        base = __shfl_sync(0xffffffffu, base, 0) + __popc(b0 & lt) + 2 * __popc(b1 & lt);
-        if (nr > 0) stage_put(c, s_rec, base, r0);
-        if (nr > 1) stage_put(c, s_rec, base + 1, r1);
     }
 }
 
@@ -838,12 +812,7 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
                 const int idx = cls == 0 ? t : (cls == 1 ? 9 + t : 12);
                 // R of (class, s1, s2) in lattice.py order, 4 bits each
                 const int R = (int)((0x271893a405b6cull >> (4 * idx)) & 15);
-                int4 r0 = make_int4(0, 0, 0, 0), r1 = r0;
-                int nr = 0;
-                small_pair(c, S, P, small, R, s1, s2, r0, r1, nr, s_rec, &s_n);
-#if !VF_SMALL_DIRECT
-                small_flush(c, s_rec, &s_n, lane, r0, r1, nr);
-#endif
+                small_pair(c, S, P, small, R, s1, s2, s_rec, &s_n);
             }
         }
     }

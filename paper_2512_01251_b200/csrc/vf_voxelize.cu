@@ -38,9 +38,6 @@ struct VoxFace {  // shared-memory face record (128 B): what the row loop reads
 
 constexpr int kVoxWarps = 4;
 
-#ifndef VF_VOX_COMPACT
-#define VF_VOX_COMPACT 1
-#endif
 #ifndef VF_VOX_MINB
 #define VF_VOX_MINB 6
 #endif
@@ -50,14 +47,12 @@ __global__ void __launch_bounds__(kVoxWarps * 32, VF_VOX_MINB)
                const int32_t *__restrict__ offsets, const int32_t *__restrict__ d_total,
                const int32_t *__restrict__ face_ids, const double *__restrict__ faces) {
     __shared__ VoxFace s_face[kVoxWarps][32];
-#if VF_VOX_COMPACT
     // per block: the (row, face) pairs whose row pierces the face, and per
     // (row, cell) slot the best (|d|, face id) and its mask value
     __shared__ uint16_t s_hit[kVoxWarps][16 * 32];
     __shared__ unsigned long long s_ad[kVoxWarps][64], s_fad[kVoxWarps][64];  // best |d|; |d| of s_fid
     __shared__ int32_t s_fid[kVoxWarps][64];
     __shared__ uint8_t s_hv[kVoxWarps][64];
-#endif
     const int64_t n_bins = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
     const int32_t total = *d_total;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -102,7 +97,6 @@ __global__ void __launch_bounds__(kVoxWarps * 32, VF_VOX_MINB)
         double x[4];
 #pragma unroll
         for (int I = 0; I < 4; ++I) x[I] = node_c(4 * co.x + I, dx);
-#if VF_VOX_COMPACT
         // Two phases per batch of 32 faces: (1) lanes = (row, face parity)
         // classify the (row, face) pairs and compact the piercing ones into a
         // warp list; (2) the 4 cell distances of every listed pair run on
@@ -198,74 +192,6 @@ __global__ void __launch_bounds__(kVoxWarps * 32, VF_VOX_MINB)
                     bh |= (uint32_t)s_hv[wib][4 * r + I] << (8 * I);
                 }
         }
-#else
-        double bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
-        int bp[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
-        uint32_t bh = 0;  // 4 x 8-bit masks, the row's new values
-
-        for (int base = 0; base < n_f; base += 32) {
-            const int cnt = min(32, n_f - base);
-            if (lane < cnt) {
-                const int64_t f = face_ids[off + base + lane];
-                double v[9], nn[3];
-                load_face(faces, f, v, nn);
-                VoxFace &vf_ = s_face[wib][lane];
-                vf_.fid = (int32_t)f;
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    vf_.v1[d] = v[d];
-                    vf_.n[d] = nn[d];
-                }
-                vf_.yz[0] = fmin(fmin(v[1], v[4]), v[7]);
-                vf_.yz[1] = fmax(fmax(v[1], v[4]), v[7]);
-                vf_.yz[2] = fmin(fmin(v[2], v[5]), v[8]);
-                vf_.yz[3] = fmax(fmax(v[2], v[5]), v[8]);
-                row_class_init(vf_.rc, v, nn, fmin(fmin(v[0], v[3]), v[6]), fmax(fmax(v[0], v[3]), v[6]),
-                               dx, eps, lx);
-                vf_.skip = fabs(nn[0]) < li.eps_par;  // A7: no x distance
-            }
-            __syncwarp();
-            for (int q = half; q < cnt; q += 2) {
-                const VoxFace &F = s_face[wib][q];
-                if (F.skip) continue;
-                // exact box-axis reject first (most pairs), then the FP32
-                // classifier; only undecided rows run the FP64 SAT
-                if (F.yz[1] < my || My < F.yz[0] || F.yz[3] < mz || Mz < F.yz[2]) continue;
-                const int cls = row_class(F.rc, (float)VF_DSUB(y, F.v1[1]), (float)VF_DSUB(z, F.v1[2]));
-                if (cls == 0) continue;
-                if (cls == 2 && !row_sat_exact_f(faces, F.fid, y, z, eps, lx)) continue;
-                const double nx = F.n[0];
-                const int fid = F.fid;
-#pragma unroll
-                for (int I = 0; I < 4; ++I) {
-                    const double d = VF_DDIV(plane_num(F.v1, F.n, x[I], y, z), nx);
-                    const double ad = fabs(d);
-                    // A7: smaller |d|, ties -> lower face id (bins need not be sorted)
-                    if (ad < bd[I] || (ad == bd[I] && fid < bp[I])) {
-                        bd[I] = ad;
-                        bp[I] = fid;
-                        const uint32_t hv = (VF_DMUL(nx, d) > 0.0) ? VF_SOLID : VF_GUARD;
-                        bh = (bh & ~(0xffu << (8 * I))) | (hv << (8 * I));
-                    }
-                }
-            }
-            __syncwarp();
-        }
-        // merge the two face parities of each row: smaller |d|, then lower face order
-        uint32_t hit = 0;
-#pragma unroll
-        for (int I = 0; I < 4; ++I) {
-            const double od = __shfl_xor_sync(0xffffffffu, bd[I], 16);
-            const int op = __shfl_xor_sync(0xffffffffu, bp[I], 16);
-            const uint32_t oh = __shfl_xor_sync(0xffffffffu, bh, 16);
-            if (od < bd[I] || (od == bd[I] && op < bp[I])) {
-                bd[I] = od;
-                bp[I] = op;
-                bh = (bh & ~(0xffu << (8 * I))) | (oh & (0xffu << (8 * I)));
-            }
-            if (bd[I] < INFINITY) hit |= 1u << I;
-        }
-#endif
         const bool any = __any_sync(0xffffffffu, hit != 0);
         if (any && !half) {  // eta == 0 -> no write (Alg. 3 l.648)
             uint32_t *w = masks32 + b * 16 + r;
