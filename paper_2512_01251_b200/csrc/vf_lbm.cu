@@ -273,6 +273,7 @@ __global__ void k_lbm_parents(int32_t n_blocks, const int32_t *__restrict__ chil
 // (x, then y, then z).  The interpolated populations go to ff and are then
 // rescaled in place by their owning lane.
 constexpr int kFillWarps = 8;
+constexpr int kFillQ = 3;  // populations staged per load round (27 = 9 x 3)
 
 __device__ __forceinline__ float axis_w(int ord, int k) {
     return ord == 3 ? c_w3[k] : (ord == 1 ? (k ? 0.25f : 0.75f) : 1.0f);
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(kFillWarps * 32)
                       const float *__restrict__ fnew, float theta, float alpha, int order,
                       float *__restrict__ ff) {
     __shared__ int32_t s_c[kFillWarps][216];
-    __shared__ float s_v[kFillWarps][216];
+    __shared__ float s_vq[kFillWarps][kFillQ][216];  // kFillQ populations staged per round
     __shared__ float s_t1[kFillWarps][144], s_t2[kFillWarps][96];
     const int64_t nf = (int64_t)(ef - sf) * 64, nc = (int64_t)(ec - sc) * 64;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -346,23 +347,34 @@ __global__ void __launch_bounds__(kFillWarps * 32)
             st[h][2] *= 36;
         }
 #pragma unroll 1
-        for (int q = 0; q < 27; ++q) {
-            __syncwarp();
-            // 7 independent loads per lane in flight (216 = 6 x 32 + 24)
-            float v[7];
+        for (int q0 = 0; q0 < 27; q0 += kFillQ) {
+          __syncwarp();
+          // kFillQ x 7 independent loads per lane in flight (216 = 6 x 32 + 24)
+          {
+            float v[kFillQ][7];
 #pragma unroll
-            for (int i = 0; i < 7; ++i) {
-                const int r = lane + 32 * i;
-                const int32_t c = r < 216 ? s_c[w][r] : -1;
-                v[i] = 0.0f;
-                if (c >= 0) {
-                    const int64_t a = (int64_t)q * nc + c;
-                    v[i] = theta == 0.0f ? __ldg(fold + a) : th0 * __ldg(fold + a) + theta * __ldg(fnew + a);
+            for (int j = 0; j < kFillQ; ++j)
+#pragma unroll
+                for (int i = 0; i < 7; ++i) {
+                    const int r = lane + 32 * i;
+                    const int32_t c = r < 216 ? s_c[w][r] : -1;
+                    v[j][i] = 0.0f;
+                    if (c >= 0) {
+                        const int64_t a = (int64_t)(q0 + j) * nc + c;
+                        v[j][i] = theta == 0.0f ? __ldg(fold + a) : th0 * __ldg(fold + a) + theta * __ldg(fnew + a);
+                    }
                 }
-            }
 #pragma unroll
-            for (int i = 0; i < 7; ++i)
-                if (lane + 32 * i < 216) s_v[w][lane + 32 * i] = v[i];
+            for (int j = 0; j < kFillQ; ++j)
+#pragma unroll
+                for (int i = 0; i < 7; ++i)
+                    if (lane + 32 * i < 216) s_vq[w][j][lane + 32 * i] = v[j][i];
+          }
+          __syncwarp();
+#pragma unroll 1
+          for (int j = 0; j < kFillQ; ++j) {
+            const int q = q0 + j;
+            const float *sv = s_vq[w][j];
             __syncwarp();
             // separable passes at the requested order for the whole block
             // (x: 4 x 6 x 6, y: 4 x 4 x 6, z: 4 x 4 x 4); same association as
@@ -374,7 +386,7 @@ __global__ void __launch_bounds__(kFillWarps * 32)
                 const int fx = e & 3, ry = (e >> 2) % 6, rz = (e >> 2) / 6;
                 const int G = (fx >> 1) + 2, sg = (fx & 1) ? 1 : -1;
                 float a = 0.0f;
-                for (int k = 0; k < ng; ++k) a += axis_w(og, k) * s_v[w][G + sg * (k + kg) + 6 * ry + 36 * rz];
+                for (int k = 0; k < ng; ++k) a += axis_w(og, k) * sv[G + sg * (k + kg) + 6 * ry + 36 * rz];
                 s_t1[w][e] = a;
             }
             __syncwarp();
@@ -402,7 +414,7 @@ __global__ void __launch_bounds__(kFillWarps * 32)
                         for (int ky = 0; ky < n; ++ky) {
                             float ax = 0.0f;
                             const int row = base[h] + st[h][1] * (ky + k0) + st[h][2] * (kz + k0);
-                            for (int kx = 0; kx < n; ++kx) ax += axis_w(o, kx) * s_v[w][row + st[h][0] * (kx + k0)];
+                            for (int kx = 0; kx < n; ++kx) ax += axis_w(o, kx) * sv[row + st[h][0] * (kx + k0)];
                             ay += axis_w(o, ky) * ax;
                         }
                         acc += axis_w(o, kz) * ay;
@@ -410,6 +422,7 @@ __global__ void __launch_bounds__(kFillWarps * 32)
                 }
                 ff[(int64_t)q * nf + (int64_t)(b - sf) * 64 + t] = acc;
             }
+          }
         }
         if (alpha != 1.0f) {
 #pragma unroll
