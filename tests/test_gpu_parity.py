@@ -269,6 +269,16 @@ def test_embed_translated_torus(O, seed):
     _embed_compare(O, mesh, EmbedConfig(n_x=32, l_max=4))
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
+def test_embed_c2_robustness_translations(O, seed):
+    """SURVEY.md §8d robustness variants: the C2 mesh rigidly translated by
+    np.random.default_rng(seed).random(3) * dx_0 (offsets in [0, dx_0)^3),
+    seeds 0-4, at the C2 configuration."""
+    cfg = EmbedConfig(n_x=64, l_max=4)
+    mesh = translate(make_torus(280, 200), np.random.default_rng(seed).random(3) * cfg.dx0)
+    _embed_compare(O, mesh, cfg)
+
+
 def test_embed_filter_invariance_and_determinism(O, torus):
     cfg = EmbedConfig(n_x=32, l_max=3)
     eng = EmbedEngine(torus, cfg)
