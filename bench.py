@@ -437,7 +437,8 @@ def main():
                     "traffic": ncu_traffic(args.config, "k_links_small", "k_links_enum", "k_links_resolve"), "kernel_ms": lk,
                     "algorithmic_bytes": int(link_bytes), "kernel_ms_overlapped": med(link_ovl),
                     "timed": "CUDA events around the cut-link kernels run alone (vf_set_serial_links): "
-                             "the grid-independent line enumeration (k_links<2>) + the resolution after "
+                             "the grid-independent line enumeration (k_links_small: faces <= 1.5 cells, "
+                             "thread per face; k_links<2>: larger faces, warp-flattened) + the resolution after "
                              "the tables (k_links_resolve, overflow faces, band list, fallback); "
                              "kernel_ms_overlapped = the same events in the production schedule, where "
                              "the enumeration shares the SMs with the level pipeline on a side stream"}
