@@ -539,3 +539,14 @@ def test_ctx_create_destroy(O, torus):
     _embed_compare(O, torus, cfg)
     assert lib.vf_ctx_destroy(ctx) == 0
     _embed_compare(O, torus, cfg)
+
+
+def test_link_stats(torus):
+    """vf_embed_link_stats: counters of the last embed's cut-link pass."""
+    eng = EmbedEngine(torus, EmbedConfig(n_x=32, l_max=3), use_graph=False)
+    _, table = eng.run()
+    st = eng.link_stats()
+    assert st["lines"] > 0 and st["lines"] <= st["line_cap"]
+    assert st["overflow_faces"] == 0 and 0 <= st["band"] <= st["band_cap"]
+    assert 0 <= st["large_faces"] <= torus.n_faces
+    assert int((table.lengths >= 0).sum()) > 0
