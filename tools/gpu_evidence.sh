@@ -20,3 +20,10 @@ cp profiles/ncu_traffic.json gpurun_out/ncu_traffic.json
 python tools/ncu_summary.py gpurun_out/launches_c2.csv 3 > gpurun_out/launches_c2.txt
 python tools/ncu_summary.py gpurun_out/launches_c4.csv 2 > gpurun_out/launches_c4.txt
 cat gpurun_out/bench_c2.json gpurun_out/ncu_traffic_c2.txt
+# warm-cache launch lists (shares without ncu's per-kernel cache flush)
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv --log-file gpurun_out/warm_c2.csv python tools/one_embed.py c2 3 > /dev/null 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv --log-file gpurun_out/warm_c4.csv python tools/one_embed.py c4 2 > /dev/null 2>&1
+python tools/ncu_summary.py gpurun_out/warm_c2.csv 3 > gpurun_out/warm_c2.txt
+python tools/ncu_summary.py gpurun_out/warm_c4.csv 2 > gpurun_out/warm_c4.txt
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_hier.csv python tools/one_hier.py 2 > /dev/null 2>&1
+python tools/ncu_summary.py gpurun_out/launches_hier.csv 1 > gpurun_out/hier.txt
