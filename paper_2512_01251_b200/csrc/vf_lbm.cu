@@ -273,13 +273,19 @@ __global__ void k_lbm_parents(int32_t n_blocks, const int32_t *__restrict__ chil
 // (x, then y, then z).  The interpolated populations go to ff and are then
 // rescaled in place by their owning lane.
 constexpr int kFillWarps = 8;
-constexpr int kFillQ = 3;  // populations staged per load round (27 = 9 x 3)
+#ifndef VF_FILL_Q
+#define VF_FILL_Q 3
+#endif
+#ifndef VF_FILL_MINB
+#define VF_FILL_MINB 2  // <= 128 registers: 2 CTAs per SM (measured best; 1 -> 188 registers, 3 -> 80)
+#endif
+constexpr int kFillQ = VF_FILL_Q;  // populations staged per load round (27 = 9 x 3)
 
 __device__ __forceinline__ float axis_w(int ord, int k) {
     return ord == 3 ? c_w3[k] : (ord == 1 ? (k ? 0.25f : 0.75f) : 1.0f);
 }
 
-__global__ void __launch_bounds__(kFillWarps * 32)
+__global__ void __launch_bounds__(kFillWarps * 32, VF_FILL_MINB)
     k_lbm_fill_ghosts(int32_t sf, int32_t ef, int32_t sc, int32_t ec, const int32_t *__restrict__ coords,
                       const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
                       const int32_t *__restrict__ parent, const float *__restrict__ fold,
