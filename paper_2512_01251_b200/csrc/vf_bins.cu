@@ -321,7 +321,10 @@ __device__ int face_pairs(const double *v, const LevelInfo &li, int nlim, int32_
     return cnt;
 }
 
-__global__ void __launch_bounds__(256)
+#ifndef VF_PAIRS_MINB
+#define VF_PAIRS_MINB 2  // 128 registers (1: 224 registers, one CTA per SM) -- C4 embed -2%
+#endif
+__global__ void __launch_bounds__(256, VF_PAIRS_MINB)
     k_pairs(LevelInfo li, int nlim, const double *__restrict__ faces,
             const int32_t *__restrict__ map, const int32_t *__restrict__ d_n_map, int64_t n_static,
             int32_t *__restrict__ slots, int32_t *__restrict__ slot_cnt,
