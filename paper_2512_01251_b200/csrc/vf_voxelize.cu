@@ -588,8 +588,11 @@ __device__ __forceinline__ void xrow_pass_s(int L, int lane, int bx, XStage<NCH>
     }
 }
 
+#ifndef VF_XS_MINB
+#define VF_XS_MINB 4  // <= 128 registers (1 lets the 4-chunk kernel take 162)
+#endif
 template <int NCH>
-__global__ void __launch_bounds__(kXsWarps * 32)
+__global__ void __launch_bounds__(kXsWarps * 32, VF_XS_MINB)
     k_xrows_s(LevelInfo li, int L, const int32_t *__restrict__ map, const int32_t *__restrict__ nbr,
               uint8_t *__restrict__ masks, uint8_t *__restrict__ bflags, uint64_t *__restrict__ solid64) {
     extern __shared__ __align__(16) unsigned char s_raw[];
