@@ -826,7 +826,10 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
 // Resolve the recorded lines (fast class) once the grid and the block map
 // exist: thread per line, its (2, rarely 3) nodes -> block map -> the
 // oracle's FP64 num/den/d/q -> atomicMin.  Full warps, no setup.
-__global__ void __launch_bounds__(256)
+#ifndef VF_RESOLVE_MINB
+#define VF_RESOLVE_MINB 4
+#endif
+__global__ void __launch_bounds__(256, VF_RESOLVE_MINB)
     k_links_resolve(LinkCtx c) {
     const int64_t n = min((int64_t)*c.n_lines, c.line_cap);
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;

@@ -41,7 +41,10 @@ __device__ __forceinline__ uint64_t dil_z(uint64_t lo, uint64_t c, uint64_t hi) 
 
 // thread per finest-level block: 27 solid64 words -> dilation -> FLUID cells
 // of the block's masks that the dilation covers become BOUNDARY
-__global__ void __launch_bounds__(256)
+#ifndef VF_BOUNDARY_MINB
+#define VF_BOUNDARY_MINB 3
+#endif
+__global__ void __launch_bounds__(256, VF_BOUNDARY_MINB)
     k_boundary(LevelInfo li, int L, const int32_t *__restrict__ level_start,
                const int32_t *__restrict__ nbr, const int32_t *__restrict__ coords,
                uint8_t *__restrict__ bflags, uint8_t *__restrict__ masks,
