@@ -18,6 +18,9 @@
 
 namespace vf {
 
+#ifndef VF_SCAN_MINB
+#define VF_SCAN_MINB 6  // <= 40 registers: 48 warps per SM (measured best; 1 lets the compiler take 96)
+#endif
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;  // 4096
@@ -62,7 +65,7 @@ struct ScanNoEpi {
 // element's prefix is known to that thread's tile; other tiles may still be
 // emitting, so Epi must not depend on Emit's outputs)
 template <typename Load, typename Emit, typename NFn = ScanN, typename Epi = ScanNoEpi>
-__global__ void __launch_bounds__(kScanThreads)
+__global__ void __launch_bounds__(kScanThreads, VF_SCAN_MINB)
     scan_kernel(Load load, Emit emit, NFn nfn, int32_t *__restrict__ d_total,
                 uint64_t *__restrict__ status, Epi epi = Epi()) {
     __shared__ int s_warp[kScanThreads / 32];
