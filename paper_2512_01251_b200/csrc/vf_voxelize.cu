@@ -766,8 +766,11 @@ __device__ __forceinline__ void xrow_pass_hv(int L, int lane, int bx, const XHVi
     }
 }
 
+#ifndef VF_XH_MINB
+#define VF_XH_MINB 8  // 64 registers: the max_ctas(8) grid is resident in one wave (measured)
+#endif
 template <int NCH>
-__global__ void __launch_bounds__(kXsWarps * 32)
+__global__ void __launch_bounds__(kXsWarps * 32, VF_XH_MINB)
     k_xrows_h(LevelInfo li, int L, const int32_t *__restrict__ map, const int32_t *__restrict__ nbr,
               uint8_t *__restrict__ masks, uint8_t *__restrict__ bflags, uint64_t *__restrict__ solid64) {
     __shared__ int32_t s_id[kXsWarps][NCH * 32], s_cp[kXsWarps][NCH * 32], s_cm[kXsWarps][NCH * 32];
