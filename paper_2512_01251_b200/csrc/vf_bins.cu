@@ -605,7 +605,7 @@ int build_bins_impl(const LevelInfo &li, int nlim, const double *faces, int64_t 
         if ((rc = launch_iota(bins->d_map, F, bins->d_n_map, st))) return rc;
     }
     cudaMemsetAsync(bins->d_counts, 0, sizeof(int32_t) * (size_t)n_bins, st);
-    k_pairs<<<grid_for(F, 256, max_ctas(8)), 256, 0, st>>>(li, nlim, faces, map, d_n_map, F, w.slots,
+    k_pairs<<<grid_for(F, 256, max_ctas(VF_GRID_PAIRS)), 256, 0, st>>>(li, nlim, faces, map, d_n_map, F, w.slots,
                                                          w.slot_cnt, bins->d_counts, d_status);
     if ((rc = check_launch("k_pairs"))) return rc;
     if ((rc = launch_exclusive_scan(bins->d_counts, n_bins, nullptr, bins->d_offsets,

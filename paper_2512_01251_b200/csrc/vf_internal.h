@@ -16,6 +16,22 @@ int check_launch(const char *what);
 
 int sm_count();
 inline int max_ctas(int per_sm) { return sm_count() * per_sm; }
+// grid sizes (CTAs per SM) of grid-stride kernels (build-time tunables)
+#ifndef VF_GRID_PAIRS
+#define VF_GRID_PAIRS 8
+#endif
+#ifndef VF_GRID_ADAPT
+#define VF_GRID_ADAPT 4
+#endif
+#ifndef VF_GRID_RESOLVE
+#define VF_GRID_RESOLVE 8
+#endif
+#ifndef VF_GRID_BOUNDARY
+#define VF_GRID_BOUNDARY 8
+#endif
+#ifndef VF_GRID_XS4
+#define VF_GRID_XS4 8
+#endif
 
 LevelInfo make_level(const vf_config &cfg, int L);
 inline int nlim_of(const vf_config &cfg) {

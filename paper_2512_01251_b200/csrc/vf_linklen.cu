@@ -1083,7 +1083,7 @@ int link_resolve_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, con
     line_bufs(c, F, lines_ws);
     if ((rc = link_blockmap(g, li, cmap, c, d_n_b, lengths_cap, st))) return rc;
     if (events) cudaEventRecord((cudaEvent_t)events[0], st);
-    k_links_resolve<<<max_ctas(8), 256, 0, st>>>(c);
+    k_links_resolve<<<max_ctas(VF_GRID_RESOLVE), 256, 0, st>>>(c);
     if ((rc = check_launch("k_links_resolve"))) return rc;
     // faces whose lines overflowed the record buffer: the direct kernel
     k_links<0><<<link_grid(F), kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, c.ovf_list, c.n_ovf);

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256, VF_BOUNDARY_MINB)
 int boundary_impl(const vf_config &cfg, vf_grid *g, int32_t *bcount, cudaStream_t st) {
     const int L = g->n_levels - 1;
     cudaMemsetAsync(bcount, 0, sizeof(int32_t) * (size_t)g->capacity, st);
-    k_boundary<<<max_ctas(8), 256, 0, st>>>(make_level(cfg, L), L, g->d_level_start,
+    k_boundary<<<max_ctas(VF_GRID_BOUNDARY), 256, 0, st>>>(make_level(cfg, L), L, g->d_level_start,
                                                        g->d_nbr, g->d_coords, g->d_bflags,
                                                        g->d_masks, g->d_solid64, bcount);
     return check_launch("k_boundary");

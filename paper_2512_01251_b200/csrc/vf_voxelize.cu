@@ -832,7 +832,7 @@ static int launch_xrows_s(const LevelInfo &li, int L, const int32_t *map, vf_gri
     }
     const int64_t rows = (int64_t)li.bins[1] * li.bins[2];
     int64_t grid = (rows + kXsWarps - 1) / kXsWarps;
-    const int64_t cap = max_ctas(NCH <= 2 ? 16 : (NCH <= 4 ? 8 : 4));
+    const int64_t cap = max_ctas(NCH <= 2 ? 16 : (NCH <= 4 ? VF_GRID_XS4 : 4));
     if (grid > cap) grid = cap;
     k_xrows_s<NCH><<<(int)grid, kXsWarps * 32, smem, st>>>(li, L, map, g->d_nbr, g->d_masks, g->d_bflags,
                                                            g->d_solid64);
