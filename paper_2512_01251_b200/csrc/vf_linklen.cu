@@ -114,6 +114,7 @@ struct LinkCtx {
     int32_t *n_band;   // [0] count (may exceed cap), [1] overflow flag
     int64_t band_cap;
     double dx, eps, eps_par, inv_dx;
+    float epsL, dthr;  // eps in cells; the FP32 c.n threshold of the exact parallel test (host-set)
     int bx, by, cells[3];
     int fast;  // eps >> FP64 rounding of the piercing point: fast path allowed
     int pow2;  // dx is a power of two: q = dd * (1/dx) is exactly dd / dx
@@ -793,8 +794,8 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
                 S.hi[d] = min((int)floor((fhi + c.dx + 2.0 * c.eps) * c.inv_dx - 0.5) + 1 + widen, c.cells[d] - 1);
             }
         }
-        S.epsL = (float)(c.eps * c.inv_dx);
-        S.dthr = (float)(2.0 * c.eps_par * 1.7320508075688772) + 1e-5f;
+        S.epsL = c.epsL;
+        S.dthr = c.dthr;
         S.ff9 = 4e-6f * (extL + 2.0f);
         // the 13 pairs in three classes of the axis p of their first nonzero
         // component (c_p = +1): p = x: c = (1, s1, s2), all 9 sign pairs;
@@ -943,6 +944,8 @@ static int make_link_ctx(const vf_config &cfg, int L, const double *faces, float
     c.pow2 = mant == 0.5;
     widen = c.pow2 ? 0 : 1;
     c.inv_dx = 1.0 / li.dx;
+    c.epsL = (float)(li.eps * c.inv_dx);
+    c.dthr = (float)(2.0 * li.eps_par * 1.7320508075688772) + 1e-5f;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_links<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLinkSmem);
