@@ -757,15 +757,18 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
     const bool act = m < F;
     SmallFace S;
     S.f = (int)m;
-    double v[9];
+    double v[9], flo[3] = {0.0, 0.0, 0.0}, fhi[3] = {0.0, 0.0, 0.0};
     float extL = 0.0f;
     bool small = false;
     if (act) {
         load_face(c.faces, S.f, v, S.nn);
         double ext = 0.0;
 #pragma unroll
-        for (int d = 0; d < 3; ++d)
-            ext = fmax(ext, fmax(fmax(v[d], v[3 + d]), v[6 + d]) - fmin(fmin(v[d], v[3 + d]), v[6 + d]));
+        for (int d = 0; d < 3; ++d) {
+            flo[d] = fmin(fmin(v[d], v[3 + d]), v[6 + d]);
+            fhi[d] = fmax(fmax(v[d], v[3 + d]), v[6 + d]);
+            ext = fmax(ext, fhi[d] - flo[d]);
+        }
         extL = (float)(ext * c.inv_dx);
         small = extL <= small_ext;
     }
@@ -788,10 +791,8 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
                 S.V2[d] = (float)((v[6 + d] - v[d]) * c.inv_dx);
                 S.nf[d] = (float)S.nn[d];
                 // nodes within one link of the face AABB (k_links' fallback range)
-                const double flo = fmin(fmin(v[d], v[3 + d]), v[6 + d]);
-                const double fhi = fmax(fmax(v[d], v[3 + d]), v[6 + d]);
-                S.lo[d] = max((int)floor((flo - c.dx - 2.0 * c.eps) * c.inv_dx - 0.5) - widen, 0);
-                S.hi[d] = min((int)floor((fhi + c.dx + 2.0 * c.eps) * c.inv_dx - 0.5) + 1 + widen, c.cells[d] - 1);
+                S.lo[d] = max((int)floor((flo[d] - c.dx - 2.0 * c.eps) * c.inv_dx - 0.5) - widen, 0);
+                S.hi[d] = min((int)floor((fhi[d] + c.dx + 2.0 * c.eps) * c.inv_dx - 0.5) + 1 + widen, c.cells[d] - 1);
             }
         }
         S.epsL = c.epsL;
