@@ -114,6 +114,7 @@ struct LinkCtx {
     int32_t *n_band;   // [0] count (may exceed cap), [1] overflow flag
     int64_t band_cap;
     double dx, eps, eps_par, inv_dx;
+    double len[3];     // domain lengths: faces whose AABB misses [0, l]^3 have no bins, hence no links
     float epsL, dthr;  // eps in cells; the FP32 c.n threshold of the exact parallel test (host-set)
     int bx, by, cells[3];
     int fast;  // eps >> FP64 rounding of the piercing point: fast path allowed
@@ -511,7 +512,7 @@ __global__ void __launch_bounds__(kLinkWarps * 32, MODE == 1 ? 1 : VF_LINK_MINB)
     const int64_t first = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
     for (int64_t base = first; base < n; base += stride) {
         const int64_t m = base + lane;
-        const bool active = m < n;
+        bool active = m < n;
         int f = 0;
         __syncwarp();
         if (active) {
@@ -529,6 +530,7 @@ __global__ void __launch_bounds__(kLinkWarps * 32, MODE == 1 ? 1 : VF_LINK_MINB)
                 const double flo = fmin(fmin(v[d], v[3 + d]), v[6 + d]);
                 const double fhi = fmax(fmax(v[d], v[3 + d]), v[6 + d]);
                 ext = fmax(ext, fhi - flo);
+                if (fhi < 0.0 || flo > c.len[d]) active = false;  // in no bin (A5), no links
                 // nodes within one link of the face AABB (fallback range)
                 W.lohi[lane][d] = (short)max((int)floor((flo - c.dx - 2.0 * c.eps) * c.inv_dx - 0.5) - widen, 0);
                 W.lohi[lane][3 + d] =
@@ -754,7 +756,7 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
     __syncthreads();
     const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    const bool act = m < F;
+    bool act = m < F;
     SmallFace S;
     S.f = (int)m;
     double v[9], flo[3] = {0.0, 0.0, 0.0}, fhi[3] = {0.0, 0.0, 0.0};
@@ -770,7 +772,12 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
             ext = fmax(ext, fhi[d] - flo[d]);
         }
         extL = (float)(ext * c.inv_dx);
-        small = extL <= small_ext;
+        // A5 / face_pairs: a face whose AABB misses the domain is in no bin,
+        // so the oracle's per-cell MD-bin scan never sees it
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+            if (fhi[d] < 0.0 || flo[d] > c.len[d]) act = false;
+        small = act && extL <= small_ext;
     }
     // large faces: warp-aggregated append to the list of the warp-flattened kernel
     const unsigned bm = __ballot_sync(0xffffffffu, act && !small);
@@ -937,6 +944,7 @@ static int make_link_ctx(const vf_config &cfg, int L, const double *faces, float
     c.eps_par = li.eps_par;
     c.bx = li.bins[0];
     c.by = li.bins[1];
+    for (int d = 0; d < 3; ++d) c.len[d] = li.len[d];
     c.fast = li.eps >= 1e-12 * fmax(fmax(li.len[0], li.len[1]), li.len[2]);
     for (int d = 0; d < 3; ++d) c.cells[d] = li.cells[d];
     // 1/dx is exact when dx is a power of two; otherwise widen the ranges by one

@@ -182,40 +182,120 @@ def l_spec_bound(domain_lengths, n_spec, l_max, n_b) -> float:
 
 
 def refine_faces(mesh: TriangleMesh, l_spec: float) -> TriangleMesh:
-    """Midpoint subdivision until every edge < l_spec (geometry.py:355-403).
+    """Midpoint subdivision until every edge < l_spec (geometry.py:355-403),
+    with the reference's face AND vertex numbering.
 
-    Vectorised breadth-first variant: every face with an edge >= l_spec is
-    split into four per pass.  The resulting face set equals the reference's
-    depth-first result up to face order (both split exactly the same
-    triangles), which the engine does not depend on beyond face ids."""
+    The reference walks a LIFO stack seeded with the faces in order
+    (geometry.py:383-397): it pops the last face, splits it into
+    [a,ab,ca], [b,bc,ab], [c,ca,bc], [ab,bc,ca] (pushed in that order, so
+    popped last-child first), emits faces that are fine enough, numbers each
+    new midpoint at its first creation (deduplicated by exact coordinates,
+    including against the input vertices, geometry.py:370-378) and finally
+    reverses the emitted list (:399).  Hence:
+      * face order = input faces in order, each replaced by the leaves of its
+        split tree in natural child order (pre-order, children 0..3);
+      * vertex order = input vertices, then midpoints in the order the split
+        faces are popped: input faces last to first, children 3..0, pre-order;
+        each split face creates ab, bc, ca in that order.
+    This is reproduced breadth-first and vectorised: the tree is built level
+    by level with provisional midpoint handles, then faces and midpoints are
+    renumbered by those two orders.  The per-face test uses the 1-D
+    ``np.linalg.norm`` of the reference (a BLAS dot); the vectorised norm is
+    recomputed that way wherever it is within 1e-12 relative of l_spec."""
     if l_spec <= 0:
         raise MeshError("l_spec must be positive")
-    verts = mesh.vertices
-    faces = mesh.faces_indexed
-    done = []
-    while True:
-        v = verts[faces]
+    if np.all(mesh.max_edge_lengths() < l_spec):    # geometry.py:361-362
+        return mesh
+    V0 = mesh.vertices
+    n0 = len(V0)
+    # per tree node: vertex handles (h < n0: input vertex; else midpoint
+    # handle n0 + 3 * split_index + k), root face, path code, depth
+    faces = mesh.faces_indexed.astype(np.int64)
+    root = np.arange(len(faces), dtype=np.int64)
+    path = np.zeros(len(faces), dtype=np.int64)     # child digits, base 4
+    depth = 0
+    coords = [V0]                                   # coordinates of every handle
+    leaves, splits = [], []                         # (faces, root, path, depth)
+    n_split = 0
+    while len(faces):
+        P = np.concatenate(coords, axis=0) if len(coords) > 1 else coords[0]
+        v = P[faces]
         e = np.stack([np.linalg.norm(v[:, (k + 1) % 3] - v[:, k], axis=1) for k in range(3)], 1)
-        big = e.max(axis=1) >= l_spec
-        done.append(faces[~big])
+        emax = e.max(axis=1)
+        near = np.nonzero(np.abs(emax - l_spec) <= 1e-12 * l_spec)[0]
+        for i in near:                              # the reference's own per-face norms
+            pa, pb, pc = v[i]
+            emax[i] = max(np.linalg.norm(pb - pa), np.linalg.norm(pc - pb), np.linalg.norm(pa - pc))
+        big = ~(emax < l_spec)
+        leaves.append((faces[~big], root[~big], path[~big], depth))
         if not big.any():
             break
-        verts, faces = _split_plain(verts, faces[big])
-    out = np.concatenate(done, axis=0)
-    if len(out) == len(mesh.faces_indexed) and np.array_equal(out, mesh.faces_indexed):
-        return mesh
+        fb, rb, pb_ = faces[big], root[big], path[big]
+        k = len(fb)
+        vb = v[big]
+        mid = np.stack([(vb[:, 0] + vb[:, 1]) / 2.0, (vb[:, 1] + vb[:, 2]) / 2.0,
+                        (vb[:, 2] + vb[:, 0]) / 2.0], 1)            # ab, bc, ca
+        h = n0 + 3 * (n_split + np.arange(k, dtype=np.int64))
+        ab, bc, ca = h, h + 1, h + 2
+        splits.append((rb, pb_, depth, mid.reshape(-1, 3)))
+        coords.append(mid.reshape(-1, 3))
+        n_split += k
+        a, b, c = fb[:, 0], fb[:, 1], fb[:, 2]
+        faces = np.stack([np.stack([a, ab, ca], 1), np.stack([b, bc, ab], 1),
+                          np.stack([c, ca, bc], 1), np.stack([ab, bc, ca], 1)], 1).reshape(-1, 3)
+        root = np.repeat(rb, 4)
+        path = (np.repeat(pb_, 4) << 2) | np.tile(np.arange(4, dtype=np.int64), k)
+        depth += 1
+    dmax = depth + 1
+
+    def code(p, d, flip):
+        # pre-order key over paths of mixed depth: digits 1..4, padded with 0
+        out = np.zeros(len(p), dtype=np.int64)
+        for i in range(dmax):
+            sh = d - 1 - i                          # digit i of a depth-d path
+            dig = np.where(sh >= 0, (p >> (2 * np.maximum(sh, 0))) & 3, -1)
+            if flip:
+                dig = np.where(dig >= 0, 3 - dig, -1)
+            out = out * 5 + (dig + 1)
+        return out
+
+    # midpoints in pop order: roots descending, children 3..0, pre-order
+    r_s = np.concatenate([s[0] for s in splits])
+    d_s = np.concatenate([np.full(len(s[0]), s[2], np.int64) for s in splits])
+    c_s = code(np.concatenate([s[1] for s in splits]), d_s, True)
+    pop = np.lexsort((c_s, -r_s))                   # split index in pop order
+    cand = np.concatenate([s[3] for s in splits]).reshape(-1, 3, 3)[pop].reshape(-1, 3)
+    cand_h = (n0 + 3 * pop[:, None] + np.arange(3)[None, :]).reshape(-1)
+
+    def keys(x):
+        x = np.ascontiguousarray(x + 0.0)           # -0.0 == 0.0 as a dict key
+        return x.view(np.dtype((np.void, 24))).reshape(-1)
+
+    k0, kc = keys(V0), keys(cand)
+    # input vertices: dict built in order, so a duplicated coordinate maps to
+    # its LAST index (geometry.py:364)
+    u0, inv0 = np.unique(k0[::-1], return_index=True)
+    last0 = n0 - 1 - inv0
+    pos = np.searchsorted(u0, kc)
+    pos_c = np.minimum(pos, len(u0) - 1)
+    hit = u0[pos_c] == kc
+    lut = np.empty(n0 + 3 * n_split, dtype=np.int64)
+    lut[:n0] = np.arange(n0)
+    new = ~hit
+    kn = kc[new]
+    un, first, invn = np.unique(kn, return_index=True, return_inverse=True)
+    rank = np.empty(len(un), dtype=np.int64)
+    rank[np.argsort(first, kind="stable")] = np.arange(len(un))
+    ids = np.empty(len(kc), dtype=np.int64)
+    ids[hit] = last0[pos_c[hit]]
+    ids[new] = n0 + rank[invn.reshape(-1)]
+    lut[cand_h] = ids
+    newv = cand[new][np.sort(first)]
+    verts = np.concatenate([V0, newv], axis=0)
+    # leaves in the reversed emission order: roots ascending, children 0..3
+    f_l = np.concatenate([x[0] for x in leaves])
+    r_l = np.concatenate([x[1] for x in leaves])
+    d_l = np.concatenate([np.full(len(x[0]), x[3], np.int64) for x in leaves])
+    c_l = code(np.concatenate([x[2] for x in leaves]), d_l, False)
+    out = lut[f_l[np.lexsort((c_l, r_l))]]
     return TriangleMesh(verts, out)
-
-
-def _split_plain(verts, faces):
-    a, b, c = faces[:, 0], faces[:, 1], faces[:, 2]
-    e = np.stack([np.stack([a, b], 1), np.stack([b, c], 1), np.stack([c, a], 1)], 1).reshape(-1, 2)
-    key = np.sort(e, axis=1)
-    uniq, inv = np.unique(key, axis=0, return_inverse=True)
-    mid = (verts[uniq[:, 0]] + verts[uniq[:, 1]]) / 2.0
-    ids = len(verts) + inv.reshape(-1)
-    nv = np.concatenate([verts, mid], axis=0)
-    ab, bc, ca = ids.reshape(-1, 3).T
-    out = np.stack([np.stack([a, ab, ca], 1), np.stack([b, bc, ab], 1),
-                    np.stack([c, ca, bc], 1), np.stack([ab, bc, ca], 1)], 1).reshape(-1, 3)
-    return nv, out

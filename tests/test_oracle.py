@@ -429,6 +429,17 @@ def test_refine_faces_cap():
     assert refine_faces(r, ls) is r  # identity when already fine
 
 
+@pytest.mark.parametrize("case", ["ico1", "torus", "rand", "dup", "mixed"])
+def test_refine_faces_reference_order(case):
+    """refine_faces reproduces the reference's face AND vertex numbering
+    (geometry.py:355-403, depth-first stack walk), pinned by vectors generated
+    from the reference (tests/golden/make_refine_golden.py)."""
+    z = np.load(os.path.join(GOLD, "refine_golden.npz"))
+    r = refine_faces(TriangleMesh(z[case + "_V"], z[case + "_F"]), float(z[case + "_l"]))
+    assert np.array_equal(r.faces_indexed, z[case + "_RF"])
+    assert np.array_equal(r.vertices, z[case + "_RV"])
+
+
 def test_torus_generator():
     m = make_torus(40, 20)
     assert m.n_faces == 1600
