@@ -279,37 +279,235 @@ __global__ void __launch_bounds__(256, 3)
 // --------------------------------------------------------------------------
 // K-pairs
 
-// Candidate bins of one face (Alg. 2); returns the count or -1 on cap violation.
-__device__ int face_pairs(const double *v, const LevelInfo &li, int nlim, int32_t *slot,
-                          int32_t *counts /* nullable: fused histogram */) {
+// exact SAT of one candidate bin box (the classifier's undecided case): the
+// face is re-read (L1) and the SAT set up here, out of line, so the hot loop
+// of k_pairs does not carry the SatFace registers
+static __device__ __noinline__ bool bin_sat_exact_f(const double *__restrict__ faces, int64_t f,
+                                                    double mx, double my, double mz, double Mx,
+                                                    double My, double Mz) {
+    double v[9], n[3];
+    load_face(faces, f, v, n);
+    SatFace sf;
+    sat_face_init(sf, v);
+    return sat_exact(sf, mx, my, mz, Mx, My, Mz);
+}
+
+// Alg. 2 literally: every candidate bin through the exact SAT (faces with
+// more than 32 candidate bins along an axis -- long slivers)
+static __device__ __noinline__ int face_pairs_generic(const double *__restrict__ faces, int64_t fid,
+                                                      const LevelInfo &li, int nlim, int32_t *slot,
+                                                      int32_t *counts) {
+    double v[9], n[3];
+    load_face(faces, fid, v, n);
     SatFace f;
     sat_face_init(f, v);
-#pragma unroll
-    for (int d = 0; d < 3; ++d)
-        if (f.hi[d] < 0.0 || f.lo[d] > li.len[d]) return 0;  // outside domain
     const double dx = li.dx, h = li.h;
     int a[3], b[3];
-#pragma unroll
     for (int d = 0; d < 3; ++d) {
         const double s = VF_DDIV((double)li.bins[d], li.len[d]);
-        double fa = floor(VF_DMUL(f.lo[d], s)) - 1.0, fb = floor(VF_DMUL(f.hi[d], s)) + 1.0;
-        fa = fmax(fa, 0.0);
-        fb = fmin(fb, (double)(li.bins[d] - 1));
-        if (fa > fb) return 0;
-        a[d] = (int)fa;
-        b[d] = (int)fb;
+        a[d] = (int)fmax(floor(VF_DMUL(f.lo[d], s)) - 1.0, 0.0);
+        b[d] = (int)fmin(floor(VF_DMUL(f.hi[d], s)) + 1.0, (double)(li.bins[d] - 1));
     }
     int cnt = 0;
     for (int bk = a[2]; bk <= b[2]; ++bk) {
         const double mz = VF_DSUB(VF_DMUL((double)bk, h), dx), Mz = VF_DADD(VF_DMUL((double)(bk + 1), h), dx);
         for (int bj = a[1]; bj <= b[1]; ++bj) {
-            if (!owns_row(li, bj, bk)) continue;  // multi-GPU: bins of other ranks
+            if (!owns_row(li, bj, bk)) continue;
             const double my = VF_DSUB(VF_DMUL((double)bj, h), dx), My = VF_DADD(VF_DMUL((double)(bj + 1), h), dx);
             for (int bi = a[0]; bi <= b[0]; ++bi) {
                 const double mx = VF_DSUB(VF_DMUL((double)bi, h), dx), Mx = VF_DADD(VF_DMUL((double)(bi + 1), h), dx);
                 if (sat_exact(f, mx, my, mz, Mx, My, Mz)) {
-                    if (cnt >= nlim) return -1;  // no histogram entry was made yet
+                    if (cnt >= nlim) return -1;
                     slot[cnt++] = bi + li.bins[0] * (bj + li.bins[1] * bk);
+                }
+            }
+        }
+    }
+    if (counts)
+        for (int k = 0; k < cnt; ++k) atomicAdd(&counts[slot[k]], 1);
+    return cnt;
+}
+
+// FP32 classifier of the SAT of a face against one (Delta x-expanded) bin
+// box: 1 = the reference SAT (geometry.py:441-500) certainly accepts, 0 =
+// certainly rejects, 2 = undecided (run the exact SAT).  Face-local frame:
+// u2, u3 = FP32(v2 - v1), FP32(v3 - v1) (v1 at the origin); (cx, cy, cz) =
+// FP32(box centre - v1), (rx, ry, rz) the half widths.
+// The SAT is the conjunction of per-axis tests; the box axes are decided
+// exactly by the caller.  For each of the 9 edge axes e of the planes yz, xy,
+// zx and for the plane-cut test the separation s (box-centre projection vs
+// the triangle's projection widened by the box's) is evaluated in FP32:
+//   edge axes: |s_32 - s_ref| <= 2 W |de|_1 + FP32 rounding + the reference's
+//     own FP64 rounding (<= 6u C |e|_1), with |de| <= 2.4e-7 E the FP32
+//     rounding of the local axis; tau_e = |e|_1 (4e-6 W + Ct) + 4e-6 E W
+//     (W: largest local |coordinate| + box half width, E: largest edge
+//     component, Ct = 1e-14 C, C >= every |absolute coordinate|);
+//   plane: |n_32 - n_ref| <= 8.3e-7 E^2 per component, the reference's pn
+//     rounding <= 8u E^2; tau_p = E^2 (4e-5 W + 6 Ct).
+// An axis whose reference components are exactly zero (edge parallel to the
+// plane's normal axis: bit in `zero`) never separates and is skipped.  Sure
+// separation on one axis => the reference rejects; sure overlap on every
+// axis => it accepts (every per-axis outcome agrees with the reference's).
+__device__ __forceinline__ int bin_class(const float *u2, const float *u3, float cx, float cy,
+                                         float cz, float rx, float ry, float rz, float E, float W,
+                                         float Ct, uint32_t zero) {
+    const float c[3] = {cx, cy, cz}, r[3] = {rx, ry, rz};
+    bool sure = true;
+#pragma unroll
+    for (int pl = 0; pl < 3; ++pl) {
+        const int A = pl == 0 ? 1 : (pl == 1 ? 0 : 2), B = pl == 0 ? 2 : (pl == 1 ? 1 : 0);
+        const float a2 = u2[A], b2 = u2[B], a3 = u3[A], b3 = u3[B];
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            if ((zero >> (3 * pl + e)) & 1u) continue;
+            // edge j -> j+1: (e_x, e_y) = (b_{j+1} - b_j, a_j - a_{j+1}), v1 = 0
+            const float ex = e == 0 ? b2 : (e == 1 ? b3 - b2 : -b3);
+            const float ey = e == 0 ? -a2 : (e == 1 ? a2 - a3 : a3);
+            const float t2 = a2 * ex + b2 * ey, t3 = a3 * ex + b3 * ey;
+            const float lo = fminf(0.0f, fminf(t2, t3)) - (r[A] * fabsf(ex) + r[B] * fabsf(ey));
+            const float hi = fmaxf(0.0f, fmaxf(t2, t3)) + (r[A] * fabsf(ex) + r[B] * fabsf(ey));
+            const float p = c[A] * ex + c[B] * ey;
+            const float tau = (fabsf(ex) + fabsf(ey)) * (4e-6f * W + Ct) + 4e-6f * E * W;
+            if (p < lo - tau || p > hi + tau) return 0;
+            if (p < lo + tau || p > hi - tau) sure = false;
+        }
+    }
+    const float nx = u2[1] * u3[2] - u2[2] * u3[1];
+    const float ny = u2[2] * u3[0] - u2[0] * u3[2];
+    const float nz = u2[0] * u3[1] - u2[1] * u3[0];
+    const float Rn = rx * fabsf(nx) + ry * fabsf(ny) + rz * fabsf(nz);
+    const float pn = fabsf(nx * cx + ny * cy + nz * cz);
+    const float taup = E * E * (4e-5f * W + 6.0f * Ct);
+    if (pn > Rn + taup) return 0;
+    if (pn > Rn - taup) sure = false;
+    return sure ? 1 : 2;
+}
+
+// Candidate bins of one face (Alg. 2, pins A5); returns the count or -1 on
+// cap violation.  Every candidate bin I_min-1..I_max+1 is decided exactly as
+// the reference SAT (geometry.py:441-500) decides it, but the FP64 SAT only
+// runs where its outcome is not certain:
+//   * box axes: the SAT's three box-axis tests are exact comparisons of the
+//     face extent with the bin box [I h - dx, (I+1) h + dx]; they are
+//     separable, so each axis' candidate range is pruned to the bins that
+//     pass them (bit masks, same FP64 box bounds as the SAT call);
+//   * a vertex strictly inside the box by mg = 1e-10 C (C >= every |coord|
+//     of face and box) in all three axes: the SAT accepts.  Each of the 9
+//     edge axes projects that vertex into the box's projection with slack
+//     mg (|e_x| + |e_y|) >> the FP64 rounding of the projections (~6u C);
+//     the plane-cut test has (d + d1) >= mg |n|_1 and (d + d2) <= -mg |n|_1
+//     up to ~6u |n|_1 C for the plane's anchor v1.  For v2 / v3 the computed
+//     normal misses them by |dn . e| <= 24u E^3 (E: largest edge
+//     component), so they are used only when the face is well conditioned,
+//     |n|_1 >= 1e-3 E^2 (FP32 estimate >= 2e-3 E^2), where mg |n|_1 >=
+//     1e-13 E^3 dominates;
+//   * the FP32 classifier bin_class; its undecided band: the exact SAT.
+// The accepted set -- hence the pairs, their x-fastest order and the cap
+// check -- is identical to testing every candidate with the SAT.
+__device__ __forceinline__ int face_pairs(const double *__restrict__ faces, int64_t fid, const double *v,
+                          const LevelInfo &li, int nlim, int32_t *slot,
+                          int32_t *counts /* nullable: fused histogram */) {
+    double lo[3], hi[3];
+    double C = fmax(fmax(li.len[0], li.len[1]), li.len[2]) + li.h;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        lo[d] = fmin(fmin(v[d], v[3 + d]), v[6 + d]);
+        hi[d] = fmax(fmax(v[d], v[3 + d]), v[6 + d]);
+        if (hi[d] < 0.0 || lo[d] > li.len[d]) return 0;  // outside domain
+        C = fmax(C, fmax(fabs(lo[d]), fabs(hi[d])));
+    }
+    const double mg = 1e-10 * C;
+    // face-local FP32 frame (bin_class) and the conditioning of the plane
+    // test for v2 / v3
+    float u2[3], u3[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        u2[d] = (float)(v[3 + d] - v[d]);
+        u3[d] = (float)(v[6 + d] - v[d]);
+    }
+    const float E = fmaxf(fmaxf(fmaxf(fabsf(u2[0]), fabsf(u2[1])), fmaxf(fabsf(u2[2]), fabsf(u3[0]))),
+                          fmaxf(fabsf(u3[1]), fabsf(u3[2])));
+    bool cond;
+    {
+        const float nx = u2[1] * u3[2] - u2[2] * u3[1], ny = u2[2] * u3[0] - u2[0] * u3[2],
+                    nz = u2[0] * u3[1] - u2[1] * u3[0];
+        cond = fabsf(nx) + fabsf(ny) + fabsf(nz) >= 2e-3f * E * E;
+    }
+    // edge axes whose reference components are exactly zero (never separate)
+    uint32_t zero = 0;
+    {
+        const int A[3] = {1, 0, 2}, B[3] = {2, 1, 0};
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl)
+#pragma unroll
+            for (int e = 0; e < 3; ++e) {
+                const int j = e, k = (e + 1) % 3;
+                if (v[3 * j + A[pl]] == v[3 * k + A[pl]] && v[3 * j + B[pl]] == v[3 * k + B[pl]])
+                    zero |= 1u << (3 * pl + e);
+            }
+    }
+    const float Ct = (float)(1e-14 * C);
+    const double dx = li.dx, h = li.h;
+    const float rh = (float)(0.5 * h + dx);
+    int a[3], b[3];
+    uint32_t pass[3], in[3][3];  // per axis: box-axis pass bits; per vertex: inside-with-margin bits
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const double s = VF_DDIV((double)li.bins[d], li.len[d]);
+        double fa = floor(VF_DMUL(lo[d], s)) - 1.0, fb = floor(VF_DMUL(hi[d], s)) + 1.0;
+        fa = fmax(fa, 0.0);
+        fb = fmin(fb, (double)(li.bins[d] - 1));
+        if (fa > fb) return 0;
+        a[d] = (int)fa;
+        b[d] = (int)fb;
+        if (b[d] - a[d] >= 32) return face_pairs_generic(faces, fid, li, nlim, slot, counts);
+        pass[d] = 0;
+        in[0][d] = in[1][d] = in[2][d] = 0;
+        for (int I = a[d]; I <= b[d]; ++I) {
+            const double m = VF_DSUB(VF_DMUL((double)I, h), dx), M = VF_DADD(VF_DMUL((double)(I + 1), h), dx);
+            const uint32_t bit = 1u << (I - a[d]);
+            if (!(hi[d] < m || M < lo[d])) pass[d] |= bit;
+            const double ml = m + mg, Ml = M - mg;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                if (ml < v[3 * k + d] && v[3 * k + d] < Ml) in[k][d] |= bit;
+        }
+    }
+    // W: largest local |coordinate| (vertices, candidate box centres) + box half width
+    float W = E;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+        W = fmaxf(W, fmaxf(fabsf((float)(((double)a[d] + 0.5) * h - v[d])),
+                           fabsf((float)(((double)b[d] + 0.5) * h - v[d]))));
+    W += rh * 1.0001f;
+    const int64_t nbx = li.bins[0], nby = li.bins[1];
+    int cnt = 0;
+    for (uint32_t mz = pass[2]; mz; mz &= mz - 1) {
+        const int oz = __ffs(mz) - 1, bk = a[2] + oz;
+        const double bz0 = VF_DSUB(VF_DMUL((double)bk, h), dx), bz1 = VF_DADD(VF_DMUL((double)(bk + 1), h), dx);
+        const float cz = (float)(0.5 * (bz0 + bz1) - v[2]), rz = (float)(0.5 * (bz1 - bz0));
+        for (uint32_t my = pass[1]; my; my &= my - 1) {
+            const int oy = __ffs(my) - 1, bj = a[1] + oy;
+            if (!owns_row(li, bj, bk)) continue;  // multi-GPU: bins of other ranks
+            const double by0 = VF_DSUB(VF_DMUL((double)bj, h), dx), by1 = VF_DADD(VF_DMUL((double)(bj + 1), h), dx);
+            const float cy = (float)(0.5 * (by0 + by1) - v[1]), ry = (float)(0.5 * (by1 - by0));
+            // vertices inside (y, z) of this bin, per x bit
+            uint32_t fx = 0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                if (((in[k][1] >> oy) & (in[k][2] >> oz) & 1u) && (k == 0 || cond)) fx |= in[k][0];
+            for (uint32_t mx = pass[0]; mx; mx &= mx - 1) {
+                const int ox = __ffs(mx) - 1, bi = a[0] + ox;
+                bool acc = (fx >> ox) & 1u;
+                if (!acc) {
+                    const double bx0 = VF_DSUB(VF_DMUL((double)bi, h), dx), bx1 = VF_DADD(VF_DMUL((double)(bi + 1), h), dx);
+                    const int cls = bin_class(u2, u3, (float)(0.5 * (bx0 + bx1) - v[0]), cy, cz,
+                                              (float)(0.5 * (bx1 - bx0)), ry, rz, E, W, Ct, zero);
+                    acc = cls == 1 || (cls == 2 && bin_sat_exact_f(faces, fid, bx0, by0, bz0, bx1, by1, bz1));
+                }
+                if (acc) {
+                    if (cnt >= nlim) return -1;  // no histogram entry was made yet
+                    slot[cnt++] = (int32_t)(bi + nbx * (bj + nby * (int64_t)bk));
                 }
             }
         }
@@ -321,10 +519,15 @@ __device__ int face_pairs(const double *v, const LevelInfo &li, int nlim, int32_
     return cnt;
 }
 
+// K-pairs: thread per kept face (face_pairs).  A warp-flattened variant
+// ((face, candidate bin) work spread over the lanes, per-face 64-bit accept
+// masks in shared memory) was measured slower on the B200: the candidate
+// decode and the shared 64-bit atomics cost more than the idle lanes.
 #ifndef VF_PAIRS_MINB
-#define VF_PAIRS_MINB 2  // 128 registers (1: 224 registers, one CTA per SM) -- C4 embed -2%
+#define VF_PAIRS_MINB 4
 #endif
-__global__ void __launch_bounds__(256, VF_PAIRS_MINB)
+constexpr int kPairThreads = 128;
+__global__ void __launch_bounds__(kPairThreads, VF_PAIRS_MINB)
     k_pairs(LevelInfo li, int nlim, const double *__restrict__ faces,
             const int32_t *__restrict__ map, const int32_t *__restrict__ d_n_map, int64_t n_static,
             int32_t *__restrict__ slots, int32_t *__restrict__ slot_cnt,
@@ -335,7 +538,7 @@ __global__ void __launch_bounds__(256, VF_PAIRS_MINB)
         const int64_t f = map ? (int64_t)map[m] : m;
         double v[9], nn[3];
         load_face(faces, f, v, nn);
-        int c = face_pairs(v, li, nlim, slots + m * nlim, counts);
+        int c = face_pairs(faces, f, v, li, nlim, slots + m * nlim, counts);
         if (c < 0) {
             latch_status(d_status, VF_ENLIM);
             c = 0;
@@ -605,7 +808,7 @@ int build_bins_impl(const LevelInfo &li, int nlim, const double *faces, int64_t 
         if ((rc = launch_iota(bins->d_map, F, bins->d_n_map, st))) return rc;
     }
     cudaMemsetAsync(bins->d_counts, 0, sizeof(int32_t) * (size_t)n_bins, st);
-    k_pairs<<<grid_for(F, 256, max_ctas(VF_GRID_PAIRS)), 256, 0, st>>>(li, nlim, faces, map, d_n_map, F, w.slots,
+    k_pairs<<<grid_for(F, kPairThreads, max_ctas(VF_GRID_PAIRS * 2)), kPairThreads, 0, st>>>(li, nlim, faces, map, d_n_map, F, w.slots,
                                                          w.slot_cnt, bins->d_counts, d_status);
     if ((rc = check_launch("k_pairs"))) return rc;
     if ((rc = launch_exclusive_scan(bins->d_counts, n_bins, nullptr, bins->d_offsets,
@@ -650,7 +853,7 @@ int bin_pairs_impl(const LevelInfo &li, int nlim, const double *faces, int64_t F
     BinsWs w;
     if (bins_ws_layout(F, nlim, 1, (char *)ws, &w) > ws_bytes)
         return set_error(VF_EARG, "pairs workspace too small");
-    k_pairs<<<grid_for(F, 256, max_ctas(8)), 256, 0, st>>>(li, nlim, faces, map, d_n_map, F,
+    k_pairs<<<grid_for(F, kPairThreads, max_ctas(16)), kPairThreads, 0, st>>>(li, nlim, faces, map, d_n_map, F,
                                                          w.slots, w.slot_cnt, nullptr, d_status);
     int rc = check_launch("k_pairs");
     if (rc) return rc;

@@ -47,3 +47,20 @@ def test_fuzz_margins_no_filter(O, seed):
     """filter off: every face through every level's row classifier"""
     mesh, cfg = fuzz_case("nx48", seed)
     _embed_compare(O, mesh, cfg, use_filter=False)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("name", sorted(FUZZ_CONFIGS))
+def test_fuzz_bins(O, name, seed):
+    """The bin-pair classifier (box-axis pruning, vertex fast accept, FP32
+    bin_class, exact SAT in the band) against the oracle's per-candidate SAT:
+    every level's bins, 1D filter on and off."""
+    from paper_2512_01251_b200 import binning
+    import numpy as np
+    mesh, cfg = fuzz_case(name, seed)
+    for L in range(cfg.l_max):
+        for use_filter in (True, False):
+            bl = binning.build_level(mesh, L, cfg, 0, use_filter)
+            c, o, f = bl.to_numpy()
+            cr, orr, fr = O.build_bins(mesh.faces_coord, mesh.normals, cfg, L, 0, use_filter)
+            assert np.array_equal(c, cr) and np.array_equal(o, orr) and np.array_equal(f, fr), (L, use_filter)

@@ -1,10 +1,11 @@
 """Per-source-line stall samples / executed instructions of one kernel from an
-ncu report (needs -lineinfo).  usage: ncu_lines.py <rep> <kernel> [top]"""
+ncu report (needs -lineinfo).  usage: ncu_lines.py <rep> <kernel> [top] [launch skip]"""
 import csv, io, subprocess, sys
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+skip = sys.argv[4] if len(sys.argv) > 4 else "0"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", kern,
-                      "--launch-count", "1", "--print-source", "cuda,sass"],
+                      "--launch-skip", skip, "--launch-count", "1", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 res, fname, h = [], None, None
