@@ -230,6 +230,14 @@ void vf_graph_destroy(void *graph_exec);
 int vf_side_sync(void);
 /* number of kernels this library has launched in the process (bench hook) */
 int64_t vf_launch_count(void);
+/* Per-kernel timer (bench / profiling hook).  vf_ktimer_start: the embed
+ * calls that follow on `stream` run every kernel on that stream in order (no
+ * side streams) behind a spin kernel of `gate_us` microseconds, and an event
+ * is recorded after every launch and memset.  vf_ktimer_stop synchronises and
+ * writes "name<TAB>launches<TAB>total ms\n" lines (first-appearance order)
+ * into buf; returns the byte count (negative status on a CUDA error). */
+int vf_ktimer_start(void *stream, double gate_us);
+int vf_ktimer_stop(char *buf, int buflen);
 
 /* Counters of the last embed's cut-link pass on this workspace (synchronous):
  * out[6] = {piercing lines recorded, line capacity, faces whose lines
@@ -284,8 +292,9 @@ typedef struct {
 int vf_lbm_init(const vf_grid *grid, int32_t s, int32_t e, double rho, const double *u,
                 float *d_f, void *stream);
 /* one step: d_fout = collide(stream(d_fin)); the wall-link momentum exchange
- * is ADDED to d_force[3] (lattice units) when d_force is not NULL.  d_scratch:
- * e - s + 1 int32 (the wall-link block list of the step) */
+ * is ADDED to d_force[3] (lattice units) when d_force is not NULL, summed in
+ * block order (deterministic).  d_scratch: 7 (e - s) + 4 int32 (the wall-link
+ * block list of the step, then 3 doubles of per-block force partials) */
 int vf_lbm_step(const vf_config *cfg, const vf_grid *grid, int level, int32_t s, int32_t e,
                 const int32_t *d_cmap, const float *d_lengths, const float *d_fin,
                 float *d_fout, const vf_flow *flow, double *d_force, int32_t *d_scratch,

@@ -90,6 +90,8 @@ _SIGS = {
     "vf_graph_launch": (_I32, [_P, _P]),
     "vf_graph_destroy": (None, [_P]),
     "vf_launch_count": (_I64, []),
+    "vf_ktimer_start": (_I32, [_P, C.c_double]),
+    "vf_ktimer_stop": (_I32, [C.c_char_p, _I32]),
     "vf_embed_link_stats": (_I32, [_CP, _I64, _I32, _P, _SZ, _P]),
     "vf_side_sync": (_I32, []),
     "vf_check_status": (_I32, [_GP, _P]),

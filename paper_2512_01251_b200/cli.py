@@ -153,9 +153,17 @@ def cmd_simulate(c) -> int:
             fh.write(",".join(str(x) for x in r) + "\n")
     fx = float(np.mean([r[1] for r in rows])) if rows else None
     d_f = d0 * 2 ** L
-    cd = 2.0 * fx / (c["u_in"] ** 2 * np.pi * d_f * d_f / 4.0) if fx is not None else None
+    # C_D = 2 F_x / (u^2 A_ref): the frontal disc pi d^2 / 4 is the sphere's
+    # reference area; for other bodies (d = largest bounding-box extent) the
+    # same disc is only a convention, so C_D is reported for spheres alone
+    sphere = not c.get("stl") and c["primitive"] == "sphere"
+    area = np.pi * d_f * d_f / 4.0
+    cd = 2.0 * fx / (c["u_in"] ** 2 * area) if (fx is not None and sphere) else None
     summary = {"levels": grid.n_levels, "taus": h.taus, "substeps": h.substeps, "samples": len(rows),
-               "F_x_mean_lattice": fx, "C_D": cd, "D_s_finest_cells": d_f}
+               "F_x_mean_lattice": fx, "C_D": cd, "D_s_finest_cells": d_f,
+               "reference_area_finest_cells2": area,
+               "area_convention": "pi D^2/4 (sphere frontal disc)" if sphere else
+               "C_D not reported: non-sphere body; F_x / (u^2 A / 2) with A = pi d^2/4, d = largest extent"}
     print(json.dumps(summary))
     return 0
 

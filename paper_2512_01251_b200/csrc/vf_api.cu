@@ -7,6 +7,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <vector>
 
 #include <new>
 
@@ -30,10 +31,45 @@ int set_cuda_error(cudaError_t e, const char *what) {
 
 static std::atomic<long long> g_launches{0};
 
+// Per-kernel timer (vf_ktimer_start / vf_ktimer_stop): the embed runs
+// eagerly with every kernel on ONE stream (no side streams), behind a spin
+// kernel that holds the stream until the host has enqueued the whole embed,
+// so consecutive events bracket each kernel exactly.  An event is recorded
+// after every launch (check_launch) and after the memsets of the path.
+struct KTimer {
+    bool on = false;
+    cudaStream_t st = nullptr;
+    std::vector<cudaEvent_t> pool;
+    std::vector<const char *> names;
+    size_t used = 0;
+};
+static KTimer g_kt;
+
+bool kt_on() { return g_kt.on; }
+
+void kt_point(const char *name) {
+    if (!g_kt.on) return;
+    if (g_kt.used == g_kt.pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        g_kt.pool.push_back(e);
+    }
+    cudaEventRecord(g_kt.pool[g_kt.used], g_kt.st);
+    g_kt.names.push_back(name);
+    ++g_kt.used;
+}
+
 int check_launch(const char *what) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    kt_point(what);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? VF_OK : set_cuda_error(e, what);
+}
+
+__global__ void k_gate(long long cycles) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < cycles) {
+    }
 }
 
 int sm_count() {
@@ -486,7 +522,9 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     cudaStream_t st = (cudaStream_t)stream;
     SideStream *side = nullptr;
     VF_TRY(side_stream(&side));
-    cudaStream_t s2 = side->st;
+    // per-kernel timing: everything on the main stream, in order
+    const bool one = kt_on();
+    cudaStream_t s2 = one ? st : side->st;
     vf_bins *buf[2] = {&w.bins, &w.bins2};
     const int n_ev = 64;
     int k = 0;
@@ -497,7 +535,8 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     // in phase 2, where the recorded lines are resolved)
     cudaEventRecord(side->fork, st);
     cudaStreamWaitEvent(s2, side->fork, 0);
-    if (!g_serial_links) {
+    const bool serial_links = g_serial_links || one;
+    if (!serial_links) {
         cudaStreamWaitEvent(side->st3, side->fork, 0);
         VF_TRY(link_enum_impl(*cfg, faces, F, w.link_ws, w.lines_ws, side->st3, events ? events + 58 : nullptr));
         cudaEventRecord(side->join3, side->st3);
@@ -534,7 +573,7 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     VF_TRY(boundary_impl(*cfg, g, w.bcount, st));
     VF_TRY(tables_impl(g, w.bcount, cmap, d_n_b, w.tab_ws, w.tab_b, st));
     rec(events, n_ev, &k, st);  // boundary + tables done
-    if (g_serial_links) {  // measurement mode: the enumeration alone on the main stream
+    if (serial_links) {  // measurement mode: the enumeration alone on the main stream
         VF_TRY(link_enum_impl(*cfg, faces, F, w.link_ws, w.lines_ws, st, events ? events + 58 : nullptr));
         cudaEventRecord(side->join3, st);
     }
@@ -708,6 +747,54 @@ int vf_shard_links(const vf_config *cfg, const double *faces, int64_t F, vf_grid
     VF_TRY(shard_face_subset_impl(*cfg, faces, F, w.bins.d_map, w.bins.d_n_map, w.shard_ws, st));
     return link_impl(*cfg, g, cmap, faces, F, w.bins.d_map, w.bins.d_n_map, lengths, w.link_ws,
                      w.link_b, st, nullptr, d_n_b, lengths_cap);
+}
+
+int vf_ktimer_start(void *stream, double gate_us) {
+    if (g_kt.on) return set_error(VF_EARG, "vf_ktimer_start: timer already running");
+    g_kt.on = true;
+    g_kt.st = (cudaStream_t)stream;
+    g_kt.used = 0;
+    g_kt.names.clear();
+    int dev = 0, khz = 1965000;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev);
+    k_gate<<<1, 1, 0, g_kt.st>>>((long long)(gate_us * 1e-3 * khz));
+    kt_point("_start");
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? VF_OK : set_cuda_error(e, "vf_ktimer_start");
+}
+
+// stop, synchronise and report: "name<TAB>launches<TAB>total ms" lines,
+// first-appearance order; returns the bytes written (or needed)
+int vf_ktimer_stop(char *buf, int buflen) {
+    if (!g_kt.on) return set_error(VF_EARG, "vf_ktimer_stop: timer not running");
+    g_kt.on = false;
+    cudaError_t e = cudaStreamSynchronize(g_kt.st);
+    if (e != cudaSuccess) return -set_cuda_error(e, "vf_ktimer_stop");
+    std::vector<const char *> keys;
+    std::vector<double> ms;
+    std::vector<int> cnt;
+    for (size_t i = 1; i < g_kt.used; ++i) {
+        float t = 0.0f;
+        cudaEventElapsedTime(&t, g_kt.pool[i - 1], g_kt.pool[i]);
+        size_t k = 0;
+        while (k < keys.size() && strcmp(keys[k], g_kt.names[i]) != 0) ++k;
+        if (k == keys.size()) {
+            keys.push_back(g_kt.names[i]);
+            ms.push_back(0.0);
+            cnt.push_back(0);
+        }
+        ms[k] += t;
+        cnt[k] += 1;
+    }
+    int n = 0;
+    for (size_t k = 0; k < keys.size(); ++k) {
+        char line[160];
+        const int w = snprintf(line, sizeof(line), "%s\t%d\t%.6f\n", keys[k], cnt[k], ms[k]);
+        if (buf && n + w < buflen) memcpy(buf + n, line, (size_t)w + 1);
+        n += w;
+    }
+    return n;
 }
 
 int vf_check_status(const vf_grid *g, void *stream) {

@@ -728,18 +728,21 @@ struct EmitOffsets {
 int launch_compact(const uint8_t *ind, int64_t n, int32_t *map, int32_t *d_count, void *ws,
                    cudaStream_t st) {
     cudaError_t e = scan_launch(LoadU8{ind}, EmitCompact{map}, n, nullptr, d_count, ws, st);
+    kt_point("scan_kernel");
     return e == cudaSuccess ? VF_OK : set_cuda_error(e, "compact scan");
 }
 
 int launch_compact_bits(const uint16_t *bits, int L, int64_t n, int32_t *map, int32_t *d_count,
                         void *ws, cudaStream_t st) {
     cudaError_t e = scan_launch(LoadBit{bits, L}, EmitCompact{map}, n, nullptr, d_count, ws, st);
+    kt_point("scan_kernel");
     return e == cudaSuccess ? VF_OK : set_cuda_error(e, "compact scan (bits)");
 }
 
 int launch_exclusive_scan(const int32_t *in, int64_t n_bound, const int32_t *d_n, int32_t *out,
                           int32_t *d_total, void *ws, cudaStream_t st) {
     cudaError_t e = scan_launch(LoadI32{in}, EmitOffsets{out}, n_bound, d_n, d_total, ws, st);
+    kt_point("scan_kernel");
     return e == cudaSuccess ? VF_OK : set_cuda_error(e, "exclusive scan");
 }
 
@@ -808,6 +811,7 @@ int build_bins_impl(const LevelInfo &li, int nlim, const double *faces, int64_t 
         if ((rc = launch_iota(bins->d_map, F, bins->d_n_map, st))) return rc;
     }
     cudaMemsetAsync(bins->d_counts, 0, sizeof(int32_t) * (size_t)n_bins, st);
+    kt_point("memset:bin_counts");
     k_pairs<<<grid_for(F, kPairThreads, max_ctas(VF_GRID_PAIRS * 2)), kPairThreads, 0, st>>>(li, nlim, faces, map, d_n_map, F, w.slots,
                                                          w.slot_cnt, bins->d_counts, d_status);
     if ((rc = check_launch("k_pairs"))) return rc;

@@ -13,6 +13,10 @@ namespace vf {
 int set_error(int code, const char *msg);
 int set_cuda_error(cudaError_t e, const char *what);
 int check_launch(const char *what);
+// per-kernel timing (vf_ktimer_*): an event on the timed stream after each
+// launch / memset while the timer is on; no-op otherwise
+void kt_point(const char *name);
+bool kt_on();
 
 int sm_count();
 inline int max_ctas(int per_sm) { return sm_count() * per_sm; }

@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_MINB)
                 const uint64_t *__restrict__ solid64, const int32_t *__restrict__ cmap,
                 const float *__restrict__ lengths, const float *__restrict__ fin,
                 float *__restrict__ fout, vf_flow flow, int32_t *__restrict__ wall_list,
-                int32_t *__restrict__ n_wall, double *__restrict__ d_force) {
+                int32_t *__restrict__ n_wall, double *__restrict__ part) {
     __shared__ int32_t s_nb[kLbmWarps][27];
     __shared__ unsigned long long s_sol[kLbmWarps][27];
     const int64_t n = (int64_t)(e - s) * 64;
@@ -71,8 +71,8 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_MINB)
     const float omega = 1.0f / (float)flow.tau;
     const float uin[3] = {(float)flow.u_in[0], (float)flow.u_in[1], (float)flow.u_in[2]};
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    float Fx = 0.f, Fy = 0.f, Fz = 0.f;
     for (int it = blockIdx.x * kLbmWarps + w; it < nitems; it += gridDim.x * kLbmWarps) {
+        float Fx = 0.f, Fy = 0.f, Fz = 0.f;  // this block's wall momentum exchange
         const int lb = WALLS ? wall_list[it] : it;
         const int32_t b = s + lb;
         __syncwarp();
@@ -182,20 +182,44 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_MINB)
         }
         if (!WALLS && __any_sync(0xffffffffu, wall_blk) && lane == 0)
             wall_list[atomicAdd(n_wall, 1)] = lb;
-    }
-    if (WALLS && d_force) {
+        if (WALLS && part) {
+            // per-block partial: a fixed lane tree, stored at the block's
+            // local id -- independent of which warp took the block
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            Fx += __shfl_xor_sync(0xffffffffu, Fx, off);
-            Fy += __shfl_xor_sync(0xffffffffu, Fy, off);
-            Fz += __shfl_xor_sync(0xffffffffu, Fz, off);
-        }
-        if (lane == 0 && (Fx != 0.f || Fy != 0.f || Fz != 0.f)) {
-            atomicAdd(d_force + 0, (double)Fx);
-            atomicAdd(d_force + 1, (double)Fy);
-            atomicAdd(d_force + 2, (double)Fz);
+            for (int off = 16; off > 0; off >>= 1) {
+                Fx += __shfl_xor_sync(0xffffffffu, Fx, off);
+                Fy += __shfl_xor_sync(0xffffffffu, Fy, off);
+                Fz += __shfl_xor_sync(0xffffffffu, Fz, off);
+            }
+            if (lane == 0) {
+                part[3 * (int64_t)lb + 0] = (double)Fx;
+                part[3 * (int64_t)lb + 1] = (double)Fy;
+                part[3 * (int64_t)lb + 2] = (double)Fz;
+            }
         }
     }
+}
+
+// d_force += sum over the level's blocks of the per-block partials, in block
+// order with a fixed reduction tree (identical force series
+// across runs; the wall-block list order depends on atomics)
+__global__ void __launch_bounds__(256) k_lbm_force_reduce(int32_t nb, const double *__restrict__ part,
+                                                          double *__restrict__ d_force) {
+    __shared__ double s_r[3][256];
+    double a[3] = {0.0, 0.0, 0.0};
+    for (int32_t b = threadIdx.x; b < nb; b += blockDim.x)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) a[c] += part[3 * (int64_t)b + c];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) s_r[c][threadIdx.x] = a[c];
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) s_r[c][threadIdx.x] += s_r[c][threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x < 3) d_force[threadIdx.x] += s_r[threadIdx.x][0];
 }
 
 // equilibrium initialisation of the level's fluid cells (SOLID cells zero)
@@ -551,7 +575,10 @@ int vf_lbm_step(const vf_config *cfg, const vf_grid *g, int level, int32_t s, in
     cudaStream_t st = (cudaStream_t)stream;
     const int cells_x = 4 * (cfg->nb[0] << level);
     int32_t *n_wall = d_scratch, *wall_list = d_scratch + 1;
+    // per-block force partials after the wall list, 8-byte aligned
+    double *part = d_force ? reinterpret_cast<double *>(d_scratch + ((e - s + 2 + 1) & ~1)) : nullptr;
     cudaMemsetAsync(n_wall, 0, sizeof(int32_t), st);
+    if (part) cudaMemsetAsync(part, 0, sizeof(double) * 3 * (size_t)(e - s), st);
     int64_t grid = ((int64_t)(e - s) + kLbmWarps - 1) / kLbmWarps;
     if (grid > max_ctas(VF_LBM_MINB)) grid = max_ctas(VF_LBM_MINB);
     k_lbm_cells<false><<<(int)grid, kLbmWarps * 32, 0, st>>>(
@@ -561,8 +588,11 @@ int vf_lbm_step(const vf_config *cfg, const vf_grid *g, int level, int32_t s, in
     if (rc) return rc;
     k_lbm_cells<true><<<max_ctas(2), kLbmWarps * 32, 0, st>>>(
         s, e, cells_x, g->d_coords, g->d_nbr, g->d_masks, g->d_solid64, cmap, lengths, fin, fout, *flow,
-        wall_list, n_wall, d_force);
-    return check_launch("k_lbm_walls");
+        wall_list, n_wall, part);
+    int rc2 = check_launch("k_lbm_walls");
+    if (rc2 || !d_force) return rc2;
+    k_lbm_force_reduce<<<1, 256, 0, st>>>(e - s, part, d_force);
+    return check_launch("k_lbm_force_reduce");
 }
 
 }  // extern "C"

@@ -977,6 +977,7 @@ static int link_blockmap(vf_grid *g, const LevelInfo &li, const int32_t *cmap, c
     const int L = li.level;
     const int64_t nb = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
     cudaMemsetAsync(const_cast<int32_t *>(c.bmap), 0xff, sizeof(int32_t) * (size_t)nb, st);
+    kt_point("memset:block_map");
     k_blockmap<<<max_ctas(8), 256, 0, st>>>(li, L, g->d_level_start, g->d_coords, cmap,
                                             const_cast<int32_t *>(c.bmap), d_n_b, lengths_cap);
     return check_launch("k_blockmap");
@@ -1041,6 +1042,7 @@ int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *w
     cudaMemsetAsync(c.n_band, 0, 2 * sizeof(int32_t), st);
     cudaMemsetAsync(c.n_lines, 0, 3 * sizeof(int32_t), st);
     cudaMemsetAsync(c.ovf_bits, 0, ((size_t)F + 32) / 32 * sizeof(uint32_t), st);
+    kt_point("memset:link_counters");
     if (events) cudaEventRecord((cudaEvent_t)events[0], st);
     // small faces thread per face; the rest through the warp-flattened
     // kernel.  Short CTAs (no grid-stride loop in the small pass): they

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(256, VF_BOUNDARY_MINB)
 int boundary_impl(const vf_config &cfg, vf_grid *g, int32_t *bcount, cudaStream_t st) {
     const int L = g->n_levels - 1;
     cudaMemsetAsync(bcount, 0, sizeof(int32_t) * (size_t)g->capacity, st);
+    kt_point("memset:bcount");
     k_boundary<<<max_ctas(VF_GRID_BOUNDARY), 256, 0, st>>>(make_level(cfg, L), L, g->d_level_start,
                                                        g->d_nbr, g->d_coords, g->d_bflags,
                                                        g->d_masks, g->d_solid64, bcount);
@@ -150,6 +151,7 @@ int tables_impl(vf_grid *g, const int32_t *bcount, int32_t *cmap, int32_t *d_n_b
     void *scan_ws = (char *)ws + 256;
     // non-finest blocks are never mapped
     cudaMemsetAsync(cmap, 0xff, sizeof(int32_t) * (size_t)g->capacity, st);
+    kt_point("memset:cmap");
     (void)scal;
     cudaError_t ce = scan_launch_fn(LoadBnd{g->d_level_start, L, bcount}, EmitCmap{g->d_level_start, L, cmap},
                                     g->capacity, ScanLevelN{g->d_level_start, L}, d_n_b, scan_ws, st);

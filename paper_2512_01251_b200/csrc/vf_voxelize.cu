@@ -850,6 +850,7 @@ int propagate_level_impl(const LevelInfo &li, vf_grid *g, int L, void *ws, size_
     if (ws_bytes < (size_t)nb * sizeof(int32_t)) return set_error(VF_EARG, "propagate workspace too small");
     int32_t *map = (int32_t *)ws;
     cudaMemsetAsync(map, 0xff, sizeof(int32_t) * (size_t)nb, st);
+    kt_point("memset:level_map");
     k_level_map<<<max_ctas(8), 256, 0, st>>>(L, li, g->d_level_start, g->d_coords, map);
     int rc = check_launch("k_level_map");
     if (rc) return rc;

@@ -128,6 +128,8 @@ class ForestGrid:
     status: object          # (4,) int32 latched device errors
     solid64: object = None  # (cap,) int64: bit t = cell t SOLID (set by finalize)
     n_levels: int = 0
+    bcount: object = None   # (cap,) int32 boundary-cell counts of the last identify_boundary_cells
+    table: object = None    # LinkTable of the last build_boundary_tables (SPEC.md:328-345 chaining)
 
     @classmethod
     def allocate(cls, cfg: EmbedConfig, capacity: int) -> "ForestGrid":

@@ -62,18 +62,29 @@ def adapt(grid: ForestGrid, marks=None) -> ForestGrid:
 
 
 def index_maps(I, c) -> Tuple[int, int, Tuple[int, int, int], bool]:
-    """(t, t_h, I', violation) of SPEC.md:228-236.
+    """(t, t_h, I', violation) of SPEC.md:228-236, literally:
 
     t = LINEAR(I,4), t_h = LINEAR(I+1,6), I'_d = mod(4+mod(I_d+c_d,4),4)
-    (PAPER.md:949 adds c twice, pin A15), violation = the
-    increment left the block along some axis."""
+    (PAPER.md:949 adds c twice, pin A15) and the violation flag
+    AND_d ((I'_d != I_d + c_d) or c_d = 0) of SPEC.md:229 / PAPER.md:954.
+    That flag is true only when the step leaves the block along EVERY
+    non-zero axis of c (and for c = 0); the kernels read a neighbour cell
+    through the general neighbour-block direction of neighbour_direction()
+    (pin A15), which also covers steps that leave along some axes only."""
     I = tuple(int(v) for v in I)
     c = tuple(int(v) for v in c)
     t = I[0] + 4 * I[1] + 16 * I[2]
     th = (I[0] + 1) + 6 * (I[1] + 1) + 36 * (I[2] + 1)
     Ip = tuple((4 + ((I[d] + c[d]) % 4)) % 4 for d in range(3))
-    viol = any(c[d] != 0 and Ip[d] != I[d] + c[d] for d in range(3))
+    viol = all(Ip[d] != I[d] + c[d] or c[d] == 0 for d in range(3))
     return t, th, Ip, viol
+
+
+def neighbor_direction(I, c) -> Tuple[int, int, int]:
+    """Pin A15: the neighbour block holding cell I + c is the block in
+    direction (c_d if the step wraps axis d else 0)_d -- (0, 0, 0) = the
+    block itself.  This is what the boundary-cell and LBM kernels use."""
+    return tuple(int(c[d]) if not (0 <= int(I[d]) + int(c[d]) < 4) else 0 for d in range(3))
 
 
 def neighbor_slot(c) -> int:
@@ -94,12 +105,16 @@ def block_of_point(grid: ForestGrid, point, level: Optional[int] = None) -> Opti
         return None
     nb = cfg.nb
     h0 = 4.0 * cfg.dx0
-    ijk = [min(int(np.floor(p[d] / h0)), nb[d] - 1) for d in range(3)]
+
+    def cell(x, hh, n):  # block index along an axis; a point on a face -> lower index
+        return min(max(int(np.ceil(x / hh)) - 1, 0), n - 1)
+
+    ijk = [cell(p[d], h0, nb[d]) for d in range(3)]
     b = ijk[0] + nb[0] * (ijk[1] + nb[1] * ijk[2])
     L = 0
     while (level is None or L < level) and h["child"][b] >= 0:
         hL1 = h0 / 2 ** (L + 1)
-        sub = [min(int(np.floor(p[d] / hL1)), (nb[d] << (L + 1)) - 1) & 1 for d in range(3)]
+        sub = [cell(p[d], hL1, nb[d] << (L + 1)) & 1 for d in range(3)]
         b = int(h["child"][b] + sub[0] + 2 * sub[1] + 4 * sub[2])
         L += 1
     if level is not None and L != level:

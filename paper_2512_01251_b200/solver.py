@@ -93,7 +93,7 @@ class LbmLevel:
         self.f = [torch.empty((27, n), dtype=torch.float32, device="cuda") for _ in range(2)]
         self.cur = 0
         self.force = torch.zeros(3, dtype=torch.float64, device="cuda")
-        self.scratch = torch.zeros(self.e - self.s + 1, dtype=torch.int32, device="cuda")
+        self.scratch = torch.zeros(7 * (self.e - self.s) + 4, dtype=torch.int32, device="cuda")
         self.c = _lib.make_config(grid.cfg)
         self.vf = VfFlow()
         self.vf.tau = float(tau if tau is not None else flow.tau)

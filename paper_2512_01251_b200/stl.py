@@ -64,13 +64,39 @@ def _message(text: str, info, off: int) -> str:
     return f"line {ln}: bad number '{tok}' in {ctx}"
 
 
+def _ascii_canonical(text: str):
+    """A str input with non-ASCII characters (geometry.py:138-149 parses a
+    str without the ASCII check) as an equivalent ASCII stream: the
+    reference's own line split (str.splitlines) and token split (str.split,
+    Unicode whitespace included), one line per line so line numbers stay.
+    Non-ASCII tokens become a number's repr when float() accepts them, else a
+    unique ASCII placeholder that error messages map back."""
+    lines, subst = [], {}
+    for line in text.splitlines():
+        toks = []
+        for tok in line.split():
+            if not tok.isascii():
+                try:
+                    tok = repr(float(tok))
+                except ValueError:
+                    key = f"@u{len(subst)}@"
+                    subst[key] = tok
+                    tok = key
+            toks.append(tok)
+        lines.append(" ".join(toks))
+    return "\n".join(lines), subst
+
+
 def parse_stl(data: Union[bytes, str], weld_tol: Optional[float] = None,
               stream=None) -> TriangleMesh:
     """geometry.parse_stl on the GPU.  Same result arrays (bit-identical) and
     the same StlParseError / MeshError conditions and messages."""
     import torch
     lib = _lib.require_cuda()
-    raw = data.encode("latin-1") if isinstance(data, str) else bytes(data)
+    subst = {}
+    if isinstance(data, str) and not data.isascii():
+        data, subst = _ascii_canonical(data)
+    raw = data.encode("ascii") if isinstance(data, str) else bytes(data)
     n = len(raw)
     st = _lib.stream_ptr(stream)
     # one pageable H2D copy of the text (no host-side copy / pinning of the bytes)
@@ -86,11 +112,14 @@ def parse_stl(data: Union[bytes, str], weld_tol: Optional[float] = None,
     _lib.check(lib.vf_stl_scan(_lib.ptr(d_text), n, _lib.ptr(ws), ws.numel(), info, ext, C.byref(off), st),
                "parse_stl")
     info = list(info)
-    if info[1] == 4 or (isinstance(data, str) and not data.isascii()):
+    if info[1] == 4:  # bytes input only: a str is canonicalised to ASCII above
         raise StlParseError("not an ASCII STL stream")
     text = raw.decode("ascii") if info[1] else ""
     if info[1]:
-        raise StlParseError(_message(text, info, int(off.value)))
+        msg = _message(text, info, int(off.value))
+        for k, v in subst.items():
+            msg = msg.replace(k, v)
+        raise StlParseError(msg)
     nf = int(info[0])
     if nf == 0:
         raise StlParseError("empty mesh: STL contains zero facets")

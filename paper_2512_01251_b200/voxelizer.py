@@ -7,8 +7,10 @@ Drop-in for the SPEC ops of ``voxforest.voxelizer``:
   finalize_masks(grid, L)                         PAPER.md:832
   mark_near_wall_refinement(grid, L, d_spec)      PAPER.md:858-871
   identify_boundary_cells(grid)                   PAPER.md:941-959
-  build_boundary_tables(grid, counts)             PAPER.md:961-969
-  compute_link_lengths(grid, bins, mesh, table)   PAPER.md:971-977
+  build_boundary_tables(grid)                     PAPER.md:961-969
+  compute_link_lengths(grid, bins, mesh)          PAPER.md:971-977
+  (SPEC.md:328 / :337 signatures; the counts and the table may also be
+  passed explicitly, else the grid carries them from the previous op)
   embed_geometry(grid, mesh, config)              SPEC.md:346-354 (native driver)
 """
 from __future__ import annotations
@@ -84,13 +86,23 @@ def identify_boundary_cells(grid: ForestGrid):
     counts = torch.empty(grid.capacity, dtype=torch.int32, device="cuda")
     _lib.check(lib.vf_boundary_cells(C.byref(c), C.byref(gs), _lib.ptr(counts), _lib.stream_ptr()),
                "identify_boundary_cells")
+    grid.bcount = counts
     return counts
 
 
-def build_boundary_tables(grid: ForestGrid, counts) -> LinkTable:
-    """Contraction map (ascending block id) and LUT allocation, lengths = -1."""
+def build_boundary_tables(grid: ForestGrid, counts=None) -> LinkTable:
+    """contraction map (ascending block id) and LUT
+    allocation, lengths = -1.  ``counts``: per-block boundary-cell counts;
+    default: those of the grid's last identify_boundary_cells, else counted
+    from the finest level's BOUNDARY cell masks."""
     import torch
     lib = _lib.require_cuda()
+    if counts is None:
+        counts = grid.bcount
+    if counts is None:
+        counts = torch.zeros(grid.capacity, dtype=torch.int32, device="cuda")
+        s, e = grid.level_range(grid.n_levels - 1)
+        counts[s:e] = (grid.masks[s:e] == _lib.BOUNDARY).sum(dim=1, dtype=torch.int32)
     gs = grid._struct()
     c = _lib.make_config(grid.cfg)
     cmap = torch.empty(grid.capacity, dtype=torch.int32, device="cuda")
@@ -102,16 +114,23 @@ def build_boundary_tables(grid: ForestGrid, counts) -> LinkTable:
     n_b = int(nb.item())
     lengths = torch.full((n_b, 27, 64), -1.0, dtype=torch.float32, device="cuda")
     bc_ids = torch.zeros((n_b, 27, 64), dtype=torch.int8, device="cuda")
-    return LinkTable(lengths, bc_ids, cmap[:grid.n_used], n_b)
+    grid.table = LinkTable(lengths, bc_ids, cmap[:grid.n_used], n_b)
+    return grid.table
 
 
 def compute_link_lengths(grid: ForestGrid, bins: Optional[BinLevel], mesh,
-                         table: LinkTable) -> LinkTable:
-    """Fill ``table.lengths`` with q = d/dx in (0, 1] (min over faces) for every
-    cell of every mapped block and q = 1..26; -1 where no wall is within one
-    link.  ``bins`` (all-directions BinLevel) only restricts the face set via
-    its filter map; the result is invariant to it."""
+                         table: Optional[LinkTable] = None) -> LinkTable:
+    """fill the LUT with q = d/dx in (0, 1] (min over faces)
+    for every cell of every mapped block and q = 1..26; -1 where no wall is
+    within one link.  ``table``: default the grid's last
+    build_boundary_tables.  ``bins`` (all-directions BinLevel) only restricts
+    the face set via its filter map; the result is invariant to it
+    (SPEC.md:174)."""
     lib = _lib.require_cuda()
+    if table is None:
+        table = grid.table
+    if table is None:
+        raise ValueError("compute_link_lengths: no LinkTable (call build_boundary_tables first)")
     dm = as_device_mesh(mesh)
     gs = grid._struct()
     c = _lib.make_config(grid.cfg)
@@ -317,6 +336,8 @@ class EmbedEngine:
                 self._host_async = torch.zeros(8, dtype=torch.int32).pin_memory()
             self._host_async[0:4].copy_(self.grid.status, non_blocking=True)
             self._host_async[4:5].copy_(self.n_b_dev, non_blocking=True)
+            L = self.cfg.l_max
+            self._host_async[5:6].copy_(self.grid.level_start[L:L + 1], non_blocking=True)
         table = LinkTable(self.lengths[:n_b], self.bc_ids[:n_b], self.cmap, n_b)
         return self.grid, table
 
@@ -329,6 +350,9 @@ class EmbedEngine:
             _lib.check(self.lib.vf_check_status(C.byref(gs), _lib.stream_ptr(self.stream)), "embed_geometry")
         if h[4] != int(self.host[4]):
             raise RuntimeError("N_b changed between pipelined embeds of the same mesh")
+        if hasattr(self, "_host_async") and h[5] != self._n_used:
+            raise RuntimeError("the block count changed between pipelined embeds: the downloaded "
+                               "grid slices were sized by the previous synchronous run")
 
     def embed_host_async(self, faces_coord, normals, out, in_stream, out_stream):
         """One pipelined end-to-end step: pinned host faces -> H2D on
@@ -403,6 +427,35 @@ class EmbedEngine:
         t.total = ev[0].elapsed_time(ev[self.n_events - 1])
         return t
 
+    def kernel_times(self, gate_us: float = 3000.0, use_filter: Optional[bool] = None) -> dict:
+        """Per-kernel device times of one eager embed with every kernel on
+        the engine stream in order (vf_ktimer_*): {name: (launches, total
+        ms)}.  Attribution only -- the production schedule overlaps the bins
+        and the cut-link enumeration with the level pipeline."""
+        import torch
+        if self.lengths is None:
+            self.run()
+        uf = bool(self.cfg.use_filter if use_filter is None else use_filter)
+        st = _lib.stream_ptr(self.stream)
+        torch.cuda.synchronize()
+        _lib.check(self.lib.vf_ktimer_start(st, float(gate_us)), "kernel_times")
+        try:
+            with torch.cuda.stream(self.stream):
+                self.grid.status.zero_()
+                gs = self._phase1(uf, st, None)
+                self._phase2(gs, st, None)
+        finally:
+            buf = C.create_string_buffer(1 << 16)
+            n = self.lib.vf_ktimer_stop(buf, len(buf))
+        if n < 0:
+            _lib.check(-n, "kernel_times")
+        self._finish(self.stream)
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, cnt, ms = line.split("\t")
+            out[name] = (int(cnt), float(ms))
+        return out
+
     def link_stats(self) -> dict:
         """Counters of the last embed's cut-link pass (synchronises): lines
         recorded by the enumeration and the buffer capacity, faces whose lines
@@ -466,12 +519,58 @@ class EmbedEngine:
         return out, h2d, d2h
 
 
+_ENGINES: "collections.OrderedDict" = None
+_ENGINE_CACHE = 4
+
+
+def _mesh_key(mesh):
+    """Identity of a mesh's geometry: the face/normal arrays (object and
+    buffer address) -- a TriangleMesh is immutable (geometry.py:65-111)."""
+    import weakref
+    fc, nrm = mesh.faces_coord, mesh.normals
+    try:
+        ref = weakref.ref(mesh)
+    except TypeError:
+        ref = None
+    addr = lambda a: a.ctypes.data if hasattr(a, "ctypes") else (a.data_ptr() if hasattr(a, "data_ptr") else id(a))
+    return (id(mesh), id(fc), addr(fc), id(nrm), addr(nrm), tuple(getattr(fc, "shape", ()))), ref
+
+
 def embed_geometry(grid: Optional[ForestGrid], mesh, cfg: EmbedConfig,
-                   capacity: Optional[int] = None) -> Tuple[ForestGrid, LinkTable]:
+                   capacity: Optional[int] = None, copy: bool = False) -> Tuple[ForestGrid, LinkTable]:
     """build the forest level by level around the mesh and
     return (grid, LinkTable).  ``grid`` may be a fresh root grid from
-    init_forest (its capacity is reused) or None."""
+    init_forest (its capacity is reused) or None.
+
+    The EmbedEngine (device mesh, forest arrays, workspace, LUT, CUDA graph)
+    is cached per (mesh geometry, cfg, capacity), up to 4 engines: a repeated
+    call is one graph launch.  The returned grid / table are that engine's
+    buffers and are overwritten by the next call with the same key; pass
+    ``copy=True`` for independent copies."""
+    import collections
+    global _ENGINES
     if grid is not None and capacity is None:
         capacity = grid.capacity
-    eng = EmbedEngine(mesh, cfg, capacity, use_graph=False)
-    return eng.run()
+    if _ENGINES is None:
+        _ENGINES = collections.OrderedDict()
+    mk, ref = _mesh_key(mesh)
+    key = (mk, cfg, capacity)
+    hit = _ENGINES.get(key)
+    eng = None
+    if hit is not None:
+        eng, r = hit
+        if r is not None and r() is not mesh:   # id reused by another object
+            eng = None
+    if eng is None:
+        eng = EmbedEngine(mesh, cfg, capacity)
+        _ENGINES[key] = (eng, ref)
+        while len(_ENGINES) > _ENGINE_CACHE:
+            _ENGINES.popitem(last=False)
+    else:
+        _ENGINES.move_to_end(key)
+    g, t = eng.run()
+    if copy:
+        g = dataclasses.replace(g, **{f.name: getattr(g, f.name).clone() for f in dataclasses.fields(g)
+                                      if hasattr(getattr(g, f.name), "clone")})
+        t = LinkTable(t.lengths.clone(), t.bc_ids.clone(), t.contraction_map.clone(), t.n_b)
+    return g, t

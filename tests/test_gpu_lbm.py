@@ -116,3 +116,19 @@ def test_closed_box_mass_conservation():
     lv.step(10)
     m1 = lv.state[:, fluid].double().sum().item()
     assert abs(m1 - m0) / m0 < 2e-6
+
+
+def test_force_deterministic(emb):
+    """the wall force is summed per block in block order, so the
+    force series is bitwise identical across runs."""
+    cfg, grid, table = emb
+    L = grid.n_levels - 1
+    g = grid.to_numpy()
+    f0 = perturbed_state(g["masks"], *grid.level_range(L), np.random.default_rng(11), u=(0.04, 0, 0))
+    series = []
+    for _ in range(3):
+        lv = LbmLevel(grid, L, table, FlowConfig(Re=20.0, u_in=0.04, D_s=16.0, bc_scheme="IBB"))
+        lv.state.copy_(torch.from_numpy(f0))
+        series.append(np.stack([lv.step(1).cpu().numpy().copy() for _ in range(4)]))
+    assert np.abs(series[0]).max() > 0
+    assert np.array_equal(series[0], series[1]) and np.array_equal(series[0], series[2])

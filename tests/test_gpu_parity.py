@@ -230,14 +230,68 @@ def test_stage_boundary_tables_links(O, torus):
     grid_equal(gg.to_numpy(), g)
     n = g.n_used
     assert np.array_equal(counts.cpu().numpy()[:n], bc[:n])
-    table = voxelizer.build_boundary_tables(gg, counts)
+    table = voxelizer.build_boundary_tables(gg)           # SPEC.md:328 signature
     nb, cmap = O.tables(g, bc)
     assert table.n_b == nb
     assert np.array_equal(table.contraction_map.cpu().numpy(), cmap)
     md = O.build_bins(torus.faces_coord, torus.normals, cfg, 2, mode=1)
     lr = O.link_lengths(g, cfg, cmap, nb, md, torus.faces_coord, torus.normals)
-    voxelizer.compute_link_lengths(gg, None, torus, table)
+    t2 = voxelizer.compute_link_lengths(gg, None, torus)   # SPEC.md:337 signature
+    assert t2 is table
     check_links(table.lengths.cpu().numpy(), lr)
+    # explicit counts / table (the extended form) and counts from the masks
+    gg.bcount = None
+    t3 = voxelizer.build_boundary_tables(gg)
+    assert t3.n_b == nb and np.array_equal(t3.contraction_map.cpu().numpy(), cmap)
+    voxelizer.compute_link_lengths(gg, None, torus, voxelizer.build_boundary_tables(gg, counts))
+    check_links(gg.table.lengths.cpu().numpy(), lr)
+
+
+def test_block_of_point_exhaustive():
+    """1,000 random points, block_of_point vs an exhaustive
+    containment scan over the leaves and over each level; SPEC.md:244 ties
+    at block faces go to the lower index."""
+    from paper_2512_01251_b200.forest import block_of_point
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    grid, _ = EmbedEngine(make_torus(60, 30), cfg).run()
+    g = grid.to_numpy()
+    n = int(g["level_start"][grid.n_levels])
+    co, child = g["coords"][:n], g["child"][:n]
+    h = 4.0 * cfg.dx0 / 2.0 ** co[:, 3]
+    lo = co[:, :3] * h[:, None]
+    hi = lo + h[:, None]
+    rng = np.random.default_rng(7)
+    for p in rng.random((1000, 3)):
+        inside = np.all((lo <= p) & (p <= hi), axis=1)
+        leaves = np.nonzero(inside & (child < 0))[0]
+        assert len(leaves) == 1
+        assert block_of_point(grid, p) == leaves[0]
+        for L in range(grid.n_levels):
+            at = np.nonzero(inside & (co[:, 3] == L))[0]
+            got = block_of_point(grid, p, L)
+            assert (got is None and len(at) == 0) or (len(at) == 1 and got == at[0])
+    # a point on a root-block corner goes to the lower-index block
+    h0 = 4.0 * cfg.dx0
+    b = block_of_point(grid, (h0, h0, h0), 0)
+    assert tuple(co[b, :3]) == (0, 0, 0)
+
+
+def test_embed_geometry_cached(O, torus):
+    """SPEC.md:346 embed_geometry: the engine (and its graph) is reused for
+    the same mesh + config; results equal the oracle; copy=True detaches."""
+    from paper_2512_01251_b200.voxelizer import embed_geometry, _ENGINES
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    g1, t1 = embed_geometry(None, torus, cfg)
+    g2, t2 = embed_geometry(None, torus, cfg)
+    assert g1 is g2 and t2.lengths.data_ptr() == t1.lengths.data_ptr()
+    g3, t3 = embed_geometry(None, torus, cfg, copy=True)
+    assert t3.lengths.data_ptr() != t1.lengths.data_ptr()
+    ref = O.embed(torus.faces_coord, torus.normals, cfg, capacity=g3.capacity)
+    grid_equal(g3.to_numpy(), ref.grid)
+    check_links(t3.lengths.cpu().numpy(), ref.lengths)
+    other = make_icosphere((0.5, 0.5, 0.5), 0.5, 3)
+    g4, _ = embed_geometry(None, other, cfg)
+    assert g4 is not g1
 
 
 def _embed_compare(O, mesh, cfg, use_filter=True):
@@ -550,3 +604,18 @@ def test_link_stats(torus):
     assert st["overflow_faces"] == 0 and 0 <= st["band"] <= st["band_cap"]
     assert 0 <= st["large_faces"] <= torus.n_faces
     assert int((table.lengths >= 0).sum()) > 0
+
+
+def test_kernel_timer(O, torus):
+    """vf_ktimer_*: per-kernel times of one serial eager embed; the embed it
+    times gives the oracle's result (same kernels, one stream)."""
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    eng = EmbedEngine(torus, cfg)
+    eng.run()
+    kt = eng.kernel_times()
+    assert "k_voxelize" in kt and "k_pairs" in kt and kt["k_voxelize"][0] == cfg.l_max
+    assert all(c > 0 and ms >= 0 for c, ms in kt.values())
+    ref = O.embed(torus.faces_coord, torus.normals, cfg, capacity=eng.grid.capacity)
+    grid_equal(eng.grid.to_numpy(), ref.grid)
+    tab = eng.run()[1]
+    check_links(tab.lengths.cpu().numpy(), ref.lengths)

@@ -103,6 +103,23 @@ def test_index_maps_examples():
     assert Ip == (2, 1, 1) and not v
 
 
+def test_index_maps_spec_formula_and_neighbor_direction():
+    """Every (I, c): the SPEC.md:229 violation flag literally (AND over the
+    axes), and the general neighbour-block direction of pin A15 the kernels
+    use: cell I + c lies in the block at neighbor_direction(I, c), at I'."""
+    import itertools
+    from paper_2512_01251_b200.forest import index_maps, neighbor_direction
+    from paper_2512_01251_b200.lattice import D3Q27_C
+    for I in itertools.product(range(4), repeat=3):
+        for c in D3Q27_C:
+            t, th, Ip, v = index_maps(I, c)
+            assert t == I[0] + 4 * I[1] + 16 * I[2] and th == (I[0] + 1) + 6 * (I[1] + 1) + 36 * (I[2] + 1)
+            assert v == all((Ip[d] != I[d] + c[d]) or c[d] == 0 for d in range(3))
+            nd = neighbor_direction(I, c)
+            for d in range(3):
+                assert 4 * nd[d] + Ip[d] == I[d] + c[d]
+
+
 def test_init_forest_links(O):
     cfg = EmbedConfig(n_x=16, l_max=2)
     g = O.init_forest(cfg, 64)
