@@ -129,22 +129,150 @@ def ncu_traffic(config, *kernels):
     return float(sum(d[k]["dram_bytes"] for k in kernels if k in d))
 
 
-def cpu_baseline(mesh, cfg, cells, repeat=1):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(mesh, cfg, cells, repeat=3):
+    """The oracle port (the reference ships no implementation of this path)
+    on all host cores: median of `repeat` full embeds; also returns the
+    oracle's algorithmic operation counters."""
     from oracle import oracle as O
     O.build()
     thr = len(os.sched_getaffinity(0))
     O.set_threads(thr)
     fc, nrm = mesh.faces_coord, mesh.normals
     cap = cfg.block_capacity(float(mesh.face_areas().sum()))
-    best = None
+    ts = []
     for _ in range(repeat):
         t0 = time.perf_counter()
         O.embed(fc, nrm, cfg, cap)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    return {"value": cells / best, "unit": UNIT, "cores": thr, "kind": "port",
-            "sample": f"full embed of the same mesh ({repeat} run, best), {best * 1e3:.1f} ms",
-            "ms": best * 1e3}
+        ts.append(time.perf_counter() - t0)
+    ops = O.op_counters()
+    med_s = float(np.median(ts))
+    return {"value": cells / med_s, "unit": UNIT, "cores": thr, "kind": "port", "cpu_model": cpu_model(),
+            "sample": f"full embed of the same mesh, median of {repeat} runs: {med_s * 1e3:.1f} ms "
+                      f"(min {min(ts) * 1e3:.1f})",
+            "ms": med_s * 1e3}, ops
+
+
+def fp_peaks():
+    """Measured FP32 / FP64 instruction rates (tools/micro/fp_peak.cu on this
+    pool's B200, profiles/fp_peaks.json): one counted op = one instruction."""
+    p = os.path.join(ROOT, "profiles", "fp_peaks.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["fp32_add_tinstr"] * 1e12, d["fp64_add_tinstr"] * 1e12, "measured (profiles/fp_peaks.json)"
+    # nominal: 148 SMs x 128 FP32 / 64 FP64 lanes x 1.965 GHz
+    return 37.2e12, 18.6e12, "nominal"
+
+
+def level_counts(eng, mesh, cfg):
+    """Per-level counts behind the algorithmic bytes: blocks N_L, kept faces
+    F_k,L and pairs P_L of the 1D bins, bin faces of the level's blocks W_L
+    (sum over blocks of their bin's face count), through the SPEC API."""
+    import torch
+    from paper_2512_01251_b200 import binning
+    g = eng.grid
+    ls = g.level_starts()
+    out = []
+    for L in range(g.n_levels):
+        s, e = int(ls[L]), int(ls[L + 1])
+        bl = binning.build_level(mesh, L, cfg)
+        Bx, By, _ = cfg.bins(L)
+        co = g.coords[s:e].long()
+        idx = co[:, 0] + Bx * (co[:, 1] + By * co[:, 2])
+        W = int(bl.counts.long()[idx].sum().item())
+        out.append({"level": L, "blocks": e - s, "kept_faces": int(bl.filter_map.compact_map.numel()),
+                    "pairs": int(bl.counts.long().sum().item()), "bin_faces_of_blocks": W,
+                    "bins": cfg.n_bins(L)})
+        del bl
+        torch.cuda.empty_cache()
+    return out
+
+
+def kernel_rooflines(kt, lv, cfg, F, n_b, stats, ops, hbm, fp32, fp64, traffic):
+    """Per-kernel roofline entries: algorithmic bytes (SURVEY.md §8d
+    formulas) and ops (the oracle's counters for the FP64
+    stages, the enumeration's FP32 intersection tests) per embed, over the
+    kernel's device time from the per-kernel CUDA events (kt: {name:
+    (launches, ms)}); frac = max(bytes/t / HBM, ops/t / FP peak)."""
+    Lf = len(lv) - 1
+    N = [x["blocks"] for x in lv]
+    nprop = cfg.n_prop
+    b_ind = F * (96 + 2)
+    b_pairs = sum(x["kept_faces"] * 104 + x["pairs"] * 8 for x in lv)
+    b_scat = sum(x["kept_faces"] * 8 + x["pairs"] * 16 for x in lv)
+    b_scan = sum(x["bins"] * 8 + F * 2 + x["kept_faces"] * 4 for x in lv)
+    b_vox = sum(x["blocks"] * 136 + x["bin_faces_of_blocks"] * 100 for x in lv)
+    b_rows = sum(n * (128 + 4) for n in N)
+    b_mark = sum(N[L] * (27 * 4 + 27 + 1) * (nprop + 2) for L in range(Lf))
+    b_adapt = sum(N[L + 1] * 304 + N[L] * 108 for L in range(Lf))
+    b_bnd = N[Lf] * (27 * (4 + 8) + 64 + 64)
+    lines, tests = stats["lines"], stats["tests"]
+    b_enum = F * 96 + lines * 16
+    b_res = lines * 16 + n_b * 27 * 64 * 4
+    b_fill = n_b * 27 * 64 * 4
+    o = lambda k: ops.get(k, {}).get("sat_ops", 0) + ops.get(k, {}).get("other_ops", 0) if ops else None
+    rows = [
+        ("k_indicators_all", ["k_indicators_all"], b_ind, o("indicators"), "fp64",
+         "1D ray indicators of every level, one pass over the 96-B face records; ops: the oracle's SAT ops"),
+        ("k_pairs", ["k_pairs"], b_pairs, o("pairs"), "fp64",
+         "Alg. 2 bin pairs of every level; ops: the oracle's per-candidate SAT ops"),
+        ("scan_kernel", ["scan_kernel"], b_scan, None, None, "compactions + dense bin offsets + tables"),
+        ("k_scatter_slots", ["k_scatter_slots"], b_scat, None, None, "counting-sort scatter"),
+        ("k_voxelize", ["k_voxelize"], b_vox, o("voxelize"), "fp64",
+         "Alg. 3, every level; ops: the oracle's slab-SAT ops + 4 x 11 per accepted (row, face)"),
+        ("k_xrows", ["k_level_map", "k_xrows"], b_rows, None, None, "Alg. 5 +-x rows + finalize (+ level map)"),
+        ("k_mark", ["k_mark_sb", "k_mark_adj", "k_mark_prop"], b_mark, None, None,
+         "near-wall marking, (N_prop + 2) passes"),
+        ("k_adapt", ["k_adapt_level", "k_adapt_children"], b_adapt, None, None, "refine-only adapt"),
+        ("k_boundary", ["k_boundary"], b_bnd, None, None, "boundary cells (finest level)"),
+        ("k_links_enum", ["k_links_small", "k_links_enum"], b_enum, tests * 18 if tests else None, "fp32",
+         "cut-link line enumeration; ops: 18 FP32 ops per lattice line classified (3 edge functions + tests)"),
+        ("k_links_resolve", ["k_links_resolve", "k_links_band", "k_links_ovf", "k_links_full", "k_blockmap"],
+         b_res, None, None, "line records -> FP64 q -> LUT (atomicMin)"),
+        ("k_fill_lut", ["k_fill_lut"], b_fill, None, None, "LUT -1 initialisation"),
+    ]
+    out = []
+    for name, ks, nbytes, nops, pipe, note in rows:
+        ms = sum(kt[k][1] for k in ks if k in kt)
+        launches = sum(kt[k][0] for k in ks if k in kt)
+        if ms <= 0:
+            continue
+        gbs = nbytes / (ms / 1e3) / 1e9
+        e = {"kernel": name, "launches_per_embed": launches, "ms_per_embed": ms,
+             "algorithmic_bytes": int(nbytes), "achieved_gbs": gbs, "hbm_frac": gbs / hbm,
+             "traffic": (sum(traffic[k]["dram_bytes"] * traffic[k].get("launches_per_embed", 1)
+                             for k in ks if k in traffic) if traffic else None), "note": note}
+        if nops:
+            peak = fp64 if pipe == "fp64" else fp32
+            rate = nops / (ms / 1e3)
+            e.update({"algorithmic_ops": int(nops), "ops_pipe": pipe, "achieved_tops": rate / 1e12,
+                      "ops_frac": rate / peak})
+        # every kernel of the path is bounded by HBM bytes or by latency /
+        # issue (none is a dense FP pipe workload): frac is the HBM fraction.
+        # ops_frac is context: for the FP64 stages it counts the ORACLE's
+        # exact SAT work (>1 = the FP32 classifiers skip that much of it), for
+        # the enumeration the FP32 intersection tests actually executed
+        e["bound"], e["frac"] = "hbm", e["hbm_frac"]
+        out.append(e)
+    return out
+
+
+def ncu_kernel_traffic(config):
+    """Per-kernel DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum)
+    per launch from the committed ncu --set full summary, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    return json.load(open(p)).get(config + "_kernels")
 
 
 def dist_setup():
@@ -337,7 +465,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="shard", choices=["shard", "objects"],
                     help="N>1: block-shard ONE mesh (strong scaling, NCCL flag exchange) or "
                          "embed independent translated copies (weak scaling, no collective)")
@@ -398,6 +526,7 @@ def main():
     F = eng.mesh.n_faces
     peak, peak_kind = peaks()
     stages, roofline, kernels_per_step = None, None, launches // max(args.steps, 1)
+    per_kernel = None
     if not sharded:
         n_b = int(eng.n_b_host[0])
         # kernels per step: count one eager (non-graph) embed
@@ -425,6 +554,11 @@ def main():
             link_ovl.append(eng.link_kernel_ms())
         stages = {k: med([getattr(s, k) for s in stage]) for k in
                   ("binning", "voxelization", "refinement", "boundary", "links", "total")}
+        # per-kernel device times: every kernel of one eager embed on the
+        # engine stream in order, CUDA events after each launch (median of 3)
+        kts = [eng.kernel_times() for _ in range(3)]
+        kt = {k: (kts[0][k][0], med([x[k][1] for x in kts if k in x])) for k in kts[0]}
+        link_stats = eng.link_stats()
         # dominant kernel k_links (the cut-link LUT):
         # algorithmic bytes per launch = the face records read once (96 B/face)
         # + the LUT of the mapped blocks written once (27 x 64 x 4 = 6912 B per
@@ -432,16 +566,16 @@ def main():
         link_bytes = F * 96 + n_b * 27 * 64 * 4
         lk = med(link_ms)
         achieved = link_bytes / (lk / 1e3) / 1e9
-        roofline = {"kernel": "k_links", "bound": "hbm", "achieved": achieved, "peak": peak,
+        roofline = {"kernel": "cut-link group", "bound": "hbm", "achieved": achieved, "peak": peak,
                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": ncu_traffic(args.config, "k_links_small", "k_links_enum", "k_links_resolve"), "kernel_ms": lk,
-                    "algorithmic_bytes": int(link_bytes), "kernel_ms_overlapped": med(link_ovl),
+                    "traffic": ncu_traffic(args.config, "k_links_small", "k_links_enum", "k_links_resolve",
+                                           "k_fill_lut"),
+                    "kernel_ms": lk, "algorithmic_bytes": int(link_bytes),
+                    "kernel_ms_overlapped": med(link_ovl),
                     "timed": "CUDA events around the cut-link kernels run alone (vf_set_serial_links): "
-                             "the grid-independent line enumeration (k_links_small: faces <= 1.5 cells, "
-                             "thread per face; k_links<2>: larger faces, warp-flattened) + the resolution after "
-                             "the tables (k_links_resolve, overflow faces, band list, fallback); "
-                             "kernel_ms_overlapped = the same events in the production schedule, where "
-                             "the enumeration shares the SMs with the level pipeline on a side stream"}
+                             "the grid-independent line enumeration + the resolution after the tables + the "
+                             "LUT -1 fill (k_fill_lut, the kernel that writes the LUT's 6912 B per boundary "
+                             "block); kernel_ms_overlapped = the same events in the production schedule"}
     else:
         n_b = int(run()[1].n_b)
 
@@ -499,9 +633,27 @@ def main():
 
     if rank != 0:
         return
-    cpu = None
+    cpu, ops = None, None
     if not args.no_cpu_baseline and ws == 1:
-        cpu = cpu_baseline(mesh, cfg, cells)
+        cpu, ops = cpu_baseline(mesh, cfg, cells, repeat=3 if F > 1_000_000 else 10)
+    if not sharded:
+        fp32, fp64, fp_kind = fp_peaks()
+        lv = level_counts(eng, mesh, cfg)
+        per_kernel = kernel_rooflines(kt, lv, cfg, F, n_b, link_stats, ops, peak, fp32, fp64,
+                                      ncu_kernel_traffic(args.config))
+        dom = max(per_kernel, key=lambda e: e["ms_per_embed"])
+        roofline = {"kernel": dom["kernel"], "bound": "hbm", "achieved": dom["achieved_gbs"], "peak": peak,
+                    "peak_kind": peak_kind, "unit": "GB/s", "frac": dom["frac"],
+                    "traffic": dom["traffic"], "kernel_ms": dom["ms_per_embed"],
+                    "algorithmic_bytes": dom["algorithmic_bytes"],
+                    "algorithmic_ops": dom.get("algorithmic_ops"),
+                    "timed": "the dominant kernel (largest device time per embed) from per-kernel CUDA events "
+                             "of one eager embed with every kernel on one stream (vf_ktimer); roofline.kernels "
+                             "holds every kernel: frac = algorithmic bytes/t / measured HBM copy peak; ops_frac "
+                             "= algorithmic ops/t / measured FP32 or FP64 instruction rate (context)",
+                    "links_group": roofline, "level_counts": lv, "link_stats": link_stats,
+                    "fp_peaks_tops": {"fp32": fp32 / 1e12, "fp64": fp64 / 1e12, "kind": fp_kind},
+                    "kernels": per_kernel}
     par = "single GPU"
     if ws > 1:
         par = (f"block-sharded x{ws} (row ownership, NCCL all-reduce of per-level flags, "

@@ -240,9 +240,10 @@ int vf_ktimer_start(void *stream, double gate_us);
 int vf_ktimer_stop(char *buf, int buflen);
 
 /* Counters of the last embed's cut-link pass on this workspace (synchronous):
- * out[6] = {piercing lines recorded, line capacity, faces whose lines
+ * out[7] = {piercing lines recorded, line capacity, faces whose lines
  * overflowed (redone by the direct kernel), band candidates, band capacity,
- * faces enumerated by the large-face kernel}. */
+ * faces enumerated by the large-face kernel, lattice lines classified by the
+ * enumeration (FP32 intersection tests)}. */
 int vf_embed_link_stats(const vf_config *cfg, int64_t F, int32_t capacity, void *ws, size_t ws_bytes,
                         int64_t *out);
 /* multi-GPU exchange helper: zero the level-L entries of blocks this rank

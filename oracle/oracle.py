@@ -74,6 +74,7 @@ def lib():
             "orc_link_lengths": (i32, [P, P, P, i64, P, P, P, P, P, P]),
             "orc_embed": (i32, [P, P, P, P, i64, i32, C.POINTER(P), P]),
             "orc_links_nb": (i64, [P]),
+            "orc_op_counters": (None, [P]),
             "orc_links_copy": (None, [P, P, P]),
             "orc_links_free": (None, [P]),
             "orc_parity_inside": (None, [P, i64, P, i64, C.c_double, P]),
@@ -325,6 +326,18 @@ def embed(fc, nrm, cfg, capacity, use_filter=True):
     lib().orc_links_copy(h, _p(cmap), _p(lengths))
     lib().orc_links_free(h)
     return EmbedResult(g, nb, cmap[:g.n_used].copy(), lengths[:nb * 27 * 64].reshape(nb, 27, 64), st)
+
+
+OP_STAGES = ("indicators", "pairs", "voxelize", "md_bins", "link_lengths")
+
+
+def op_counters():
+    """Algorithmic operation counts of the last embed() (then reset), per
+    stage: {stage: {"sat_calls", "sat_ops", "other_ops"}}."""
+    out = np.zeros((5, 3), dtype=np.uint64)
+    lib().orc_op_counters(_p(out))
+    return {k: {"sat_calls": int(r[0]), "sat_ops": int(r[1]), "other_ops": int(r[2])}
+            for k, r in zip(OP_STAGES, out)}
 
 
 def parity_inside(fc, pts, tol=1e-9):

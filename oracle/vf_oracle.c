@@ -103,24 +103,63 @@ static inline int axis_gap_2d(int axis, double v1x, double v1y, double v2x,
     return (tmax < rmin) || (rmax < tmin);
 }
 
+/* Algorithmic operation counters (the roofline's ops come
+ * from the oracle's branch path).  Per thread, flushed per stage by
+ * orc_ops_flush: SAT calls, SAT FP64 ops executed (54 for the plane-cut test
+ * + 34 per axis-gap test evaluated, geometry.py:441-500) and the stage's
+ * other FP64 ops (distance evaluations). */
+static _Thread_local uint64_t t_sat_calls, t_sat_ops, t_eval_ops;
+enum { ORC_ST_IND = 0, ORC_ST_PAIRS, ORC_ST_VOX, ORC_ST_MD, ORC_ST_LINKS, ORC_NST };
+static uint64_t g_ops[ORC_NST][3];
+
+static void orc_ops_flush(int stage) {
+#pragma omp parallel
+    {
+#pragma omp atomic
+        g_ops[stage][0] += t_sat_calls;
+#pragma omp atomic
+        g_ops[stage][1] += t_sat_ops;
+#pragma omp atomic
+        g_ops[stage][2] += t_eval_ops;
+        t_sat_calls = t_sat_ops = t_eval_ops = 0;
+    }
+    /* the calling thread too (outside a team it is thread 0 of the region) */
+}
+
+/* counters of the stages since the last call, then reset:
+ * out[5][3] = {indicators 1D, bin pairs, voxelize, MD bins, link lengths} x
+ * {SAT calls, SAT ops, other ops} */
+void orc_op_counters(uint64_t *out) {
+    memcpy(out, g_ops, sizeof(g_ops));
+    memset(g_ops, 0, sizeof(g_ops));
+}
+
 /* geometry.py:484-500 */
 static inline int sat3(const double *v, double mx, double my, double mz,
                        double Mx, double My, double Mz) {
     const double v1x = v[0], v1y = v[1], v1z = v[2];
     const double v2x = v[3], v2y = v[4], v2z = v[5];
     const double v3x = v[6], v3y = v[7], v3z = v[8];
+    ++t_sat_calls;
+    t_sat_ops += 54;
     if (!plane_cuts_box(v1x, v1y, v1z, v2x, v2y, v2z, v3x, v3y, v3z, mx, my,
                         mz, Mx, My, Mz))
         return 0;
-    for (int k = 0; k < 5; ++k)
+    for (int k = 0; k < 5; ++k) {
+        t_sat_ops += 34;
         if (axis_gap_2d(k, v1x, v1y, v2x, v2y, v3x, v3y, mx, my, Mx, My))
             return 0;
-    for (int k = 0; k < 5; ++k)
+    }
+    for (int k = 0; k < 5; ++k) {
+        t_sat_ops += 34;
         if (axis_gap_2d(k, v1y, v1z, v2y, v2z, v3y, v3z, my, mz, My, Mz))
             return 0;
-    for (int k = 0; k < 5; ++k)
+    }
+    for (int k = 0; k < 5; ++k) {
+        t_sat_ops += 34;
         if (axis_gap_2d(k, v1z, v1x, v2z, v2x, v3z, v3x, mz, mx, Mz, Mx))
             return 0;
+    }
     return 1;
 }
 
@@ -394,6 +433,7 @@ int orc_voxelize_level(orc_grid *g, const orc_config *c, int L,
                     const double *v = fc + 9 * f, *n = nrm + 3 * f;
                     if (fabs(n[0]) < c->eps_parallel) continue; /* A7 */
                     if (!sat3(v, 0.0, y - eps, z - eps, lx, y + eps, z + eps)) continue;
+                    t_eval_ops += 4 * 11; /* per cell: num (8), /n_x, |d|, compare */
                     for (int I = 0; I < 4; ++I) {
                         const double x = node_c(4 * i + I, dx);
                         const double d = plane_num(v, n, x, y, z) / n[0];
@@ -747,12 +787,14 @@ int orc_link_lengths(const orc_grid *g, const orc_config *c, const int32_t *cmap
                 const int64_t f = face_ids[off + p];
                 const double *v = fc + 9 * f, *n = nrm + 3 * f;
                 const double num = plane_num(v, n, x, y, z);
+                t_eval_ops += 8 + 26 * 9; /* num; per q: den (5), |den| test (2), d, range */
                 for (int q = 1; q < 27; ++q) {
                     const double c0 = C27[q][0], c1 = C27[q][1], c2 = C27[q][2];
                     const double den = (c0 * n[0] + c1 * n[1]) + c2 * n[2];
                     if (fabs(den) < c->eps_parallel * cn[q]) continue;
                     const double d = num / den;
                     if (!(d > 0.0 && d <= dx)) continue;
+                    t_eval_ops += 6; /* the piercing point */
                     const double xi = x + d * c0, yi = y + d * c1, zi = z + d * c2;
                     if (!sat3(v, xi - eps, yi - eps, zi - eps, xi + eps, yi + eps, zi + eps)) continue;
                     if (d < best[q]) best[q] = d;
@@ -794,6 +836,7 @@ static int build_bins(const orc_config *c, const double *fc, const double *nrm,
     int64_t nmap;
     if (use_filter) {
         orc_ray_indicators(fc, nrm, F, c, L, mode, ind);
+        orc_ops_flush(mode == 0 ? ORC_ST_IND : ORC_ST_MD);
         nmap = orc_compact(ind, F, map);
     } else {
         for (int64_t f = 0; f < F; ++f) map[f] = (int32_t)f;
@@ -805,6 +848,7 @@ static int build_bins(const orc_config *c, const double *fc, const double *nrm,
     int32_t *pf = (int32_t *)malloc(sizeof(int32_t) * (size_t)cap);
     int64_t P = 0;
     int rc = orc_bin_pairs(fc, F, map, nmap, c, L, pb, pf, cap, &P);
+    orc_ops_flush(mode == 0 ? ORC_ST_PAIRS : ORC_ST_MD);
     const int64_t nb = (int64_t)bins_axis(c, 0, L) * bins_axis(c, 1, L) * bins_axis(c, 2, L);
     out->n_bins = nb;
     out->counts = (int32_t *)malloc(sizeof(int32_t) * (size_t)nb);
@@ -826,6 +870,8 @@ int orc_embed(orc_grid *g, const orc_config *c, const double *fc, const double *
               int64_t F, int use_filter, orc_links **out, double *st) {
     double acc[8] = {0};
     const double t_start = now_s();
+    orc_ops_flush(ORC_ST_IND);          /* drop counts of earlier direct calls */
+    memset(g_ops, 0, sizeof(g_ops));
     int rc = orc_init_forest(g, c);
     if (rc) return rc;
     for (int L = 0; L < c->l_max; ++L) {
@@ -833,9 +879,11 @@ int orc_embed(orc_grid *g, const orc_config *c, const double *fc, const double *
         orc_binlevel bl;
         rc = build_bins(c, fc, nrm, F, L, 0, use_filter, &bl);
         acc[0] += now_s() - t0;
+        /* build_bins flushes indicators and pairs separately (below) */
         if (rc) { free_bins(&bl); return rc; }
         t0 = now_s();
         orc_voxelize_level(g, c, L, bl.counts, bl.offsets, bl.face_ids, fc, nrm);
+        orc_ops_flush(ORC_ST_VOX);
         free_bins(&bl);
         orc_propagate(g, c, L, +1);
         if (L > 0) orc_propagate(g, c, L, -1);
@@ -867,6 +915,7 @@ int orc_embed(orc_grid *g, const orc_config *c, const double *fc, const double *
     if (rc) { free_bins(&md); orc_links_free(h); return rc; }
     t0 = now_s();
     orc_link_lengths(g, c, h->cmap, h->nb, md.counts, md.offsets, md.face_ids, fc, nrm, h->lengths);
+    orc_ops_flush(ORC_ST_LINKS);
     acc[6] += now_s() - t0;
     free_bins(&md);
     acc[7] = now_s() - t_start;

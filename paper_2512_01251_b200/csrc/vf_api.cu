@@ -608,10 +608,14 @@ int vf_embed_phase2(const vf_config *cfg, const double *faces, int64_t F, vf_gri
     cudaStream_t st = (cudaStream_t)stream;
     SideStream *side = nullptr;
     VF_TRY(side_stream(&side));
+    // link_events[0..1] bracket the LUT fill + the resolution (the cut-link
+    // kernels after the tables)
+    if (link_events) cudaEventRecord((cudaEvent_t)link_events[0], st);
     VF_TRY(fill_lut_impl(d_n_b, lengths, lengths_cap, g->d_status, st));
     cudaStreamWaitEvent(st, side->join3, 0);  // the line enumeration of phase 1
-    return link_resolve_impl(*cfg, g, cmap, faces, F, lengths, w.link_ws, w.lines_ws, st, link_events,
-                             d_n_b, lengths_cap);
+    void *end_only[2] = {nullptr, link_events ? link_events[1] : nullptr};
+    return link_resolve_impl(*cfg, g, cmap, faces, F, lengths, w.link_ws, w.lines_ws, st,
+                             link_events ? end_only : nullptr, d_n_b, lengths_cap);
 }
 
 int vf_embed_graph_create(const vf_config *cfg, const double *faces, int64_t F, int use_filter,

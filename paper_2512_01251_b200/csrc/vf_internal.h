@@ -121,7 +121,7 @@ int shard_face_subset_impl(const vf_config &cfg, const double *faces, int64_t F,
 // stream, early) + resolution once the grid and the LUT slots exist
 size_t link_lines_bytes(int64_t F);
 const void *link_enum_kernel(int small);  // graph node priorities
-int link_stats(const vf_config &cfg, int64_t F, void *ws, void *lines_ws, int64_t out[6]);
+int link_stats(const vf_config &cfg, int64_t F, void *ws, void *lines_ws, int64_t out[7]);
 int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *ws, void *lines_ws,
                    cudaStream_t st, void **events);
 int link_resolve_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,

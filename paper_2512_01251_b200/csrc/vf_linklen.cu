@@ -127,7 +127,16 @@ struct LinkCtx {
     int64_t line_cap;
     int32_t *ovf_list, *n_ovf;
     uint32_t *ovf_bits;   // one bit per face: already listed
+    unsigned long long *n_tests;  // lattice lines classified (FP32 intersection tests; roofline ops)
 };
+
+// add a per-thread count to the global test counter, one atomic per warp
+__device__ __forceinline__ void add_tests(const LinkCtx &c, unsigned long long n) {
+    if (!c.n_tests) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if ((threadIdx.x & 31) == 0 && n) atomicAdd(c.n_tests, n);
+}
 
 // representative directions q = 2r+1 (lattice.py order) in constant memory
 __constant__ int8_t c_rep[13][3] = {
@@ -478,14 +487,15 @@ __device__ __forceinline__ bool row_interval(const LinkCtx &c, const LinkDir &D,
 // is widened by one lattice point on each side -- a superset of the points
 // that pass point_class, which alone decides.
 template <int MODE>
-__device__ __forceinline__ void link_row(LinkWarp &W, int o, const LinkCtx &c, const LinkDir &D,
+__device__ __forceinline__ int link_row(LinkWarp &W, int o, const LinkCtx &c, const LinkDir &D,
                                          const double *fv, int m2, int R, int p, int cp, int s1,
                                          int s2, int n1, int n2) {
     const float Rb = (float)(((double)m2 + 0.5 * (1 - s2)) * c.dx + D.off2);
     int m1lo, m1hi;
-    if (!row_interval(c, D, Rb, s1, m1lo, m1hi)) return;
+    if (!row_interval(c, D, Rb, s1, m1lo, m1hi)) return 0;
     for (int m1 = m1lo; m1 <= m1hi; ++m1)
         link_point<MODE>(W, o, c, D, fv, m1, m2, Rb, R, p, cp, s1, s2, n1, n2);
+    return m1hi - m1lo + 1;
 }
 
 constexpr size_t kLinkSmem = kLinkWarps * sizeof(LinkWarp);
@@ -510,6 +520,7 @@ __global__ void __launch_bounds__(kLinkWarps * 32, MODE == 1 ? 1 : VF_LINK_MINB)
     // all lanes of a warp iterate together (uniform trip count); lanes past
     // the end are inactive
     const int64_t first = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    unsigned long long tests = 0;
     for (int64_t base = first; base < n; base += stride) {
         const int64_t m = base + lane;
         bool active = m < n;
@@ -575,13 +586,14 @@ __global__ void __launch_bounds__(kLinkWarps * 32, MODE == 1 ? 1 : VF_LINK_MINB)
                     for (int st = 16; st > 0; st >>= 1)
                         if (W.excl[o + st] <= it) o += st;
                     const LinkDir &D = W.d[o];
-                    link_row<MODE>(W, o, c, D, W.fv[o], D.m2a + it - W.excl[o], R, p, cp, s1, s2, n1, n2);
+                    tests += link_row<MODE>(W, o, c, D, W.fv[o], D.m2a + it - W.excl[o], R, p, cp, s1, s2, n1, n2);
                 }
                 line_drain<MODE>(W, lane, c, false, R, p, cp, s1, s2, n1, n2);
             }
             line_drain<MODE>(W, lane, c, true, R, p, cp, s1, s2, n1, n2);
         }
     }
+    if (MODE == 2) add_tests(c, tests);
 }
 
 // ---- small faces: thread per face ----------------------------------------
@@ -676,17 +688,17 @@ __device__ __forceinline__ void small_project(const LinkCtx &c, const SmallFace 
 // the lattice points of the projected bounding box, their class, piercing
 // lines as records (CTA stage slots) and the undecided ones node by node to
 // the band list
-__device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S, const SmallProj &P,
-                                           bool small, int R, int s1, int s2, int4 *s_rec, int *s_n) {
+__device__ __forceinline__ int small_pair(const LinkCtx &c, const SmallFace &S, const SmallProj &P,
+                                          bool small, int R, int s1, int s2, int4 *s_rec, int *s_n) {
     // exact den / EPS_PARALLEL, as link_dir_setup: c = (1, s1, s2) over
     // (p, q1, q2) -- the same FP64 sum in the same order (a zero term is exact)
-    if (!small) return;
+    if (!small) return 0;
     const float dn = P.nfp + (float)s1 * P.nfa + (float)s2 * P.nfb;  // c.n in FP32 (error < 1e-6)
     if (!(fabsf(dn) > S.dthr)) {  // only then can |c.n| be below EPS_PARALLEL |c|: decide exactly
         const double den = VF_DADD(VF_DADD(P.np, cmul(s1, P.nq1)), cmul(s2, P.nq2));
         const int nz = (s1 != 0) + (s2 != 0);
         const double cn = nz == 0 ? 1.0 : (nz == 1 ? 1.4142135623730951 : 1.7320508075688772);
-        if (fabs(den) < VF_DMUL(c.eps_par, cn)) return;
+        if (fabs(den) < VF_DMUL(c.eps_par, cn)) return 0;
     }
     const float P1a = P.V1a - (float)s1 * P.V1p, P1b = P.V1b - (float)s2 * P.V1p;
     const float P2a = P.V2a - (float)s1 * P.V2p, P2b = P.V2b - (float)s2 * P.V2p;
@@ -697,7 +709,7 @@ __device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S,
     const int m1b = (int)floorf(fmaxf(fmaxf(0.0f, P1a), P2a) + tol - o1 + 1e-4f);
     const int m2a = (int)ceilf(fminf(fminf(0.0f, P1b), P2b) - tol - o2 - 1e-4f);
     const int m2b = (int)floorf(fmaxf(fmaxf(0.0f, P1b), P2b) + tol - o2 + 1e-4f);
-    if (m1a > m1b || m2a > m2b) return;
+    if (m1a > m1b || m2a > m2b) return 0;
     const float cr = P1a * P2b - P1b * P2a;
     const float ab = 4e-6f * (ext + 1.0f) * (ext + 1.0f);
     // edge margins with the L1 length |a| + |b| >= |e| (no square root: a
@@ -745,6 +757,7 @@ __device__ __forceinline__ void small_pair(const LinkCtx &c, const SmallFace &S,
             }
         }
     }
+    return (m2b - m2a + 1) * (m1b - m1a + 1);
 }
 
 __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
@@ -787,6 +800,7 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
         base = __shfl_sync(0xffffffffu, base, 0);
         if (act && !small) big[base + __popc(bm & ((1u << lane) - 1u))] = S.f;
     }
+    unsigned long long tests = 0;
     if (__any_sync(0xffffffffu, small)) {
         if (small) {
 #pragma unroll
@@ -804,6 +818,7 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
         }
         S.epsL = c.epsL;
         S.dthr = c.dthr;
+        (void)0;
         S.ff9 = 4e-6f * (extL + 2.0f);
         // the 13 pairs in three classes of the axis p of their first nonzero
         // component (c_p = +1): p = x: c = (1, s1, s2), all 9 sign pairs;
@@ -821,10 +836,11 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
                 const int idx = cls == 0 ? t : (cls == 1 ? 9 + t : 12);
                 // R of (class, s1, s2) in lattice.py order, 4 bits each
                 const int R = (int)((0x271893a405b6cull >> (4 * idx)) & 15);
-                small_pair(c, S, P, small, R, s1, s2, s_rec, &s_n);
+                tests += small_pair(c, S, P, small, R, s1, s2, s_rec, &s_n);
             }
         }
     }
+    add_tests(c, tests);
     __syncthreads();
     const int n = min(s_n, kLineStage);
     if (threadIdx.x == 0) s_base = n ? atomicAdd(c.n_lines, n) : 0;
@@ -1025,6 +1041,7 @@ static int32_t *line_bufs(LinkCtx &c, int64_t F, void *lines_ws) {
     c.line_cap = F * 2 > (1 << 22) ? F * 2 : (1 << 22);
     c.n_lines = (int32_t *)lines_ws;
     c.n_ovf = c.n_lines + 1;
+    c.n_tests = (unsigned long long *)((char *)lines_ws + 16);
     c.lines = (int4 *)((char *)lines_ws + 256);
     c.ovf_list = (int32_t *)((char *)c.lines + (size_t)c.line_cap * sizeof(int4));
     c.ovf_bits = (uint32_t *)((char *)c.ovf_list + list_bytes(F));
@@ -1040,7 +1057,7 @@ int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *w
     if (rc) return rc;
     int32_t *big = line_bufs(c, F, lines_ws);
     cudaMemsetAsync(c.n_band, 0, 2 * sizeof(int32_t), st);
-    cudaMemsetAsync(c.n_lines, 0, 3 * sizeof(int32_t), st);
+    cudaMemsetAsync(c.n_lines, 0, 24, st);  // n_lines, n_ovf, n_big, (pad), n_tests
     cudaMemsetAsync(c.ovf_bits, 0, ((size_t)F + 32) / 32 * sizeof(uint32_t), st);
     kt_point("memset:link_counters");
     if (events) cudaEventRecord((cudaEvent_t)events[0], st);
@@ -1065,7 +1082,7 @@ const void *link_enum_kernel(int small) { return small ? (const void *)k_links_s
 // counters of the last embed's cut-link pass (synchronous read):
 // {lines recorded, line capacity, overflow faces, band candidates, band capacity,
 //  faces of the warp-flattened (large-face) enumeration}
-int link_stats(const vf_config &cfg, int64_t F, void *ws, void *lines_ws, int64_t out[6]) {
+int link_stats(const vf_config &cfg, int64_t F, void *ws, void *lines_ws, int64_t out[7]) {
     LinkCtx c;
     int widen;
     LevelInfo li;
@@ -1082,6 +1099,10 @@ int link_stats(const vf_config &cfg, int64_t F, void *ws, void *lines_ws, int64_
     out[3] = b[0];
     out[4] = c.band_cap;
     out[5] = a[2];
+    unsigned long long t = 0;
+    if (cudaMemcpy(&t, c.n_tests, sizeof(t), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return set_cuda_error(cudaGetLastError(), "link stats");
+    out[6] = (int64_t)t;
     return VF_OK;
 }
 
@@ -1096,7 +1117,7 @@ int link_resolve_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, con
     if (rc) return rc;
     line_bufs(c, F, lines_ws);
     if ((rc = link_blockmap(g, li, cmap, c, d_n_b, lengths_cap, st))) return rc;
-    if (events) cudaEventRecord((cudaEvent_t)events[0], st);
+    if (events && events[0]) cudaEventRecord((cudaEvent_t)events[0], st);
     k_links_resolve<<<max_ctas(VF_GRID_RESOLVE), 256, 0, st>>>(c);
     if ((rc = check_launch("k_links_resolve"))) return rc;
     // faces whose lines overflowed the record buffer: the direct kernel
@@ -1106,7 +1127,7 @@ int link_resolve_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, con
     if ((rc = check_launch("k_links_band"))) return rc;
     k_links<1><<<link_grid(F), kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, nullptr, nullptr);
     rc = check_launch("k_links_full");
-    if (events) cudaEventRecord((cudaEvent_t)events[1], st);
+    if (events && events[1]) cudaEventRecord((cudaEvent_t)events[1], st);
     return rc;
 }
 

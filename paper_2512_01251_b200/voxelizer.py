@@ -460,20 +460,22 @@ class EmbedEngine:
         """Counters of the last embed's cut-link pass (synchronises): lines
         recorded by the enumeration and the buffer capacity, faces whose lines
         overflowed it (redone by the direct kernel), band candidates (exact
-        SAT path), the band capacity and the faces of the large-face kernel."""
+        SAT path), the band capacity, the faces of the large-face kernel and
+        the lattice lines the enumeration classified (FP32 intersection tests)."""
         import torch
         torch.cuda.current_stream().synchronize()
         self.lib.vf_side_sync()
-        out = (C.c_int64 * 6)()
+        out = (C.c_int64 * 7)()
         _lib.check(self.lib.vf_embed_link_stats(C.byref(self.c), self.mesh.n_faces, self.grid.capacity,
                                                 _lib.ptr(self.ws), self.ws.numel(), out), "link_stats")
-        return dict(zip(("lines", "line_cap", "overflow_faces", "band", "band_cap", "large_faces"),
+        return dict(zip(("lines", "line_cap", "overflow_faces", "band", "band_cap", "large_faces", "tests"),
                         map(int, out)))
 
     def link_kernel_ms(self) -> float:
         """Device time of the cut-link kernels of the last timed run: the line
         enumeration (side stream, overlapped with the level pipeline, events
-        58-59) plus the resolution after the tables (events 61-62)."""
+        58-59) plus the LUT fill and the resolution after the tables (events
+        61-62)."""
         enum = self.events[58].elapsed_time(self.events[59])
         return enum + self.events[self.n_events - 3].elapsed_time(self.events[self.n_events - 2])
 
