@@ -46,7 +46,8 @@ enum {
     VF_ECAPACITY = 2,  /* forest / pair capacity exhausted */
     VF_ENLIM = 3,      /* N_lim pair cap violated               */
     VF_ECUDA = 4,      /* CUDA error                                         */
-    VF_ENCCL = 5       /* NCCL error (multi-GPU path)                        */
+    VF_ENCCL = 5,      /* NCCL error (multi-GPU path)                        */
+    VF_EMESH = 6       /* invalid mesh: face index out of range / degenerate face (MeshError) */
 };
 
 /* cell mask enum (SPEC.md:197 cell_mask values) */
@@ -228,6 +229,20 @@ void vf_graph_destroy(void *graph_exec);
  * grid-independent cut-link enumeration there; phase 2 joins it).  Call after
  * a phase 1 that is not followed by phase 2 before releasing its workspace. */
 int vf_side_sync(void);
+/* End-to-end (serving) formats.  vf_pack_indexed: the engine's 96-B face
+ * records from an indexed mesh -- the reference TriangleMesh's vertices (V,3)
+ * f64 and faces_indexed (F,3) (here int32) -- with the unit normals computed
+ * as TriangleMesh._face_normals does (geometry.py:114-124, np.cross / norm,
+ * bit-identical); an out-of-range index or a zero normal latches VF_EMESH in
+ * d_status.  vf_lut_sparse: the cut links of lengths[N_b][27][64] (N_b read
+ * from d_n_b) as (flat index, q) pairs in index order -- the index is the
+ * unsigned 32-bit (slot * 27 + q) * 64 + t stored in int32 --; *d_count = the
+ * number of links (only the first `cap` are written). */
+int vf_pack_indexed(const double *verts, int64_t V, const int32_t *faces_idx, int64_t F, double *out,
+                    int32_t *d_status, void *stream);
+size_t vf_lut_sparse_workspace_size(int64_t lengths_cap);
+int vf_lut_sparse(const float *lengths, int64_t lengths_cap, const int32_t *d_n_b, int32_t *idx, float *val,
+                  int64_t cap, int32_t *d_count, void *ws, size_t ws_bytes, void *stream);
 /* number of kernels this library has launched in the process (bench hook) */
 int64_t vf_launch_count(void);
 /* Per-kernel timer (bench / profiling hook).  vf_ktimer_start: the embed

@@ -91,6 +91,9 @@ _SIGS = {
     "vf_graph_destroy": (None, [_P]),
     "vf_launch_count": (_I64, []),
     "vf_ktimer_start": (_I32, [_P, C.c_double]),
+    "vf_pack_indexed": (_I32, [_P, _I64, _P, _I64, _P, _P, _P]),
+    "vf_lut_sparse_workspace_size": (_SZ, [_I64]),
+    "vf_lut_sparse": (_I32, [_P, _I64, _P, _P, _P, _I64, _P, _P, _SZ, _P]),
     "vf_ktimer_stop": (_I32, [C.c_char_p, _I32]),
     "vf_embed_link_stats": (_I32, [_CP, _I64, _I32, _P, _SZ, _P]),
     "vf_side_sync": (_I32, []),
@@ -168,6 +171,8 @@ def check(rc: int, what: str = ""):
         raise BinCapError(msg)
     if rc == 4:
         raise CudaError(msg)
+    if rc == 6:
+        raise MeshError(msg)
     raise VoxforestError(f"rc={rc}: {msg}")
 
 

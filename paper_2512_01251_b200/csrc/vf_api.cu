@@ -816,6 +816,7 @@ int vf_check_status(const vf_grid *g, void *stream) {
         return set_error(VF_ECAPACITY, buf);
     }
     if (h[0] == VF_ENLIM) return set_error(VF_ENLIM, "N_lim pair cap violated (refine_faces the mesh)");
+    if (h[0] == VF_EMESH) return set_error(VF_EMESH, "invalid mesh: face index out of range or degenerate face (zero normal)");
     if (h[0]) return set_error(h[0], "device-side error latched");
     return VF_OK;
 }

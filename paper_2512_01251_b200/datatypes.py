@@ -225,3 +225,13 @@ class LinkTable:
     def to_numpy(self):
         return (self.lengths.cpu().numpy(), self.bc_ids.cpu().numpy(),
                 self.contraction_map.cpu().numpy())
+
+
+def lengths_from_sparse(n_b: int, link_index, link_q) -> np.ndarray:
+    """Host expansion of the sparse LUT download (vf_lut_sparse: unsigned
+    32-bit flat indices (slot * 27 + q) * 64 + t and their q) to the SPEC
+    layout lengths[N_b][27][64] with -1 where there is no cut link."""
+    out = np.full(n_b * 27 * 64, -1.0, dtype=np.float32)
+    idx = np.asarray(link_index).view(np.uint32).astype(np.int64)
+    out[idx] = np.asarray(link_q, dtype=np.float32)
+    return out.reshape(n_b, 27, 64)

@@ -345,6 +345,10 @@ class EmbedEngine:
         """Validate the last run_async (synchronizes the engine stream)."""
         self.stream.synchronize()
         h = self._host_async.tolist() if hasattr(self, "_host_async") else self.host.tolist()
+        indexed = getattr(self, "_indexed_pending", False)
+        self._indexed_pending = False
+        if indexed and h[7]:      # the uploaded mesh was invalid: nothing else is meaningful
+            _lib.check(int(h[7]), "pack_indexed (invalid mesh)")
         if h[0]:
             gs = self.grid._struct()
             _lib.check(self.lib.vf_check_status(C.byref(gs), _lib.stream_ptr(self.stream)), "embed_geometry")
@@ -353,6 +357,9 @@ class EmbedEngine:
         if hasattr(self, "_host_async") and h[5] != self._n_used:
             raise RuntimeError("the block count changed between pipelined embeds: the downloaded "
                                "grid slices were sized by the previous synchronous run")
+        if indexed:
+            if h[6] != self._n_links:
+                raise RuntimeError("the cut-link count changed between pipelined embeds of the same mesh")
 
     def embed_host_async(self, faces_coord, normals, out, in_stream, out_stream):
         """One pipelined end-to-end step: pinned host faces -> H2D on
@@ -404,6 +411,94 @@ class EmbedEngine:
             self._ev_d2h.record(out_stream)
         h2d = faces_coord.numel() * 8 + normals.numel() * 8
         return out, h2d, d2h
+
+    def _indexed_setup(self, V: int, F: int):
+        """Device buffers of the indexed serving path; sizes the sparse LUT
+        download from the current LUT (one sync, outside any timed step)."""
+        import torch
+        self._dverts = torch.empty((V, 3), dtype=torch.float64, device="cuda")
+        self._dfidx = torch.empty((F, 3), dtype=torch.int32, device="cuda")
+        self._pack_status = torch.zeros(4, dtype=torch.int32, device="cuda")
+        self._sp_count = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self._sp_ws = torch.empty(int(self.lib.vf_lut_sparse_workspace_size(self.lengths_cap)), dtype=torch.uint8,
+                                  device="cuda")
+        dummy = torch.empty(1, dtype=torch.int32, device="cuda")
+        _lib.check(self.lib.vf_lut_sparse(_lib.ptr(self.lengths), self.lengths_cap, _lib.ptr(self.n_b_dev),
+                                          _lib.ptr(dummy), _lib.ptr(dummy), 0, _lib.ptr(self._sp_count),
+                                          _lib.ptr(self._sp_ws), self._sp_ws.numel(), _lib.stream_ptr(self.stream)),
+                   "lut_sparse")
+        self.stream.synchronize()
+        self._n_links = int(self._sp_count.item())
+        cap = self._n_links + 1024
+        self._sp_idx = torch.empty(cap, dtype=torch.int32, device="cuda")
+        self._sp_val = torch.empty(cap, dtype=torch.float32, device="cuda")
+        self._ev_sp = torch.cuda.Event()
+
+    def embed_indexed_async(self, vertices, faces_idx, out, in_stream, out_stream):
+        """One pipelined end-to-end step from the reference mesh's own fields:
+        pinned host ``vertices`` (V,3) f64 and ``faces_idx`` (F,3) int32 ->
+        H2D on ``in_stream`` (24 B/vertex + 12 B/face) -> face records and
+        unit normals on the device (vf_pack_indexed, TriangleMesh's
+        np.cross / norm bit for bit) -> embed -> the cut links of the LUT as
+        (flat index, q) pairs (vf_lut_sparse) -> D2H on ``out_stream`` of the
+        grid (coords, nbr, child, bflags, masks, contraction map) and the
+        sparse LUT into pinned ``out`` buffers.  No host sync; check_async()
+        validates the step.  Returns (out, h2d bytes, d2h bytes)."""
+        import torch
+        V, F = int(vertices.shape[0]), int(faces_idx.shape[0])
+        if F != self.mesh.n_faces:
+            raise ValueError("embed_indexed_async: face count differs from the engine's mesh")
+        if self.lengths is None:
+            self.run()
+        if not hasattr(self, "_dfidx") or self._dverts.shape[0] != V:
+            self._indexed_setup(V, F)
+            self._ev_pack = torch.cuda.Event()
+            self._ev_h2d = torch.cuda.Event()
+            self._ev_done = torch.cuda.Event()
+            self._ev_d2h = torch.cuda.Event()
+            self._ev_pack.record(self.stream)
+            self._ev_d2h.record(out_stream)
+        in_stream.wait_event(self._ev_pack)        # the previous pack has read the buffers
+        with torch.cuda.stream(in_stream):
+            self._dverts.copy_(vertices, non_blocking=True)
+            self._dfidx.copy_(faces_idx, non_blocking=True)
+            self._ev_h2d.record(in_stream)
+        self.stream.wait_event(self._ev_h2d)
+        self.stream.wait_event(self._ev_d2h)       # the previous results were copied out
+        st = _lib.stream_ptr(self.stream)
+        _lib.check(self.lib.vf_pack_indexed(_lib.ptr(self._dverts), V, _lib.ptr(self._dfidx), F,
+                                            _lib.ptr(self.mesh.faces), _lib.ptr(self._pack_status), st),
+                   "pack_indexed")
+        self._ev_pack.record(self.stream)
+        grid, table = self.run_async()
+        _lib.check(self.lib.vf_lut_sparse(_lib.ptr(self.lengths), self.lengths_cap, _lib.ptr(self.n_b_dev),
+                                          _lib.ptr(self._sp_idx), _lib.ptr(self._sp_val), self._sp_idx.numel(),
+                                          _lib.ptr(self._sp_count), _lib.ptr(self._sp_ws), self._sp_ws.numel(), st),
+                   "lut_sparse")
+        with torch.cuda.stream(self.stream):
+            self._host_async[6:7].copy_(self._sp_count, non_blocking=True)
+            self._host_async[7:8].copy_(self._pack_status[0:1], non_blocking=True)
+        self._ev_done.record(self.stream)
+        out_stream.wait_event(self._ev_done)
+        n, k = self._n_used, self._n_links
+        res = {"coords": grid.coords[:n], "nbr": grid.nbr[:n], "child": grid.child[:n],
+               "bflags": grid.bflags[:n], "masks": grid.masks[:n],
+               "contraction_map": table.contraction_map[:n], "link_index": self._sp_idx[:k],
+               "link_q": self._sp_val[:k]}
+        if out is None:
+            out = {}
+        d2h = 0
+        with torch.cuda.stream(out_stream):
+            for key, t in res.items():
+                buf = out.get(key)
+                if buf is None or buf.shape != t.shape:
+                    buf = torch.empty(t.shape, dtype=t.dtype).pin_memory()
+                    out[key] = buf
+                buf.copy_(t, non_blocking=True)
+                d2h += t.numel() * t.element_size()
+            self._ev_d2h.record(out_stream)
+        self._indexed_pending = True
+        return out, V * 24 + F * 12, d2h
 
     @property
     def n_b_host(self):

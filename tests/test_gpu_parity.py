@@ -619,3 +619,53 @@ def test_kernel_timer(O, torus):
     grid_equal(eng.grid.to_numpy(), ref.grid)
     tab = eng.run()[1]
     check_links(tab.lengths.cpu().numpy(), ref.lengths)
+
+
+def test_indexed_e2e_path(O, torus):
+    """The serving path from the indexed mesh: vf_pack_indexed's face records
+    and normals are bit-identical to TriangleMesh's (np.cross / norm), and the
+    downloaded grid + sparse cut links expand to the oracle's LUT."""
+    from paper_2512_01251_b200 import _lib
+    from paper_2512_01251_b200.datatypes import lengths_from_sparse
+    from paper_2512_01251_b200.errors import MeshError
+    lib = _lib.require_cuda()
+    cfg = EmbedConfig(n_x=32, l_max=3)
+    for mesh in (torus, make_icosphere((0.5, 0.5, 0.5), 0.5, 4)):
+        V = torch.from_numpy(np.ascontiguousarray(mesh.vertices)).cuda()
+        Fi = torch.from_numpy(np.ascontiguousarray(mesh.faces_indexed, dtype=np.int32)).cuda()
+        rec = torch.empty((mesh.n_faces, 12), dtype=torch.float64, device="cuda")
+        st = torch.zeros(4, dtype=torch.int32, device="cuda")
+        _lib.check(lib.vf_pack_indexed(_lib.ptr(V), V.shape[0], _lib.ptr(Fi), mesh.n_faces, _lib.ptr(rec),
+                                       _lib.ptr(st), _lib.stream_ptr()))
+        r = rec.cpu().numpy()
+        assert int(st[0]) == 0
+        assert np.array_equal(r[:, :9].view(np.uint64), mesh.faces_coord.view(np.uint64))
+        assert np.array_equal(r[:, 9:].view(np.uint64), np.ascontiguousarray(mesh.normals).view(np.uint64))
+        eng = EmbedEngine(mesh, cfg)
+        eng.run()
+        verts = torch.from_numpy(np.ascontiguousarray(mesh.vertices)).pin_memory()
+        fidx = torch.from_numpy(np.ascontiguousarray(mesh.faces_indexed, dtype=np.int32)).pin_memory()
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        out = None
+        for _ in range(2):
+            out, h2d, d2h = eng.embed_indexed_async(verts, fidx, out, s_in, s_out)
+        torch.cuda.synchronize()
+        eng.check_async()
+        assert h2d == mesh.vertices.shape[0] * 24 + mesh.n_faces * 12
+        ref = O.embed(mesh.faces_coord, mesh.normals, cfg, capacity=eng.grid.capacity)
+        host = {k: v.numpy() for k, v in out.items()}
+        grid_equal(host, ref.grid, keys=("coords", "nbr", "child", "bflags", "masks"))
+        assert np.array_equal(host["contraction_map"], ref.contraction_map)
+        check_links(lengths_from_sparse(ref.n_b, host["link_index"], host["link_q"]), ref.lengths)
+    # an out-of-range face index latches a mesh error
+    bad = np.ascontiguousarray(torus.faces_indexed, dtype=np.int32).copy()
+    bad[5, 1] = torus.vertices.shape[0] + 3
+    eng = EmbedEngine(torus, cfg)
+    eng.run()
+    vb = torch.from_numpy(np.ascontiguousarray(torus.vertices)).pin_memory()
+    fb = torch.from_numpy(bad).pin_memory()
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    eng.embed_indexed_async(vb, fb, None, s_in, s_out)
+    torch.cuda.synchronize()
+    with pytest.raises(MeshError):
+        eng.check_async()
