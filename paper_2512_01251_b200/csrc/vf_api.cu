@@ -778,9 +778,18 @@ int vf_ktimer_stop(char *buf, int buflen) {
     std::vector<const char *> keys;
     std::vector<double> ms;
     std::vector<int> cnt;
+    // VF_KT_EACH=1: one line per launch ("name#k") instead of per kernel name
+    const char *each = getenv("VF_KT_EACH");
+    std::vector<char> names_each;
+    if (each && *each == '1') names_each.resize(g_kt.used * 48);
     for (size_t i = 1; i < g_kt.used; ++i) {
         float t = 0.0f;
         cudaEventElapsedTime(&t, g_kt.pool[i - 1], g_kt.pool[i]);
+        if (!names_each.empty()) {
+            char *nm = &names_each[i * 48];
+            snprintf(nm, 48, "%s#%zu", g_kt.names[i], i);
+            g_kt.names[i] = nm;
+        }
         size_t k = 0;
         while (k < keys.size() && strcmp(keys[k], g_kt.names[i]) != 0) ++k;
         if (k == keys.size()) {

@@ -235,6 +235,34 @@ __device__ __forceinline__ uint32_t compose(uint32_t g, uint32_t f) {
     return A | (B << 16);
 }
 
+// byte-SIMD on a row word (the 4 cells of an x-row, one mask byte each)
+__device__ __forceinline__ uint32_t bytes_eq(uint32_t x, uint32_t v) { return __vcmpeq4(x, v * 0x01010101u); }
+// 0xff / 0x00 bytes -> 4 bits (byte i -> bit i)
+__device__ __forceinline__ uint32_t nib4(uint32_t m) { return ((m & 0x01010101u) * 0x01020408u) >> 24; }
+
+// Alg. 5 transfer function of a block from its rows' trailing cells (A10):
+// bit r of A = (H_trail != GUARD), of B = (H_trail == SOLID)
+__device__ __forceinline__ void row_fn(const uint32_t w[16], int trail, uint32_t &A, uint32_t &B) {
+    A = B = 0;
+    const uint32_t sel = (uint32_t)trail | ((4u + (uint32_t)trail) << 4);
+#pragma unroll
+    for (int r = 0; r < 16; r += 4) {
+        const uint32_t t4 = __byte_perm(__byte_perm(w[r], w[r + 1], sel), __byte_perm(w[r + 2], w[r + 3], sel),
+                                        0x5410);  // trailing bytes of rows r..r+3
+        A |= nib4(~bytes_eq(t4, VF_GUARD)) << r;
+        B |= nib4(bytes_eq(t4, VF_SOLID)) << r;
+    }
+}
+
+// Alg. 5 update of one row word: carried SOLID turns every non-GUARD cell
+// SOLID; on level 0 GUARD -> FLUID afterwards
+__device__ __forceinline__ uint32_t row_apply(uint32_t xw, bool solid, bool l0) {
+    const uint32_t g = bytes_eq(xw, VF_GUARD);
+    if (solid) xw = (xw & g) | ((0x01010101u * VF_SOLID) & ~g);
+    if (l0) xw &= ~g;  // GUARD bytes are unchanged by the update; FLUID = 0
+    return xw;
+}
+
 __device__ __forceinline__ void load_masks64(const uint8_t *masks, int64_t b, uint32_t w[16]) {
     const uint4 *p = reinterpret_cast<const uint4 *>(masks + 64 * b);
 #pragma unroll
@@ -259,13 +287,8 @@ __global__ void __launch_bounds__(256)
          b += (int64_t)gridDim.x * blockDim.x) {
         uint32_t w[16];
         load_masks64(masks, b, w);
-        uint32_t A = 0, B = 0;
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const uint32_t h3 = (w[r] >> (8 * trail)) & 0xffu;
-            A |= (uint32_t)(h3 != VF_GUARD) << r;
-            B |= (uint32_t)(h3 == VF_SOLID) << r;
-        }
+        uint32_t A, B;
+        row_fn(w, trail, A, B);
         const int32_t code = nbr[27 * b + back];
         uint32_t fn = A | (B << 16);
         if (code < 0) {
@@ -303,13 +326,8 @@ __device__ __forceinline__ void finalize_block(uint32_t w[16], bool &changed, ui
     uint64_t sm = 0;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-        uint32_t x = w[r];
-#pragma unroll
-        for (int I = 0; I < 4; ++I) {
-            const uint32_t h = (x >> (8 * I)) & 0xffu;
-            if (h == VF_GUARD) x &= ~(0xffu << (8 * I));  // -> FLUID (0)
-            sm |= (uint64_t)(h == VF_SOLID) << (4 * r + I);
-        }
+        const uint32_t x = w[r] & ~bytes_eq(w[r], VF_GUARD);  // GUARD -> FLUID (0)
+        sm |= (uint64_t)nib4(bytes_eq(w[r], VF_SOLID)) << (4 * r);
         changed |= (x != w[r]);
         w[r] = x;
     }
@@ -334,15 +352,7 @@ __global__ void __launch_bounds__(256)
             const uint32_t st = G[pred] & 0xffffu;  // constant: status leaving pred
 #pragma unroll
             for (int r = 0; r < 16; ++r) {
-                uint32_t x = w[r];
-#pragma unroll
-                for (int I = 0; I < 4; ++I) {
-                    const uint32_t h = (x >> (8 * I)) & 0xffu;
-                    uint32_t hn = h;
-                    if ((st >> r & 1u) && h != VF_GUARD) hn = VF_SOLID;
-                    if (L == 0 && hn == VF_GUARD) hn = VF_FLUID;
-                    x = (x & ~(0xffu << (8 * I))) | (hn << (8 * I));
-                }
+                const uint32_t x = row_apply(w[r], (st >> r) & 1u, L == 0);
                 changed |= (x != w[r]);
                 w[r] = x;
             }
@@ -416,13 +426,8 @@ __device__ __forceinline__ void xrow_pass(int L, int lane, const int32_t *__rest
         bool head = true;
         if (present) {
             load_masks64(masks, id, w);
-            uint32_t A = 0, B = 0;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                const uint32_t h3 = (w[r] >> (8 * trail)) & 0xffu;
-                A |= (uint32_t)(h3 != VF_GUARD) << r;
-                B |= (uint32_t)(h3 == VF_SOLID) << r;
-            }
+            uint32_t A, B;
+            row_fn(w, trail, A, B);
             fn = A | (B << 16);
             if (!pred) {  // run start: back neighbour is not a level-L block
                 const int32_t code = nbr[27 * (int64_t)id + back];
@@ -452,15 +457,7 @@ __device__ __forceinline__ void xrow_pass(int L, int lane, const int32_t *__rest
             if (pred) {
 #pragma unroll
                 for (int r = 0; r < 16; ++r) {
-                    uint32_t xw = w[r];
-#pragma unroll
-                    for (int I = 0; I < 4; ++I) {
-                        const uint32_t h = (xw >> (8 * I)) & 0xffu;
-                        uint32_t hn = h;
-                        if ((st >> r & 1u) && h != VF_GUARD) hn = VF_SOLID;
-                        if (L == 0 && hn == VF_GUARD) hn = VF_FLUID;
-                        xw = (xw & ~(0xffu << (8 * I))) | (hn << (8 * I));
-                    }
+                    const uint32_t xw = row_apply(w[r], (st >> r) & 1u, L == 0);
                     changed |= (xw != w[r]);
                     w[r] = xw;
                 }
@@ -534,13 +531,8 @@ __device__ __forceinline__ void xrow_pass_s(int L, int lane, int bx, XStage<NCH>
         uint32_t fn = 0;
         bool head = true;
         if (present) {
-            uint32_t A = 0, B = 0;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                const uint32_t h3 = (w[r] >> (8 * trail)) & 0xffu;
-                A |= (uint32_t)(h3 != VF_GUARD) << r;
-                B |= (uint32_t)(h3 == VF_SOLID) << r;
-            }
+            uint32_t A, B;
+            row_fn(w, trail, A, B);
             fn = A | (B << 16);
             if (!pred) {
                 const int32_t code = DIR > 0 ? S.cp[x] : S.cm[x];
@@ -568,15 +560,7 @@ __device__ __forceinline__ void xrow_pass_s(int L, int lane, int bx, XStage<NCH>
             bool changed = false;
 #pragma unroll
             for (int r = 0; r < 16; ++r) {
-                uint32_t xw = w[r];
-#pragma unroll
-                for (int I = 0; I < 4; ++I) {
-                    const uint32_t h = (xw >> (8 * I)) & 0xffu;
-                    uint32_t hn = h;
-                    if ((st >> r & 1u) && h != VF_GUARD) hn = VF_SOLID;
-                    if (L == 0 && hn == VF_GUARD) hn = VF_FLUID;
-                    xw = (xw & ~(0xffu << (8 * I))) | (hn << (8 * I));
-                }
+                const uint32_t xw = row_apply(w[r], (st >> r) & 1u, L == 0);
                 changed |= (xw != w[r]);
                 w[r] = xw;
             }
@@ -710,13 +694,8 @@ __device__ __forceinline__ void xrow_pass_hv(int L, int lane, int bx, const XHVi
         bool head = true;
         if (present) {
             load_masks64(masks, id, w);
-            uint32_t A = 0, B = 0;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                const uint32_t h3 = (w[r] >> (8 * trail)) & 0xffu;
-                A |= (uint32_t)(h3 != VF_GUARD) << r;
-                B |= (uint32_t)(h3 == VF_SOLID) << r;
-            }
+            uint32_t A, B;
+            row_fn(w, trail, A, B);
             fn = A | (B << 16);
             if (!pred) {
                 const int32_t code = DIR > 0 ? S.cp[x] : S.cm[x];
@@ -745,15 +724,7 @@ __device__ __forceinline__ void xrow_pass_hv(int L, int lane, int bx, const XHVi
             if (pred) {
 #pragma unroll
                 for (int r = 0; r < 16; ++r) {
-                    uint32_t xw = w[r];
-#pragma unroll
-                    for (int I = 0; I < 4; ++I) {
-                        const uint32_t h = (xw >> (8 * I)) & 0xffu;
-                        uint32_t hn = h;
-                        if ((st >> r & 1u) && h != VF_GUARD) hn = VF_SOLID;
-                        if (L == 0 && hn == VF_GUARD) hn = VF_FLUID;
-                        xw = (xw & ~(0xffu << (8 * I))) | (hn << (8 * I));
-                    }
+                    const uint32_t xw = row_apply(w[r], (st >> r) & 1u, L == 0);
                     changed |= (xw != w[r]);
                     w[r] = xw;
                 }
