@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define VF_ABI_VERSION 3
+#define VF_ABI_VERSION 4
 #define VF_MAX_LEVELS 16
 
 /* status codes (SURVEY.md §8b "Errors") */
@@ -77,6 +77,10 @@ typedef struct {
     int32_t shard_rank;
     int32_t shard_count;
     uint8_t *d_row_owner;
+    /* embed (bin, face) pair list capacity per level; 0 = 4 F + 65536.  An
+     * overflow latches VF_ECAPACITY with the required count in d_status[3]
+     * (EmbedEngine re-sizes and reruns). */
+    int64_t pair_cap;
 } vf_config;
 
 /* ForestGrid as flat device arrays, ids grouped by level:

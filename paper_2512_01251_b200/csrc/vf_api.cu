@@ -158,9 +158,14 @@ static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // embed workspace layout
 struct EmbedWs {
-    vf_bins bins;
-    vf_bins bins2;       // second bins buffer: bins(L+1) built while level L runs
-    void *bins_ws;
+    int2 *pairs[2];       // per-level (bin, face) lists, ping-pong: pairs(L+1) built while level L runs
+    int32_t *n_pairs[2];
+    int32_t *map[2];      // kept faces of the level (compact_map)
+    int32_t *n_map[2];
+    int64_t pair_cap;
+    BlockBins bb;         // the level's block-indexed bins
+    uint8_t *ind8;        // [F] per-level indicators (sharded path)
+    void *bins_ws;        // compaction scan over F
     size_t bins_ws_bytes;
     void *prop_ws, *mark_ws, *adapt_ws, *tab_ws, *link_ws;
     size_t prop_b, mark_b, adapt_b, tab_b, link_b;
@@ -170,6 +175,28 @@ struct EmbedWs {
     void *shard_ws;      // multi-GPU: row histogram / owner scan / face subset
 };
 
+int64_t pair_cap_of(const vf_config &cfg, int64_t F) {
+    return cfg.pair_cap > 0 ? cfg.pair_cap : 4 * F + 65536;
+}
+
+size_t block_bins_bytes(int32_t capacity, int64_t pair_cap) {
+    const size_t c = al(sizeof(int32_t) * ((size_t)capacity + 1)), p = al(sizeof(int32_t) * ((size_t)pair_cap + 1));
+    return 2 * p + 4 * c + 256 + al(scan_workspace_bytes(capacity));
+}
+
+void block_bins_layout(int32_t capacity, int64_t pair_cap, char *base, BlockBins *bb) {
+    const size_t c = al(sizeof(int32_t) * ((size_t)capacity + 1)), p = al(sizeof(int32_t) * ((size_t)pair_cap + 1));
+    bb->blk = (int32_t *)base;
+    bb->face_ids = (int32_t *)(base + p);
+    bb->cnt = (int32_t *)(base + 2 * p);
+    bb->base = (int32_t *)(base + 2 * p + c);
+    bb->cur = (int32_t *)(base + 2 * p + 2 * c);
+    bb->ne = (int32_t *)(base + 2 * p + 3 * c);
+    bb->d_n_ne = (int32_t *)(base + 2 * p + 4 * c);
+    bb->d_total = bb->d_n_ne + 1;
+    bb->scan_ws = base + 2 * p + 4 * c + 256;
+}
+
 static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *base, EmbedWs *w) {
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -178,25 +205,19 @@ static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *b
         return (void *)p;
     };
     const int Lf = cfg.l_max - 1;
-    const int nlim = nlim_of(cfg);
-    const int64_t nbins = (int64_t)(cfg.nb[0] << Lf) * (cfg.nb[1] << Lf) * (cfg.nb[2] << Lf);
     EmbedWs t;
     memset(&t, 0, sizeof(t));
-    t.bins.d_counts = (int32_t *)take(sizeof(int32_t) * (size_t)nbins);
-    t.bins.d_offsets = (int32_t *)take(sizeof(int32_t) * (size_t)nbins);
-    t.bins.face_ids_cap = F * nlim;
-    t.bins.d_face_ids = (int32_t *)take(sizeof(int32_t) * (size_t)(F * nlim + 1));
-    t.bins.d_map = (int32_t *)take(sizeof(int32_t) * (size_t)(F + 1));
-    t.bins.d_n_map = (int32_t *)take(64);
-    t.bins.d_n_face_ids = (int32_t *)take(64);
-    t.bins2 = t.bins;
-    t.bins2.d_counts = (int32_t *)take(sizeof(int32_t) * (size_t)nbins);
-    t.bins2.d_offsets = (int32_t *)take(sizeof(int32_t) * (size_t)nbins);
-    t.bins2.d_face_ids = (int32_t *)take(sizeof(int32_t) * (size_t)(F * nlim + 1));
-    t.bins2.d_map = (int32_t *)take(sizeof(int32_t) * (size_t)(F + 1));
-    t.bins2.d_n_map = (int32_t *)take(64);
-    t.bins2.d_n_face_ids = (int32_t *)take(64);
-    t.bins_ws_bytes = bins_workspace_size(F, nlim, nbins);
+    t.pair_cap = pair_cap_of(cfg, F);
+    for (int k = 0; k < 2; ++k) {
+        t.pairs[k] = (int2 *)take(sizeof(int2) * (size_t)(t.pair_cap + 1));
+        t.n_pairs[k] = (int32_t *)take(64);
+        t.map[k] = (int32_t *)take(sizeof(int32_t) * (size_t)(F + 1));
+        t.n_map[k] = (int32_t *)take(64);
+    }
+    char *bbp = (char *)take(block_bins_bytes(cap, t.pair_cap));
+    if (base) block_bins_layout(cap, t.pair_cap, bbp, &t.bb);
+    t.ind8 = (uint8_t *)take((size_t)F + 1);
+    t.bins_ws_bytes = scan_workspace_bytes(F + 1);
     t.bins_ws = take(t.bins_ws_bytes);
     t.prop_b = propagate_level_workspace_size(cfg, Lf);
     t.prop_ws = take(t.prop_b);
@@ -214,6 +235,28 @@ static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *b
     t.shard_ws = cfg.shard_count > 1 ? take(shard_scratch_size(cfg, F)) : nullptr;
     if (w) *w = t;
     return off;
+}
+
+// the (bin, face) pairs of level L: kept faces (1D indicators: precomputed
+// bits, or computed here), then k_pairs_append
+static int level_pairs(const vf_config &cfg, const LevelInfo &li, const double *faces, int64_t F,
+                       int use_filter, const uint16_t *ind_bits, EmbedWs &w, int k, int32_t *d_status,
+                       cudaStream_t st) {
+    const int32_t *map = nullptr, *nmap = nullptr;
+    int rc;
+    if (use_filter) {
+        if (ind_bits) {
+            rc = launch_compact_bits(ind_bits, li.level, F, w.map[k], w.n_map[k], w.bins_ws, st);
+        } else {
+            if ((rc = launch_indicators(li, 0, faces, F, w.ind8, st))) return rc;
+            rc = launch_compact(w.ind8, F, w.map[k], w.n_map[k], w.bins_ws, st);
+        }
+        if (rc) return rc;
+        map = w.map[k];
+        nmap = w.n_map[k];
+    }
+    return pairs_append_impl(li, nlim_of(cfg), faces, F, map, nmap, w.pairs[k], w.n_pairs[k], w.pair_cap,
+                             d_status, st);
 }
 
 }  // namespace vf
@@ -525,7 +568,6 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     // per-kernel timing: everything on the main stream, in order
     const bool one = kt_on();
     cudaStream_t s2 = one ? st : side->st;
-    vf_bins *buf[2] = {&w.bins, &w.bins2};
     const int n_ev = 64;
     int k = 0;
     rec(events, n_ev, &k, st);  // 0: start
@@ -544,22 +586,26 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     // Alg. 1 indicators of every level in one pass over the face records
     if (use_filter) VF_TRY(launch_indicators_all(*cfg, faces, F, w.ind_bits, s2));
     auto build = [&](int L) {
-        return build_bins_impl(make_level(*cfg, L), nlim_of(*cfg), faces, F, 0, use_filter, buf[L & 1],
-                               g->d_status, w.bins_ws, w.bins_ws_bytes, s2, w.ind_bits, false);
+        return level_pairs(*cfg, make_level(*cfg, L), faces, F, use_filter, w.ind_bits, w, L & 1, g->d_status, s2);
     };
+    // the block histograms start from zero (each level's voxelizer restores them)
+    cudaMemsetAsync(w.bb.cnt, 0, sizeof(int32_t) * (size_t)g->capacity, st);
+    kt_point("memset:block_counts");
     VF_TRY(build(0));
     cudaEventRecord(side->bins[0], s2);
     for (int L = 0; L < cfg->l_max; ++L) {
         const LevelInfo li = make_level(*cfg, L);
-        if (L + 1 < cfg->l_max) {  // side stream: bins(L+1) while the main stream runs level L
-            if (L >= 1) cudaStreamWaitEvent(s2, side->vox[(L + 1) & 1], 0);  // voxelize(L-1) done
+        if (L + 1 < cfg->l_max) {  // side stream: pairs(L+1) while the main stream runs level L
+            if (L >= 1) cudaStreamWaitEvent(s2, side->vox[(L + 1) & 1], 0);  // pairs(L-1) consumed
             VF_TRY(build(L + 1));
             cudaEventRecord(side->bins[(L + 1) & 1], s2);
         }
         cudaStreamWaitEvent(st, side->bins[L & 1], 0);
         rec(events, n_ev, &k, st);  // bins done
-        VF_TRY(voxelize_impl(li, g, L, buf[L & 1], faces, st));
+        // pairs -> level-L blocks (needs the level's blocks: after adapt(L-1))
+        VF_TRY(block_bins_impl(li, L, g, w.pairs[L & 1], w.n_pairs[L & 1], w.pair_cap, w.bb, st));
         cudaEventRecord(side->vox[L & 1], st);
+        VF_TRY(voxelize_blocks_impl(li, g, L, w.bb, faces, true, st));
         VF_TRY(propagate_level_impl(li, g, L, w.prop_ws, w.prop_b, st));
         rec(events, n_ev, &k, st);  // voxelization done
         if (L == cfg->l_max - 1) break;
@@ -716,9 +762,13 @@ int vf_shard_level(const vf_config *cfg, const double *faces, int64_t F, int use
         return set_error(VF_EARG, "vf_shard_level: bad argument");
     cudaStream_t st = (cudaStream_t)stream;
     const LevelInfo li = make_level(*cfg, L);
-    VF_TRY(build_bins_impl(li, nlim_of(*cfg), faces, F, 0, use_filter, &w.bins, g->d_status,
-                           w.bins_ws, w.bins_ws_bytes, st, nullptr, false));
-    VF_TRY(voxelize_impl(li, g, L, &w.bins, faces, st));
+    if (L == 0) {  // the block histograms start from zero
+        cudaMemsetAsync(w.bb.cnt, 0, sizeof(int32_t) * (size_t)g->capacity, st);
+        kt_point("memset:block_counts");
+    }
+    VF_TRY(level_pairs(*cfg, li, faces, F, use_filter, nullptr, w, 0, g->d_status, st));
+    VF_TRY(block_bins_impl(li, L, g, w.pairs[0], w.n_pairs[0], w.pair_cap, w.bb, st));
+    VF_TRY(voxelize_blocks_impl(li, g, L, w.bb, faces, true, st));
     VF_TRY(propagate_level_impl(li, g, L, w.prop_ws, w.prop_b, st));
     return shard_zero_impl(li, g, L, nullptr, st);
 }
@@ -748,8 +798,8 @@ int vf_shard_links(const vf_config *cfg, const double *faces, int64_t F, vf_grid
         return set_error(VF_EARG, "vf_shard_links: bad argument");
     cudaStream_t st = (cudaStream_t)stream;
     VF_TRY(fill_lut_impl(d_n_b, lengths, lengths_cap, g->d_status, st));
-    VF_TRY(shard_face_subset_impl(*cfg, faces, F, w.bins.d_map, w.bins.d_n_map, w.shard_ws, st));
-    return link_impl(*cfg, g, cmap, faces, F, w.bins.d_map, w.bins.d_n_map, lengths, w.link_ws,
+    VF_TRY(shard_face_subset_impl(*cfg, faces, F, w.map[0], w.n_map[0], w.shard_ws, st));
+    return link_impl(*cfg, g, cmap, faces, F, w.map[0], w.n_map[0], lengths, w.link_ws,
                      w.link_b, st, nullptr, d_n_b, lengths_cap);
 }
 
@@ -818,7 +868,9 @@ int vf_check_status(const vf_grid *g, void *stream) {
     if (e != cudaSuccess) return set_cuda_error(e, "vf_check_status");
     if (h[0] == VF_ECAPACITY) {
         char buf[160];
-        if (h[2] > 0)
+        if (h[3] > 0)
+            snprintf(buf, sizeof(buf), "pair list capacity exhausted: %d (bin, face) pairs needed", h[3]);
+        else if (h[2] > 0)
             snprintf(buf, sizeof(buf), "link table capacity exhausted: %d boundary blocks", h[2]);
         else
             snprintf(buf, sizeof(buf), "forest capacity exhausted while refining level %d", h[1]);

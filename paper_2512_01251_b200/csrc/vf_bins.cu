@@ -547,6 +547,160 @@ __global__ void __launch_bounds__(kPairThreads, VF_PAIRS_MINB)
     }
 }
 
+// Embed pairs (block-indexed bins): the same accepted (bin, face) set as
+// k_pairs, appended compactly to one (bin, face) list -- one global slot
+// reservation per warp -- instead of a per-face row of N_lim slots: the
+// reserved memory is the list capacity, not F * N_lim.  The per-face slots
+// are staged in shared memory (row stride N_lim + 1: no bank conflicts).
+// Capacity overflow latches VF_ECAPACITY with the required count in
+// status[3] (the engine re-sizes and reruns).
+__global__ void __launch_bounds__(kPairThreads, VF_PAIRS_MINB)
+    k_pairs_append(LevelInfo li, int nlim, const double *__restrict__ faces,
+                   const int32_t *__restrict__ map, const int32_t *__restrict__ d_n_map,
+                   int64_t n_static, int2 *__restrict__ pairs, int32_t *__restrict__ d_n_pairs,
+                   int64_t cap, int32_t *__restrict__ d_status) {
+    extern __shared__ int32_t s_slots[];
+    int32_t *slot = s_slots + threadIdx.x * (nlim + 1);
+    const int lane = threadIdx.x & 31;
+    const int64_t n = d_n_map ? (int64_t)*d_n_map : n_static;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t m0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); m0 < n; m0 += stride) {
+        const int64_t m = m0 + lane;
+        int c = 0;
+        int32_t f = 0;
+        if (m < n) {
+            f = map ? map[m] : (int32_t)m;
+            double v[9], nn[3];
+            load_face(faces, f, v, nn);
+            c = face_pairs(faces, f, v, li, nlim, slot, nullptr);
+            if (c < 0) {
+                latch_status(d_status, VF_ENLIM);
+                c = 0;
+            }
+        }
+        int inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        const int total = __shfl_sync(0xffffffffu, inc, 31);
+        int base = 0;
+        if (lane == 31 && total) base = atomicAdd(d_n_pairs, total);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        const int64_t p0 = (int64_t)base + inc - c;
+        if (p0 + c > cap) {
+            latch_status(d_status, VF_ECAPACITY);
+            atomicMax(d_status + 3, (int32_t)min(p0 + c, (int64_t)0x7fffffff));
+        }
+        for (int k = 0; k < c; ++k)
+            if (p0 + k < cap) pairs[p0 + k] = make_int2(slot[k], f);
+    }
+}
+
+int pairs_append_impl(const LevelInfo &li, int nlim, const double *faces, int64_t F,
+                      const int32_t *map, const int32_t *d_n_map, int2 *pairs, int32_t *d_n_pairs,
+                      int64_t cap, int32_t *d_status, cudaStream_t st) {
+    const size_t smem = (size_t)kPairThreads * (nlim + 1) * sizeof(int32_t);
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaFuncSetAttribute(k_pairs_append, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
+    cudaMemsetAsync(d_n_pairs, 0, sizeof(int32_t), st);
+    kt_point("memset:n_pairs");
+    int64_t g = (F + kPairThreads - 1) / kPairThreads;
+    if (g > max_ctas(VF_GRID_PAIRS * 2)) g = max_ctas(VF_GRID_PAIRS * 2);
+    k_pairs_append<<<(int)(g < 1 ? 1 : g), kPairThreads, smem, st>>>(li, nlim, faces, map, d_n_map, F, pairs,
+                                                                     d_n_pairs, cap, d_status);
+    return check_launch("k_pairs");
+}
+
+// Bins matched to blocks (pin A4): the voxelizer of level L
+// reads the bin of each level-L block only, so the embed groups the pairs by
+// level-L BLOCK instead of by bin.  A pair's bin key (I, J, K) is the block
+// key; the block is found by descending the forest from the root block
+// (I, J, K) >> L through the child links (child ids are parent-first + octant,
+// ox + 2 oy + 4 oz, vf_forest.cu) -- no dense B_L^3 map, no hash table.
+// Pairs whose bin holds no level-L block are dropped (never read).
+// (a level dropped on capacity exhaustion leaves child ids >= n_used: no block)
+__device__ __forceinline__ int32_t block_of_key(int L, int bi, int bj, int bk, const int3 nb0,
+                                                const int32_t *__restrict__ child, int32_t n_used) {
+    int32_t b = (bi >> L) + nb0.x * ((bj >> L) + nb0.y * (bk >> L));
+    for (int l = L - 1; l >= 0; --l) {
+        const int32_t c = child[b];
+        if (c < 0 || c >= n_used) return -1;
+        b = c + ((bi >> l) & 1) + 2 * ((bj >> l) & 1) + 4 * ((bk >> l) & 1);
+    }
+    return b;
+}
+
+// K1: pair -> level-local block u, per-block pair counts, the nonempty blocks
+__global__ void __launch_bounds__(256)
+    k_pair_blocks(int L, int bx, int by, int3 nb0, const int2 *__restrict__ pairs,
+                  const int32_t *__restrict__ d_n_pairs, int64_t cap,
+                  const int32_t *__restrict__ level_start, const int32_t *__restrict__ child,
+                  int32_t *__restrict__ blk, int32_t *__restrict__ cnt, int32_t *__restrict__ ne,
+                  int32_t *__restrict__ d_n_ne) {
+    const int64_t n = min((int64_t)*d_n_pairs, cap);
+    const int32_t s = level_start[L], n_used = level_start[VF_MAX_LEVELS];
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t key = pairs[p].x;
+        const int bi = key % bx, r = key / bx, bj = r % by, bk = r / by;
+        const int32_t b = block_of_key(L, bi, bj, bk, nb0, child, n_used);
+        int32_t u = -1;
+        if (b >= 0) {
+            u = b - s;
+            if (atomicAdd(&cnt[u], 1) == 0) ne[atomicAdd(d_n_ne, 1)] = u;
+        }
+        blk[p] = u;
+    }
+}
+
+struct LoadCnt {
+    const int32_t *p;
+    __device__ int operator()(int64_t i) const { return p[i]; }
+};
+struct EmitBase {
+    int32_t *base, *cur;
+    __device__ void operator()(int64_t i, int, int ex) const {
+        base[i] = ex;
+        cur[i] = ex;
+    }
+};
+
+// K3: counting-sort scatter of the face ids into their block's slice
+__global__ void __launch_bounds__(256)
+    k_pair_scatter(const int2 *__restrict__ pairs, const int32_t *__restrict__ d_n_pairs, int64_t cap,
+                   const int32_t *__restrict__ blk, int32_t *__restrict__ cur,
+                   int32_t *__restrict__ face_ids) {
+    const int64_t n = min((int64_t)*d_n_pairs, cap);
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t u = blk[p];
+        if (u >= 0) face_ids[atomicAdd(&cur[u], 1)] = pairs[p].y;
+    }
+}
+
+int block_bins_impl(const LevelInfo &li, int L, vf_grid *g, const int2 *pairs,
+                    const int32_t *d_n_pairs, int64_t cap, const BlockBins &bb, cudaStream_t st) {
+    const int3 nb0 = make_int3(li.bins[0] >> L, li.bins[1] >> L, li.bins[2] >> L);
+    cudaMemsetAsync(bb.d_n_ne, 0, sizeof(int32_t), st);
+    kt_point("memset:n_ne");
+    k_pair_blocks<<<max_ctas(8), 256, 0, st>>>(L, li.bins[0], li.bins[1], nb0, pairs, d_n_pairs, cap,
+                                               g->d_level_start, g->d_child, bb.blk, bb.cnt, bb.ne,
+                                               bb.d_n_ne);
+    int rc = check_launch("k_pair_blocks");
+    if (rc) return rc;
+    cudaError_t e = scan_launch_fn(LoadCnt{bb.cnt}, EmitBase{bb.base, bb.cur}, (int64_t)g->capacity,
+                                   ScanLevelN{g->d_level_start, L}, bb.d_total, bb.scan_ws, st);
+    kt_point("scan_kernel");
+    if (e != cudaSuccess) return set_cuda_error(e, "block bins scan");
+    k_pair_scatter<<<max_ctas(8), 256, 0, st>>>(pairs, d_n_pairs, cap, bb.blk, bb.cur, bb.face_ids);
+    return check_launch("k_pair_scatter");
+}
+
 // pair list in face-major order (API compute_bin_pairs)
 __global__ void k_pairs_emit(int nlim, const int32_t *__restrict__ map, const int32_t *__restrict__ d_n_map,
                              int64_t n_static, const int32_t *__restrict__ slots,

@@ -48,6 +48,8 @@ int launch_iota(int32_t *out, int64_t n, int32_t *d_n, cudaStream_t st);
 // scans
 int launch_compact(const uint8_t *ind, int64_t n, int32_t *map, int32_t *d_count, void *ws,
                    cudaStream_t st);
+int launch_compact_bits(const uint16_t *bits, int L, int64_t n, int32_t *map, int32_t *d_count,
+                        void *ws, cudaStream_t st);
 int launch_exclusive_scan(const int32_t *in, int64_t n_bound, const int32_t *d_n, int32_t *out,
                           int32_t *d_total, void *ws, cudaStream_t st);
 
@@ -79,7 +81,35 @@ int assemble_impl(const int32_t *pair_bin, const int32_t *pair_face, const int32
                   int64_t pair_cap, int64_t n_bins, int32_t *counts, int32_t *offsets,
                   int32_t *face_ids, void *ws, size_t ws_bytes, cudaStream_t st);
 
+// block-indexed bins of one level (the embed's bins; pin A4): the bin faces
+// of level-local block u are face_ids[base[u] .. base[u] + cnt[u]); ne lists
+// the blocks with at least one face (unordered)
+struct BlockBins {
+    int32_t *blk;       // [pair_cap] level-local block of each pair (-1: no block)
+    int32_t *face_ids;  // [pair_cap] grouped by block
+    int32_t *cnt;       // [capacity] pairs per block (all zero between levels)
+    int32_t *base;      // [capacity] first face_ids slot of the block
+    int32_t *cur;       // [capacity] scatter cursors
+    int32_t *ne;        // [capacity] nonempty blocks
+    int32_t *d_n_ne;    // [1]
+    int32_t *d_total;   // [1] pairs kept
+    void *scan_ws;      // scan over capacity
+};
+size_t block_bins_bytes(int32_t capacity, int64_t pair_cap);
+void block_bins_layout(int32_t capacity, int64_t pair_cap, char *base, BlockBins *bb);
+// embed pairs: compact (bin, face) list of one level (k_pairs' accepted set)
+int pairs_append_impl(const LevelInfo &li, int nlim, const double *faces, int64_t F,
+                      const int32_t *map, const int32_t *d_n_map, int2 *pairs, int32_t *d_n_pairs,
+                      int64_t cap, int32_t *d_status, cudaStream_t st);
+// pairs -> level-L blocks (forest descent), counts, scan, scatter
+int block_bins_impl(const LevelInfo &li, int L, vf_grid *g, const int2 *pairs,
+                    const int32_t *d_n_pairs, int64_t cap, const BlockBins &bb, cudaStream_t st);
+
 // voxelizer
+// block-indexed bins (embed): zero_cnt restores bb.cnt to zero for the next level
+int voxelize_blocks_impl(const LevelInfo &li, vf_grid *g, int L, const BlockBins &bb,
+                         const double *faces, bool zero_cnt, cudaStream_t st);
+// dense BinLevel (SPEC op partial_surface_voxelize): gathered per block first
 int voxelize_impl(const LevelInfo &li, vf_grid *g, int L, const vf_bins *bins,
                   const double *faces, cudaStream_t st);
 size_t propagate_workspace_size(int32_t capacity);

@@ -18,6 +18,7 @@
 //   K-xapply status entering each block -> SOLID fill; fused finalize
 //            (GUARD->FLUID, block solid flag).
 #include <math.h>
+#include <string.h>
 
 #include "vf_common.cuh"
 #include "vf_internal.h"
@@ -25,199 +26,249 @@
 namespace vf {
 
 // --------------------------------------------------------------------------
-// K-vox
+// K-vox: Alg. 3 over block-indexed bins, flattened over (block, face) pairs.
+//
+// A CTA takes a group of 32 nonempty level-L blocks and spreads the group's
+// (block, bin face) pairs over its threads, one pair per thread: every face
+// record load is independent, so the dependent coords -> bin -> face-id ->
+// record chain of a warp-per-block loop no longer serialises the level.
+// Per pair: the x-rows of the block whose centre (y, z) lies within eps of the
+// face's y / z extent (the SAT's exact box-axis comparisons), then the FP32
+// row classifier (exact SAT in its undecided band); per hit row the 4 cell
+// distances d = ((v1 - x) . n) / n_x (A7 association).  The A7 minimum per
+// cell -- |d|, ties to the lowest face id -- is reduced in shared memory in
+// rounds of one hit row per thread:
+//   (1) every candidate notes the cell's best |d| before the round,
+//   (2) 64-bit atomicMin of |d| (IEEE bits of a non-negative double are
+//       ordered as the values),
+//   (3) a cell whose best |d| dropped forgets the previous winner's id,
+//   (4) atomicMin of the face id among the candidates at the best |d|,
+//   (5) the winner records SOLID (n_x d > 0) or GUARD.
+// Order-free, hence deterministic.  Write-back per row word with the A9 rule,
+// only for rows with a hit (eta == 0: no write, Alg. 3 l.648).  Internal
+// propagation is a provable no-op with matched bins (A8).
+constexpr int kVoxT = 128;  // threads per CTA
+constexpr int kVoxG = 32;   // nonempty blocks per group
 
-struct VoxFace {  // shared-memory face record (128 B): what the row loop reads
-    double v1[3];    // first vertex (distances, classifier offsets)
-    double n[3];     // host unit normal
-    double yz[4];    // y / z extent of the face (exact box-axis reject)
-    RowClass rc;     // FP32 row classifier
-    int32_t fid;     // face id (A7 tie-break)
-    int32_t skip;    // |n_x| < EPS_PARALLEL: no x distance (A7)
+struct VoxGroup {
+    unsigned long long bd[kVoxG * 64];  // best |d| per (block, cell); +inf = no hit
+    int32_t bfid[kVoxG * 64];           // face id of the best
+    uint8_t bval[kVoxG * 64];           // SOLID / GUARD of the best
+    int32_t pre[kVoxG + 1];             // exclusive prefix of the blocks' pair counts
+    int32_t base[kVoxG];                // first face_ids slot of each block
+    int32_t bid[kVoxG];                 // block id (-1: past the list)
+    int4 co[kVoxG];                     // block coordinates
 };
 
-constexpr int kVoxWarps = 4;
+constexpr unsigned long long kInf64 = 0x7ff0000000000000ull;
 
 #ifndef VF_VOX_MINB
-#define VF_VOX_MINB 6
+#define VF_VOX_MINB 4
 #endif
-__global__ void __launch_bounds__(kVoxWarps * 32, VF_VOX_MINB)
+__global__ void __launch_bounds__(kVoxT, VF_VOX_MINB)
     k_voxelize(LevelInfo li, int L, const int32_t *__restrict__ level_start,
                const int32_t *__restrict__ coords, uint8_t *__restrict__ masks,
-               const int32_t *__restrict__ offsets, const int32_t *__restrict__ d_total,
+               const int32_t *__restrict__ ne, const int32_t *__restrict__ d_n_ne,
+               const int32_t *__restrict__ base, int32_t *__restrict__ cnt, int zero_cnt,
                const int32_t *__restrict__ face_ids, const double *__restrict__ faces) {
-    __shared__ VoxFace s_face[kVoxWarps][32];
-    // per block: the (row, face) pairs whose row pierces the face, and per
-    // (row, cell) slot the best (|d|, face id) and its mask value
-    __shared__ uint16_t s_hit[kVoxWarps][16 * 32];
-    __shared__ unsigned long long s_ad[kVoxWarps][64], s_fad[kVoxWarps][64];  // best |d|; |d| of s_fid
-    __shared__ int32_t s_fid[kVoxWarps][64];
-    __shared__ uint8_t s_hv[kVoxWarps][64];
-    const int64_t n_bins = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
-    const int32_t total = *d_total;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t gw = (int64_t)blockIdx.x * kVoxWarps + wib, nw = (int64_t)gridDim.x * kVoxWarps;
-    const int32_t s = level_start[L], e = level_start[L + 1];
-    const int r = lane & 15, half = lane >> 4;
-    const int J = r & 3, K = r >> 2;
+    __shared__ VoxGroup S;
+    const int t = threadIdx.x;
+    const int n_ne = *d_n_ne;
+    const int32_t s = level_start[L];
+    const int n_groups = (n_ne + kVoxG - 1) / kVoxG;
     const double dx = li.dx, eps = li.eps, lx = li.len[0];
     uint32_t *masks32 = reinterpret_cast<uint32_t *>(masks);
-
-    // tiles of 32 blocks: each lane fetches one block's bin header, so the
-    // dependent coords -> counts loads of 32 blocks overlap; only blocks with
-    // a non-empty bin are then processed, one at a time by the whole warp
-    // (warp gw owns blocks s + gw + k*nw; a tile is 32 consecutive k, which
-    // keeps the strided spread of busy blocks over warps)
-    for (int64_t k0 = 0; s + gw + k0 * nw < e; k0 += 32) {
-      const int64_t bl = s + gw + (k0 + lane) * nw;
-      int4 co_l = make_int4(0, 0, 0, 0);
-      int nf_l = 0, off_l = 0;
-      if (bl < e) {
-          co_l = *reinterpret_cast<const int4 *>(coords + 4 * bl);
-          const int64_t bin_l = co_l.x + (int64_t)li.bins[0] * (co_l.y + (int64_t)li.bins[1] * co_l.z);
-          // bin slice [offsets[bin], offsets[bin+1]) -- counts are not read, so
-          // the embed can skip restoring them after the counting-sort scatter
-          off_l = offsets[bin_l];
-          nf_l = (bin_l + 1 < n_bins ? offsets[bin_l + 1] : total) - off_l;
-      }
-      uint32_t todo = __ballot_sync(0xffffffffu, nf_l > 0);
-      while (todo) {
-        const int src = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const int64_t b = s + gw + (k0 + src) * nw;
-        int4 co;
-        co.x = __shfl_sync(0xffffffffu, co_l.x, src);
-        co.y = __shfl_sync(0xffffffffu, co_l.y, src);
-        co.z = __shfl_sync(0xffffffffu, co_l.z, src);
-        const int n_f = __shfl_sync(0xffffffffu, nf_l, src);
-        const int32_t off = __shfl_sync(0xffffffffu, off_l, src);
-        const double y = node_c(4 * co.y + J, dx), z = node_c(4 * co.z + K, dx);
-        const double my = VF_DSUB(y, eps), My = VF_DADD(y, eps);
-        const double mz = VF_DSUB(z, eps), Mz = VF_DADD(z, eps);
-        double x[4];
-#pragma unroll
-        for (int I = 0; I < 4; ++I) x[I] = node_c(4 * co.x + I, dx);
-        // Two phases per batch of 32 faces: (1) lanes = (row, face parity)
-        // classify the (row, face) pairs and compact the piercing ones into a
-        // warp list; (2) the 4 cell distances of every listed pair run on
-        // full warps (one (pair, cell) per lane), each reduced into its
-        // (row, cell) slot by the A7 order (|d| then face id) with shared
-        // 64-bit atomicMin on the IEEE bits of |d| (>= 0: monotone) and then
-        // on the face id among equal |d|; the winner records SOLID / GUARD.
-        if (lane < 64 / 2) {
-            s_ad[wib][lane] = 0x7ff0000000000000ull;  // +inf
-            s_ad[wib][lane + 32] = 0x7ff0000000000000ull;
-            s_fad[wib][lane] = 0x7ff0000000000000ull;
-            s_fad[wib][lane + 32] = 0x7ff0000000000000ull;
-            s_fid[wib][lane] = 0x7fffffff;
-            s_fid[wib][lane + 32] = 0x7fffffff;
-        }
-        for (int base = 0; base < n_f; base += 32) {
-            const int cnt = min(32, n_f - base);
-            if (lane < cnt) {
-                const int64_t f = face_ids[off + base + lane];
-                double v[9], nn[3];
-                load_face(faces, f, v, nn);
-                VoxFace &vf_ = s_face[wib][lane];
-                vf_.fid = (int32_t)f;
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    vf_.v1[d] = v[d];
-                    vf_.n[d] = nn[d];
-                }
-                vf_.yz[0] = fmin(fmin(v[1], v[4]), v[7]);
-                vf_.yz[1] = fmax(fmax(v[1], v[4]), v[7]);
-                vf_.yz[2] = fmin(fmin(v[2], v[5]), v[8]);
-                vf_.yz[3] = fmax(fmax(v[2], v[5]), v[8]);
-                row_class_init(vf_.rc, v, nn, fmin(fmin(v[0], v[3]), v[6]), fmax(fmax(v[0], v[3]), v[6]),
-                               dx, eps, lx);
-                vf_.skip = fabs(nn[0]) < li.eps_par;  // A7: no x distance
+    for (int gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
+        if (t < 32) {  // group header: blocks, pair counts, prefix
+            const int idx = gi * kVoxG + t;
+            int u = -1, c = 0, bs = 0;
+            if (idx < n_ne) {
+                u = ne[idx];
+                c = cnt[u];
+                bs = base[u];
+                S.co[t] = reinterpret_cast<const int4 *>(coords)[s + u];
+                if (zero_cnt) cnt[u] = 0;  // the next level's histogram starts from zero
             }
-            __syncwarp();
-            int nh = 0;
-            for (int q0 = 0; q0 < cnt; q0 += 2) {
-                const int q = q0 + half;
-                bool hit = false;
-                if (q < cnt) {
-                    const VoxFace &F = s_face[wib][q];
-                    if (!F.skip && !(F.yz[1] < my || My < F.yz[0] || F.yz[3] < mz || Mz < F.yz[2])) {
-                        const int cls = row_class(F.rc, (float)VF_DSUB(y, F.v1[1]), (float)VF_DSUB(z, F.v1[2]));
-                        hit = cls == 1 || (cls == 2 && row_sat_exact_f(faces, F.fid, y, z, eps, lx));
+            int inc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (t >= o) inc += y;
+            }
+            S.pre[t + 1] = inc;
+            if (t == 0) S.pre[0] = 0;
+            S.base[t] = bs;
+            S.bid[t] = u < 0 ? -1 : s + u;
+        }
+        for (int i = t; i < kVoxG * 64; i += kVoxT) {
+            S.bd[i] = kInf64;
+            S.bfid[i] = 0x7fffffff;
+        }
+        __syncthreads();
+        const int np = S.pre[kVoxG];
+        for (int c0 = 0; c0 < np; c0 += kVoxT) {
+            const int j = c0 + t;
+            uint32_t hm = 0;  // hit rows r = J + 4K of this thread's pair
+            int w = 0, fid = 0;
+            double v1[3] = {0.0, 0.0, 0.0}, nn[3] = {0.0, 0.0, 0.0};
+            int4 co = make_int4(0, 0, 0, 0);
+            if (j < np) {
+#pragma unroll
+                for (int st = 16; st > 0; st >>= 1)  // block of pair j: pre[w] <= j < pre[w + 1]
+                    if (S.pre[w + st] <= j) w += st;
+                fid = face_ids[S.base[w] + (j - S.pre[w])];
+                co = S.co[w];
+                double v[9];
+                load_face(faces, fid, v, nn);
+                v1[0] = v[0]; v1[1] = v[1]; v1[2] = v[2];
+                if (!(fabs(nn[0]) < li.eps_par)) {  // A7: no x distance for faces parallel to x
+                    const double ylo = fmin(fmin(v[1], v[4]), v[7]), yhi = fmax(fmax(v[1], v[4]), v[7]);
+                    const double zlo = fmin(fmin(v[2], v[5]), v[8]), zhi = fmax(fmax(v[2], v[5]), v[8]);
+                    uint32_t jm = 0, km = 0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const double y = node_c(4 * co.y + q, dx), z = node_c(4 * co.z + q, dx);
+                        if (!(yhi < VF_DSUB(y, eps) || VF_DADD(y, eps) < ylo)) jm |= 1u << q;
+                        if (!(zhi < VF_DSUB(z, eps) || VF_DADD(z, eps) < zlo)) km |= 1u << q;
+                    }
+                    if (jm && km) {
+                        RowClass rc;
+                        row_class_init(rc, v, nn, fmin(fmin(v[0], v[3]), v[6]), fmax(fmax(v[0], v[3]), v[6]),
+                                       dx, eps, lx);
+                        for (uint32_t kk = km; kk; kk &= kk - 1) {
+                            const int K = __ffs(kk) - 1;
+                            const double z = node_c(4 * co.z + K, dx);
+                            for (uint32_t jj = jm; jj; jj &= jj - 1) {
+                                const int J = __ffs(jj) - 1;
+                                const double y = node_c(4 * co.y + J, dx);
+                                const int cls = row_class(rc, (float)VF_DSUB(y, v[1]), (float)VF_DSUB(z, v[2]));
+                                if (cls == 1 || (cls == 2 && row_sat_exact_f(faces, fid, y, z, eps, lx)))
+                                    hm |= 1u << (J + 4 * K);
+                            }
+                        }
                     }
                 }
-                const uint32_t m = __ballot_sync(0xffffffffu, hit);
-                if (hit) s_hit[wib][nh + __popc(m & ((1u << lane) - 1u))] = (uint16_t)(r | (q << 4));
-                nh += __popc(m);
             }
-            __syncwarp();
-            for (int k0 = 0; k0 < 4 * nh; k0 += 32) {
-                const int k = k0 + lane;
-                bool act = k < 4 * nh;
-                int slot = 0, fid = 0;
-                unsigned long long adb = 0;
-                double nx = 0.0, d = 0.0;
-                if (act) {
-                    const uint32_t h = s_hit[wib][k >> 2];
-                    const int rr = h & 15, q = h >> 4, I = k & 3;
-                    const VoxFace &F = s_face[wib][q];
-                    const double yy = node_c(4 * co.y + (rr & 3), dx), zz = node_c(4 * co.z + (rr >> 2), dx);
-                    nx = F.n[0];
-                    d = VF_DDIV(plane_num(F.v1, F.n, x[I], yy, zz), nx);
-                    adb = (unsigned long long)__double_as_longlong(fabs(d));
-                    slot = 4 * rr + I;
-                    fid = F.fid;
-                    atomicMin(&s_ad[wib][slot], adb);
+            // rounds of one hit row per thread (A7 reduction, see above)
+            while (__syncthreads_or(hm != 0)) {
+                const bool has = hm != 0;
+                int slot0 = 0;
+                unsigned long long db[4] = {kInf64, kInf64, kInf64, kInf64}, old[4];
+                bool solid[4] = {false, false, false, false};
+                if (has) {
+                    const int r = __ffs(hm) - 1;
+                    hm &= hm - 1;
+                    const double y = node_c(4 * co.y + (r & 3), dx), z = node_c(4 * co.z + (r >> 2), dx);
+                    slot0 = w * 64 + 4 * r;
+#pragma unroll
+                    for (int I = 0; I < 4; ++I) {
+                        const double d = VF_DDIV(plane_num(v1, nn, node_c(4 * co.x + I, dx), y, z), nn[0]);
+                        db[I] = (unsigned long long)__double_as_longlong(fabs(d));
+                        solid[I] = VF_DMUL(nn[0], d) > 0.0;
+                        old[I] = S.bd[slot0 + I];
+                    }
                 }
-                __syncwarp();
-                act = act && s_ad[wib][slot] == adb;
-                if (act && s_fad[wib][slot] != adb) s_fid[wib][slot] = 0x7fffffff;  // a new best |d|
-                __syncwarp();
-                if (act) {
-                    s_fad[wib][slot] = adb;
-                    atomicMin(&s_fid[wib][slot], fid);
-                }
-                __syncwarp();
-                if (act && s_fid[wib][slot] == fid)
-                    s_hv[wib][slot] = (VF_DMUL(nx, d) > 0.0) ? VF_SOLID : VF_GUARD;
-                __syncwarp();
+                __syncthreads();
+                if (has)
+#pragma unroll
+                    for (int I = 0; I < 4; ++I) atomicMin(&S.bd[slot0 + I], db[I]);
+                __syncthreads();
+                bool best[4] = {false, false, false, false};
+                if (has)
+#pragma unroll
+                    for (int I = 0; I < 4; ++I) {
+                        const unsigned long long b = S.bd[slot0 + I];
+                        best[I] = b == db[I];
+                        if (best[I] && b < old[I]) S.bfid[slot0 + I] = 0x7fffffff;  // new best |d|
+                    }
+                __syncthreads();
+#pragma unroll
+                for (int I = 0; I < 4; ++I)
+                    if (best[I]) atomicMin(&S.bfid[slot0 + I], fid);
+                __syncthreads();
+#pragma unroll
+                for (int I = 0; I < 4; ++I)
+                    if (best[I] && S.bfid[slot0 + I] == fid) S.bval[slot0 + I] = solid[I] ? VF_SOLID : VF_GUARD;
             }
-            __syncwarp();
         }
-        uint32_t hit = 0, bh = 0;
-        if (!half) {
+        __syncthreads();
+        // write-back: one row word (4 cells) per thread, A9 rule
+        for (int i = t; i < kVoxG * 16; i += kVoxT) {
+            const int w = i >> 4, r = i & 15;
+            const int32_t b = S.bid[w];
+            if (b < 0) continue;
+            uint32_t hit = 0, bh = 0;
 #pragma unroll
             for (int I = 0; I < 4; ++I)
-                if (s_ad[wib][4 * r + I] != 0x7ff0000000000000ull) {
+                if (S.bd[w * 64 + 4 * r + I] != kInf64) {
                     hit |= 1u << I;
-                    bh |= (uint32_t)s_hv[wib][4 * r + I] << (8 * I);
+                    bh |= (uint32_t)S.bval[w * 64 + 4 * r + I] << (8 * I);
                 }
-        }
-        const bool any = __any_sync(0xffffffffu, hit != 0);
-        if (any && !half) {  // eta == 0 -> no write (Alg. 3 l.648)
-            uint32_t *w = masks32 + b * 16 + r;
-            const uint32_t orig = *w;
+            if (!hit) continue;
+            uint32_t *wp = masks32 + (int64_t)b * 16 + r;
+            const uint32_t orig = *wp;
             uint32_t out = orig;
 #pragma unroll
             for (int I = 0; I < 4; ++I) {
                 if (!(hit >> I & 1)) continue;
                 const uint32_t o = (orig >> (8 * I)) & 0xffu, hn = (bh >> (8 * I)) & 0xffu;
-                // A9 write rule
                 if (hn == VF_SOLID || (o != VF_GHOST && o != VF_INTERFACE))
                     out = (out & ~(0xffu << (8 * I))) | (hn << (8 * I));
             }
-            if (out != orig) *w = out;
+            if (out != orig) *wp = out;
         }
-        __syncwarp();
-      }
+        __syncthreads();
     }
 }
 
-int voxelize_impl(const LevelInfo &li, vf_grid *g, int L, const vf_bins *bins,
-                  const double *faces, cudaStream_t st) {
-    k_voxelize<<<max_ctas(VF_VOX_MINB), kVoxWarps * 32, 0, st>>>(li, L, g->d_level_start, g->d_coords,
-                                                      g->d_masks, bins->d_offsets, bins->d_n_face_ids,
-                                                      bins->d_face_ids, faces);
+int voxelize_blocks_impl(const LevelInfo &li, vf_grid *g, int L, const BlockBins &bb,
+                         const double *faces, bool zero_cnt, cudaStream_t st) {
+    k_voxelize<<<max_ctas(VF_VOX_MINB), kVoxT, 0, st>>>(li, L, g->d_level_start, g->d_coords, g->d_masks,
+                                                         bb.ne, bb.d_n_ne, bb.base, bb.cnt, zero_cnt ? 1 : 0,
+                                                         bb.face_ids, faces);
     return check_launch("k_voxelize");
+}
+
+// dense BinLevel -> per-block (base, count) + nonempty list (SPEC op path)
+__global__ void k_dense_to_blocks(int L, LevelInfo li, const int32_t *__restrict__ level_start,
+                                  const int32_t *__restrict__ coords, const int32_t *__restrict__ counts,
+                                  const int32_t *__restrict__ offsets, int32_t *__restrict__ cnt,
+                                  int32_t *__restrict__ base, int32_t *__restrict__ ne,
+                                  int32_t *__restrict__ d_n_ne) {
+    const int32_t s = level_start[L], e = level_start[L + 1];
+    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int4 c = reinterpret_cast<const int4 *>(coords)[b];
+        const int64_t bin = c.x + (int64_t)li.bins[0] * (c.y + (int64_t)li.bins[1] * c.z);
+        const int32_t u = (int32_t)(b - s), n = counts[bin];
+        cnt[u] = n;
+        base[u] = offsets[bin];
+        if (n > 0) ne[atomicAdd(d_n_ne, 1)] = u;
+    }
+}
+
+int voxelize_impl(const LevelInfo &li, vf_grid *g, int L, const vf_bins *bins, const double *faces,
+                  cudaStream_t st) {
+    // stream-ordered scratch (the library keeps no pointer past the call)
+    const size_t n = (size_t)g->capacity;
+    char *tmp = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&tmp, 3 * n * sizeof(int32_t) + 256, st);
+    if (e != cudaSuccess) return set_cuda_error(e, "voxelize scratch");
+    BlockBins bb;
+    memset(&bb, 0, sizeof(bb));
+    bb.cnt = (int32_t *)tmp;
+    bb.base = bb.cnt + n;
+    bb.ne = bb.base + n;
+    bb.d_n_ne = bb.ne + n;
+    bb.face_ids = bins->d_face_ids;
+    cudaMemsetAsync(bb.d_n_ne, 0, sizeof(int32_t), st);
+    k_dense_to_blocks<<<max_ctas(8), 256, 0, st>>>(L, li, g->d_level_start, g->d_coords, bins->d_counts,
+                                                   bins->d_offsets, bb.cnt, bb.base, bb.ne, bb.d_n_ne);
+    int rc = check_launch("k_dense_to_blocks");
+    if (!rc) rc = voxelize_blocks_impl(li, g, L, bb, faces, false, st);
+    e = cudaFreeAsync(tmp, st);
+    if (!rc && e != cudaSuccess) rc = set_cuda_error(e, "voxelize scratch");
+    return rc;
 }
 
 // --------------------------------------------------------------------------

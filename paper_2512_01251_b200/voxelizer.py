@@ -250,6 +250,26 @@ class EmbedEngine:
             _lib.ptr(self.cmap), _lib.ptr(self.n_b_dev), _lib.ptr(self.lengths), self.lengths_cap,
             _lib.ptr(self.ws), self.ws.numel(), st, lev), "embed_geometry")
 
+    def _grow_pairs(self) -> bool:
+        """After a phase 1: if the per-level (bin, face) pair list overflowed
+        (VF_ECAPACITY with the required count in status[3]), enlarge it and
+        the workspace; True = rerun."""
+        import torch
+        self.host[0:4].copy_(self.grid.status, non_blocking=True)
+        self.stream.synchronize()
+        _lib.check(self.lib.vf_side_sync(), "embed_geometry")
+        need = int(self.host[3])
+        if int(self.host[0]) != 2 or need <= 0:
+            return False
+        self.c.pair_cap = int(need * 1.25) + 65536
+        wsb = self.lib.vf_embed_workspace_size(C.byref(self.c), self.mesh.n_faces, self.grid.capacity)
+        self.ws = None
+        self.ws = torch.empty(int(wsb), dtype=torch.uint8, device="cuda")
+        for g in self._graphs.values():
+            self.lib.vf_graph_destroy(g)
+        self._graphs.clear()
+        return True
+
     def _finish(self, st_obj):
         """Async read of status + N_b, one sync, error mapping."""
         import torch
@@ -275,10 +295,15 @@ class EmbedEngine:
         st = _lib.stream_ptr(self.stream)
         with torch.cuda.stream(self.stream):
             if self.lengths is None:
-                # first run: learn N_b (one extra sync), size the LUT
-                self.grid.status.zero_()
-                gs = self._phase1(uf, st, None)
-                n_b = self._finish(self.stream)
+                # first run: learn N_b (one extra sync), size the LUT; a
+                # (bin, face) pair list that overflowed is re-sized and rerun
+                while True:
+                    self.grid.status.zero_()
+                    gs = self._phase1(uf, st, None)
+                    if self._grow_pairs():
+                        continue
+                    n_b = self._finish(self.stream)
+                    break
                 self._alloc_lut(n_b)
             if timed or not self.use_graph:
                 self._ensure_events()
