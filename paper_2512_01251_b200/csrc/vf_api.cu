@@ -160,8 +160,10 @@ static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 struct EmbedWs {
     int2 *pairs[2];       // per-level (bin, face) lists, ping-pong: pairs(L+1) built while level L runs
     int32_t *n_pairs[2];
-    int32_t *map[2];      // kept faces of the level (compact_map)
+    int32_t *map[2];      // kept faces of one level (sharded path: per-level indicators)
     int32_t *n_map[2];
+    int32_t *maps;        // [l_max][F + 1] kept faces of every level (k_indicators_all)
+    int32_t *n_maps;      // [l_max]
     int64_t pair_cap;
     BlockBins bb;         // the level's block-indexed bins
     uint8_t *ind8;        // [F] per-level indicators (sharded path)
@@ -170,7 +172,6 @@ struct EmbedWs {
     void *prop_ws, *mark_ws, *adapt_ws, *tab_ws, *link_ws;
     size_t prop_b, mark_b, adapt_b, tab_b, link_b;
     int32_t *bcount;
-    uint16_t *ind_bits;  // [F] per-level 1D indicator bits
     void *lines_ws;      // recorded piercing lines of the link enumeration
     void *shard_ws;      // multi-GPU: row histogram / owner scan / face subset
 };
@@ -227,31 +228,30 @@ static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *b
     t.adapt_ws = take(t.adapt_b);
     t.tab_b = tables_workspace_size(cap);
     t.tab_ws = take(t.tab_b);
-    t.link_b = link_workspace_size(cfg, Lf);
+    t.link_b = link_workspace_size(cfg, Lf, cap);
     t.link_ws = take(t.link_b);
-    t.ind_bits = (uint16_t *)take(sizeof(uint16_t) * (size_t)(F + 1));
-    t.lines_ws = take(link_lines_bytes(F));
+    t.maps = (int32_t *)take(sizeof(int32_t) * (size_t)(F + 1) * cfg.l_max);
+    t.n_maps = (int32_t *)take(sizeof(int32_t) * VF_MAX_LEVELS);
+    t.lines_ws = take(link_lines_bytes(cfg, F, cap));
     t.bcount = (int32_t *)take(sizeof(int32_t) * (size_t)cap);
     t.shard_ws = cfg.shard_count > 1 ? take(shard_scratch_size(cfg, F)) : nullptr;
     if (w) *w = t;
     return off;
 }
 
-// the (bin, face) pairs of level L: kept faces (1D indicators: precomputed
-// bits, or computed here), then k_pairs_append
+// the (bin, face) pairs of level L: kept faces (1D indicators: the embed's
+// per-level maps from k_indicators_all, or computed here), then k_pairs_append
 static int level_pairs(const vf_config &cfg, const LevelInfo &li, const double *faces, int64_t F,
-                       int use_filter, const uint16_t *ind_bits, EmbedWs &w, int k, int32_t *d_status,
+                       int use_filter, bool pre_maps, EmbedWs &w, int k, int32_t *d_status,
                        cudaStream_t st) {
     const int32_t *map = nullptr, *nmap = nullptr;
     int rc;
-    if (use_filter) {
-        if (ind_bits) {
-            rc = launch_compact_bits(ind_bits, li.level, F, w.map[k], w.n_map[k], w.bins_ws, st);
-        } else {
-            if ((rc = launch_indicators(li, 0, faces, F, w.ind8, st))) return rc;
-            rc = launch_compact(w.ind8, F, w.map[k], w.n_map[k], w.bins_ws, st);
-        }
-        if (rc) return rc;
+    if (use_filter && pre_maps) {
+        map = w.maps + (int64_t)li.level * (F + 1);
+        nmap = w.n_maps + li.level;
+    } else if (use_filter) {
+        if ((rc = launch_indicators(li, 0, faces, F, w.ind8, st))) return rc;
+        if ((rc = launch_compact(w.ind8, F, w.map[k], w.n_map[k], w.bins_ws, st))) return rc;
         map = w.map[k];
         nmap = w.n_map[k];
     }
@@ -425,7 +425,7 @@ int vf_link_tables(const vf_config *cfg, vf_grid *grid, const int32_t *bcount, i
 
 size_t vf_link_workspace_size(const vf_config *cfg, const vf_grid *g) {
     if (!valid_cfg(cfg) || !g) return 0;
-    return link_workspace_size(*cfg, g->n_levels - 1);
+    return link_workspace_size(*cfg, g->n_levels - 1, g->capacity);
 }
 
 int vf_link_lengths(const vf_config *cfg, vf_grid *grid, const int32_t *cmap, const double *faces,
@@ -580,13 +580,16 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     const bool serial_links = g_serial_links || one;
     if (!serial_links) {
         cudaStreamWaitEvent(side->st3, side->fork, 0);
-        VF_TRY(link_enum_impl(*cfg, faces, F, w.link_ws, w.lines_ws, side->st3, events ? events + 58 : nullptr));
+        VF_TRY(link_enum_impl(*cfg, faces, F, w.link_ws, w.lines_ws, g->capacity, side->st3,
+                              events ? events + 58 : nullptr));
         cudaEventRecord(side->join3, side->st3);
     }
     // Alg. 1 indicators of every level in one pass over the face records
-    if (use_filter) VF_TRY(launch_indicators_all(*cfg, faces, F, w.ind_bits, s2));
+    // (its per-warp map queues cover 8 levels; deeper forests: per-level indicators)
+    const bool pre = cfg->l_max <= 8;
+    if (use_filter && pre) VF_TRY(launch_indicators_all(*cfg, faces, F, nullptr, w.maps, F + 1, w.n_maps, s2));
     auto build = [&](int L) {
-        return level_pairs(*cfg, make_level(*cfg, L), faces, F, use_filter, w.ind_bits, w, L & 1, g->d_status, s2);
+        return level_pairs(*cfg, make_level(*cfg, L), faces, F, use_filter, pre, w, L & 1, g->d_status, s2);
     };
     // the block histograms start from zero (each level's voxelizer restores them)
     cudaMemsetAsync(w.bb.cnt, 0, sizeof(int32_t) * (size_t)g->capacity, st);
@@ -617,10 +620,11 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     cudaEventRecord(side->join, s2);
     cudaStreamWaitEvent(st, side->join, 0);
     VF_TRY(boundary_impl(*cfg, g, w.bcount, st));
-    VF_TRY(tables_impl(g, w.bcount, cmap, d_n_b, w.tab_ws, w.tab_b, st));
+    VF_TRY(tables_impl(g, w.bcount, cmap, d_n_b, w.tab_ws, w.tab_b, st,
+                       link_slot_inverse(*cfg, F, w.lines_ws, g->capacity)));
     rec(events, n_ev, &k, st);  // boundary + tables done
     if (serial_links) {  // measurement mode: the enumeration alone on the main stream
-        VF_TRY(link_enum_impl(*cfg, faces, F, w.link_ws, w.lines_ws, st, events ? events + 58 : nullptr));
+        VF_TRY(link_enum_impl(*cfg, faces, F, w.link_ws, w.lines_ws, g->capacity, st, events ? events + 58 : nullptr));
         cudaEventRecord(side->join3, st);
     }
     return VF_OK;
@@ -656,8 +660,8 @@ int vf_embed_phase2(const vf_config *cfg, const double *faces, int64_t F, vf_gri
     VF_TRY(side_stream(&side));
     // link_events[0..1] bracket the LUT fill + the resolution (the cut-link
     // kernels after the tables)
+    // (the LUT tiles are written whole by the resolution: no separate -1 fill)
     if (link_events) cudaEventRecord((cudaEvent_t)link_events[0], st);
-    VF_TRY(fill_lut_impl(d_n_b, lengths, lengths_cap, g->d_status, st));
     cudaStreamWaitEvent(st, side->join3, 0);  // the line enumeration of phase 1
     void *end_only[2] = {nullptr, link_events ? link_events[1] : nullptr};
     return link_resolve_impl(*cfg, g, cmap, faces, F, lengths, w.link_ws, w.lines_ws, st,
@@ -766,7 +770,7 @@ int vf_shard_level(const vf_config *cfg, const double *faces, int64_t F, int use
         cudaMemsetAsync(w.bb.cnt, 0, sizeof(int32_t) * (size_t)g->capacity, st);
         kt_point("memset:block_counts");
     }
-    VF_TRY(level_pairs(*cfg, li, faces, F, use_filter, nullptr, w, 0, g->d_status, st));
+    VF_TRY(level_pairs(*cfg, li, faces, F, use_filter, false, w, 0, g->d_status, st));
     VF_TRY(block_bins_impl(li, L, g, w.pairs[0], w.n_pairs[0], w.pair_cap, w.bb, st));
     VF_TRY(voxelize_blocks_impl(li, g, L, w.bb, faces, true, st));
     VF_TRY(propagate_level_impl(li, g, L, w.prop_ws, w.prop_b, st));

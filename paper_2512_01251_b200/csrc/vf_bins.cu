@@ -132,15 +132,30 @@ __global__ void __launch_bounds__(kIndWarps * 32, 3)
 // of face f at level L.  Candidate rows are decided by the FP32 row
 // classifier (vf_common.cuh); only undecided rows run the exact SAT.  Same
 // predicate as indicator_rows, row for row.
+constexpr int kIndQLevels = 8;  // per-warp queues: levels 0..7 (the embed's l_max <= 8)
+
+// The kept faces of every level are appended straight to that level's
+// compact_map: no compaction scan over F per level.  Each warp queues its
+// kept faces per level in shared memory and reserves global slots 32 at a
+// time (one atomic per 32 faces: per-warp-iteration atomics on the few level
+// counters serialised in L2).  The maps are unordered -- the embed's pair
+// lists and block bins are order-free (the voxelizer breaks ties by face id).
 __global__ void __launch_bounds__(256, VF_IND_MINB)
     k_indicators_all(LevelSet ls, const double *__restrict__ faces, int64_t F,
-                     uint16_t *__restrict__ out) {
-    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < F;
-         f += (int64_t)gridDim.x * blockDim.x) {
-        double v[9], n[3];
-        load_face(faces, f, v, n);
+                     uint16_t *__restrict__ out, int32_t *__restrict__ maps, int64_t map_stride,
+                     int32_t *__restrict__ n_maps) {
+    __shared__ int32_t s_q[8][kIndQLevels][64];
+    __shared__ int s_qn[8][kIndQLevels];  // queue lengths (warp-uniform)
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    if (lane < kIndQLevels) s_qn[wq][lane] = 0;
+    __syncwarp();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t f0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); f0 < F; f0 += stride) {
+        const int64_t f = f0 + lane;
         uint32_t bits = 0;
-        if (!(fabs(n[0]) < ls.li[0].eps_par)) {
+        double v[9], n[3];
+        if (f < F) load_face(faces, f, v, n);
+        if (f < F && !(fabs(n[0]) < ls.li[0].eps_par)) {
             const double xlo = fmin(fmin(v[0], v[3]), v[6]), xhi = fmax(fmax(v[0], v[3]), v[6]);
             // level-independent part of the row classifier (row_class_init):
             // the yz edge functions, their lengths, orientation, fast-accept
@@ -202,12 +217,50 @@ __global__ void __launch_bounds__(256, VF_IND_MINB)
                 if (hit) bits |= 1u << L;
             }
         }
-        out[f] = (uint16_t)bits;
+        if (out && f < F) out[f] = (uint16_t)bits;
+        if (maps) {
+#pragma unroll
+            for (int L = 0; L < kIndQLevels; ++L) {
+                if (L >= ls.n) break;
+                const uint32_t m = __ballot_sync(0xffffffffu, (bits >> L) & 1u);
+                if (!m) continue;
+                int qn = s_qn[wq][L];
+                if ((bits >> L) & 1u) s_q[wq][L][qn + __popc(m & ((1u << lane) - 1u))] = (int32_t)f;
+                qn += __popc(m);
+                if (qn >= 32) {  // flush 32
+                    __syncwarp();
+                    int b = 0;
+                    if (lane == 0) b = atomicAdd(&n_maps[L], 32);
+                    b = __shfl_sync(0xffffffffu, b, 0);
+                    maps[L * map_stride + b + lane] = s_q[wq][L][lane];
+                    const int rest = qn - 32;
+                    const int32_t x = lane < rest ? s_q[wq][L][32 + lane] : 0;
+                    __syncwarp();
+                    if (lane < rest) s_q[wq][L][lane] = x;
+                    qn = rest;
+                }
+                __syncwarp();
+                if (lane == 0) s_qn[wq][L] = qn;
+                __syncwarp();
+            }
+        }
+    }
+    if (maps) {  // the warp's remainders
+#pragma unroll
+        for (int L = 0; L < kIndQLevels; ++L) {
+            __syncwarp();
+            const int qn = L < ls.n ? s_qn[wq][L] : 0;
+            if (!qn) continue;
+            int b = 0;
+            if (lane == 0) b = atomicAdd(&n_maps[L], qn);
+            b = __shfl_sync(0xffffffffu, b, 0);
+            if (lane < qn) maps[L * map_stride + b + lane] = s_q[wq][L][lane];
+        }
     }
 }
 
 int launch_indicators_all(const vf_config &cfg, const double *faces, int64_t F, uint16_t *out,
-                          cudaStream_t st) {
+                          int32_t *maps, int64_t map_stride, int32_t *n_maps, cudaStream_t st) {
     if (F <= 0) return VF_OK;
     LevelSet ls;
     ls.n = cfg.l_max;
@@ -219,7 +272,11 @@ int launch_indicators_all(const vf_config &cfg, const double *faces, int64_t F, 
     }
     int64_t g = (F + 255) / 256;
     if (g > max_ctas(8)) g = max_ctas(8);
-    k_indicators_all<<<(int)g, 256, 0, st>>>(ls, faces, F, out);
+    if (maps) {
+        cudaMemsetAsync(n_maps, 0, sizeof(int32_t) * cfg.l_max, st);
+        kt_point("memset:n_maps");
+    }
+    k_indicators_all<<<(int)g, 256, 0, st>>>(ls, faces, F, out, maps, map_stride, n_maps);
     return check_launch("k_indicators_all");
 }
 
@@ -623,18 +680,6 @@ int pairs_append_impl(const LevelInfo &li, int nlim, const double *faces, int64_
 // (I, J, K) >> L through the child links (child ids are parent-first + octant,
 // ox + 2 oy + 4 oz, vf_forest.cu) -- no dense B_L^3 map, no hash table.
 // Pairs whose bin holds no level-L block are dropped (never read).
-// (a level dropped on capacity exhaustion leaves child ids >= n_used: no block)
-__device__ __forceinline__ int32_t block_of_key(int L, int bi, int bj, int bk, const int3 nb0,
-                                                const int32_t *__restrict__ child, int32_t n_used) {
-    int32_t b = (bi >> L) + nb0.x * ((bj >> L) + nb0.y * (bk >> L));
-    for (int l = L - 1; l >= 0; --l) {
-        const int32_t c = child[b];
-        if (c < 0 || c >= n_used) return -1;
-        b = c + ((bi >> l) & 1) + 2 * ((bj >> l) & 1) + 4 * ((bk >> l) & 1);
-    }
-    return b;
-}
-
 // K1: pair -> level-local block u, per-block pair counts, the nonempty blocks
 __global__ void __launch_bounds__(256)
     k_pair_blocks(int L, int bx, int by, int3 nb0, const int2 *__restrict__ pairs,

@@ -270,6 +270,21 @@ __device__ __forceinline__ int warp_sum(int v) {
     return v;
 }
 
+// level-L block with block coordinates (bi, bj, bk), found by descending the
+// forest from its root block through the child links (child ids are
+// parent-first + octant, ox + 2 oy + 4 oz, vf_forest.cu); -1: no such block.
+// (a level dropped on capacity exhaustion leaves child ids >= n_used: no block)
+__device__ __forceinline__ int32_t block_of_key(int L, int bi, int bj, int bk, const int3 nb0,
+                                                const int32_t *__restrict__ child, int32_t n_used) {
+    int32_t b = (bi >> L) + nb0.x * ((bj >> L) + nb0.y * (bk >> L));
+    for (int l = L - 1; l >= 0; --l) {
+        const int32_t c = child[b];
+        if (c < 0 || c >= n_used) return -1;
+        b = c + ((bi >> l) & 1) + 2 * ((bj >> l) & 1) + 4 * ((bk >> l) & 1);
+    }
+    return b;
+}
+
 __device__ __forceinline__ void latch_status(int32_t *d_status, int code) {
     if (d_status) atomicMax(d_status, code);
 }

@@ -68,8 +68,10 @@ struct LevelSet {
     int widen[VF_MAX_LEVELS];
     int n;
 };
+// out (nullable): bit L of out[f]; maps (nullable): level L's kept faces at
+// maps + L * map_stride, count n_maps[L] (unordered)
 int launch_indicators_all(const vf_config &cfg, const double *faces, int64_t F, uint16_t *out,
-                          cudaStream_t st);
+                          int32_t *maps, int64_t map_stride, int32_t *n_maps, cudaStream_t st);
 int sort_bins(int64_t n_bins, const int32_t *offsets, const int32_t *d_total, int32_t *counts,
               int32_t *face_ids, int32_t *large, int32_t *scalars, int32_t *scratch,
               cudaStream_t st);
@@ -134,9 +136,10 @@ int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_byte
 // boundary / tables / links
 int boundary_impl(const vf_config &cfg, vf_grid *g, int32_t *bcount, cudaStream_t st);
 size_t tables_workspace_size(int32_t capacity);
+// inv (nullable): slot -> block id of every mapped block
 int tables_impl(vf_grid *g, const int32_t *bcount, int32_t *cmap, int32_t *d_n_b, void *ws,
-                size_t ws_bytes, cudaStream_t st);
-size_t link_workspace_size(const vf_config &cfg, int finest);
+                size_t ws_bytes, cudaStream_t st, int32_t *inv = nullptr);
+size_t link_workspace_size(const vf_config &cfg, int finest, int32_t capacity);
 int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
               int64_t F, const int32_t *map, const int32_t *d_n_map, float *lengths, void *ws,
               size_t ws_bytes, cudaStream_t st, void **events, const int32_t *d_n_b,
@@ -149,14 +152,17 @@ int shard_face_subset_impl(const vf_config &cfg, const double *faces, int64_t F,
                            int32_t *d_n_map, void *scratch, cudaStream_t st);
 // embed split of the link lengths: grid-independent line enumeration (side
 // stream, early) + resolution once the grid and the LUT slots exist
-size_t link_lines_bytes(int64_t F);
+size_t link_lines_bytes(const vf_config &cfg, int64_t F, int32_t capacity);
 const void *link_enum_kernel(int small);  // graph node priorities
 int link_stats(const vf_config &cfg, int64_t F, void *ws, void *lines_ws, int64_t out[7]);
 int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *ws, void *lines_ws,
-                   cudaStream_t st, void **events);
+                   int32_t capacity, cudaStream_t st, void **events);
+// inv: slot -> finest block (tables_impl's inverse output; nullptr: the
+// lines workspace's copy, link_slot_inverse)
 int link_resolve_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
                       int64_t F, float *lengths, void *ws, void *lines_ws, cudaStream_t st,
-                      void **events, const int32_t *d_n_b, int64_t lengths_cap);
+                      void **events, const int32_t *d_n_b, int64_t lengths_cap, const int32_t *inv = nullptr);
+int32_t *link_slot_inverse(const vf_config &cfg, int64_t F, void *lines_ws, int32_t capacity);
 int fill_lut_impl(const int32_t *d_n_b, float *lengths, int64_t cap, int32_t *d_status,
                   cudaStream_t st);
 

@@ -37,8 +37,11 @@
 #include <math.h>
 #include <string.h>
 
+#include <algorithm>
+
 #include "vf_common.cuh"
 #include "vf_internal.h"
+#include "vf_scan.cuh"
 
 #ifndef VF_LINK_MINB
 #define VF_LINK_MINB 6
@@ -46,15 +49,43 @@
 
 namespace vf {
 
-// dense finest-level block -> LUT slot map; nothing is mapped when the
-// device-resident N_b exceeds the LUT capacity (error latched by k_fill_lut)
-// (multi-GPU: only this rank's blocks are mapped, so every rank fills the
-// LUT slots of the blocks it owns)
-__global__ void k_blockmap(LevelInfo li, int L, const int32_t *__restrict__ level_start,
-                           const int32_t *__restrict__ coords, const int32_t *__restrict__ cmap,
-                           int32_t *__restrict__ bmap, const int32_t *__restrict__ d_n_b,
-                           int64_t cap) {
+// Finest-level block -> LUT slot: an open-addressing hash of the MAPPED
+// blocks only (N_b entries at load <= 1/2; a few MB, L2-resident) instead of
+// a dense B_L^3 map.  Entry = key << 24 | slot (key = bi + B_x (bj + B_y bk)
+// < 2^40, slot < 2^24), empty = ~0.  The table size follows the
+// device-resident N_b (pow2 >= 2 N_b, hinfo[0] = log2 size), so only the used
+// part is cleared.  Nothing is mapped when N_b exceeds the LUT capacity
+// (error latched by k_fill_lut).  Multi-GPU: only this rank's blocks are
+// mapped, so every rank fills the LUT slots of the blocks it owns.
+constexpr unsigned long long kHashEmpty = ~0ull;
+
+__device__ __forceinline__ uint64_t hash_slot0(uint64_t key, int bits) {
+    key ^= key >> 33;  // murmur3 finaliser: block keys are highly structured
+    key *= 0xff51afd7ed558ccdull;
+    key ^= key >> 33;
+    key *= 0xc4ceb9fe1a85ec53ull;
+    key ^= key >> 33;
+    return key >> (64 - bits);
+}
+
+__global__ void k_hash_clear(const int32_t *__restrict__ d_n_b, int64_t nb_static, int32_t *__restrict__ hinfo,
+                             unsigned long long *__restrict__ htab) {
+    const int64_t nb = d_n_b ? (int64_t)*d_n_b : nb_static;  // (SPEC op path: the grid capacity)
+    int bits = 10;
+    while ((1ll << bits) < 4 * nb) ++bits;  // load <= 1/4
+    if (blockIdx.x == 0 && threadIdx.x == 0) hinfo[0] = bits;
+    const int64_t n = 1ll << bits;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        htab[i] = kHashEmpty;
+}
+
+__global__ void k_hash_insert(LevelInfo li, int L, const int32_t *__restrict__ level_start,
+                              const int32_t *__restrict__ coords, const int32_t *__restrict__ cmap,
+                              const int32_t *__restrict__ hinfo, unsigned long long *__restrict__ htab,
+                              const int32_t *__restrict__ d_n_b, int64_t cap) {
     if (d_n_b && *d_n_b > cap) return;
+    const int bits = hinfo[0];
+    const uint64_t mask = (1ull << bits) - 1;
     const int32_t s = level_start[L], e = level_start[L + 1];
     for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
          b += (int64_t)gridDim.x * blockDim.x) {
@@ -62,7 +93,10 @@ __global__ void k_blockmap(LevelInfo li, int L, const int32_t *__restrict__ leve
         if (slot < 0) continue;
         const int4 c = reinterpret_cast<const int4 *>(coords)[b];
         if (!owns_row(li, c.y, c.z)) continue;
-        bmap[c.x + (int64_t)li.bins[0] * (c.y + (int64_t)li.bins[1] * c.z)] = slot;
+        const uint64_t key = (uint64_t)c.x + (uint64_t)li.bins[0] * ((uint64_t)c.y + (uint64_t)li.bins[1] * c.z);
+        const unsigned long long ent = (key << 24) | (uint64_t)slot;
+        for (uint64_t h = hash_slot0(key, bits);; h = (h + 1) & mask)
+            if (atomicCAS(&htab[h], kHashEmpty, ent) == kHashEmpty) break;
     }
 }
 
@@ -108,7 +142,8 @@ constexpr int kLinkWarps = 4;
 
 struct LinkCtx {
     const double *faces;
-    const int32_t *bmap;
+    const unsigned long long *htab;  // mapped finest blocks -> LUT slot (k_hash_insert)
+    const int32_t *hinfo;            // [0] log2 table size
     float *lengths;
     int4 *band;        // band candidates (face, slot, i | j<<16, k | r<<16)
     int32_t *n_band;   // [0] count (may exceed cap), [1] overflow flag
@@ -129,6 +164,18 @@ struct LinkCtx {
     uint32_t *ovf_bits;   // one bit per face: already listed
     unsigned long long *n_tests;  // lattice lines classified (FP32 intersection tests; roofline ops)
 };
+
+// LUT slot of the finest block holding lattice node (i, j, k); -1: not mapped
+__device__ __forceinline__ int32_t slot_at(const LinkCtx &c, int i, int j, int k) {
+    const int bits = c.hinfo[0];
+    const uint64_t mask = (1ull << bits) - 1;
+    const uint64_t key = (uint64_t)(i >> 2) + (uint64_t)c.bx * ((uint64_t)(j >> 2) + (uint64_t)c.by * (uint64_t)(k >> 2));
+    for (uint64_t h = hash_slot0(key, bits);; h = (h + 1) & mask) {
+        const unsigned long long e = __ldg(&c.htab[h]);
+        if (e == kHashEmpty) return -1;
+        if ((e >> 24) == key) return (int32_t)(e & 0xffffffu);
+    }
+}
 
 // add a per-thread count to the global test counter, one atomic per warp
 __device__ __forceinline__ void add_tests(const LinkCtx &c, unsigned long long n) {
@@ -347,7 +394,7 @@ __device__ __forceinline__ void link_line(const LinkCtx &c, const LinkDir &D, co
             link_slow<MODE>(c, D.f, -1, i, j, k, R);
             continue;
         }
-        const int32_t slot = c.bmap[(i >> 2) + (int64_t)c.bx * ((j >> 2) + (int64_t)c.by * (k >> 2))];
+        const int32_t slot = slot_at(c, i, j, k);
         if (slot < 0) continue;
         if (fast) link_fast(c, fv, R, D.den, i, j, k, slot);
         else link_slow<MODE>(c, D.f, slot, i, j, k, R);
@@ -760,6 +807,8 @@ __device__ __forceinline__ int small_pair(const LinkCtx &c, const SmallFace &S, 
     return (m2b - m2a + 1) * (m1b - m1a + 1);
 }
 
+__device__ __forceinline__ int4 qrec_convert(const LinkCtx &c, const int4 rec);
+
 __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
     k_links_small(LinkCtx c, int widen, int64_t F, float small_ext, int32_t *__restrict__ big,
                   int32_t *__restrict__ n_big) {
@@ -845,45 +894,239 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
     const int n = min(s_n, kLineStage);
     if (threadIdx.x == 0) s_base = n ? atomicAdd(c.n_lines, n) : 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) line_store(c, s_base + i, s_rec[i]);
+    // the staged lines leave as q-records: their faces were just read by
+    // this CTA (L1 / L2), so the exact q costs no extra DRAM pass
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        int4 r = s_rec[i];
+        if (s_base + i < c.line_cap) r = qrec_convert(c, r);
+        line_store(c, s_base + i, r);
+    }
 }
 
-// Resolve the recorded lines (fast class) once the grid and the block map
-// exist: thread per line, its (2, rarely 3) nodes -> block map -> the
-// oracle's FP64 num/den/d/q -> atomicMin.  Full warps, no setup.
+// The recorded lines (fast class) get their exact q values right after the
+// enumeration, still in phase 1 on the enumeration's side stream (the face
+// records are re-read while the latency-bound level pipeline leaves HBM
+// idle): k_links_q evaluates the oracle's FP64 num/den/d/q on the line's
+// (2, rarely 3) candidate nodes and rewrites the record in place as a
+// q-record -- base node, direction pair, and up to two accepted links
+// (node offset along c, direction sign, q).  Phase 2 (k_links_resolve) then
+// only maps nodes to LUT slots and min-merges q: no face access after the
+// tables.  A line with more than two accepted nodes (FP64 rounding at the
+// d = 0 / d = dx boundaries) sends its nodes to the band list instead.
+//   q-record: x = i | j << 15 (base node = the first accepted one),
+//             y = k | R << 15 | n << 19 | (o0 | s0 << 3) << 21 | (o1 | s1 << 3) << 25,
+//             z, w = q0, q1 bits  (o: node offset along c, s: 1 = the -c link)
+constexpr uint32_t kQRec = 1u << 31;  // y flag: the record is a q-record
+
+// raw line record -> q-record (see above)
+__device__ __forceinline__ int4 qrec_convert(const LinkCtx &c, const int4 rec) {
+    const int f = rec.x, R = rec.y & 15, cnt = (rec.y >> 5) & 7, ip_lo = (rec.y >> 8) & 0x7fff;
+    const int m1 = rec.z, m2 = rec.w;
+    const int cx = c27(2 * R + 1, 0), cy = c27(2 * R + 1, 1), cz = c27(2 * R + 1, 2);  // c_rep[R], per-thread R
+    const int p = cx != 0 ? 0 : (cy != 0 ? 1 : 2);
+    const int q1 = p == 0 ? 1 : 0, q2 = p == 2 ? 1 : 2;
+    const int cp = pick3(p, cx, cy, cz);
+    const int s1 = pick3(q1, cx, cy, cz) * cp, s2 = pick3(q2, cx, cy, cz) * cp;
+    const int n1 = pick3(q1, c.cells[0], c.cells[1], c.cells[2]);
+    const int n2 = pick3(q2, c.cells[0], c.cells[1], c.cells[2]);
+    const double2 *fp = reinterpret_cast<const double2 *>(c.faces + (int64_t)f * kFaceStride);
+    const double2 a0 = __ldg(fp), a1 = __ldg(fp + 1), a4 = __ldg(fp + 4), a5 = __ldg(fp + 5);
+    const double fv[6] = {a0.x, a0.y, a1.x, a4.y, a5.x, a5.y};  // v1, n
+    // exact c.n (link_dir_setup / link_candidate; nonzero: the pair passed EPS_PARALLEL)
+    const double den = VF_DADD(VF_DADD(cmul(cx, fv[3]), cmul(cy, fv[4])), cmul(cz, fv[5]));
+    const double dx = c.dx;
+    int ne = 0, bi = 0, bj = 0, bk = 0, ip0 = 0;
+    uint32_t code[2] = {0, 0};
+    float qv[2] = {0.0f, 0.0f};
+    for (int ip = ip_lo; ip <= ip_lo + cnt; ++ip) {
+        const int a = m1 + s1 * ip, b = m2 + s2 * ip;
+        if (a < 0 || a >= n1 || b < 0 || b >= n2) continue;
+        const int i = p == 0 ? ip : a;
+        const int j = p == 1 ? ip : (p == 0 ? a : b);
+        const int k = p == 2 ? ip : b;
+        // = link_fast: d, the (0, dx] range and q bit-identical to the oracle
+        const double d = VF_DDIV(plane_num(fv, fv + 3, node_c(i, dx), node_c(j, dx), node_c(k, dx)), den);
+        const bool pos = d > 0.0;
+        const double dd = pos ? d : -d;
+        if (!(dd > 0.0 && dd <= dx)) continue;
+        const double qd = c.pow2 ? VF_DMUL(dd, c.inv_dx) : VF_DDIV(dd, dx);
+        if (ne == 0) {  // base node: the first accepted one
+            bi = i; bj = j; bk = k; ip0 = ip;
+        }
+        if (ne < 2) {
+            code[ne] = (uint32_t)(ip - ip0) | ((pos ? 0u : 1u) << 3);
+            qv[ne] = __double2float_rn(qd);
+        }
+        ++ne;
+    }
+    if (ne > 2) {  // rounding at the range ends: node by node through the exact band path
+        for (int ip = ip_lo; ip <= ip_lo + cnt; ++ip) {
+            const int a = m1 + s1 * ip, b = m2 + s2 * ip;
+            if (a < 0 || a >= n1 || b < 0 || b >= n2) continue;
+            link_slow<2>(c, f, -1, p == 0 ? ip : a, p == 1 ? ip : (p == 0 ? a : b), p == 2 ? ip : b, R);
+        }
+        ne = 0;
+    }
+    return make_int4(bi | (bj << 15), (int)(kQRec | bk | (R << 15) | (ne << 19) | (code[0] << 21) | (code[1] << 25)),
+                     __float_as_int(qv[0]), __float_as_int(qv[1]));
+}
+
 #ifndef VF_RESOLVE_MINB
 #define VF_RESOLVE_MINB 4
 #endif
+// records the enumeration kernels did not convert themselves (stage overflow,
+// large faces)
 __global__ void __launch_bounds__(256, VF_RESOLVE_MINB)
-    k_links_resolve(LinkCtx c) {
+    k_links_q(LinkCtx c) {
     const int64_t n = min((int64_t)*c.n_lines, c.line_cap);
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int4 rec = c.lines[e];
-        const int f = rec.x, R = rec.y & 15, cnt = (rec.y >> 5) & 7, ip_lo = rec.y >> 8;
-        const int m1 = rec.z, m2 = rec.w;
-        const int cx = c27(2 * R + 1, 0), cy = c27(2 * R + 1, 1), cz = c27(2 * R + 1, 2);  // c_rep[R], per-thread R
-        const int p = cx != 0 ? 0 : (cy != 0 ? 1 : 2);
-        const int q1 = p == 0 ? 1 : 0, q2 = p == 2 ? 1 : 2;
-        const int cp = pick3(p, cx, cy, cz);
-        const int s1 = pick3(q1, cx, cy, cz) * cp, s2 = pick3(q2, cx, cy, cz) * cp;
-        const int n1 = pick3(q1, c.cells[0], c.cells[1], c.cells[2]);
-        const int n2 = pick3(q2, c.cells[0], c.cells[1], c.cells[2]);
-        const double2 *fp = reinterpret_cast<const double2 *>(c.faces + (int64_t)f * kFaceStride);
-        const double2 a0 = __ldg(fp), a1 = __ldg(fp + 1), a4 = __ldg(fp + 4), a5 = __ldg(fp + 5);
-        const double fv[6] = {a0.x, a0.y, a1.x, a4.y, a5.x, a5.y};  // v1, n
-        // exact c.n (link_dir_setup / link_candidate; nonzero: the pair passed EPS_PARALLEL)
-        const double den = VF_DADD(VF_DADD(cmul(cx, fv[3]), cmul(cy, fv[4])), cmul(cz, fv[5]));
-        for (int ip = ip_lo; ip <= ip_lo + cnt; ++ip) {
-            const int a = m1 + s1 * ip, b = m2 + s2 * ip;
-            if (a < 0 || a >= n1 || b < 0 || b >= n2) continue;
-            const int i = p == 0 ? ip : a;
-            const int j = p == 1 ? ip : (p == 0 ? a : b);
-            const int k = p == 2 ? ip : b;
-            const int32_t slot = c.bmap[(i >> 2) + (int64_t)c.bx * ((j >> 2) + (int64_t)c.by * (k >> 2))];
-            if (slot < 0) continue;
-            link_fast(c, fv, R, den, i, j, k, slot);
+        if (!((uint32_t)rec.y & kQRec)) c.lines[e] = qrec_convert(c, rec);
+    }
+}
+
+// The q-records' links reach the LUT without global atomics on it:
+//   phase 1, right after the enumeration (grid-independent, on the
+//   enumeration's side stream): (1) every link -> the key of its finest
+//   cell's PARENT block P (level L_max - 2 coordinates = node >> 3);
+//   per-parent link counts (warp-aggregated atomics), (2) scan over the
+//   parent keys (B_P^3 = B_L^3 / 8 counters), (3) scatter the links into
+//   parent order;
+//   phase 2, after the tables: ONE kernel, a warp per LUT slot (the
+//   contraction map's inverse): the slot's 27 x 64 lengths initialised to -1
+//   in shared memory, the links of its parent's bucket that fall in this
+//   block (octant) min-merged there (shared atomicMin on the IEEE bits:
+//   order-free, deterministic), the slot written once with 16-B stores.
+//   No separate -1 fill, no LUT sector read back, no block map or hash
+//   lookup per link.
+__device__ __forceinline__ void qrec_entry(const int4 rec, int k, int &i, int &j, int &kk, int &q, int &t) {
+    const int bi = rec.x & 0x7fff, bj = (rec.x >> 15) & 0x7fff, bk = rec.y & 0x7fff, R = (rec.y >> 15) & 15;
+    const uint32_t cd = ((uint32_t)rec.y >> (21 + 4 * k)) & 15u;
+    const int o = cd & 7;
+    i = bi + o * c27(2 * R + 1, 0);
+    j = bj + o * c27(2 * R + 1, 1);
+    kk = bk + o * c27(2 * R + 1, 2);
+    q = (cd >> 3) ? 2 * R + 2 : 2 * R + 1;
+    t = (i & 3) + 4 * (j & 3) + 16 * (kk & 3);
+}
+
+// (1) resolved link: its parent key (resu, -1: none) and octant << 41 |
+// (q 64 + t) << 30 | q bits (rese; q in (0, 1]: 30 bits).  Neighbouring
+// lines of a warp mostly share parents: one counter atomic per distinct
+// parent of the warp (__match_any_sync)
+__global__ void __launch_bounds__(256)
+    k_block_count(LinkCtx c, int3 pdim, int32_t *__restrict__ bcnt, int32_t *__restrict__ resu,
+                  unsigned long long *__restrict__ rese) {
+    const int64_t n = min((int64_t)*c.n_lines, c.line_cap);
+    const int lane = threadIdx.x & 31;
+    for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); e0 < n;
+         e0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = e0 + lane;
+        const int4 rec = e < n ? c.lines[e] : make_int4(0, 0, 0, 0);
+        const int ne = (rec.y >> 19) & 3;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            int i = 0, j = 0, kk = 0, q = 0, t = 0;
+            int32_t key = -1;
+            if (k < ne) {
+                qrec_entry(rec, k, i, j, kk, q, t);
+                key = (i >> 3) + pdim.x * ((j >> 3) + pdim.y * (kk >> 3));
+            }
+            const uint32_t grp = __match_any_sync(0xffffffffu, key);
+            if (key >= 0 && lane == __ffs(grp) - 1) atomicAdd(&bcnt[key], __popc(grp));
+            if (e < n) {
+                resu[2 * e + k] = key;
+                const int oct = ((i >> 2) & 1) + 2 * ((j >> 2) & 1) + 4 * ((kk >> 2) & 1);
+                rese[2 * e + k] = ((unsigned long long)oct << 41) | ((unsigned long long)(q * 64 + t) << 30) |
+                                  (uint32_t)(k ? rec.w : rec.z);
+            }
         }
+    }
+}
+
+// (3) links into parent order; four per thread in flight (the cursor
+// atomics' returns are the latency)
+__global__ void __launch_bounds__(256)
+    k_block_scatter(const int32_t *__restrict__ d_n_lines, int64_t line_cap,
+                    const int32_t *__restrict__ resu, const unsigned long long *__restrict__ rese,
+                    int32_t *__restrict__ bcur, unsigned long long *__restrict__ ent) {
+    const int64_t n = 2 * min((int64_t)*d_n_lines, line_cap);
+    const int lane = threadIdx.x & 31;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x * 4;
+    for (int64_t e0 = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * 4; e0 < n; e0 += step) {
+        unsigned long long x[4];
+        int32_t g[4], base[4];
+        uint32_t grp[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t e = e0 + 32 * u + lane;
+            g[u] = e < n ? resu[e] : -1;
+            x[u] = e < n ? rese[e] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            grp[u] = __match_any_sync(0xffffffffu, g[u]);
+            base[u] = 0;
+            if (g[u] >= 0 && lane == __ffs(grp[u]) - 1) base[u] = atomicAdd(&bcur[g[u]], __popc(grp[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int32_t bs = __shfl_sync(0xffffffffu, base[u], __ffs(grp[u]) - 1);
+            if (g[u] >= 0) ent[bs + __popc(grp[u] & ((1u << lane) - 1u))] = x[u];
+        }
+    }
+}
+
+struct LoadBlk {
+    const int32_t *p;
+    __device__ int operator()(int64_t i) const { return p[i]; }
+};
+struct EmitBlk {
+    int32_t *off, *cur;
+    __device__ void operator()(int64_t i, int, int ex) const {
+        off[i] = ex;
+        cur[i] = ex;
+    }
+};
+
+// phase 2: warp per LUT slot; N_b > cap latches VF_ECAPACITY with the count
+// (the LUT stays unwritten), as the -1 fill did
+constexpr int kLutWarps = 6;  // 6 x 6912 B of static shared memory
+__global__ void __launch_bounds__(kLutWarps * 32)
+    k_lut_blocks(int3 pdim, const int32_t *__restrict__ coords, const int32_t *__restrict__ inv,
+                 const int32_t *__restrict__ d_n_b, int64_t cap, const int32_t *__restrict__ boff,
+                 const int32_t *__restrict__ bcnt, const unsigned long long *__restrict__ ent,
+                 float *__restrict__ lengths, int32_t *__restrict__ status) {
+    __shared__ __align__(16) uint32_t s_lut[kLutWarps][27 * 64];
+    const int64_t nb = *d_n_b;
+    if (nb > cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            atomicMax(status, VF_ECAPACITY);
+            status[2] = (int32_t)nb;
+        }
+        return;
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t *S = s_lut[w];
+    uint4 *S4 = reinterpret_cast<uint4 *>(S);
+    for (int64_t slot = (int64_t)blockIdx.x * kLutWarps + w; slot < nb; slot += (int64_t)gridDim.x * kLutWarps) {
+        const int4 co = reinterpret_cast<const int4 *>(coords)[inv[slot]];
+        const int32_t key = (co.x >> 1) + pdim.x * ((co.y >> 1) + pdim.y * (co.z >> 1));
+        const uint32_t oct = (uint32_t)((co.x & 1) + 2 * (co.y & 1) + 4 * (co.z & 1));
+        const int32_t e0 = boff[key], ne = bcnt[key];
+        for (int i = lane; i < 27 * 64 / 4; i += 32)
+            S4[i] = make_uint4(0xBF800000u, 0xBF800000u, 0xBF800000u, 0xBF800000u);  // -1.0f
+        __syncwarp();
+        for (int i = lane; i < ne; i += 32) {
+            const unsigned long long x = ent[e0 + i];
+            // the parent's links in this block; q > 0: uint order is float order, below -1's bits
+            if ((uint32_t)(x >> 41) == oct) atomicMin(&S[(uint32_t)(x >> 30) & 0x7ffu], (uint32_t)x & 0x3fffffffu);
+        }
+        __syncwarp();
+        uint4 *dst = reinterpret_cast<uint4 *>(lengths + slot * (27 * 64));
+        for (int i = lane; i < 27 * 64 / 4; i += 32) dst[i] = S4[i];
+        __syncwarp();
     }
 }
 
@@ -898,7 +1141,7 @@ __global__ void __launch_bounds__(256)
         const int i = x.z & 0xffff, j = x.z >> 16, k = x.w & 0xffff;
         int32_t slot = x.y;
         if (slot < 0) {  // queued by the line enumeration before the block map existed
-            slot = c.bmap[(i >> 2) + (int64_t)c.bx * ((j >> 2) + (int64_t)c.by * (k >> 2))];
+            slot = slot_at(c, i, j, k);
             if (slot < 0) continue;
         }
         link_candidate(c.faces, x.x, x.w >> 16, i, j, k, c.dx, c.eps, c.eps_par, slot, c.lengths);
@@ -909,13 +1152,16 @@ __global__ void __launch_bounds__(256)
 constexpr int64_t kBandCap = 1 << 20;  // 16 MB; overflow only costs the fallback pass
 static int64_t g_band_cap = kBandCap;    // vf_set_link_band_cap (test hook)
 
-static size_t bmap_bytes(const vf_config &cfg, int finest) {
-    const int64_t nb = (int64_t)(cfg.nb[0] << finest) * (cfg.nb[1] << finest) * (cfg.nb[2] << finest);
-    return ((size_t)nb * sizeof(int32_t) + 255) & ~(size_t)255;
+// workspace: band counters | slot hash size | band list | slot hash (pow2 >=
+// 2 x the grid capacity entries: N_b <= the finest-level blocks <= capacity)
+static size_t hash_entries(int32_t capacity) {
+    size_t n = 1024;
+    while (n < 4 * (size_t)capacity) n <<= 1;
+    return n;
 }
 
-size_t link_workspace_size(const vf_config &cfg, int finest) {
-    return bmap_bytes(cfg, finest) + 256 + (size_t)kBandCap * sizeof(int4);
+size_t link_workspace_size(const vf_config &, int, int32_t capacity) {
+    return 512 + (size_t)kBandCap * sizeof(int4) + hash_entries(capacity) * sizeof(unsigned long long);
 }
 
 // LUT initialisation to -1 for the device-resident N_b slots (graph-safe:
@@ -950,10 +1196,11 @@ static int make_link_ctx(const vf_config &cfg, int L, const double *faces, float
         return set_error(VF_EARG, "link lengths: > 32767 cells per axis");
     memset(&c, 0, sizeof(c));
     c.faces = faces;
-    c.bmap = (int32_t *)ws;
     c.lengths = lengths;
-    c.n_band = (int32_t *)((char *)ws + bmap_bytes(cfg, L));
-    c.band = (int4 *)((char *)c.n_band + 256);
+    c.n_band = (int32_t *)ws;
+    c.hinfo = (int32_t *)((char *)ws + 256);
+    c.band = (int4 *)((char *)ws + 512);
+    c.htab = (const unsigned long long *)((char *)ws + 512 + (size_t)kBandCap * sizeof(int4));
     c.band_cap = g_band_cap;
     c.dx = li.dx;
     c.eps = li.eps;
@@ -987,15 +1234,16 @@ static int link_grid(int64_t F) {
     return grid < 1 ? 1 : (int)grid;
 }
 
-// the block map of the finest level (LUT slots of mapped blocks)
+// the slot hash of the finest level's mapped blocks
 static int link_blockmap(vf_grid *g, const LevelInfo &li, const int32_t *cmap, const LinkCtx &c,
                          const int32_t *d_n_b, int64_t lengths_cap, cudaStream_t st) {
-    const int L = li.level;
-    const int64_t nb = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
-    cudaMemsetAsync(const_cast<int32_t *>(c.bmap), 0xff, sizeof(int32_t) * (size_t)nb, st);
-    kt_point("memset:block_map");
-    k_blockmap<<<max_ctas(8), 256, 0, st>>>(li, L, g->d_level_start, g->d_coords, cmap,
-                                            const_cast<int32_t *>(c.bmap), d_n_b, lengths_cap);
+    unsigned long long *htab = const_cast<unsigned long long *>(c.htab);
+    int32_t *hinfo = const_cast<int32_t *>(c.hinfo);
+    k_hash_clear<<<max_ctas(4), 256, 0, st>>>(d_n_b, g->capacity, hinfo, htab);
+    int rc = check_launch("k_hash_clear");
+    if (rc) return rc;
+    k_hash_insert<<<max_ctas(8), 256, 0, st>>>(li, li.level, g->d_level_start, g->d_coords, cmap, hinfo, htab,
+                                               d_n_b, lengths_cap);
     return check_launch("k_blockmap");
 }
 
@@ -1004,7 +1252,7 @@ int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const doubl
               size_t ws_bytes, cudaStream_t st, void **events, const int32_t *d_n_b,
               int64_t lengths_cap) {
     const int L = g->n_levels - 1;
-    if (ws_bytes < link_workspace_size(cfg, L)) return set_error(VF_EARG, "link workspace too small");
+    if (ws_bytes < link_workspace_size(cfg, L, g->capacity)) return set_error(VF_EARG, "link workspace too small");
     LinkCtx c;
     int widen;
     LevelInfo li;
@@ -1030,26 +1278,67 @@ int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const doubl
 // lines workspace: counters (n_lines, n_ovf, n_big) | lines | overflow face
 // list | overflow bits | big-face list (the warp-flattened enumeration)
 static size_t list_bytes(int64_t F) { return (((size_t)(F + 1) * sizeof(int32_t) + 255) & ~(size_t)255); }
-
-size_t link_lines_bytes(int64_t F) {
-    const int64_t cap = F * 2 > (1 << 22) ? F * 2 : (1 << 22);
-    return 256 + (size_t)cap * sizeof(int4) + 2 * list_bytes(F) +
-           ((((size_t)F + 32) / 32 * sizeof(uint32_t) + 255) & ~(size_t)255);
+static int64_t line_cap_of(int64_t F) { return F * 2 > (1 << 22) ? F * 2 : (1 << 22); }
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+// parent buckets: level L_max - 2 coordinates of the finest level (B_L^3 / 8)
+static int3 parent_dims(const vf_config &cfg) {
+    const int Lf = cfg.l_max - 1;
+    return make_int3((cfg.nb[0] << Lf) / 2, (cfg.nb[1] << Lf) / 2, (cfg.nb[2] << Lf) / 2);
+}
+static int64_t parents_of(const vf_config &cfg) {
+    const int3 p = parent_dims(cfg);
+    return (int64_t)p.x * p.y * p.z + 1;
 }
 
-static int32_t *line_bufs(LinkCtx &c, int64_t F, void *lines_ws) {
-    c.line_cap = F * 2 > (1 << 22) ? F * 2 : (1 << 22);
+// ... | parent counts | parent offsets | parent cursors | slot -> block | scan |
+// parent-ordered links | resolved links (<= 2 links per q-record each)
+size_t link_lines_bytes(const vf_config &cfg, int64_t F, int32_t capacity) {
+    const int64_t cap = line_cap_of(F), nt = parents_of(cfg);
+    return 256 + (size_t)cap * sizeof(int4) + 2 * list_bytes(F) +
+           al256(((size_t)F + 32) / 32 * sizeof(uint32_t)) + 3 * al256((size_t)nt * sizeof(int32_t)) +
+           al256((size_t)capacity * sizeof(int32_t)) +
+           al256(scan_workspace_bytes(nt)) + (size_t)(2 * cap) * (2 * sizeof(unsigned long long) + sizeof(int32_t));
+}
+
+struct BlockLinkBufs {
+    int32_t *bcnt, *boff, *bcur, *inv;  // per parent bucket: links, first, cursor; slot -> block
+    void *scan_ws;
+    unsigned long long *ent, *rese;  // block-ordered links; resolved links in record order
+    int32_t *resu;                   // finest block of each resolved link
+    int64_t n_max;
+};
+
+static int32_t *line_bufs(LinkCtx &c, int64_t F, void *lines_ws, const vf_config *cfg = nullptr, int32_t capacity = 0,
+                          BlockLinkBufs *tb = nullptr) {
+    c.line_cap = line_cap_of(F);
     c.n_lines = (int32_t *)lines_ws;
     c.n_ovf = c.n_lines + 1;
     c.n_tests = (unsigned long long *)((char *)lines_ws + 16);
     c.lines = (int4 *)((char *)lines_ws + 256);
     c.ovf_list = (int32_t *)((char *)c.lines + (size_t)c.line_cap * sizeof(int4));
     c.ovf_bits = (uint32_t *)((char *)c.ovf_list + list_bytes(F));
-    return (int32_t *)((char *)c.ovf_bits + ((((size_t)F + 32) / 32 * sizeof(uint32_t) + 255) & ~(size_t)255));
+    int32_t *big = (int32_t *)((char *)c.ovf_bits + al256(((size_t)F + 32) / 32 * sizeof(uint32_t)));
+    if (tb) {
+        const int64_t nt = parents_of(*cfg);
+        char *p = (char *)big + list_bytes(F);
+        tb->n_max = nt;
+        tb->bcnt = (int32_t *)p;
+        tb->boff = (int32_t *)(p + al256((size_t)nt * sizeof(int32_t)));
+        tb->bcur = (int32_t *)(p + 2 * al256((size_t)nt * sizeof(int32_t)));
+        tb->inv = (int32_t *)(p + 3 * al256((size_t)nt * sizeof(int32_t)));
+        tb->scan_ws = p + 3 * al256((size_t)nt * sizeof(int32_t)) + al256((size_t)capacity * sizeof(int32_t));
+        tb->ent = (unsigned long long *)((char *)tb->scan_ws + al256(scan_workspace_bytes(nt)));
+        tb->rese = tb->ent + 2 * c.line_cap;
+        tb->resu = (int32_t *)(tb->rese + 2 * c.line_cap);
+    }
+    return big;
 }
 
+static int link_bucket(const vf_config &cfg, LinkCtx &c, int64_t F, void *lines_ws, int32_t capacity,
+                       cudaStream_t st);
+
 int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *ws, void *lines_ws,
-                   cudaStream_t st, void **events) {
+                   int32_t capacity, cudaStream_t st, void **events) {
     LinkCtx c;
     int widen;
     LevelInfo li;
@@ -1072,7 +1361,11 @@ int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *w
     int64_t g2 = (F + 32 * kLinkWarps - 1) / (32 * kLinkWarps);
     if (g2 > 4 * (int64_t)max_ctas(VF_LINK_MINB)) g2 = 4 * (int64_t)max_ctas(VF_LINK_MINB);
     k_links<2><<<(unsigned)(g2 < 1 ? 1 : g2), kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, big, n_big);
-    rc = check_launch("k_links_enum");
+    if ((rc = check_launch("k_links_enum"))) return rc;
+    // exact q of the recorded lines (records rewritten in place as q-records)
+    k_links_q<<<max_ctas(VF_GRID_RESOLVE), 256, 0, st>>>(c);
+    if ((rc = check_launch("k_links_q"))) return rc;
+    rc = link_bucket(cfg, c, F, lines_ws, capacity, st);
     if (events) cudaEventRecord((cudaEvent_t)events[1], st);
     return rc;
 }
@@ -1106,20 +1399,50 @@ int link_stats(const vf_config &cfg, int64_t F, void *ws, void *lines_ws, int64_
     return VF_OK;
 }
 
+// phase 1, right after the enumeration: the links of the q-records bucketed
+// by finest-level parent key (see k_lut_blocks)
+static int link_bucket(const vf_config &cfg, LinkCtx &c, int64_t F, void *lines_ws, int32_t capacity,
+                       cudaStream_t st) {
+    BlockLinkBufs tb;
+    line_bufs(c, F, lines_ws, &cfg, capacity, &tb);
+    cudaMemsetAsync(tb.bcnt, 0, sizeof(int32_t) * (size_t)tb.n_max, st);
+    kt_point("memset:parent_counts");
+    k_block_count<<<max_ctas(8), 256, 0, st>>>(c, parent_dims(cfg), tb.bcnt, tb.resu, tb.rese);
+    int rc = check_launch("k_block_count");
+    if (rc) return rc;
+    cudaError_t e = scan_launch(LoadBlk{tb.bcnt}, EmitBlk{tb.boff, tb.bcur}, tb.n_max, nullptr, nullptr, tb.scan_ws, st);
+    kt_point("scan_kernel");
+    if (e != cudaSuccess) return set_cuda_error(e, "parent link scan");
+    k_block_scatter<<<max_ctas(8), 256, 0, st>>>(c.n_lines, c.line_cap, tb.resu, tb.rese, tb.bcur, tb.ent);
+    return check_launch("k_block_scatter");
+}
+
+// the slot -> block inverse of the contraction map lives in the lines workspace
+int32_t *link_slot_inverse(const vf_config &cfg, int64_t F, void *lines_ws, int32_t capacity) {
+    LinkCtx c;
+    memset(&c, 0, sizeof(c));
+    BlockLinkBufs tb;
+    line_bufs(c, F, lines_ws, &cfg, capacity, &tb);
+    return tb.inv;
+}
+
 int link_resolve_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
                       int64_t F, float *lengths, void *ws, void *lines_ws, cudaStream_t st,
-                      void **events, const int32_t *d_n_b, int64_t lengths_cap) {
+                      void **events, const int32_t *d_n_b, int64_t lengths_cap, const int32_t *inv) {
     LinkCtx c;
     int widen;
     LevelInfo li;
     if (g->n_levels != cfg.l_max) return set_error(VF_EARG, "link resolve: the grid must reach L_max");
     int rc = make_link_ctx(cfg, cfg.l_max - 1, faces, lengths, ws, c, widen, li);
     if (rc) return rc;
-    line_bufs(c, F, lines_ws);
+    BlockLinkBufs tb;
+    line_bufs(c, F, lines_ws, &cfg, g->capacity, &tb);
+    // slot hash for the rare paths (overflowed faces, band candidates)
     if ((rc = link_blockmap(g, li, cmap, c, d_n_b, lengths_cap, st))) return rc;
     if (events && events[0]) cudaEventRecord((cudaEvent_t)events[0], st);
-    k_links_resolve<<<max_ctas(VF_GRID_RESOLVE), 256, 0, st>>>(c);
-    if ((rc = check_launch("k_links_resolve"))) return rc;
+    k_lut_blocks<<<max_ctas(5), kLutWarps * 32, 0, st>>>(parent_dims(cfg), g->d_coords, inv ? inv : tb.inv, d_n_b,
+                                                         lengths_cap, tb.boff, tb.bcnt, tb.ent, lengths, g->d_status);
+    if ((rc = check_launch("k_lut_blocks"))) return rc;
     // faces whose lines overflowed the record buffer: the direct kernel
     k_links<0><<<link_grid(F), kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, c.ovf_list, c.n_ovf);
     if ((rc = check_launch("k_links_ovf"))) return rc;

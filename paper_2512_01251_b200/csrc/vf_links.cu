@@ -134,8 +134,11 @@ struct EmitCmap {
     const int32_t *level_start;
     int L;
     int32_t *cmap;
+    int32_t *inv;  // nullable: slot -> block
     __device__ void operator()(int64_t i, int v, int ex) const {
-        cmap[level_start[L] + i] = v ? ex : -1;
+        const int32_t b = level_start[L] + (int32_t)i;
+        cmap[b] = v ? ex : -1;
+        if (v && inv) inv[ex] = b;
     }
 };
 
@@ -144,7 +147,7 @@ size_t tables_workspace_size(int32_t capacity) {
 }
 
 int tables_impl(vf_grid *g, const int32_t *bcount, int32_t *cmap, int32_t *d_n_b, void *ws,
-                size_t ws_bytes, cudaStream_t st) {
+                size_t ws_bytes, cudaStream_t st, int32_t *inv) {
     if (ws_bytes < tables_workspace_size(g->capacity)) return set_error(VF_EARG, "tables workspace too small");
     const int L = g->n_levels - 1;
     int32_t *scal = (int32_t *)ws;
@@ -153,7 +156,7 @@ int tables_impl(vf_grid *g, const int32_t *bcount, int32_t *cmap, int32_t *d_n_b
     cudaMemsetAsync(cmap, 0xff, sizeof(int32_t) * (size_t)g->capacity, st);
     kt_point("memset:cmap");
     (void)scal;
-    cudaError_t ce = scan_launch_fn(LoadBnd{g->d_level_start, L, bcount}, EmitCmap{g->d_level_start, L, cmap},
+    cudaError_t ce = scan_launch_fn(LoadBnd{g->d_level_start, L, bcount}, EmitCmap{g->d_level_start, L, cmap, inv},
                                     g->capacity, ScanLevelN{g->d_level_start, L}, d_n_b, scan_ws, st);
     return ce == cudaSuccess ? VF_OK : set_cuda_error(ce, "tables scan");
 }

@@ -35,9 +35,10 @@ namespace vf {
 // Per pair: the x-rows of the block whose centre (y, z) lies within eps of the
 // face's y / z extent (the SAT's exact box-axis comparisons), then the FP32
 // row classifier (exact SAT in its undecided band); per hit row the 4 cell
-// distances d = ((v1 - x) . n) / n_x (A7 association).  The A7 minimum per
-// cell -- |d|, ties to the lowest face id -- is reduced in shared memory in
-// rounds of one hit row per thread:
+// distances d = ((v1 - x) . n) / n_x (A7 association).  The chunk's (pair,
+// hit row) items are compacted, and the A7 minimum per cell -- |d|, ties to
+// the lowest face id -- is reduced in shared memory in rounds of one item
+// (4 cells) per thread:
 //   (1) every candidate notes the cell's best |d| before the round,
 //   (2) 64-bit atomicMin of |d| (IEEE bits of a non-negative double are
 //       ordered as the values),
@@ -58,12 +59,21 @@ struct VoxGroup {
     int32_t base[kVoxG];                // first face_ids slot of each block
     int32_t bid[kVoxG];                 // block id (-1: past the list)
     int4 co[kVoxG];                     // block coordinates
+    uint4 m[kVoxG][4];                  // the blocks' cell masks (loaded with the header)
+    // one chunk of pairs: face v1 / n, id and block of each pair, the
+    // (pair, hit row) items
+    double pv[kVoxT][6];
+    int32_t pfid[kVoxT];
+    int16_t pw[kVoxT];
+    uint16_t item[kVoxT * 16];
+    int wsum[kVoxT / 32];
+    int n_item;
 };
 
 constexpr unsigned long long kInf64 = 0x7ff0000000000000ull;
 
 #ifndef VF_VOX_MINB
-#define VF_VOX_MINB 4
+#define VF_VOX_MINB 5
 #endif
 __global__ void __launch_bounds__(kVoxT, VF_VOX_MINB)
     k_voxelize(LevelInfo li, int L, const int32_t *__restrict__ level_start,
@@ -87,6 +97,9 @@ __global__ void __launch_bounds__(kVoxT, VF_VOX_MINB)
                 c = cnt[u];
                 bs = base[u];
                 S.co[t] = reinterpret_cast<const int4 *>(coords)[s + u];
+                const uint4 *mp = reinterpret_cast<const uint4 *>(masks + 64 * (int64_t)(s + u));
+#pragma unroll
+                for (int q = 0; q < 4; ++q) S.m[t][q] = mp[q];
                 if (zero_cnt) cnt[u] = 0;  // the next level's histogram starts from zero
             }
             int inc = c;
@@ -149,22 +162,48 @@ __global__ void __launch_bounds__(kVoxT, VF_VOX_MINB)
                     }
                 }
             }
-            // rounds of one hit row per thread (A7 reduction, see above)
-            while (__syncthreads_or(hm != 0)) {
-                const bool has = hm != 0;
-                int slot0 = 0;
+            // the chunk's (pair, hit row) items, compacted in pair order
+            {
+                const int c = __popc(hm);
+                int inc = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if ((t & 31) >= o) inc += y;
+                }
+                if ((t & 31) == 31) S.wsum[t >> 5] = inc;
+                S.pv[t][0] = v1[0]; S.pv[t][1] = v1[1]; S.pv[t][2] = v1[2];
+                S.pv[t][3] = nn[0]; S.pv[t][4] = nn[1]; S.pv[t][5] = nn[2];
+                S.pfid[t] = fid;
+                S.pw[t] = (int16_t)w;
+                __syncthreads();
+                int pos = inc - c;
+                for (int k = 0; k < (t >> 5); ++k) pos += S.wsum[k];
+                for (uint32_t m = hm; m; m &= m - 1) S.item[pos++] = (uint16_t)(t | ((__ffs(m) - 1) << 8));
+                if (t == kVoxT - 1) S.n_item = pos;
+                __syncthreads();
+            }
+            // rounds of one item per thread (the A7 reduction, see above)
+            const int n_item = S.n_item;
+            for (int i0 = 0; i0 < n_item; i0 += kVoxT) {
+                const bool has = i0 + t < n_item;
+                int slot0 = 0, ifid = 0;
                 unsigned long long db[4] = {kInf64, kInf64, kInf64, kInf64}, old[4];
                 bool solid[4] = {false, false, false, false};
                 if (has) {
-                    const int r = __ffs(hm) - 1;
-                    hm &= hm - 1;
-                    const double y = node_c(4 * co.y + (r & 3), dx), z = node_c(4 * co.z + (r >> 2), dx);
-                    slot0 = w * 64 + 4 * r;
+                    const uint32_t it = S.item[i0 + t];
+                    const int pl = it & 0xff, r = it >> 8, iw = S.pw[pl];
+                    const int4 ico = S.co[iw];
+                    const double pv1[3] = {S.pv[pl][0], S.pv[pl][1], S.pv[pl][2]};
+                    const double pn[3] = {S.pv[pl][3], S.pv[pl][4], S.pv[pl][5]};
+                    ifid = S.pfid[pl];
+                    const double y = node_c(4 * ico.y + (r & 3), dx), z = node_c(4 * ico.z + (r >> 2), dx);
+                    slot0 = iw * 64 + 4 * r;
 #pragma unroll
                     for (int I = 0; I < 4; ++I) {
-                        const double d = VF_DDIV(plane_num(v1, nn, node_c(4 * co.x + I, dx), y, z), nn[0]);
+                        const double d = VF_DDIV(plane_num(pv1, pn, node_c(4 * ico.x + I, dx), y, z), pn[0]);
                         db[I] = (unsigned long long)__double_as_longlong(fabs(d));
-                        solid[I] = VF_DMUL(nn[0], d) > 0.0;
+                        solid[I] = VF_DMUL(pn[0], d) > 0.0;
                         old[I] = S.bd[slot0 + I];
                     }
                 }
@@ -184,11 +223,12 @@ __global__ void __launch_bounds__(kVoxT, VF_VOX_MINB)
                 __syncthreads();
 #pragma unroll
                 for (int I = 0; I < 4; ++I)
-                    if (best[I]) atomicMin(&S.bfid[slot0 + I], fid);
+                    if (best[I]) atomicMin(&S.bfid[slot0 + I], ifid);
                 __syncthreads();
 #pragma unroll
                 for (int I = 0; I < 4; ++I)
-                    if (best[I] && S.bfid[slot0 + I] == fid) S.bval[slot0 + I] = solid[I] ? VF_SOLID : VF_GUARD;
+                    if (best[I] && S.bfid[slot0 + I] == ifid) S.bval[slot0 + I] = solid[I] ? VF_SOLID : VF_GUARD;
+                __syncthreads();
             }
         }
         __syncthreads();
@@ -205,8 +245,7 @@ __global__ void __launch_bounds__(kVoxT, VF_VOX_MINB)
                     bh |= (uint32_t)S.bval[w * 64 + 4 * r + I] << (8 * I);
                 }
             if (!hit) continue;
-            uint32_t *wp = masks32 + (int64_t)b * 16 + r;
-            const uint32_t orig = *wp;
+            const uint32_t orig = reinterpret_cast<const uint32_t *>(&S.m[w][0])[r];
             uint32_t out = orig;
 #pragma unroll
             for (int I = 0; I < 4; ++I) {
@@ -215,7 +254,7 @@ __global__ void __launch_bounds__(kVoxT, VF_VOX_MINB)
                 if (hn == VF_SOLID || (o != VF_GHOST && o != VF_INTERFACE))
                     out = (out & ~(0xffu << (8 * I))) | (hn << (8 * I));
             }
-            if (out != orig) *wp = out;
+            if (out != orig) masks32[(int64_t)b * 16 + r] = out;
         }
         __syncthreads();
     }
