@@ -361,7 +361,6 @@ float vf_set_link_small_ext(float e);
 /* Test hook: 1 = Alg. 5 rows through the chunked kernel at every level,
  * 0 = the shared-memory staged kernel for rows of <= 128 blocks (default;
  * results identical).  Returns the old value; on < 0 only queries. */
-int vf_set_xrows_chunked(int on);
 
 #ifdef __cplusplus
 }

@@ -102,7 +102,6 @@ _SIGS = {
     "vf_set_link_band_cap": (_I64, [_I64]),
     "vf_set_serial_links": (_I32, [_I32]),
     "vf_set_link_small_ext": (C.c_float, [C.c_float]),
-    "vf_set_xrows_chunked": (_I32, [_I32]),
     "vf_shard_owner_bytes": (_SZ, [_CP]),
     "vf_shard_owner_map": (_I32, [_CP, _GP, _I32, _P, _SZ, _P]),
     "vf_shard_level": (_I32, [_CP, _P, _I64, _I32, _GP, _I32, _P, _SZ, _P]),

@@ -209,6 +209,9 @@ static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *b
     EmbedWs t;
     memset(&t, 0, sizeof(t));
     t.pair_cap = pair_cap_of(cfg, F);
+    // (capacity-only items first: the sharded calls lay out with F = 1)
+    t.prop_b = rows_workspace_size(cap);
+    t.prop_ws = take(t.prop_b);
     for (int k = 0; k < 2; ++k) {
         t.pairs[k] = (int2 *)take(sizeof(int2) * (size_t)(t.pair_cap + 1));
         t.n_pairs[k] = (int32_t *)take(64);
@@ -220,8 +223,6 @@ static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *b
     t.ind8 = (uint8_t *)take((size_t)F + 1);
     t.bins_ws_bytes = scan_workspace_bytes(F + 1);
     t.bins_ws = take(t.bins_ws_bytes);
-    t.prop_b = propagate_level_workspace_size(cfg, Lf);
-    t.prop_ws = take(t.prop_b);
     t.mark_b = mark_workspace_size(cap);
     t.mark_ws = take(t.mark_b);
     t.adapt_b = adapt_workspace_size(cap);
@@ -457,6 +458,8 @@ static void rec(void **ev, int n_ev, int *k, cudaStream_t st) {
 // first use; the embed is single-threaded per device, see the header)
 struct SideStream {
     cudaStream_t st = nullptr, st3 = nullptr;  // bins pipeline, link line enumeration
+    cudaStream_t st4 = nullptr;                // next level's sparse row order
+    cudaEvent_t adapted = nullptr, rowsok = nullptr;
     cudaEvent_t fork = nullptr, bins[2] = {nullptr, nullptr}, vox[2] = {nullptr, nullptr}, join = nullptr;
     cudaEvent_t join3 = nullptr;
 };
@@ -474,7 +477,8 @@ static int side_stream(SideStream **out) {
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         e = cudaStreamCreateWithPriority(&s.st, cudaStreamNonBlocking, hi);
         if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&s.st3, cudaStreamNonBlocking, lo);
-        cudaEvent_t *evs[] = {&s.fork, &s.bins[0], &s.bins[1], &s.vox[0], &s.vox[1], &s.join, &s.join3};
+        if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&s.st4, cudaStreamNonBlocking, hi);
+        cudaEvent_t *evs[] = {&s.fork, &s.bins[0], &s.bins[1], &s.vox[0], &s.vox[1], &s.join, &s.join3, &s.adapted, &s.rowsok};
         for (cudaEvent_t *ev : evs)
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
         if (e != cudaSuccess) return set_cuda_error(e, "side stream");
@@ -518,11 +522,13 @@ extern "C" int vf_ctx_destroy(void *ctx) {
     if (s.st) {
         e = cudaStreamSynchronize(s.st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s.st3);
-        cudaEvent_t evs[] = {s.fork, s.bins[0], s.bins[1], s.vox[0], s.vox[1], s.join, s.join3};
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s.st4);
+        cudaEvent_t evs[] = {s.fork, s.bins[0], s.bins[1], s.vox[0], s.vox[1], s.join, s.join3, s.adapted, s.rowsok};
         for (cudaEvent_t ev : evs)
             if (ev) cudaEventDestroy(ev);
         cudaStreamDestroy(s.st);
         cudaStreamDestroy(s.st3);
+        cudaStreamDestroy(s.st4);
         s = SideStream();
     }
     cudaSetDevice(cur);
@@ -540,6 +546,7 @@ extern "C" int vf_side_sync(void) {
     VF_TRY(side_stream(&side));
     cudaError_t e = cudaStreamSynchronize(side->st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(side->st3);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(side->st4);
     return e == cudaSuccess ? VF_OK : set_cuda_error(e, "vf_side_sync");
 }
 
@@ -572,6 +579,7 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     int k = 0;
     rec(events, n_ev, &k, st);  // 0: start
     VF_TRY(init_forest_impl(*cfg, g, st));
+    VF_TRY(rows_init_impl(*cfg, g, w.prop_ws, st));
     // fork the bins pipeline (after init: it shares the status word) and the
     // grid-independent cut-link line enumeration of the finest level (joined
     // in phase 2, where the recorded lines are resolved)
@@ -609,11 +617,18 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
         VF_TRY(block_bins_impl(li, L, g, w.pairs[L & 1], w.n_pairs[L & 1], w.pair_cap, w.bb, st));
         cudaEventRecord(side->vox[L & 1], st);
         VF_TRY(voxelize_blocks_impl(li, g, L, w.bb, faces, true, st));
-        VF_TRY(propagate_level_impl(li, g, L, w.prop_ws, w.prop_b, st));
+        if (L > 0) cudaStreamWaitEvent(st, side->rowsok, 0);  // level L's row order
+        VF_TRY(propagate_rows_impl(li, g, L, w.prop_ws, st));
         rec(events, n_ev, &k, st);  // voxelization done
         if (L == cfg->l_max - 1) break;
         VF_TRY(mark_impl(*cfg, g, L, w.mark_ws, w.mark_b, st));
         VF_TRY(adapt_impl(*cfg, g, L, w.adapt_ws, w.adapt_b, st));
+        // level L+1's row order beside its bins and voxelization
+        cudaStream_t s4 = one ? st : side->st4;
+        cudaEventRecord(side->adapted, st);
+        cudaStreamWaitEvent(s4, side->adapted, 0);
+        VF_TRY(rows_next_impl(g, L, w.prop_ws, s4));
+        cudaEventRecord(side->rowsok, s4);
         rec(events, n_ev, &k, st);  // refinement done
     }
     // join the side stream (required to end a capture; bins are all consumed)
@@ -755,6 +770,8 @@ int vf_shard_owner_map(const vf_config *cfg, vf_grid *g, int level, void *ws, si
     // the owner map only needs the shard scratch; F = 1 sizes the layout
     if (!shard_args(cfg, g, ws, ws_bytes, 1, &w) || level < 0 || level >= cfg->l_max)
         return set_error(VF_EARG, "vf_shard_owner_map: bad argument");
+    // level 0 also starts the sparse row order (the root grid)
+    if (level == 0) VF_TRY(rows_init_impl(*cfg, g, w.prop_ws, (cudaStream_t)stream));
     return shard_owner_map_impl(*cfg, g, level, w.shard_ws, (cudaStream_t)stream);
 }
 
@@ -773,7 +790,7 @@ int vf_shard_level(const vf_config *cfg, const double *faces, int64_t F, int use
     VF_TRY(level_pairs(*cfg, li, faces, F, use_filter, false, w, 0, g->d_status, st));
     VF_TRY(block_bins_impl(li, L, g, w.pairs[0], w.n_pairs[0], w.pair_cap, w.bb, st));
     VF_TRY(voxelize_blocks_impl(li, g, L, w.bb, faces, true, st));
-    VF_TRY(propagate_level_impl(li, g, L, w.prop_ws, w.prop_b, st));
+    VF_TRY(propagate_rows_impl(li, g, L, w.prop_ws, st));
     return shard_zero_impl(li, g, L, nullptr, st);
 }
 
@@ -785,6 +802,7 @@ int vf_shard_refine(const vf_config *cfg, vf_grid *g, int L, void *ws, size_t ws
     cudaStream_t st = (cudaStream_t)stream;
     VF_TRY(mark_impl(*cfg, g, L, w.mark_ws, w.mark_b, st));
     VF_TRY(adapt_impl(*cfg, g, L, w.adapt_ws, w.adapt_b, st));
+    VF_TRY(rows_next_impl(g, L, w.prop_ws, st));
     return shard_owner_map_impl(*cfg, g, L + 1, w.shard_ws, st);
 }
 

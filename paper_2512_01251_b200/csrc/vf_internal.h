@@ -118,11 +118,13 @@ size_t propagate_workspace_size(int32_t capacity);
 int propagate_impl(const LevelInfo &li, vf_grid *g, int L, int dir, int finalize, void *ws,
                    size_t ws_bytes, cudaStream_t st);
 int finalize_impl(vf_grid *g, int L, cudaStream_t st);
-// Alg. 5 (+x, -x for L > 0) + finalize of one level, warp per block row
-size_t propagate_level_workspace_size(const vf_config &cfg, int L);
-int propagate_level_impl(const LevelInfo &li, vf_grid *g, int L, void *ws, size_t ws_bytes,
-                         cudaStream_t st);
 int shard_zero_impl(const LevelInfo &li, vf_grid *g, int L, int32_t *bcount, cudaStream_t st);
+// sparse block rows (vf_rows.cu): level 0 after init_forest, level L+1 after
+// adapt(L); Alg. 5 (+x, -x for L > 0) + finalize of level L over them
+size_t rows_workspace_size(int32_t capacity);
+int rows_init_impl(const vf_config &cfg, vf_grid *g, void *ws, cudaStream_t st);
+int rows_next_impl(vf_grid *g, int L, void *ws, cudaStream_t st);
+int propagate_rows_impl(const LevelInfo &li, vf_grid *g, int L, void *ws, cudaStream_t st);
 
 // forest
 int init_forest_impl(const vf_config &cfg, vf_grid *g, cudaStream_t st);

@@ -22,6 +22,7 @@
 
 #include "vf_common.cuh"
 #include "vf_internal.h"
+#include "vf_rowops.cuh"
 
 namespace vf {
 
@@ -317,57 +318,6 @@ int voxelize_impl(const LevelInfo &li, vf_grid *g, int L, const vf_bins *bins, c
 // packed as A | B << 16.  A run start (back slot < 0) carries the constant
 // f_b(sigma) with sigma = SOLID iff its back code is SOLID_NBR.
 
-__device__ __forceinline__ uint32_t compose(uint32_t g, uint32_t f) {
-    // (g o f)(x) = g(f(x)); per row: f(x)=1 -> g(S) else g(O)
-    const uint32_t gA = g & 0xffffu, gB = g >> 16, fA = f & 0xffffu, fB = f >> 16;
-    const uint32_t A = (fA & gA) | (~fA & gB & 0xffffu);
-    const uint32_t B = (fB & gA) | (~fB & gB & 0xffffu);
-    return A | (B << 16);
-}
-
-// byte-SIMD on a row word (the 4 cells of an x-row, one mask byte each)
-__device__ __forceinline__ uint32_t bytes_eq(uint32_t x, uint32_t v) { return __vcmpeq4(x, v * 0x01010101u); }
-// 0xff / 0x00 bytes -> 4 bits (byte i -> bit i)
-__device__ __forceinline__ uint32_t nib4(uint32_t m) { return ((m & 0x01010101u) * 0x01020408u) >> 24; }
-
-// Alg. 5 transfer function of a block from its rows' trailing cells (A10):
-// bit r of A = (H_trail != GUARD), of B = (H_trail == SOLID)
-__device__ __forceinline__ void row_fn(const uint32_t w[16], int trail, uint32_t &A, uint32_t &B) {
-    A = B = 0;
-    const uint32_t sel = (uint32_t)trail | ((4u + (uint32_t)trail) << 4);
-#pragma unroll
-    for (int r = 0; r < 16; r += 4) {
-        const uint32_t t4 = __byte_perm(__byte_perm(w[r], w[r + 1], sel), __byte_perm(w[r + 2], w[r + 3], sel),
-                                        0x5410);  // trailing bytes of rows r..r+3
-        A |= nib4(~bytes_eq(t4, VF_GUARD)) << r;
-        B |= nib4(bytes_eq(t4, VF_SOLID)) << r;
-    }
-}
-
-// Alg. 5 update of one row word: carried SOLID turns every non-GUARD cell
-// SOLID; on level 0 GUARD -> FLUID afterwards
-__device__ __forceinline__ uint32_t row_apply(uint32_t xw, bool solid, bool l0) {
-    const uint32_t g = bytes_eq(xw, VF_GUARD);
-    if (solid) xw = (xw & g) | ((0x01010101u * VF_SOLID) & ~g);
-    if (l0) xw &= ~g;  // GUARD bytes are unchanged by the update; FLUID = 0
-    return xw;
-}
-
-__device__ __forceinline__ void load_masks64(const uint8_t *masks, int64_t b, uint32_t w[16]) {
-    const uint4 *p = reinterpret_cast<const uint4 *>(masks + 64 * b);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const uint4 u = p[k];
-        w[4 * k] = u.x; w[4 * k + 1] = u.y; w[4 * k + 2] = u.z; w[4 * k + 3] = u.w;
-    }
-}
-
-__device__ __forceinline__ void store_masks64(uint8_t *masks, int64_t b, const uint32_t w[16]) {
-    uint4 *p = reinterpret_cast<uint4 *>(masks + 64 * b);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) p[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
-}
-
 __global__ void __launch_bounds__(256)
     k_xfun(int L, int back, int trail, const int32_t *__restrict__ level_start,
            const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
@@ -408,24 +358,6 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// finalize (pin A11): GUARD -> FLUID, block solid flag, and the
-// block's 64-bit SOLID-cell mask (bit t = cell t) used by the boundary halo
-// and exchanged between ranks at the finest level
-__device__ __forceinline__ void finalize_block(uint32_t w[16], bool &changed, uint8_t *bflags,
-                                               uint64_t *solid64, int64_t b) {
-    uint64_t sm = 0;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-        const uint32_t x = w[r] & ~bytes_eq(w[r], VF_GUARD);  // GUARD -> FLUID (0)
-        sm |= (uint64_t)nib4(bytes_eq(w[r], VF_SOLID)) << (4 * r);
-        changed |= (x != w[r]);
-        w[r] = x;
-    }
-    const uint8_t f0 = bflags[b];
-    bflags[b] = (uint8_t)((f0 & ~VF_BF_SOLID) | (sm ? VF_BF_SOLID : 0));
-    solid64[b] = sm;
-}
-
 __global__ void __launch_bounds__(256)
     k_xapply(int L, int back, int finalize, const int32_t *__restrict__ level_start,
              const int32_t *__restrict__ nbr, uint8_t *__restrict__ masks,
@@ -464,479 +396,6 @@ __global__ void __launch_bounds__(256)
         finalize_block(w, changed, bflags, solid64, b);
         if (changed) store_masks64(masks, b, w);
     }
-}
-
-// --------------------------------------------------------------------------
-// K-xrows: Alg. 5 in both directions + finalize as ONE kernel per level.
-//
-// A dense map of the level's blocks (B_L^3 ids, -1 = no level-L block) turns
-// every x-row of blocks into a contiguous array, so one warp owns one row
-// (j, k) and reads its positions 32 at a time (coalesced) instead of walking
-// the neighbour chain (the paper's sequential walk) or pointer-jumping over
-// it (k_xfun/k_xjump/k_xapply: 2 + ceil(log2 B_L) launches per direction).
-// Per chunk: transfer functions of the 32 blocks, a warp segmented scan with
-// compose() (segments start at run starts, which carry f_b(sigma), and at
-// lane 0, which folds in the status leaving the previous chunk), the status
-// entering each block = the scan value of its predecessor, then the fill /
-// finalize of that block.  The -x pass re-reads the +x results of the same
-// row (same warp, ordered by __syncwarp).  Identical results to the
-// pointer-jumping operators (same f_b, same composition, same apply).
-
-__global__ void k_level_map(int L, LevelInfo li, const int32_t *__restrict__ level_start,
-                            const int32_t *__restrict__ coords, int32_t *__restrict__ map) {
-    const int32_t s = level_start[L], e = level_start[L + 1];
-    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
-         b += (int64_t)gridDim.x * blockDim.x) {
-        const int4 c = reinterpret_cast<const int4 *>(coords)[b];
-        map[c.x + (int64_t)li.bins[0] * (c.y + (int64_t)li.bins[1] * c.z)] = (int32_t)b;
-    }
-}
-
-// one direction over one row; returns nothing, masks updated in place
-template <int DIR>
-__device__ __forceinline__ void xrow_pass(int L, int lane, const int32_t *__restrict__ row, int bx,
-                                          const int32_t *__restrict__ nbr, uint8_t *__restrict__ masks,
-                                          bool finalize, uint8_t *__restrict__ bflags,
-                                          uint64_t *__restrict__ solid64) {
-    constexpr int back = DIR > 0 ? 2 : 1, trail = DIR > 0 ? 3 : 0;
-    uint32_t carry = 0;        // status leaving the last block of the previous chunk
-    bool prev_present = false;  // ... and whether that position holds a level-L block
-    for (int x0 = 0; x0 < bx; x0 += 32) {
-        const int x = DIR > 0 ? x0 + lane : bx - 1 - (x0 + lane);
-        const int32_t id = (x0 + lane < bx) ? row[x] : -1;
-        const bool present = id >= 0;
-        const uint32_t pm = __ballot_sync(0xffffffffu, present);
-        if (pm == 0) {
-            prev_present = false;
-            continue;
-        }
-        const bool pred = lane > 0 ? ((pm >> (lane - 1)) & 1u) : prev_present;
-        uint32_t w[16];
-        uint32_t fn = 0;
-        bool head = true;
-        if (present) {
-            load_masks64(masks, id, w);
-            uint32_t A, B;
-            row_fn(w, trail, A, B);
-            fn = A | (B << 16);
-            if (!pred) {  // run start: back neighbour is not a level-L block
-                const int32_t code = nbr[27 * (int64_t)id + back];
-                const uint32_t c = (code == VF_NB_SOLID_NBR) ? A : B;  // f_b(sigma)
-                fn = c | (c << 16);
-            } else if (lane == 0) {  // continue the previous chunk's run
-                fn = compose(fn, carry | (carry << 16));
-            } else {
-                head = false;
-            }
-        }
-        // segmented inclusive scan (compose) across the warp
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t g = __shfl_up_sync(0xffffffffu, fn, o);
-            const int hd = __shfl_up_sync(0xffffffffu, (int)head, o);
-            if (lane >= o && !head) {
-                fn = compose(fn, g);
-                head = hd;
-            }
-        }
-        const uint32_t out = fn & 0xffffu;  // constant: status leaving this block
-        uint32_t st = __shfl_up_sync(0xffffffffu, out, 1);
-        if (lane == 0) st = carry;
-        if (present) {
-            bool changed = false;
-            if (pred) {
-#pragma unroll
-                for (int r = 0; r < 16; ++r) {
-                    const uint32_t xw = row_apply(w[r], (st >> r) & 1u, L == 0);
-                    changed |= (xw != w[r]);
-                    w[r] = xw;
-                }
-            }
-            if (finalize) finalize_block(w, changed, bflags, solid64, id);
-            if (changed) store_masks64(masks, id, w);
-        }
-        carry = __shfl_sync(0xffffffffu, out, 31);
-        prev_present = (pm >> 31) & 1u;
-    }
-}
-
-constexpr int kXrowWarps = 8;
-
-__global__ void __launch_bounds__(kXrowWarps * 32)
-    k_xrows(LevelInfo li, int L, const int32_t *__restrict__ map, const int32_t *__restrict__ nbr,
-            uint8_t *__restrict__ masks, uint8_t *__restrict__ bflags,
-            uint64_t *__restrict__ solid64) {
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = (int64_t)blockIdx.x * kXrowWarps + (threadIdx.x >> 5);
-    const int64_t nw = (int64_t)gridDim.x * kXrowWarps;
-    const int bx = li.bins[0], by = li.bins[1];
-    const int64_t rows = (int64_t)by * li.bins[2];
-    for (int64_t r = gw; r < rows; r += nw) {
-        const int j = (int)(r % by), k = (int)(r / by);
-        if (!owns_row(li, j, k)) continue;  // multi-GPU: rows of other ranks
-        const int32_t *row = map + r * bx;
-        xrow_pass<+1>(L, lane, row, bx, nbr, masks, L == 0, bflags, solid64);
-        if (L > 0) {
-            __syncwarp();
-            xrow_pass<-1>(L, lane, row, bx, nbr, masks, true, bflags, solid64);
-        }
-    }
-}
-
-// Staged variant for rows of up to 32 * NCH blocks (levels with B_L <= 128): the row's block ids, masks (row stride 17 words: no bank
-// conflicts), run-start neighbour codes of both directions and changed
-// flags are staged in shared memory with all global loads issued up front,
-// then both passes run out of shared memory and only changed blocks are
-// stored -- the chunked passes above wait on a dependent load chain per
-// chunk and per direction.
-constexpr int kXsWarps = 4;
-static int g_xrows_chunked = 0;  // vf_set_xrows_chunked (test hook): force the chunked kernel
-
-template <int NCH>
-struct XStage {
-    int32_t id[NCH * 32];
-    int32_t cp[NCH * 32];  // +x run start: code of the -x neighbour (slot 2)
-    int32_t cm[NCH * 32];  // -x run start: code of the +x neighbour (slot 1)
-    uint8_t chg[NCH * 32];
-    uint32_t m[NCH * 32 * 17];
-};
-
-template <int DIR, int NCH>
-__device__ __forceinline__ void xrow_pass_s(int L, int lane, int bx, XStage<NCH> &S) {
-    constexpr int trail = DIR > 0 ? 3 : 0;
-    uint32_t carry = 0;
-    bool prev_present = false;
-#pragma unroll 1
-    for (int x0 = 0; x0 < bx; x0 += 32) {
-        const int x = DIR > 0 ? x0 + lane : bx - 1 - (x0 + lane);
-        const int32_t id = (x0 + lane < bx) ? S.id[x] : -1;
-        const bool present = id >= 0;
-        const uint32_t pm = __ballot_sync(0xffffffffu, present);
-        if (pm == 0) {
-            prev_present = false;
-            continue;
-        }
-        const bool pred = lane > 0 ? ((pm >> (lane - 1)) & 1u) : prev_present;
-        uint32_t *w = S.m + 17 * (x < 0 ? 0 : x);
-        uint32_t fn = 0;
-        bool head = true;
-        if (present) {
-            uint32_t A, B;
-            row_fn(w, trail, A, B);
-            fn = A | (B << 16);
-            if (!pred) {
-                const int32_t code = DIR > 0 ? S.cp[x] : S.cm[x];
-                const uint32_t c = (code == VF_NB_SOLID_NBR) ? A : B;
-                fn = c | (c << 16);
-            } else if (lane == 0) {
-                fn = compose(fn, carry | (carry << 16));
-            } else {
-                head = false;
-            }
-        }
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t g = __shfl_up_sync(0xffffffffu, fn, o);
-            const int hd = __shfl_up_sync(0xffffffffu, (int)head, o);
-            if (lane >= o && !head) {
-                fn = compose(fn, g);
-                head = hd;
-            }
-        }
-        const uint32_t out = fn & 0xffffu;
-        uint32_t st = __shfl_up_sync(0xffffffffu, out, 1);
-        if (lane == 0) st = carry;
-        if (present && pred) {
-            bool changed = false;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                const uint32_t xw = row_apply(w[r], (st >> r) & 1u, L == 0);
-                changed |= (xw != w[r]);
-                w[r] = xw;
-            }
-            if (changed) S.chg[x] = 1;
-        }
-        carry = __shfl_sync(0xffffffffu, out, 31);
-        prev_present = (pm >> 31) & 1u;
-        __syncwarp();
-    }
-}
-
-#ifndef VF_XS_MINB
-#define VF_XS_MINB 4  // <= 128 registers (1 lets the 4-chunk kernel take 162)
-#endif
-template <int NCH>
-__global__ void __launch_bounds__(kXsWarps * 32, VF_XS_MINB)
-    k_xrows_s(LevelInfo li, int L, const int32_t *__restrict__ map, const int32_t *__restrict__ nbr,
-              uint8_t *__restrict__ masks, uint8_t *__restrict__ bflags, uint64_t *__restrict__ solid64) {
-    extern __shared__ __align__(16) unsigned char s_raw[];
-    const int lane = threadIdx.x & 31;
-    XStage<NCH> &S = reinterpret_cast<XStage<NCH> *>(s_raw)[threadIdx.x >> 5];
-    const int64_t gw = (int64_t)blockIdx.x * kXsWarps + (threadIdx.x >> 5);
-    const int64_t nw = (int64_t)gridDim.x * kXsWarps;
-    const int bx = li.bins[0], by = li.bins[1];
-    const int64_t rows = (int64_t)by * li.bins[2];
-    for (int64_t rw = gw; rw < rows; rw += nw) {
-        const int j = (int)(rw % by), k = (int)(rw / by);
-        if (!owns_row(li, j, k)) continue;
-        const int32_t *row = map + rw * bx;
-        int32_t ids[NCH];
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) ids[c] = (32 * c + lane < bx) ? row[32 * c + lane] : -1;
-        uint32_t anyp = 0;
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            S.id[32 * c + lane] = ids[c];
-            S.chg[32 * c + lane] = 0;
-            anyp |= __ballot_sync(0xffffffffu, ids[c] >= 0);
-        }
-        if (!anyp) continue;  // empty row
-        __syncwarp();
-        // masks + run-start codes, all loads in flight together
-        uint4 mv[NCH][4];
-        int32_t cpv[NCH], cmv[NCH];
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            const int x = 32 * c + lane;
-            const int32_t id = ids[c];
-            cpv[c] = 0;
-            cmv[c] = 0;
-            if (id >= 0) {
-                const uint4 *p = reinterpret_cast<const uint4 *>(masks + 64 * (int64_t)id);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) mv[c][q] = p[q];
-                if (!(x > 0 && S.id[x - 1] >= 0)) cpv[c] = nbr[27 * (int64_t)id + 2];
-                if (L > 0 && !(x + 1 < bx && S.id[x + 1] >= 0)) cmv[c] = nbr[27 * (int64_t)id + 1];
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            const int x = 32 * c + lane;
-            if (ids[c] >= 0) {
-                uint32_t *w = S.m + 17 * x;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    w[4 * q] = mv[c][q].x; w[4 * q + 1] = mv[c][q].y;
-                    w[4 * q + 2] = mv[c][q].z; w[4 * q + 3] = mv[c][q].w;
-                }
-                S.cp[x] = cpv[c];
-                S.cm[x] = cmv[c];
-            }
-        }
-        __syncwarp();
-        xrow_pass_s<+1, NCH>(L, lane, bx, S);
-        if (L > 0) xrow_pass_s<-1, NCH>(L, lane, bx, S);
-        // finalize every block of the row and store the changed ones
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            const int x = 32 * c + lane;
-            const int32_t id = ids[c];
-            if (id < 0) continue;
-            uint32_t w[16];
-#pragma unroll
-            for (int r = 0; r < 16; ++r) w[r] = S.m[17 * x + r];
-            bool changed = S.chg[x] != 0;
-            finalize_block(w, changed, bflags, solid64, id);
-            if (changed) store_masks64(masks, id, w);
-        }
-        __syncwarp();
-    }
-}
-
-// Hybrid for wide, sparse rows (B_L = 256): block ids and run-start codes are
-// staged (all loads up front, empty 32-block chunks skipped without a load);
-// masks stay in global memory, loaded per non-empty chunk as in k_xrows,
-// with finalize fused into the last pass.
-template <int NCH>
-struct XHView {
-    const int32_t *id, *cp, *cm;
-};
-
-template <int DIR, int NCH>
-__device__ __forceinline__ void xrow_pass_hv(int L, int lane, int bx, const XHView<NCH> &S, uint32_t cmask,
-                                            uint8_t *__restrict__ masks, bool finalize,
-                                            uint8_t *__restrict__ bflags, uint64_t *__restrict__ solid64) {
-    constexpr int trail = DIR > 0 ? 3 : 0;
-    uint32_t carry = 0;
-    bool prev_present = false;
-#pragma unroll 1
-    for (int c = 0; c < NCH; ++c) {
-        const int x0 = 32 * c;
-        // chunk of this pass: +x walks chunks 0.., -x walks x = bx-1-(x0+lane)
-        const int cc = DIR > 0 ? c : (bx - 1 - x0) >> 5;
-        const bool any = DIR > 0 ? ((cmask >> c) & 1u) : (((cmask >> cc) & 1u) || (x0 + 31 < bx && ((cmask >> ((bx - 1 - x0 - 31) >> 5)) & 1u)));
-        if (x0 >= bx) break;
-        if (!any) {
-            prev_present = false;
-            continue;
-        }
-        const int x = DIR > 0 ? x0 + lane : bx - 1 - (x0 + lane);
-        const int32_t id = (x0 + lane < bx) ? S.id[x] : -1;
-        const bool present = id >= 0;
-        const uint32_t pm = __ballot_sync(0xffffffffu, present);
-        if (pm == 0) {
-            prev_present = false;
-            continue;
-        }
-        const bool pred = lane > 0 ? ((pm >> (lane - 1)) & 1u) : prev_present;
-        uint32_t w[16];
-        uint32_t fn = 0;
-        bool head = true;
-        if (present) {
-            load_masks64(masks, id, w);
-            uint32_t A, B;
-            row_fn(w, trail, A, B);
-            fn = A | (B << 16);
-            if (!pred) {
-                const int32_t code = DIR > 0 ? S.cp[x] : S.cm[x];
-                const uint32_t cb = (code == VF_NB_SOLID_NBR) ? A : B;
-                fn = cb | (cb << 16);
-            } else if (lane == 0) {
-                fn = compose(fn, carry | (carry << 16));
-            } else {
-                head = false;
-            }
-        }
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t g = __shfl_up_sync(0xffffffffu, fn, o);
-            const int hd = __shfl_up_sync(0xffffffffu, (int)head, o);
-            if (lane >= o && !head) {
-                fn = compose(fn, g);
-                head = hd;
-            }
-        }
-        const uint32_t out = fn & 0xffffu;
-        uint32_t st = __shfl_up_sync(0xffffffffu, out, 1);
-        if (lane == 0) st = carry;
-        if (present) {
-            bool changed = false;
-            if (pred) {
-#pragma unroll
-                for (int r = 0; r < 16; ++r) {
-                    const uint32_t xw = row_apply(w[r], (st >> r) & 1u, L == 0);
-                    changed |= (xw != w[r]);
-                    w[r] = xw;
-                }
-            }
-            if (finalize) finalize_block(w, changed, bflags, solid64, id);
-            if (changed) store_masks64(masks, id, w);
-        }
-        carry = __shfl_sync(0xffffffffu, out, 31);
-        prev_present = (pm >> 31) & 1u;
-    }
-}
-
-#ifndef VF_XH_MINB
-#define VF_XH_MINB 8  // 64 registers: the max_ctas(8) grid is resident in one wave (measured)
-#endif
-template <int NCH>
-__global__ void __launch_bounds__(kXsWarps * 32, VF_XH_MINB)
-    k_xrows_h(LevelInfo li, int L, const int32_t *__restrict__ map, const int32_t *__restrict__ nbr,
-              uint8_t *__restrict__ masks, uint8_t *__restrict__ bflags, uint64_t *__restrict__ solid64) {
-    __shared__ int32_t s_id[kXsWarps][NCH * 32], s_cp[kXsWarps][NCH * 32], s_cm[kXsWarps][NCH * 32];
-    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-    const int64_t gw = (int64_t)blockIdx.x * kXsWarps + wi;
-    const int64_t nw = (int64_t)gridDim.x * kXsWarps;
-    const int bx = li.bins[0], by = li.bins[1];
-    const int64_t rows = (int64_t)by * li.bins[2];
-    for (int64_t rw = gw; rw < rows; rw += nw) {
-        const int j = (int)(rw % by), k = (int)(rw / by);
-        if (!owns_row(li, j, k)) continue;
-        const int32_t *row = map + rw * bx;
-        int32_t ids[NCH];
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) ids[c] = (32 * c + lane < bx) ? row[32 * c + lane] : -1;
-        uint32_t cmask = 0;
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            s_id[wi][32 * c + lane] = ids[c];
-            cmask |= (__ballot_sync(0xffffffffu, ids[c] >= 0) ? 1u : 0u) << c;
-        }
-        if (!cmask) continue;
-        __syncwarp();
-        int32_t cpv[NCH], cmv[NCH];
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            const int x = 32 * c + lane;
-            const int32_t id = ids[c];
-            cpv[c] = 0;
-            cmv[c] = 0;
-            if (id >= 0) {
-                if (!(x > 0 && s_id[wi][x - 1] >= 0)) cpv[c] = nbr[27 * (int64_t)id + 2];
-                if (L > 0 && !(x + 1 < bx && s_id[wi][x + 1] >= 0)) cmv[c] = nbr[27 * (int64_t)id + 1];
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            s_cp[wi][32 * c + lane] = cpv[c];
-            s_cm[wi][32 * c + lane] = cmv[c];
-        }
-        __syncwarp();
-        XHView<NCH> V{s_id[wi], s_cp[wi], s_cm[wi]};
-        xrow_pass_hv<+1, NCH>(L, lane, bx, V, cmask, masks, L == 0, bflags, solid64);
-        if (L > 0) {
-            __syncwarp();
-            xrow_pass_hv<-1, NCH>(L, lane, bx, V, cmask, masks, true, bflags, solid64);
-        }
-        __syncwarp();
-    }
-}
-
-template <int NCH>
-static int launch_xrows_s(const LevelInfo &li, int L, const int32_t *map, vf_grid *g, cudaStream_t st) {
-    const size_t smem = kXsWarps * sizeof(XStage<NCH>);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_xrows_s<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    const int64_t rows = (int64_t)li.bins[1] * li.bins[2];
-    int64_t grid = (rows + kXsWarps - 1) / kXsWarps;
-    const int64_t cap = max_ctas(NCH <= 2 ? 16 : (NCH <= 4 ? VF_GRID_XS4 : 4));
-    if (grid > cap) grid = cap;
-    k_xrows_s<NCH><<<(int)grid, kXsWarps * 32, smem, st>>>(li, L, map, g->d_nbr, g->d_masks, g->d_bflags,
-                                                           g->d_solid64);
-    return check_launch("k_xrows");
-}
-
-size_t propagate_level_workspace_size(const vf_config &cfg, int L) {
-    const int64_t nb = (int64_t)(cfg.nb[0] << L) * (cfg.nb[1] << L) * (cfg.nb[2] << L);
-    return ((size_t)nb * sizeof(int32_t) + 255) & ~(size_t)255;
-}
-
-int propagate_level_impl(const LevelInfo &li, vf_grid *g, int L, void *ws, size_t ws_bytes,
-                         cudaStream_t st) {
-    const int64_t nb = (int64_t)li.bins[0] * li.bins[1] * li.bins[2];
-    if (ws_bytes < (size_t)nb * sizeof(int32_t)) return set_error(VF_EARG, "propagate workspace too small");
-    int32_t *map = (int32_t *)ws;
-    cudaMemsetAsync(map, 0xff, sizeof(int32_t) * (size_t)nb, st);
-    kt_point("memset:level_map");
-    k_level_map<<<max_ctas(8), 256, 0, st>>>(L, li, g->d_level_start, g->d_coords, map);
-    int rc = check_launch("k_level_map");
-    if (rc) return rc;
-    const int bx = li.bins[0];
-    if (!g_xrows_chunked) {
-        if (bx <= 32) return launch_xrows_s<1>(li, L, map, g, st);
-        if (bx <= 64) return launch_xrows_s<2>(li, L, map, g, st);
-        if (bx <= 128) return launch_xrows_s<4>(li, L, map, g, st);
-        // (8 chunks staged: 215 registers and 83 KB of shared memory per CTA --
-        // slower next to the concurrent link enumeration; ids / codes only)
-        if (bx <= 256) {
-            const int64_t rows = (int64_t)li.bins[1] * li.bins[2];
-            int64_t grid = (rows + kXsWarps - 1) / kXsWarps;
-            if (grid > max_ctas(8)) grid = max_ctas(8);
-            k_xrows_h<8><<<(int)grid, kXsWarps * 32, 0, st>>>(li, L, map, g->d_nbr, g->d_masks, g->d_bflags,
-                                                              g->d_solid64);
-            return check_launch("k_xrows");
-        }
-    }
-    int64_t rows = (int64_t)li.bins[1] * li.bins[2];
-    int64_t grid = (rows + kXrowWarps - 1) / kXrowWarps;
-    if (grid > max_ctas(8)) grid = max_ctas(8);
-    k_xrows<<<(int)grid, kXrowWarps * 32, 0, st>>>(li, L, map, g->d_nbr, g->d_masks, g->d_bflags,
-                                                   g->d_solid64);
-    return check_launch("k_xrows");
 }
 
 // multi-GPU exchange: zero what this rank does not own on level L
@@ -997,9 +456,3 @@ int finalize_impl(vf_grid *g, int L, cudaStream_t st) {
 }
 
 }  // namespace vf
-
-extern "C" int vf_set_xrows_chunked(int on) {
-    const int old = vf::g_xrows_chunked;
-    if (on >= 0) vf::g_xrows_chunked = on ? 1 : 0;
-    return old;
-}

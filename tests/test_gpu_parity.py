@@ -468,19 +468,15 @@ def test_links_small_face_split(O, torus, small_ext):
         lib.vf_set_link_small_ext(old)
 
 
-@pytest.mark.parametrize("chunked", [1, 0])
-def test_xrows_kernels(O, torus, chunked):
-    """Alg. 5 rows: the shared-memory staged kernel (rows <= 128 blocks), the
-    hybrid (256) and the chunked one give the oracle's masks."""
-    from paper_2512_01251_b200 import _lib
-    lib = _lib.require_cuda()
-    old = lib.vf_set_xrows_chunked(chunked)
-    try:
-        _embed_compare(O, torus, EmbedConfig(n_x=32, l_max=3))
-        _embed_compare(O, make_icosphere((0.5, 0.5, 0.5), 0.5, 4), EmbedConfig(n_x=64, l_max=3))
-        _embed_compare(O, make_torus(300, 120), EmbedConfig(n_x=64, l_max=5))  # B_L = 256 rows
-    finally:
-        lib.vf_set_xrows_chunked(old)
+def test_sparse_rows(O, torus):
+    """Alg. 5 over the sparse row order (vf_rows.cu): short rows, rows of
+    B_L = 256, and long x-runs spanning several 32-block chunks (a slab whose
+    faces parallel to x refine whole rows) give the oracle's masks."""
+    _embed_compare(O, torus, EmbedConfig(n_x=32, l_max=3))
+    _embed_compare(O, make_icosphere((0.5, 0.5, 0.5), 0.5, 4), EmbedConfig(n_x=64, l_max=3))
+    _embed_compare(O, make_torus(300, 120), EmbedConfig(n_x=64, l_max=5))  # B_L = 256 rows
+    slab = _box_mesh([0.03 + 0.5 / 512, 0.41 + 0.3 / 512, 0.44 + 0.7 / 512], [0.97 - 0.5 / 512, 0.6, 0.55], 24)
+    _embed_compare(O, slab, EmbedConfig(n_x=64, l_max=4))
 
 
 def test_serial_links_identical(torus):
