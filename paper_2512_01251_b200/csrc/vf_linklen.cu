@@ -49,57 +49,6 @@
 
 namespace vf {
 
-// Finest-level block -> LUT slot: an open-addressing hash of the MAPPED
-// blocks only (N_b entries at load <= 1/2; a few MB, L2-resident) instead of
-// a dense B_L^3 map.  Entry = key << 24 | slot (key = bi + B_x (bj + B_y bk)
-// < 2^40, slot < 2^24), empty = ~0.  The table size follows the
-// device-resident N_b (pow2 >= 2 N_b, hinfo[0] = log2 size), so only the used
-// part is cleared.  Nothing is mapped when N_b exceeds the LUT capacity
-// (error latched by k_fill_lut).  Multi-GPU: only this rank's blocks are
-// mapped, so every rank fills the LUT slots of the blocks it owns.
-constexpr unsigned long long kHashEmpty = ~0ull;
-
-__device__ __forceinline__ uint64_t hash_slot0(uint64_t key, int bits) {
-    key ^= key >> 33;  // murmur3 finaliser: block keys are highly structured
-    key *= 0xff51afd7ed558ccdull;
-    key ^= key >> 33;
-    key *= 0xc4ceb9fe1a85ec53ull;
-    key ^= key >> 33;
-    return key >> (64 - bits);
-}
-
-__global__ void k_hash_clear(const int32_t *__restrict__ d_n_b, int64_t nb_static, int32_t *__restrict__ hinfo,
-                             unsigned long long *__restrict__ htab) {
-    const int64_t nb = d_n_b ? (int64_t)*d_n_b : nb_static;  // (SPEC op path: the grid capacity)
-    int bits = 10;
-    while ((1ll << bits) < 4 * nb) ++bits;  // load <= 1/4
-    if (blockIdx.x == 0 && threadIdx.x == 0) hinfo[0] = bits;
-    const int64_t n = 1ll << bits;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        htab[i] = kHashEmpty;
-}
-
-__global__ void k_hash_insert(LevelInfo li, int L, const int32_t *__restrict__ level_start,
-                              const int32_t *__restrict__ coords, const int32_t *__restrict__ cmap,
-                              const int32_t *__restrict__ hinfo, unsigned long long *__restrict__ htab,
-                              const int32_t *__restrict__ d_n_b, int64_t cap) {
-    if (d_n_b && *d_n_b > cap) return;
-    const int bits = hinfo[0];
-    const uint64_t mask = (1ull << bits) - 1;
-    const int32_t s = level_start[L], e = level_start[L + 1];
-    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e;
-         b += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t slot = cmap[b];
-        if (slot < 0) continue;
-        const int4 c = reinterpret_cast<const int4 *>(coords)[b];
-        if (!owns_row(li, c.y, c.z)) continue;
-        const uint64_t key = (uint64_t)c.x + (uint64_t)li.bins[0] * ((uint64_t)c.y + (uint64_t)li.bins[1] * c.z);
-        const unsigned long long ent = (key << 24) | (uint64_t)slot;
-        for (uint64_t h = hash_slot0(key, bits);; h = (h + 1) & mask)
-            if (atomicCAS(&htab[h], kHashEmpty, ent) == kHashEmpty) break;
-    }
-}
-
 // exact decision for one (face, node, direction pair) candidate: num and
 // d = num/den bit-identical to the oracle (orc_link_lengths), then the
 // eps-box SAT at the piercing point
@@ -142,8 +91,10 @@ constexpr int kLinkWarps = 4;
 
 struct LinkCtx {
     const double *faces;
-    const unsigned long long *htab;  // mapped finest blocks -> LUT slot (k_hash_insert)
-    const int32_t *hinfo;            // [0] log2 table size
+    // finest block of a lattice node -> LUT slot: forest descent + contraction map
+    const int32_t *child, *cmap, *level_start;
+    LevelInfo li;                    // the finest level (multi-GPU: the rank's rows)
+    int64_t lut_cap;                 // slots the LUT holds
     float *lengths;
     int4 *band;        // band candidates (face, slot, i | j<<16, k | r<<16)
     int32_t *n_band;   // [0] count (may exceed cap), [1] overflow flag
@@ -165,16 +116,19 @@ struct LinkCtx {
     unsigned long long *n_tests;  // lattice lines classified (FP32 intersection tests; roofline ops)
 };
 
-// LUT slot of the finest block holding lattice node (i, j, k); -1: not mapped
+// LUT slot of the finest block holding lattice node (i, j, k); -1: not
+// mapped (no finest block there, not a boundary block, another rank's row,
+// or N_b beyond the LUT capacity).  The forest descent costs L_max dependent
+// loads: only the rare exact paths and the SPEC-op / sharded cut links use it.
 __device__ __forceinline__ int32_t slot_at(const LinkCtx &c, int i, int j, int k) {
-    const int bits = c.hinfo[0];
-    const uint64_t mask = (1ull << bits) - 1;
-    const uint64_t key = (uint64_t)(i >> 2) + (uint64_t)c.bx * ((uint64_t)(j >> 2) + (uint64_t)c.by * (uint64_t)(k >> 2));
-    for (uint64_t h = hash_slot0(key, bits);; h = (h + 1) & mask) {
-        const unsigned long long e = __ldg(&c.htab[h]);
-        if (e == kHashEmpty) return -1;
-        if ((e >> 24) == key) return (int32_t)(e & 0xffffffu);
-    }
+    const int L = c.li.level;
+    const int bi = i >> 2, bj = j >> 2, bk = k >> 2;
+    if (!owns_row(c.li, bj, bk)) return -1;
+    const int3 nb0 = make_int3(c.li.bins[0] >> L, c.li.bins[1] >> L, c.li.bins[2] >> L);
+    const int32_t b = block_of_key(L, bi, bj, bk, nb0, c.child, c.level_start[VF_MAX_LEVELS]);
+    if (b < 0) return -1;
+    const int32_t slot = c.cmap[b];
+    return slot < c.lut_cap ? slot : -1;
 }
 
 // add a per-thread count to the global test counter, one atomic per warp
@@ -1011,13 +965,20 @@ __device__ __forceinline__ void qrec_entry(const int4 rec, int k, int &i, int &j
     t = (i & 3) + 4 * (j & 3) + 16 * (kk & 3);
 }
 
-// (1) resolved link: its parent key (resu, -1: none) and octant << 41 |
-// (q 64 + t) << 30 | q bits (rese; q in (0, 1]: 30 bits).  Neighbouring
-// lines of a warp mostly share parents: one counter atomic per distinct
-// parent of the warp (__match_any_sync)
+// a link's parent bucket key and its bucket entry octant << 41 | (q 64 + t)
+// << 30 | q bits (q in (0, 1]: 30 bits)
+__device__ __forceinline__ int32_t link_bucket_entry(const int4 rec, int k, int3 pdim, unsigned long long &x) {
+    int i, j, kk, q, t;
+    qrec_entry(rec, k, i, j, kk, q, t);
+    const int oct = ((i >> 2) & 1) + 2 * ((j >> 2) & 1) + 4 * ((kk >> 2) & 1);
+    x = ((unsigned long long)oct << 41) | ((unsigned long long)(q * 64 + t) << 30) | (uint32_t)(k ? rec.w : rec.z);
+    return (i >> 3) + pdim.x * ((j >> 3) + pdim.y * (kk >> 3));
+}
+
+// (1) per-parent link counts.  Neighbouring lines of a warp mostly share
+// parents: one counter atomic per distinct parent of the warp (__match_any_sync)
 __global__ void __launch_bounds__(256)
-    k_block_count(LinkCtx c, int3 pdim, int32_t *__restrict__ bcnt, int32_t *__restrict__ resu,
-                  unsigned long long *__restrict__ rese) {
+    k_block_count(LinkCtx c, int3 pdim, int32_t *__restrict__ bcnt) {
     const int64_t n = min((int64_t)*c.n_lines, c.line_cap);
     const int lane = threadIdx.x & 31;
     for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); e0 < n;
@@ -1027,42 +988,32 @@ __global__ void __launch_bounds__(256)
         const int ne = (rec.y >> 19) & 3;
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            int i = 0, j = 0, kk = 0, q = 0, t = 0;
-            int32_t key = -1;
-            if (k < ne) {
-                qrec_entry(rec, k, i, j, kk, q, t);
-                key = (i >> 3) + pdim.x * ((j >> 3) + pdim.y * (kk >> 3));
-            }
+            unsigned long long x;
+            const int32_t key = k < ne ? link_bucket_entry(rec, k, pdim, x) : -1;
             const uint32_t grp = __match_any_sync(0xffffffffu, key);
             if (key >= 0 && lane == __ffs(grp) - 1) atomicAdd(&bcnt[key], __popc(grp));
-            if (e < n) {
-                resu[2 * e + k] = key;
-                const int oct = ((i >> 2) & 1) + 2 * ((j >> 2) & 1) + 4 * ((kk >> 2) & 1);
-                rese[2 * e + k] = ((unsigned long long)oct << 41) | ((unsigned long long)(q * 64 + t) << 30) |
-                                  (uint32_t)(k ? rec.w : rec.z);
-            }
         }
     }
 }
 
-// (3) links into parent order; four per thread in flight (the cursor
-// atomics' returns are the latency)
+// (3) links into parent order (the records are re-read; the cursor atomics'
+// returns are the latency: two records per thread in flight)
 __global__ void __launch_bounds__(256)
-    k_block_scatter(const int32_t *__restrict__ d_n_lines, int64_t line_cap,
-                    const int32_t *__restrict__ resu, const unsigned long long *__restrict__ rese,
-                    int32_t *__restrict__ bcur, unsigned long long *__restrict__ ent) {
-    const int64_t n = 2 * min((int64_t)*d_n_lines, line_cap);
+    k_block_scatter(LinkCtx c, int3 pdim, int32_t *__restrict__ bcur, unsigned long long *__restrict__ ent) {
+    const int64_t n = min((int64_t)*c.n_lines, c.line_cap);
     const int lane = threadIdx.x & 31;
-    const int64_t step = (int64_t)gridDim.x * blockDim.x * 4;
-    for (int64_t e0 = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * 4; e0 < n; e0 += step) {
+    const int64_t step = (int64_t)gridDim.x * blockDim.x * 2;
+    for (int64_t e0 = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * 2; e0 < n; e0 += step) {
         unsigned long long x[4];
         int32_t g[4], base[4];
         uint32_t grp[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 2; ++u) {
             const int64_t e = e0 + 32 * u + lane;
-            g[u] = e < n ? resu[e] : -1;
-            x[u] = e < n ? rese[e] : 0;
+            const int4 rec = e < n ? c.lines[e] : make_int4(0, 0, 0, 0);
+            const int ne = (rec.y >> 19) & 3;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) g[2 * u + k] = k < ne ? link_bucket_entry(rec, k, pdim, x[2 * u + k]) : -1;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -1152,16 +1103,9 @@ __global__ void __launch_bounds__(256)
 constexpr int64_t kBandCap = 1 << 20;  // 16 MB; overflow only costs the fallback pass
 static int64_t g_band_cap = kBandCap;    // vf_set_link_band_cap (test hook)
 
-// workspace: band counters | slot hash size | band list | slot hash (pow2 >=
-// 2 x the grid capacity entries: N_b <= the finest-level blocks <= capacity)
-static size_t hash_entries(int32_t capacity) {
-    size_t n = 1024;
-    while (n < 4 * (size_t)capacity) n <<= 1;
-    return n;
-}
-
-size_t link_workspace_size(const vf_config &, int, int32_t capacity) {
-    return 512 + (size_t)kBandCap * sizeof(int4) + hash_entries(capacity) * sizeof(unsigned long long);
+// workspace: band counters | band list
+size_t link_workspace_size(const vf_config &, int, int32_t) {
+    return 512 + (size_t)kBandCap * sizeof(int4);
 }
 
 // LUT initialisation to -1 for the device-resident N_b slots (graph-safe:
@@ -1198,9 +1142,9 @@ static int make_link_ctx(const vf_config &cfg, int L, const double *faces, float
     c.faces = faces;
     c.lengths = lengths;
     c.n_band = (int32_t *)ws;
-    c.hinfo = (int32_t *)((char *)ws + 256);
     c.band = (int4 *)((char *)ws + 512);
-    c.htab = (const unsigned long long *)((char *)ws + 512 + (size_t)kBandCap * sizeof(int4));
+    c.li = li;
+    c.lut_cap = INT64_MAX;
     c.band_cap = g_band_cap;
     c.dx = li.dx;
     c.eps = li.eps;
@@ -1234,17 +1178,14 @@ static int link_grid(int64_t F) {
     return grid < 1 ? 1 : (int)grid;
 }
 
-// the slot hash of the finest level's mapped blocks
-static int link_blockmap(vf_grid *g, const LevelInfo &li, const int32_t *cmap, const LinkCtx &c,
-                         const int32_t *d_n_b, int64_t lengths_cap, cudaStream_t st) {
-    unsigned long long *htab = const_cast<unsigned long long *>(c.htab);
-    int32_t *hinfo = const_cast<int32_t *>(c.hinfo);
-    k_hash_clear<<<max_ctas(4), 256, 0, st>>>(d_n_b, g->capacity, hinfo, htab);
-    int rc = check_launch("k_hash_clear");
-    if (rc) return rc;
-    k_hash_insert<<<max_ctas(8), 256, 0, st>>>(li, li.level, g->d_level_start, g->d_coords, cmap, hinfo, htab,
-                                               d_n_b, lengths_cap);
-    return check_launch("k_blockmap");
+// the slot lookup of the finest level (slot_at): grid + contraction map,
+// slots bounded by the LUT capacity (N_b > cap is latched as VF_ECAPACITY by
+// the LUT kernels)
+static void link_lookup(vf_grid *g, const int32_t *cmap, LinkCtx &c, int64_t lengths_cap) {
+    c.child = g->d_child;
+    c.cmap = cmap;
+    c.level_start = g->d_level_start;
+    c.lut_cap = lengths_cap > 0 ? lengths_cap : INT64_MAX;
 }
 
 int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
@@ -1259,7 +1200,7 @@ int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const doubl
     int rc = make_link_ctx(cfg, L, faces, lengths, ws, c, widen, li);
     if (rc) return rc;
     cudaMemsetAsync(c.n_band, 0, 2 * sizeof(int32_t), st);
-    if ((rc = link_blockmap(g, li, cmap, c, d_n_b, lengths_cap, st))) return rc;
+    link_lookup(g, cmap, c, lengths_cap);
     const int grid = link_grid(F);
     if (events) cudaEventRecord((cudaEvent_t)events[0], st);
     k_links<0><<<grid, kLinkWarps * 32, kLinkSmem, st>>>(c, widen, F, map, d_n_map);
@@ -1291,20 +1232,19 @@ static int64_t parents_of(const vf_config &cfg) {
 }
 
 // ... | parent counts | parent offsets | parent cursors | slot -> block | scan |
-// parent-ordered links | resolved links (<= 2 links per q-record each)
+// parent-ordered links (<= 2 links per q-record)
 size_t link_lines_bytes(const vf_config &cfg, int64_t F, int32_t capacity) {
     const int64_t cap = line_cap_of(F), nt = parents_of(cfg);
     return 256 + (size_t)cap * sizeof(int4) + 2 * list_bytes(F) +
            al256(((size_t)F + 32) / 32 * sizeof(uint32_t)) + 3 * al256((size_t)nt * sizeof(int32_t)) +
            al256((size_t)capacity * sizeof(int32_t)) +
-           al256(scan_workspace_bytes(nt)) + (size_t)(2 * cap) * (2 * sizeof(unsigned long long) + sizeof(int32_t));
+           al256(scan_workspace_bytes(nt)) + (size_t)(2 * cap) * sizeof(unsigned long long);
 }
 
 struct BlockLinkBufs {
     int32_t *bcnt, *boff, *bcur, *inv;  // per parent bucket: links, first, cursor; slot -> block
     void *scan_ws;
-    unsigned long long *ent, *rese;  // block-ordered links; resolved links in record order
-    int32_t *resu;                   // finest block of each resolved link
+    unsigned long long *ent;  // parent-ordered links
     int64_t n_max;
 };
 
@@ -1328,8 +1268,6 @@ static int32_t *line_bufs(LinkCtx &c, int64_t F, void *lines_ws, const vf_config
         tb->inv = (int32_t *)(p + 3 * al256((size_t)nt * sizeof(int32_t)));
         tb->scan_ws = p + 3 * al256((size_t)nt * sizeof(int32_t)) + al256((size_t)capacity * sizeof(int32_t));
         tb->ent = (unsigned long long *)((char *)tb->scan_ws + al256(scan_workspace_bytes(nt)));
-        tb->rese = tb->ent + 2 * c.line_cap;
-        tb->resu = (int32_t *)(tb->rese + 2 * c.line_cap);
     }
     return big;
 }
@@ -1407,13 +1345,13 @@ static int link_bucket(const vf_config &cfg, LinkCtx &c, int64_t F, void *lines_
     line_bufs(c, F, lines_ws, &cfg, capacity, &tb);
     cudaMemsetAsync(tb.bcnt, 0, sizeof(int32_t) * (size_t)tb.n_max, st);
     kt_point("memset:parent_counts");
-    k_block_count<<<max_ctas(8), 256, 0, st>>>(c, parent_dims(cfg), tb.bcnt, tb.resu, tb.rese);
+    k_block_count<<<max_ctas(8), 256, 0, st>>>(c, parent_dims(cfg), tb.bcnt);
     int rc = check_launch("k_block_count");
     if (rc) return rc;
     cudaError_t e = scan_launch(LoadBlk{tb.bcnt}, EmitBlk{tb.boff, tb.bcur}, tb.n_max, nullptr, nullptr, tb.scan_ws, st);
     kt_point("scan_kernel");
     if (e != cudaSuccess) return set_cuda_error(e, "parent link scan");
-    k_block_scatter<<<max_ctas(8), 256, 0, st>>>(c.n_lines, c.line_cap, tb.resu, tb.rese, tb.bcur, tb.ent);
+    k_block_scatter<<<max_ctas(8), 256, 0, st>>>(c, parent_dims(cfg), tb.bcur, tb.ent);
     return check_launch("k_block_scatter");
 }
 
@@ -1438,7 +1376,7 @@ int link_resolve_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, con
     BlockLinkBufs tb;
     line_bufs(c, F, lines_ws, &cfg, g->capacity, &tb);
     // slot hash for the rare paths (overflowed faces, band candidates)
-    if ((rc = link_blockmap(g, li, cmap, c, d_n_b, lengths_cap, st))) return rc;
+    link_lookup(g, cmap, c, lengths_cap);
     if (events && events[0]) cudaEventRecord((cudaEvent_t)events[0], st);
     k_lut_blocks<<<max_ctas(5), kLutWarps * 32, 0, st>>>(parent_dims(cfg), g->d_coords, inv ? inv : tb.inv, d_n_b,
                                                          lengths_cap, tb.boff, tb.bcnt, tb.ent, lengths, g->d_status);
