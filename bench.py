@@ -122,7 +122,7 @@ def ncu_traffic(config, *kernels):
     if not os.path.exists(p):
         return None
     d = json.load(open(p)).get(config, {})
-    if "k_links_resolve" not in d:  # the capture must hold the resolution at least
+    if "k_lut_blocks" not in d:  # the capture must hold the LUT kernel at least
         return None
     # kernels absent from the capture did not run in it (e.g. no large faces
     # at C4: the warp-flattened enumeration is not launched with work)
@@ -206,39 +206,60 @@ def kernel_rooflines(kt, lv, cfg, F, n_b, stats, ops, hbm, fp32, fp64, traffic):
     Lf = len(lv) - 1
     N = [x["blocks"] for x in lv]
     nprop = cfg.n_prop
-    b_ind = F * (96 + 2)
-    b_pairs = sum(x["kept_faces"] * 104 + x["pairs"] * 8 for x in lv)
-    b_scat = sum(x["kept_faces"] * 8 + x["pairs"] * 16 for x in lv)
-    b_scan = sum(x["bins"] * 8 + F * 2 + x["kept_faces"] * 4 for x in lv)
-    b_vox = sum(x["blocks"] * 136 + x["bin_faces_of_blocks"] * 100 for x in lv)
-    b_rows = sum(n * (128 + 4) for n in N)
+    P = [x["pairs"] for x in lv]            # (bin, face) pairs per level
+    K = [x["kept_faces"] for x in lv]       # kept faces per level
+    W = [x["bin_faces_of_blocks"] for x in lv]  # pairs whose bin holds a block
+    # 1D indicators: face records read once, kept-face map entries written
+    b_ind = F * 96 + sum(K) * 4
+    # embed pairs: kept face ids + records read, (bin, face) pairs written
+    b_pairs = sum(k * 100 + p * 8 for k, p in zip(K, P))
+    # pairs -> blocks (K1) and the counting-sort scatter (K3)
+    b_pblk = sum(p * (8 + 4) + n * 4 for p, n in zip(P, N))
+    b_pscat = sum(p * (8 + 4) + w * 4 for p, w in zip(P, W))
+    # scans: block-bin offsets, row order (2), adapt child ids, tables, cut-link parents
+    parents = (cfg.nb[0] << Lf) * (cfg.nb[1] << Lf) * (cfg.nb[2] << Lf) // 8
+    b_scan = sum(n * 12 * 4 for n in N) + N[Lf] * 12 + parents * 12
+    b_vox = sum(n * 136 + w * 100 for n, w in zip(N, W))
+    # sparse rows: masks read + written, the row order (ids, rows) read; the
+    # next level's order written (ids + rows of its positions)
+    b_rows = sum(n * (128 + 4 + 16) for n in N) + sum(N[L + 1] * 8 + N[L] * 12 for L in range(Lf))
     b_mark = sum(N[L] * (27 * 4 + 27 + 1) * (nprop + 2) for L in range(Lf))
     b_adapt = sum(N[L + 1] * 304 + N[L] * 108 for L in range(Lf))
     b_bnd = N[Lf] * (27 * (4 + 8) + 64 + 64)
     lines, tests = stats["lines"], stats["tests"]
+    links = 2 * lines  # <= 2 links per recorded line (q-records)
+    # enumeration: face records read once, q-records written
     b_enum = F * 96 + lines * 16
-    b_res = lines * 16 + n_b * 27 * 64 * 4
-    b_fill = n_b * 27 * 64 * 4
+    # parent buckets: q-records read twice, parent-ordered links written
+    b_bucket = 2 * lines * 16 + links * 8 + parents * 4
+    # LUT: every slot written once (6912 B), its links read
+    b_lut = n_b * (27 * 64 * 4 + 4 + 16) + links * 8
     o = lambda k: ops.get(k, {}).get("sat_ops", 0) + ops.get(k, {}).get("other_ops", 0) if ops else None
     rows = [
         ("k_indicators_all", ["k_indicators_all"], b_ind, o("indicators"), "fp64",
-         "1D ray indicators of every level, one pass over the 96-B face records; ops: the oracle's SAT ops"),
+         "1D ray indicators of every level + per-level kept-face maps, one pass over the 96-B face records; "
+         "ops: the oracle's SAT ops"),
         ("k_pairs", ["k_pairs"], b_pairs, o("pairs"), "fp64",
-         "Alg. 2 bin pairs of every level; ops: the oracle's per-candidate SAT ops"),
-        ("scan_kernel", ["scan_kernel"], b_scan, None, None, "compactions + dense bin offsets + tables"),
-        ("k_scatter_slots", ["k_scatter_slots"], b_scat, None, None, "counting-sort scatter"),
+         "Alg. 2 bin pairs of every level (compact append); ops: the oracle's per-candidate SAT ops"),
+        ("k_pair_blocks", ["k_pair_blocks"], b_pblk, None, None, "pairs -> level-L blocks (forest descent) + counts"),
+        ("k_pair_scatter", ["k_pair_scatter"], b_pscat, None, None, "counting-sort scatter into block bins"),
+        ("scan_kernel", ["scan_kernel"], b_scan, None, None,
+         "block-bin offsets, row order, child ids, tables, cut-link parent buckets"),
         ("k_voxelize", ["k_voxelize"], b_vox, o("voxelize"), "fp64",
          "Alg. 3, every level; ops: the oracle's slab-SAT ops + 4 x 11 per accepted (row, face)"),
-        ("k_xrows", ["k_level_map", "k_xrows"], b_rows, None, None, "Alg. 5 +-x rows + finalize (+ level map)"),
+        ("k_xrows", ["k_xrows", "k_rows_children", "k_rows_init"], b_rows, None, None,
+         "Alg. 5 +-x over the sparse rows + finalize; next level's row order"),
         ("k_mark", ["k_mark_sb", "k_mark_adj", "k_mark_prop"], b_mark, None, None,
          "near-wall marking, (N_prop + 2) passes"),
         ("k_adapt", ["k_adapt_level", "k_adapt_children"], b_adapt, None, None, "refine-only adapt"),
         ("k_boundary", ["k_boundary"], b_bnd, None, None, "boundary cells (finest level)"),
-        ("k_links_enum", ["k_links_small", "k_links_enum"], b_enum, tests * 18 if tests else None, "fp32",
-         "cut-link line enumeration; ops: 18 FP32 ops per lattice line classified (3 edge functions + tests)"),
-        ("k_links_resolve", ["k_links_resolve", "k_links_band", "k_links_ovf", "k_links_full", "k_blockmap"],
-         b_res, None, None, "line records -> FP64 q -> LUT (atomicMin)"),
-        ("k_fill_lut", ["k_fill_lut"], b_fill, None, None, "LUT -1 initialisation"),
+        ("k_links_enum", ["k_links_small", "k_links_enum", "k_links_q"], b_enum, tests * 18 if tests else None,
+         "fp32", "cut-link line enumeration -> q-records (exact FP64 q); ops: 18 FP32 ops per lattice line "
+         "classified (3 edge functions + tests)"),
+        ("k_link_buckets", ["k_block_count", "k_block_scatter"], b_bucket, None, None,
+         "links bucketed by finest parent key (counts + scatter)"),
+        ("k_lut_blocks", ["k_lut_blocks", "k_links_band", "k_links_ovf", "k_links_full"], b_lut, None, None,
+         "LUT slots written once from shared memory (-1 + min-merged links); exact band / overflow paths"),
     ]
     out = []
     for name, ks, nbytes, nops, pipe, note in rows:
@@ -561,23 +582,23 @@ def main():
         kts = [eng.kernel_times() for _ in range(3)]
         kt = {k: (kts[0][k][0], med([x[k][1] for x in kts if k in x])) for k in kts[0]}
         link_stats = eng.link_stats()
-        # dominant kernel k_links (the cut-link LUT):
-        # algorithmic bytes per launch = the face records read once (96 B/face)
-        # + the LUT of the mapped blocks written once (27 x 64 x 4 = 6912 B per
-        # boundary block); the -1 initialisation is the separate k_fill_lut.
+        # the cut-link group: algorithmic bytes = the face
+        # records read once (96 B/face) + the LUT of the mapped blocks written
+        # once (27 x 64 x 4 = 6912 B per boundary block); the group's kernels
+        # write each LUT slot exactly once (no separate -1 fill)
         link_bytes = F * 96 + n_b * 27 * 64 * 4
         lk = med(link_ms)
         achieved = link_bytes / (lk / 1e3) / 1e9
         roofline = {"kernel": "cut-link group", "bound": "hbm", "achieved": achieved, "peak": peak,
                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": ncu_traffic(args.config, "k_links_small", "k_links_enum", "k_links_resolve",
-                                           "k_fill_lut"),
+                    "traffic": ncu_traffic(args.config, "k_links_small", "k_links_enum", "k_links_q",
+                                           "k_block_count", "k_block_scatter", "k_lut_blocks"),
                     "kernel_ms": lk, "algorithmic_bytes": int(link_bytes),
                     "kernel_ms_overlapped": med(link_ovl),
                     "timed": "CUDA events around the cut-link kernels run alone (vf_set_serial_links): "
-                             "the grid-independent line enumeration + the resolution after the tables + the "
-                             "LUT -1 fill (k_fill_lut, the kernel that writes the LUT's 6912 B per boundary "
-                             "block); kernel_ms_overlapped = the same events in the production schedule"}
+                             "the grid-independent line enumeration with its exact q and parent bucketing, "
+                             "then the LUT kernel after the tables (writes every slot's 6912 B once); "
+                             "kernel_ms_overlapped = the same events in the production schedule"}
     else:
         n_b = int(run()[1].n_b)
 
