@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define VF_ABI_VERSION 4
+#define VF_ABI_VERSION 5
 #define VF_MAX_LEVELS 16
 
 /* status codes (SURVEY.md §8b "Errors") */
@@ -81,6 +81,11 @@ typedef struct {
      * overflow latches VF_ECAPACITY with the required count in d_status[3]
      * (EmbedEngine re-sizes and reruns). */
     int64_t pair_cap;
+    /* cut-link line record capacity (the enumeration's piercing lines);
+     * 0 = max(2 F, 2^22).  Lines beyond it are redone by a slower exact
+     * kernel (EmbedEngine sizes it from the surface area and re-sizes after
+     * its first run); the band list holds max(2^20, line_cap / 16). */
+    int64_t line_cap;
 } vf_config;
 
 /* ForestGrid as flat device arrays, ids grouped by level:

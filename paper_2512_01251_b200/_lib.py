@@ -15,7 +15,7 @@ from .errors import (BinCapError, CapacityError, CudaError, MeshError, Voxforest
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # VF_LIB_PATH: an alternative in-tree build of the same library (A/B kernel experiments)
 LIB_PATH = os.environ.get("VF_LIB_PATH") or os.path.join(_HERE, "libvoxforest_b200.so")
-ABI_VERSION = 4
+ABI_VERSION = 5
 MAX_LEVELS = 16
 
 # cell masks / block flags / neighbour codes (voxforest_b200.h)
@@ -29,7 +29,8 @@ class VfConfig(C.Structure):
                 ("n_prop", C.c_int32), ("dx0", C.c_double), ("len", C.c_double * 3),
                 ("eps_slab", C.c_double), ("eps_parallel", C.c_double),
                 ("shard_rank", C.c_int32), ("shard_count", C.c_int32),
-                ("d_row_owner", C.c_void_p), ("pair_cap", C.c_int64)]
+                ("d_row_owner", C.c_void_p), ("pair_cap", C.c_int64),
+                ("line_cap", C.c_int64)]
 
 
 class VfGrid(C.Structure):

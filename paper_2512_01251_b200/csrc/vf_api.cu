@@ -229,7 +229,7 @@ static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *b
     t.adapt_ws = take(t.adapt_b);
     t.tab_b = tables_workspace_size(cap);
     t.tab_ws = take(t.tab_b);
-    t.link_b = link_workspace_size(cfg, Lf, cap);
+    t.link_b = link_workspace_size(cfg, Lf, cap, F);
     t.link_ws = take(t.link_b);
     t.maps = (int32_t *)take(sizeof(int32_t) * (size_t)(F + 1) * cfg.l_max);
     t.n_maps = (int32_t *)take(sizeof(int32_t) * VF_MAX_LEVELS);
@@ -426,7 +426,7 @@ int vf_link_tables(const vf_config *cfg, vf_grid *grid, const int32_t *bcount, i
 
 size_t vf_link_workspace_size(const vf_config *cfg, const vf_grid *g) {
     if (!valid_cfg(cfg) || !g) return 0;
-    return link_workspace_size(*cfg, g->n_levels - 1, g->capacity);
+    return link_workspace_size(*cfg, g->n_levels - 1, g->capacity, 0);
 }
 
 int vf_link_lengths(const vf_config *cfg, vf_grid *grid, const int32_t *cmap, const double *faces,

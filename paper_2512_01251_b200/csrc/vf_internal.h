@@ -141,7 +141,7 @@ size_t tables_workspace_size(int32_t capacity);
 // inv (nullable): slot -> block id of every mapped block
 int tables_impl(vf_grid *g, const int32_t *bcount, int32_t *cmap, int32_t *d_n_b, void *ws,
                 size_t ws_bytes, cudaStream_t st, int32_t *inv = nullptr);
-size_t link_workspace_size(const vf_config &cfg, int finest, int32_t capacity);
+size_t link_workspace_size(const vf_config &cfg, int finest, int32_t capacity, int64_t F);
 int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,
               int64_t F, const int32_t *map, const int32_t *d_n_map, float *lengths, void *ws,
               size_t ws_bytes, cudaStream_t st, void **events, const int32_t *d_n_b,

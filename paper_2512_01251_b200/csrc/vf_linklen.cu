@@ -1100,12 +1100,21 @@ __global__ void __launch_bounds__(256)
 }
 
 // workspace: dense block map of the finest level | band counters | band list
-constexpr int64_t kBandCap = 1 << 20;  // 16 MB; overflow only costs the fallback pass
-static int64_t g_band_cap = kBandCap;    // vf_set_link_band_cap (test hook)
+static int64_t g_band_cap = -1;  // vf_set_link_band_cap (test hook: a smaller cap; -1 none)
+
+static int64_t line_cap_of(const vf_config &cfg, int64_t F) {
+    if (cfg.line_cap > 0) return cfg.line_cap;
+    return F * 2 > (1 << 22) ? F * 2 : (1 << 22);
+}
+// band list: overflow only costs the fallback pass
+static int64_t band_cap_of(const vf_config &cfg, int64_t F) {
+    const int64_t b = line_cap_of(cfg, F) / 16;
+    return b > (1 << 20) ? b : (1 << 20);
+}
 
 // workspace: band counters | band list
-size_t link_workspace_size(const vf_config &, int, int32_t) {
-    return 512 + (size_t)kBandCap * sizeof(int4);
+size_t link_workspace_size(const vf_config &cfg, int, int32_t, int64_t F) {
+    return 512 + (size_t)band_cap_of(cfg, F) * sizeof(int4);
 }
 
 // LUT initialisation to -1 for the device-resident N_b slots (graph-safe:
@@ -1133,7 +1142,7 @@ int fill_lut_impl(const int32_t *d_n_b, float *lengths, int64_t cap, int32_t *d_
     return check_launch("k_fill_lut");
 }
 
-static int make_link_ctx(const vf_config &cfg, int L, const double *faces, float *lengths, void *ws,
+static int make_link_ctx(const vf_config &cfg, int L, int64_t F_band, const double *faces, float *lengths, void *ws,
                          LinkCtx &c, int &widen, LevelInfo &li) {
     li = make_level(cfg, L);
     if (li.cells[0] > 32767 || li.cells[1] > 32767 || li.cells[2] > 32767)
@@ -1145,7 +1154,8 @@ static int make_link_ctx(const vf_config &cfg, int L, const double *faces, float
     c.band = (int4 *)((char *)ws + 512);
     c.li = li;
     c.lut_cap = INT64_MAX;
-    c.band_cap = g_band_cap;
+    c.band_cap = band_cap_of(cfg, F_band);  // (F_band = 0: the SPEC-op workspace's list)
+    if (g_band_cap >= 0 && g_band_cap < c.band_cap) c.band_cap = g_band_cap;
     c.dx = li.dx;
     c.eps = li.eps;
     c.eps_par = li.eps_par;
@@ -1193,11 +1203,11 @@ int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const doubl
               size_t ws_bytes, cudaStream_t st, void **events, const int32_t *d_n_b,
               int64_t lengths_cap) {
     const int L = g->n_levels - 1;
-    if (ws_bytes < link_workspace_size(cfg, L, g->capacity)) return set_error(VF_EARG, "link workspace too small");
+    if (ws_bytes < link_workspace_size(cfg, L, g->capacity, 0)) return set_error(VF_EARG, "link workspace too small");
     LinkCtx c;
     int widen;
     LevelInfo li;
-    int rc = make_link_ctx(cfg, L, faces, lengths, ws, c, widen, li);
+    int rc = make_link_ctx(cfg, L, 0, faces, lengths, ws, c, widen, li);
     if (rc) return rc;
     cudaMemsetAsync(c.n_band, 0, 2 * sizeof(int32_t), st);
     link_lookup(g, cmap, c, lengths_cap);
@@ -1219,7 +1229,6 @@ int link_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const doubl
 // lines workspace: counters (n_lines, n_ovf, n_big) | lines | overflow face
 // list | overflow bits | big-face list (the warp-flattened enumeration)
 static size_t list_bytes(int64_t F) { return (((size_t)(F + 1) * sizeof(int32_t) + 255) & ~(size_t)255); }
-static int64_t line_cap_of(int64_t F) { return F * 2 > (1 << 22) ? F * 2 : (1 << 22); }
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 // parent buckets: level L_max - 2 coordinates of the finest level (B_L^3 / 8)
 static int3 parent_dims(const vf_config &cfg) {
@@ -1234,7 +1243,7 @@ static int64_t parents_of(const vf_config &cfg) {
 // ... | parent counts | parent offsets | parent cursors | slot -> block | scan |
 // parent-ordered links (<= 2 links per q-record)
 size_t link_lines_bytes(const vf_config &cfg, int64_t F, int32_t capacity) {
-    const int64_t cap = line_cap_of(F), nt = parents_of(cfg);
+    const int64_t cap = line_cap_of(cfg, F), nt = parents_of(cfg);
     return 256 + (size_t)cap * sizeof(int4) + 2 * list_bytes(F) +
            al256(((size_t)F + 32) / 32 * sizeof(uint32_t)) + 3 * al256((size_t)nt * sizeof(int32_t)) +
            al256((size_t)capacity * sizeof(int32_t)) +
@@ -1248,9 +1257,9 @@ struct BlockLinkBufs {
     int64_t n_max;
 };
 
-static int32_t *line_bufs(LinkCtx &c, int64_t F, void *lines_ws, const vf_config *cfg = nullptr, int32_t capacity = 0,
+static int32_t *line_bufs(LinkCtx &c, const vf_config &cfg, int64_t F, void *lines_ws, int32_t capacity = 0,
                           BlockLinkBufs *tb = nullptr) {
-    c.line_cap = line_cap_of(F);
+    c.line_cap = line_cap_of(cfg, F);
     c.n_lines = (int32_t *)lines_ws;
     c.n_ovf = c.n_lines + 1;
     c.n_tests = (unsigned long long *)((char *)lines_ws + 16);
@@ -1259,7 +1268,7 @@ static int32_t *line_bufs(LinkCtx &c, int64_t F, void *lines_ws, const vf_config
     c.ovf_bits = (uint32_t *)((char *)c.ovf_list + list_bytes(F));
     int32_t *big = (int32_t *)((char *)c.ovf_bits + al256(((size_t)F + 32) / 32 * sizeof(uint32_t)));
     if (tb) {
-        const int64_t nt = parents_of(*cfg);
+        const int64_t nt = parents_of(cfg);
         char *p = (char *)big + list_bytes(F);
         tb->n_max = nt;
         tb->bcnt = (int32_t *)p;
@@ -1280,9 +1289,9 @@ int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *w
     LinkCtx c;
     int widen;
     LevelInfo li;
-    int rc = make_link_ctx(cfg, cfg.l_max - 1, faces, nullptr, ws, c, widen, li);
+    int rc = make_link_ctx(cfg, cfg.l_max - 1, F, faces, nullptr, ws, c, widen, li);
     if (rc) return rc;
-    int32_t *big = line_bufs(c, F, lines_ws);
+    int32_t *big = line_bufs(c, cfg, F, lines_ws);
     cudaMemsetAsync(c.n_band, 0, 2 * sizeof(int32_t), st);
     cudaMemsetAsync(c.n_lines, 0, 24, st);  // n_lines, n_ovf, n_big, (pad), n_tests
     cudaMemsetAsync(c.ovf_bits, 0, ((size_t)F + 32) / 32 * sizeof(uint32_t), st);
@@ -1317,9 +1326,9 @@ int link_stats(const vf_config &cfg, int64_t F, void *ws, void *lines_ws, int64_
     LinkCtx c;
     int widen;
     LevelInfo li;
-    int rc = make_link_ctx(cfg, cfg.l_max - 1, nullptr, nullptr, ws, c, widen, li);
+    int rc = make_link_ctx(cfg, cfg.l_max - 1, F, nullptr, nullptr, ws, c, widen, li);
     if (rc) return rc;
-    line_bufs(c, F, lines_ws);
+    line_bufs(c, cfg, F, lines_ws);
     int32_t a[3] = {0, 0, 0}, b[2] = {0, 0};
     cudaError_t e = cudaMemcpy(a, c.n_lines, sizeof(a), cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(b, c.n_band, sizeof(b), cudaMemcpyDeviceToHost);
@@ -1342,7 +1351,7 @@ int link_stats(const vf_config &cfg, int64_t F, void *ws, void *lines_ws, int64_
 static int link_bucket(const vf_config &cfg, LinkCtx &c, int64_t F, void *lines_ws, int32_t capacity,
                        cudaStream_t st) {
     BlockLinkBufs tb;
-    line_bufs(c, F, lines_ws, &cfg, capacity, &tb);
+    line_bufs(c, cfg, F, lines_ws, capacity, &tb);
     cudaMemsetAsync(tb.bcnt, 0, sizeof(int32_t) * (size_t)tb.n_max, st);
     kt_point("memset:parent_counts");
     k_block_count<<<max_ctas(8), 256, 0, st>>>(c, parent_dims(cfg), tb.bcnt);
@@ -1360,7 +1369,7 @@ int32_t *link_slot_inverse(const vf_config &cfg, int64_t F, void *lines_ws, int3
     LinkCtx c;
     memset(&c, 0, sizeof(c));
     BlockLinkBufs tb;
-    line_bufs(c, F, lines_ws, &cfg, capacity, &tb);
+    line_bufs(c, cfg, F, lines_ws, capacity, &tb);
     return tb.inv;
 }
 
@@ -1371,10 +1380,10 @@ int link_resolve_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, con
     int widen;
     LevelInfo li;
     if (g->n_levels != cfg.l_max) return set_error(VF_EARG, "link resolve: the grid must reach L_max");
-    int rc = make_link_ctx(cfg, cfg.l_max - 1, faces, lengths, ws, c, widen, li);
+    int rc = make_link_ctx(cfg, cfg.l_max - 1, F, faces, lengths, ws, c, widen, li);
     if (rc) return rc;
     BlockLinkBufs tb;
-    line_bufs(c, F, lines_ws, &cfg, g->capacity, &tb);
+    line_bufs(c, cfg, F, lines_ws, g->capacity, &tb);
     // slot hash for the rare paths (overflowed faces, band candidates)
     link_lookup(g, cmap, c, lengths_cap);
     if (events && events[0]) cudaEventRecord((cudaEvent_t)events[0], st);
@@ -1402,6 +1411,6 @@ extern "C" float vf_set_link_small_ext(float e) {
 
 extern "C" int64_t vf_set_link_band_cap(int64_t n) {
     const int64_t old = vf::g_band_cap;
-    if (n >= 0) vf::g_band_cap = n < vf::kBandCap ? n : vf::kBandCap;
+    if (n >= -1) vf::g_band_cap = n;
     return old;
 }

@@ -193,6 +193,11 @@ class EmbedEngine:
         cap = int(capacity if capacity is not None else cfg.block_capacity(self.mesh.area))
         self.grid = ForestGrid.allocate(cfg, cap)
         self.c = _lib.make_config(cfg)
+        # cut-link line records: ~9 piercing lines per finest cell area of
+        # surface over the 13 direction pairs (measured on the torus meshes);
+        # re-sized after the first run if they overflow
+        dxf = cfg.dx(cfg.l_max - 1)
+        self.c.line_cap = max(2 * self.mesh.n_faces, int(12 * self.mesh.area / (dxf * dxf)), 1 << 22)
         wsb = self.lib.vf_embed_workspace_size(C.byref(self.c), self.mesh.n_faces, cap)
         if wsb == 0:
             raise ValueError("invalid embed configuration")
@@ -262,13 +267,29 @@ class EmbedEngine:
         if int(self.host[0]) != 2 or need <= 0:
             return False
         self.c.pair_cap = int(need * 1.25) + 65536
+        self._realloc_ws()
+        return True
+
+    def _grow_lines(self) -> bool:
+        """After a phase 1: if the cut-link line records or the band list
+        overflowed (correct, but redone by the slow exact kernels), enlarge
+        them and the workspace; True = rerun."""
+        st = self.link_stats()
+        need = max(st["lines"], 16 * st["band"])
+        if need <= st["line_cap"] and st["band"] <= st["band_cap"]:
+            return False
+        self.c.line_cap = int(need * 1.25) + 65536
+        self._realloc_ws()
+        return True
+
+    def _realloc_ws(self):
+        import torch
         wsb = self.lib.vf_embed_workspace_size(C.byref(self.c), self.mesh.n_faces, self.grid.capacity)
         self.ws = None
         self.ws = torch.empty(int(wsb), dtype=torch.uint8, device="cuda")
         for g in self._graphs.values():
             self.lib.vf_graph_destroy(g)
         self._graphs.clear()
-        return True
 
     def _finish(self, st_obj):
         """Async read of status + N_b, one sync, error mapping."""
@@ -303,6 +324,8 @@ class EmbedEngine:
                     if self._grow_pairs():
                         continue
                     n_b = self._finish(self.stream)
+                    if self._grow_lines():
+                        continue
                     break
                 self._alloc_lut(n_b)
             if timed or not self.use_graph:
