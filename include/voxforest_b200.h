@@ -127,6 +127,11 @@ int         vf_abi_version(void);
 void       *vf_ctx_create(int device, void *nccl_comm);
 int         vf_ctx_destroy(void *ctx);
 int         vf_ctx_device(const void *ctx);
+/* NCCL communicator created by the library: rank 0 calls vf_nccl_unique_id
+ * (128 bytes), the caller shares the bytes (torch.distributed broadcast) and
+ * every rank calls vf_ctx_create_nccl.  NULL on error (vf_last_error). */
+int         vf_nccl_unique_id(void *out, int out_bytes);
+void       *vf_ctx_create_nccl(int device, int nranks, int rank, const void *unique_id);
 const char *vf_last_error(void);
 int         vf_device_info(int *sm_count, int *cc_major, int *cc_minor);
 
@@ -298,6 +303,14 @@ int vf_shard_refine(const vf_config *cfg, vf_grid *grid, int level, void *d_ws,
 /* finest level: boundary cells of owned blocks (counts -> d_bcount, zeroed
  * for unowned blocks) */
 int vf_shard_boundary(const vf_config *cfg, vf_grid *grid, int32_t *d_bcount, void *stream);
+/* native sharded embed through the tables: every level above with the
+ * block-flag all-reduce (MAX) on ctx's NCCL communicator, then the finest
+ * level's SOLID-mask and boundary-count all-reduces and the replicated
+ * tables; stream-ordered, no host sync (graph-capturable).  ctx from
+ * vf_ctx_create_nccl or vf_ctx_create with the caller's ncclComm_t. */
+int vf_shard_embed_phase1(void *ctx, const vf_config *cfg, const double *d_faces, int64_t n_faces,
+                          int use_filter, vf_grid *grid, int32_t *d_bcount, int32_t *d_cmap,
+                          int32_t *d_n_b, void *d_ws, size_t ws_bytes, void *stream);
 /* cut-link LUT slots of the owned blocks: LUT init (-1), faces near owned
  * rows, k_links on them (the LUT stays distributed) */
 int vf_shard_links(const vf_config *cfg, const double *d_faces, int64_t n_faces,

@@ -57,6 +57,9 @@ _SIGS = {
     "vf_ctx_create": (_P, [_I32, _P]),
     "vf_ctx_destroy": (_I32, [_P]),
     "vf_ctx_device": (_I32, [_P]),
+    "vf_nccl_unique_id": (_I32, [_P, _I32]),
+    "vf_ctx_create_nccl": (_P, [_I32, _I32, _I32, _P]),
+    "vf_shard_embed_phase1": (_I32, [_P, _CP, _P, _I64, _I32, _GP, _P, _P, _P, _P, _SZ, _P]),
     "vf_last_error": (C.c_char_p, []),
     "vf_device_info": (_I32, [C.POINTER(C.c_int)] * 3),
     "vf_pack_faces": (_I32, [_P, _P, _I64, _P, _P]),

@@ -15,6 +15,8 @@
 #include "vf_internal.h"
 #include "vf_scan.cuh"
 
+#include <nccl.h>
+
 namespace vf {
 
 static thread_local char g_err[512] = "";
@@ -489,13 +491,15 @@ static int side_stream(SideStream **out) {
 
 // Per-device context (SURVEY.md §8b vf_ctx_create): selects the device,
 // creates its side streams / events (otherwise created on first use) and
-// records the caller's NCCL communicator.  The library never calls NCCL
-// itself: the multi-GPU exchanges are flag all-reduces issued by the caller
-// (parallel.py over torch.distributed) between the sharded stage calls; the
-// handle is carried for callers that keep it with the device state.
+// holds the NCCL communicator of the block-sharded embed: the caller's
+// (vf_ctx_create) or one the library creates from a unique id the ranks
+// share (vf_ctx_create_nccl; parallel.py broadcasts it over
+// torch.distributed).  vf_shard_embed_phase1 issues the per-level flag
+// exchanges on it, in stream order, with no host synchronisation.
 struct vf_ctx_s {
     int device;
     void *nccl_comm;
+    int own_comm;  // created here (destroyed with the context)
 };
 
 extern "C" void *vf_ctx_create(int device, void *nccl_comm) {
@@ -506,8 +510,38 @@ extern "C" void *vf_ctx_create(int device, void *nccl_comm) {
     }
     SideStream *side = nullptr;
     if (side_stream(&side) != VF_OK) return nullptr;
-    vf_ctx_s *c = new (std::nothrow) vf_ctx_s{device, nccl_comm};
+    vf_ctx_s *c = new (std::nothrow) vf_ctx_s{device, nccl_comm, 0};
     if (!c) set_error(VF_EARG, "vf_ctx_create: out of host memory");
+    return c;
+}
+
+extern "C" int vf_nccl_unique_id(void *out, int out_bytes) {
+    if (!out || out_bytes < (int)sizeof(ncclUniqueId)) return set_error(VF_EARG, "vf_nccl_unique_id: bad argument");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return set_error(VF_ENCCL, ncclGetErrorString(r));
+    memcpy(out, &id, sizeof(id));
+    return VF_OK;
+}
+
+extern "C" void *vf_ctx_create_nccl(int device, int nranks, int rank, const void *unique_id) {
+    if (!unique_id || nranks < 1 || rank < 0 || rank >= nranks) {
+        set_error(VF_EARG, "vf_ctx_create_nccl: bad argument");
+        return nullptr;
+    }
+    vf_ctx_s *c = static_cast<vf_ctx_s *>(vf_ctx_create(device, nullptr));
+    if (!c) return nullptr;
+    ncclUniqueId id;
+    memcpy(&id, unique_id, sizeof(id));
+    ncclComm_t comm = nullptr;
+    const ncclResult_t r = ncclCommInitRank(&comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        set_error(VF_ENCCL, ncclGetErrorString(r));
+        delete c;
+        return nullptr;
+    }
+    c->nccl_comm = comm;
+    c->own_comm = 1;
     return c;
 }
 
@@ -531,6 +565,7 @@ extern "C" int vf_ctx_destroy(void *ctx) {
         cudaStreamDestroy(s.st4);
         s = SideStream();
     }
+    if (c->own_comm && c->nccl_comm) ncclCommDestroy((ncclComm_t)c->nccl_comm);
     cudaSetDevice(cur);
     delete c;
     return e == cudaSuccess ? VF_OK : set_cuda_error(e, "vf_ctx_destroy");
@@ -815,14 +850,68 @@ int vf_shard_links(const vf_config *cfg, const double *faces, int64_t F, vf_grid
                    const int32_t *cmap, const int32_t *d_n_b, float *lengths, int64_t lengths_cap,
                    void *ws, size_t ws_bytes, void *stream) {
     EmbedWs w;
-    if (!faces || F <= 0 || !cmap || !d_n_b || !lengths || lengths_cap < 1 ||
-        !shard_args(cfg, g, ws, ws_bytes, F, &w))
+    // (shard_count 1: the native driver on a 1-rank communicator -- all faces)
+    if (!faces || F <= 0 || !cmap || !d_n_b || !lengths || lengths_cap < 1 || !valid_cfg(cfg) || !g ||
+        (cfg->shard_count > 1 && !cfg->d_row_owner) || embed_layout(*cfg, F, g->capacity, (char *)ws, &w) > ws_bytes)
         return set_error(VF_EARG, "vf_shard_links: bad argument");
     cudaStream_t st = (cudaStream_t)stream;
     VF_TRY(fill_lut_impl(d_n_b, lengths, lengths_cap, g->d_status, st));
-    VF_TRY(shard_face_subset_impl(*cfg, faces, F, w.map[0], w.n_map[0], w.shard_ws, st));
-    return link_impl(*cfg, g, cmap, faces, F, w.map[0], w.n_map[0], lengths, w.link_ws,
-                     w.link_b, st, nullptr, d_n_b, lengths_cap);
+    const bool sub = cfg->shard_count > 1;
+    if (sub) VF_TRY(shard_face_subset_impl(*cfg, faces, F, w.map[0], w.n_map[0], w.shard_ws, st));
+    return link_impl(*cfg, g, cmap, faces, F, sub ? w.map[0] : nullptr, sub ? w.n_map[0] : nullptr, lengths,
+                     w.link_ws, w.link_b, st, nullptr, d_n_b, lengths_cap);
+}
+
+// Native block-sharded embed through the tables, one call
+// per rank, exchanges on the context's NCCL communicator in stream order: no
+// host synchronisation, graph-capturable.  Per level: this rank's bins /
+// voxelization / Alg. 5 rows, non-owned flags zeroed, then ONE all-reduce
+// (MAX) of the block flags; mark + adapt + row order + next owner map
+// replicated.  Finest level: all-reduce (MAX) of the owner-zeroed SOLID
+// masks (boundary halo), boundary cells of owned blocks, all-reduce (MAX) of
+// the owner-zeroed boundary counts, replicated tables (the global
+// contraction map).  The all-reduces span the grid capacity: entries outside
+// the level are identical on every rank (replicated or zero), so MAX leaves
+// them unchanged, and no host-side level size is needed.  The cut links of
+// owned blocks follow with vf_shard_links once the LUT is sized.
+int vf_shard_embed_phase1(void *ctx, const vf_config *cfg, const double *faces, int64_t F, int use_filter,
+                          vf_grid *g, int32_t *bcount, int32_t *cmap, int32_t *d_n_b, void *ws, size_t ws_bytes,
+                          void *stream) {
+    EmbedWs w;
+    vf_ctx_s *cx = static_cast<vf_ctx_s *>(ctx);
+    // (shard_count 1: a 1-rank communicator, every row owned)
+    if (!cx || !cx->nccl_comm || !faces || F <= 0 || !bcount || !cmap || !d_n_b || !valid_cfg(cfg) || !g ||
+        (cfg->shard_count > 1 && !cfg->d_row_owner) || embed_layout(*cfg, F, g->capacity, (char *)ws, &w) > ws_bytes)
+        return set_error(VF_EARG, "vf_shard_embed_phase1: bad argument");
+    ncclComm_t comm = (ncclComm_t)cx->nccl_comm;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t cap = (size_t)g->capacity;
+    auto allmax = [&](void *buf, size_t n, ncclDataType_t ty) -> int {
+        const ncclResult_t r = ncclAllReduce(buf, buf, n, ty, ncclMax, comm, st);
+        return r == ncclSuccess ? VF_OK : set_error(VF_ENCCL, ncclGetErrorString(r));
+    };
+    VF_TRY(init_forest_impl(*cfg, g, st));
+    VF_TRY(rows_init_impl(*cfg, g, w.prop_ws, st));
+    VF_TRY(shard_owner_map_impl(*cfg, g, 0, w.shard_ws, st));
+    cudaMemsetAsync(w.bb.cnt, 0, sizeof(int32_t) * cap, st);
+    for (int L = 0; L < cfg->l_max; ++L) {
+        const LevelInfo li = make_level(*cfg, L);
+        VF_TRY(level_pairs(*cfg, li, faces, F, use_filter, false, w, 0, g->d_status, st));
+        VF_TRY(block_bins_impl(li, L, g, w.pairs[0], w.n_pairs[0], w.pair_cap, w.bb, st));
+        VF_TRY(voxelize_blocks_impl(li, g, L, w.bb, faces, true, st));
+        VF_TRY(propagate_rows_impl(li, g, L, w.prop_ws, st));
+        VF_TRY(shard_zero_impl(li, g, L, nullptr, st));
+        VF_TRY(allmax(g->d_bflags, cap, ncclUint8));  // the level's block flags, 1 B/block
+        if (L == cfg->l_max - 1) break;
+        VF_TRY(mark_impl(*cfg, g, L, w.mark_ws, w.mark_b, st));
+        VF_TRY(adapt_impl(*cfg, g, L, w.adapt_ws, w.adapt_b, st));
+        VF_TRY(rows_next_impl(g, L, w.prop_ws, st));
+        VF_TRY(shard_owner_map_impl(*cfg, g, L + 1, w.shard_ws, st));
+    }
+    VF_TRY(allmax(g->d_solid64, cap, ncclUint64));  // SOLID-cell masks for the boundary halo
+    VF_TRY(boundary_impl(*cfg, g, bcount, st));
+    VF_TRY(allmax(bcount, cap, ncclInt32));  // boundary counts: the global contraction map
+    return tables_impl(g, bcount, cmap, d_n_b, w.tab_ws, w.tab_b, st);
 }
 
 int vf_ktimer_start(void *stream, double gate_us) {

@@ -30,6 +30,16 @@ consumes it.
 
 Results on owned data are bit-identical to the single-GPU embed
 (tests/test_gpu_sharded.py); topology and flags are identical on every rank.
+
+Two drivers run this schedule:
+  * ``NcclShardedEmbed`` -- the NATIVE one: ``vf_shard_embed_phase1`` runs every
+    level and issues the exchanges itself on the library's NCCL communicator
+    (MAX all-reduces over owner-zeroed arrays, stream-ordered, no host sync,
+    graph-capturable); used when the process group's backend is NCCL;
+  * ``ShardedEmbed`` over any torch.distributed backend (the stage calls with
+    ``dist.all_reduce`` between them); on an NCCL group it delegates to the
+    native driver, on gloo (CPU tests, several ranks sharing one GPU) it runs
+    the exchanges from Python.
 """
 from __future__ import annotations
 
@@ -71,10 +81,117 @@ def owner_zero_allreduce(t, owned_mask, op, group=None):
     return t
 
 
-class ShardedEmbed:
-    """embed_geometry split across the ranks of a process group."""
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it, the ranks share it)."""
+    lib = _lib.require_cuda()
+    buf = (C.c_char * 128)()
+    _lib.check(lib.vf_nccl_unique_id(buf, 128), "vf_nccl_unique_id")
+    return bytes(buf)
 
-    def __init__(self, mesh, cfg: EmbedConfig, group=None, capacity: Optional[int] = None):
+
+class NcclShardedEmbed:
+    """Native block-sharded embed of one rank: the library's NCCL
+    communicator (``vf_ctx_create_nccl``) carries the per-level exchanges
+    inside ``vf_shard_embed_phase1`` (no host synchronisation until the LUT
+    is sized), then ``vf_shard_links`` fills the LUT slots of owned blocks."""
+
+    def __init__(self, mesh, cfg: EmbedConfig, rank: int, world: int, unique_id: bytes,
+                 capacity: Optional[int] = None):
+        import torch
+        self.torch = torch
+        self.lib = _lib.require_cuda()
+        self.rank, self.world = int(rank), int(world)
+        self.cfg = cfg
+        self.mesh = as_device_mesh(mesh)
+        cap = int(capacity if capacity is not None else cfg.block_capacity(self.mesh.area))
+        self.grid = ForestGrid.allocate(cfg, cap)
+        self.c = _lib.make_config(cfg, shard=(self.rank, self.world))
+        nown = self.lib.vf_shard_owner_bytes(C.byref(self.c))
+        self.row_owner = torch.zeros(max(int(nown), 1), dtype=torch.uint8, device="cuda")
+        self.c.d_row_owner = self.row_owner.data_ptr()
+        wsb = self.lib.vf_embed_workspace_size(C.byref(self.c), self.mesh.n_faces, cap)
+        if wsb == 0:
+            raise ValueError("invalid embed configuration")
+        self.ws = torch.empty(int(wsb), dtype=torch.uint8, device="cuda")
+        self.bcount = torch.empty(cap, dtype=torch.int32, device="cuda")
+        self.cmap = torch.empty(cap, dtype=torch.int32, device="cuda")
+        self.nb_dev = torch.zeros(1, dtype=torch.int32, device="cuda")
+        uid = (C.c_char * 128).from_buffer_copy(unique_id)
+        self.ctx = self.lib.vf_ctx_create_nccl(torch.cuda.current_device(), self.world, self.rank, uid)
+        if not self.ctx:
+            raise _lib.CudaError(f"vf_ctx_create_nccl: {_lib.last_error()}")
+        self.lengths = None
+        self.bc_ids = None
+        # bytes all-reduced per embed: L_max x capacity flags + 8 B SOLID
+        # masks + 4 B boundary counts per block of capacity
+        self.comm_bytes = cap * (cfg.l_max + 8 + 4)
+
+    def __del__(self):
+        try:
+            if self.ctx:
+                self.lib.vf_ctx_destroy(self.ctx)
+        except Exception:
+            pass
+
+    def phase1(self, use_filter: Optional[bool] = None, stream=None):
+        """Every level + exchanges + tables, enqueued on ``stream`` (no sync)."""
+        g, c = self.grid, self.c
+        uf = int(bool(self.cfg.use_filter if use_filter is None else use_filter))
+        g.status.zero_()
+        gs = g._struct()
+        _lib.check(self.lib.vf_shard_embed_phase1(
+            self.ctx, C.byref(c), _lib.ptr(self.mesh.faces), self.mesh.n_faces, uf, C.byref(gs),
+            _lib.ptr(self.bcount), _lib.ptr(self.cmap), _lib.ptr(self.nb_dev), _lib.ptr(self.ws),
+            self.ws.numel(), _lib.stream_ptr(stream)), "embed_geometry (native sharded)")
+        g.n_levels = self.cfg.l_max
+        return gs
+
+    def run(self, use_filter: Optional[bool] = None):
+        torch, lib, g, c = self.torch, self.lib, self.grid, self.c
+        gs = self.phase1(use_filter)
+        st = _lib.stream_ptr()
+        _lib.check(lib.vf_check_status(C.byref(gs), st), "embed_geometry (native sharded)")
+        n_b = int(self.nb_dev.item())
+        if self.lengths is None or self.lengths.shape[0] < n_b:
+            cap = int(n_b * 1.25) + 16
+            self.lengths = torch.empty((cap, 27, 64), dtype=torch.float32, device="cuda")
+            self.bc_ids = torch.zeros((cap, 27, 64), dtype=torch.int8, device="cuda")
+        _lib.check(lib.vf_shard_links(C.byref(c), _lib.ptr(self.mesh.faces), self.mesh.n_faces, C.byref(gs),
+                                      _lib.ptr(self.cmap), _lib.ptr(self.nb_dev), _lib.ptr(self.lengths),
+                                      self.lengths.shape[0], _lib.ptr(self.ws), self.ws.numel(), st),
+                   "link lengths")
+        _lib.check(lib.vf_check_status(C.byref(gs), st), "embed_geometry (native sharded links)")
+        return g, LinkTable(self.lengths[:n_b], self.bc_ids[:n_b], self.cmap[:g.n_used], n_b)
+
+    def owned_blocks(self, L: int):
+        s, e = self.grid.level_range(L)
+        co = self.grid.coords[s:e].long()
+        by = self.cfg.bins(L)[1]
+        base = sum(self.cfg.bins(l)[1] * self.cfg.bins(l)[2] for l in range(L))
+        return self.row_owner[base + co[:, 1] + by * co[:, 2]] == self.rank
+
+    def cells_classified(self) -> int:
+        return 64 * self.grid.n_used
+
+
+class ShardedEmbed:
+    """embed_geometry split across the ranks of a process group (NCCL group:
+    the native driver; other backends: Python-driven exchanges)."""
+
+    def __new__(cls, mesh, cfg: EmbedConfig, group=None, capacity: Optional[int] = None,
+                native: Optional[bool] = None):
+        import torch.distributed as dist
+        if native is None:
+            native = dist.get_backend(group) == "nccl"
+        if not native:
+            return super().__new__(cls)
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return NcclShardedEmbed(mesh, cfg, rank, world, obj[0], capacity)
+
+    def __init__(self, mesh, cfg: EmbedConfig, group=None, capacity: Optional[int] = None,
+                 native: Optional[bool] = None):
         import torch
         import torch.distributed as dist
         self.torch = torch

@@ -113,3 +113,50 @@ def test_sharded_embed_matches_single_gpu(world):
     for r in res:
         assert r[1] == [], r
     assert all(r[3] > 0 for r in res)  # every rank owns LUT slots
+
+
+def test_native_nccl_single_rank():
+    """The native driver (vf_shard_embed_phase1: the exchanges on the
+    library's NCCL communicator, no host sync) on a 1-rank communicator --
+    the only NCCL world one GPU allows -- equals the single-GPU embed
+    bitwise, eager and replayed from a CUDA graph of phase 1."""
+    from paper_2512_01251_b200 import EmbedConfig, make_torus
+    from paper_2512_01251_b200.mesh import translate
+    from paper_2512_01251_b200.parallel import NcclShardedEmbed, nccl_unique_id
+    from paper_2512_01251_b200.voxelizer import EmbedEngine
+    mesh = translate(make_torus(120, 60), (0.0031, -0.0017, 0.0023))
+    cfg = EmbedConfig(n_x=32, l_max=4)
+    ref_g, ref_t = EmbedEngine(mesh, cfg, use_graph=False).run()
+    R = ref_g.to_numpy()
+    sh = NcclShardedEmbed(mesh, cfg, 0, 1, nccl_unique_id(), capacity=ref_g.capacity)
+    g, t = sh.run()
+
+    def check(g, t):
+        G = g.to_numpy()
+        assert np.array_equal(G["level_start"], R["level_start"])
+        for k in ("coords", "nbr", "nbr_child", "child", "bflags", "masks"):
+            assert np.array_equal(G[k][:ref_g.n_used], R[k][:ref_g.n_used]), k
+        assert t.n_b == ref_t.n_b
+        assert np.array_equal(t.contraction_map.cpu().numpy(), ref_t.contraction_map.cpu().numpy()[:ref_g.n_used])
+        assert np.array_equal(t.lengths.cpu().numpy(), ref_t.lengths.cpu().numpy())
+
+    check(g, t)
+    # phase 1 captured into a CUDA graph (kernels + NCCL all-reduces) and replayed
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        sh.phase1()  # warm-up on the capture stream
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            sh.phase1(stream=s)
+    torch.cuda.current_stream().wait_stream(s)
+    sh.grid.masks.zero_()
+    sh.grid.bflags.zero_()
+    sh.cmap.fill_(-7)
+    graph.replay()
+    torch.cuda.synchronize()
+    G = sh.grid.to_numpy()
+    for k in ("coords", "nbr", "nbr_child", "child", "bflags", "masks"):
+        assert np.array_equal(G[k][:ref_g.n_used], R[k][:ref_g.n_used]), k
+    assert int(sh.nb_dev.item()) == ref_t.n_b
+    assert np.array_equal(sh.cmap.cpu().numpy()[:ref_g.n_used], ref_t.contraction_map.cpu().numpy()[:ref_g.n_used])
