@@ -854,12 +854,17 @@ int vf_shard_links(const vf_config *cfg, const double *faces, int64_t F, vf_grid
     if (!faces || F <= 0 || !cmap || !d_n_b || !lengths || lengths_cap < 1 || !valid_cfg(cfg) || !g ||
         (cfg->shard_count > 1 && !cfg->d_row_owner) || embed_layout(*cfg, F, g->capacity, (char *)ws, &w) > ws_bytes)
         return set_error(VF_EARG, "vf_shard_links: bad argument");
+    // the single-GPU cut-link pipeline on the faces near owned rows: line
+    // enumeration -> q-records -> parent buckets, then the LUT slots of owned
+    // blocks (other ranks' slots -1)
     cudaStream_t st = (cudaStream_t)stream;
-    VF_TRY(fill_lut_impl(d_n_b, lengths, lengths_cap, g->d_status, st));
     const bool sub = cfg->shard_count > 1;
     if (sub) VF_TRY(shard_face_subset_impl(*cfg, faces, F, w.map[0], w.n_map[0], w.shard_ws, st));
-    return link_impl(*cfg, g, cmap, faces, F, sub ? w.map[0] : nullptr, sub ? w.n_map[0] : nullptr, lengths,
-                     w.link_ws, w.link_b, st, nullptr, d_n_b, lengths_cap);
+    VF_TRY(link_enum_impl(*cfg, faces, F, w.link_ws, w.lines_ws, g->capacity, st, nullptr,
+                          sub ? w.map[0] : nullptr, sub ? w.n_map[0] : nullptr));
+    VF_TRY(link_inverse_impl(*cfg, g, cmap, d_n_b, lengths_cap, F, w.lines_ws, st));
+    return link_resolve_impl(*cfg, g, cmap, faces, F, lengths, w.link_ws, w.lines_ws, st, nullptr, d_n_b,
+                             lengths_cap);
 }
 
 // Native block-sharded embed through the tables, one call
@@ -894,9 +899,17 @@ int vf_shard_embed_phase1(void *ctx, const vf_config *cfg, const double *faces, 
     VF_TRY(rows_init_impl(*cfg, g, w.prop_ws, st));
     VF_TRY(shard_owner_map_impl(*cfg, g, 0, w.shard_ws, st));
     cudaMemsetAsync(w.bb.cnt, 0, sizeof(int32_t) * cap, st);
+    // 1D indicators of every level in one face pass, unfiltered by ownership
+    // (future levels' owners are not known yet); the pairs keep owned bins only
+    const bool pre = use_filter && cfg->l_max <= 8;
+    if (pre) {
+        vf_config c1 = *cfg;
+        c1.shard_count = 1;
+        VF_TRY(launch_indicators_all(c1, faces, F, nullptr, w.maps, F + 1, w.n_maps, st));
+    }
     for (int L = 0; L < cfg->l_max; ++L) {
         const LevelInfo li = make_level(*cfg, L);
-        VF_TRY(level_pairs(*cfg, li, faces, F, use_filter, false, w, 0, g->d_status, st));
+        VF_TRY(level_pairs(*cfg, li, faces, F, use_filter, pre, w, 0, g->d_status, st));
         VF_TRY(block_bins_impl(li, L, g, w.pairs[0], w.n_pairs[0], w.pair_cap, w.bb, st));
         VF_TRY(voxelize_blocks_impl(li, g, L, w.bb, faces, true, st));
         VF_TRY(propagate_rows_impl(li, g, L, w.prop_ws, st));

@@ -158,7 +158,10 @@ size_t link_lines_bytes(const vf_config &cfg, int64_t F, int32_t capacity);
 const void *link_enum_kernel(int small);  // graph node priorities
 int link_stats(const vf_config &cfg, int64_t F, void *ws, void *lines_ws, int64_t out[7]);
 int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *ws, void *lines_ws,
-                   int32_t capacity, cudaStream_t st, void **events);
+                   int32_t capacity, cudaStream_t st, void **events, const int32_t *map = nullptr,
+                   const int32_t *d_n_map = nullptr);
+int link_inverse_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const int32_t *d_n_b, int64_t cap,
+                      int64_t F, void *lines_ws, cudaStream_t st);
 // inv: slot -> finest block (tables_impl's inverse output; nullptr: the
 // lines workspace's copy, link_slot_inverse)
 int link_resolve_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const double *faces,

@@ -765,16 +765,18 @@ __device__ __forceinline__ int4 qrec_convert(const LinkCtx &c, const int4 rec);
 
 __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
     k_links_small(LinkCtx c, int widen, int64_t F, float small_ext, int32_t *__restrict__ big,
-                  int32_t *__restrict__ n_big) {
+                  int32_t *__restrict__ n_big, const int32_t *__restrict__ map,
+                  const int32_t *__restrict__ d_n_map) {
     __shared__ int4 s_rec[kLineStage];
     __shared__ int s_n, s_base;
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
     const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    bool act = m < F;
+    // (map: a face subset -- the sharded embed's faces near owned rows)
+    bool act = m < (d_n_map ? (int64_t)*d_n_map : F);
     SmallFace S;
-    S.f = (int)m;
+    S.f = act && map ? map[m] : (int)m;
     double v[9], flo[3] = {0.0, 0.0, 0.0}, fhi[3] = {0.0, 0.0, 0.0};
     float extL = 0.0f;
     bool small = false;
@@ -1045,7 +1047,7 @@ struct EmitBlk {
 // (the LUT stays unwritten), as the -1 fill did
 constexpr int kLutWarps = 6;  // 6 x 6912 B of static shared memory
 __global__ void __launch_bounds__(kLutWarps * 32)
-    k_lut_blocks(int3 pdim, const int32_t *__restrict__ coords, const int32_t *__restrict__ inv,
+    k_lut_blocks(LevelInfo li, int3 pdim, const int32_t *__restrict__ coords, const int32_t *__restrict__ inv,
                  const int32_t *__restrict__ d_n_b, int64_t cap, const int32_t *__restrict__ boff,
                  const int32_t *__restrict__ bcnt, const unsigned long long *__restrict__ ent,
                  float *__restrict__ lengths, int32_t *__restrict__ status) {
@@ -1065,6 +1067,9 @@ __global__ void __launch_bounds__(kLutWarps * 32)
         const int4 co = reinterpret_cast<const int4 *>(coords)[inv[slot]];
         const int32_t key = (co.x >> 1) + pdim.x * ((co.y >> 1) + pdim.y * (co.z >> 1));
         const uint32_t oct = (uint32_t)((co.x & 1) + 2 * (co.y & 1) + 4 * (co.z & 1));
+        // multi-GPU: the LUT is distributed -- a rank writes the slots of
+        // the blocks it owns (another rank's slots are left to their owner)
+        if (!owns_row(li, co.y, co.z)) continue;
         const int32_t e0 = boff[key], ne = bcnt[key];
         for (int i = lane; i < 27 * 64 / 4; i += 32)
             S4[i] = make_uint4(0xBF800000u, 0xBF800000u, 0xBF800000u, 0xBF800000u);  // -1.0f
@@ -1285,7 +1290,8 @@ static int link_bucket(const vf_config &cfg, LinkCtx &c, int64_t F, void *lines_
                        cudaStream_t st);
 
 int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *ws, void *lines_ws,
-                   int32_t capacity, cudaStream_t st, void **events) {
+                   int32_t capacity, cudaStream_t st, void **events, const int32_t *map,
+                   const int32_t *d_n_map) {
     LinkCtx c;
     int widen;
     LevelInfo li;
@@ -1303,7 +1309,7 @@ int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *w
     // between them.
     int32_t *n_big = c.n_lines + 2;
     const int64_t gs = (F + VF_SMALL_THREADS - 1) / VF_SMALL_THREADS;
-    k_links_small<<<(unsigned)gs, VF_SMALL_THREADS, 0, st>>>(c, widen, F, g_small_ext, big, n_big);
+    k_links_small<<<(unsigned)gs, VF_SMALL_THREADS, 0, st>>>(c, widen, F, g_small_ext, big, n_big, map, d_n_map);
     if ((rc = check_launch("k_links_small"))) return rc;
     int64_t g2 = (F + 32 * kLinkWarps - 1) / (32 * kLinkWarps);
     if (g2 > 4 * (int64_t)max_ctas(VF_LINK_MINB)) g2 = 4 * (int64_t)max_ctas(VF_LINK_MINB);
@@ -1364,6 +1370,25 @@ static int link_bucket(const vf_config &cfg, LinkCtx &c, int64_t F, void *lines_
     return check_launch("k_block_scatter");
 }
 
+// slot -> block from a contraction map (for tables computed without the
+// inverse output: the sharded stage calls)
+__global__ void k_cmap_inverse(int L, const int32_t *__restrict__ level_start, const int32_t *__restrict__ cmap,
+                               const int32_t *__restrict__ d_n_b, int64_t cap, int32_t *__restrict__ inv) {
+    if (*d_n_b > cap) return;
+    const int32_t s = level_start[L], e = level_start[L + 1];
+    for (int64_t b = s + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < e; b += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t slot = cmap[b];
+        if (slot >= 0) inv[slot] = (int32_t)b;
+    }
+}
+
+int link_inverse_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, const int32_t *d_n_b, int64_t cap,
+                      int64_t F, void *lines_ws, cudaStream_t st) {
+    k_cmap_inverse<<<max_ctas(8), 256, 0, st>>>(g->n_levels - 1, g->d_level_start, cmap, d_n_b, cap,
+                                                link_slot_inverse(cfg, F, lines_ws, g->capacity));
+    return check_launch("k_cmap_inverse");
+}
+
 // the slot -> block inverse of the contraction map lives in the lines workspace
 int32_t *link_slot_inverse(const vf_config &cfg, int64_t F, void *lines_ws, int32_t capacity) {
     LinkCtx c;
@@ -1387,7 +1412,7 @@ int link_resolve_impl(const vf_config &cfg, vf_grid *g, const int32_t *cmap, con
     // slot hash for the rare paths (overflowed faces, band candidates)
     link_lookup(g, cmap, c, lengths_cap);
     if (events && events[0]) cudaEventRecord((cudaEvent_t)events[0], st);
-    k_lut_blocks<<<max_ctas(5), kLutWarps * 32, 0, st>>>(parent_dims(cfg), g->d_coords, inv ? inv : tb.inv, d_n_b,
+    k_lut_blocks<<<max_ctas(5), kLutWarps * 32, 0, st>>>(li, parent_dims(cfg), g->d_coords, inv ? inv : tb.inv, d_n_b,
                                                          lengths_cap, tb.boff, tb.bcnt, tb.ent, lengths, g->d_status);
     if ((rc = check_launch("k_lut_blocks"))) return rc;
     // faces whose lines overflowed the record buffer: the direct kernel
