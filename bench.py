@@ -270,8 +270,9 @@ def kernel_rooflines(kt, lv, cfg, F, n_b, stats, ops, hbm, fp32, fp64, traffic):
         gbs = nbytes / (ms / 1e3) / 1e9
         e = {"kernel": name, "launches_per_embed": launches, "ms_per_embed": ms,
              "algorithmic_bytes": int(nbytes), "achieved_gbs": gbs, "hbm_frac": gbs / hbm,
-             "traffic": (sum(traffic[k]["dram_bytes"] * traffic[k].get("launches_per_embed", 1)
-                             for k in ks if k in traffic) if traffic else None), "note": note}
+             # ncu DRAM bytes per launch x this embed's launches of each kernel
+             "traffic": (sum(traffic[k]["dram_bytes"] * kt[k][0] for k in ks if k in traffic and k in kt)
+                         if traffic else None), "note": note}
         if nops:
             peak = fp64 if pipe == "fp64" else fp32
             rate = nops / (ms / 1e3)
@@ -289,11 +290,13 @@ def kernel_rooflines(kt, lv, cfg, F, n_b, stats, ops, hbm, fp32, fp64, traffic):
 
 def ncu_kernel_traffic(config):
     """Per-kernel DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum)
-    per launch from the committed ncu --set full summary, or None."""
+    per launch (mean over the captured launches) from the committed ncu --set
+    full summary, or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
-    return json.load(open(p)).get(config + "_kernels")
+    d = json.load(open(p)).get(config)
+    return d.get("kernels") if d else None
 
 
 def dist_setup():
