@@ -296,7 +296,14 @@ def ncu_kernel_traffic(config):
     if not os.path.exists(p):
         return None
     d = json.load(open(p)).get(config)
-    return d.get("kernels") if d else None
+    if not d:
+        return None
+    k = dict(d.get("kernels", {}))
+    # kernel-timer names (check_launch) that differ from the device symbols
+    for kt_name, sym in (("k_pairs", "k_pairs_append"), ("k_adapt_children", "k_adapt_children_t")):
+        if sym in k:
+            k[kt_name] = k[sym]
+    return k
 
 
 def dist_setup():
