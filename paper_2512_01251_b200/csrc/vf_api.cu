@@ -164,6 +164,7 @@ struct EmbedWs {
     int32_t *n_pairs[2];
     int32_t *map[2];      // kept faces of one level (sharded path: per-level indicators)
     int32_t *n_map[2];
+    uint16_t *ind_bits;   // [F] per-level 1D indicator bits
     int32_t *maps;        // [l_max][F + 1] kept faces of every level (k_indicators_all)
     int32_t *n_maps;      // [l_max]
     int64_t pair_cap;
@@ -233,6 +234,7 @@ static size_t embed_layout(const vf_config &cfg, int64_t F, int32_t cap, char *b
     t.tab_ws = take(t.tab_b);
     t.link_b = link_workspace_size(cfg, Lf, cap, F);
     t.link_ws = take(t.link_b);
+    t.ind_bits = (uint16_t *)take(sizeof(uint16_t) * (size_t)(F + 1));
     t.maps = (int32_t *)take(sizeof(int32_t) * (size_t)(F + 1) * cfg.l_max);
     t.n_maps = (int32_t *)take(sizeof(int32_t) * VF_MAX_LEVELS);
     t.lines_ws = take(link_lines_bytes(cfg, F, cap));
@@ -630,7 +632,7 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
     // Alg. 1 indicators of every level in one pass over the face records
     // (its per-warp map queues cover 8 levels; deeper forests: per-level indicators)
     const bool pre = cfg->l_max <= 8;
-    if (use_filter && pre) VF_TRY(launch_indicators_all(*cfg, faces, F, nullptr, w.maps, F + 1, w.n_maps, s2));
+    if (use_filter && pre) VF_TRY(launch_indicators_all(*cfg, faces, F, w.ind_bits, w.maps, F + 1, w.n_maps, s2));
     auto build = [&](int L) {
         return level_pairs(*cfg, make_level(*cfg, L), faces, F, use_filter, pre, w, L & 1, g->d_status, s2);
     };
@@ -905,7 +907,7 @@ int vf_shard_embed_phase1(void *ctx, const vf_config *cfg, const double *faces, 
     if (pre) {
         vf_config c1 = *cfg;
         c1.shard_count = 1;
-        VF_TRY(launch_indicators_all(c1, faces, F, nullptr, w.maps, F + 1, w.n_maps, st));
+        VF_TRY(launch_indicators_all(c1, faces, F, w.ind_bits, w.maps, F + 1, w.n_maps, st));
     }
     for (int L = 0; L < cfg->l_max; ++L) {
         const LevelInfo li = make_level(*cfg, L);

@@ -132,30 +132,15 @@ __global__ void __launch_bounds__(kIndWarps * 32, 3)
 // of face f at level L.  Candidate rows are decided by the FP32 row
 // classifier (vf_common.cuh); only undecided rows run the exact SAT.  Same
 // predicate as indicator_rows, row for row.
-constexpr int kIndQLevels = 8;  // per-warp queues: levels 0..7 (the embed's l_max <= 8)
-
-// The kept faces of every level are appended straight to that level's
-// compact_map: no compaction scan over F per level.  Each warp queues its
-// kept faces per level in shared memory and reserves global slots 32 at a
-// time (one atomic per 32 faces: per-warp-iteration atomics on the few level
-// counters serialised in L2).  The maps are unordered -- the embed's pair
-// lists and block bins are order-free (the voxelizer breaks ties by face id).
 __global__ void __launch_bounds__(256, VF_IND_MINB)
     k_indicators_all(LevelSet ls, const double *__restrict__ faces, int64_t F,
-                     uint16_t *__restrict__ out, int32_t *__restrict__ maps, int64_t map_stride,
-                     int32_t *__restrict__ n_maps) {
-    __shared__ int32_t s_q[8][kIndQLevels][64];
-    __shared__ int s_qn[8][kIndQLevels];  // queue lengths (warp-uniform)
-    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-    if (lane < kIndQLevels) s_qn[wq][lane] = 0;
-    __syncwarp();
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t f0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); f0 < F; f0 += stride) {
-        const int64_t f = f0 + lane;
-        uint32_t bits = 0;
+                     uint16_t *__restrict__ out) {
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < F;
+         f += (int64_t)gridDim.x * blockDim.x) {
         double v[9], n[3];
-        if (f < F) load_face(faces, f, v, n);
-        if (f < F && !(fabs(n[0]) < ls.li[0].eps_par)) {
+        load_face(faces, f, v, n);
+        uint32_t bits = 0;
+        if (!(fabs(n[0]) < ls.li[0].eps_par)) {
             const double xlo = fmin(fmin(v[0], v[3]), v[6]), xhi = fmax(fmax(v[0], v[3]), v[6]);
             // level-independent part of the row classifier (row_class_init):
             // the yz edge functions, their lengths, orientation, fast-accept
@@ -217,44 +202,54 @@ __global__ void __launch_bounds__(256, VF_IND_MINB)
                 if (hit) bits |= 1u << L;
             }
         }
-        if (out && f < F) out[f] = (uint16_t)bits;
-        if (maps) {
-#pragma unroll
-            for (int L = 0; L < kIndQLevels; ++L) {
-                if (L >= ls.n) break;
-                const uint32_t m = __ballot_sync(0xffffffffu, (bits >> L) & 1u);
-                if (!m) continue;
-                int qn = s_qn[wq][L];
-                if ((bits >> L) & 1u) s_q[wq][L][qn + __popc(m & ((1u << lane) - 1u))] = (int32_t)f;
-                qn += __popc(m);
-                if (qn >= 32) {  // flush 32
-                    __syncwarp();
-                    int b = 0;
-                    if (lane == 0) b = atomicAdd(&n_maps[L], 32);
-                    b = __shfl_sync(0xffffffffu, b, 0);
-                    maps[L * map_stride + b + lane] = s_q[wq][L][lane];
-                    const int rest = qn - 32;
-                    const int32_t x = lane < rest ? s_q[wq][L][32 + lane] : 0;
-                    __syncwarp();
-                    if (lane < rest) s_q[wq][L][lane] = x;
-                    qn = rest;
-                }
-                __syncwarp();
-                if (lane == 0) s_qn[wq][L] = qn;
-                __syncwarp();
-            }
-        }
+        out[f] = (uint16_t)bits;
     }
-    if (maps) {  // the warp's remainders
+}
+
+// The kept faces of every level appended to that level's compact_map from the
+// indicator bits (2 B/face, instead of a compaction scan over F per level).
+// A warp owns a contiguous segment of 1024 faces: pass 1 counts the kept
+// faces per level (ballots), one atomic per level reserves the warp's slots,
+// pass 2 re-reads the bits (L1) and writes the face ids.  No shared memory,
+// no barriers.  The maps are unordered across warps -- the embed's pair
+// lists and block bins are order-free (the voxelizer breaks ties by face id).
+constexpr int kMapSeg = 1024;
+
+__global__ void __launch_bounds__(256)
+    k_bits_to_maps(const uint16_t *__restrict__ bits_in, int64_t F, int nL, int32_t *__restrict__ maps,
+                   int64_t map_stride, int32_t *__restrict__ n_maps) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nseg = (F + kMapSeg - 1) / kMapSeg;
+    for (int64_t sg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); sg < nseg;
+         sg += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+        const int64_t f0 = sg * kMapSeg;
+        uint32_t cnt[VF_MAX_LEVELS];
 #pragma unroll
-        for (int L = 0; L < kIndQLevels; ++L) {
-            __syncwarp();
-            const int qn = L < ls.n ? s_qn[wq][L] : 0;
-            if (!qn) continue;
+        for (int L = 0; L < VF_MAX_LEVELS; ++L) cnt[L] = 0;
+        for (int i = 0; i < kMapSeg; i += 32) {
+            const int64_t f = f0 + i + lane;
+            const uint32_t bits = f < F ? __ldg(bits_in + f) : 0u;
+#pragma unroll
+            for (int L = 0; L < VF_MAX_LEVELS; ++L)
+                if (L < nL) cnt[L] += __popc(__ballot_sync(0xffffffffu, (bits >> L) & 1u));
+        }
+        uint32_t base[VF_MAX_LEVELS];
+#pragma unroll
+        for (int L = 0; L < VF_MAX_LEVELS; ++L) {
             int b = 0;
-            if (lane == 0) b = atomicAdd(&n_maps[L], qn);
-            b = __shfl_sync(0xffffffffu, b, 0);
-            if (lane < qn) maps[L * map_stride + b + lane] = s_q[wq][L][lane];
+            if (L < nL && lane == 0 && cnt[L]) b = atomicAdd(&n_maps[L], (int)cnt[L]);
+            base[L] = (uint32_t)__shfl_sync(0xffffffffu, b, 0);
+        }
+        for (int i = 0; i < kMapSeg; i += 32) {
+            const int64_t f = f0 + i + lane;
+            const uint32_t bits = f < F ? __ldg(bits_in + f) : 0u;
+#pragma unroll
+            for (int L = 0; L < VF_MAX_LEVELS; ++L) {
+                if (L >= nL) break;
+                const uint32_t m = __ballot_sync(0xffffffffu, (bits >> L) & 1u);
+                if ((bits >> L) & 1u) maps[L * map_stride + base[L] + __popc(m & ((1u << lane) - 1u))] = (int32_t)f;
+                base[L] += __popc(m);
+            }
         }
     }
 }
@@ -272,12 +267,15 @@ int launch_indicators_all(const vf_config &cfg, const double *faces, int64_t F, 
     }
     int64_t g = (F + 255) / 256;
     if (g > max_ctas(8)) g = max_ctas(8);
-    if (maps) {
-        cudaMemsetAsync(n_maps, 0, sizeof(int32_t) * cfg.l_max, st);
-        kt_point("memset:n_maps");
-    }
-    k_indicators_all<<<(int)g, 256, 0, st>>>(ls, faces, F, out, maps, map_stride, n_maps);
-    return check_launch("k_indicators_all");
+    k_indicators_all<<<(int)g, 256, 0, st>>>(ls, faces, F, out);
+    int rc = check_launch("k_indicators_all");
+    if (rc || !maps) return rc;
+    cudaMemsetAsync(n_maps, 0, sizeof(int32_t) * cfg.l_max, st);
+    kt_point("memset:n_maps");
+    int64_t gm = ((F + kMapSeg - 1) / kMapSeg + 7) / 8;
+    if (gm > max_ctas(8)) gm = max_ctas(8);
+    k_bits_to_maps<<<(int)(gm < 1 ? 1 : gm), 256, 0, st>>>(out, F, cfg.l_max, maps, map_stride, n_maps);
+    return check_launch("k_bits_to_maps");
 }
 
 __device__ bool indicator_md(const double *v, const double *n, const LevelInfo &li) {

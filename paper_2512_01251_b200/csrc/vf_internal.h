@@ -68,8 +68,8 @@ struct LevelSet {
     int widen[VF_MAX_LEVELS];
     int n;
 };
-// out (nullable): bit L of out[f]; maps (nullable): level L's kept faces at
-// maps + L * map_stride, count n_maps[L] (unordered)
+// out: bit L of out[f]; maps (nullable): level L's kept faces at
+// maps + L * map_stride, count n_maps[L] (unordered, from the bits)
 int launch_indicators_all(const vf_config &cfg, const double *faces, int64_t F, uint16_t *out,
                           int32_t *maps, int64_t map_stride, int32_t *n_maps, cudaStream_t st);
 int sort_bins(int64_t n_bins, const int32_t *offsets, const int32_t *d_total, int32_t *counts,

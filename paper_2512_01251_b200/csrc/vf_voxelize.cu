@@ -49,8 +49,14 @@ namespace vf {
 // Order-free, hence deterministic.  Write-back per row word with the A9 rule,
 // only for rows with a hit (eta == 0: no write, Alg. 3 l.648).  Internal
 // propagation is a provable no-op with matched bins (A8).
-constexpr int kVoxT = 128;  // threads per CTA
-constexpr int kVoxG = 32;   // nonempty blocks per group
+#ifndef VF_VOX_T
+#define VF_VOX_T 128
+#endif
+#ifndef VF_VOX_G
+#define VF_VOX_G 16
+#endif
+constexpr int kVoxT = VF_VOX_T;  // threads per CTA
+constexpr int kVoxG = VF_VOX_G;  // nonempty blocks per group (<= 32)
 
 struct VoxGroup {
     unsigned long long bd[kVoxG * 64];  // best |d| per (block, cell); +inf = no hit
@@ -93,7 +99,7 @@ __global__ void __launch_bounds__(kVoxT, VF_VOX_MINB)
         if (t < 32) {  // group header: blocks, pair counts, prefix
             const int idx = gi * kVoxG + t;
             int u = -1, c = 0, bs = 0;
-            if (idx < n_ne) {
+            if (t < kVoxG && idx < n_ne) {
                 u = ne[idx];
                 c = cnt[u];
                 bs = base[u];
@@ -109,10 +115,12 @@ __global__ void __launch_bounds__(kVoxT, VF_VOX_MINB)
                 const int y = __shfl_up_sync(0xffffffffu, inc, o);
                 if (t >= o) inc += y;
             }
-            S.pre[t + 1] = inc;
+            if (t < kVoxG) {
+                S.pre[t + 1] = inc;
+                S.base[t] = bs;
+                S.bid[t] = u < 0 ? -1 : s + u;
+            }
             if (t == 0) S.pre[0] = 0;
-            S.base[t] = bs;
-            S.bid[t] = u < 0 ? -1 : s + u;
         }
         for (int i = t; i < kVoxG * 64; i += kVoxT) {
             S.bd[i] = kInf64;
@@ -128,7 +136,7 @@ __global__ void __launch_bounds__(kVoxT, VF_VOX_MINB)
             int4 co = make_int4(0, 0, 0, 0);
             if (j < np) {
 #pragma unroll
-                for (int st = 16; st > 0; st >>= 1)  // block of pair j: pre[w] <= j < pre[w + 1]
+                for (int st = kVoxG / 2; st > 0; st >>= 1)  // block of pair j: pre[w] <= j < pre[w + 1]
                     if (S.pre[w + st] <= j) w += st;
                 fid = face_ids[S.base[w] + (j - S.pre[w])];
                 co = S.co[w];
