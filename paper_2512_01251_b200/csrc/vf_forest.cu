@@ -260,11 +260,15 @@ __global__ void __launch_bounds__(kAdaptTBatch, VF_ADAPT_MINB)
                        uint64_t *__restrict__ solid64) {
     __shared__ int32_t s_row[kAdaptTBatch * 27];
     __shared__ int4 s_pc[kAdaptTBatch / 8];
-    __shared__ int32_t s_nb[kAdaptTBatch / 8][27], s_ch[kAdaptTBatch / 8][27];
-    __shared__ uint8_t s_fl[kAdaptTBatch / 8][27];
+    // per parent and parent-side slot: the neighbour's first child (>= 0: the
+    // child's neighbour is that child + sub-octant) or the code the child
+    // inherits (OUTSIDE / SOLID_NBR / MISSING)
+    __shared__ int32_t s_code[kAdaptTBatch / 8][27];
+    __shared__ uint8_t s_slot[27];  // slot of (dx, dy, dz), index (dx+1) + 3 (dy+1) + 9 (dz+1)
     const int64_t e = level_start[L + 1];
     const int64_t nc = 8 * (int64_t)(*n_marked);
     const int t = threadIdx.x;
+    if (t < 27) s_slot[t] = (uint8_t)slot_of(t % 3 - 1, (t / 3) % 3 - 1, t / 9 - 1);
     for (int64_t c0 = (int64_t)blockIdx.x * kAdaptTBatch; c0 < nc; c0 += (int64_t)gridDim.x * kAdaptTBatch) {
         const int nb = (int)min((int64_t)kAdaptTBatch, nc - c0);
         const int np = (nb + 7) >> 3;
@@ -273,11 +277,15 @@ __global__ void __launch_bounds__(kAdaptTBatch, VF_ADAPT_MINB)
             const int p = it / 27, q = it - 27 * p;
             const int32_t P = parents[(c0 >> 3) + p];
             const int32_t Pn = (q == 0) ? P : nbr[27 * (int64_t)P + q];
-            s_nb[p][q] = Pn;
+            int32_t code = VF_NB_OUTSIDE;
             if (Pn >= 0) {
-                s_ch[p][q] = child[Pn];
-                s_fl[p][q] = bflags[Pn];
+                const int32_t ch = child[Pn];
+                code = ch >= 0 ? ch : ((bflags[Pn] & VF_BF_SOLID) ? VF_NB_SOLID_NBR : VF_NB_MISSING);
+            } else if (Pn != VF_NB_OUTSIDE) {  // marked parents are eligible: cannot happen
+                atomicMax(status, VF_EARG);
+                code = VF_NB_MISSING;
             }
+            s_code[p][q] = code;
         }
         __syncthreads();
         const int64_t id = e + c0 + t;
@@ -290,25 +298,15 @@ __global__ void __launch_bounds__(kAdaptTBatch, VF_ADAPT_MINB)
 #pragma unroll
             for (int q = 0; q < 27; ++q) {
                 const int cx = c27(q, 0), cy = c27(q, 1), cz = c27(q, 2);
-                const int ti = ci + cx, tj = cj + cy, tk = ck + cz;
-                int32_t v;
-                if (ti < 0 || tj < 0 || tk < 0 || ti >= nbx1 || tj >= nby1 || tk >= nbz1) {
-                    v = VF_NB_OUTSIDE;
-                } else {
-                    // parent-side direction: (o + c) >> 1 per axis (floor)
-                    const int qp = slot_of((ox + cx) >> 1, (oy + cy) >> 1, (oz + cz) >> 1);
-                    const int32_t Pn = s_nb[p][qp];
-                    if (Pn < 0) {  // marked parents are eligible: cannot happen
-                        atomicMax(status, VF_EARG);
-                        v = VF_NB_MISSING;
-                    } else {
-                        const int32_t ch = s_ch[p][qp];
-                        if (ch >= 0)
-                            v = ch + (ti & 1) + 2 * (tj & 1) + 4 * (tk & 1);
-                        else
-                            v = (s_fl[p][qp] & VF_BF_SOLID) ? VF_NB_SOLID_NBR : VF_NB_MISSING;
-                    }
-                }
+                // parent-side direction (o + c) >> 1 per axis (floor); the
+                // child's target is outside the domain iff that parent-side
+                // neighbour is (its code is then OUTSIDE)
+                const int px = cx < 0 ? ox - 1 : (cx > 0 ? ox : 0);
+                const int py = cy < 0 ? oy - 1 : (cy > 0 ? oy : 0);
+                const int pz = cz < 0 ? oz - 1 : (cz > 0 ? oz : 0);
+                const int32_t code = s_code[p][s_slot[(px + 1) + 3 * (py + 1) + 9 * (pz + 1)]];
+                const int sub = ((ox + cx) & 1) + 2 * ((oy + cy) & 1) + 4 * ((oz + cz) & 1);
+                const int32_t v = code >= 0 ? code + sub : code;
                 s_row[27 * t + q] = v;
                 if (v == VF_NB_MISSING || v == VF_NB_SOLID_NBR) missing |= 1u << dir_code(cx, cy, cz);
             }
