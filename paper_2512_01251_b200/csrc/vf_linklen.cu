@@ -35,6 +35,7 @@
 // Every stored value is the oracle's FP64 value; only the SAT evaluation is
 // skipped where its outcome is certain.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -640,162 +641,138 @@ __device__ __forceinline__ void stage_put(const LinkCtx &c, int4 *st, int pos, i
     else line_store(c, atomicAdd(c.n_lines, 1), rec);
 }
 
-// per-face state of the thread-per-face enumeration
-struct SmallFace {
-    double nn[3];                  // FP64 normal (exact den)
-    float w[3], V1[3], V2[3], nf[3];
-    int b[3], lo[3], hi[3];        // base node, fallback node range per axis
-    float epsL, ff9;
-    float dthr;  // 2 EPS_PARALLEL sqrt(3) + 1e-5 > the FP32 error of c.n plus the exact threshold
+__device__ __forceinline__ int4 qrec_convert(const LinkCtx &c, const int4 rec);
+
+// ---- small faces: thread per face, queued -----------------------------------
+// Faces smaller than ~1.5 cells (the north-star resolution: ~1.3 piercing
+// lines per face over all 13 pairs) are enumerated in lattice-local FP32:
+// lengths in units of dx, relative to v1, with v1 = (b + w + 1/2) dx for the
+// node b = floor(v1/dx - 1/2) and w in [0, 1).  The trace of the line through
+// node b + I (pair R: p, q1, q2, s_j = c_qj c_p) in the plane x_p = v1_p is
+// then (M1 + o1, M2 + o2), M_j = I_qj - s_j I_p, o_j = s_j w_p - w_qj -- the
+// quantities link_dir_setup / link_point form in absolute FP64/FP32
+// coordinates, scaled by 1/dx, with smaller rounding; the margins t_k, tol,
+// the crossing estimate and the node range are the same formulas in these
+// units, so the miss / interior / band classes remain conservative and the
+// recorded lines, band candidates and hence the LUT are identical.  Larger
+// faces go to the warp-flattened kernel.  Two phases per warp, so the
+// expensive part runs on full warps:
+//   phase 1 (lane = face): the face's lattice-local FP32 frame into shared
+//     memory, then the 13 pairs' lattice boxes (the projected triangle
+//     widened by tol); the (face, pair) items with a lattice point in their
+//     box are appended to the warp's queue (~30% of the items at C4);
+//   phase 2 (lane = item): the queued items, 32 at a time: the pair's
+//     EPS_PARALLEL test, edge margins, lattice points (miss / interior /
+//     band), line records and band candidates.
+// With a lane per face (round 1) the point loop ran on the ~30% of lanes
+// whose pair had points while the rest idled through it (C4: 0.98 -> 0.81 ms).
+struct QFace {                      // one face of the warp, lattice-local
+    float V1[3], V2[3], w[3], nf[3];
+    int b[3];
+    short lo[3], hi[3];
+    float ff9;
     int f;
 };
-
-// the face permuted to (p, q1, q2) for one class of pairs
-struct SmallProj {
-    double np, nq1, nq2;
-    float V1p, V1a, V1b, V2p, V2a, V2b;  // a = q1, b = q2
-    float wp, wa, wb, nfp, nfa, nfb;
-    int bp, ba, bb, lop, hip, n1, n2, p;
+struct QWarp {
+    QFace fc[32];
+    uint16_t q[32 * 13];            // items: lane | idx << 5 (idx = class-major pair index 0..12)
+    int qn;
 };
 
-__device__ __forceinline__ void small_project(const LinkCtx &c, const SmallFace &S, int cls, SmallProj &P) {
+// pair index -> (class, s1, s2, R) without memory: idx 0..8 class 0 (t = idx),
+// 9..11 class 1, 12 class 2; R in lattice.py order, 4 bits each
+__device__ __forceinline__ void pair_of(int idx, int &cls, int &s1, int &s2, int &R) {
+    cls = idx < 9 ? 0 : (idx < 12 ? 1 : 2);
+    const int t = idx - (cls == 0 ? 0 : (cls == 1 ? 9 : 12));
+    s1 = cls == 0 ? t / 3 - 1 : 0;
+    s2 = cls == 0 ? t % 3 - 1 : (cls == 1 ? t - 1 : 0);
+    R = (int)((0x271893a405b6cull >> (4 * idx)) & 15);
+}
+
+// the class projection (p, q1, q2) of a queued face (small_project, from shared memory)
+struct QProj {
+    float V1p, V1a, V1b, V2p, V2a, V2b, wp, wa, wb, nfp, nfa, nfb;
+    int bp, ba, bb, lop, hip, n1, n2;
+};
+__device__ __forceinline__ void qproject(const LinkCtx &c, const QFace &F, int cls, QProj &P) {
     const int p = cls, q1 = cls == 0 ? 1 : 0, q2 = cls == 2 ? 1 : 2;
-    P.p = p;
-    P.np = pick3(p, S.nn[0], S.nn[1], S.nn[2]);
-    P.nq1 = pick3(q1, S.nn[0], S.nn[1], S.nn[2]);
-    P.nq2 = pick3(q2, S.nn[0], S.nn[1], S.nn[2]);
-    P.V1p = pick3(p, S.V1[0], S.V1[1], S.V1[2]);
-    P.V1a = pick3(q1, S.V1[0], S.V1[1], S.V1[2]);
-    P.V1b = pick3(q2, S.V1[0], S.V1[1], S.V1[2]);
-    P.V2p = pick3(p, S.V2[0], S.V2[1], S.V2[2]);
-    P.V2a = pick3(q1, S.V2[0], S.V2[1], S.V2[2]);
-    P.V2b = pick3(q2, S.V2[0], S.V2[1], S.V2[2]);
-    P.wp = pick3(p, S.w[0], S.w[1], S.w[2]);
-    P.wa = pick3(q1, S.w[0], S.w[1], S.w[2]);
-    P.wb = pick3(q2, S.w[0], S.w[1], S.w[2]);
-    P.nfp = pick3(p, S.nf[0], S.nf[1], S.nf[2]);
-    P.nfa = pick3(q1, S.nf[0], S.nf[1], S.nf[2]);
-    P.nfb = pick3(q2, S.nf[0], S.nf[1], S.nf[2]);
-    P.bp = pick3(p, S.b[0], S.b[1], S.b[2]);
-    P.ba = pick3(q1, S.b[0], S.b[1], S.b[2]);
-    P.bb = pick3(q2, S.b[0], S.b[1], S.b[2]);
-    P.lop = pick3(p, S.lo[0], S.lo[1], S.lo[2]);
-    P.hip = pick3(p, S.hi[0], S.hi[1], S.hi[2]);
+    P.V1p = F.V1[p]; P.V1a = F.V1[q1]; P.V1b = F.V1[q2];
+    P.V2p = F.V2[p]; P.V2a = F.V2[q1]; P.V2b = F.V2[q2];
+    P.wp = F.w[p]; P.wa = F.w[q1]; P.wb = F.w[q2];
+    P.nfp = F.nf[p]; P.nfa = F.nf[q1]; P.nfb = F.nf[q2];
+    P.bp = F.b[p]; P.ba = F.b[q1]; P.bb = F.b[q2];
+    P.lop = F.lo[p]; P.hip = F.hi[p];
     P.n1 = pick3(q1, c.cells[0], c.cells[1], c.cells[2]);
     P.n2 = pick3(q2, c.cells[0], c.cells[1], c.cells[2]);
 }
 
-// one (face, pair R = (class p, s1, s2)) of the thread-per-face enumeration:
-// the lattice points of the projected bounding box, their class, piercing
-// lines as records (CTA stage slots) and the undecided ones node by node to
-// the band list
-__device__ __forceinline__ int small_pair(const LinkCtx &c, const SmallFace &S, const SmallProj &P,
-                                          bool small, int R, int s1, int s2, int4 *s_rec, int *s_n) {
-    // exact den / EPS_PARALLEL, as link_dir_setup: c = (1, s1, s2) over
-    // (p, q1, q2) -- the same FP64 sum in the same order (a zero term is exact)
-    if (!small) return 0;
-    const float dn = P.nfp + (float)s1 * P.nfa + (float)s2 * P.nfb;  // c.n in FP32 (error < 1e-6)
-    if (!(fabsf(dn) > S.dthr)) {  // only then can |c.n| be below EPS_PARALLEL |c|: decide exactly
-        const double den = VF_DADD(VF_DADD(P.np, cmul(s1, P.nq1)), cmul(s2, P.nq2));
-        const int nz = (s1 != 0) + (s2 != 0);
-        const double cn = nz == 0 ? 1.0 : (nz == 1 ? 1.4142135623730951 : 1.7320508075688772);
-        if (fabs(den) < VF_DMUL(c.eps_par, cn)) return 0;
-    }
-    const float P1a = P.V1a - (float)s1 * P.V1p, P1b = P.V1b - (float)s2 * P.V1p;
-    const float P2a = P.V2a - (float)s1 * P.V2p, P2b = P.V2b - (float)s2 * P.V2p;
-    const float ext = fmaxf(fmaxf(fabsf(P1a), fabsf(P1b)), fmaxf(fabsf(P2a), fabsf(P2b)));
-    const float tol = 1e-5f * (ext + 1.0f) + 6.0f * S.epsL;
-    const float o1 = (float)s1 * P.wp - P.wa, o2 = (float)s2 * P.wp - P.wb;
-    const int m1a = (int)ceilf(fminf(fminf(0.0f, P1a), P2a) - tol - o1 - 1e-4f);
-    const int m1b = (int)floorf(fmaxf(fmaxf(0.0f, P1a), P2a) + tol - o1 + 1e-4f);
-    const int m2a = (int)ceilf(fminf(fminf(0.0f, P1b), P2b) - tol - o2 - 1e-4f);
-    const int m2b = (int)floorf(fmaxf(fmaxf(0.0f, P1b), P2b) + tol - o2 + 1e-4f);
-    if (m1a > m1b || m2a > m2b) return 0;
-    const float cr = P1a * P2b - P1b * P2a;
-    const float ab = 4e-6f * (ext + 1.0f) * (ext + 1.0f);
-    // edge margins with the L1 length |a| + |b| >= |e| (no square root: a
-    // larger margin only moves lines from the miss / interior classes into
-    // the exactly-decided band, so every class stays conservative)
-    const float t0 = tol * (fabsf(P1a) + fabsf(P1b)) * 1.0001f + ab;
-    const float t1 = tol * (fabsf(P2a - P1a) + fabsf(P2b - P1b)) * 1.0001f + ab;
-    const float t2 = tol * (fabsf(P2a) + fabsf(P2b)) * 1.0001f + ab;
-    const float sg = cr >= 0.0f ? 1.0f : -1.0f;
-    const bool steep = fabsf(dn) >= 1e-3f;
-    const bool fast = steep && c.fast;
-    const int gm1 = P.ba - s1 * P.bp, gm2 = P.bb - s2 * P.bp;
-    for (int M2 = m2a; M2 <= m2b; ++M2) {
-        const float Rb = (float)M2 + o2;
-        for (int M1 = m1a; M1 <= m1b; ++M1) {
-            const float Ra = (float)M1 + o1;
-            const float E0 = sg * (P1a * Rb - P1b * Ra);
-            const float E1 = sg * ((P2a - P1a) * (Rb - P1b) - (P2b - P1b) * (Ra - P1a));
-            const float E2 = sg * (P2b * Ra - P2a * Rb);
-            if (E0 < -t0 || E1 < -t1 || E2 < -t2) continue;  // misses the face
-            const bool inner = fast && E0 >= t0 && E1 >= t1 && E2 >= t2;
-            // node range along p (line_nodes in lattice units; c_p = 1)
-            int ip_lo = P.lop, ip_hi = P.hip;
-            if (steep) {
-                const float xs = -__fdividef(P.nfa * Ra + P.nfb * Rb, dn);
-                const float wid0 = 1.0f + 1e-4f + 1e-5f + __fdividef(S.ff9, fabsf(dn)) * 1.0001f;
-                const float wid = wid0 + 1.0001e-6f * __fdividef(fabsf(xs), fabsf(dn));
-                ip_lo = max(P.bp + (int)ceilf(xs + P.wp - wid), ip_lo);
-                ip_hi = min(P.bp + (int)floorf(xs + P.wp + wid), ip_hi);
-            }
-            const int mg1 = M1 + gm1, mg2 = M2 + gm2;
-            if (inner && ip_lo <= ip_hi && ip_hi - ip_lo < 8) {
-                const int4 rec = make_int4(S.f, R | (1 << 4) | ((ip_hi - ip_lo) << 5) | (ip_lo << 8), mg1, mg2);
-                stage_put(c, s_rec, atomicAdd(s_n, 1), rec);  // CTA stage slot (shared atomic)
-                continue;
-            }
-            // margin band / ill-conditioned / long range: exact path later
-            for (int ip = ip_lo; ip <= ip_hi; ++ip) {
-                const int a = mg1 + s1 * ip, bq = mg2 + s2 * ip;
-                if (a < 0 || a >= P.n1 || bq < 0 || bq >= P.n2) continue;
-                const int i = P.p == 0 ? ip : a;
-                const int j = P.p == 1 ? ip : (P.p == 0 ? a : bq);
-                const int k = P.p == 2 ? ip : bq;
-                link_slow<2>(c, S.f, -1, i, j, k, R);
-            }
-        }
-    }
-    return (m2b - m2a + 1) * (m1b - m1a + 1);
+// the pair's lattice box (the projected triangle widened by tol); false: empty
+__device__ __forceinline__ bool qbox(const QProj &P, float epsL, int s1, int s2, float &P1a, float &P1b,
+                                     float &P2a, float &P2b, float &ext, float &tol, float &o1, float &o2,
+                                     int &m1a, int &m1b, int &m2a, int &m2b) {
+    P1a = P.V1a - (float)s1 * P.V1p; P1b = P.V1b - (float)s2 * P.V1p;
+    P2a = P.V2a - (float)s1 * P.V2p; P2b = P.V2b - (float)s2 * P.V2p;
+    ext = fmaxf(fmaxf(fabsf(P1a), fabsf(P1b)), fmaxf(fabsf(P2a), fabsf(P2b)));
+    tol = 1e-5f * (ext + 1.0f) + 6.0f * epsL;
+    o1 = (float)s1 * P.wp - P.wa;
+    o2 = (float)s2 * P.wp - P.wb;
+    m1a = (int)ceilf(fminf(fminf(0.0f, P1a), P2a) - tol - o1 - 1e-4f);
+    m1b = (int)floorf(fmaxf(fmaxf(0.0f, P1a), P2a) + tol - o1 + 1e-4f);
+    m2a = (int)ceilf(fminf(fminf(0.0f, P1b), P2b) - tol - o2 - 1e-4f);
+    m2b = (int)floorf(fmaxf(fmaxf(0.0f, P1b), P2b) + tol - o2 + 1e-4f);
+    return m1a <= m1b && m2a <= m2b;
 }
 
-__device__ __forceinline__ int4 qrec_convert(const LinkCtx &c, const int4 rec);
-
 __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
-    k_links_small(LinkCtx c, int widen, int64_t F, float small_ext, int32_t *__restrict__ big,
-                  int32_t *__restrict__ n_big, const int32_t *__restrict__ map,
-                  const int32_t *__restrict__ d_n_map) {
+    k_links_smallq(LinkCtx c, int widen, int64_t F, float small_ext, int32_t *__restrict__ big,
+                   int32_t *__restrict__ n_big, const int32_t *__restrict__ map,
+                   const int32_t *__restrict__ d_n_map) {
     __shared__ int4 s_rec[kLineStage];
     __shared__ int s_n, s_base;
+    __shared__ QWarp s_w[VF_SMALL_THREADS / 32];
+    const int lane = threadIdx.x & 31;
+    QWarp &W = s_w[threadIdx.x >> 5];
     if (threadIdx.x == 0) s_n = 0;
+    if (lane == 0) W.qn = 0;
     __syncthreads();
     const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
     // (map: a face subset -- the sharded embed's faces near owned rows)
     bool act = m < (d_n_map ? (int64_t)*d_n_map : F);
-    SmallFace S;
-    S.f = act && map ? map[m] : (int)m;
-    double v[9], flo[3] = {0.0, 0.0, 0.0}, fhi[3] = {0.0, 0.0, 0.0};
-    float extL = 0.0f;
+    const int f = act && map ? map[m] : (int)m;
     bool small = false;
+    QFace &Q = W.fc[lane];
     if (act) {
-        load_face(c.faces, S.f, v, S.nn);
+        double v[9], nn[3], flo[3], fhi[3];
+        load_face(c.faces, f, v, nn);
         double ext = 0.0;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
             flo[d] = fmin(fmin(v[d], v[3 + d]), v[6 + d]);
             fhi[d] = fmax(fmax(v[d], v[3 + d]), v[6 + d]);
             ext = fmax(ext, fhi[d] - flo[d]);
-        }
-        extL = (float)(ext * c.inv_dx);
-        // A5 / face_pairs: a face whose AABB misses the domain is in no bin,
-        // so the oracle's per-cell MD-bin scan never sees it
-#pragma unroll
-        for (int d = 0; d < 3; ++d)
+            // A5 / face_pairs: a face whose AABB misses the domain is in no
+            // bin, so the oracle's per-cell MD-bin scan never sees it
             if (fhi[d] < 0.0 || flo[d] > c.len[d]) act = false;
+        }
+        const float extL = (float)(ext * c.inv_dx);
         small = act && extL <= small_ext;
+        if (small) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const double t = v[d] * c.inv_dx - 0.5, bd = floor(t);
+                Q.b[d] = (int)bd;
+                Q.w[d] = (float)(t - bd);
+                Q.V1[d] = (float)((v[3 + d] - v[d]) * c.inv_dx);
+                Q.V2[d] = (float)((v[6 + d] - v[d]) * c.inv_dx);
+                Q.nf[d] = (float)nn[d];
+                // nodes within one link of the face AABB (k_links' fallback range)
+                Q.lo[d] = (short)max((int)floor((flo[d] - c.dx - 2.0 * c.eps) * c.inv_dx - 0.5) - widen, 0);
+                Q.hi[d] = (short)min((int)floor((fhi[d] + c.dx + 2.0 * c.eps) * c.inv_dx - 0.5) + 1 + widen,
+                                     c.cells[d] - 1);
+            }
+            Q.ff9 = 4e-6f * (extL + 2.0f);
+            Q.f = f;
+        }
     }
     // large faces: warp-aggregated append to the list of the warp-flattened kernel
     const unsigned bm = __ballot_sync(0xffffffffu, act && !small);
@@ -803,45 +780,102 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
         int base = 0;
         if (lane == 0) base = atomicAdd(n_big, __popc(bm));
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (act && !small) big[base + __popc(bm & ((1u << lane) - 1u))] = S.f;
+        if (act && !small) big[base + __popc(bm & ((1u << lane) - 1u))] = f;
     }
+    __syncwarp();
+    // phase 1: the 13 pairs' boxes, non-empty items queued
     unsigned long long tests = 0;
     if (__any_sync(0xffffffffu, small)) {
-        if (small) {
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                const double t = v[d] * c.inv_dx - 0.5, bd = floor(t);
-                S.b[d] = (int)bd;
-                S.w[d] = (float)(t - bd);
-                S.V1[d] = (float)((v[3 + d] - v[d]) * c.inv_dx);
-                S.V2[d] = (float)((v[6 + d] - v[d]) * c.inv_dx);
-                S.nf[d] = (float)S.nn[d];
-                // nodes within one link of the face AABB (k_links' fallback range)
-                S.lo[d] = max((int)floor((flo[d] - c.dx - 2.0 * c.eps) * c.inv_dx - 0.5) - widen, 0);
-                S.hi[d] = min((int)floor((fhi[d] + c.dx + 2.0 * c.eps) * c.inv_dx - 0.5) + 1 + widen, c.cells[d] - 1);
-            }
-        }
-        S.epsL = c.epsL;
-        S.dthr = c.dthr;
-        (void)0;
-        S.ff9 = 4e-6f * (extL + 2.0f);
-        // the 13 pairs in three classes of the axis p of their first nonzero
-        // component (c_p = +1): p = x: c = (1, s1, s2), all 9 sign pairs;
-        // p = y: (0, 1, s2); p = z: (0, 0, 1).  The face is permuted to
-        // (p, q1, q2) once per class instead of per pair.
 #pragma unroll 1
         for (int cls = 0; cls < 3; ++cls) {
-            SmallProj P;
-            small_project(c, S, cls, P);
+            QProj P;
+            if (small) qproject(c, Q, cls, P);
             const int ns = cls == 0 ? 9 : (cls == 1 ? 3 : 1);
 #pragma unroll 1
             for (int t = 0; t < ns; ++t) {
-                const int s1 = cls == 0 ? t / 3 - 1 : 0;
-                const int s2 = cls == 0 ? t % 3 - 1 : (cls == 1 ? t - 1 : 0);
-                const int idx = cls == 0 ? t : (cls == 1 ? 9 + t : 12);
-                // R of (class, s1, s2) in lattice.py order, 4 bits each
-                const int R = (int)((0x271893a405b6cull >> (4 * idx)) & 15);
-                tests += small_pair(c, S, P, small, R, s1, s2, s_rec, &s_n);
+                const int idx = (cls == 0 ? 0 : (cls == 1 ? 9 : 12)) + t;
+                bool ok = false;
+                if (small) {
+                    const int s1 = cls == 0 ? t / 3 - 1 : 0;
+                    const int s2 = cls == 0 ? t % 3 - 1 : (cls == 1 ? t - 1 : 0);
+                    float P1a, P1b, P2a, P2b, ext, tol, o1, o2;
+                    int m1a, m1b, m2a, m2b;
+                    ok = qbox(P, c.epsL, s1, s2, P1a, P1b, P2a, P2b, ext, tol, o1, o2, m1a, m1b, m2a, m2b);
+                }
+                const uint32_t qm = __ballot_sync(0xffffffffu, ok);
+                if (ok) W.q[W.qn + __popc(qm & ((1u << lane) - 1u))] = (uint16_t)(lane | (idx << 5));
+                __syncwarp();
+                if (lane == 0) W.qn += __popc(qm);
+                __syncwarp();
+            }
+        }
+    }
+    // phase 2: the queued items on full warps
+    const int nq = W.qn;
+    for (int i0 = 0; i0 < nq; i0 += 32) {
+        if (i0 + lane >= nq) continue;
+        const uint32_t it = W.q[i0 + lane];
+        const QFace &Fq = W.fc[it & 31];
+        int cls, s1, s2, R;
+        pair_of((int)(it >> 5), cls, s1, s2, R);
+        QProj P;
+        qproject(c, Fq, cls, P);
+        float P1a, P1b, P2a, P2b, ext, tol, o1, o2;
+        int m1a, m1b, m2a, m2b;
+        qbox(P, c.epsL, s1, s2, P1a, P1b, P2a, P2b, ext, tol, o1, o2, m1a, m1b, m2a, m2b);
+        tests += (unsigned long long)((m2b - m2a + 1) * (m1b - m1a + 1));
+        // exact den / EPS_PARALLEL (link_dir_setup): only where the FP32 c.n is near 0
+        const float dn = P.nfp + (float)s1 * P.nfa + (float)s2 * P.nfb;
+        if (!(fabsf(dn) > c.dthr)) {
+            const double *nr = c.faces + (int64_t)Fq.f * kFaceStride + 9;  // the face's FP64 normal
+            const int p = cls, q1 = cls == 0 ? 1 : 0, q2 = cls == 2 ? 1 : 2;
+            const double den = VF_DADD(VF_DADD(nr[p], cmul(s1, nr[q1])), cmul(s2, nr[q2]));
+            const int nz = (s1 != 0) + (s2 != 0);
+            const double cn = nz == 0 ? 1.0 : (nz == 1 ? 1.4142135623730951 : 1.7320508075688772);
+            if (fabs(den) < VF_DMUL(c.eps_par, cn)) continue;
+        }
+        const float cr = P1a * P2b - P1b * P2a;
+        const float ab = 4e-6f * (ext + 1.0f) * (ext + 1.0f);
+        const float t0 = tol * (fabsf(P1a) + fabsf(P1b)) * 1.0001f + ab;
+        const float t1 = tol * (fabsf(P2a - P1a) + fabsf(P2b - P1b)) * 1.0001f + ab;
+        const float t2 = tol * (fabsf(P2a) + fabsf(P2b)) * 1.0001f + ab;
+        const float sg = cr >= 0.0f ? 1.0f : -1.0f;
+        const bool steep = fabsf(dn) >= 1e-3f;
+        const bool fast = steep && c.fast;
+        const int gm1 = P.ba - s1 * P.bp, gm2 = P.bb - s2 * P.bp;
+        for (int M2 = m2a; M2 <= m2b; ++M2) {
+            const float Rb = (float)M2 + o2;
+            for (int M1 = m1a; M1 <= m1b; ++M1) {
+                const float Ra = (float)M1 + o1;
+                const float E0 = sg * (P1a * Rb - P1b * Ra);
+                const float E1 = sg * ((P2a - P1a) * (Rb - P1b) - (P2b - P1b) * (Ra - P1a));
+                const float E2 = sg * (P2b * Ra - P2a * Rb);
+                if (E0 < -t0 || E1 < -t1 || E2 < -t2) continue;  // misses the face
+                const bool inner = fast && E0 >= t0 && E1 >= t1 && E2 >= t2;
+                // node range along p (line_nodes in lattice units; c_p = 1)
+                int ip_lo = P.lop, ip_hi = P.hip;
+                if (steep) {
+                    const float xs = -__fdividef(P.nfa * Ra + P.nfb * Rb, dn);
+                    const float wid0 = 1.0f + 1e-4f + 1e-5f + __fdividef(Fq.ff9, fabsf(dn)) * 1.0001f;
+                    const float wid = wid0 + 1.0001e-6f * __fdividef(fabsf(xs), fabsf(dn));
+                    ip_lo = max(P.bp + (int)ceilf(xs + P.wp - wid), ip_lo);
+                    ip_hi = min(P.bp + (int)floorf(xs + P.wp + wid), ip_hi);
+                }
+                const int mg1 = M1 + gm1, mg2 = M2 + gm2;
+                if (inner && ip_lo <= ip_hi && ip_hi - ip_lo < 8) {
+                    const int4 rec = make_int4(Fq.f, R | (1 << 4) | ((ip_hi - ip_lo) << 5) | (ip_lo << 8), mg1, mg2);
+                    stage_put(c, s_rec, atomicAdd(&s_n, 1), rec);  // CTA stage slot (shared atomic)
+                    continue;
+                }
+                // margin band / ill-conditioned / long range: exact path later
+                for (int ip = ip_lo; ip <= ip_hi; ++ip) {
+                    const int a = mg1 + s1 * ip, bq = mg2 + s2 * ip;
+                    if (a < 0 || a >= P.n1 || bq < 0 || bq >= P.n2) continue;
+                    const int i = cls == 0 ? ip : a;
+                    const int j = cls == 1 ? ip : (cls == 0 ? a : bq);
+                    const int k = cls == 2 ? ip : bq;
+                    link_slow<2>(c, Fq.f, -1, i, j, k, R);
+                }
             }
         }
     }
@@ -1309,7 +1343,7 @@ int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *w
     // between them.
     int32_t *n_big = c.n_lines + 2;
     const int64_t gs = (F + VF_SMALL_THREADS - 1) / VF_SMALL_THREADS;
-    k_links_small<<<(unsigned)gs, VF_SMALL_THREADS, 0, st>>>(c, widen, F, g_small_ext, big, n_big, map, d_n_map);
+    k_links_smallq<<<(unsigned)gs, VF_SMALL_THREADS, 0, st>>>(c, widen, F, g_small_ext, big, n_big, map, d_n_map);
     if ((rc = check_launch("k_links_small"))) return rc;
     int64_t g2 = (F + 32 * kLinkWarps - 1) / (32 * kLinkWarps);
     if (g2 > 4 * (int64_t)max_ctas(VF_LINK_MINB)) g2 = 4 * (int64_t)max_ctas(VF_LINK_MINB);
@@ -1323,7 +1357,7 @@ int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *w
     return rc;
 }
 
-const void *link_enum_kernel(int small) { return small ? (const void *)k_links_small : (const void *)k_links<2>; }
+const void *link_enum_kernel(int small) { return small ? (const void *)k_links_smallq : (const void *)k_links<2>; }
 
 // counters of the last embed's cut-link pass (synchronous read):
 // {lines recorded, line capacity, overflow faces, band candidates, band capacity,
