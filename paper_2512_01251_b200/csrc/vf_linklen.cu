@@ -679,13 +679,14 @@ struct QWarp {
     int qn;
 };
 
-// pair index -> (class, s1, s2, R) without memory: idx 0..8 class 0 (t = idx),
-// 9..11 class 1, 12 class 2; R in lattice.py order, 4 bits each
+// pair index -> (class, s1, s2, R) from packed immediates (2 bits per pair
+// for the class, s1 + 1 and s2 + 1; 4 bits for R in lattice.py order):
+// idx 0..8 class 0 (s1, s2) = (t / 3 - 1, t % 3 - 1), 9..11 class 1
+// (0, t - 1), 12 class 2 (0, 0)
 __device__ __forceinline__ void pair_of(int idx, int &cls, int &s1, int &s2, int &R) {
-    cls = idx < 9 ? 0 : (idx < 12 ? 1 : 2);
-    const int t = idx - (cls == 0 ? 0 : (cls == 1 ? 9 : 12));
-    s1 = cls == 0 ? t / 3 - 1 : 0;
-    s2 = cls == 0 ? t % 3 - 1 : (cls == 1 ? t - 1 : 0);
+    cls = (int)((0x2540000u >> (2 * idx)) & 3u);
+    s1 = (int)((0x156a540u >> (2 * idx)) & 3u) - 1;
+    s2 = (int)((0x1924924u >> (2 * idx)) & 3u) - 1;
     R = (int)((0x271893a405b6cull >> (4 * idx)) & 15);
 }
 
@@ -783,32 +784,63 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
         if (act && !small) big[base + __popc(bm & ((1u << lane) - 1u))] = f;
     }
     __syncwarp();
-    // phase 1: the 13 pairs' boxes, non-empty items queued
+    // phase 1: which of the 13 pairs can have a lattice point.  Per class
+    // the box range along q1 depends on s1 only and along q2 on s2 only; with
+    // the class's largest tolerance (a bound on every pair's ext) the ranges
+    // are supersets of the pairs' exact boxes, so a pair is queued iff both
+    // of its axis ranges are non-empty (phase 2 re-derives the exact box).
     unsigned long long tests = 0;
-    if (__any_sync(0xffffffffu, small)) {
-#pragma unroll 1
+    uint32_t cand = 0;  // bit idx: pair idx may have lattice points
+    if (small) {
+#pragma unroll
         for (int cls = 0; cls < 3; ++cls) {
-            QProj P;
-            if (small) qproject(c, Q, cls, P);
+            const int p = cls, q1 = cls == 0 ? 1 : 0, q2 = cls == 2 ? 1 : 2;
+            const float V1p = Q.V1[p], V2p = Q.V2[p], wp = Q.w[p];
+            const float V1a = Q.V1[q1], V2a = Q.V2[q1], wa = Q.w[q1];
+            const float V1b = Q.V1[q2], V2b = Q.V2[q2], wb = Q.w[q2];
+            // |V_q - s V_p| <= |V_q| + |V_p| for every s in {-1, 0, 1}
+            const float extc = fmaxf(fmaxf(fabsf(V1a), fabsf(V2a)), fmaxf(fabsf(V1b), fabsf(V2b))) +
+                               fmaxf(fabsf(V1p), fabsf(V2p));
+            const float tolc = 1e-5f * (extc + 1.0f) + 6.0f * c.epsL;
+            uint32_t okA = 0, okB = 0;  // bit s + 1
+#pragma unroll
+            for (int sg = -1; sg <= 1; ++sg) {
+                if (cls != 0 && sg != 0) continue;  // classes 1, 2: s1 = 0
+                const float A1 = V1a - (float)sg * V1p, A2 = V2a - (float)sg * V2p, o = (float)sg * wp - wa;
+                if ((int)ceilf(fminf(fminf(0.0f, A1), A2) - tolc - o - 1e-4f) <=
+                    (int)floorf(fmaxf(fmaxf(0.0f, A1), A2) + tolc - o + 1e-4f))
+                    okA |= 1u << (sg + 1);
+            }
+#pragma unroll
+            for (int sg = -1; sg <= 1; ++sg) {
+                if (cls == 2 && sg != 0) continue;  // class 2: s2 = 0
+                const float B1 = V1b - (float)sg * V1p, B2 = V2b - (float)sg * V2p, o = (float)sg * wp - wb;
+                if ((int)ceilf(fminf(fminf(0.0f, B1), B2) - tolc - o - 1e-4f) <=
+                    (int)floorf(fmaxf(fmaxf(0.0f, B1), B2) + tolc - o + 1e-4f))
+                    okB |= 1u << (sg + 1);
+            }
+            const int i0 = cls == 0 ? 0 : (cls == 1 ? 9 : 12);
             const int ns = cls == 0 ? 9 : (cls == 1 ? 3 : 1);
-#pragma unroll 1
+#pragma unroll
             for (int t = 0; t < ns; ++t) {
-                const int idx = (cls == 0 ? 0 : (cls == 1 ? 9 : 12)) + t;
-                bool ok = false;
-                if (small) {
-                    const int s1 = cls == 0 ? t / 3 - 1 : 0;
-                    const int s2 = cls == 0 ? t % 3 - 1 : (cls == 1 ? t - 1 : 0);
-                    float P1a, P1b, P2a, P2b, ext, tol, o1, o2;
-                    int m1a, m1b, m2a, m2b;
-                    ok = qbox(P, c.epsL, s1, s2, P1a, P1b, P2a, P2b, ext, tol, o1, o2, m1a, m1b, m2a, m2b);
-                }
-                const uint32_t qm = __ballot_sync(0xffffffffu, ok);
-                if (ok) W.q[W.qn + __popc(qm & ((1u << lane) - 1u))] = (uint16_t)(lane | (idx << 5));
-                __syncwarp();
-                if (lane == 0) W.qn += __popc(qm);
-                __syncwarp();
+                const int s1 = cls == 0 ? t / 3 - 1 : 0;
+                const int s2 = cls == 0 ? t % 3 - 1 : (cls == 1 ? t - 1 : 0);
+                cand |= ((okA >> (s1 + 1)) & (okB >> (s2 + 1)) & 1u) << (i0 + t);
             }
         }
+    }
+    {  // the warp's items: one exclusive scan of the per-lane counts
+        const int cnt = __popc(cand);
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        int pos = inc - cnt;
+        for (uint32_t mm = cand; mm; mm &= mm - 1) W.q[pos++] = (uint16_t)(lane | ((__ffs(mm) - 1) << 5));
+        if (lane == 31) W.qn = inc;
+        __syncwarp();
     }
     // phase 2: the queued items on full warps
     const int nq = W.qn;
