@@ -115,6 +115,8 @@ struct LinkCtx {
     int32_t *ovf_list, *n_ovf;
     uint32_t *ovf_bits;   // one bit per face: already listed
     unsigned long long *n_tests;  // lattice lines classified (FP32 intersection tests; roofline ops)
+    int32_t *pcnt;                // links per finest parent key (the LUT buckets), counted at conversion
+    int3 pdim;                    // parent-key grid
 };
 
 // LUT slot of the finest block holding lattice node (i, j, k); -1: not
@@ -643,6 +645,40 @@ __device__ __forceinline__ void stage_put(const LinkCtx &c, int4 *st, int pos, i
 
 __device__ __forceinline__ int4 qrec_convert(const LinkCtx &c, const int4 rec);
 
+__device__ __forceinline__ void qrec_entry(const int4 rec, int k, int &i, int &j, int &kk, int &q, int &t) {
+    const int bi = rec.x & 0x7fff, bj = (rec.x >> 15) & 0x7fff, bk = rec.y & 0x7fff, R = (rec.y >> 15) & 15;
+    const uint32_t cd = ((uint32_t)rec.y >> (21 + 4 * k)) & 15u;
+    const int o = cd & 7;
+    i = bi + o * c27(2 * R + 1, 0);
+    j = bj + o * c27(2 * R + 1, 1);
+    kk = bk + o * c27(2 * R + 1, 2);
+    q = (cd >> 3) ? 2 * R + 2 : 2 * R + 1;
+    t = (i & 3) + 4 * (j & 3) + 16 * (kk & 3);
+}
+
+// a link's parent bucket key and its bucket entry octant << 41 | (q 64 + t)
+// << 30 | q bits (q in (0, 1]: 30 bits)
+__device__ __forceinline__ int32_t link_bucket_entry(const int4 rec, int k, int3 pdim, unsigned long long &x) {
+    int i, j, kk, q, t;
+    qrec_entry(rec, k, i, j, kk, q, t);
+    const int oct = ((i >> 2) & 1) + 2 * ((j >> 2) & 1) + 4 * ((kk >> 2) & 1);
+    x = ((unsigned long long)oct << 41) | ((unsigned long long)(q * 64 + t) << 30) | (uint32_t)(k ? rec.w : rec.z);
+    return (i >> 3) + pdim.x * ((j >> 3) + pdim.y * (kk >> 3));
+}
+
+// count the links of a q-record into their parent buckets (warp-aggregated
+// over the active lanes: neighbouring records mostly share parents)
+__device__ __forceinline__ void count_qrec(const LinkCtx &c, const int4 rec) {
+    const int ne = (rec.y >> 19) & 3;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        unsigned long long x;
+        const int32_t key = k < ne ? link_bucket_entry(rec, k, c.pdim, x) : -1;
+        const uint32_t grp = __match_any_sync(__activemask(), key);
+        if (key >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&c.pcnt[key], __popc(grp));
+    }
+}
+
 // ---- small faces: thread per face, queued -----------------------------------
 // Faces smaller than ~1.5 cells (the north-star resolution: ~1.3 piercing
 // lines per face over all 13 pairs) are enumerated in lattice-local FP32:
@@ -920,7 +956,10 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
     // this CTA (L1 / L2), so the exact q costs no extra DRAM pass
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         int4 r = s_rec[i];
-        if (s_base + i < c.line_cap) r = qrec_convert(c, r);
+        if (s_base + i < c.line_cap) {
+            r = qrec_convert(c, r);
+            count_qrec(c, r);
+        }
         line_store(c, s_base + i, r);
     }
 }
@@ -1004,7 +1043,11 @@ __global__ void __launch_bounds__(256, VF_RESOLVE_MINB)
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int4 rec = c.lines[e];
-        if (!((uint32_t)rec.y & kQRec)) c.lines[e] = qrec_convert(c, rec);
+        if (!((uint32_t)rec.y & kQRec)) {
+            const int4 q = qrec_convert(c, rec);
+            c.lines[e] = q;
+            count_qrec(c, q);
+        }
     }
 }
 
@@ -1022,47 +1065,6 @@ __global__ void __launch_bounds__(256, VF_RESOLVE_MINB)
 //   order-free, deterministic), the slot written once with 16-B stores.
 //   No separate -1 fill, no LUT sector read back, no block map or hash
 //   lookup per link.
-__device__ __forceinline__ void qrec_entry(const int4 rec, int k, int &i, int &j, int &kk, int &q, int &t) {
-    const int bi = rec.x & 0x7fff, bj = (rec.x >> 15) & 0x7fff, bk = rec.y & 0x7fff, R = (rec.y >> 15) & 15;
-    const uint32_t cd = ((uint32_t)rec.y >> (21 + 4 * k)) & 15u;
-    const int o = cd & 7;
-    i = bi + o * c27(2 * R + 1, 0);
-    j = bj + o * c27(2 * R + 1, 1);
-    kk = bk + o * c27(2 * R + 1, 2);
-    q = (cd >> 3) ? 2 * R + 2 : 2 * R + 1;
-    t = (i & 3) + 4 * (j & 3) + 16 * (kk & 3);
-}
-
-// a link's parent bucket key and its bucket entry octant << 41 | (q 64 + t)
-// << 30 | q bits (q in (0, 1]: 30 bits)
-__device__ __forceinline__ int32_t link_bucket_entry(const int4 rec, int k, int3 pdim, unsigned long long &x) {
-    int i, j, kk, q, t;
-    qrec_entry(rec, k, i, j, kk, q, t);
-    const int oct = ((i >> 2) & 1) + 2 * ((j >> 2) & 1) + 4 * ((kk >> 2) & 1);
-    x = ((unsigned long long)oct << 41) | ((unsigned long long)(q * 64 + t) << 30) | (uint32_t)(k ? rec.w : rec.z);
-    return (i >> 3) + pdim.x * ((j >> 3) + pdim.y * (kk >> 3));
-}
-
-// (1) per-parent link counts.  Neighbouring lines of a warp mostly share
-// parents: one counter atomic per distinct parent of the warp (__match_any_sync)
-__global__ void __launch_bounds__(256)
-    k_block_count(LinkCtx c, int3 pdim, int32_t *__restrict__ bcnt) {
-    const int64_t n = min((int64_t)*c.n_lines, c.line_cap);
-    const int lane = threadIdx.x & 31;
-    for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); e0 < n;
-         e0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t e = e0 + lane;
-        const int4 rec = e < n ? c.lines[e] : make_int4(0, 0, 0, 0);
-        const int ne = (rec.y >> 19) & 3;
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            unsigned long long x;
-            const int32_t key = k < ne ? link_bucket_entry(rec, k, pdim, x) : -1;
-            const uint32_t grp = __match_any_sync(0xffffffffu, key);
-            if (key >= 0 && lane == __ffs(grp) - 1) atomicAdd(&bcnt[key], __popc(grp));
-        }
-    }
-}
 
 // (3) links into parent order (the records are re-read; the cursor atomics'
 // returns are the latency: two records per thread in flight)
@@ -1363,9 +1365,13 @@ int link_enum_impl(const vf_config &cfg, const double *faces, int64_t F, void *w
     LevelInfo li;
     int rc = make_link_ctx(cfg, cfg.l_max - 1, F, faces, nullptr, ws, c, widen, li);
     if (rc) return rc;
-    int32_t *big = line_bufs(c, cfg, F, lines_ws);
+    BlockLinkBufs tb;
+    int32_t *big = line_bufs(c, cfg, F, lines_ws, capacity, &tb);
+    c.pcnt = tb.bcnt;
+    c.pdim = parent_dims(cfg);
     cudaMemsetAsync(c.n_band, 0, 2 * sizeof(int32_t), st);
     cudaMemsetAsync(c.n_lines, 0, 24, st);  // n_lines, n_ovf, n_big, (pad), n_tests
+    cudaMemsetAsync(tb.bcnt, 0, sizeof(int32_t) * (size_t)tb.n_max, st);
     cudaMemsetAsync(c.ovf_bits, 0, ((size_t)F + 32) / 32 * sizeof(uint32_t), st);
     kt_point("memset:link_counters");
     if (events) cudaEventRecord((cudaEvent_t)events[0], st);
@@ -1424,11 +1430,7 @@ static int link_bucket(const vf_config &cfg, LinkCtx &c, int64_t F, void *lines_
                        cudaStream_t st) {
     BlockLinkBufs tb;
     line_bufs(c, cfg, F, lines_ws, capacity, &tb);
-    cudaMemsetAsync(tb.bcnt, 0, sizeof(int32_t) * (size_t)tb.n_max, st);
-    kt_point("memset:parent_counts");
-    k_block_count<<<max_ctas(8), 256, 0, st>>>(c, parent_dims(cfg), tb.bcnt);
-    int rc = check_launch("k_block_count");
-    if (rc) return rc;
+    // (the counts were made as the records became q-records: count_qrec)
     cudaError_t e = scan_launch(LoadBlk{tb.bcnt}, EmitBlk{tb.boff, tb.bcur}, tb.n_max, nullptr, nullptr, tb.scan_ws, st);
     kt_point("scan_kernel");
     if (e != cudaSuccess) return set_cuda_error(e, "parent link scan");
