@@ -230,8 +230,9 @@ def kernel_rooflines(kt, lv, cfg, F, n_b, stats, ops, hbm, fp32, fp64, traffic):
     links = 2 * lines  # <= 2 links per recorded line (q-records)
     # enumeration: face records read once, q-records written
     b_enum = F * 96 + lines * 16
-    # parent buckets: q-records read twice, parent-ordered links written
-    b_bucket = 2 * lines * 16 + links * 8 + parents * 4
+    # parent buckets (counted as the records become q-records): q-records
+    # read once, parent-ordered links written, the parent-key scan
+    b_bucket = lines * 16 + links * 8 + parents * 12
     # LUT: every slot written once (6912 B), its links read
     b_lut = n_b * (27 * 64 * 4 + 4 + 16) + links * 8
     o = lambda k: ops.get(k, {}).get("sat_ops", 0) + ops.get(k, {}).get("other_ops", 0) if ops else None
@@ -256,8 +257,8 @@ def kernel_rooflines(kt, lv, cfg, F, n_b, stats, ops, hbm, fp32, fp64, traffic):
         ("k_links_enum", ["k_links_small", "k_links_enum", "k_links_q"], b_enum, tests * 18 if tests else None,
          "fp32", "cut-link line enumeration -> q-records (exact FP64 q); ops: 18 FP32 ops per lattice line "
          "classified (3 edge functions + tests)"),
-        ("k_link_buckets", ["k_block_count", "k_block_scatter"], b_bucket, None, None,
-         "links bucketed by finest parent key (counts + scatter)"),
+        ("k_link_buckets", ["k_block_scatter"], b_bucket, None, None,
+         "links scattered into finest-parent-key buckets (the counts are made in the enumeration)"),
         ("k_lut_blocks", ["k_lut_blocks", "k_links_band", "k_links_ovf", "k_links_full"], b_lut, None, None,
          "LUT slots written once from shared memory (-1 + min-merged links); exact band / overflow paths"),
     ]
