@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(kLinkWarps * 32, MODE == 1 ? 1 : VF_LINK_MINB)
 // hence the LUT are identical.  Larger faces are appended to a list for the
 // warp-flattened kernel.
 #ifndef VF_SMALL_MINB
-#define VF_SMALL_MINB 4
+#define VF_SMALL_MINB 8
 #endif
 static float g_small_ext = 1.5f;  // vf_set_link_small_ext (test / tuning hook)
 
@@ -634,7 +634,7 @@ __device__ __forceinline__ void line_store(const LinkCtx &c, int pos, int4 rec) 
 // reservation per CTA (a per-warp-per-pair atomicAdd on the shared line
 // counter was the kernel's top stall); a full stage falls back to direct slots
 #ifndef VF_SMALL_THREADS
-#define VF_SMALL_THREADS 256
+#define VF_SMALL_THREADS 128
 #endif
 constexpr int kLineStage = 4 * VF_SMALL_THREADS;
 
