@@ -802,9 +802,12 @@ __global__ void __launch_bounds__(VF_SMALL_THREADS, VF_SMALL_MINB)
                 Q.V1[d] = (float)((v[3 + d] - v[d]) * c.inv_dx);
                 Q.V2[d] = (float)((v[6 + d] - v[d]) * c.inv_dx);
                 Q.nf[d] = (float)nn[d];
-                // nodes within one link of the face AABB (k_links' fallback range)
-                Q.lo[d] = (short)max((int)floor((flo[d] - c.dx - 2.0 * c.eps) * c.inv_dx - 0.5) - widen, 0);
-                Q.hi[d] = (short)min((int)floor((fhi[d] + c.dx + 2.0 * c.eps) * c.inv_dx - 0.5) + 1 + widen,
+                // nodes within one link of the face AABB (k_links' fallback
+                // range), from the lattice-local frame in FP32 and widened by
+                // 1e-3 cells (a superset only adds exactly-tested nodes)
+                const float mn = fminf(0.0f, fminf(Q.V1[d], Q.V2[d])), mx = fmaxf(0.0f, fmaxf(Q.V1[d], Q.V2[d]));
+                Q.lo[d] = (short)max(Q.b[d] + (int)floorf(Q.w[d] + mn - 1.0f - 2.0f * c.epsL - 1e-3f) - widen, 0);
+                Q.hi[d] = (short)min(Q.b[d] + (int)floorf(Q.w[d] + mx + 1.0f + 2.0f * c.epsL + 1e-3f) + 1 + widen,
                                      c.cells[d] - 1);
             }
             Q.ff9 = 4e-6f * (extL + 2.0f);
