@@ -659,18 +659,24 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
         rec(events, n_ev, &k, st);  // voxelization done
         if (L == cfg->l_max - 1) break;
         VF_TRY(mark_impl(*cfg, g, L, w.mark_ws, w.mark_b, st));
-        VF_TRY(adapt_impl(*cfg, g, L, w.adapt_ws, w.adapt_b, st));
-        // level L+1's row order beside its bins and voxelization
+        VF_TRY(adapt_impl(*cfg, g, L, w.adapt_ws, w.adapt_b, st, false));
+        // level L+1's row order beside its bins and voxelization, then level
+        // L's neighbour-child links / interface layer (outputs only)
         cudaStream_t s4 = one ? st : side->st4;
         cudaEventRecord(side->adapted, st);
         cudaStreamWaitEvent(s4, side->adapted, 0);
         VF_TRY(rows_next_impl(g, L, w.prop_ws, s4));
         cudaEventRecord(side->rowsok, s4);
+        VF_TRY(adapt_links_impl(g, L, s4));
         rec(events, n_ev, &k, st);  // refinement done
     }
-    // join the side stream (required to end a capture; bins are all consumed)
+    // join the side streams (required to end a capture; bins are all consumed)
     cudaEventRecord(side->join, s2);
     cudaStreamWaitEvent(st, side->join, 0);
+    if (!one && cfg->l_max > 1) {
+        cudaEventRecord(side->adapted, side->st4);
+        cudaStreamWaitEvent(st, side->adapted, 0);
+    }
     VF_TRY(boundary_impl(*cfg, g, w.bcount, st));
     VF_TRY(tables_impl(g, w.bcount, cmap, d_n_b, w.tab_ws, w.tab_b, st,
                        link_slot_inverse(*cfg, F, w.lines_ws, g->capacity)));

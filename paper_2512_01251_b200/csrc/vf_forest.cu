@@ -405,7 +405,8 @@ size_t adapt_workspace_size(int32_t capacity) {
            al256(scan_workspace_bytes(capacity));
 }
 
-int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_bytes, cudaStream_t st) {
+int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_bytes, cudaStream_t st,
+               bool links) {
     if (ws_bytes < adapt_workspace_size(g->capacity)) return set_error(VF_EARG, "adapt workspace too small");
     if (L != g->n_levels - 1 || L + 1 >= VF_MAX_LEVELS) return set_error(VF_EARG, "adapt: level must be the finest");
     char *base = (char *)ws;
@@ -425,11 +426,17 @@ int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_byte
         g->d_level_start, scalars + 1, parents, g->d_coords, g->d_nbr, g->d_nbr_child, g->d_child,
         g->d_bflags, g->d_masks, g->d_status, g->d_solid64);
     if ((rc = check_launch("k_adapt_children"))) return rc;
+    g->n_levels = L + 2;
+    return links ? adapt_links_impl(g, L, st) : VF_OK;
+}
+
+// level L's neighbour-child links and interface layer (after its children
+// exist): outputs only -- no later stage of the embed reads them -- so the
+// embed runs them on a side stream
+int adapt_links_impl(vf_grid *g, int L, cudaStream_t st) {
     k_adapt_level<<<max_ctas(8), 256, 0, st>>>(L, g->d_level_start, g->d_nbr, g->d_nbr_child,
                                                g->d_child, g->d_masks);
-    if ((rc = check_launch("k_adapt_level"))) return rc;
-    g->n_levels = L + 2;
-    return VF_OK;
+    return check_launch("k_adapt_level");
 }
 
 }  // namespace vf

@@ -132,8 +132,11 @@ size_t mark_workspace_size(int32_t capacity);
 int mark_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_bytes,
               cudaStream_t st);
 size_t adapt_workspace_size(int32_t capacity);
+// links = false: the trailing neighbour-child / interface kernel is left to
+// the caller (adapt_links_impl, after the children)
 int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_bytes,
-               cudaStream_t st);
+               cudaStream_t st, bool links = true);
+int adapt_links_impl(vf_grid *g, int L, cudaStream_t st);
 
 // boundary / tables / links
 int boundary_impl(const vf_config &cfg, vf_grid *g, int32_t *bcount, cudaStream_t st);
