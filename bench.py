@@ -301,7 +301,8 @@ def ncu_kernel_traffic(config):
         return None
     k = dict(d.get("kernels", {}))
     # kernel-timer names (check_launch) that differ from the device symbols
-    for kt_name, sym in (("k_pairs", "k_pairs_append"), ("k_adapt_children", "k_adapt_children_t")):
+    for kt_name, sym in (("k_pairs", "k_pairs_append"), ("k_adapt_children", "k_adapt_children_t"),
+                         ("k_links_small", "k_links_smallq")):
         if sym in k:
             k[kt_name] = k[sym]
     return k
@@ -602,8 +603,8 @@ def main():
         achieved = link_bytes / (lk / 1e3) / 1e9
         roofline = {"kernel": "cut-link group", "bound": "hbm", "achieved": achieved, "peak": peak,
                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": ncu_traffic(args.config, "k_links_small", "k_links_enum", "k_links_q",
-                                           "k_block_count", "k_block_scatter", "k_lut_blocks"),
+                    "traffic": ncu_traffic(args.config, "k_links_smallq", "k_links_enum", "k_links_q",
+                                           "k_block_scatter", "k_lut_blocks"),
                     "kernel_ms": lk, "algorithmic_bytes": int(link_bytes),
                     "kernel_ms_overlapped": med(link_ovl),
                     "timed": "CUDA events around the cut-link kernels run alone (vf_set_serial_links): "

@@ -19,5 +19,5 @@ timeout 1500 ncu --set full --clock-control none -s $SKIP -c 80 -o /tmp/full_c4 
 cp profiles/ncu_traffic.json gpurun_out/ncu_traffic.json 2>/dev/null
 python tools/ncu_traffic.py /tmp/full_c4.ncu-rep c4 > gpurun_out/r02_ncu_full_c4.txt 2>&1
 cp profiles/ncu_traffic.json gpurun_out/ncu_traffic_new.json
-timeout 1200 python bench.py --impl reference > gpurun_out/r02_bench_ref_c4.json 2> gpurun_out/r02_bench_ref_c4.err
+# (reference arm: run separately, ~4 min)
 tail -c 400 gpurun_out/r02_bench_c4.json; cat gpurun_out/r02_ncu_full_c4.txt | head -40
