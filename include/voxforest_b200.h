@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define VF_ABI_VERSION 5
+#define VF_ABI_VERSION 6
 #define VF_MAX_LEVELS 16
 
 /* status codes (SURVEY.md §8b "Errors") */
@@ -331,8 +331,9 @@ int vf_lbm_init(const vf_grid *grid, int32_t s, int32_t e, double rho, const dou
                 float *d_f, void *stream);
 /* one step: d_fout = collide(stream(d_fin)); the wall-link momentum exchange
  * is ADDED to d_force[3] (lattice units) when d_force is not NULL, summed in
- * block order (deterministic).  d_scratch: 7 (e - s) + 4 int32 (the wall-link
- * block list of the step, then 3 doubles of per-block force partials) */
+ * block order (deterministic).  d_scratch: 7 (e - s) + 4 int32 (the list of
+ * blocks with a non-simple cell -- SOLID / GHOST / next to a wall, a missing
+ * block or the domain boundary -- then 3 doubles of per-block force partials) */
 int vf_lbm_step(const vf_config *cfg, const vf_grid *grid, int level, int32_t s, int32_t e,
                 const int32_t *d_cmap, const float *d_lengths, const float *d_fin,
                 float *d_fout, const vf_flow *flow, double *d_force, int32_t *d_scratch,
@@ -343,18 +344,19 @@ int vf_lbm_step(const vf_config *cfg, const vf_grid *grid, int level, int32_t s,
  * vf_lbm_parents: d_parent[b] = parent block of every child (-1 elsewhere)
  * over ids [0, n_blocks).
  * vf_lbm_fill_ghosts: fine GHOST cells <- tensor-product interpolation
+ * ([sf, ef) a whole level >= 1: groups of 8 siblings, else VF_EARG)
  * (order 3 cubic / 1 linear / 0 copy, falling back when a stencil cell is
  * outside the level or SOLID) of (1 - theta) fc_old + theta fc_new, then
  * f = feq + alpha (f - feq) (alpha = 1: no rescale).
  * vf_lbm_restrict: coarse cells of refined blocks (not SOLID / INTERFACE /
  * GHOST, no GHOST child) <- mean of their non-SOLID children, rescaled by
- * beta. */
+ * beta ([sf, ef) whole sibling groups as for the fill; d_parent as there). */
 int vf_lbm_parents(const vf_grid *grid, int32_t n_blocks, int32_t *d_parent, void *stream);
 int vf_lbm_fill_ghosts(const vf_grid *grid, int32_t sf, int32_t ef, int32_t sc, int32_t ec,
                        const int32_t *d_parent, const float *d_fc_old, const float *d_fc_new,
                        double theta, double alpha, int order, float *d_ff, void *stream);
 int vf_lbm_restrict(const vf_grid *grid, int32_t sc, int32_t ec, int32_t sf, int32_t ef,
-                    const float *d_ff, double beta, float *d_fc, void *stream);
+                    const int32_t *d_parent, const float *d_ff, double beta, float *d_fc, void *stream);
 /* copy the grid's latched device status to the host (synchronizes) */
 int vf_check_status(const vf_grid *grid, void *stream);
 /* test hook: capacity of the link-length band list (candidates the FP32

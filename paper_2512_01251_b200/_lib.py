@@ -15,7 +15,7 @@ from .errors import (BinCapError, CapacityError, CudaError, MeshError, Voxforest
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # VF_LIB_PATH: an alternative in-tree build of the same library (A/B kernel experiments)
 LIB_PATH = os.environ.get("VF_LIB_PATH") or os.path.join(_HERE, "libvoxforest_b200.so")
-ABI_VERSION = 5
+ABI_VERSION = 6
 MAX_LEVELS = 16
 
 # cell masks / block flags / neighbour codes (voxforest_b200.h)
@@ -121,7 +121,7 @@ _SIGS = {
     "vf_lbm_parents": (_I32, [_GP, C.c_int32, _P, _P]),
     "vf_lbm_fill_ghosts": (_I32, [_GP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, C.c_double,
                                   C.c_double, _I32, _P, _P]),
-    "vf_lbm_restrict": (_I32, [_GP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_double, _P, _P]),
+    "vf_lbm_restrict": (_I32, [_GP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P, C.c_double, _P, _P]),
 }
 
 EXPORTED = tuple(_SIGS)

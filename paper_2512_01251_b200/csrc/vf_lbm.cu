@@ -14,9 +14,9 @@
 //   q = opp(o)); inlet / outlet / SBB on the domain faces;
 //   moments, BGK relaxation to the second-order equilibrium, store.
 // GHOST cells are held (interface exchange), SOLID cells untouched.  The
-// momentum exchange of the wall links is reduced per warp and accumulated in
-// FP64.  Bytes per fluid cell: 27 x 4 read + 27 x 4 written (+ 64 B masks
-// per block): HBM-bound.
+// momentum exchange of the wall links is reduced per block and accumulated
+// in FP64.  Bytes per cell: 27 x 4 read + 27 x 4 written (+ 1 B mask, 108 +
+// 216 B of neighbour ids / solid words per block): HBM-bound.
 #include "vf_common.cuh"
 #include "vf_internal.h"
 
@@ -40,172 +40,313 @@ __device__ __forceinline__ int32_t cell_at(const int32_t *__restrict__ nbr, int3
     return __ldg(nbr + 27 * (int64_t)b + slot_of(ox, oy, oz));
 }
 
-// Warp per block (two 32-cell halves): the block's 27 neighbour ids, their
-// solid64 words (finalize; bit t = cell t SOLID) and the block's x index are
-// staged in per-warp shared memory, indexed by direction code
-// (dx+1) + 3(dy+1) + 9(dz+1), so a pulled population costs one shared-memory
-// lookup and one global load that is coalesced within a block.  Domain faces
-// (lateral SBB, inlet velocity bounce-back, outlet anti-bounce-back) are
-// resolved inline.  WALLS = false is the bulk pass over every block: a wall
-// link gets a provisional SBB value and its block is appended to the wall
-// list; WALLS = true re-runs the listed blocks with the wall rule (SBB or
-// Bouzidi linear IBB with q_w from the LUT) and the momentum exchange, and
-// overwrites those cells (same f_in, so the two passes commute).
+// A step is two passes over the level's blocks, split by cell.  A cell is
+// SIMPLE when it is not GHOST and none of the 27 cells around it (itself
+// included) is SOLID or outside the level / domain: its pull needs no
+// boundary rule.  The simple set of a block is one 64-bit word, the
+// 26-neighbour dilation (dil_x/y/z) of the "bad" words of the 27 blocks
+// around it (solid64; every cell of a missing or outside neighbour is bad).
+//   k_lbm_bulk    every block, its simple cells only: 27 unconditional
+//                 pulls through a per-CTA table (source neighbour code and
+//                 cell of population o at cell t), BGK, store.  Blocks with
+//                 any other cell are appended to a list.
+//   k_lbm_special the listed blocks, their other cells only: SOLID / GHOST
+//                 held, domain faces (lateral SBB, inlet velocity
+//                 bounce-back, outlet anti-bounce-back), wall links (SBB or
+//                 Bouzidi linear IBB with q_w from the LUT) with the
+//                 momentum exchange.
+// The passes write disjoint cells from the same f_in, so they commute.
 constexpr int kLbmWarps = 8;
 #ifndef VF_LBM_MINB
-#define VF_LBM_MINB 3
+#define VF_LBM_MINB 4
+#endif
+#ifndef VF_LBM_FUSED_MINB  // fused variant (-DVF_LBM_FUSED): measured slower
+#define VF_LBM_FUSED_MINB 3
+#endif
+#ifndef VF_LBM_SPECIAL_MINB
+#define VF_LBM_SPECIAL_MINB 3
 #endif
 
-template <bool WALLS>
+// bad words of the 27 blocks around b (code (dx+1) + 3(dy+1) + 9(dz+1)) ->
+// the simple cells of b (ghost: the block's GHOST cells)
+__device__ __forceinline__ uint64_t simple_cells(const unsigned long long *bad, uint64_t ghost) {
+    uint64_t pl[3];
+#pragma unroll
+    for (int dz = 0; dz < 3; ++dz) {
+        uint64_t col[3];
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy) {
+            const int c = 3 * dy + 9 * dz;
+            col[dy] = dil_x(bad[c], bad[c + 1], bad[c + 2]);
+        }
+        pl[dz] = dil_y(col[0], col[1], col[2]);
+    }
+    return ~(dil_z(pl[0], pl[1], pl[2]) | ghost);
+}
+
+// stage the 27 neighbour ids (code order) and bad words of block b; returns
+// the block's GHOST cells (bit t)
+__device__ __forceinline__ uint64_t stage_block(int32_t s, int32_t e, int32_t b, int lane,
+                                                const int32_t *__restrict__ nbr,
+                                                const uint8_t *__restrict__ masks,
+                                                const uint64_t *__restrict__ solid64, int32_t *nb,
+                                                unsigned long long *bad) {
+    if (lane < 27) {
+        const int dx = lane % 3 - 1, dy = (lane / 3) % 3 - 1, dz = lane / 9 - 1;
+        const int32_t v = (lane == 13) ? b : __ldg(nbr + 27 * (int64_t)b + slot_of(dx, dy, dz));
+        nb[lane] = v;
+        bad[lane] = (v >= s && v < e) ? __ldg(reinterpret_cast<const unsigned long long *>(solid64) + v) : ~0ull;
+    }
+    const bool g0 = masks[64 * (int64_t)b + lane] == VF_GHOST, g1 = masks[64 * (int64_t)b + lane + 32] == VF_GHOST;
+    const uint64_t ghost = (uint64_t)__ballot_sync(0xffffffffu, g0) | ((uint64_t)__ballot_sync(0xffffffffu, g1) << 32);
+    __syncwarp();
+    return ghost;
+}
+
+// source of population o at cell t: (neighbour code << 6) | cell
+__device__ __forceinline__ uint16_t pull_entry(int o, int t) {
+    const int X = (t & 3) - c27(o, 0), Y = ((t >> 2) & 3) - c27(o, 1), Z = (t >> 4) - c27(o, 2);
+    const int code = ((X >> 2) + 1) + 3 * ((Y >> 2) + 1) + 9 * ((Z >> 2) + 1);
+    return (uint16_t)((code << 6) | ((X & 3) + 4 * (Y & 3) + 16 * (Z & 3)));
+}
+
+// BGK relaxation of the pulled populations of cell x to the second-order
+// equilibrium, stored to fout
+__device__ __forceinline__ void bgk_store(float *f, float omega, float *__restrict__ fout, int64_t n, int64_t x) {
+    float rho = 0.f, u0 = 0.f, u1 = 0.f, u2 = 0.f;
+#pragma unroll
+    for (int o = 0; o < 27; ++o) {
+        rho += f[o];
+        u0 += f[o] * c27(o, 0);
+        u1 += f[o] * c27(o, 1);
+        u2 += f[o] * c27(o, 2);
+    }
+    const float ir = 1.0f / rho;
+    u0 *= ir; u1 *= ir; u2 *= ir;
+    const float uu = 1.5f * (u0 * u0 + u1 * u1 + u2 * u2);
+#pragma unroll
+    for (int o = 0; o < 27; ++o) {
+        const float cu = c27(o, 0) * u0 + c27(o, 1) * u1 + c27(o, 2) * u2;
+        const float feq = c_lw[o] * rho * (1.0f + 3.0f * cu + 4.5f * cu * cu - uu);
+        fout[o * n + x] = f[o] + (feq - f[o]) * omega;
+    }
+}
+
 __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_MINB)
-    k_lbm_cells(int32_t s, int32_t e, int cells_x, const int32_t *__restrict__ coords,
-                const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
-                const uint64_t *__restrict__ solid64, const int32_t *__restrict__ cmap,
-                const float *__restrict__ lengths, const float *__restrict__ fin,
-                float *__restrict__ fout, vf_flow flow, int32_t *__restrict__ wall_list,
-                int32_t *__restrict__ n_wall, double *__restrict__ part) {
+    k_lbm_bulk(int32_t s, int32_t e, const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
+               const uint64_t *__restrict__ solid64, const float *__restrict__ fin, float *__restrict__ fout,
+               float omega, int32_t *__restrict__ list, int32_t *__restrict__ n_list) {
+    __shared__ uint16_t s_pull[27 * 64];
     __shared__ int32_t s_nb[kLbmWarps][27];
-    __shared__ unsigned long long s_sol[kLbmWarps][27];
+    __shared__ unsigned long long s_bad[kLbmWarps][27];
+    for (int i = threadIdx.x; i < 27 * 64; i += blockDim.x) s_pull[i] = pull_entry(i >> 6, i & 63);
+    __syncthreads();
     const int64_t n = (int64_t)(e - s) * 64;
-    const int nitems = WALLS ? *n_wall : e - s;
-    const float omega = 1.0f / (float)flow.tau;
-    const float uin[3] = {(float)flow.u_in[0], (float)flow.u_in[1], (float)flow.u_in[2]};
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int it = blockIdx.x * kLbmWarps + w; it < nitems; it += gridDim.x * kLbmWarps) {
-        float Fx = 0.f, Fy = 0.f, Fz = 0.f;  // this block's wall momentum exchange
-        const int lb = WALLS ? wall_list[it] : it;
+    for (int lb = blockIdx.x * kLbmWarps + w; lb < e - s; lb += gridDim.x * kLbmWarps) {
         const int32_t b = s + lb;
         __syncwarp();
-        if (lane < 27) {
-            const int dx = lane % 3 - 1, dy = (lane / 3) % 3 - 1, dz = lane / 9 - 1;
-            const int32_t v = (lane == 13) ? b : __ldg(nbr + 27 * (int64_t)b + slot_of(dx, dy, dz));
-            s_nb[w][lane] = v;
-            s_sol[w][lane] = (v >= s && v < e)
-                                 ? __ldg(reinterpret_cast<const unsigned long long *>(solid64) + v)
-                                 : ~0ull;
-        }
-        const int bx = __ldg(coords + 4 * (int64_t)b);
-        const int32_t slot = (WALLS && flow.ibb) ? cmap[b] : -1;
+        const uint64_t ghost = stage_block(s, e, b, lane, nbr, masks, solid64, s_nb[w], s_bad[w]);
+        const uint64_t simple = simple_cells(s_bad[w], ghost);
+        if (lane < 27) s_nb[w][lane] = (s_nb[w][lane] - s) * 64;  // pulls only reach level cells
         __syncwarp();
-        bool wall_blk = false;
+        if (simple != ~0ull && lane == 0) list[atomicAdd(n_list, 1)] = lb;
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
             const int t = lane + 32 * h;
-            const int I = t & 3, J = (t >> 2) & 3, K = t >> 4;
-            const int64_t x = (int64_t)lb * 64 + t;
-            const uint8_t m = masks[64 * (int64_t)b + t];
-            if (m == VF_SOLID || m == VF_GHOST) {
-                if (!WALLS) {
+            if (!((simple >> t) & 1ull)) continue;
+            float f[27];
 #pragma unroll
-                    for (int q = 0; q < 27; ++q) fout[q * n + x] = fin[q * n + x];
-                }
+            for (int o = 0; o < 27; ++o) {
+                const uint32_t p = s_pull[o * 64 + t];
+                f[o] = __ldg(fin + o * n + (s_nb[w][p >> 6] + (int)(p & 63u)));
+            }
+            bgk_store(f, omega, fout, n, (int64_t)lb * 64 + t);
+        }
+    }
+}
+
+// the special cells of block b (staged: nb ids, sol words, ghost), packed
+// onto the lanes (k-th set bit of spec); wall momentum exchange into F
+__device__ __forceinline__ void special_cells(int32_t s, int32_t e, int cells_x, int32_t b, int lb, int lane,
+                                              uint64_t ghost, uint64_t spec, const int32_t *nb,
+                                              const unsigned long long *sol, const uint16_t *s_pull,
+                                              const int32_t *__restrict__ coords, const int32_t *__restrict__ cmap,
+                                              const float *__restrict__ lengths, const float *__restrict__ fin,
+                                              float *__restrict__ fout, const vf_flow &flow, float &Fx, float &Fy,
+                                              float &Fz) {
+    const int64_t n = (int64_t)(e - s) * 64;
+    const float omega = 1.0f / (float)flow.tau;
+    const float uin[3] = {(float)flow.u_in[0], (float)flow.u_in[1], (float)flow.u_in[2]};
+    const uint64_t held = ghost | sol[13];
+    const int bx = __ldg(coords + 4 * (int64_t)b);
+    const int32_t slot = flow.ibb ? cmap[b] : -1;
+    // the block's special cells, packed onto the lanes (k-th set bit)
+    const uint32_t lo = (uint32_t)spec, hi = (uint32_t)(spec >> 32);
+    const int nlo = __popc(lo), cnt = nlo + __popc(hi);
+#pragma unroll 1
+    for (int k0 = 0; k0 < cnt; k0 += 32) {
+        const int k = k0 + lane;
+        if (k >= cnt) continue;
+        const int t = k < nlo ? (int)__fns(lo, 0, k + 1) : 32 + (int)__fns(hi, 0, k - nlo + 1);
+        const int64_t x = (int64_t)lb * 64 + t;
+        if ((held >> t) & 1ull) {  // SOLID / GHOST: held
+#pragma unroll
+            for (int q = 0; q < 27; ++q) fout[q * n + x] = fin[q * n + x];
+            continue;
+        }
+        const int I = t & 3;
+        // outlet cells (x = l_x face): velocity of x for the anti-bounce-back
+        float v0 = 0.f, v1 = 0.f, v2 = 0.f;
+        if (flow.open_x && 4 * bx + I == cells_x - 1) {
+            float rx = 0.f;
+#pragma unroll
+            for (int q = 0; q < 27; ++q) {
+                const float v = fin[q * n + x];
+                rx += v;
+                v0 += v * c27(q, 0);
+                v1 += v * c27(q, 1);
+                v2 += v * c27(q, 2);
+            }
+            v0 /= rx; v1 /= rx; v2 /= rx;
+        }
+        float f[27];
+#pragma unroll
+        for (int o = 0; o < 27; ++o) {
+            const uint32_t p = s_pull[o * 64 + t];
+            const int code = (int)(p >> 6), ty = (int)(p & 63u);
+            const int32_t y = nb[code];
+            if (!((sol[code] >> ty) & 1ull)) {  // a level cell that is not SOLID
+                f[o] = fin[o * n + (int64_t)(y - s) * 64 + ty];
                 continue;
             }
-            // outlet cells (x = l_x face): velocity of x for the anti-bounce-back
-            float v0 = 0.f, v1 = 0.f, v2 = 0.f;
-            if (flow.open_x && 4 * bx + I == cells_x - 1) {
-                float rx = 0.f;
-#pragma unroll
-                for (int k = 0; k < 27; ++k) {
-                    const float v = fin[k * n + x];
-                    rx += v;
-                    v0 += v * c27(k, 0);
-                    v1 += v * c27(k, 1);
-                    v2 += v * c27(k, 2);
+            const int q = o == 0 ? 0 : ((o & 1) ? o + 1 : o - 1);
+            const float fq = fin[q * n + x];
+            float v = fq;  // SBB: lateral faces, SBB walls
+            if (y == VF_NB_OUTSIDE) {
+                const int gx = 4 * bx + I - c27(o, 0);
+                if (flow.open_x && gx < 0) {  // inlet: velocity bounce-back, rho_w = 1
+                    v -= 6.0f * c_lw[q] * (c27(q, 0) * uin[0] + c27(q, 1) * uin[1] + c27(q, 2) * uin[2]);
+                } else if (flow.open_x && gx >= cells_x) {  // outlet: anti-bounce-back, rho_w = 1
+                    const float cq = c27(q, 0) * v0 + c27(q, 1) * v1 + c27(q, 2) * v2;
+                    v = -fq + 2.0f * c_lw[q] * (1.0f + 4.5f * cq * cq - 1.5f * (v0 * v0 + v1 * v1 + v2 * v2));
                 }
-                v0 /= rx; v1 /= rx; v2 /= rx;
-            }
-            float f[27];
-            bool wall = false;
-#pragma unroll
-            for (int o = 0; o < 27; ++o) {
-                const int X = I - c27(o, 0), Y = J - c27(o, 1), Z = K - c27(o, 2);
-                const int code = ((X >> 2) + 1) + 3 * ((Y >> 2) + 1) + 9 * ((Z >> 2) + 1);
-                const int ty = (X & 3) + 4 * (Y & 3) + 16 * (Z & 3);
-                const int32_t y = s_nb[w][code];
-                if (!((s_sol[w][code] >> ty) & 1ull)) {  // a level cell that is not SOLID
-                    f[o] = fin[o * n + (int64_t)(y - s) * 64 + ty];
-                    continue;
+            } else {  // wall link x -> y (SOLID cell, or a missing block next to ghosts)
+                const float qw = slot >= 0 ? lengths[((int64_t)slot * 27 + q) * 64 + t] : -1.0f;
+                if (qw > 0.0f && qw < 0.5f) {
+                    // second node behind x: x + c_o = x - c_q (the source of population q)
+                    const uint32_t p2 = s_pull[q * 64 + t];
+                    const int code2 = (int)(p2 >> 6), tz = (int)(p2 & 63u);
+                    if (!((sol[code2] >> tz) & 1ull))
+                        v = 2.0f * qw * fq + (1.0f - 2.0f * qw) *
+                                                 fin[q * n + (int64_t)(nb[code2] - s) * 64 + tz];
+                } else if (qw >= 0.5f) {
+                    v = fq / (2.0f * qw) + (2.0f * qw - 1.0f) / (2.0f * qw) * fin[o * n + x];
                 }
-                const int q = o == 0 ? 0 : ((o & 1) ? o + 1 : o - 1);
-                const float fq = fin[q * n + x];
-                float v = fq;  // SBB: lateral faces, SBB walls (provisional in the bulk pass)
-                if (y == VF_NB_OUTSIDE) {
-                    const int gx = 4 * bx + X;
-                    if (flow.open_x && gx < 0) {  // inlet: velocity bounce-back, rho_w = 1
-                        v -= 6.0f * c_lw[q] * (c27(q, 0) * uin[0] + c27(q, 1) * uin[1] + c27(q, 2) * uin[2]);
-                    } else if (flow.open_x && gx >= cells_x) {  // outlet: anti-bounce-back, rho_w = 1
-                        const float cq = c27(q, 0) * v0 + c27(q, 1) * v1 + c27(q, 2) * v2;
-                        v = -fq + 2.0f * c_lw[q] * (1.0f + 4.5f * cq * cq - 1.5f * (v0 * v0 + v1 * v1 + v2 * v2));
-                    }
-                } else {  // wall link x -> y (SOLID cell, or a missing block next to ghosts)
-                    wall = true;
-                    if (WALLS) {
-                        const float qw = slot >= 0 ? lengths[((int64_t)slot * 27 + q) * 64 + t] : -1.0f;
-                        if (qw > 0.0f && qw < 0.5f) {
-                            // second node behind x: x + c_o = x - c_q
-                            const int X2 = I + c27(o, 0), Y2 = J + c27(o, 1), Z2 = K + c27(o, 2);
-                            const int code2 = ((X2 >> 2) + 1) + 3 * ((Y2 >> 2) + 1) + 9 * ((Z2 >> 2) + 1);
-                            const int tz = (X2 & 3) + 4 * (Y2 & 3) + 16 * (Z2 & 3);
-                            if (!((s_sol[w][code2] >> tz) & 1ull))
-                                v = 2.0f * qw * fq + (1.0f - 2.0f * qw) *
-                                                         fin[q * n + (int64_t)(s_nb[w][code2] - s) * 64 + tz];
-                        } else if (qw >= 0.5f) {
-                            v = fq / (2.0f * qw) + (2.0f * qw - 1.0f) / (2.0f * qw) * fin[o * n + x];
-                        }
-                        Fx += (fq + v) * c27(q, 0);
-                        Fy += (fq + v) * c27(q, 1);
-                        Fz += (fq + v) * c27(q, 2);
-                    }
-                }
-                f[o] = v;
+                Fx += (fq + v) * c27(q, 0);
+                Fy += (fq + v) * c27(q, 1);
+                Fz += (fq + v) * c27(q, 2);
             }
-            wall_blk |= wall;
-            if (WALLS && !wall) continue;  // the bulk pass's value is exact
-            float rho = 0.f, u0 = 0.f, u1 = 0.f, u2 = 0.f;
-#pragma unroll
-            for (int o = 0; o < 27; ++o) {
-                rho += f[o];
-                u0 += f[o] * c27(o, 0);
-                u1 += f[o] * c27(o, 1);
-                u2 += f[o] * c27(o, 2);
-            }
-            const float ir = 1.0f / rho;
-            u0 *= ir; u1 *= ir; u2 *= ir;
-            const float uu = 1.5f * (u0 * u0 + u1 * u1 + u2 * u2);
-#pragma unroll
-            for (int o = 0; o < 27; ++o) {
-                const float cu = c27(o, 0) * u0 + c27(o, 1) * u1 + c27(o, 2) * u2;
-                const float feq = c_lw[o] * rho * (1.0f + 3.0f * cu + 4.5f * cu * cu - uu);
-                fout[o * n + x] = f[o] + (feq - f[o]) * omega;
-            }
+            f[o] = v;
         }
-        if (!WALLS && __any_sync(0xffffffffu, wall_blk) && lane == 0)
-            wall_list[atomicAdd(n_wall, 1)] = lb;
-        if (WALLS && part) {
-            // per-block partial: a fixed lane tree, stored at the block's
-            // local id -- independent of which warp took the block
+        bgk_store(f, omega, fout, n, x);
+    }
+}
+
+// per-block force partial: a fixed lane tree, stored at the block's local
+// id -- independent of which warp took the block
+__device__ __forceinline__ void block_force(double *part, int lb, int lane, float Fx, float Fy, float Fz) {
+    __syncwarp();
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                Fx += __shfl_xor_sync(0xffffffffu, Fx, off);
-                Fy += __shfl_xor_sync(0xffffffffu, Fy, off);
-                Fz += __shfl_xor_sync(0xffffffffu, Fz, off);
+    for (int off = 16; off > 0; off >>= 1) {
+        Fx += __shfl_xor_sync(0xffffffffu, Fx, off);
+        Fy += __shfl_xor_sync(0xffffffffu, Fy, off);
+        Fz += __shfl_xor_sync(0xffffffffu, Fz, off);
+    }
+    if (lane == 0) {
+        part[3 * (int64_t)lb + 0] = (double)Fx;
+        part[3 * (int64_t)lb + 1] = (double)Fy;
+        part[3 * (int64_t)lb + 2] = (double)Fz;
+    }
+}
+
+__global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_SPECIAL_MINB)
+    k_lbm_special(int32_t s, int32_t e, int cells_x, const int32_t *__restrict__ coords,
+                  const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
+                  const uint64_t *__restrict__ solid64, const int32_t *__restrict__ cmap,
+                  const float *__restrict__ lengths, const float *__restrict__ fin,
+                  float *__restrict__ fout, vf_flow flow, const int32_t *__restrict__ list,
+                  const int32_t *__restrict__ n_list, double *__restrict__ part) {
+    __shared__ uint16_t s_pull[27 * 64];
+    __shared__ int32_t s_nb[kLbmWarps][27];
+    __shared__ unsigned long long s_sol[kLbmWarps][27];
+    for (int i = threadIdx.x; i < 27 * 64; i += blockDim.x) s_pull[i] = pull_entry(i >> 6, i & 63);
+    __syncthreads();
+    const int nitems = *n_list;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int it = blockIdx.x * kLbmWarps + w; it < nitems; it += gridDim.x * kLbmWarps) {
+        float Fx = 0.f, Fy = 0.f, Fz = 0.f;  // this block's wall momentum exchange
+        const int lb = list[it];
+        const int32_t b = s + lb;
+        __syncwarp();
+        const uint64_t ghost = stage_block(s, e, b, lane, nbr, masks, solid64, s_nb[w], s_sol[w]);
+        const uint64_t spec = ~simple_cells(s_sol[w], ghost);  // the cells of this pass
+        special_cells(s, e, cells_x, b, lb, lane, ghost, spec, s_nb[w], s_sol[w], s_pull, coords, cmap, lengths,
+                      fin, fout, flow, Fx, Fy, Fz);
+        if (part) block_force(part, lb, lane, Fx, Fy, Fz);
+    }
+}
+
+// fused step: every block's simple cells (fast pulls), then its special
+// cells (the general path) in the same warp
+__global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_FUSED_MINB)
+    k_lbm_cells(int32_t s, int32_t e, int cells_x, const int32_t *__restrict__ coords,
+                const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
+                const uint64_t *__restrict__ solid64, const int32_t *__restrict__ cmap,
+                const float *__restrict__ lengths, const float *__restrict__ fin, float *__restrict__ fout,
+                vf_flow flow, double *__restrict__ part) {
+    __shared__ uint16_t s_pull[27 * 64];
+    __shared__ int32_t s_nb[kLbmWarps][27], s_off[kLbmWarps][27];
+    __shared__ unsigned long long s_sol[kLbmWarps][27];
+    for (int i = threadIdx.x; i < 27 * 64; i += blockDim.x) s_pull[i] = pull_entry(i >> 6, i & 63);
+    __syncthreads();
+    const int64_t n = (int64_t)(e - s) * 64;
+    const float omega = 1.0f / (float)flow.tau;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int lb = blockIdx.x * kLbmWarps + w; lb < e - s; lb += gridDim.x * kLbmWarps) {
+        const int32_t b = s + lb;
+        __syncwarp();
+        const uint64_t ghost = stage_block(s, e, b, lane, nbr, masks, solid64, s_nb[w], s_sol[w]);
+        const uint64_t simple = simple_cells(s_sol[w], ghost);
+        if (lane < 27) s_off[w][lane] = (s_nb[w][lane] - s) * 64;  // used for level cells only
+        __syncwarp();
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const int t = lane + 32 * h;
+            if (!((simple >> t) & 1ull)) continue;
+            float f[27];
+#pragma unroll
+            for (int o = 0; o < 27; ++o) {
+                const uint32_t p = s_pull[o * 64 + t];
+                f[o] = __ldg(fin + o * n + (s_off[w][p >> 6] + (int)(p & 63u)));
             }
-            if (lane == 0) {
-                part[3 * (int64_t)lb + 0] = (double)Fx;
-                part[3 * (int64_t)lb + 1] = (double)Fy;
-                part[3 * (int64_t)lb + 2] = (double)Fz;
-            }
+            bgk_store(f, omega, fout, n, (int64_t)lb * 64 + t);
+        }
+        if (simple != ~0ull) {  // warp-uniform
+            float Fx = 0.f, Fy = 0.f, Fz = 0.f;
+            special_cells(s, e, cells_x, b, lb, lane, ghost, ~simple, s_nb[w], s_sol[w], s_pull, coords, cmap,
+                          lengths, fin, fout, flow, Fx, Fy, Fz);
+            if (part) block_force(part, lb, lane, Fx, Fy, Fz);
         }
     }
 }
 
 // d_force += sum over the level's blocks of the per-block partials, in block
 // order with a fixed reduction tree (identical force series
-// across runs; the wall-block list order depends on atomics)
-__global__ void __launch_bounds__(256) k_lbm_force_reduce(int32_t nb, const double *__restrict__ part,
-                                                          double *__restrict__ d_force) {
-    __shared__ double s_r[3][256];
+// across runs; the special-block list order depends on atomics)
+__global__ void __launch_bounds__(1024) k_lbm_force_reduce(int32_t nb, const double *__restrict__ part,
+                                                           double *__restrict__ d_force) {
+    __shared__ double s_r[3][1024];
     double a[3] = {0.0, 0.0, 0.0};
     for (int32_t b = threadIdx.x; b < nb; b += blockDim.x)
 #pragma unroll
@@ -213,7 +354,7 @@ __global__ void __launch_bounds__(256) k_lbm_force_reduce(int32_t nb, const doub
 #pragma unroll
     for (int c = 0; c < 3; ++c) s_r[c][threadIdx.x] = a[c];
     __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
+    for (int o = 512; o > 0; o >>= 1) {
         if ((int)threadIdx.x < o)
 #pragma unroll
             for (int c = 0; c < 3; ++c) s_r[c][threadIdx.x] += s_r[c][threadIdx.x + o];
@@ -289,176 +430,211 @@ __global__ void k_lbm_parents(int32_t n_blocks, const int32_t *__restrict__ chil
     }
 }
 
-// Warp per fine block: the block's 64 cells lie in 2x2x2 coarse cells, so
-// every stencil (cubic: +-2 coarse cells) lies in the 6x6x6 coarse cells
-// around them.  Their level-local ids (or -1: outside the level / SOLID) are
-// staged once; then per population the 216 time-blended coarse values are
-// staged and each lane interpolates its (<= 2) ghost cells separably
-// (x, then y, then z).  The interpolated populations go to ff and are then
-// rescaled in place by their owning lane.
-constexpr int kFillWarps = 8;
-#ifndef VF_FILL_Q
-#define VF_FILL_Q 3
-#endif
+// CTA per sibling group: the fine level is made of groups of 8 children of
+// one coarse parent P (ids first child + octant), warp w <-> child octant w.
+// Every stencil of the group (cubic: +-2 coarse cells around a fine cell's
+// coarse cell) lies in the 8x8x8 coarse cells around P, box index
+// (lx + 2) + 8 (ly + 2) + 64 (lz + 2) for P-local cell l.  Their level-local
+// ids (or -1: outside the level / SOLID) are staged once per group, with a
+// bit plane per box z (bit x + 8 y: usable) for the per-cell order test.
+// Per round of kFillQ populations the CTA stages the 512 time-blended coarse
+// values and interpolates the whole group separably: x (fine X 0..7 of the
+// group x box rows y, z: 512 outputs), y (fine X, Y x box z: 512), then z for
+// the ghost cells -- two outputs per thread per pass, taps in ascending
+// coarse index so the separable passes and the per-cell fallback (a stencil
+// cell missing: cubic -> linear -> the coarse cell itself) sum identically.
+// A thread's x parity in pass 1 is tid & 1, its y parity in pass 2
+// (tid >> 3) & 1 and its cells' z parity (lane >> 4) & 1: the tap weights
+// are registers.
+constexpr int kFillQ = 9;  // populations per round (3 rounds)
 #ifndef VF_FILL_MINB
-#define VF_FILL_MINB 2  // <= 128 registers: 2 CTAs per SM (measured best; 1 -> 188 registers, 3 -> 80)
+#define VF_FILL_MINB 2
 #endif
-constexpr int kFillQ = VF_FILL_Q;  // populations staged per load round (27 = 9 x 3)
 
 __device__ __forceinline__ float axis_w(int ord, int k) {
     return ord == 3 ? c_w3[k] : (ord == 1 ? (k ? 0.25f : 0.75f) : 1.0f);
 }
+__host__ __device__ constexpr int ntaps(int ord) { return ord == 3 ? 4 : (ord == 1 ? 2 : 1); }
+// first tap relative to the coarse cell of a fine cell with odd (pos) or
+// even index; weight of the j-th tap in ascending order
+__host__ __device__ constexpr int tap0(int ord, bool pos) {
+    return ord == 3 ? (pos ? -1 : -2) : (ord == 1 ? (pos ? 0 : -1) : 0);
+}
+__device__ __forceinline__ float wtap(int ord, bool pos, int j) {
+    return axis_w(ord, pos ? j : ntaps(ord) - 1 - j);
+}
+// stencil of order ord starting at box cell (x0, y0, z0) entirely usable
+__device__ __forceinline__ bool stencil_ok(const unsigned long long *ok, int ord, int x0, int y0, int z0) {
+    const int nt = ntaps(ord);
+    const uint64_t m = nt == 4 ? 0x0F0F0F0Full : (nt == 2 ? 0x0303ull : 1ull);
+    for (int k = 0; k < nt; ++k)
+        if (((ok[z0 + k] >> (x0 + 8 * y0)) & m) != m) return false;
+    return true;
+}
 
-__global__ void __launch_bounds__(kFillWarps * 32, VF_FILL_MINB)
-    k_lbm_fill_ghosts(int32_t sf, int32_t ef, int32_t sc, int32_t ec, const int32_t *__restrict__ coords,
-                      const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
+template <int ORD, bool BLEND>
+__global__ void __launch_bounds__(256, VF_FILL_MINB)
+    k_lbm_fill_ghosts(int32_t sf, int32_t ef, int32_t sc, int32_t ec, const int32_t *__restrict__ nbr,
+                      const int32_t *__restrict__ child, const uint8_t *__restrict__ masks,
                       const int32_t *__restrict__ parent, const float *__restrict__ fold,
-                      const float *__restrict__ fnew, float theta, float alpha, int order,
-                      float *__restrict__ ff) {
-    __shared__ int32_t s_c[kFillWarps][216];
-    __shared__ float s_vq[kFillWarps][kFillQ][216];  // kFillQ populations staged per round
-    __shared__ float s_t1[kFillWarps][144], s_t2[kFillWarps][96];
+                      const float *__restrict__ fnew, float theta, float alpha, float *__restrict__ ff) {
+    constexpr int NT = ntaps(ORD);
+    __shared__ int32_t s_pn[27];
+    __shared__ int32_t s_c[512];
+    __shared__ unsigned long long s_ok[8];
+    __shared__ float s_a[kFillQ][512];  // staged values, then pass-2 outputs
+    __shared__ float s_b[kFillQ][512];  // pass-1 outputs
     const int64_t nf = (int64_t)(ef - sf) * 64, nc = (int64_t)(ec - sc) * 64;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int ox = w & 1, oy = (w >> 1) & 1, oz = w >> 2;
     const float th0 = 1.0f - theta;
-    for (int32_t b = sf + blockIdx.x * kFillWarps + w; b < ef; b += gridDim.x * kFillWarps) {
+    const bool p1 = tid & 1, p2 = (tid >> 3) & 1, p3 = (lane >> 4) & 1;
+    float W1[NT], W2[NT], W3[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+        W1[j] = wtap(ORD, p1, j);
+        W2[j] = wtap(ORD, p2, j);
+        W3[j] = wtap(ORD, p3, j);
+    }
+    // pass 1: s_b[idx] = sum_k W1[k] s_a[i1 + k], idx = tid + 256 i
+    const int i1 = (((tid & 7) >> 1) + 2 + tap0(ORD, p1)) + 8 * ((tid >> 3) & 7) + 64 * (tid >> 6);
+    // pass 2: s_a[idx] = sum_k W2[k] s_b[i2 + 8 k]
+    const int i2 = (tid & 7) + 8 * ((((tid >> 3) & 7) >> 1) + 2 + tap0(ORD, p2)) + 64 * (tid >> 6);
+    // pass 3 (cell t = lane + 32 h of child w): sum_k W3[k] s_a[i3 + 64 (h + k)]
+    const int i3 = (4 * ox + (lane & 3)) + 8 * (4 * oy + ((lane >> 2) & 3)) + 64 * (2 * oz + 2 + tap0(ORD, p3));
+    const int ngroups = (ef - sf) >> 3;
+    for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const int32_t b0 = sf + 8 * g, b = b0 + w;
         const bool g0 = masks[64 * (int64_t)b + lane] == VF_GHOST;
         const bool g1 = masks[64 * (int64_t)b + lane + 32] == VF_GHOST;
-        if (!__any_sync(0xffffffffu, g0 || g1)) continue;
-        const int32_t P = parent[b];
-        if (P < sc || P >= ec) continue;  // warp-uniform
-        int R0[3];  // the fine block's first coarse cell, relative to P
+        const int32_t P = parent[b0];
+        const bool ok = P >= sc && P < ec && child[P] == b0;  // uniform over the CTA
+        if (!__syncthreads_or(g0 || g1) || !ok) continue;
+        if (tid < 27) {
+            const int dx = tid % 3 - 1, dy = (tid / 3) % 3 - 1, dz = tid / 9 - 1;
+            s_pn[tid] = tid == 13 ? P : __ldg(nbr + 27 * (int64_t)P + slot_of(dx, dy, dz));
+        }
+        __syncthreads();
 #pragma unroll
-        for (int d = 0; d < 3; ++d) R0[d] = 2 * coords[4 * (int64_t)b + d] - 4 * coords[4 * (int64_t)P + d];
-        // staged coarse cells: local (R0 - 2 + rx, ...), r = rx + 6 ry + 36 rz
-        for (int r = lane; r < 216; r += 32) {
-            const int lx = R0[0] - 2 + r % 6, ly = R0[1] - 2 + (r / 6) % 6, lz = R0[2] - 2 + r / 36;
-            const int ox = lx < 0 ? -1 : (lx > 3 ? 1 : 0), oy = ly < 0 ? -1 : (ly > 3 ? 1 : 0),
-                      oz = lz < 0 ? -1 : (lz > 3 ? 1 : 0);
-            const int32_t Y = (ox | oy | oz) ? __ldg(nbr + 27 * (int64_t)P + slot_of(ox, oy, oz)) : P;
+        for (int i = 0; i < 2; ++i) {
+            const int r = tid + 256 * i;
+            const int lx = (r & 7) - 2, ly = ((r >> 3) & 7) - 2, lz = (r >> 6) - 2;
+            const int32_t Y = s_pn[((lx >> 2) + 1) + 3 * ((ly >> 2) + 1) + 9 * ((lz >> 2) + 1)];
             int32_t c = -1;
             if (Y >= sc && Y < ec) {
                 const int tt = (lx & 3) + 4 * (ly & 3) + 16 * (lz & 3);
                 if (masks[64 * (int64_t)Y + tt] != VF_SOLID) c = (Y - sc) * 64 + tt;
             }
-            s_c[w][r] = c;
+            s_c[r] = c;
+            const uint32_t bal = __ballot_sync(0xffffffffu, c >= 0);
+            if (lane == 0) reinterpret_cast<uint32_t *>(s_ok)[w + 8 * i] = bal;
         }
-        __syncwarp();
-        // per owned ghost cell: staged base index, axis steps, order
-        int base[2], st[2][3], ord[2];
+        __syncthreads();
+        // order of each owned ghost cell (ORD unless a stencil cell is missing)
+        int ord[2], cb[2];  // cb: box index of the first tap at order ord
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int t = lane + 32 * h;
             ord[h] = -1;
-            base[h] = 0;
-            st[h][0] = st[h][1] = st[h][2] = 0;
+            cb[h] = 0;
             if (!(h ? g1 : g0)) continue;
-            const int I[3] = {t & 3, (t >> 2) & 3, t >> 4};
-            int bx[3];
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                bx[d] = (I[d] >> 1) + 2;  // G relative to the staged box
-                st[h][d] = (I[d] & 1) ? 1 : -1;  // fine cell 4c + I: odd iff I odd
-            }
-            const int sx = st[h][0], sy = 6 * st[h][1], sz = 36 * st[h][2];
-            base[h] = bx[0] + 6 * bx[1] + 36 * bx[2];
-            int o = order >= 3 ? 3 : (order >= 1 ? 1 : 0);
-            if (o == 3) {
-                for (int k = 0; k < 64 && o == 3; ++k)
-                    if (s_c[w][base[h] + sx * ((k & 3) - 1) + sy * (((k >> 2) & 3) - 1) + sz * ((k >> 4) - 1)] < 0) o = 1;
-            }
-            if (o == 1) {
-                for (int k = 0; k < 8 && o == 1; ++k)
-                    if (s_c[w][base[h] + sx * (k & 1) + sy * ((k >> 1) & 1) + sz * (k >> 2)] < 0) o = 0;
-            }
-            if (o == 0 && s_c[w][base[h]] < 0) o = -1;  // held
+            const int t = lane + 32 * h;
+            const int I = t & 3, J = (t >> 2) & 3, K = t >> 4;
+            const int gx = 2 * ox + (I >> 1) + 2, gy = 2 * oy + (J >> 1) + 2, gz = 2 * oz + (K >> 1) + 2;
+            const bool qx = I & 1, qy = J & 1, qz = K & 1;
+            int o = ORD;
+            if (o == 3 && !stencil_ok(s_ok, 3, gx + tap0(3, qx), gy + tap0(3, qy), gz + tap0(3, qz))) o = 1;
+            if (o == 1 && !stencil_ok(s_ok, 1, gx + tap0(1, qx), gy + tap0(1, qy), gz + tap0(1, qz))) o = 0;
+            if (o == 0 && !stencil_ok(s_ok, 0, gx, gy, gz)) o = -1;  // held
             ord[h] = o;
-            st[h][1] *= 6;
-            st[h][2] *= 36;
+            if (o >= 0) cb[h] = (gx + tap0(o, qx)) + 8 * (gy + tap0(o, qy)) + 64 * (gz + tap0(o, qz));
         }
+        const int64_t xf = (int64_t)(b - sf) * 64;
+        const int32_t c0 = s_c[tid], c1 = s_c[tid + 256];
 #pragma unroll 1
         for (int q0 = 0; q0 < 27; q0 += kFillQ) {
-          __syncwarp();
-          // kFillQ x 7 independent loads per lane in flight (216 = 6 x 32 + 24)
-          {
-            float v[kFillQ][7];
+            float v[kFillQ][2];
+#pragma unroll
+            for (int j = 0; j < kFillQ; ++j) {
+                const int64_t a = (int64_t)(q0 + j) * nc;
+                v[j][0] = v[j][1] = 0.0f;
+                if (c0 >= 0) v[j][0] = BLEND ? th0 * __ldg(fold + a + c0) + theta * __ldg(fnew + a + c0) : __ldg(fold + a + c0);
+                if (c1 >= 0) v[j][1] = BLEND ? th0 * __ldg(fold + a + c1) + theta * __ldg(fnew + a + c1) : __ldg(fold + a + c1);
+            }
+            __syncthreads();  // the previous round's pass 3 has read s_a
+#pragma unroll
+            for (int j = 0; j < kFillQ; ++j) {
+                s_a[j][tid] = v[j][0];
+                s_a[j][tid + 256] = v[j][1];
+            }
+            __syncthreads();
 #pragma unroll
             for (int j = 0; j < kFillQ; ++j)
 #pragma unroll
-                for (int i = 0; i < 7; ++i) {
-                    const int r = lane + 32 * i;
-                    const int32_t c = r < 216 ? s_c[w][r] : -1;
-                    v[j][i] = 0.0f;
-                    if (c >= 0) {
-                        const int64_t a = (int64_t)(q0 + j) * nc + c;
-                        v[j][i] = theta == 0.0f ? __ldg(fold + a) : th0 * __ldg(fold + a) + theta * __ldg(fnew + a);
-                    }
+                for (int i = 0; i < 2; ++i) {
+                    const float *p = s_a[j] + i1 + 256 * i;
+                    float a = 0.0f;
+#pragma unroll
+                    for (int k = 0; k < NT; ++k) a += W1[k] * p[k];
+                    s_b[j][tid + 256 * i] = a;
                 }
+            __syncthreads();
 #pragma unroll
             for (int j = 0; j < kFillQ; ++j)
 #pragma unroll
-                for (int i = 0; i < 7; ++i)
-                    if (lane + 32 * i < 216) s_vq[w][j][lane + 32 * i] = v[j][i];
-          }
-          __syncwarp();
-#pragma unroll 1
-          for (int j = 0; j < kFillQ; ++j) {
-            const int q = q0 + j;
-            const float *sv = s_vq[w][j];
-            __syncwarp();
-            // separable passes at the requested order for the whole block
-            // (x: 4 x 6 x 6, y: 4 x 4 x 6, z: 4 x 4 x 4); same association as
-            // the per-cell sum below, so a cell's value does not depend on
-            // which path computed it
-            const int og = order >= 3 ? 3 : (order >= 1 ? 1 : 0);
-            const int ng = og == 3 ? 4 : (og == 1 ? 2 : 1), kg = og == 3 ? -1 : 0;
-            for (int e = lane; e < 144; e += 32) {  // (fx, ry, rz)
-                const int fx = e & 3, ry = (e >> 2) % 6, rz = (e >> 2) / 6;
-                const int G = (fx >> 1) + 2, sg = (fx & 1) ? 1 : -1;
-                float a = 0.0f;
-                for (int k = 0; k < ng; ++k) a += axis_w(og, k) * sv[G + sg * (k + kg) + 6 * ry + 36 * rz];
-                s_t1[w][e] = a;
-            }
-            __syncwarp();
-            for (int e = lane; e < 96; e += 32) {  // (fx, fy, rz)
-                const int fx = e & 3, fy = (e >> 2) & 3, rz = e >> 4;
-                const int G = (fy >> 1) + 2, sg = (fy & 1) ? 1 : -1;
-                float a = 0.0f;
-                for (int k = 0; k < ng; ++k) a += axis_w(og, k) * s_t1[w][fx + 4 * (G + sg * (k + kg)) + 24 * rz];
-                s_t2[w][e] = a;
-            }
-            __syncwarp();
+                for (int i = 0; i < 2; ++i) {
+                    const float *p = s_b[j] + i2 + 256 * i;
+                    float a = 0.0f;
+#pragma unroll
+                    for (int k = 0; k < NT; ++k) a += W2[k] * p[8 * k];
+                    s_a[j][tid + 256 * i] = a;
+                }
+            __syncthreads();
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int o = ord[h];
-                if (o < 0) continue;
-                const int t = lane + 32 * h;
-                float acc = 0.0f;
-                if (o == og) {
-                    const int fz = t >> 4, G = (fz >> 1) + 2, sg = (fz & 1) ? 1 : -1;
-                    for (int k = 0; k < ng; ++k) acc += axis_w(og, k) * s_t2[w][(t & 15) + 16 * (G + sg * (k + kg))];
-                } else {  // fallback order of this cell (a stencil cell is missing)
-                    const int n = o == 3 ? 4 : (o == 1 ? 2 : 1), k0 = o == 3 ? -1 : 0;
-                    for (int kz = 0; kz < n; ++kz) {
-                        float ay = 0.0f;
-                        for (int ky = 0; ky < n; ++ky) {
-                            float ax = 0.0f;
-                            const int row = base[h] + st[h][1] * (ky + k0) + st[h][2] * (kz + k0);
-                            for (int kx = 0; kx < n; ++kx) ax += axis_w(o, kx) * sv[row + st[h][0] * (kx + k0)];
-                            ay += axis_w(o, ky) * ax;
-                        }
-                        acc += axis_w(o, kz) * ay;
-                    }
+                if (ord[h] != ORD) continue;  // held, or a fallback cell (below)
+#pragma unroll 3
+                for (int j = 0; j < kFillQ; ++j) {
+                    const float *p = s_a[j] + i3 + 64 * h;
+                    float acc = 0.0f;
+#pragma unroll
+                    for (int k = 0; k < NT; ++k) acc += W3[k] * p[64 * k];
+                    ff[(int64_t)(q0 + j) * nf + xf + lane + 32 * h] = acc;
                 }
-                ff[(int64_t)q * nf + (int64_t)(b - sf) * 64 + t] = acc;
             }
-          }
+        }
+        // fallback cells: their own tensor product from the coarse values
+        // (rare: a stencil cell outside the level or SOLID)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int o = ord[h];
+            if (o < 0 || o == ORD) continue;
+            const int t = lane + 32 * h;
+            const bool qx = t & 1, qy = (t >> 2) & 1, qz = (t >> 4) & 1;
+            const int nt = ntaps(o);
+            for (int q = 0; q < 27; ++q) {
+                float acc = 0.0f;
+                for (int kz = 0; kz < nt; ++kz) {
+                    float ay = 0.0f;
+                    for (int ky = 0; ky < nt; ++ky) {
+                        float ax = 0.0f;
+                        for (int kx = 0; kx < nt; ++kx) {
+                            const int32_t c = s_c[cb[h] + kx + 8 * ky + 64 * kz];
+                            const int64_t a = (int64_t)q * nc + c;
+                            const float val = BLEND ? th0 * __ldg(fold + a) + theta * __ldg(fnew + a) : __ldg(fold + a);
+                            ax += wtap(o, qx, kx) * val;
+                        }
+                        ay += wtap(o, qy, ky) * ax;
+                    }
+                    acc += wtap(o, qz, kz) * ay;
+                }
+                ff[(int64_t)q * nf + xf + t] = acc;
+            }
         }
         if (alpha != 1.0f) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 if (ord[h] < 0) continue;
-                const int64_t x = (int64_t)(b - sf) * 64 + lane + 32 * h;
+                const int64_t x = xf + lane + 32 * h;
                 float f[27];
 #pragma unroll
                 for (int q = 0; q < 27; ++q) f[q] = ff[(int64_t)q * nf + x];
@@ -467,44 +643,110 @@ __global__ void __launch_bounds__(kFillWarps * 32, VF_FILL_MINB)
                 for (int q = 0; q < 27; ++q) ff[(int64_t)q * nf + x] = f[q];
             }
         }
+        __syncthreads();  // s_c / s_ok / s_a of this group are done
     }
 }
 
-__global__ void k_lbm_restrict(int32_t sc, int32_t ec, int32_t sf, int32_t ef, const int32_t *__restrict__ child,
-                               const uint8_t *__restrict__ masks, const float *__restrict__ ff, float beta,
-                               float *__restrict__ fc) {
+// CTA per sibling group of the fine level (its parent P = parent[first
+// child]); thread (t, r) = (tid & 63, tid >> 6) takes coarse cell t of P and
+// populations r, r + 4, ...: the 8 children x <= 7 populations are loaded in
+// one round (SOLID children contribute +0, summed in child order), the
+// moments for the rescale are reduced over the 4 population quarters in a
+// fixed order through shared memory.
+__global__ void __launch_bounds__(256, 3) k_lbm_restrict(int32_t sc, int32_t ec, int32_t sf, int32_t ef,
+                                                         const int32_t *__restrict__ child,
+                                                         const int32_t *__restrict__ parent,
+                                                         const uint8_t *__restrict__ masks,
+                                                         const float *__restrict__ ff, float beta,
+                                                         float *__restrict__ fc) {
+    __shared__ float s_m[4][4][64];  // [quarter][rho, m_x, m_y, m_z][cell]
     const int64_t nf = (int64_t)(ef - sf) * 64, nc = (int64_t)(ec - sc) * 64;
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nc; x += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t b = sc + (int32_t)(x >> 6);
-        const int t = (int)(x & 63);
-        const int32_t c0 = child[b];
-        if (c0 < 0) continue;
-        const uint8_t m = masks[64 * (int64_t)b + t];
-        if (m == VF_SOLID || m == VF_INTERFACE || m == VF_GHOST) continue;
+    const int t = threadIdx.x & 63, r = threadIdx.x >> 6;
+    const int ngroups = (ef - sf) >> 3;
+    for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const int32_t c0 = sf + 8 * g;
+        const int32_t P = __ldg(parent + c0);
+        if (P < sc || P >= ec || __ldg(child + P) != c0) continue;  // uniform over the CTA
+        const uint8_t m = masks[64 * (int64_t)P + t];
         const int I = t & 3, J = (t >> 2) & 3, K = t >> 4;
         const int32_t C = c0 + (I >> 1) + 2 * (J >> 1) + 4 * (K >> 1);
-        if (C < sf || C >= ef) continue;
-        int fine[8], n = 0;
+        const int base = 2 * (I & 1) + 8 * (J & 1) + 32 * (K & 1);  // first child cell
+        uint32_t use = 0;
         bool ghost = false;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const int tt = (2 * (I & 1) + (k & 1)) + 4 * (2 * (J & 1) + ((k >> 1) & 1)) + 16 * (2 * (K & 1) + (k >> 2));
-            const uint8_t mf = masks[64 * (int64_t)C + tt];
+            const uint8_t mf = masks[64 * (int64_t)C + base + (k & 1) + 4 * ((k >> 1) & 1) + 16 * (k >> 2)];
             ghost |= mf == VF_GHOST;
-            if (mf != VF_SOLID) fine[n++] = (C - sf) * 64 + tt;
+            if (mf != VF_SOLID) use |= 1u << k;
         }
-        if (ghost || n == 0) continue;
-        const float inv = 1.0f / (float)n;
-        float f[27];
+        const bool act = !(m == VF_SOLID || m == VF_INTERFACE || m == VF_GHOST || ghost || !use);
+        float f[7];
+        const float *src = ff + (int64_t)(C - sf) * 64 + base;
+        if (act) {
+            const float inv = 1.0f / (float)__popc(use);
 #pragma unroll
-        for (int q = 0; q < 27; ++q) {
-            float acc = 0.0f;
-            for (int k = 0; k < n; ++k) acc += ff[(int64_t)q * nf + fine[k]];
-            f[q] = acc * inv;
+            for (int j = 0; j < 7; ++j) f[j] = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int o = (k & 1) + 4 * ((k >> 1) & 1) + 16 * (k >> 2);
+                const bool u = (use >> k) & 1u;
+#pragma unroll
+                for (int j = 0; j < 7; ++j) {
+                    const int q = r + 4 * j;
+                    if (q < 27) {
+                        const float v = __ldg(src + (int64_t)q * nf + o);
+                        f[j] += u ? v : 0.0f;
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 7; ++j) f[j] *= inv;
         }
-        neq_rescale(f, beta);
+        if (beta != 1.0f) {  // uniform
+            float m4[4] = {0.f, 0.f, 0.f, 0.f};
+            if (act)
 #pragma unroll
-        for (int q = 0; q < 27; ++q) fc[(int64_t)q * nc + x] = f[q];
+                for (int j = 0; j < 7; ++j) {
+                    const int q = r + 4 * j;
+                    if (q < 27) {
+                        m4[0] += f[j];
+                        m4[1] += f[j] * c27(q, 0);
+                        m4[2] += f[j] * c27(q, 1);
+                        m4[3] += f[j] * c27(q, 2);
+                    }
+                }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) s_m[r][c][t] = m4[c];
+            __syncthreads();
+            if (act) {
+                float M[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) M[c] = (s_m[0][c][t] + s_m[1][c][t]) + (s_m[2][c][t] + s_m[3][c][t]);
+                if (M[0] > 0.0f) {
+                    const float ir = 1.0f / M[0];
+                    const float u0 = M[1] * ir, u1 = M[2] * ir, u2 = M[3] * ir;
+                    const float uu = 1.5f * (u0 * u0 + u1 * u1 + u2 * u2);
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) {
+                        const int q = r + 4 * j;
+                        if (q < 27) {
+                            const float cu = c27(q, 0) * u0 + c27(q, 1) * u1 + c27(q, 2) * u2;
+                            const float feq = c_lw[q] * M[0] * (1.0f + 3.0f * cu + 4.5f * cu * cu - uu);
+                            f[j] = feq + beta * (f[j] - feq);
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (act) {
+            const int64_t x = (int64_t)(P - sc) * 64 + t;
+#pragma unroll
+            for (int j = 0; j < 7; ++j) {
+                const int q = r + 4 * j;
+                if (q < 27) fc[(int64_t)q * nc + x] = f[j];
+            }
+        }
     }
 }
 
@@ -543,23 +785,33 @@ int vf_lbm_fill_ghosts(const vf_grid *g, int32_t sf, int32_t ef, int32_t sc, int
         ec > g->capacity || !(theta >= 0.0 && theta <= 1.0) || (theta > 0.0 && !fc_new) ||
         !(order == 0 || order == 1 || order == 3))
         return set_error(VF_EARG, "vf_lbm_fill_ghosts: bad argument");
+    if ((ef - sf) % 8) return set_error(VF_EARG, "vf_lbm_fill_ghosts: the fine range must be whole sibling groups (a level >= 1)");
     if (ef == sf || ec == sc) return VF_OK;
-    int64_t grid = ((int64_t)(ef - sf) + kFillWarps - 1) / kFillWarps;
-    if (grid > max_ctas(8)) grid = max_ctas(8);
-    k_lbm_fill_ghosts<<<(int)grid, kFillWarps * 32, 0, (cudaStream_t)stream>>>(
-        sf, ef, sc, ec, g->d_coords, g->d_nbr, g->d_masks, d_parent, fc_old, fc_new ? fc_new : fc_old,
-        (float)theta, (float)alpha, order, ff);
+    int64_t grid = (ef - sf) / 8;
+    if (grid > max_ctas(VF_FILL_MINB)) grid = max_ctas(VF_FILL_MINB);
+    cudaStream_t st = (cudaStream_t)stream;
+    const float *fn = fc_new ? fc_new : fc_old;
+#define VF_FILL_LAUNCH(O, B)                                                                                   \
+    k_lbm_fill_ghosts<O, B><<<(int)grid, 256, 0, st>>>(sf, ef, sc, ec, g->d_nbr, g->d_child, g->d_masks, d_parent, \
+                                                       fc_old, fn, (float)theta, (float)alpha, ff)
+    const bool blend = theta != 0.0;
+    if (order == 3) { if (blend) VF_FILL_LAUNCH(3, true); else VF_FILL_LAUNCH(3, false); }
+    else if (order == 1) { if (blend) VF_FILL_LAUNCH(1, true); else VF_FILL_LAUNCH(1, false); }
+    else { if (blend) VF_FILL_LAUNCH(0, true); else VF_FILL_LAUNCH(0, false); }
+#undef VF_FILL_LAUNCH
     return check_launch("k_lbm_fill_ghosts");
 }
 
-int vf_lbm_restrict(const vf_grid *g, int32_t sc, int32_t ec, int32_t sf, int32_t ef, const float *ff, double beta,
-                    float *fc, void *stream) {
-    if (!g || !ff || !fc || sf < 0 || ef < sf || ef > g->capacity || sc < 0 || ec < sc || ec > g->capacity)
+int vf_lbm_restrict(const vf_grid *g, int32_t sc, int32_t ec, int32_t sf, int32_t ef, const int32_t *d_parent,
+                    const float *ff, double beta, float *fc, void *stream) {
+    if (!g || !d_parent || !ff || !fc || sf < 0 || ef < sf || ef > g->capacity || sc < 0 || ec < sc ||
+        ec > g->capacity)
         return set_error(VF_EARG, "vf_lbm_restrict: bad argument");
+    if ((ef - sf) % 8) return set_error(VF_EARG, "vf_lbm_restrict: the fine range must be whole sibling groups (a level >= 1)");
     if (ef == sf || ec == sc) return VF_OK;
-    int64_t grid = ((int64_t)(ec - sc) * 64 + 255) / 256;
-    if (grid > max_ctas(8)) grid = max_ctas(8);
-    k_lbm_restrict<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(sc, ec, sf, ef, g->d_child, g->d_masks, ff,
+    int64_t grid = (ef - sf) / 8;
+    if (grid > max_ctas(3)) grid = max_ctas(3);
+    k_lbm_restrict<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(sc, ec, sf, ef, g->d_child, d_parent, g->d_masks, ff,
                                                                  (float)beta, fc);
     return check_launch("k_lbm_restrict");
 }
@@ -574,24 +826,37 @@ int vf_lbm_step(const vf_config *cfg, const vf_grid *g, int level, int32_t s, in
     if (e == s) return VF_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const int cells_x = 4 * (cfg->nb[0] << level);
-    int32_t *n_wall = d_scratch, *wall_list = d_scratch + 1;
-    // per-block force partials after the wall list, 8-byte aligned
+    int32_t *n_list = d_scratch, *list = d_scratch + 1;
+    // per-block force partials after the special-block list, 8-byte aligned
     double *part = d_force ? reinterpret_cast<double *>(d_scratch + ((e - s + 2 + 1) & ~1)) : nullptr;
-    cudaMemsetAsync(n_wall, 0, sizeof(int32_t), st);
+#ifndef VF_LBM_FUSED
+    cudaMemsetAsync(n_list, 0, sizeof(int32_t), st);
+#endif
     if (part) cudaMemsetAsync(part, 0, sizeof(double) * 3 * (size_t)(e - s), st);
+    int rc;
+#ifndef VF_LBM_FUSED
     int64_t grid = ((int64_t)(e - s) + kLbmWarps - 1) / kLbmWarps;
     if (grid > max_ctas(VF_LBM_MINB)) grid = max_ctas(VF_LBM_MINB);
-    k_lbm_cells<false><<<(int)grid, kLbmWarps * 32, 0, st>>>(
-        s, e, cells_x, g->d_coords, g->d_nbr, g->d_masks, g->d_solid64, cmap, lengths, fin, fout, *flow,
-        wall_list, n_wall, nullptr);
-    int rc = check_launch("k_lbm_cells");
+    k_lbm_bulk<<<(int)grid, kLbmWarps * 32, 0, st>>>(s, e, g->d_nbr, g->d_masks, g->d_solid64, fin, fout,
+                                                     1.0f / (float)flow->tau, list, n_list);
+    rc = check_launch("k_lbm_bulk");
     if (rc) return rc;
-    k_lbm_cells<true><<<max_ctas(2), kLbmWarps * 32, 0, st>>>(
-        s, e, cells_x, g->d_coords, g->d_nbr, g->d_masks, g->d_solid64, cmap, lengths, fin, fout, *flow,
-        wall_list, n_wall, part);
-    int rc2 = check_launch("k_lbm_walls");
-    if (rc2 || !d_force) return rc2;
-    k_lbm_force_reduce<<<1, 256, 0, st>>>(e - s, part, d_force);
+    int64_t grid2 = ((int64_t)(e - s) + kLbmWarps - 1) / kLbmWarps;
+    if (grid2 > max_ctas(VF_LBM_SPECIAL_MINB)) grid2 = max_ctas(VF_LBM_SPECIAL_MINB);
+    k_lbm_special<<<(int)grid2, kLbmWarps * 32, 0, st>>>(s, e, cells_x, g->d_coords, g->d_nbr, g->d_masks,
+                                                         g->d_solid64, cmap, lengths, fin, fout, *flow, list,
+                                                         n_list, part);
+    rc = check_launch("k_lbm_special");
+#else
+    (void)list;
+    int64_t grid = ((int64_t)(e - s) + kLbmWarps - 1) / kLbmWarps;
+    if (grid > max_ctas(VF_LBM_FUSED_MINB)) grid = max_ctas(VF_LBM_FUSED_MINB);
+    k_lbm_cells<<<(int)grid, kLbmWarps * 32, 0, st>>>(s, e, cells_x, g->d_coords, g->d_nbr, g->d_masks,
+                                                      g->d_solid64, cmap, lengths, fin, fout, *flow, part);
+    rc = check_launch("k_lbm_cells");
+#endif
+    if (rc || !d_force) return rc;
+    k_lbm_force_reduce<<<1, 1024, 0, st>>>(e - s, part, d_force);
     return check_launch("k_lbm_force_reduce");
 }
 

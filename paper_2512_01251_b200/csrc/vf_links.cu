@@ -18,27 +18,8 @@
 
 namespace vf {
 
-// Bit-parallel 26-neighbour dilation of the SOLID cells.  A block's cells
-// are one 64-bit word (bit t = I + 4J + 16K, the finalize solid64 layout);
-// the 3x3x3 dilation is separable: D = Dz(Dy(Dx(S))) over the 27 blocks
-// around b -- Dx on the 9 block columns (oy, oz), Dy on the 3 planes oz, Dz
-// once -- with in-block shifts plus the facing layer of the neighbour block.
-// BOUNDARY = FLUID & D (a non-solid cell with >= 1 SOLID
-// same-level neighbour among the 26; only FLUID cells are re-marked).
-constexpr uint64_t kI0 = 0x1111111111111111ull, kI3 = 0x8888888888888888ull;
-constexpr uint64_t kJ0 = 0x000F000F000F000Full, kJ3 = 0xF000F000F000F000ull;
-constexpr uint64_t kK0 = 0x000000000000FFFFull, kK3 = 0xFFFF000000000000ull;
-
-__device__ __forceinline__ uint64_t dil_x(uint64_t lo, uint64_t c, uint64_t hi) {
-    return c | ((c << 1) & ~kI0) | ((c >> 1) & ~kI3) | ((lo & kI3) >> 3) | ((hi & kI0) << 3);
-}
-__device__ __forceinline__ uint64_t dil_y(uint64_t lo, uint64_t c, uint64_t hi) {
-    return c | ((c << 4) & ~kJ0) | ((c >> 4) & ~kJ3) | ((lo & kJ3) >> 12) | ((hi & kJ0) << 12);
-}
-__device__ __forceinline__ uint64_t dil_z(uint64_t lo, uint64_t c, uint64_t hi) {
-    return c | (c << 16) | (c >> 16) | ((lo & kK3) >> 48) | ((hi & kK0) << 48);
-}
-
+// 26-neighbour dilation of the SOLID cells: dil_x / dil_y / dil_z
+// (vf_common.cuh); BOUNDARY = FLUID & D.
 // thread per finest-level block: 27 solid64 words -> dilation -> FLUID cells
 // of the block's masks that the dilation covers become BOUNDARY
 #ifndef VF_BOUNDARY_MINB

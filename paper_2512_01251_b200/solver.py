@@ -214,8 +214,8 @@ class LbmHierarchy:
         """Covered cells of level L from level L+1."""
         fine, coarse = self.levels[L + 1], self.levels[L]
         _lib.check(self.lib.vf_lbm_restrict(
-            C.byref(self.grid._struct()), coarse.s, coarse.e, fine.s, fine.e, _lib.ptr(fine.state),
-            float(self.factors[L][1]), _lib.ptr(coarse.state), _lib.stream_ptr()), "interface_exchange (restrict)")
+            C.byref(self.grid._struct()), coarse.s, coarse.e, fine.s, fine.e, _lib.ptr(self.parent),
+            _lib.ptr(fine.state), float(self.factors[L][1]), _lib.ptr(coarse.state), _lib.stream_ptr()), "interface_exchange (restrict)")
 
     def _advance(self, L: int, force: bool):
         lv = self.levels[L]
