@@ -27,7 +27,7 @@ constexpr int kWarp = 32;
 // Component d of c_q, packed as 2-bit fields (c + 1) of one 64-bit immediate
 // per axis: a shift and a mask, no table -- a runtime-indexed table becomes a
 // constant-bank load that serialises over the distinct q of a warp.
-__host__ __device__ __forceinline__ int c27(int q, int d) {
+__host__ __device__ constexpr __forceinline__ int c27(int q, int d) {
     const uint64_t k = d == 0 ? 0x8889548889549ull : (d == 1 ? 0x220888a1549495ull : 0x20a0a096094955ull);
     return (int)((k >> (2 * q)) & 3u) - 1;
 }

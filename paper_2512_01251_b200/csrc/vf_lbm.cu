@@ -46,12 +46,12 @@ __device__ __forceinline__ int32_t cell_at(const int32_t *__restrict__ nbr, int3
 // boundary rule.  The simple set of a block is one 64-bit word, the
 // 26-neighbour dilation (dil_x/y/z) of the "bad" words of the 27 blocks
 // around it (solid64; every cell of a missing or outside neighbour is bad).
-//   k_lbm_bulk    every block, its simple cells only: 27 unconditional
-//                 pulls through a per-CTA table (source neighbour code and
-//                 cell of population o at cell t), BGK, store.  Blocks with
-//                 any other cell are appended to a list.
-//   k_lbm_special the listed blocks, their other cells only: SOLID / GHOST
-//                 held, domain faces (lateral SBB, inlet velocity
+//   k_lbm_bulk    every block, its simple cells: 27 unconditional pulls
+//                 through a per-CTA table (source neighbour code and cell of
+//                 population o at cell t), BGK, store; SOLID / GHOST cells
+//                 held (copied).  Blocks with any other cell are appended to
+//                 a list.
+//   k_lbm_special the listed blocks, their other cells only: domain faces (lateral SBB, inlet velocity
 //                 bounce-back, outlet anti-bounce-back), wall links (SBB or
 //                 Bouzidi linear IBB with q_w from the LUT) with the
 //                 momentum exchange.
@@ -104,11 +104,21 @@ __device__ __forceinline__ uint64_t stage_block(int32_t s, int32_t e, int32_t b,
 }
 
 // source of population o at cell t: (neighbour code << 6) | cell
-__device__ __forceinline__ uint16_t pull_entry(int o, int t) {
+__host__ __device__ constexpr uint16_t pull_entry(int o, int t) {
     const int X = (t & 3) - c27(o, 0), Y = ((t >> 2) & 3) - c27(o, 1), Z = (t >> 4) - c27(o, 2);
     const int code = ((X >> 2) + 1) + 3 * ((Y >> 2) + 1) + 9 * ((Z >> 2) + 1);
     return (uint16_t)((code << 6) | ((X & 3) + 4 * (Y & 3) + 16 * (Z & 3)));
 }
+struct __align__(16) PullTable {
+    uint16_t v[27 * 64];
+};
+constexpr PullTable make_pull_table() {
+    PullTable p{};
+    for (int i = 0; i < 27 * 64; ++i) p.v[i] = pull_entry(i >> 6, i & 63);
+    return p;
+}
+// compile-time table in global memory, copied to shared memory per CTA
+__device__ const __align__(16) PullTable g_pull = make_pull_table();
 
 // BGK relaxation of the pulled populations of cell x to the second-order
 // equilibrium, stored to fout
@@ -136,10 +146,11 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_MINB)
     k_lbm_bulk(int32_t s, int32_t e, const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
                const uint64_t *__restrict__ solid64, const float *__restrict__ fin, float *__restrict__ fout,
                float omega, int32_t *__restrict__ list, int32_t *__restrict__ n_list) {
-    __shared__ uint16_t s_pull[27 * 64];
+    __shared__ __align__(16) uint16_t s_pull[27 * 64];
     __shared__ int32_t s_nb[kLbmWarps][27];
     __shared__ unsigned long long s_bad[kLbmWarps][27];
-    for (int i = threadIdx.x; i < 27 * 64; i += blockDim.x) s_pull[i] = pull_entry(i >> 6, i & 63);
+    for (int i = threadIdx.x; i < 27 * 64 / 8; i += blockDim.x)
+        reinterpret_cast<uint4 *>(s_pull)[i] = reinterpret_cast<const uint4 *>(g_pull.v)[i];
     __syncthreads();
     const int64_t n = (int64_t)(e - s) * 64;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -148,9 +159,10 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_MINB)
         __syncwarp();
         const uint64_t ghost = stage_block(s, e, b, lane, nbr, masks, solid64, s_nb[w], s_bad[w]);
         const uint64_t simple = simple_cells(s_bad[w], ghost);
+        const uint64_t held = ghost | s_bad[w][13];  // GHOST / SOLID: f_out = f_in
         if (lane < 27) s_nb[w][lane] = (s_nb[w][lane] - s) * 64;  // pulls only reach level cells
         __syncwarp();
-        if (simple != ~0ull && lane == 0) list[atomicAdd(n_list, 1)] = lb;
+        if ((simple | held) != ~0ull && lane == 0) list[atomicAdd(n_list, 1)] = lb;
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
             const int t = lane + 32 * h;
@@ -163,6 +175,16 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_MINB)
             }
             bgk_store(f, omega, fout, n, (int64_t)lb * 64 + t);
         }
+        if (held) {  // warp-uniform
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int t = lane + 32 * h;
+                if (!((held >> t) & 1ull)) continue;
+                const int64_t x = (int64_t)lb * 64 + t;
+#pragma unroll
+                for (int q = 0; q < 27; ++q) fout[q * n + x] = __ldg(fin + q * n + x);
+            }
+        }
     }
 }
 
@@ -170,7 +192,7 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_MINB)
 // onto the lanes (k-th set bit of spec); wall momentum exchange into F
 __device__ __forceinline__ void special_cells(int32_t s, int32_t e, int cells_x, int32_t b, int lb, int lane,
                                               uint64_t ghost, uint64_t spec, const int32_t *nb,
-                                              const unsigned long long *sol, const uint16_t *s_pull,
+                                              const unsigned long long *sol, const uint16_t *pull,
                                               const int32_t *__restrict__ coords, const int32_t *__restrict__ cmap,
                                               const float *__restrict__ lengths, const float *__restrict__ fin,
                                               float *__restrict__ fout, const vf_flow &flow, float &Fx, float &Fy,
@@ -213,7 +235,7 @@ __device__ __forceinline__ void special_cells(int32_t s, int32_t e, int cells_x,
         float f[27];
 #pragma unroll
         for (int o = 0; o < 27; ++o) {
-            const uint32_t p = s_pull[o * 64 + t];
+            const uint32_t p = pull[o * 64 + t];
             const int code = (int)(p >> 6), ty = (int)(p & 63u);
             const int32_t y = nb[code];
             if (!((sol[code] >> ty) & 1ull)) {  // a level cell that is not SOLID
@@ -235,7 +257,7 @@ __device__ __forceinline__ void special_cells(int32_t s, int32_t e, int cells_x,
                 const float qw = slot >= 0 ? lengths[((int64_t)slot * 27 + q) * 64 + t] : -1.0f;
                 if (qw > 0.0f && qw < 0.5f) {
                     // second node behind x: x + c_o = x - c_q (the source of population q)
-                    const uint32_t p2 = s_pull[q * 64 + t];
+                    const uint32_t p2 = pull[q * 64 + t];
                     const int code2 = (int)(p2 >> 6), tz = (int)(p2 & 63u);
                     if (!((sol[code2] >> tz) & 1ull))
                         v = 2.0f * qw * fq + (1.0f - 2.0f * qw) *
@@ -277,10 +299,11 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_SPECIAL_MINB)
                   const float *__restrict__ lengths, const float *__restrict__ fin,
                   float *__restrict__ fout, vf_flow flow, const int32_t *__restrict__ list,
                   const int32_t *__restrict__ n_list, double *__restrict__ part) {
-    __shared__ uint16_t s_pull[27 * 64];
+    __shared__ __align__(16) uint16_t s_pull[27 * 64];
     __shared__ int32_t s_nb[kLbmWarps][27];
     __shared__ unsigned long long s_sol[kLbmWarps][27];
-    for (int i = threadIdx.x; i < 27 * 64; i += blockDim.x) s_pull[i] = pull_entry(i >> 6, i & 63);
+    for (int i = threadIdx.x; i < 27 * 64 / 8; i += blockDim.x)
+        reinterpret_cast<uint4 *>(s_pull)[i] = reinterpret_cast<const uint4 *>(g_pull.v)[i];
     __syncthreads();
     const int nitems = *n_list;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -290,7 +313,8 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_SPECIAL_MINB)
         const int32_t b = s + lb;
         __syncwarp();
         const uint64_t ghost = stage_block(s, e, b, lane, nbr, masks, solid64, s_nb[w], s_sol[w]);
-        const uint64_t spec = ~simple_cells(s_sol[w], ghost);  // the cells of this pass
+        // the cells of this pass: neither simple nor held (the bulk pass's)
+        const uint64_t spec = ~(simple_cells(s_sol[w], ghost) | ghost | s_sol[w][13]);
         special_cells(s, e, cells_x, b, lb, lane, ghost, spec, s_nb[w], s_sol[w], s_pull, coords, cmap, lengths,
                       fin, fout, flow, Fx, Fy, Fz);
         if (part) block_force(part, lb, lane, Fx, Fy, Fz);
@@ -305,10 +329,11 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_FUSED_MINB)
                 const uint64_t *__restrict__ solid64, const int32_t *__restrict__ cmap,
                 const float *__restrict__ lengths, const float *__restrict__ fin, float *__restrict__ fout,
                 vf_flow flow, double *__restrict__ part) {
-    __shared__ uint16_t s_pull[27 * 64];
+    __shared__ __align__(16) uint16_t s_pull[27 * 64];
     __shared__ int32_t s_nb[kLbmWarps][27], s_off[kLbmWarps][27];
     __shared__ unsigned long long s_sol[kLbmWarps][27];
-    for (int i = threadIdx.x; i < 27 * 64; i += blockDim.x) s_pull[i] = pull_entry(i >> 6, i & 63);
+    for (int i = threadIdx.x; i < 27 * 64 / 8; i += blockDim.x)
+        reinterpret_cast<uint4 *>(s_pull)[i] = reinterpret_cast<const uint4 *>(g_pull.v)[i];
     __syncthreads();
     const int64_t n = (int64_t)(e - s) * 64;
     const float omega = 1.0f / (float)flow.tau;

@@ -131,12 +131,10 @@ int tables_impl(vf_grid *g, const int32_t *bcount, int32_t *cmap, int32_t *d_n_b
                 size_t ws_bytes, cudaStream_t st, int32_t *inv) {
     if (ws_bytes < tables_workspace_size(g->capacity)) return set_error(VF_EARG, "tables workspace too small");
     const int L = g->n_levels - 1;
-    int32_t *scal = (int32_t *)ws;
     void *scan_ws = (char *)ws + 256;
     // non-finest blocks are never mapped
     cudaMemsetAsync(cmap, 0xff, sizeof(int32_t) * (size_t)g->capacity, st);
     kt_point("memset:cmap");
-    (void)scal;
     cudaError_t ce = scan_launch_fn(LoadBnd{g->d_level_start, L, bcount}, EmitCmap{g->d_level_start, L, cmap, inv},
                                     g->capacity, ScanLevelN{g->d_level_start, L}, d_n_b, scan_ws, st);
     return ce == cudaSuccess ? VF_OK : set_cuda_error(ce, "tables scan");
