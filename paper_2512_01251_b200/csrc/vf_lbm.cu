@@ -856,8 +856,12 @@ int vf_lbm_step(const vf_config *cfg, const vf_grid *g, int level, int32_t s, in
     double *part = d_force ? reinterpret_cast<double *>(d_scratch + ((e - s + 2 + 1) & ~1)) : nullptr;
 #ifndef VF_LBM_FUSED
     cudaMemsetAsync(n_list, 0, sizeof(int32_t), st);
+    kt_point("memset:lbm_list");
 #endif
-    if (part) cudaMemsetAsync(part, 0, sizeof(double) * 3 * (size_t)(e - s), st);
+    if (part) {
+        cudaMemsetAsync(part, 0, sizeof(double) * 3 * (size_t)(e - s), st);
+        kt_point("memset:lbm_part");
+    }
     int rc;
 #ifndef VF_LBM_FUSED
     int64_t grid = ((int64_t)(e - s) + kLbmWarps - 1) / kLbmWarps;
