@@ -7,6 +7,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include <new>
@@ -84,6 +85,21 @@ int sm_count() {
             n = 148;
     });
     return n;
+}
+
+int resident_ctas(const void *kernel, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::unordered_map<const void *, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(kernel);
+    if (it != cache.end()) return it->second;
+    int r = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kernel, threads, smem) != cudaSuccess || r <= 0) {
+        cudaGetLastError();
+        r = 1;
+    }
+    cache[kernel] = r;
+    return r;
 }
 
 LevelInfo make_level(const vf_config &cfg, int L) {

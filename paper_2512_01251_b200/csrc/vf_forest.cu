@@ -421,7 +421,7 @@ int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_byte
                                     st, AdaptFinish{L, g->capacity, g->d_level_start, g->d_status});
     if (ce != cudaSuccess) return set_cuda_error(ce, "adapt scan");
     int rc;
-    k_adapt_children_t<<<max_ctas(VF_GRID_ADAPT), kAdaptTBatch, 0, st>>>(
+    k_adapt_children_t<<<wave_ctas(k_adapt_children_t, kAdaptTBatch), kAdaptTBatch, 0, st>>>(
         L, g->capacity, cfg.nb[0] << (L + 1), cfg.nb[1] << (L + 1), cfg.nb[2] << (L + 1),
         g->d_level_start, scalars + 1, parents, g->d_coords, g->d_nbr, g->d_nbr_child, g->d_child,
         g->d_bflags, g->d_masks, g->d_status, g->d_solid64);

@@ -20,18 +20,20 @@ bool kt_on();
 
 int sm_count();
 inline int max_ctas(int per_sm) { return sm_count() * per_sm; }
+// CTAs of `kernel` resident per SM at this block size (occupancy API, cached)
+int resident_ctas(const void *kernel, int threads, size_t smem = 0);
+// one full wave of a grid-stride kernel: SMs x resident CTAs (a grid that is
+// not a whole number of waves leaves the last wave partly idle)
+template <typename K>
+int wave_ctas(K kernel, int threads, size_t smem = 0) {
+    return sm_count() * resident_ctas(reinterpret_cast<const void *>(kernel), threads, smem);
+}
 // grid sizes (CTAs per SM) of grid-stride kernels (build-time tunables)
 #ifndef VF_GRID_PAIRS
 #define VF_GRID_PAIRS 8
 #endif
-#ifndef VF_GRID_ADAPT
-#define VF_GRID_ADAPT 4
-#endif
 #ifndef VF_GRID_RESOLVE
 #define VF_GRID_RESOLVE 8
-#endif
-#ifndef VF_GRID_BOUNDARY
-#define VF_GRID_BOUNDARY 8
 #endif
 #ifndef VF_GRID_XS4
 #define VF_GRID_XS4 8

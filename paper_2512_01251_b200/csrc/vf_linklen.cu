@@ -1437,7 +1437,7 @@ static int link_bucket(const vf_config &cfg, LinkCtx &c, int64_t F, void *lines_
     cudaError_t e = scan_launch(LoadBlk{tb.bcnt}, EmitBlk{tb.boff, tb.bcur}, tb.n_max, nullptr, nullptr, tb.scan_ws, st);
     kt_point("scan_kernel");
     if (e != cudaSuccess) return set_cuda_error(e, "parent link scan");
-    k_block_scatter<<<max_ctas(8), 256, 0, st>>>(c, parent_dims(cfg), tb.bcur, tb.ent);
+    k_block_scatter<<<wave_ctas(k_block_scatter, 256), 256, 0, st>>>(c, parent_dims(cfg), tb.bcur, tb.ent);
     return check_launch("k_block_scatter");
 }
 

@@ -96,7 +96,7 @@ int boundary_impl(const vf_config &cfg, vf_grid *g, int32_t *bcount, cudaStream_
     const int L = g->n_levels - 1;
     cudaMemsetAsync(bcount, 0, sizeof(int32_t) * (size_t)g->capacity, st);
     kt_point("memset:bcount");
-    k_boundary<<<max_ctas(VF_GRID_BOUNDARY), 256, 0, st>>>(make_level(cfg, L), L, g->d_level_start,
+    k_boundary<<<wave_ctas(k_boundary, 256), 256, 0, st>>>(make_level(cfg, L), L, g->d_level_start,
                                                        g->d_nbr, g->d_coords, g->d_bflags,
                                                        g->d_masks, g->d_solid64, bcount);
     return check_launch("k_boundary");
