@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kRowWarps * 32)
 int propagate_rows_impl(const LevelInfo &li, vf_grid *g, int L, void *ws, cudaStream_t st) {
     RowWs w;
     rows_layout(g->capacity, (char *)ws, &w);
-    k_xrows<<<max_ctas(8), kRowWarps * 32, 0, st>>>  // 2.7 waves: measured faster than one(li, L, w.set[L & 1], g->d_level_start, g->d_coords, g->d_nbr,
+    k_xrows<<<max_ctas(8), kRowWarps * 32, 0, st>>>(li, L, w.set[L & 1], g->d_level_start, g->d_coords, g->d_nbr,
                                                     g->d_masks,
                                                     g->d_bflags, g->d_solid64);
     return check_launch("k_xrows");
