@@ -132,13 +132,51 @@ __global__ void __launch_bounds__(kIndWarps * 32, 3)
 // of face f at level L.  Candidate rows are decided by the FP32 row
 // classifier (vf_common.cuh); only undecided rows run the exact SAT.  Same
 // predicate as indicator_rows, row for row.
+// The face records reach the warps through shared memory: a warp takes 32
+// consecutive faces (3 KB) at a time and prefetches its next 32 with
+// cp.async (16 B per lane-copy, L2 only) while it classifies the current
+// ones, so the record stream keeps flowing through the long, divergent row
+// loops (double-buffered per warp; no block barriers).
+constexpr int kIndFaceD2 = kFaceStride / 2;  // double2 per face record
+__device__ __forceinline__ void ind_prefetch(const double *__restrict__ faces, int64_t F, int64_t c, double2 *dst,
+                                             int lane) {
+    const int64_t f0 = c * 32;
+    const int64_t nf = F - f0 < 32 ? F - f0 : 32;
+    const double2 *src = reinterpret_cast<const double2 *>(faces + f0 * kFaceStride);
+    for (int i = lane; i < nf * kIndFaceD2; i += 32) {
+        const unsigned d = (unsigned)__cvta_generic_to_shared(dst + i);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + i) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(256, VF_IND_MINB)
     k_indicators_all(LevelSet ls, const double *__restrict__ faces, int64_t F,
                      uint16_t *__restrict__ out) {
-    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < F;
-         f += (int64_t)gridDim.x * blockDim.x) {
+    __shared__ double2 s_rec[8][2][32 * kIndFaceD2];  // per warp: two 32-face buffers (48 KB)
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const int64_t nchunk = (F + 31) / 32, cstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+    int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + wi;
+    if (c < nchunk) ind_prefetch(faces, F, c, s_rec[wi][0], lane);
+    for (int buf = 0; c < nchunk; c += cstride, buf ^= 1) {
+        if (c + cstride < nchunk) {
+            ind_prefetch(faces, F, c + cstride, s_rec[wi][buf ^ 1], lane);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncwarp();
+        const int64_t f = c * 32 + lane;
         double v[9], n[3];
-        load_face(faces, f, v, n);
+        if (f < F) {
+            const double2 *p = s_rec[wi][buf] + lane * kIndFaceD2;
+            const double2 a = p[0], b = p[1], cc = p[2], d = p[3], e = p[4], g = p[5];
+            v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = cc.x; v[5] = cc.y;
+            v[6] = d.x; v[7] = d.y; v[8] = e.x;
+            n[0] = e.y; n[1] = g.x; n[2] = g.y;
+        }
+        __syncwarp();  // the buffer is refilled two chunks later
+        if (f >= F) continue;
         uint32_t bits = 0;
         if (!(fabs(n[0]) < ls.li[0].eps_par)) {
             const double xlo = fmin(fmin(v[0], v[3]), v[6]), xhi = fmax(fmax(v[0], v[3]), v[6]);
