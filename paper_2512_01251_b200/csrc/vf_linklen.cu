@@ -1134,27 +1134,59 @@ __global__ void __launch_bounds__(kLutWarps * 32)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     uint32_t *S = s_lut[w];
     uint4 *S4 = reinterpret_cast<uint4 *>(S);
-    for (int64_t slot = (int64_t)blockIdx.x * kLutWarps + w; slot < nb; slot += (int64_t)gridDim.x * kLutWarps) {
-        const int4 co = reinterpret_cast<const int4 *>(coords)[inv[slot]];
-        const int32_t key = (co.x >> 1) + pdim.x * ((co.y >> 1) + pdim.y * (co.z >> 1));
-        const uint32_t oct = (uint32_t)((co.x & 1) + 2 * (co.y & 1) + 4 * (co.z & 1));
-        // multi-GPU: the LUT is distributed -- a rank writes the slots of
-        // the blocks it owns (another rank's slots are left to their owner)
-        if (!owns_row(li, co.y, co.z)) continue;
-        const int32_t e0 = boff[key], ne = bcnt[key];
-        for (int i = lane; i < 27 * 64 / 4; i += 32)
-            S4[i] = make_uint4(0xBF800000u, 0xBF800000u, 0xBF800000u, 0xBF800000u);  // -1.0f
-        __syncwarp();
-        for (int i = lane; i < ne; i += 32) {
-            const unsigned long long x = ent[e0 + i];
-            // the parent's links in this block; q > 0: uint order is float order, below -1's bits
-            if ((uint32_t)(x >> 41) == oct) atomicMin(&S[(uint32_t)(x >> 30) & 0x7ffu], (uint32_t)x & 0x3fffffffu);
+    const int64_t stride = (int64_t)gridDim.x * kLutWarps;
+    // the warp's slots in batches of 32: lane k resolves slot k's block ->
+    // parent bucket chain (inv -> coords -> key -> offsets) for the batch
+    // at once, then the warp writes the 32 slots one after another
+    for (int64_t sbase = (int64_t)blockIdx.x * kLutWarps + w; sbase < nb; sbase += 32 * stride) {
+        uint32_t m_oct = 0;
+        int32_t m_e0 = 0, m_ne = -1;  // -1: not this rank's slot / past the end
+        {
+            const int64_t my = sbase + lane * stride;
+            if (my < nb) {
+                const int4 co = reinterpret_cast<const int4 *>(coords)[inv[my]];
+                const int32_t key = (co.x >> 1) + pdim.x * ((co.y >> 1) + pdim.y * (co.z >> 1));
+                m_oct = (uint32_t)((co.x & 1) + 2 * (co.y & 1) + 4 * (co.z & 1));
+                // multi-GPU: the LUT is distributed -- a rank writes the slots
+                // of the blocks it owns (another rank's are left to their owner)
+                if (owns_row(li, co.y, co.z)) {
+                    m_e0 = boff[key];
+                    m_ne = bcnt[key];
+                }
+            }
         }
-        __syncwarp();
-        uint4 *dst = reinterpret_cast<uint4 *>(lengths + slot * (27 * 64));
-        for (int i = lane; i < 27 * 64 / 4; i += 32) dst[i] = S4[i];
-        __syncwarp();
+        for (int k = 0; k < 32; ++k) {
+            const int64_t slot = sbase + k * stride;
+            if (slot >= nb) break;
+            const int32_t ne = __shfl_sync(0xffffffffu, m_ne, k);
+            if (ne < 0) continue;
+            const int32_t e0 = __shfl_sync(0xffffffffu, m_e0, k);
+            const uint32_t oct = __shfl_sync(0xffffffffu, m_oct, k);
+            // the previous slot's bulk store has read the buffer
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+            for (int i = lane; i < 27 * 64 / 4; i += 32)
+                S4[i] = make_uint4(0xBF800000u, 0xBF800000u, 0xBF800000u, 0xBF800000u);  // -1.0f
+            __syncwarp();
+            for (int i = lane; i < ne; i += 32) {
+                const unsigned long long x = ent[e0 + i];
+                // the parent's links in this block; q > 0: uint order is float order, below -1's bits
+                if ((uint32_t)(x >> 41) == oct) atomicMin(&S[(uint32_t)(x >> 30) & 0x7ffu], (uint32_t)x & 0x3fffffffu);
+            }
+            // the slot (6,912 contiguous bytes) leaves through one TMA bulk
+            // store: shared-memory writes made visible to the async proxy first
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                const unsigned src = (unsigned)__cvta_generic_to_shared(S);
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(lengths + slot * (27 * 64)),
+                             "r"(src), "r"(27 * 64 * 4)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // the band candidates: full exact path (num, den, d, eps-box SAT), one per
