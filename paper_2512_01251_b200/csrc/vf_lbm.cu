@@ -69,7 +69,8 @@ constexpr int kLbmWarps = 8;
 
 // bad words of the 27 blocks around b (code (dx+1) + 3(dy+1) + 9(dz+1)) ->
 // the simple cells of b (ghost: the block's GHOST cells)
-__device__ __forceinline__ uint64_t simple_cells(const unsigned long long *bad, uint64_t ghost) {
+// (codes in `skip` count as not bad)
+__device__ __forceinline__ uint64_t simple_cells(const unsigned long long *bad, uint64_t ghost, uint32_t skip = 0) {
     uint64_t pl[3];
 #pragma unroll
     for (int dz = 0; dz < 3; ++dz) {
@@ -77,7 +78,9 @@ __device__ __forceinline__ uint64_t simple_cells(const unsigned long long *bad, 
 #pragma unroll
         for (int dy = 0; dy < 3; ++dy) {
             const int c = 3 * dy + 9 * dz;
-            col[dy] = dil_x(bad[c], bad[c + 1], bad[c + 2]);
+            const uint64_t b0 = (skip >> c) & 1u ? 0ull : bad[c], b1 = (skip >> (c + 1)) & 1u ? 0ull : bad[c + 1],
+                           b2 = (skip >> (c + 2)) & 1u ? 0ull : bad[c + 2];
+            col[dy] = dil_x(b0, b1, b2);
         }
         pl[dz] = dil_y(col[0], col[1], col[2]);
     }
@@ -101,6 +104,22 @@ __device__ __forceinline__ uint64_t stage_block(int32_t s, int32_t e, int32_t b,
     const uint64_t ghost = (uint64_t)__ballot_sync(0xffffffffu, g0) | ((uint64_t)__ballot_sync(0xffffffffu, g1) << 32);
     __syncwarp();
     return ghost;
+}
+
+// Codes whose neighbour lies outside the domain through a lateral face
+// (lateral SBB: f_o(x) = f_opp(o)(x)) -- every outside face when the x faces
+// are walls too, else those not through the x = 0 / x = l_x faces of an
+// x-boundary block (inlet / outlet).  lane < 27 holds code `lane`'s id.
+__device__ __forceinline__ uint32_t lateral_codes(int32_t v, int lane, int bx, int cells_x, int open_x) {
+    const int dx = lane % 3 - 1;
+    const bool xout = (dx < 0 && bx == 0) || (dx > 0 && 4 * bx + 4 >= cells_x);
+    return __ballot_sync(0xffffffffu, lane < 27 && v == VF_NB_OUTSIDE && !(open_x && xout));
+}
+// the cells whose only boundary rule is the lateral SBB (not simple, not
+// held): the complement of the dilation of the other bad words
+__device__ __forceinline__ uint64_t lateral_cells(const unsigned long long *bad, uint64_t ghost, uint32_t lat,
+                                                  uint64_t simple, uint64_t held) {
+    return lat ? (simple_cells(bad, ghost, lat) & ~simple & ~held) : 0ull;
 }
 
 // source of population o at cell t: (neighbour code << 6) | cell
@@ -143,7 +162,8 @@ __device__ __forceinline__ void bgk_store(float *f, float omega, float *__restri
 }
 
 __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_MINB)
-    k_lbm_bulk(int32_t s, int32_t e, const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
+    k_lbm_bulk(int32_t s, int32_t e, int cells_x, int open_x, const int32_t *__restrict__ coords,
+               const int32_t *__restrict__ nbr, const uint8_t *__restrict__ masks,
                const uint64_t *__restrict__ solid64, const float *__restrict__ fin, float *__restrict__ fout,
                float omega, int32_t *__restrict__ list, int32_t *__restrict__ n_list) {
     __shared__ __align__(16) uint16_t s_pull[27 * 64];
@@ -160,9 +180,14 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_MINB)
         const uint64_t ghost = stage_block(s, e, b, lane, nbr, masks, solid64, s_nb[w], s_bad[w]);
         const uint64_t simple = simple_cells(s_bad[w], ghost);
         const uint64_t held = ghost | s_bad[w][13];  // GHOST / SOLID: f_out = f_in
-        if (lane < 27) s_nb[w][lane] = (s_nb[w][lane] - s) * 64;  // pulls only reach level cells
+        const int32_t v = lane < 27 ? s_nb[w][lane] : 0;
+        uint32_t lat = 0;
+        if (__any_sync(0xffffffffu, lane < 27 && v == VF_NB_OUTSIDE))  // a domain-face block
+            lat = lateral_codes(v, lane, __ldg(coords + 4 * (int64_t)b), cells_x, open_x);
+        const uint64_t sbb = lateral_cells(s_bad[w], ghost, lat, simple, held);
+        if (lane < 27) s_nb[w][lane] = (v - s) * 64;  // pulls only reach level cells (or lateral SBB)
         __syncwarp();
-        if ((simple | held) != ~0ull && lane == 0) list[atomicAdd(n_list, 1)] = lb;
+        if ((simple | held | sbb) != ~0ull && lane == 0) list[atomicAdd(n_list, 1)] = lb;
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
             const int t = lane + 32 * h;
@@ -174,6 +199,23 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_MINB)
                 f[o] = __ldg(fin + o * n + (s_nb[w][p >> 6] + (int)(p & 63u)));
             }
             bgk_store(f, omega, fout, n, (int64_t)lb * 64 + t);
+        }
+        if (sbb) {  // warp-uniform: cells next to a lateral domain face only
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int t = lane + 32 * h;
+                if (!((sbb >> t) & 1ull)) continue;
+                const int64_t x = (int64_t)lb * 64 + t;
+                float f[27];
+#pragma unroll
+                for (int o = 0; o < 27; ++o) {
+                    const uint32_t p = s_pull[o * 64 + t];
+                    const int q = o == 0 ? 0 : ((o & 1) ? o + 1 : o - 1);
+                    f[o] = (lat >> (p >> 6)) & 1u ? __ldg(fin + q * n + x)
+                                                  : __ldg(fin + o * n + (s_nb[w][p >> 6] + (int)(p & 63u)));
+                }
+                bgk_store(f, omega, fout, n, x);
+            }
         }
         if (held) {  // warp-uniform
 #pragma unroll 1
@@ -313,8 +355,14 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_SPECIAL_MINB)
         const int32_t b = s + lb;
         __syncwarp();
         const uint64_t ghost = stage_block(s, e, b, lane, nbr, masks, solid64, s_nb[w], s_sol[w]);
-        // the cells of this pass: neither simple nor held (the bulk pass's)
-        const uint64_t spec = ~(simple_cells(s_sol[w], ghost) | ghost | s_sol[w][13]);
+        // the cells of this pass: neither simple, lateral-SBB-only nor held
+        // (the bulk pass's)
+        const uint64_t simple = simple_cells(s_sol[w], ghost), held = ghost | s_sol[w][13];
+        const int32_t v = lane < 27 ? s_nb[w][lane] : 0;
+        uint32_t lat = 0;
+        if (__any_sync(0xffffffffu, lane < 27 && v == VF_NB_OUTSIDE))
+            lat = lateral_codes(v, lane, __ldg(coords + 4 * (int64_t)b), cells_x, flow.open_x);
+        const uint64_t spec = ~(simple | held | lateral_cells(s_sol[w], ghost, lat, simple, held));
         special_cells(s, e, cells_x, b, lb, lane, ghost, spec, s_nb[w], s_sol[w], s_pull, coords, cmap, lengths,
                       fin, fout, flow, Fx, Fy, Fz);
         if (part) block_force(part, lb, lane, Fx, Fy, Fz);
@@ -866,8 +914,8 @@ int vf_lbm_step(const vf_config *cfg, const vf_grid *g, int level, int32_t s, in
 #ifndef VF_LBM_FUSED
     int64_t grid = ((int64_t)(e - s) + kLbmWarps - 1) / kLbmWarps;
     if (grid > max_ctas(VF_LBM_MINB)) grid = max_ctas(VF_LBM_MINB);
-    k_lbm_bulk<<<(int)grid, kLbmWarps * 32, 0, st>>>(s, e, g->d_nbr, g->d_masks, g->d_solid64, fin, fout,
-                                                     1.0f / (float)flow->tau, list, n_list);
+    k_lbm_bulk<<<(int)grid, kLbmWarps * 32, 0, st>>>(s, e, cells_x, flow->open_x, g->d_coords, g->d_nbr, g->d_masks,
+                                                     g->d_solid64, fin, fout, 1.0f / (float)flow->tau, list, n_list);
     rc = check_launch("k_lbm_bulk");
     if (rc) return rc;
     int64_t grid2 = ((int64_t)(e - s) + kLbmWarps - 1) / kLbmWarps;
