@@ -58,7 +58,7 @@ __device__ __forceinline__ int32_t cell_at(const int32_t *__restrict__ nbr, int3
 // The passes write disjoint cells from the same f_in, so they commute.
 constexpr int kLbmWarps = 8;
 #ifndef VF_LBM_MINB
-#define VF_LBM_MINB 4
+#define VF_LBM_MINB 3  // 85 registers (with the staging prefetch; 4: 64 + 96 B spills, measured slower)
 #endif
 #ifndef VF_LBM_FUSED_MINB  // fused variant (-DVF_LBM_FUSED): measured slower
 #define VF_LBM_FUSED_MINB 3
@@ -174,10 +174,42 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_MINB)
     __syncthreads();
     const int64_t n = (int64_t)(e - s) * 64;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int lb = blockIdx.x * kLbmWarps + w; lb < e - s; lb += gridDim.x * kLbmWarps) {
+    const int nblk = e - s, stride = gridDim.x * kLbmWarps;
+    // the next block's staging is prefetched into registers: its neighbour
+    // ids and GHOST bits while this block starts, its solid words between
+    // this block's two halves (their ids have arrived by then)
+    int32_t nv = 0;
+    unsigned long long nbad = 0ull;
+    bool ng0 = false, ng1 = false;
+    auto fetch_ids = [&](int lbn) {
+        const int32_t bn = s + lbn;
+        if (lane < 27) {
+            const int dx = lane % 3 - 1, dy = (lane / 3) % 3 - 1, dz = lane / 9 - 1;
+            nv = (lane == 13) ? bn : __ldg(nbr + 27 * (int64_t)bn + slot_of(dx, dy, dz));
+        }
+        ng0 = masks[64 * (int64_t)bn + lane] == VF_GHOST;
+        ng1 = masks[64 * (int64_t)bn + lane + 32] == VF_GHOST;
+    };
+    auto fetch_bad = [&]() {
+        if (lane < 27)
+            nbad = (nv >= s && nv < e) ? __ldg(reinterpret_cast<const unsigned long long *>(solid64) + nv) : ~0ull;
+    };
+    int lb = blockIdx.x * kLbmWarps + w;
+    if (lb < nblk) {
+        fetch_ids(lb);
+        fetch_bad();
+    }
+    for (; lb < nblk; lb += stride) {
         const int32_t b = s + lb;
+        const int lbn = lb + stride;
         __syncwarp();
-        const uint64_t ghost = stage_block(s, e, b, lane, nbr, masks, solid64, s_nb[w], s_bad[w]);
+        if (lane < 27) {
+            s_nb[w][lane] = nv;
+            s_bad[w][lane] = nbad;
+        }
+        const uint64_t ghost = (uint64_t)__ballot_sync(0xffffffffu, ng0) | ((uint64_t)__ballot_sync(0xffffffffu, ng1) << 32);
+        if (lbn < nblk) fetch_ids(lbn);  // in flight while this block is classified and its first half pulled
+        __syncwarp();
         const uint64_t simple = simple_cells(s_bad[w], ghost);
         const uint64_t held = ghost | s_bad[w][13];  // GHOST / SOLID: f_out = f_in
         const int32_t v = lane < 27 ? s_nb[w][lane] : 0;
@@ -190,6 +222,7 @@ __global__ void __launch_bounds__(kLbmWarps * 32, VF_LBM_MINB)
         if ((simple | held | sbb) != ~0ull && lane == 0) list[atomicAdd(n_list, 1)] = lb;
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
+            if (h == 1 && lbn < nblk) fetch_bad();
             const int t = lane + 32 * h;
             if (!((simple >> t) & 1ull)) continue;
             float f[27];
