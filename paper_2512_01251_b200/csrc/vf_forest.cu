@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(256)
          b += (int64_t)gridDim.x * blockDim.x) {
         const int32_t *nb = nbr + 27 * b;
         bool el = true, fluid_nb = false;
-#pragma unroll 2
+        // fully unrolled: the 26 id loads, then the 26 flag gathers, in flight together
+#pragma unroll
         for (int q = 1; q < 27; ++q) {
             const int32_t v = nb[q];
             if (v == VF_NB_MISSING || v == VF_NB_SOLID_NBR) el = false;
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(256)
          b += (int64_t)gridDim.x * blockDim.x) {
         const int32_t *nb = nbr + 27 * b;
         bool has_sb = false;
-#pragma unroll 2
+#pragma unroll
         for (int q = 1; q < 27; ++q) {
             const int32_t v = nb[q];
             if (v >= 0 && (aux[v] & AUX_SB)) has_sb = true;
@@ -119,10 +120,13 @@ __global__ void __launch_bounds__(256)
         uint8_t m = src[b];
         if (!m && (aux[b] & AUX_ELIG) && (!(bflags[b] & VF_BF_SOLID) || it == 0)) {
             const int32_t *nb = nbr + 27 * b;
+            bool any = false;
+#pragma unroll
             for (int q = 1; q < 27; ++q) {
                 const int32_t v = nb[q];
-                if (v >= 0 && src[v]) { m = 1; break; }
+                any |= v >= 0 && src[v];
             }
+            m = any ? 1 : 0;
         }
         dst[b] = m;
         // last sweep: commit (only this thread touches bflags[b]; neighbours
