@@ -255,8 +255,11 @@ __device__ __forceinline__ void xrow_pass_sorted(int L, int lane, const int32_t 
 }
 
 constexpr int kRowWarps = 8;
+#ifndef VF_XROWS_MINB
+#define VF_XROWS_MINB 1
+#endif
 
-__global__ void __launch_bounds__(kRowWarps * 32)
+__global__ void __launch_bounds__(kRowWarps * 32, VF_XROWS_MINB)
     k_xrows(LevelInfo li, int L, RowSet rs, const int32_t *__restrict__ level_start,
             const int32_t *__restrict__ coords, const int32_t *__restrict__ nbr,
             uint8_t *__restrict__ masks, uint8_t *__restrict__ bflags, uint64_t *__restrict__ solid64) {
