@@ -223,9 +223,13 @@ def kernel_rooflines(kt, lv, cfg, F, n_b, stats, ops, hbm, fp32, fp64, traffic):
     # sparse rows: masks read + written, the row order (ids, rows) read; the
     # next level's order written (ids + rows of its positions)
     b_rows = sum(n * (128 + 4 + 16) for n in N) + sum(N[L + 1] * 8 + N[L] * 12 for L in range(Lf))
-    b_mark = sum(N[L] * (27 * 4 + 27 + 1) * (nprop + 2) for L in range(Lf))
+    # per pass: the block's own 27-slot neighbour row and flag bytes (the
+    # neighbours' flags are the same bytes re-read through L2, not HBM)
+    b_mark = sum(N[L] * (27 * 4 + 2) * (nprop + 2) for L in range(Lf))
     b_adapt = sum(N[L + 1] * 304 + N[L] * 108 for L in range(Lf))
-    b_bnd = N[Lf] * (27 * (4 + 8) + 64 + 64)
+    # the neighbour row, the block's own solid word (the 26 neighbours' words
+    # are L2 re-reads), masks read + written, count, flags
+    b_bnd = N[Lf] * (27 * 4 + 8 + 64 + 64 + 4 + 2)
     lines, tests = stats["lines"], stats["tests"]
     links = 2 * lines  # <= 2 links per recorded line (q-records)
     # enumeration: face records read once, q-records written
