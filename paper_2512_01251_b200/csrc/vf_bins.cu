@@ -14,6 +14,8 @@
 //           for long ones.
 #include <math.h>
 
+#include <algorithm>
+
 #include "vf_common.cuh"
 #include "vf_internal.h"
 #include "vf_scan.cuh"
@@ -774,7 +776,9 @@ int block_bins_impl(const LevelInfo &li, int L, vf_grid *g, const int2 *pairs,
                                                bb.d_n_ne);
     int rc = check_launch("k_pair_blocks");
     if (rc) return rc;
-    cudaError_t e = scan_launch_fn(LoadCnt{bb.cnt}, EmitBase{bb.base, bb.cur}, (int64_t)g->capacity,
+    // grid bound: the level's blocks <= its bins (coarse levels: a few tiles)
+    const int64_t nbound = std::min((int64_t)g->capacity, (int64_t)li.bins[0] * li.bins[1] * li.bins[2]);
+    cudaError_t e = scan_launch_fn(LoadCnt{bb.cnt}, EmitBase{bb.base, bb.cur}, nbound,
                                    ScanLevelN{g->d_level_start, L}, bb.d_total, bb.scan_ws, st);
     kt_point("scan_kernel");
     if (e != cudaSuccess) return set_cuda_error(e, "block bins scan");

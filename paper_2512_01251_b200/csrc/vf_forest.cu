@@ -9,6 +9,8 @@
 //             [n_used, capacity), pin A13), child metadata + links from the
 //             parent's neighbours, ghost layer (A14); then the level's
 //             neighbour-child links and interface layer.
+#include <algorithm>
+
 #include "vf_common.cuh"
 #include "vf_internal.h"
 #include "vf_scan.cuh"
@@ -421,7 +423,9 @@ int adapt_impl(const vf_config &cfg, vf_grid *g, int L, void *ws, size_t ws_byte
     // also appends the new level (AdaptFinish: level_start[L+2..], capacity)
     cudaError_t ce = scan_launch_fn(LoadMark{g->d_level_start, L, g->d_bflags},
                                     EmitChild{g->d_level_start, L, g->d_child, g->d_bflags, parents},
-                                    g->capacity, ScanLevelN{g->d_level_start, L}, scalars + 1, scan_ws,
+                                    std::min((int64_t)g->capacity, (int64_t)(cfg.nb[0] << L) * (cfg.nb[1] << L) *
+                                                                         (int64_t)(cfg.nb[2] << L)),
+                                    ScanLevelN{g->d_level_start, L}, scalars + 1, scan_ws,
                                     st, AdaptFinish{L, g->capacity, g->d_level_start, g->d_status});
     if (ce != cudaSuccess) return set_cuda_error(ce, "adapt scan");
     int rc;
