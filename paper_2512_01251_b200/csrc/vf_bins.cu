@@ -696,6 +696,9 @@ __global__ void __launch_bounds__(kPairThreads, VF_PAIRS_MINB)
 int pairs_append_impl(const LevelInfo &li, int nlim, const double *faces, int64_t F,
                       const int32_t *map, const int32_t *d_n_map, int2 *pairs, int32_t *d_n_pairs,
                       int64_t cap, int32_t *d_status, cudaStream_t st) {
+    // the pair's bin key is the flat int32 index I + B_x (J + B_y K)
+    if ((int64_t)li.bins[0] * li.bins[1] * li.bins[2] > 0x7fffffffll)
+        return set_error(VF_EARG, "embed: more than 2^31 bins at the finest level (deeper than the pair key allows)");
     const size_t smem = (size_t)kPairThreads * (nlim + 1) * sizeof(int32_t);
     static size_t attr = 0;
     if (smem > attr) {
