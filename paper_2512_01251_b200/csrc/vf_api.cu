@@ -491,11 +491,15 @@ static int side_stream(SideStream **out) {
     if (e != cudaSuccess) return set_cuda_error(e, "cudaGetDevice");
     SideStream &s = g_side[dev & 63];
     if (!s.st) {
-        // bins feed the level pipeline: highest priority; the link line
-        // enumeration only has to finish by phase 2: lowest priority
+        // the link line enumeration only has to finish by phase 2: lowest
+        // priority; the next level's row order: highest
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        e = cudaStreamCreateWithPriority(&s.st, cudaStreamNonBlocking, hi);
+        // the bins stream one step above the lowest priority -- level with
+        // EmbedEngine's level stream (-1 of the B200's [0, -3]): above it, its
+        // pairs kernels took SMs from the latency-bound level kernels (C4
+        // embed -1.2% measured)
+        e = cudaStreamCreateWithPriority(&s.st, cudaStreamNonBlocking, lo - 1 > hi ? lo - 1 : hi);
         if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&s.st3, cudaStreamNonBlocking, lo);
         if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&s.st4, cudaStreamNonBlocking, hi);
         cudaEvent_t *evs[] = {&s.fork, &s.bins[0], &s.bins[1], &s.vox[0], &s.vox[1], &s.join, &s.join3, &s.adapted, &s.rowsok};
