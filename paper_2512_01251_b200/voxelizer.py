@@ -205,9 +205,10 @@ class EmbedEngine:
         self.cmap = torch.empty(cap, dtype=torch.int32, device="cuda")
         self.n_b_dev = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.host = torch.zeros(8, dtype=torch.int32).pin_memory()  # 0-3 status, 4 n_b
-        # high priority: the level pipeline is the critical path; the library's
-        # cut-link line enumeration runs beside it on a low-priority stream
-        self.stream = torch.cuda.Stream(priority=-1)
+        # the level pipeline is the critical path: above the library's bins
+        # stream (-1) and its low-priority cut-link enumeration (0), below its
+        # next-level row order (-3)
+        self.stream = torch.cuda.Stream(priority=-2)
         self.lengths = None
         self.bc_ids = None
         self.lengths_cap = 0
