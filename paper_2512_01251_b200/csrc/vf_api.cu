@@ -680,14 +680,21 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
         if (L == cfg->l_max - 1) break;
         VF_TRY(mark_impl(*cfg, g, L, w.mark_ws, w.mark_b, st));
         VF_TRY(adapt_impl(*cfg, g, L, w.adapt_ws, w.adapt_b, st, false));
-        // level L+1's row order beside its bins and voxelization, then level
-        // L's neighbour-child links / interface layer (outputs only)
+        // level L+1's row order beside its bins and voxelization; level L's
+        // neighbour-child links / interface layer (outputs only: no later
+        // kernel of the embed reads them) at the lowest priority, behind the
+        // cut-link enumeration (joined with it in phase 2)
         cudaStream_t s4 = one ? st : side->st4;
         cudaEventRecord(side->adapted, st);
         cudaStreamWaitEvent(s4, side->adapted, 0);
         VF_TRY(rows_next_impl(g, L, w.prop_ws, s4));
         cudaEventRecord(side->rowsok, s4);
-        VF_TRY(adapt_links_impl(g, L, s4));
+        if (serial_links) {
+            VF_TRY(adapt_links_impl(g, L, s4));
+        } else {
+            cudaStreamWaitEvent(side->st3, side->adapted, 0);
+            VF_TRY(adapt_links_impl(g, L, side->st3));
+        }
         rec(events, n_ev, &k, st);  // refinement done
     }
     // join the side streams (required to end a capture; bins are all consumed)
@@ -697,6 +704,7 @@ int vf_embed_phase1(const vf_config *cfg, const double *faces, int64_t F, int us
         cudaEventRecord(side->adapted, side->st4);
         cudaStreamWaitEvent(st, side->adapted, 0);
     }
+    if (!serial_links) cudaEventRecord(side->join3, side->st3);  // enumeration + adapt links
     VF_TRY(boundary_impl(*cfg, g, w.bcount, st));
     VF_TRY(tables_impl(g, w.bcount, cmap, d_n_b, w.tab_ws, w.tab_b, st,
                        link_slot_inverse(*cfg, F, w.lines_ws, g->capacity)));
