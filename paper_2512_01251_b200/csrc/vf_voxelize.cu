@@ -37,16 +37,14 @@ namespace vf {
 // face's y / z extent (the SAT's exact box-axis comparisons), then the FP32
 // row classifier (exact SAT in its undecided band); per hit row the 4 cell
 // distances d = ((v1 - x) . n) / n_x (A7 association).  The chunk's (pair,
-// hit row) items are compacted, and the A7 minimum per cell -- |d|, ties to
-// the lowest face id -- is reduced in shared memory in rounds of one item
-// (4 cells) per thread:
-//   (1) every candidate notes the cell's best |d| before the round,
-//   (2) 64-bit atomicMin of |d| (IEEE bits of a non-negative double are
-//       ordered as the values),
-//   (3) a cell whose best |d| dropped forgets the previous winner's id,
-//   (4) atomicMin of the face id among the candidates at the best |d|,
-//   (5) the winner records SOLID (n_x d > 0) or GUARD.
-// Order-free, hence deterministic.  Write-back per row word with the A9 rule,
+// hit row) items are bucketed by row (shared-memory counts, a warp prefix,
+// cursors), and every row -- 4 cells -- is reduced by ONE owner thread: the
+// A7 minimum per cell, |d| with ties to the lowest face id, as the
+// lexicographic minimum of (|d| bits, face id) over the row's items and the
+// best of the group's earlier chunks (IEEE bits of a non-negative double are
+// ordered as the values); the winner records SOLID (n_x d > 0) or GUARD.
+// Order-free, hence deterministic; no atomics on the cells (the round-based
+// atomicMin protocol it replaces needed five barriers per 128 items).  Write-back per row word with the A9 rule,
 // only for rows with a hit (eta == 0: no write, Alg. 3 l.648).  Internal
 // propagation is a provable no-op with matched bins (A8).
 #ifndef VF_VOX_T
@@ -72,9 +70,10 @@ struct VoxGroup {
     double pv[kVoxT][6];
     int32_t pfid[kVoxT];
     int16_t pw[kVoxT];
-    uint16_t item[kVoxT * 16];
-    int wsum[kVoxT / 32];
-    int n_item;
+    uint16_t item[kVoxT * 16];      // the chunk's pair slots bucketed by row (block w, row r)
+    int32_t rcnt[kVoxG * 16];       // items per row
+    int32_t rcur[kVoxG * 16];       // scatter cursors
+    int32_t roff[kVoxG * 16 + 1];   // exclusive prefix of rcnt
 };
 
 constexpr unsigned long long kInf64 = 0x7ff0000000000000ull;
@@ -130,6 +129,7 @@ __global__ void __launch_bounds__(kVoxT, VF_VOX_MINB)
         const int np = S.pre[kVoxG];
         for (int c0 = 0; c0 < np; c0 += kVoxT) {
             const int j = c0 + t;
+            for (int i = t; i < kVoxG * 16; i += kVoxT) S.rcnt[i] = 0;
             uint32_t hm = 0;  // hit rows r = J + 4K of this thread's pair
             int w = 0, fid = 0;
             double v1[3] = {0.0, 0.0, 0.0}, nn[3] = {0.0, 0.0, 0.0};
@@ -171,74 +171,83 @@ __global__ void __launch_bounds__(kVoxT, VF_VOX_MINB)
                     }
                 }
             }
-            // the chunk's (pair, hit row) items, compacted in pair order
-            {
-                const int c = __popc(hm);
-                int inc = c;
+            // the chunk's (pair, hit row) items bucketed by row (block w, row
+            // r); every row -- 4 cells -- is then reduced by ONE owner thread:
+            // A7's minimum |d| per cell, ties to the lowest face id, as a
+            // lexicographic (|d|, face id) minimum over the row's items and the
+            // best of the earlier chunks -- order-free, no atomics on the cells
+            S.pv[t][0] = v1[0]; S.pv[t][1] = v1[1]; S.pv[t][2] = v1[2];
+            S.pv[t][3] = nn[0]; S.pv[t][4] = nn[1]; S.pv[t][5] = nn[2];
+            S.pfid[t] = fid;
+            S.pw[t] = (int16_t)w;
+            __syncthreads();  // rcnt zeroed, pair records staged
+            for (uint32_t m = hm; m; m &= m - 1) atomicAdd(&S.rcnt[w * 16 + (__ffs(m) - 1)], 1);
+            __syncthreads();
+            if (t < 32) {  // exclusive prefix over the rows (warp 0)
+                constexpr int kPer = kVoxG * 16 / 32;
+                int loc[kPer], sum = 0;
+#pragma unroll
+                for (int k = 0; k < kPer; ++k) {
+                    loc[k] = S.rcnt[t * kPer + k];
+                    sum += loc[k];
+                }
+                int inc = sum;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const int y = __shfl_up_sync(0xffffffffu, inc, o);
-                    if ((t & 31) >= o) inc += y;
+                    if (t >= o) inc += y;
                 }
-                if ((t & 31) == 31) S.wsum[t >> 5] = inc;
-                S.pv[t][0] = v1[0]; S.pv[t][1] = v1[1]; S.pv[t][2] = v1[2];
-                S.pv[t][3] = nn[0]; S.pv[t][4] = nn[1]; S.pv[t][5] = nn[2];
-                S.pfid[t] = fid;
-                S.pw[t] = (int16_t)w;
-                __syncthreads();
-                int pos = inc - c;
-                for (int k = 0; k < (t >> 5); ++k) pos += S.wsum[k];
-                for (uint32_t m = hm; m; m &= m - 1) S.item[pos++] = (uint16_t)(t | ((__ffs(m) - 1) << 8));
-                if (t == kVoxT - 1) S.n_item = pos;
-                __syncthreads();
+                int ex = inc - sum;
+#pragma unroll
+                for (int k = 0; k < kPer; ++k) {
+                    S.roff[t * kPer + k] = ex;
+                    S.rcur[t * kPer + k] = ex;
+                    ex += loc[k];
+                }
+                if (t == 31) S.roff[kVoxG * 16] = inc;
             }
-            // rounds of one item per thread (the A7 reduction, see above)
-            const int n_item = S.n_item;
-            for (int i0 = 0; i0 < n_item; i0 += kVoxT) {
-                const bool has = i0 + t < n_item;
-                int slot0 = 0, ifid = 0;
-                unsigned long long db[4] = {kInf64, kInf64, kInf64, kInf64}, old[4];
-                bool solid[4] = {false, false, false, false};
-                if (has) {
-                    const uint32_t it = S.item[i0 + t];
-                    const int pl = it & 0xff, r = it >> 8, iw = S.pw[pl];
-                    const int4 ico = S.co[iw];
+            __syncthreads();
+            for (uint32_t m = hm; m; m &= m - 1) S.item[atomicAdd(&S.rcur[w * 16 + (__ffs(m) - 1)], 1)] = (uint16_t)t;
+            __syncthreads();
+            for (int R = t; R < kVoxG * 16; R += kVoxT) {
+                const int e0 = S.roff[R], e1 = S.roff[R + 1];
+                if (e0 == e1) continue;
+                const int iw = R >> 4, r = R & 15, slot0 = iw * 64 + 4 * r;
+                const int4 ico = S.co[iw];
+                const double y = node_c(4 * ico.y + (r & 3), dx), z = node_c(4 * ico.z + (r >> 2), dx);
+                unsigned long long bd[4];
+                int32_t bf[4];
+                uint8_t bv[4];
+#pragma unroll
+                for (int I = 0; I < 4; ++I) {
+                    bd[I] = S.bd[slot0 + I];
+                    bf[I] = S.bfid[slot0 + I];
+                    bv[I] = S.bval[slot0 + I];
+                }
+                for (int e = e0; e < e1; ++e) {
+                    const int pl = S.item[e];
                     const double pv1[3] = {S.pv[pl][0], S.pv[pl][1], S.pv[pl][2]};
                     const double pn[3] = {S.pv[pl][3], S.pv[pl][4], S.pv[pl][5]};
-                    ifid = S.pfid[pl];
-                    const double y = node_c(4 * ico.y + (r & 3), dx), z = node_c(4 * ico.z + (r >> 2), dx);
-                    slot0 = iw * 64 + 4 * r;
+                    const int32_t ifid = S.pfid[pl];
 #pragma unroll
                     for (int I = 0; I < 4; ++I) {
                         const double d = VF_DDIV(plane_num(pv1, pn, node_c(4 * ico.x + I, dx), y, z), pn[0]);
-                        db[I] = (unsigned long long)__double_as_longlong(fabs(d));
-                        solid[I] = VF_DMUL(pn[0], d) > 0.0;
-                        old[I] = S.bd[slot0 + I];
+                        const unsigned long long db = (unsigned long long)__double_as_longlong(fabs(d));
+                        if (db < bd[I] || (db == bd[I] && ifid < bf[I])) {
+                            bd[I] = db;
+                            bf[I] = ifid;
+                            bv[I] = VF_DMUL(pn[0], d) > 0.0 ? VF_SOLID : VF_GUARD;
+                        }
                     }
                 }
-                __syncthreads();
-                if (has)
 #pragma unroll
-                    for (int I = 0; I < 4; ++I) atomicMin(&S.bd[slot0 + I], db[I]);
-                __syncthreads();
-                bool best[4] = {false, false, false, false};
-                if (has)
-#pragma unroll
-                    for (int I = 0; I < 4; ++I) {
-                        const unsigned long long b = S.bd[slot0 + I];
-                        best[I] = b == db[I];
-                        if (best[I] && b < old[I]) S.bfid[slot0 + I] = 0x7fffffff;  // new best |d|
-                    }
-                __syncthreads();
-#pragma unroll
-                for (int I = 0; I < 4; ++I)
-                    if (best[I]) atomicMin(&S.bfid[slot0 + I], ifid);
-                __syncthreads();
-#pragma unroll
-                for (int I = 0; I < 4; ++I)
-                    if (best[I] && S.bfid[slot0 + I] == ifid) S.bval[slot0 + I] = solid[I] ? VF_SOLID : VF_GUARD;
-                __syncthreads();
+                for (int I = 0; I < 4; ++I) {
+                    S.bd[slot0 + I] = bd[I];
+                    S.bfid[slot0 + I] = bf[I];
+                    S.bval[slot0 + I] = bv[I];
+                }
             }
+            __syncthreads();
         }
         __syncthreads();
         // write-back: one row word (4 cells) per thread, A9 rule
