@@ -22,7 +22,10 @@ namespace vf {
 #define VF_SCAN_MINB 6  // <= 40 registers: 48 warps per SM (measured best; 1 lets the compiler take 96)
 #endif
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;
+#ifndef VF_SCAN_ITEMS
+#define VF_SCAN_ITEMS 16
+#endif
+constexpr int kScanItems = VF_SCAN_ITEMS;
 constexpr int kScanTile = kScanThreads * kScanItems;  // 4096
 
 constexpr uint64_t kFlagAgg = 1ull << 32;
